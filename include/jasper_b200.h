@@ -1,0 +1,209 @@
+/*
+ * jasper_b200.h — C ABI of the B200-native hot paths of the `beamann` reference
+ * (arxiv 2601.07048, "Jasper"): Vamana greedy beam search, RaBitQ estimation +
+ * fp32 rerank, batch-parallel lock-free insertion, sharded top-k merge.
+ *
+ * Conventions
+ *  - Every entry point returns an int status (JB_OK == 0). On failure
+ *    jb_last_error() returns a thread-local, NUL-terminated message.
+ *  - All array arguments are DEVICE pointers (cudaMalloc / torch CUDA tensors)
+ *    unless the name ends in `_host`. The caller owns every buffer passed in;
+ *    the library only allocates stream-ordered scratch (cudaMallocAsync) that
+ *    it frees before returning.
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *    Calls are asynchronous w.r.t. the host unless documented otherwise; calls
+ *    that must read a device value back (loop trip counts) synchronize `stream`.
+ *  - Arithmetic follows the reference's numpy rounding order bit-exactly
+ *    ("A1": 4-lane SSE einsum order, separate multiply and add, no FMA), so
+ *    device results are identical to the reference on the same inputs.
+ *  - Search keys are the reference's u64 keys: (f32 bits of max(d,0)) << 32 | id
+ *    (search.py:139-156). Bit 31 of the low word is used on device only as the
+ *    "expanded" flag and is always cleared in outputs.
+ *
+ * Each function names the reference function it replaces (file:line relative
+ * to pkg/src/beamann/ of the reference).
+ */
+#ifndef JASPER_B200_H
+#define JASPER_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define JB_OK 0
+#define JB_EINVAL 1        /* bad argument (mirrors the reference's ValueError) */
+#define JB_ECUDA 2         /* CUDA runtime / launch failure                     */
+#define JB_ENODONOR 3      /* connectivity repair found no donor (RuntimeError) */
+#define JB_EOVERFLOW 4     /* a bounded device buffer overflowed                */
+
+/* ---- library ---------------------------------------------------------- */
+const char* jb_last_error(void);
+int jb_abi_version(void);
+/* Number of SMs of `device` (grids are sized in multiples of it). */
+int jb_sm_count(int device, int32_t* out);
+
+/* ---- data model -------------------------------------------------------- */
+
+/* Row squared norms in A1 order: out[i] = einsum("nd,nd->n", x, x)[i].
+ * Replaces ExactDistances.__init__ xnorm (search.py:101),
+ * ExactDistances.bind qnorm (search.py:113) and _PairwiseDistances norms
+ * (build.py:120). */
+int jb_row_sq_norms(const float* x, int64_t n, int32_t dims, float* out, void* stream);
+
+/* Medoid: argmin_i ||x_i - mean||^2 in f64 (mean = sequential f64 row sum / n,
+ * distance = 2-lane einsum order), lowest id on ties. Writes the index to
+ * *out_host (synchronizes). Replaces graph.medoid (graph.py:159-171). */
+int jb_medoid(const float* x, int64_t n, int32_t dims, int64_t* out_host, void* stream);
+
+/* ---- search (north-star 1) -------------------------------------------- */
+
+/* Distance source of a search. */
+#define JB_SRC_EXACT 0     /* ExactDistances over raw f32 rows (search.py:82-130) */
+#define JB_SRC_RABITQ 1    /* RaBitQ estimator (rabitq.py:225-244)                 */
+
+typedef struct jb_search_args {
+    /* graph (GraphIndex, graph.py:36-99): fixed-stride int32 slab padded -1 */
+    const int32_t* adjacency;      /* [capacity, degree_cap]                   */
+    int32_t degree_cap;            /* R                                        */
+    int64_t active_count;          /* vertices visible to the search           */
+    /* distance source */
+    int32_t source;                /* JB_SRC_*                                 */
+    int32_t dims;                  /* D                                        */
+    const float* data;             /* EXACT: [N, D] f32 rows                   */
+    const float* data_norms;       /* EXACT: [N] A1 row norms                  */
+    const uint8_t* records;        /* RABITQ: [N, record_bytes] packed records */
+    int32_t record_bytes;          /* RABITQ: see jb_rabitq_pack_records        */
+    int32_t bits;                  /* RABITQ: 1, 2, 4 or 8                      */
+    /* queries */
+    const float* queries;          /* EXACT: [nq, D] f32; RABITQ: rotated [nq, D] */
+    const float* query_add;        /* EXACT: [nq] qnorm; RABITQ: [nq] query_add  */
+    const float* query_sumq;       /* RABITQ: [nq] query_sumq; EXACT: unused     */
+    int64_t nq;
+    const int32_t* starts;         /* [nq] start vertices, or NULL => start_vertex */
+    int64_t start_vertex;
+    /* search parameters */
+    int32_t beam_width;            /* L, 1..1024                               */
+    int32_t hash_slots;            /* visited-table slots per query (pow2) or 0 = auto */
+    int32_t trace_cap;             /* visited-trace capacity per query; 0 = no trace */
+    /* outputs */
+    uint64_t* frontier_keys;       /* [nq, L] ascending keys, UMAX padded      */
+    int32_t* hops;                 /* [nq] SearchStats.hops                    */
+    int32_t* evals;                /* [nq] device distance evaluations          */
+    int32_t* trace_ids;            /* [nq, trace_cap] visited ids in hop order  */
+    float* trace_dists;            /* [nq, trace_cap] their f32 distances       */
+    int32_t* flags;                /* [nq] bit0: visited table overflowed (lossy) */
+} jb_search_args;
+
+/* Batched greedy beam search, one warp per query (persistent grid).
+ * Replaces run_beam_searches/_run_lockstep (search.py:171-304). Frontier and
+ * visited trace are identical to the reference's (same keys, same order). */
+int jb_beam_search(const jb_search_args* args, void* stream);
+
+/* Top-k extraction from frontier keys: ids (int32, -1 padded) and dists (f64,
+ * +inf padded). Replaces the exact-source branch of search_knn_batch
+ * (search.py:366-383). */
+int jb_frontier_topk(const uint64_t* frontier_keys, int64_t nq, int32_t beam_width, int32_t k,
+                     int32_t* out_ids, double* out_dists, void* stream);
+
+/* Exact fp32 rerank of the full frontier: dist = einsum(x-q, x-q) (A1),
+ * ordered by (dist, id), first k. Replaces _exact_rescore + lexsort
+ * (search.py:318-320, 375-382). */
+int jb_rerank_topk(const float* data, int32_t dims, const float* queries, int64_t nq,
+                   const uint64_t* frontier_keys, int32_t beam_width, int32_t k,
+                   int32_t* out_ids, double* out_dists, void* stream);
+
+/* ---- RaBitQ (north-star 2) --------------------------------------------- */
+
+/* Packed device record of one vector: code bytes, zero padding to 8, then
+ * (data_add, data_rescale) f32, total rounded up to 16 bytes. */
+int32_t jb_rabitq_record_bytes(int32_t dims, int32_t bits);
+
+/* Build records from reference-layout codes [n, ceil(D*m/8)] and meta [n, 2].
+ * (RaBitQIndex layout, rabitq.py:113-168). */
+int jb_rabitq_pack_records(const uint8_t* codes, const float* meta, int64_t n, int32_t dims,
+                           int32_t bits, uint8_t* records, void* stream);
+
+/* Quantize rows: codes [n, ceil(D*m/8)] and meta [n, 2], bit-exact with
+ * rabitq.fit's per-block math (rabitq.py:282-299) given the same centroid (f32)
+ * and rotation (f64 [D, D], from the seed on the host). */
+int jb_rabitq_encode(const float* x, int64_t n, int32_t dims, int32_t bits,
+                     const float* centroid, const double* rotation,
+                     uint8_t* codes, float* meta, void* stream);
+
+/* Centroid: f32(sequential f64 column mean) (rabitq.py:273). */
+int jb_column_mean_f32(const float* x, int64_t n, int32_t dims, float* out, void* stream);
+
+/* Per-query prep (RaBitQIndex.bind, rabitq.py:170-181): rotated = f32(f64(q-c) @ rot^T),
+ * query_add = A1 dot(q-c, q-c), query_sumq = f32(pairwise_sum_f32(rotated) * mid). */
+int jb_rabitq_bind(const float* queries, int64_t nq, int32_t dims, int32_t bits,
+                   const float* centroid, const double* rotation,
+                   float* rotated, float* query_add, float* query_sumq, void* stream);
+
+/* ---- construction / insertion (north-star 3) --------------------------- */
+
+typedef struct jb_insert_args {
+    /* graph, mutated in place on device */
+    int32_t* adjacency;            /* [capacity, R] */
+    int32_t* degrees;              /* [capacity]    */
+    int32_t degree_cap;            /* R             */
+    int64_t capacity;
+    /* dataset (exact construction only) */
+    const float* data;             /* [count, D]    */
+    const float* data_norms;       /* [count]       */
+    int32_t dims;
+    int64_t count;
+    /* BuildParams (build.py:35-62) */
+    int32_t build_beam_width;
+    double alpha;
+    int32_t always_prune;
+    int32_t reverse_all_visited;
+    /* batch */
+    int64_t start, stop;           /* new ids [start, stop); start == active_count */
+    int64_t entry_point;           /* in: current entry point                */
+    /* outputs (host) */
+    int64_t* entry_point_out_host; /* entry point after the batch            */
+    int64_t* bridges_out_host;     /* bridges added by connectivity repair   */
+    int32_t* stats_out_host;       /* [8] diagnostics, may be NULL           */
+} jb_insert_args;
+
+/* One three-phase batch: search -> prune + reverse triples -> grouped merge,
+ * then connectivity repair. On an empty graph (start == 0) the batch seeds it
+ * by mutual pruning. Replaces batch_insert (build.py:296-348) with
+ * _seed_batch (246-266), _merge_reverse_edges (269-293) and
+ * _repair_connectivity (154-224). Synchronizes `stream`. */
+int jb_batch_insert(const jb_insert_args* args, void* stream);
+
+/* Connectivity repair only (after the entry point moves, build.py:415-418). */
+int jb_repair_connectivity(const jb_insert_args* args, void* stream);
+
+/* Batched robust prune (graph.robust_prune, graph.py:174-228) of `count`
+ * independent pivots: pivots[i] with candidates cand_ids/cand_dists[offsets[i]:offsets[i+1]]
+ * (f32 distances to the pivot; any order). Kept ids/dists written to
+ * out_ids/out_dists[i*degree_cap ...], out_counts[i] = number kept. */
+int jb_robust_prune(const float* data, const float* data_norms, int32_t dims,
+                    const int64_t* pivots, int64_t count, const int64_t* offsets,
+                    const int32_t* cand_ids, const float* cand_dists,
+                    double alpha, int32_t degree_cap,
+                    int32_t* out_ids, float* out_dists, int32_t* out_counts, void* stream);
+
+/* ---- measurement -------------------------------------------------------- */
+
+/* Exact top-k in f64 (oracle.exact_knn, oracle.py:20-62): (dist, id) ascending. */
+int jb_exact_knn(const float* data, int64_t n, int32_t dims, const float* queries, int64_t nq,
+                 int32_t k, int32_t* out_ids, float* out_dists, void* stream);
+
+/* ---- sharding (north-star 4) ------------------------------------------- */
+
+/* Merge per-shard top-k lists gathered from `shards` ranks into a global top-k
+ * by (dist, global id). in_ids/in_dists: [shards, nq, k] with shard-local ids;
+ * id_offsets[s] converts to global ids. -1 ids are padding. */
+int jb_merge_shard_topk(const int32_t* in_ids, const double* in_dists, int32_t shards, int64_t nq,
+                        int32_t k, const int64_t* id_offsets_host, int64_t* out_ids,
+                        double* out_dists, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* JASPER_B200_H */

@@ -1,0 +1,38 @@
+"""ORACLE — test infrastructure only. Exact kNN and recall.
+
+  * exact_knn: f64 xn - 2 q.x + qn, clamp, stable argsort   oracle.py:20-62
+  * recall_at_k: distance-threshold matching, eps 1e-6      bench.py:44-66
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+QBLOCK = 256
+EPS = 1e-6
+
+
+def exact_knn(data: np.ndarray, queries: np.ndarray, k: int):
+    x = data.astype(np.float64)
+    qa = queries.astype(np.float64)
+    xn = np.einsum("nd,nd->n", x, x)
+    ids = np.empty((qa.shape[0], k), dtype=np.int32)
+    ds = np.empty((qa.shape[0], k), dtype=np.float32)
+    for lo in range(0, qa.shape[0], QBLOCK):
+        q = qa[lo:lo + QBLOCK]
+        s = xn[None, :] - 2.0 * (q @ x.T) + np.einsum("bd,bd->b", q, q)[:, None]
+        np.maximum(s, 0.0, out=s)
+        o = np.argsort(s, axis=1, kind="stable")[:, :k]
+        ids[lo:lo + QBLOCK] = o
+        ds[lo:lo + QBLOCK] = np.take_along_axis(s, o, axis=1)
+    return ids, ds
+
+
+def recall_at_k(result_ids, gt_ids: np.ndarray, gt_dists: np.ndarray, k: int) -> float:
+    g = gt_dists.astype(np.float64)
+    thr = g[:, k - 1] + EPS * np.abs(g[:, k - 1])
+    tot = 0.0
+    for i in range(len(result_ids)):
+        got = np.asarray(result_ids[i], dtype=np.int64)[:k]
+        tot += np.isin(got, gt_ids[i][g[i] <= thr[i]]).sum() / k
+    return tot / len(result_ids)

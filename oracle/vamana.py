@@ -1,0 +1,242 @@
+"""ORACLE — test infrastructure only. Graph construction restated in numpy.
+
+  * medoid: f64 mean, f64 einsum distances, lowest id         graph.py:159-171
+  * robust_prune: (dist, id) order, alpha^2 * d* > d keeps    graph.py:174-228
+  * pairwise distance, rows in the data role, pivot last      build.py:105-134
+  * reverse-edge buffer sorted by (target, dist, source)      build.py:65-102
+  * seed batch, 3-phase batch insert, group merge             build.py:246-348
+  * connectivity repair (BFS + nearest-donor bridges)         build.py:137-224
+  * build schedule (R+1 doubling, entry -> medoid)            build.py:389-424
+  * insert_stream chunking                                    build.py:427-447
+
+The graph is a plain dict-free structure: adjacency int32[cap, R] padded -1,
+degrees int32[cap], entry, active.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from .search import ExactSource, beam_search
+
+
+class Graph:
+    def __init__(self, capacity: int, R: int):
+        self.adj = np.full((capacity, R), -1, dtype=np.int32)
+        self.deg = np.zeros(capacity, dtype=np.int32)
+        self.R = R
+        self.entry = 0
+        self.active = 0
+
+    def nbrs(self, u: int) -> np.ndarray:
+        return self.adj[u, : self.deg[u]].copy()
+
+    def put(self, u: int, ids) -> None:
+        ids = np.asarray(ids, dtype=np.int32).ravel()
+        assert ids.size <= self.R
+        if ids.size:
+            assert ids.min() >= 0 and ids.max() < self.active and not (ids == u).any()
+            assert np.unique(ids).size == ids.size
+        self.adj[u, : ids.size] = ids
+        self.adj[u, ids.size:] = -1
+        self.deg[u] = ids.size
+
+
+class Pairwise:
+    """build.py:105-134 (exact branch)."""
+
+    def __init__(self, x: np.ndarray):
+        self.x = x
+        self.n = np.einsum("nd,nd->n", x, x)
+
+    def __call__(self, pivot: int, ids) -> np.ndarray:
+        ids = np.asarray(ids, dtype=np.int64)
+        dots = np.einsum("md,d->m", self.x[ids], self.x[pivot])
+        return np.maximum(self.n[ids] - 2 * dots + self.n[pivot], np.float32(0)).astype(np.float64)
+
+
+def medoid(x: np.ndarray) -> int:
+    if x.shape[0] == 0:
+        raise ValueError("medoid of an empty dataset")
+    x64 = x.astype(np.float64)
+    diff = x64 - x64.mean(axis=0)
+    return int(np.argmin(np.einsum("nd,nd->n", diff, diff)))
+
+
+def robust_prune(p: int, ids, dists, alpha: float, R: int, dist) -> tuple[np.ndarray, np.ndarray]:
+    if alpha < 1.0:
+        raise ValueError("alpha must be >= 1")
+    if R < 1:
+        raise ValueError("degree_cap must be >= 1")
+    ids = np.asarray(ids, dtype=np.int64).ravel()
+    ds = np.asarray(dists, dtype=np.float64).ravel()
+    if ids.shape != ds.shape:
+        raise ValueError("candidate ids and dists length mismatch")
+    if (ids == p).any():
+        raise ValueError("candidate set must not contain the pivot")
+    if np.unique(ids).size != ids.size:
+        raise ValueError("candidate set must be deduplicated")
+    o = np.lexsort((ids, ds))
+    ids, ds = ids[o], ds[o]
+    a2 = float(alpha) * float(alpha)
+    out_i, out_d = [], []
+    while ids.size and len(out_i) < R:
+        s = int(ids[0])
+        out_i.append(s)
+        out_d.append(float(ds[0]))
+        ids, ds = ids[1:], ds[1:]
+        if not ids.size:
+            break
+        survive = a2 * np.asarray(dist(s, ids), dtype=np.float64) > ds
+        ids, ds = ids[survive], ds[survive]
+    return np.asarray(out_i, dtype=np.int32), np.asarray(out_d, dtype=np.float64)
+
+
+def reachable(g: Graph) -> np.ndarray:
+    seen = np.zeros(g.active, dtype=bool)
+    seen[g.entry] = True
+    front = np.array([g.entry])
+    while front.size:
+        nxt = g.adj[front].ravel()
+        nxt = nxt[nxt >= 0]
+        nxt = np.unique(nxt[~seen[nxt]])
+        seen[nxt] = True
+        front = nxt
+    return seen
+
+
+def repair(g: Graph, dist: Pairwise) -> int:
+    """build.py:154-224."""
+    if g.active < 2:
+        return 0
+    R = g.R
+    fan = min(R, 16)
+    bridges = 0
+    pins: dict[int, set] = {}
+    while True:
+        seen = reachable(g)
+        lost = np.flatnonzero(~seen)
+        if not lost.size:
+            return bridges
+        ok = np.flatnonzero(seen)
+        donors = np.empty((lost.size, fan), dtype=np.int64)
+        best = np.empty(lost.size)
+        for i, x in enumerate(lost):
+            d = dist(int(x), ok)
+            top = np.argpartition(d, min(fan, d.size) - 1)[:fan]
+            top = top[np.lexsort((ok[top], d[top]))]
+            donors[i] = ok[top]
+            best[i] = d[top[0]]
+        for i in np.lexsort((lost, best)):
+            x = int(lost[i])
+            if seen[x]:
+                continue
+            placed = False
+            for u in donors[i]:
+                u = int(u)
+                row = g.nbrs(u)
+                pin = pins.setdefault(u, set())
+                if row.size >= R:
+                    ev = row[~np.isin(row, list(pin))] if pin else row
+                    if not ev.size:
+                        continue
+                    drop = ev[np.argmax(dist(u, ev))]
+                    row = row[row != drop]
+                g.put(u, np.append(row, x))
+                pin.add(x)
+                bridges += 1
+                placed = True
+                break
+            if not placed:
+                raise RuntimeError(f"connectivity repair: no donor for vertex {x}")
+            front = np.array([x])
+            seen[x] = True
+            while front.size:
+                nxt = g.adj[front].ravel()
+                nxt = nxt[nxt >= 0]
+                nxt = np.unique(nxt[~seen[nxt]])
+                seen[nxt] = True
+                front = nxt
+
+
+def batch_insert(g: Graph, x: np.ndarray, start: int, stop: int, R: int, L: int, alpha: float,
+                 dist: Pairwise | None = None, always_prune=False, reverse_all=False) -> int:
+    """build.py:296-348. Returns the number of repair bridges."""
+    if start == stop:
+        return 0
+    dist = dist or Pairwise(x)
+    if g.active == 0:
+        g.active = stop
+        g.entry = medoid(x[:stop])
+        if stop - start > 1:
+            everyone = np.arange(start, stop)
+            for v in range(start, stop):
+                rest = everyone[everyone != v]
+                kept, _ = robust_prune(v, rest, dist(v, rest), alpha, R, dist)
+                g.put(v, kept)
+        return repair(g, dist)
+    src = ExactSource(x, x[start:stop])
+    found = beam_search(g.adj, g.active, g.entry, src, stop - start, L)
+    g.active = stop
+    tgt, srcs, dd = [], [], []
+    for v, res in zip(range(start, stop), found):
+        kept, kd = robust_prune(v, res.visited_ids, res.visited_dists, alpha, R, dist)
+        g.put(v, kept)
+        e_ids, e_d = (res.visited_ids, res.visited_dists) if reverse_all else (kept, kd)
+        tgt.append(np.asarray(e_ids, dtype=np.int64))
+        srcs.append(np.full(len(e_ids), v, dtype=np.int64))
+        dd.append(np.asarray(e_d, dtype=np.float64))
+    if tgt:
+        t = np.concatenate(tgt)
+        s = np.concatenate(srcs)
+        d = np.concatenate(dd)
+        o = np.lexsort((s, d, t))
+        t, s, d = t[o], s[o], d[o]
+        heads = np.flatnonzero(np.r_[True, t[1:] != t[:-1]])
+        bounds = np.r_[heads, t.size]
+        for a, b in zip(bounds[:-1], bounds[1:]):
+            target = int(t[a])
+            have = g.nbrs(target)
+            keep = ~np.isin(s[a:b], have)
+            fs, fd = s[a:b][keep], d[a:b][keep]
+            if not fs.size:
+                continue
+            if not always_prune and have.size + fs.size <= R:
+                g.put(target, np.concatenate([have, fs.astype(np.int32)]))
+                continue
+            hd = dist(target, have) if have.size else np.empty(0)
+            kept, _ = robust_prune(target, np.concatenate([have.astype(np.int64), fs]),
+                                   np.concatenate([np.asarray(hd, dtype=np.float64), fd]), alpha, R, dist)
+            g.put(target, kept)
+    return repair(g, dist)
+
+
+def build(x: np.ndarray, R: int, L: int, alpha: float, max_batch: int = 100_000) -> Graph:
+    """build.py:389-424 (two_pass=False)."""
+    x = np.ascontiguousarray(x, dtype=np.float32)
+    n = x.shape[0]
+    if n == 0:
+        raise ValueError("cannot build over an empty dataset")
+    g = Graph(n, R)
+    dist = Pairwise(x)
+    m = medoid(x)
+    size, pos = R + 1, 0
+    while pos < n:
+        stop = min(n, pos + size)
+        batch_insert(g, x, pos, stop, R, L, alpha, dist)
+        if m < g.active and g.entry != m:
+            g.entry = m
+            repair(g, dist)
+        pos = stop
+        size = min(size * 2, max_batch)
+    return g
+
+
+def insert_stream(g: Graph, x: np.ndarray, start: int, stop: int, R: int, L: int, alpha: float,
+                  max_batch: int) -> None:
+    dist = Pairwise(x)
+    pos = start
+    while pos < stop:
+        nxt = min(stop, pos + max_batch)
+        batch_insert(g, x, pos, nxt, R, L, alpha, dist)
+        pos = nxt

@@ -1,0 +1,213 @@
+"""Vector datasets and synthetic generators (mirror of the reference's core.py).
+
+`VectorDataset` keeps the reference contract (core.py:55-107): an immutable,
+finite, C-contiguous (count, dims) f32 (or u8) array. The B200 path adds a
+lazily created device mirror — the f32 rows in HBM plus their A1-order
+squared norms — that every kernel reads; it is built once per dataset.
+"""
+
+from __future__ import annotations
+
+import enum
+import threading
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+
+__all__ = ["ElementKind", "DistanceKind", "VectorDataset", "sq_l2", "dot", "gen_synthetic", "gen_lowrank"]
+
+
+class ElementKind(enum.Enum):
+    U8 = "u8"
+    F32 = "f32"
+
+    @property
+    def dtype(self) -> np.dtype:
+        return np.dtype(np.uint8) if self is ElementKind.U8 else np.dtype(np.float32)
+
+    @property
+    def itemsize(self) -> int:
+        return self.dtype.itemsize
+
+
+class DistanceKind(enum.Enum):
+    SQUARED_EUCLIDEAN = "sq_l2"
+    INNER_PRODUCT = "ip"
+
+
+@dataclass
+class DeviceRows:
+    """HBM mirror of a dataset: rows [n, D] f32 and A1 norms [n] f32."""
+    x: object
+    norms: object
+    count: int
+    dims: int
+
+
+class VectorDataset:
+    """Immutable row-major store of `count` vectors of `dims` elements (core.py:55-107)."""
+
+    def __init__(self, data: np.ndarray):
+        arr = np.asarray(data)
+        if arr.ndim != 2:
+            raise ValueError(f"dataset array must be 2-D, got shape {arr.shape}")
+        if arr.shape[1] < 1:
+            raise ValueError("dims must be >= 1")
+        if arr.dtype == np.uint8:
+            self._kind = ElementKind.U8
+        elif arr.dtype == np.float32:
+            self._kind = ElementKind.F32
+        else:
+            raise ValueError(f"unsupported element dtype {arr.dtype}; use uint8 or float32")
+        arr = np.ascontiguousarray(arr)
+        if self._kind is ElementKind.F32 and arr.size and not np.isfinite(arr).all():
+            raise ValueError("dataset contains non-finite values")
+        arr.setflags(write=False)
+        self._data = arr
+        self._dev: DeviceRows | None = None
+        self._dev_lock = threading.Lock()
+
+    @classmethod
+    def from_device(cls, x_dev, host: np.ndarray | None = None) -> "VectorDataset":
+        """Wrap rows already resident in HBM (torch f32 [n, D] CUDA tensor).
+
+        The host copy is materialized lazily only if a host-side caller asks
+        for `.data`; the kernels read the device rows directly.
+        """
+        torch = _lib.require_cuda()
+        if x_dev.dtype != torch.float32 or x_dev.dim() != 2 or not x_dev.is_cuda:
+            raise ValueError("from_device expects a CUDA float32 (n, D) tensor")
+        obj = cls.__new__(cls)
+        obj._kind = ElementKind.F32
+        obj._data = host
+        obj._dev_lock = threading.Lock()
+        x_dev = x_dev.contiguous()
+        norms = torch.empty(x_dev.shape[0], dtype=torch.float32, device=x_dev.device)
+        _lib.check(_lib.lib().jb_row_sq_norms(_lib.ptr(x_dev), x_dev.shape[0], x_dev.shape[1],
+                                             _lib.ptr(norms), _lib.stream_ptr()))
+        obj._dev = DeviceRows(x_dev, norms, x_dev.shape[0], x_dev.shape[1])
+        obj._shape = tuple(x_dev.shape)
+        return obj
+
+    @property
+    def data(self) -> np.ndarray:
+        if self._data is None:
+            arr = self._dev.x.cpu().numpy()
+            arr.setflags(write=False)
+            self._data = arr
+        return self._data
+
+    @property
+    def element_kind(self) -> ElementKind:
+        return self._kind
+
+    @property
+    def dims(self) -> int:
+        return self._data.shape[1] if self._data is not None else self._dev.dims
+
+    @property
+    def count(self) -> int:
+        return self._data.shape[0] if self._data is not None else self._dev.count
+
+    def row(self, i: int) -> np.ndarray:
+        return self.data[i]
+
+    def slice_rows(self, start: int, stop: int) -> "VectorDataset":
+        return VectorDataset(self.data[start:stop])
+
+    def __len__(self) -> int:
+        return self.count
+
+    def __repr__(self) -> str:
+        return f"VectorDataset(count={self.count}, dims={self.dims}, kind={self._kind.value})"
+
+    # ---- device mirror -------------------------------------------------
+    def device(self) -> DeviceRows:
+        """Upload once (rows + A1 norms computed on device) and cache."""
+        if self._dev is not None:
+            return self._dev
+        if self._kind is not ElementKind.F32:
+            raise ValueError("the B200 path supports f32 datasets (u8 is not built yet)")
+        torch = _lib.require_cuda()
+        with self._dev_lock:
+            if self._dev is None:
+                x = torch.from_numpy(np.ascontiguousarray(self._data)).to("cuda", non_blocking=False)
+                norms = torch.empty(x.shape[0], dtype=torch.float32, device=x.device)
+                if x.shape[0]:
+                    _lib.check(_lib.lib().jb_row_sq_norms(_lib.ptr(x), x.shape[0], x.shape[1], _lib.ptr(norms),
+                                                         _lib.stream_ptr()))
+                self._dev = DeviceRows(x, norms, x.shape[0], x.shape[1])
+        return self._dev
+
+
+def as_dataset(obj) -> VectorDataset:
+    """Accept this package's VectorDataset or any object with a 2-D `.data` array
+    (e.g. the reference's beamann.VectorDataset) — the drop-in path."""
+    if isinstance(obj, VectorDataset):
+        return obj
+    data = getattr(obj, "data", None)
+    if isinstance(data, np.ndarray) and data.ndim == 2:
+        cache = getattr(obj, "_jb_dataset", None)
+        if cache is None:
+            cache = VectorDataset(data)
+            try:
+                object.__setattr__(obj, "_jb_dataset", cache)
+            except Exception:
+                pass
+        return cache
+    raise TypeError(f"unsupported dataset {type(obj).__name__}")
+
+
+def _require_same_shape(a: np.ndarray, b: np.ndarray) -> None:
+    if a.shape != b.shape:
+        raise ValueError(f"dimension mismatch: {a.shape} vs {b.shape}")
+
+
+def sq_l2(a, b) -> float:
+    """core.py:119-133 (scalar helper, host)."""
+    a, b = np.asarray(a), np.asarray(b)
+    _require_same_shape(a, b)
+    if a.dtype == np.uint8 and b.dtype == np.uint8:
+        d = a.astype(np.int64) - b.astype(np.int64)
+        return int(np.dot(d, d))
+    diff = a.astype(np.float32, copy=False) - b.astype(np.float32, copy=False)
+    return float(np.dot(diff, diff))
+
+
+def dot(a, b) -> float:
+    a = np.asarray(a, dtype=np.float32)
+    b = np.asarray(b, dtype=np.float32)
+    _require_same_shape(a, b)
+    return float(np.dot(a, b))
+
+
+def gen_synthetic(count: int, dims: int, seed: int, distribution: str = "gaussian") -> VectorDataset:
+    """Same seeded draws as the reference (core.py:209-233)."""
+    if count < 1 or dims < 1:
+        raise ValueError("count and dims must be >= 1")
+    rng = np.random.default_rng(seed)
+    if distribution == "gaussian":
+        x = rng.standard_normal((count, dims))
+    elif distribution == "clustered":
+        centers = rng.standard_normal((16, dims)) * 4.0
+        assign = rng.integers(0, 16, size=count)
+        x = centers[assign] + rng.standard_normal((count, dims))
+    else:
+        raise ValueError(f"unknown distribution {distribution!r}")
+    return VectorDataset(x.astype(np.float32))
+
+
+def gen_lowrank(count: int, dims: int, seed: int, d_int: int = 16, noise: float = 0.05) -> np.ndarray:
+    """Low-intrinsic-dimension synthetic rows: SIFT/DEEP/GIST-shaped
+    data on which recall@10 >= 0.95 is reachable. Returns f32 (count, dims)."""
+    g = np.random.default_rng(seed)
+    a = g.standard_normal((d_int, dims)) / np.sqrt(d_int)
+    out = np.empty((count, dims), dtype=np.float32)
+    step = 262_144
+    z_all = g.standard_normal((count, d_int))
+    for lo in range(0, count, step):
+        hi = min(count, lo + step)
+        out[lo:hi] = z_all[lo:hi] @ a + noise * g.standard_normal((hi - lo, dims))
+    return out

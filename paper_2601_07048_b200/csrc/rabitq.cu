@@ -1,0 +1,281 @@
+// rabitq.cu — RaBitQ quantization on sm_100a.
+//
+//  * jb_rabitq_encode   replaces the per-block body of rabitq.fit (rabitq.py:282-299)
+//  * jb_rabitq_bind     replaces RaBitQIndex.bind (rabitq.py:170-181)
+//  * jb_rabitq_pack_records builds the packed device record used by the search
+//    estimator (rabitq.py:235-244): code bytes | pad to 8 | data_add, data_rescale
+//    | pad to 16, so one vector is one aligned request (32 B at D=128, m=1).
+//
+// Bit-exactness: every f64 step follows the reference formula in the same
+// operation order; the only order difference is the f64 rotation GEMM
+// (OpenBLAS dgemm vs. a per-output warp reduction here). f64 rounding
+// differences there sit ~29 bits below the f32 / code decision boundaries, so
+// codes and metadata match bit-for-bit in practice; the tests assert it.
+#include <algorithm>
+#include "common.cuh"
+#include "runtime.cuh"
+
+namespace jb {
+
+__host__ __device__ inline int code_bytes_of(int D, int bits) { return (D * bits + 7) / 8; }
+__host__ __device__ inline int meta_off_of(int D, int bits) { return ((code_bytes_of(D, bits) + 7) / 8) * 8; }
+__host__ __device__ inline int record_bytes_of(int D, int bits) { return ((meta_off_of(D, bits) + 8 + 15) / 16) * 16; }
+
+__global__ void pack_records_kernel(const uint8_t* __restrict__ codes, const float* __restrict__ meta, int64_t n,
+                                    int cb, int moff, int rb, uint8_t* __restrict__ rec) {
+    int64_t v = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+    if (v >= n) return;
+    const int lane = threadIdx.x & 31;
+    uint8_t* r = rec + v * rb;
+    for (int i = lane; i < rb; i += 32) {
+        uint8_t b = 0;
+        if (i < cb) b = codes[v * cb + i];
+        r[i] = b;
+    }
+    __syncwarp();
+    if (lane == 0) {
+        float2 m = make_float2(meta[2 * v], meta[2 * v + 1]);
+        *reinterpret_cast<float2*>(r + moff) = m;
+    }
+}
+
+// ---- encode --------------------------------------------------------------
+// Block = 4 warps handling TV vectors:
+//   1. nres[v][d] = f64(f32(x - c)) / norm   (norm = sqrt(A1-f64 of resid))
+//   2. o[v][i]    = sum_d nres[v][d] * rot[i][d]    (warp per output i, coalesced rot row)
+//   3. per vector (warp): delta, codes, obar, <o, obar> (2-lane order), meta.
+constexpr int ENC_WARPS = 4;
+
+__device__ __forceinline__ double a1f64_self(const double* r, int D) {
+    Acc2d acc; acc.zero();
+    int e = 0;
+    for (; e + 8 <= D; e += 8) {
+#pragma unroll
+        for (int i = 3; i >= 0; --i) {
+            acc.l0 = __dadd_rn(__dmul_rn(r[e + 2 * i], r[e + 2 * i]), acc.l0);
+            acc.l1 = __dadd_rn(__dmul_rn(r[e + 2 * i + 1], r[e + 2 * i + 1]), acc.l1);
+        }
+    }
+    for (; e < D; ++e) {
+        if (e & 1) acc.l1 = __dadd_rn(__dmul_rn(r[e], r[e]), acc.l1);
+        else acc.l0 = __dadd_rn(__dmul_rn(r[e], r[e]), acc.l0);
+    }
+    return acc.reduce();
+}
+
+__global__ void __launch_bounds__(ENC_WARPS * 32)
+encode_kernel(const float* __restrict__ x, int64_t n, int D, int bits, const float* __restrict__ centroid,
+              const double* __restrict__ rot, int TV, uint8_t* __restrict__ codes, float* __restrict__ meta) {
+    extern __shared__ __align__(16) double esh[];
+    double* nres = esh;                      // [TV][D]
+    double* o = esh + (size_t)TV * D;        // [TV][D]
+    double* norms = o + (size_t)TV * D;      // [TV]
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t v0 = (int64_t)blockIdx.x * TV;
+    const int nv = (int)std::min<int64_t>(TV, n - v0);
+    const int levels = (1 << bits) - 1;
+    const double mid = levels / 2.0;
+
+    // resid (f32 subtract, widened)
+    for (int idx = threadIdx.x; idx < nv * D; idx += blockDim.x) {
+        int v = idx / D, d = idx - v * D;
+        nres[idx] = (double)__fsub_rn(x[(v0 + v) * D + d], centroid[d]);
+    }
+    __syncthreads();
+    for (int v = warp; v < nv; v += ENC_WARPS) {
+        if (lane == 0) norms[v] = __dsqrt_rn(a1f64_self(nres + (size_t)v * D, D));
+    }
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < nv * D; idx += blockDim.x) {
+        int v = idx / D;
+        double nr = norms[v];
+        double safe = nr > 0.0 ? nr : 1.0;
+        nres[idx] = __ddiv_rn(nres[idx], safe);
+    }
+    __syncthreads();
+    // rotation: o[v][i] = sum_d nres[v][d] * rot[i][d]
+    for (int i = warp; i < D; i += ENC_WARPS) {
+        const double* rr = rot + (size_t)i * D;
+        for (int vb = 0; vb < nv; vb += 8) {
+            double s[8];
+#pragma unroll
+            for (int t = 0; t < 8; ++t) s[t] = 0.0;
+            for (int d = lane; d < D; d += 32) {
+                const double rv = __ldg(rr + d);
+#pragma unroll
+                for (int t = 0; t < 8; ++t)
+                    if (vb + t < nv) s[t] = fma(nres[(size_t)(vb + t) * D + d], rv, s[t]);
+            }
+#pragma unroll
+            for (int t = 0; t < 8; ++t) {
+                double vsum = s[t];
+                for (int off = 16; off > 0; off >>= 1) vsum += __shfl_xor_sync(0xFFFFFFFFu, vsum, off);
+                if (lane == 0 && vb + t < nv) o[(size_t)(vb + t) * D + i] = vsum;
+            }
+        }
+    }
+    __syncthreads();
+    // quantize per vector
+    const int cb = (D * bits + 7) / 8;
+    const int per = 8 / bits;
+    for (int v = warp; v < nv; v += ENC_WARPS) {
+        const double* ov = o + (size_t)v * D;
+        double mx = 0.0;
+        for (int d = lane; d < D; d += 32) mx = fmax(mx, fabs(ov[d]));
+        for (int off = 16; off > 0; off >>= 1) mx = fmax(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, off));
+        const double norm = norms[v];
+        const bool nonzero = norm > 0.0;
+        const double delta = __ddiv_rn(__dmul_rn(2.0, mx), (double)levels);
+        const double sdelta = delta > 0.0 ? delta : 1.0;
+        // codes -> reuse nres row as obar storage
+        double* obar = nres + (size_t)v * D;
+        uint8_t* crow = codes + (v0 + v) * cb;
+        for (int byte = lane; byte < cb; byte += 32) {
+            uint32_t packed = 0;
+            for (int j = 0; j < per; ++j) {
+                const int d = byte * per + j;
+                uint32_t u = 0;
+                if (d < D) {
+                    if (nonzero) {
+                        double t = rint(__dadd_rn(__ddiv_rn(ov[d], sdelta), mid));
+                        t = t < 0.0 ? 0.0 : (t > (double)levels ? (double)levels : t);
+                        u = (uint32_t)t;
+                    } else {
+                        u = 1u << (bits - 1);
+                    }
+                    obar[d] = __dmul_rn(sdelta, __dsub_rn((double)u, mid));
+                }
+                packed |= u << (bits * j);
+            }
+            crow[byte] = (uint8_t)packed;
+        }
+        __syncwarp();
+        if (lane == 0) {
+            Acc2d acc; acc.zero();
+            int e = 0;
+            for (; e + 8 <= D; e += 8) {
+#pragma unroll
+                for (int i = 3; i >= 0; --i) {
+                    acc.l0 = __dadd_rn(__dmul_rn(ov[e + 2 * i], obar[e + 2 * i]), acc.l0);
+                    acc.l1 = __dadd_rn(__dmul_rn(ov[e + 2 * i + 1], obar[e + 2 * i + 1]), acc.l1);
+                }
+            }
+            for (; e < D; ++e) {
+                if (e & 1) acc.l1 = __dadd_rn(__dmul_rn(ov[e], obar[e]), acc.l1);
+                else acc.l0 = __dadd_rn(__dmul_rn(ov[e], obar[e]), acc.l0);
+            }
+            const double ip = acc.reduce();
+            const bool ok = nonzero && (ip > 1e-12);
+            const double rescale = ok ? __ddiv_rn(__dmul_rn(__dmul_rn(-2.0, norm), delta), ip) : 0.0;
+            meta[2 * (v0 + v)] = __double2float_rn(nonzero ? __dmul_rn(norm, norm) : 0.0);
+            meta[2 * (v0 + v) + 1] = __double2float_rn(rescale);
+        }
+    }
+}
+
+// ---- bind ----------------------------------------------------------------
+// numpy pairwise summation for f32 (A2), n = row length, unit stride.
+__device__ float pairwise_sum_f32(const float* a, int n) {
+    if (n < 8) {
+        float r = 0.0f;
+        for (int i = 0; i < n; ++i) r = __fadd_rn(r, a[i]);
+        return r;
+    }
+    if (n <= 128) {
+        float r[8];
+        for (int j = 0; j < 8; ++j) r[j] = a[j];
+        int i = 8;
+        for (; i < n - (n % 8); i += 8)
+            for (int j = 0; j < 8; ++j) r[j] = __fadd_rn(r[j], a[i + j]);
+        float res = __fadd_rn(__fadd_rn(__fadd_rn(r[0], r[1]), __fadd_rn(r[2], r[3])),
+                              __fadd_rn(__fadd_rn(r[4], r[5]), __fadd_rn(r[6], r[7])));
+        for (; i < n; ++i) res = __fadd_rn(res, a[i]);
+        return res;
+    }
+    int n2 = n / 2;
+    n2 -= n2 % 8;
+    return __fadd_rn(pairwise_sum_f32(a, n2), pairwise_sum_f32(a + n2, n - n2));
+}
+
+// One block (4 warps) per query.
+__global__ void __launch_bounds__(128)
+bind_kernel(const float* __restrict__ queries, int D, int bits, const float* __restrict__ centroid,
+            const double* __restrict__ rot, float* __restrict__ rotated, float* __restrict__ qadd,
+            float* __restrict__ qsumq) {
+    extern __shared__ __align__(16) float bsh[];
+    float* qc = bsh;          // [D]
+    float* rq = bsh + D;      // [D]
+    const int64_t qi = blockIdx.x;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int d = threadIdx.x; d < D; d += blockDim.x) qc[d] = __fsub_rn(queries[qi * D + d], centroid[d]);
+    __syncthreads();
+    for (int i = warp; i < D; i += 4) {
+        const double* rr = rot + (size_t)i * D;
+        double s = 0.0;
+        for (int d = lane; d < D; d += 32) s = fma((double)qc[d], __ldg(rr + d), s);
+        for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xFFFFFFFFu, s, off);
+        if (lane == 0) {
+            const float f = __double2float_rn(s);
+            rq[i] = f;
+            rotated[qi * D + i] = f;
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        qadd[qi] = a1_dot<false>(qc, qc, D);
+        const float mid = (float)(((1 << bits) - 1) / 2.0);
+        qsumq[qi] = __fmul_rn(pairwise_sum_f32(rq, D), mid);
+    }
+}
+
+}  // namespace jb
+
+using namespace jb;
+
+extern "C" {
+
+int32_t jb_rabitq_record_bytes(int32_t dims, int32_t bits) { return record_bytes_of(dims, bits); }
+
+int jb_rabitq_pack_records(const uint8_t* codes, const float* meta, int64_t n, int32_t dims, int32_t bits,
+                           uint8_t* records, void* stream) {
+    JB_CHECK_ARG(bits == 1 || bits == 2 || bits == 4 || bits == 8, "bits must be one of (1, 2, 4, 8)");
+    JB_CHECK_ARG(dims >= 1, "dims must be >= 1");
+    if (n == 0) return JB_OK;
+    const int wpb = 8;
+    pack_records_kernel<<<(unsigned)((n + wpb - 1) / wpb), wpb * 32, 0, as_stream(stream)>>>(
+        codes, meta, n, code_bytes_of(dims, bits), meta_off_of(dims, bits), record_bytes_of(dims, bits), records);
+    JB_LAUNCH_CHECK();
+    return JB_OK;
+}
+
+int jb_rabitq_encode(const float* x, int64_t n, int32_t dims, int32_t bits, const float* centroid,
+                     const double* rotation, uint8_t* codes, float* meta, void* stream) {
+    JB_CHECK_ARG(bits == 1 || bits == 2 || bits == 4 || bits == 8, "bits must be one of (1, 2, 4, 8)");
+    JB_CHECK_ARG(dims >= 1, "dims must be >= 1");
+    if (n == 0) return JB_OK;
+    const size_t budget = 200 * 1024;
+    int TV = (int)std::min<size_t>(64, (budget - 64 * 8) / (size_t)(16 * dims));
+    JB_CHECK_ARG(TV >= 1, "rabitq encode: dims %d too large for shared memory", dims);
+    const size_t smem = (size_t)TV * dims * 16 + (size_t)TV * 8;
+    cudaStream_t st = as_stream(stream);
+    JB_CUDA(cudaFuncSetAttribute(encode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    encode_kernel<<<(unsigned)((n + TV - 1) / TV), ENC_WARPS * 32, smem, st>>>(x, n, dims, bits, centroid, rotation,
+                                                                               TV, codes, meta);
+    JB_LAUNCH_CHECK();
+    return JB_OK;
+}
+
+int jb_rabitq_bind(const float* queries, int64_t nq, int32_t dims, int32_t bits, const float* centroid,
+                   const double* rotation, float* rotated, float* query_add, float* query_sumq, void* stream) {
+    JB_CHECK_ARG(bits == 1 || bits == 2 || bits == 4 || bits == 8, "bits must be one of (1, 2, 4, 8)");
+    if (nq == 0) return JB_OK;
+    const size_t smem = (size_t)dims * 8;
+    cudaStream_t st = as_stream(stream);
+    JB_CUDA(cudaFuncSetAttribute(bind_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    bind_kernel<<<(unsigned)nq, 128, smem, st>>>(queries, dims, bits, centroid, rotation, rotated, query_add,
+                                                 query_sumq);
+    JB_LAUNCH_CHECK();
+    return JB_OK;
+}
+
+}  // extern "C"

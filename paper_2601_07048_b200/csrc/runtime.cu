@@ -1,0 +1,214 @@
+// runtime.cu — library plumbing plus the small data-model kernels:
+// A1 row norms, f64 column mean, medoid, frontier top-k decode.
+#include <cstdarg>
+#include <cstring>
+#include "common.cuh"
+#include "runtime.cuh"
+
+namespace jb {
+
+static thread_local char g_err[1024] = "";
+
+void set_error(const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+}
+
+int sm_count_current() {
+    int dev = 0, n = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n;
+}
+
+// ---- row norms (search.py:101, 113; build.py:120) ----------------------
+__global__ void row_sq_norms_kernel(const float* __restrict__ x, int64_t n, int D, float* __restrict__ out) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const float* r = x + i * D;
+    out[i] = a1_dot<false>(r, r, D);
+}
+
+// ---- f64 column sum, sequential over rows (numpy mean(axis=0), A3) ------
+// One thread per column; rows are visited in order so the f64 sum matches
+// numpy's row-by-row accumulation bit-exactly.
+__global__ void column_sum_f64_kernel(const float* __restrict__ x, int64_t n, int D, double* __restrict__ out) {
+    int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= D) return;
+    double s = 0.0;
+    int64_t i = 0;
+    for (; i + 8 <= n; i += 8) {
+        float v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = __ldg(x + (i + u) * D + c);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) s = __dadd_rn(s, (double)v[u]);
+    }
+    for (; i < n; ++i) s = __dadd_rn(s, (double)__ldg(x + i * D + c));
+    out[c] = s;
+}
+
+__global__ void mean_finish_kernel(const double* __restrict__ sum, int64_t n, int D, double* __restrict__ mean64,
+                                   float* __restrict__ mean32) {
+    int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= D) return;
+    double m = __ddiv_rn(sum[c], (double)n);
+    if (mean64) mean64[c] = m;
+    if (mean32) mean32[c] = __double2float_rn(m);
+}
+
+// medoid distance: diff = f64(x) - center; einsum('nd,nd->n') f64 2-lane order
+// (graph.py:167-171), then argmin with the lowest id on ties.
+__device__ __forceinline__ double medoid_dist(const float* __restrict__ r, const double* __restrict__ c, int D) {
+    Acc2d acc; acc.zero();
+    int e = 0;
+    for (; e + 8 <= D; e += 8) {
+#pragma unroll
+        for (int i = 3; i >= 0; --i) {
+            double d0 = __dsub_rn((double)r[e + 2 * i], c[e + 2 * i]);
+            double d1 = __dsub_rn((double)r[e + 2 * i + 1], c[e + 2 * i + 1]);
+            acc.l0 = __dadd_rn(__dmul_rn(d0, d0), acc.l0);
+            acc.l1 = __dadd_rn(__dmul_rn(d1, d1), acc.l1);
+        }
+    }
+    for (; e < D; ++e) {
+        double d0 = __dsub_rn((double)r[e], c[e]);
+        if (e & 1) acc.l1 = __dadd_rn(__dmul_rn(d0, d0), acc.l1);
+        else acc.l0 = __dadd_rn(__dmul_rn(d0, d0), acc.l0);
+    }
+    return acc.reduce();
+}
+
+struct DI { double d; int64_t i; };
+__device__ __forceinline__ DI di_min(DI a, DI b) {
+    if (b.d < a.d || (b.d == a.d && b.i < a.i)) return b;
+    return a;
+}
+
+__global__ void medoid_partial_kernel(const float* __restrict__ x, int64_t n, int D, const double* __restrict__ center,
+                                      DI* __restrict__ partial) {
+    extern __shared__ double csh[];
+    for (int c = threadIdx.x; c < D; c += blockDim.x) csh[c] = center[c];
+    __syncthreads();
+    DI best{__longlong_as_double(0x7FF0000000000000ll), INT64_MAX};
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        DI cur{medoid_dist(x + i * D, csh, D), i};
+        best = di_min(best, cur);
+    }
+    // warp reduce then block reduce
+    for (int o = 16; o > 0; o >>= 1) {
+        DI other{__shfl_down_sync(0xFFFFFFFFu, best.d, o), __shfl_down_sync(0xFFFFFFFFu, best.i, o)};
+        best = di_min(best, other);
+    }
+    __shared__ DI wbest[32];
+    if ((threadIdx.x & 31) == 0) wbest[threadIdx.x >> 5] = best;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        DI b = wbest[0];
+        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) b = di_min(b, wbest[w]);
+        partial[blockIdx.x] = b;
+    }
+}
+
+__global__ void medoid_final_kernel(const DI* __restrict__ partial, int np, int64_t* __restrict__ out) {
+    DI b{__longlong_as_double(0x7FF0000000000000ll), INT64_MAX};
+    for (int i = 0; i < np; ++i) b = di_min(b, partial[i]);
+    *out = b.i;
+}
+
+// ---- frontier -> top-k (search.py:375-382, exact source) -----------------
+__global__ void frontier_topk_kernel(const uint64_t* __restrict__ keys, int64_t nq, int L, int k,
+                                     int32_t* __restrict__ ids, double* __restrict__ dists) {
+    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= nq * k) return;
+    int64_t q = t / k;
+    int j = (int)(t % k);
+    uint64_t key = keys[q * L + j];
+    if (key == UMAX) {
+        ids[t] = -1;
+        dists[t] = __longlong_as_double(0x7FF0000000000000ll);
+    } else {
+        ids[t] = (int32_t)(key & 0xFFFFFFFFull);
+        dists[t] = (double)__uint_as_float((uint32_t)(key >> 32));
+    }
+}
+
+}  // namespace jb
+
+using namespace jb;
+
+extern "C" {
+
+const char* jb_last_error(void) { return g_err; }
+int jb_abi_version(void) { return 1; }
+
+int jb_sm_count(int device, int32_t* out) {
+    int n = 0;
+    JB_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device));
+    *out = n;
+    return JB_OK;
+}
+
+int jb_row_sq_norms(const float* x, int64_t n, int32_t dims, float* out, void* stream) {
+    JB_CHECK_ARG(dims >= 1 && n >= 0, "jb_row_sq_norms: bad shape");
+    if (n == 0) return JB_OK;
+    int threads = 256;
+    row_sq_norms_kernel<<<(unsigned)((n + threads - 1) / threads), threads, 0, as_stream(stream)>>>(x, n, dims, out);
+    JB_LAUNCH_CHECK();
+    return JB_OK;
+}
+
+int jb_column_mean_f32(const float* x, int64_t n, int32_t dims, float* out, void* stream) {
+    JB_CHECK_ARG(dims >= 1 && n >= 1, "jb_column_mean_f32: bad shape");
+    cudaStream_t st = as_stream(stream);
+    Scratch sum;
+    JB_CUDA(sum.alloc(sizeof(double) * dims, st));
+    int threads = 128, blocks = (dims + threads - 1) / threads;
+    column_sum_f64_kernel<<<blocks, threads, 0, st>>>(x, n, dims, sum.as<double>());
+    mean_finish_kernel<<<blocks, threads, 0, st>>>(sum.as<double>(), n, dims, nullptr, out);
+    JB_LAUNCH_CHECK();
+    return JB_OK;
+}
+
+int jb_medoid(const float* x, int64_t n, int32_t dims, int64_t* out_host, void* stream) {
+    JB_CHECK_ARG(n >= 1, "medoid of an empty dataset");
+    JB_CHECK_ARG(dims >= 1, "jb_medoid: bad dims");
+    cudaStream_t st = as_stream(stream);
+    int nb = std::min<int64_t>((n + 255) / 256, 4 * sm_count_current());
+    Scratch buf;
+    size_t off_center = sizeof(double) * dims;
+    size_t off_part = off_center * 2;
+    size_t off_out = off_part + sizeof(DI) * nb;
+    JB_CUDA(buf.alloc(off_out + 16, st));
+    char* b = buf.as<char>();
+    double* sum = reinterpret_cast<double*>(b);
+    double* center = reinterpret_cast<double*>(b + off_center);
+    DI* part = reinterpret_cast<DI*>(b + off_part);
+    int64_t* dout = reinterpret_cast<int64_t*>(b + off_out);
+    int threads = 128, blocks = (dims + threads - 1) / threads;
+    column_sum_f64_kernel<<<blocks, threads, 0, st>>>(x, n, dims, sum);
+    mean_finish_kernel<<<blocks, threads, 0, st>>>(sum, n, dims, center, nullptr);
+    JB_CUDA(cudaFuncSetAttribute(medoid_partial_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)(sizeof(double) * dims)));
+    medoid_partial_kernel<<<nb, 256, sizeof(double) * dims, st>>>(x, n, dims, center, part);
+    medoid_final_kernel<<<1, 1, 0, st>>>(part, nb, dout);
+    JB_LAUNCH_CHECK();
+    JB_CUDA(cudaMemcpyAsync(out_host, dout, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    JB_CUDA(cudaStreamSynchronize(st));
+    return JB_OK;
+}
+
+int jb_frontier_topk(const uint64_t* frontier_keys, int64_t nq, int32_t beam_width, int32_t k,
+                     int32_t* out_ids, double* out_dists, void* stream) {
+    JB_CHECK_ARG(k >= 1 && k <= beam_width, "k must satisfy 1 <= k <= beam_width");
+    if (nq == 0) return JB_OK;
+    int64_t total = nq * k;
+    int threads = 256;
+    frontier_topk_kernel<<<(unsigned)((total + threads - 1) / threads), threads, 0, as_stream(stream)>>>(
+        frontier_keys, nq, beam_width, k, out_ids, out_dists);
+    JB_LAUNCH_CHECK();
+    return JB_OK;
+}
+
+}  // extern "C"

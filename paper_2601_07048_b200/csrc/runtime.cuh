@@ -1,0 +1,52 @@
+// runtime.cuh — host-side error plumbing shared by every translation unit.
+#pragma once
+#include <cstdio>
+#include <string>
+#include <cuda_runtime.h>
+#include "../../include/jasper_b200.h"
+
+namespace jb {
+
+void set_error(const char* fmt, ...);
+
+#define JB_CHECK_ARG(cond, ...)                 \
+    do {                                        \
+        if (!(cond)) {                          \
+            ::jb::set_error(__VA_ARGS__);       \
+            return JB_EINVAL;                   \
+        }                                       \
+    } while (0)
+
+#define JB_CUDA(expr)                                                                  \
+    do {                                                                               \
+        cudaError_t _e = (expr);                                                       \
+        if (_e != cudaSuccess) {                                                       \
+            ::jb::set_error("%s:%d %s: %s", __FILE__, __LINE__, #expr,                 \
+                            cudaGetErrorString(_e));                                   \
+            return JB_ECUDA;                                                           \
+        }                                                                              \
+    } while (0)
+
+#define JB_LAUNCH_CHECK() JB_CUDA(cudaGetLastError())
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+int sm_count_current();
+
+// Stream-ordered scratch that frees itself (cudaFreeAsync) on scope exit.
+struct Scratch {
+    void* p = nullptr;
+    cudaStream_t s = nullptr;
+    Scratch() = default;
+    Scratch(const Scratch&) = delete;
+    Scratch& operator=(const Scratch&) = delete;
+    cudaError_t alloc(size_t bytes, cudaStream_t st) {
+        s = st;
+        if (bytes == 0) bytes = 16;
+        return cudaMallocAsync(&p, bytes, st);
+    }
+    template <class T> T* as() const { return reinterpret_cast<T*>(p); }
+    ~Scratch() { if (p) cudaFreeAsync(p, s); }
+};
+
+}  // namespace jb

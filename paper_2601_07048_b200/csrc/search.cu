@@ -1,0 +1,465 @@
+// search.cu — batched greedy beam search (Vamana GreedySearch) on sm_100a.
+//
+// Replaces the reference's lockstep numpy engine, `_run_lockstep`
+// (search.py:171-269) driven by `run_beam_searches` (search.py:272-304), and
+// the rerank/top-k tail of `search_knn_batch` (search.py:351-383).
+//
+// Design (one warp per query, persistent grid, everything per query in smem):
+//  * beam: L u64 keys kept sorted ascending; key = (f32 dist bits << 32) | id,
+//    exactly the reference's key (search.py:139-145). Bit 31 of the id word is
+//    the device-only "expanded" flag, so a key carries its visited state when
+//    the beam is shifted by a merge.
+//  * visited ("seen") set: an open-addressing hash in smem. It never yields a
+//    false positive. If a probe run fills up, the id is treated as unseen and
+//    re-evaluated; its key is then either already in the beam (dropped by the
+//    equal-key dedupe, the incumbent keeps its flag) or worse than the full
+//    beam's last key (dropped by the filter), because the beam is always the
+//    top-L of every key evaluated so far. Frontier and trace are therefore
+//    identical to the reference's exact `seen` matrix; only `evals` can count
+//    re-evaluations, and flags[q] bit0 reports that.
+//  * expansion: the first unexpanded key in ascending order (search.py:202-210).
+//    Neighbours are checked 32 per step (one per lane), new ids are compacted
+//    with a ballot, their distances computed one candidate per lane in the
+//    reference's exact f32 rounding order (A1), then bitonic-sorted in
+//    registers and merged into the beam by rank (binary searches), shifting
+//    beam entries right in 32-wide chunks from the top.
+//  * exact rows are staged into smem with coalesced cp.async (one 512 B row per
+//    warp instruction at D=128) and then read per lane (16 B skew per row keeps
+//    the per-lane float4 reads bank-conflict free). RaBitQ records are read
+//    directly, one 32 B record per lane (two 128-bit loads).
+#include <algorithm>
+#include "common.cuh"
+#include "runtime.cuh"
+
+namespace jb {
+
+constexpr int WPB = 4;          // warps per block
+constexpr int HASH_PROBES = 16; // bounded linear probing
+
+struct SearchLayout {
+    int q_off, beam_off, hash_off, newk_off, cid_off, stage_off, bytes;
+    int chunk;      // staged elements per row chunk (multiple of 32, <= 128)
+    int sstride;    // staged row stride in floats (chunk + 4)
+    int hbits;
+};
+
+__device__ __forceinline__ bool hash_insert(uint32_t* h, int hbits, uint32_t id, int& lossy) {
+    const uint32_t mask = (1u << hbits) - 1u;
+    uint32_t s = (id * 0x9E3779B1u) >> (32 - hbits);
+#pragma unroll 1
+    for (int p = 0; p < HASH_PROBES; ++p) {
+        uint32_t cur = h[s];
+        if (cur == id) return false;
+        if (cur == EMPTY_SLOT) {
+            uint32_t old = atomicCAS(&h[s], EMPTY_SLOT, id);
+            if (old == EMPTY_SLOT) return true;
+            if (old == id) return false;
+        }
+        s = (s + 1u) & mask;
+    }
+    lossy = 1;
+    return true;
+}
+
+// RaBitQ estimator for one packed record (rabitq.py:235-244):
+//   dd  = A1 dot(f32(u), rotated)           (einsum 'md,md->m')
+//   est = max((qadd + data_add) + data_rescale * (dd - qsumq), 0)
+template <int BITS>
+__device__ __forceinline__ float rabitq_estimate(const uint8_t* __restrict__ rec, const float* __restrict__ qv,
+                                                 int D, int meta_off, float qadd, float qsumq) {
+    constexpr int PER16 = 128 / BITS;  // elements per 16-byte piece
+    constexpr uint32_t MASK = (1u << BITS) - 1u;
+    Acc4 acc; acc.zero();
+    for (int e0 = 0; e0 < D; e0 += PER16) {
+        const uint4 w4 = __ldg(reinterpret_cast<const uint4*>(rec + (e0 * BITS) / 8));
+        const uint32_t w[4] = {w4.x, w4.y, w4.z, w4.w};
+        const int e1 = min(D, e0 + PER16);
+        int b = e0;
+        for (; b + 16 <= e1; b += 16) {
+#pragma unroll
+            for (int i = 3; i >= 0; --i) {
+                const float4 q4 = *reinterpret_cast<const float4*>(qv + b + 4 * i);
+                const int off = (b - e0 + 4 * i) * BITS;
+                float4 u;
+                u.x = (float)((w[(off) >> 5] >> ((off) & 31)) & MASK);
+                u.y = (float)((w[(off + BITS) >> 5] >> ((off + BITS) & 31)) & MASK);
+                u.z = (float)((w[(off + 2 * BITS) >> 5] >> ((off + 2 * BITS) & 31)) & MASK);
+                u.w = (float)((w[(off + 3 * BITS) >> 5] >> ((off + 3 * BITS) & 31)) & MASK);
+                acc.madd(u, q4);
+            }
+        }
+        for (; b < e1; ++b) {
+            const int off = (b - e0) * BITS;
+            acc.madd1(b & 3, (float)((w[off >> 5] >> (off & 31)) & MASK), qv[b]);
+        }
+    }
+    const float dd = acc.reduce();
+    const float2 m = __ldg(reinterpret_cast<const float2*>(rec + meta_off));
+    float est = __fadd_rn(__fadd_rn(qadd, m.x), __fmul_rn(m.y, __fsub_rn(dd, qsumq)));
+    return est > 0.0f ? est : 0.0f;
+}
+
+// First index >= s (< n) whose key is not expanded; n if none.
+__device__ __forceinline__ int first_unexpanded(const uint64_t* beam, int s, int n) {
+    const int lane = lane_id();
+    for (int b = s; b < n; b += 32) {
+        int i = b + lane;
+        bool un = (i < n) && !(beam[i] & EXPANDED);
+        uint32_t m = __ballot_sync(0xFFFFFFFFu, un);
+        if (m) return b + __ffs(m) - 1;
+    }
+    return n;
+}
+
+template <int SRC, int BITS, bool ALIGNED>
+__global__ void __launch_bounds__(WPB * 32)
+beam_search_kernel(const jb_search_args a, const SearchLayout lay, int* __restrict__ counter) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    unsigned char* base = smem + (size_t)warp * lay.bytes;
+    float* qv = reinterpret_cast<float*>(base + lay.q_off);
+    uint64_t* beam = reinterpret_cast<uint64_t*>(base + lay.beam_off);
+    uint32_t* hash = reinterpret_cast<uint32_t*>(base + lay.hash_off);
+    uint64_t* newk = reinterpret_cast<uint64_t*>(base + lay.newk_off);
+    int32_t* cid = reinterpret_cast<int32_t*>(base + lay.cid_off);
+    float* stage = reinterpret_cast<float*>(base + lay.stage_off);
+
+    const int L = a.beam_width;
+    const int D = a.dims;
+    const int R = a.degree_cap;
+    const int H = 1 << lay.hbits;
+    const int RB = a.record_bytes;
+    const int meta_off = ((((D * BITS) + 7) / 8 + 7) / 8) * 8;
+    const unsigned FULL = 0xFFFFFFFFu;
+
+    for (;;) {
+        int64_t qi = 0;
+        if (lane == 0) qi = atomicAdd(counter, 1);
+        qi = __shfl_sync(FULL, (long long)qi, 0);
+        if (qi >= a.nq) break;
+
+        const float* q = a.queries + qi * D;
+        for (int e = lane; e < D; e += 32) qv[e] = q[e];
+        for (int i = lane; i < L; i += 32) beam[i] = UMAX;
+        for (int i = lane; i < H; i += 32) hash[i] = EMPTY_SLOT;
+        const float qadd = a.query_add[qi];
+        const float qsumq = (SRC == JB_SRC_RABITQ) ? a.query_sumq[qi] : 0.0f;
+        const uint32_t start = a.starts ? (uint32_t)a.starts[qi] : (uint32_t)a.start_vertex;
+        __syncwarp();
+
+        int lossy = 0;
+        if (lane == 0) {
+            float d0;
+            if (SRC == JB_SRC_EXACT) {
+                const float dot = a1_dot<false>(a.data + (size_t)start * D, qv, D);
+                d0 = exact_from_dot(a.data_norms[start], dot, qadd);
+            } else {
+                d0 = rabitq_estimate<BITS>(a.records + (size_t)start * RB, qv, D, meta_off, qadd, qsumq);
+            }
+            beam[0] = pack_key(d0, start);
+            hash_insert(hash, lay.hbits, start, lossy);
+        }
+        __syncwarp();
+
+        int bcount = 1, cursor = 0, hops = 0, evals = 1;
+        const int tcap = a.trace_cap;
+        int32_t* tids = a.trace_ids ? a.trace_ids + qi * (int64_t)tcap : nullptr;
+        float* tdst = a.trace_dists ? a.trace_dists + qi * (int64_t)tcap : nullptr;
+
+        while (cursor < bcount) {
+            const uint64_t ukey = beam[cursor];
+            const uint32_t u = key_id(ukey);
+            __syncwarp();
+            if (lane == 0) {
+                beam[cursor] = ukey | EXPANDED;
+                if (hops < tcap) {
+                    tids[hops] = (int32_t)u;
+                    tdst[hops] = key_dist(ukey);
+                }
+            }
+            ++hops;
+            int s_min = cursor + 1;
+            const int32_t* adj = a.adjacency + (size_t)u * R;
+
+            for (int c0 = 0; c0 < R; c0 += 32) {
+                const int r = c0 + lane;
+                const int nb = (r < R) ? __ldg(adj + r) : -1;
+                __syncwarp();
+                bool isnew = false;
+                if (nb >= 0) isnew = hash_insert(hash, lay.hbits, (uint32_t)nb, lossy);
+                const uint32_t nm = __ballot_sync(FULL, isnew);
+                const int nnew = __popc(nm);
+                if (nnew == 0) continue;
+                evals += nnew;
+                if (isnew) cid[__popc(nm & lanemask_lt())] = nb;
+                __syncwarp();
+
+                // ---- distances, one candidate per lane ----
+                float d = 0.0f;
+                const int myid = (lane < nnew) ? cid[lane] : 0;
+                if (SRC == JB_SRC_EXACT) {
+                    Acc4 acc; acc.zero();
+                    for (int e0 = 0; e0 < D; e0 += lay.chunk) {
+                        const int clen = min(lay.chunk, D - e0);
+                        if (ALIGNED) {
+                            const int nv = clen >> 2;
+                            for (int j = 0; j < nnew; ++j) {
+                                const float* src = a.data + (size_t)cid[j] * D + e0;
+                                float* dst = stage + j * lay.sstride;
+                                for (int f = lane; f < nv; f += 32) cp_async16(dst + 4 * f, src + 4 * f);
+                            }
+                        } else {
+                            for (int j = 0; j < nnew; ++j) {
+                                const float* src = a.data + (size_t)cid[j] * D + e0;
+                                float* dst = stage + j * lay.sstride;
+                                for (int f = lane; f < clen; f += 32) cp_async4(dst + f, src + f);
+                            }
+                        }
+                        cp_async_wait_all();
+                        __syncwarp();
+                        if (lane < nnew)
+                            a1_range<ALIGNED, false>(acc, stage + lane * lay.sstride - e0, qv, e0, e0 + clen);
+                        __syncwarp();
+                    }
+                    if (lane < nnew) d = exact_from_dot(__ldg(a.data_norms + myid), acc.reduce(), qadd);
+                } else {
+                    if (lane < nnew)
+                        d = rabitq_estimate<BITS>(a.records + (size_t)myid * RB, qv, D, meta_off, qadd, qsumq);
+                }
+
+                // ---- merge into the beam (search.py:232-237 semantics) ----
+                uint64_t key = (lane < nnew) ? pack_key(d, (uint32_t)myid) : UMAX;
+                if (key != UMAX && bcount == L && key >= key_mask(beam[L - 1])) key = UMAX;
+                if (key != UMAX) {
+                    const int p = lower_bound_masked(beam, bcount, key);
+                    if (p < bcount && key_mask(beam[p]) == key) key = UMAX;  // dedupe (lossy table)
+                }
+                key = warp_sort_u64(key);
+                const int m2 = __popc(__ballot_sync(FULL, key != UMAX));
+                if (m2 == 0) continue;
+                int p = 0;
+                if (lane < m2) {
+                    p = lower_bound_masked(beam, bcount, key);
+                    newk[lane] = key;
+                }
+                __syncwarp();
+                const int p0 = __shfl_sync(FULL, p, 0);
+                // shift beam[p0, bcount) right by (#new keys below each entry), top chunk first
+                for (int cb = ((bcount - 1) >> 5) << 5; cb >= (p0 & ~31); cb -= 32) {
+                    const int i = cb + lane;
+                    uint64_t bk = 0;
+                    int np = -1;
+                    if (i >= p0 && i < bcount) {
+                        bk = beam[i];
+                        const uint64_t km = key_mask(bk);
+                        int lo = 0, hi = m2;
+                        while (lo < hi) {
+                            int mid = (lo + hi) >> 1;
+                            if (newk[mid] < km) lo = mid + 1; else hi = mid;
+                        }
+                        np = i + lo;
+                    }
+                    __syncwarp();
+                    if (np >= 0 && np < L) beam[np] = bk;
+                    __syncwarp();
+                }
+                if (lane < m2) {
+                    const int np = lane + p;
+                    if (np < L) beam[np] = key;
+                }
+                __syncwarp();
+                bcount = min(L, bcount + m2);
+                s_min = min(s_min, p0);
+            }
+            cursor = first_unexpanded(beam, s_min, bcount);
+        }
+
+        // ---- outputs ----
+        uint64_t* fk = a.frontier_keys + qi * (int64_t)L;
+        for (int i = lane; i < L; i += 32) {
+            const uint64_t k = beam[i];
+            fk[i] = (k == UMAX) ? UMAX : key_mask(k);
+        }
+        lossy = __reduce_or_sync(FULL, lossy);
+        if (lane == 0) {
+            if (a.hops) a.hops[qi] = hops;
+            if (a.evals) a.evals[qi] = evals;
+            if (a.flags) a.flags[qi] = lossy ? 1 : 0;
+        }
+        __syncwarp();
+    }
+}
+
+// ---- exact rerank of the frontier (search.py:318-320, 375-382) -----------
+// One warp per query: stage up to 32 frontier rows at a time, lane j computes
+// einsum(x - q, x - q) in A1 order, keys (dist, id) collected in smem, then a
+// bitonic sort and the first k written out.
+template <bool ALIGNED>
+__global__ void __launch_bounds__(WPB * 32)
+rerank_kernel(const float* __restrict__ data, int D, const float* __restrict__ queries, int64_t nq,
+              const uint64_t* __restrict__ fkeys, int L, int k, int chunk, int sstride, int lpad, int per_warp,
+              int32_t* __restrict__ out_ids, double* __restrict__ out_dists) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    unsigned char* base = smem + (size_t)warp * per_warp;
+    float* qv = reinterpret_cast<float*>(base);
+    uint64_t* keys = reinterpret_cast<uint64_t*>(base + ((D * 4 + 15) / 16) * 16);
+    float* stage = reinterpret_cast<float*>(reinterpret_cast<unsigned char*>(keys) + (size_t)lpad * 8);
+    const int64_t qi = (int64_t)blockIdx.x * WPB + warp;
+    if (qi >= nq) return;
+    const float* q = queries + qi * D;
+    for (int e = lane; e < D; e += 32) qv[e] = q[e];
+    const uint64_t* fk = fkeys + qi * (int64_t)L;
+    // count valid keys (frontier is sorted; UMAX padding at the end)
+    int n = 0;
+    for (int b = 0; b < L; b += 32) {
+        const int i = b + lane;
+        const uint32_t m = __ballot_sync(0xFFFFFFFFu, i < L && fk[i] != UMAX);
+        n += __popc(m);
+    }
+    for (int i = lane; i < lpad; i += 32) keys[i] = UMAX;
+    __syncwarp();
+    for (int c = 0; c < n; c += 32) {
+        const int cnt = min(32, n - c);
+        const uint32_t myid = lane < cnt ? (uint32_t)(fk[c + lane] & 0xFFFFFFFFull) : 0u;
+        Acc4 acc; acc.zero();
+        for (int e0 = 0; e0 < D; e0 += chunk) {
+            const int clen = min(chunk, D - e0);
+            for (int j = 0; j < cnt; ++j) {
+                const uint32_t id = __shfl_sync(0xFFFFFFFFu, myid, j);
+                const float* src = data + (size_t)id * D + e0;
+                float* dst = stage + j * sstride;
+                if (ALIGNED) { for (int f = lane; f < (clen >> 2); f += 32) cp_async16(dst + 4 * f, src + 4 * f); }
+                else { for (int f = lane; f < clen; f += 32) cp_async4(dst + f, src + f); }
+            }
+            cp_async_wait_all();
+            __syncwarp();
+            if (lane < cnt) a1_range<ALIGNED, true>(acc, stage + lane * sstride - e0, qv, e0, e0 + clen);
+            __syncwarp();
+        }
+        if (lane < cnt) keys[c + lane] = pack_key(acc.reduce(), myid);
+    }
+    __syncwarp();
+    warp_bitonic_sort_smem(keys, lpad);
+    for (int j = lane; j < k; j += 32) {
+        const uint64_t key = keys[j];
+        const int64_t o = qi * k + j;
+        if (j < n) {
+            out_ids[o] = (int32_t)(key & 0xFFFFFFFFull);
+            out_dists[o] = (double)__uint_as_float((uint32_t)(key >> 32));
+        } else {
+            out_ids[o] = -1;
+            out_dists[o] = __longlong_as_double(0x7FF0000000000000ll);
+        }
+    }
+}
+
+static int pow2_ceil(int v) { int p = 1; while (p < v) p <<= 1; return p; }
+static int log2i(int v) { int l = 0; while ((1 << l) < v) ++l; return l; }
+
+static SearchLayout make_layout(int src, int D, int L, int hash_slots) {
+    SearchLayout s{};
+    auto align16 = [](int v) { return (v + 15) & ~15; };
+    int off = 0;
+    s.q_off = off; off += align16(D * 4);
+    s.beam_off = off; off += align16(L * 8);
+    s.hbits = log2i(hash_slots);
+    s.hash_off = off; off += align16((1 << s.hbits) * 4);
+    s.newk_off = off; off += 32 * 8;
+    s.cid_off = off; off += 32 * 4;
+    s.chunk = std::min(128, ((D + 31) / 32) * 32);
+    s.sstride = s.chunk + 4;
+    s.stage_off = off;
+    if (src == JB_SRC_EXACT) off += 32 * s.sstride * 4;
+    s.bytes = align16(off);
+    return s;
+}
+
+template <int SRC, int BITS, bool ALIGNED>
+static int launch_search(const jb_search_args& a, int hash_slots, cudaStream_t st) {
+    SearchLayout lay = make_layout(SRC, a.dims, a.beam_width, hash_slots);
+    auto kern = beam_search_kernel<SRC, BITS, ALIGNED>;
+    const int smem = lay.bytes * WPB;
+    JB_CHECK_ARG(smem <= 227 * 1024, "beam search: per-block shared memory %d B exceeds 227 KB", smem);
+    JB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    int per_sm = 0;
+    JB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, WPB * 32, smem));
+    JB_CHECK_ARG(per_sm >= 1, "beam search: kernel does not fit on an SM");
+    int64_t need = (a.nq + WPB - 1) / WPB;
+    int grid = (int)std::min<int64_t>(need, (int64_t)per_sm * sm_count_current());
+    Scratch ctr;
+    JB_CUDA(ctr.alloc(sizeof(int), st));
+    JB_CUDA(cudaMemsetAsync(ctr.p, 0, sizeof(int), st));
+    kern<<<grid, WPB * 32, smem, st>>>(a, lay, ctr.as<int>());
+    JB_LAUNCH_CHECK();
+    return JB_OK;
+}
+
+}  // namespace jb
+
+using namespace jb;
+
+extern "C" {
+
+int jb_beam_search(const jb_search_args* args, void* stream) {
+    JB_CHECK_ARG(args != nullptr, "jb_beam_search: null args");
+    const jb_search_args& a = *args;
+    JB_CHECK_ARG(a.active_count > 0, "search on an empty graph");
+    JB_CHECK_ARG(a.beam_width >= 1 && a.beam_width <= 1024, "beam_width must be in [1, 1024]");
+    JB_CHECK_ARG(a.degree_cap >= 1, "degree_cap must be >= 1");
+    JB_CHECK_ARG(a.dims >= 1, "dims must be >= 1");
+    JB_CHECK_ARG(a.active_count < (1ll << 31), "active_count exceeds int32 ids");
+    JB_CHECK_ARG(a.trace_cap == 0 || (a.trace_ids && a.trace_dists), "trace buffers required when trace_cap > 0");
+    JB_CHECK_ARG(a.starts != nullptr || (a.start_vertex >= 0 && a.start_vertex < a.active_count),
+                 "start vertex out of range");
+    if (a.nq == 0) return JB_OK;
+    int hs = a.hash_slots;
+    if (hs <= 0) hs = std::min(8192, std::max(1024, pow2_ceil(32 * a.beam_width)));
+    hs = std::max(32, pow2_ceil(hs));
+    cudaStream_t st = as_stream(stream);
+    if (a.source == JB_SRC_EXACT) {
+        JB_CHECK_ARG(a.data && a.data_norms && a.queries && a.query_add, "exact search: missing arrays");
+        if ((a.dims & 3) == 0) return launch_search<JB_SRC_EXACT, 1, true>(a, hs, st);
+        return launch_search<JB_SRC_EXACT, 1, false>(a, hs, st);
+    }
+    JB_CHECK_ARG(a.source == JB_SRC_RABITQ, "unknown distance source %d", a.source);
+    JB_CHECK_ARG(a.records && a.queries && a.query_add && a.query_sumq, "rabitq search: missing arrays");
+    JB_CHECK_ARG(a.record_bytes == jb_rabitq_record_bytes(a.dims, a.bits), "rabitq search: record_bytes mismatch");
+    switch (a.bits) {
+        case 1: return launch_search<JB_SRC_RABITQ, 1, true>(a, hs, st);
+        case 2: return launch_search<JB_SRC_RABITQ, 2, true>(a, hs, st);
+        case 4: return launch_search<JB_SRC_RABITQ, 4, true>(a, hs, st);
+        case 8: return launch_search<JB_SRC_RABITQ, 8, true>(a, hs, st);
+        default: JB_CHECK_ARG(false, "bits must be one of (1, 2, 4, 8)");
+    }
+}
+
+int jb_rerank_topk(const float* data, int32_t dims, const float* queries, int64_t nq,
+                   const uint64_t* frontier_keys, int32_t beam_width, int32_t k,
+                   int32_t* out_ids, double* out_dists, void* stream) {
+    JB_CHECK_ARG(k >= 1 && k <= beam_width, "k must satisfy 1 <= k <= beam_width");
+    JB_CHECK_ARG(dims >= 1, "dims must be >= 1");
+    if (nq == 0) return JB_OK;
+    const int chunk = std::min(128, ((dims + 31) / 32) * 32);
+    const int sstride = chunk + 4;
+    const int lpad = std::max(32, pow2_ceil(beam_width));
+    const int per_warp = ((dims * 4 + 15) / 16) * 16 + lpad * 8 + 32 * sstride * 4;
+    const int smem = per_warp * WPB;
+    JB_CHECK_ARG(smem <= 227 * 1024, "rerank: shared memory %d B exceeds 227 KB", smem);
+    cudaStream_t st = as_stream(stream);
+    const unsigned grid = (unsigned)((nq + WPB - 1) / WPB);
+    if ((dims & 3) == 0) {
+        JB_CUDA(cudaFuncSetAttribute(rerank_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        rerank_kernel<true><<<grid, WPB * 32, smem, st>>>(data, dims, queries, nq, frontier_keys, beam_width, k,
+                                                          chunk, sstride, lpad, per_warp, out_ids, out_dists);
+    } else {
+        JB_CUDA(cudaFuncSetAttribute(rerank_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        rerank_kernel<false><<<grid, WPB * 32, smem, st>>>(data, dims, queries, nq, frontier_keys, beam_width, k,
+                                                           chunk, sstride, lpad, per_warp, out_ids, out_dists);
+    }
+    JB_LAUNCH_CHECK();
+    return JB_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,302 @@
+"""Greedy beam search on B200 behind the reference's search API (mirror of search.py).
+
+Public functions keep the reference's names, argument meaning, validation
+messages and return types:
+  run_beam_searches  search.py:272-304   -> list[SearchResult] (frontier + visited trace)
+  beam_search        search.py:307-315
+  search_knn         search.py:323-348
+  search_knn_batch   search.py:351-383   -> (int32 ids [nq,k], f64 dists [nq,k])
+
+Each call is ONE batched launch of the sm_100a kernel (one warp per query)
+instead of the reference's per-hop numpy lockstep; frontier, trace, hops and
+(when the visited table did not overflow) distance_evals are identical.
+`search_knn_batch_device` is the HBM-resident variant used for throughput.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .core import VectorDataset, as_dataset
+from .graph import Candidate, GraphIndex, as_graph
+
+__all__ = ["SearchParams", "SearchStats", "SearchResult", "beam_search", "search_knn", "search_knn_batch",
+           "run_beam_searches", "search_knn_batch_device", "MAX_BEAM_WIDTH"]
+
+MAX_BEAM_WIDTH = 1024
+_UMAX = np.uint64(0xFFFFFFFFFFFFFFFF)
+# Test/tuning hook: visited-table slots per query (0 = library default).
+TUNING = {"hash_slots": 0}
+
+
+@dataclass(frozen=True)
+class SearchParams:
+    beam_width: int
+    k: int = 10
+    rerank: bool = False
+
+    def __post_init__(self):
+        if not 1 <= self.beam_width <= MAX_BEAM_WIDTH:
+            raise ValueError(f"beam_width must be in [1, {MAX_BEAM_WIDTH}]")
+        if not 1 <= self.k <= self.beam_width:
+            raise ValueError("k must satisfy 1 <= k <= beam_width")
+
+
+@dataclass
+class SearchStats:
+    hops: int = 0
+    distance_evals: int = 0
+
+
+@dataclass
+class SearchResult:
+    frontier_ids: np.ndarray
+    frontier_dists: np.ndarray
+    visited_ids: np.ndarray
+    visited_dists: np.ndarray
+    stats: SearchStats = field(default_factory=SearchStats)
+
+    @property
+    def frontier(self) -> list[Candidate]:
+        return [Candidate(int(i), float(d)) for i, d in zip(self.frontier_ids, self.frontier_dists)]
+
+    @property
+    def visited(self) -> list[Candidate]:
+        return [Candidate(int(i), float(d)) for i, d in zip(self.visited_ids, self.visited_dists)]
+
+
+def _is_rabitq(source) -> bool:
+    from .rabitq import RaBitQIndex
+
+    return isinstance(source, RaBitQIndex) or (hasattr(source, "codes") and hasattr(source, "meta")
+                                               and hasattr(source, "rotation_seed"))
+
+
+class _Bound:
+    """Device-side distance source bound to a query block (search.py:159-168)."""
+
+    def __init__(self, source, q_dev):
+        torch = _lib.require_cuda()
+        self.q_dev = q_dev
+        nq, D = q_dev.shape
+        if _is_rabitq(source):
+            from .rabitq import as_rabitq
+
+            idx = as_rabitq(source)
+            if D != idx.dims:
+                raise ValueError(f"query dims {D} != index dims {idx.dims}")
+            dev = idx.device()
+            self.kind = _lib.SRC_RABITQ
+            self.dims = idx.dims
+            self.records, self.record_bytes, self.bits = dev.records, dev.record_bytes, idx.bits
+            self.rows = None
+            self.rotated = torch.empty((nq, D), dtype=torch.float32, device=q_dev.device)
+            self.qadd = torch.empty(nq, dtype=torch.float32, device=q_dev.device)
+            self.qsumq = torch.empty(nq, dtype=torch.float32, device=q_dev.device)
+            if nq:
+                _lib.check(_lib.lib().jb_rabitq_bind(_lib.ptr(q_dev), nq, D, idx.bits, _lib.ptr(dev.centroid),
+                                                     _lib.ptr(dev.rotation), _lib.ptr(self.rotated),
+                                                     _lib.ptr(self.qadd), _lib.ptr(self.qsumq), _lib.stream_ptr()))
+            self.count = idx.count
+        else:
+            ds = as_dataset(source)
+            if D != ds.dims:
+                raise ValueError(f"query dims {D} != dataset dims {ds.dims}")
+            dev = ds.device()
+            self.kind = _lib.SRC_EXACT
+            self.dims = ds.dims
+            self.rows = dev
+            self.records, self.record_bytes, self.bits = None, 0, 0
+            self.rotated = q_dev
+            self.qadd = torch.empty(nq, dtype=torch.float32, device=q_dev.device)
+            self.qsumq = None
+            if nq:
+                _lib.check(_lib.lib().jb_row_sq_norms(_lib.ptr(q_dev), nq, D, _lib.ptr(self.qadd),
+                                                     _lib.stream_ptr()))
+            self.count = ds.count
+
+
+def _queries_to_device(queries):
+    torch = _lib.require_cuda()
+    if isinstance(queries, torch.Tensor):
+        q = queries
+        if q.dim() == 1:
+            q = q[None, :]
+        return q.to(device="cuda", dtype=torch.float32).contiguous()
+    q = np.atleast_2d(np.asarray(queries))
+    q = np.ascontiguousarray(q, dtype=np.float32)
+    t = torch.from_numpy(q)
+    return t.pin_memory().to("cuda", non_blocking=True) if t.numel() * 4 >= (1 << 20) else t.to("cuda")
+
+
+def _launch(graph: GraphIndex, bound: _Bound, L: int, starts_dev=None, trace_cap: int = 0, out=None):
+    torch = _lib.require_cuda()
+    nq = bound.q_dev.shape[0]
+    adj, _ = graph.device()
+    dev = bound.q_dev.device
+    fk = torch.empty((nq, L), dtype=torch.int64, device=dev) if out is None else out
+    hops = torch.empty(nq, dtype=torch.int32, device=dev)
+    evals = torch.empty(nq, dtype=torch.int32, device=dev)
+    flags = torch.empty(nq, dtype=torch.int32, device=dev)
+    tids = tdst = None
+    if trace_cap:
+        tids = torch.empty((nq, trace_cap), dtype=torch.int32, device=dev)
+        tdst = torch.empty((nq, trace_cap), dtype=torch.float32, device=dev)
+    a = _lib.SearchArgs()
+    a.adjacency = _lib.ptr(adj)
+    a.degree_cap = graph.degree_cap
+    a.active_count = graph.active_count
+    a.source = bound.kind
+    a.dims = bound.dims
+    if bound.kind == _lib.SRC_EXACT:
+        a.data = _lib.ptr(bound.rows.x)
+        a.data_norms = _lib.ptr(bound.rows.norms)
+    else:
+        a.records = _lib.ptr(bound.records)
+        a.record_bytes = bound.record_bytes
+        a.bits = bound.bits
+    a.queries = _lib.ptr(bound.rotated)
+    a.query_add = _lib.ptr(bound.qadd)
+    a.query_sumq = _lib.ptr(bound.qsumq)
+    a.nq = nq
+    a.starts = _lib.ptr(starts_dev)
+    a.start_vertex = graph.entry_point
+    a.beam_width = L
+    a.hash_slots = int(TUNING["hash_slots"])
+    a.trace_cap = trace_cap
+    a.frontier_keys = _lib.ptr(fk)
+    a.hops = _lib.ptr(hops)
+    a.evals = _lib.ptr(evals)
+    a.trace_ids = _lib.ptr(tids)
+    a.trace_dists = _lib.ptr(tdst)
+    a.flags = _lib.ptr(flags)
+    _lib.check(_lib.lib().jb_beam_search(_lib.C.byref(a), _lib.stream_ptr()))
+    return fk, hops, evals, flags, tids, tdst
+
+
+def _validate(graph: GraphIndex, beam_width: int):
+    if graph.active_count == 0:
+        raise ValueError("search on an empty graph")
+    if not 1 <= beam_width <= MAX_BEAM_WIDTH:
+        raise ValueError(f"beam_width must be in [1, {MAX_BEAM_WIDTH}]")
+
+
+def _starts(graph: GraphIndex, starts, nq: int):
+    if starts is None:
+        return None
+    s = np.broadcast_to(np.asarray(starts, dtype=np.int64), (nq,)).copy()
+    if s.size and (s.min() < 0 or s.max() >= graph.active_count):
+        raise ValueError("start vertex out of range")
+    torch = _lib.require_cuda()
+    return torch.from_numpy(s.astype(np.int32)).cuda()
+
+
+def run_beam_searches(graph, source, queries, beam_width: int, starts=None) -> list[SearchResult]:
+    """search.py:272-304: one SearchResult (frontier + visited trace + stats) per query row."""
+    graph = as_graph(graph)
+    _validate(graph, beam_width)
+    q_dev = _queries_to_device(queries)
+    nq = q_dev.shape[0]
+    starts_dev = _starts(graph, starts, nq)
+    bound = _Bound(source, q_dev)
+    cap = max(2 * beam_width, beam_width + 64)
+    fk, hops, evals, flags, tids, tdst = _launch(graph, bound, beam_width, starts_dev, cap)
+    hops_h = hops.cpu().numpy()
+    over = np.nonzero(hops_h > cap)[0]
+    if over.size:  # trace buffer overflowed for a few queries: re-run exactly those with a larger cap
+        torch = _lib.require_cuda()
+        sel = torch.from_numpy(over).cuda()
+        cap2 = int(hops_h[over].max())
+        b2 = _Bound(source, q_dev[sel].contiguous())
+        st2 = starts_dev[sel].contiguous() if starts_dev is not None else None
+        _, _, _, _, t2i, t2d = _launch(graph, b2, beam_width, st2, cap2)
+        tids_h = np.full((nq, cap2), -1, dtype=np.int32)
+        tdst_h = np.zeros((nq, cap2), dtype=np.float32)
+        tids_h[:, :cap] = tids.cpu().numpy()
+        tdst_h[:, :cap] = tdst.cpu().numpy()
+        tids_h[over] = t2i.cpu().numpy()
+        tdst_h[over] = t2d.cpu().numpy()
+    else:
+        tids_h, tdst_h = tids.cpu().numpy(), tdst.cpu().numpy()
+    keys = fk.cpu().numpy().view(np.uint64)
+    evals_h = evals.cpu().numpy()
+    out = []
+    for i in range(nq):
+        kk = keys[i][keys[i] != _UMAX]
+        h = int(hops_h[i])
+        out.append(SearchResult(
+            frontier_ids=(kk & np.uint64(0xFFFFFFFF)).astype(np.int32),
+            frontier_dists=(kk >> np.uint64(32)).astype(np.uint32).view(np.float32).astype(np.float64),
+            visited_ids=tids_h[i, :h].copy(),
+            visited_dists=tdst_h[i, :h].astype(np.float64),
+            stats=SearchStats(hops=h, distance_evals=int(evals_h[i])),
+        ))
+    return out
+
+
+def beam_search(graph, source, query, params: SearchParams, start: int | None = None) -> SearchResult:
+    return run_beam_searches(graph, source, np.atleast_2d(query), params.beam_width, start)[0]
+
+
+def search_knn(graph, source, query, params: SearchParams, start: int | None = None,
+               exact_data=None) -> list[Candidate]:
+    """search.py:323-348."""
+    if params.rerank and not isinstance(source, VectorDataset) and _is_rabitq(source) and exact_data is None:
+        raise ValueError("rerank over a quantized source requires exact_data")
+    graph = as_graph(graph)
+    _validate(graph, params.beam_width)
+    q_dev = _queries_to_device(query)
+    ids, dists = _knn_device(graph, source, q_dev, params, exact_data, _starts(graph, start, 1))
+    ids, dists = ids.cpu().numpy()[0], dists.cpu().numpy()[0]
+    keep = ids >= 0
+    return [Candidate(int(i), float(d)) for i, d in zip(ids[keep], dists[keep])]
+
+
+def _knn_device(graph: GraphIndex, source, q_dev, params: SearchParams, exact_data=None, starts_dev=None):
+    torch = _lib.require_cuda()
+    nq = q_dev.shape[0]
+    rerank = params.rerank and _is_rabitq(source)
+    if rerank and exact_data is None:
+        raise ValueError("rerank over a quantized source requires exact_data")
+    bound = _Bound(source, q_dev)
+    L, k = params.beam_width, params.k
+    fk, *_ = _launch(graph, bound, L, starts_dev, 0)
+    ids = torch.empty((nq, k), dtype=torch.int32, device=q_dev.device)
+    dists = torch.empty((nq, k), dtype=torch.float64, device=q_dev.device)
+    if nq == 0:
+        return ids, dists
+    st = _lib.stream_ptr()
+    if rerank:
+        rows = as_dataset(exact_data).device()
+        if rows.dims != q_dev.shape[1]:
+            raise ValueError(f"query dims {q_dev.shape[1]} != dataset dims {rows.dims}")
+        _lib.check(_lib.lib().jb_rerank_topk(_lib.ptr(rows.x), rows.dims, _lib.ptr(q_dev), nq, _lib.ptr(fk), L, k,
+                                             _lib.ptr(ids), _lib.ptr(dists), st))
+    else:
+        _lib.check(_lib.lib().jb_frontier_topk(_lib.ptr(fk), nq, L, k, _lib.ptr(ids), _lib.ptr(dists), st))
+    return ids, dists
+
+
+def search_knn_batch(graph, source, queries, params: SearchParams, exact_data=None):
+    """search.py:351-383: (ids int32 [nq,k] padded -1, dists f64 [nq,k] padded +inf).
+
+    Host arrays in and out: queries are copied to HBM, one search launch plus
+    one top-k (or fp32 rerank) launch run, and the results are copied back.
+    """
+    graph = as_graph(graph)
+    _validate(graph, params.beam_width)
+    if params.rerank and _is_rabitq(source) and exact_data is None:
+        raise ValueError("rerank over a quantized source requires exact_data")
+    q_dev = _queries_to_device(queries)
+    ids, dists = _knn_device(graph, source, q_dev, params, exact_data)
+    return ids.cpu().numpy(), dists.cpu().numpy()
+
+
+def search_knn_batch_device(graph, source, q_dev, params: SearchParams, exact_data=None):
+    """HBM-resident variant: queries and results stay torch CUDA tensors (no host sync)."""
+    graph = as_graph(graph)
+    _validate(graph, params.beam_width)
+    return _knn_device(graph, source, q_dev, params, exact_data)

@@ -1,0 +1,125 @@
+"""Generate golden fixtures by running the LIVE reference (`beamann`) in this container.
+
+    PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden.py
+
+Reads /root/reference/pkg/src (read-only; present only in the build container,
+never on the GPU box). Writes tests/golden/*.npz. Inputs are regenerated from
+seeds in the tests (numpy PCG64 is deterministic), so only outputs are stored.
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+import time
+
+import numpy as np
+
+sys.dont_write_bytecode = True
+sys.path.insert(0, "/root/reference/pkg/src")
+import beamann as ref  # noqa: E402
+from beamann.search import run_beam_searches  # noqa: E402
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def lowrank(n, d, d_int, noise, seed):
+    """SURVEY.md Appendix B generator (same recipe as paper_2601_07048_b200.core.gen_lowrank)."""
+    g = np.random.default_rng(seed)
+    a = g.standard_normal((d_int, d)) / np.sqrt(d_int)
+    x = g.standard_normal((n, d_int)) @ a + noise * g.standard_normal((n, d))
+    return x.astype(np.float32)
+
+
+def ragged(results):
+    out = {}
+    for name in ("frontier_ids", "frontier_dists", "visited_ids", "visited_dists"):
+        parts = [getattr(r, name) for r in results]
+        out[name] = np.concatenate(parts) if parts else np.empty(0)
+        out[name + "_len"] = np.array([p.size for p in parts], dtype=np.int64)
+    out["hops"] = np.array([r.stats.hops for r in results], dtype=np.int64)
+    out["evals"] = np.array([r.stats.distance_evals for r in results], dtype=np.int64)
+    return out
+
+
+def save(name, **arrays):
+    path = os.path.join(HERE, name + ".npz")
+    np.savez_compressed(path, **arrays)
+    print(f"wrote {path} ({os.path.getsize(path)} B)")
+
+
+def graph_fixture(name, data, R, L, alpha, max_batch=100_000):
+    ds = ref.VectorDataset(data)
+    t = time.time()
+    g = ref.build(ds, ref.BuildParams(degree_cap=R, build_beam_width=L, alpha=alpha, max_batch=max_batch))
+    print(f"{name}: reference build {data.shape} in {time.time() - t:.1f}s")
+    n = g.active_count
+    return g, dict(adjacency=g.adjacency[:n].copy(), degrees=g.degrees[:n].copy(),
+                   entry=np.int64(g.entry_point), active=np.int64(n))
+
+
+def main():
+    # 1. exact search + build on a small Gaussian graph (D=32, R=16, L=32)
+    data = ref.gen_synthetic(3000, 32, seed=0).data
+    g, gf = graph_fixture("g32", data, R=16, L=32, alpha=1.2)
+    q = ref.gen_synthetic(200, 32, seed=1).data
+    res = run_beam_searches(g, ref.VectorDataset(data), q, 32)
+    res8 = run_beam_searches(g, ref.VectorDataset(data), q, 8)
+    ids, dists = ref.search_knn_batch(g, ref.VectorDataset(data), q, ref.SearchParams(beam_width=32, k=10))
+    save("g32", **gf, **{"L32_" + k: v for k, v in ragged(res).items()},
+         **{"L8_" + k: v for k, v in ragged(res8).items()}, knn_ids=ids, knn_dists=dists)
+
+    # 2. odd dims (non-16B-aligned rows), D=33, R=8
+    data33 = ref.gen_synthetic(800, 33, seed=5).data
+    g33, gf33 = graph_fixture("g33", data33, R=8, L=16, alpha=1.3)
+    q33 = ref.gen_synthetic(64, 33, seed=6).data
+    res33 = run_beam_searches(g33, ref.VectorDataset(data33), q33, 16)
+    save("g33", **gf33, **{"L16_" + k: v for k, v in ragged(res33).items()})
+
+    # 3. low-rank 128-d build (R=32, L=64) + incremental inserts in 2% batches
+    data128 = lowrank(4000, 128, 12, 0.05, seed=7)
+    g128, gf128 = graph_fixture("g128", data128, R=32, L=64, alpha=1.2)
+    q128 = lowrank(100, 128, 12, 0.05, seed=8)
+    res128 = run_beam_searches(g128, ref.VectorDataset(data128), q128, 64)
+    inc = ref.GraphIndex(capacity=4000, degree_cap=32)
+    p = ref.BuildParams(degree_cap=32, build_beam_width=64, alpha=1.2, max_batch=80)
+    ds128 = ref.VectorDataset(data128)
+    ref.batch_insert(inc, ds128, range(0, 33), p)
+    ref.insert_stream(inc, ds128, range(33, 1200), p)
+    save("g128", **gf128, **{"L64_" + k: v for k, v in ragged(res128).items()},
+         inc_adjacency=inc.adjacency[:1200].copy(), inc_degrees=inc.degrees[:1200].copy(),
+         inc_entry=np.int64(inc.entry_point))
+
+    # 4. RaBitQ fit / bind / quantized search + rerank on the g32 graph and 128-d data
+    fx = {}
+    x = ref.gen_synthetic(2000, 128, seed=2).data
+    qq = ref.gen_synthetic(50, 128, seed=4).data
+    for bits in (1, 2, 4, 8):
+        idx = ref.rabitq_fit(ref.VectorDataset(x), bits=bits, seed=3)
+        b = idx.bind(qq)
+        fx[f"m{bits}_centroid"] = idx.centroid
+        fx[f"m{bits}_codes"] = idx.codes
+        fx[f"m{bits}_meta"] = idx.meta
+        fx[f"m{bits}_rotated"] = b._rotated
+        fx[f"m{bits}_qadd"] = b._qadd
+        fx[f"m{bits}_sumq"] = b._qsumq
+    idx1 = ref.rabitq_fit(ref.VectorDataset(data), bits=1, seed=11)
+    idx4 = ref.rabitq_fit(ref.VectorDataset(data), bits=4, seed=11)
+    for tag, idx in (("q1", idx1), ("q4", idx4)):
+        r = run_beam_searches(g, idx, q, 32)
+        fx.update({f"{tag}_" + k: v for k, v in ragged(r).items()})
+        i2, d2 = ref.search_knn_batch(g, idx, q, ref.SearchParams(beam_width=32, k=10, rerank=True),
+                                      exact_data=ref.VectorDataset(data))
+        fx[f"{tag}_rr_ids"] = i2
+        fx[f"{tag}_rr_dists"] = d2
+    save("rabitq", **fx)
+
+    # 5. exact kNN ground truth and medoid
+    gt = ref.exact_knn(ref.VectorDataset(data), ref.VectorDataset(q), 20)
+    save("misc", gt_ids=gt.ids, gt_dists=gt.distances,
+         medoid32=np.int64(ref.medoid(ref.VectorDataset(data))),
+         medoid128=np.int64(ref.medoid(ref.VectorDataset(data128))))
+
+
+if __name__ == "__main__":
+    main()

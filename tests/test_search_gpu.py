@@ -1,0 +1,256 @@
+"""GPU parity: the sm_100a search / RaBitQ kernels vs the oracle and the live
+reference's golden outputs (identical ids, dists, traces, stats)."""
+
+import numpy as np
+import pytest
+
+from conftest import gaussian, golden, lowrank, split
+from oracle import knn as oknn
+from oracle import rabitq as orabitq
+from oracle import search as osearch
+from oracle import vamana
+
+pytestmark = pytest.mark.gpu
+
+jb = pytest.importorskip("paper_2601_07048_b200")
+
+
+def _graph(f):
+    n = int(f["active"])
+    g = jb.GraphIndex(n, f["adjacency"].shape[1])
+    g.adjacency[:] = f["adjacency"]
+    g.degrees[:] = f["degrees"]
+    g.active_count, g.entry_point = n, int(f["entry"])
+    return g
+
+
+def _graph_from_oracle(og):
+    g = jb.GraphIndex(og.adj.shape[0], og.R)
+    g.adjacency[:] = og.adj
+    g.degrees[:] = og.deg
+    g.active_count, g.entry_point = og.active, og.entry
+    return g
+
+
+def _assert_same(res, exp_fids, exp_fd, exp_vids, exp_vd, exp_hops, exp_evals=None):
+    for i, r in enumerate(res):
+        np.testing.assert_array_equal(r.frontier_ids, exp_fids[i], err_msg=f"query {i} frontier")
+        np.testing.assert_array_equal(r.frontier_dists, exp_fd[i], err_msg=f"query {i} frontier dists")
+        np.testing.assert_array_equal(r.visited_ids, exp_vids[i], err_msg=f"query {i} trace")
+        np.testing.assert_array_equal(r.visited_dists, exp_vd[i], err_msg=f"query {i} trace dists")
+        assert r.stats.hops == exp_hops[i]
+        if exp_evals is not None:
+            assert r.stats.distance_evals == exp_evals[i]
+
+
+def _golden_check(res, f, p):
+    _assert_same(res, split(f[p + "frontier_ids"], f[p + "frontier_ids_len"]),
+                 split(f[p + "frontier_dists"], f[p + "frontier_dists_len"]),
+                 split(f[p + "visited_ids"], f[p + "visited_ids_len"]),
+                 split(f[p + "visited_dists"], f[p + "visited_dists_len"]), f[p + "hops"], f[p + "evals"])
+
+
+def _oracle_check(res, ores, evals=True):
+    _assert_same(res, [r.frontier_ids for r in ores], [r.frontier_dists for r in ores],
+                 [r.visited_ids for r in ores], [r.visited_dists for r in ores], [r.hops for r in ores],
+                 [r.evals for r in ores] if evals else None)
+
+
+@pytest.mark.parametrize("L", [32, 8])
+def test_exact_search_matches_reference_golden(L):
+    f = golden("g32")
+    x, q = gaussian(3000, 32, 0), gaussian(200, 32, 1)
+    res = jb.run_beam_searches(_graph(f), jb.VectorDataset(x), q, L)
+    _golden_check(res, f, f"L{L}_")
+
+
+def test_exact_search_odd_dims_golden():
+    f = golden("g33")
+    x, q = gaussian(800, 33, 5), gaussian(64, 33, 6)
+    _golden_check(jb.run_beam_searches(_graph(f), jb.VectorDataset(x), q, 16), f, "L16_")
+
+
+def test_exact_search_128d_golden():
+    f = golden("g128")
+    x, q = lowrank(4000, 128, 12, 0.05, 7), lowrank(100, 128, 12, 0.05, 8)
+    _golden_check(jb.run_beam_searches(_graph(f), jb.VectorDataset(x), q, 64), f, "L64_")
+
+
+def test_knn_batch_matches_reference_golden():
+    f = golden("g32")
+    x, q = gaussian(3000, 32, 0), gaussian(200, 32, 1)
+    ids, ds = jb.search_knn_batch(_graph(f), jb.VectorDataset(x), q, jb.SearchParams(beam_width=32, k=10))
+    np.testing.assert_array_equal(ids, f["knn_ids"])
+    np.testing.assert_array_equal(ds, f["knn_dists"])
+    assert ids.dtype == np.int32 and ds.dtype == np.float64
+
+
+@pytest.fixture(scope="module")
+def graph64():
+    x = gaussian(6000, 64, 21)
+    og = vamana.build(x, R=24, L=48, alpha=1.2)
+    return x, og
+
+
+@pytest.mark.parametrize("L", [1, 16, 100, 256, 1024])
+def test_exact_search_matches_oracle_many_widths(graph64, L):
+    x, og = graph64
+    q = gaussian(300, 64, 22)
+    ores = osearch.beam_search(og.adj, og.active, og.entry, osearch.ExactSource(x, q), len(q), L)
+    res = jb.run_beam_searches(_graph_from_oracle(og), jb.VectorDataset(x), q, L)
+    _oracle_check(res, ores)
+
+
+def test_lossy_visited_table_keeps_frontier_and_trace(graph64):
+    x, og = graph64
+    q = gaussian(200, 64, 23)
+    L = 128
+    ores = osearch.beam_search(og.adj, og.active, og.entry, osearch.ExactSource(x, q), len(q), L)
+    jb.search.TUNING["hash_slots"] = 64   # far too small: forces re-evaluations
+    try:
+        res = jb.run_beam_searches(_graph_from_oracle(og), jb.VectorDataset(x), q, L)
+    finally:
+        jb.search.TUNING["hash_slots"] = 0
+    _oracle_check(res, ores, evals=False)
+    assert sum(r.stats.distance_evals for r in res) > sum(r.evals for r in ores)
+
+
+def test_explicit_starts_and_single_query(graph64):
+    x, og = graph64
+    q = gaussian(40, 64, 24)
+    starts = np.arange(40) * 97 % og.active
+    ores = osearch.beam_search(og.adj, og.active, og.entry, osearch.ExactSource(x, q), len(q), 24, starts=starts)
+    g = _graph_from_oracle(og)
+    _oracle_check(jb.run_beam_searches(g, jb.VectorDataset(x), q, 24, starts=starts), ores)
+    one = jb.beam_search(g, jb.VectorDataset(x), q[3], jb.SearchParams(beam_width=24), start=int(starts[3]))
+    np.testing.assert_array_equal(one.visited_ids, ores[3].visited_ids)
+    cands = jb.search_knn(g, jb.VectorDataset(x), q[5], jb.SearchParams(beam_width=24, k=7))
+    o5 = osearch.beam_search(og.adj, og.active, og.entry, osearch.ExactSource(x, q[5:6]), 1, 24)[0]
+    assert [c.id for c in cands] == o5.frontier_ids[:7].tolist()
+    assert [c.dist for c in cands] == o5.frontier_dists[:7].tolist()
+
+
+def test_degree_cap_above_warp_width():
+    x = gaussian(1500, 16, 31)
+    og = vamana.build(x, R=48, L=64, alpha=1.2)
+    q = gaussian(100, 16, 32)
+    ores = osearch.beam_search(og.adj, og.active, og.entry, osearch.ExactSource(x, q), len(q), 64)
+    _oracle_check(jb.run_beam_searches(_graph_from_oracle(og), jb.VectorDataset(x), q, 64), ores)
+
+
+def test_edge_cases_single_vertex_complete_graph_and_path():
+    # single vertex
+    g = jb.GraphIndex(1, 4)
+    g.active_count = 1
+    x = gaussian(1, 8, 1)
+    r = jb.run_beam_searches(g, jb.VectorDataset(x), gaussian(3, 8, 2), 4)
+    assert all(rr.frontier_ids.tolist() == [0] and rr.stats.hops == 1 for rr in r)
+    # complete graph N <= R+1 => exact top-k
+    n, R = 9, 8
+    x = gaussian(n, 5, 3)
+    g = jb.GraphIndex(n, R)
+    g.active_count = n
+    for u in range(n):
+        g.set_neighbors(u, [v for v in range(n) if v != u])
+    q = gaussian(20, 5, 4)
+    ids, _ = jb.search_knn_batch(g, jb.VectorDataset(x), q, jb.SearchParams(beam_width=4, k=4))
+    gt, _ = oknn.exact_knn(x, q, 4)
+    np.testing.assert_array_equal(ids, gt)
+    # path graph KAT
+    x = np.arange(10, dtype=np.float32)[:, None]
+    g = jb.GraphIndex(10, 2)
+    g.active_count = 10
+    for i in range(9):
+        g.set_neighbors(i, [i + 1])
+    r = jb.beam_search(g, jb.VectorDataset(x), np.array([9.0], np.float32), jb.SearchParams(beam_width=1, k=1))
+    assert r.visited_ids.tolist() == list(range(10)) and r.frontier_ids.tolist() == [9]
+    # k larger than the reachable set pads with -1 / inf (search.py:368-369)
+    g3 = jb.GraphIndex(3, 2)
+    g3.active_count = 3
+    ids, ds = jb.search_knn_batch(g3, jb.VectorDataset(x[:3]), np.array([[0.5]], np.float32),
+                                  jb.SearchParams(beam_width=4, k=4))
+    assert ids.tolist() == [[0, -1, -1, -1]] and ds[0, 0] == 0.25 and np.isinf(ds[0, 1:]).all()
+    # empty query batch
+    ids, ds = jb.search_knn_batch(g, jb.VectorDataset(x), np.zeros((0, 1), np.float32),
+                                  jb.SearchParams(beam_width=2, k=2))
+    assert ids.shape == (0, 2)
+
+
+def test_validation_errors_match_reference():
+    g = jb.GraphIndex(4, 2)
+    x = gaussian(4, 3, 0)
+    with pytest.raises(ValueError, match="search on an empty graph"):
+        jb.run_beam_searches(g, jb.VectorDataset(x), x, 4)
+    g.active_count = 4
+    with pytest.raises(ValueError, match="beam_width must be in"):
+        jb.run_beam_searches(g, jb.VectorDataset(x), x, 2000)
+    with pytest.raises(ValueError, match="start vertex out of range"):
+        jb.run_beam_searches(g, jb.VectorDataset(x), x, 4, starts=9)
+    with pytest.raises(ValueError, match="k must satisfy"):
+        jb.SearchParams(beam_width=4, k=5)
+
+
+# ---- RaBitQ ------------------------------------------------------------------
+
+@pytest.mark.parametrize("bits", [1, 2, 4, 8])
+def test_rabitq_fit_and_bind_bit_exact(bits):
+    f = golden("rabitq")
+    x, qq = gaussian(2000, 128, 2), gaussian(50, 128, 4)
+    idx = jb.rabitq_fit(jb.VectorDataset(x), bits=bits, seed=3)
+    np.testing.assert_array_equal(idx.centroid, f[f"m{bits}_centroid"])
+    np.testing.assert_array_equal(idx.codes, f[f"m{bits}_codes"])
+    np.testing.assert_array_equal(idx.meta.view(np.uint32), f[f"m{bits}_meta"].view(np.uint32))
+    rot, qadd, sumq = idx.bind(qq)
+    np.testing.assert_array_equal(rot, f[f"m{bits}_rotated"])
+    np.testing.assert_array_equal(qadd, f[f"m{bits}_qadd"])
+    np.testing.assert_array_equal(sumq, f[f"m{bits}_sumq"])
+
+
+@pytest.mark.parametrize("bits,D", [(1, 96), (4, 960), (2, 37), (8, 20)])
+def test_rabitq_fit_bit_exact_vs_oracle_shapes(bits, D):
+    x = lowrank(3000 if D < 500 else 1200, D, 16, 0.05, 40 + D)
+    x[7] = x.astype(np.float64).mean(axis=0).astype(np.float32)  # near-centroid row
+    c, codes, meta = orabitq.fit(x, bits, 5)
+    idx = jb.rabitq_fit(jb.VectorDataset(x), bits=bits, seed=5)
+    np.testing.assert_array_equal(idx.centroid, c)
+    np.testing.assert_array_equal(idx.codes, codes)
+    np.testing.assert_array_equal(idx.meta.view(np.uint32), meta.view(np.uint32))
+
+
+@pytest.mark.parametrize("bits,tag", [(1, "q1"), (4, "q4")])
+def test_rabitq_search_and_rerank_match_reference_golden(bits, tag):
+    f, fr = golden("g32"), golden("rabitq")
+    x, q = gaussian(3000, 32, 0), gaussian(200, 32, 1)
+    g = _graph(f)
+    idx = jb.rabitq_fit(jb.VectorDataset(x), bits=bits, seed=11)
+    _golden_check(jb.run_beam_searches(g, idx, q, 32), fr, tag + "_")
+    ids, ds = jb.search_knn_batch(g, idx, q, jb.SearchParams(beam_width=32, k=10, rerank=True),
+                                  exact_data=jb.VectorDataset(x))
+    np.testing.assert_array_equal(ids, fr[tag + "_rr_ids"])
+    np.testing.assert_array_equal(ds, fr[tag + "_rr_dists"])
+    with pytest.raises(ValueError, match="requires exact_data"):
+        jb.search_knn_batch(g, idx, q, jb.SearchParams(beam_width=32, k=10, rerank=True))
+
+
+def test_rabitq_search_oracle_960d_m4():
+    x = lowrank(1500, 960, 32, 0.05, 50)
+    og = vamana.build(x, R=16, L=32, alpha=1.2)
+    q = lowrank(60, 960, 32, 0.05, 51)
+    c, codes, meta = orabitq.fit(x, 4, 9)
+    rot, qadd, sumq = orabitq.bind(q, c, 4, 9)
+    src = orabitq.QuantSource(codes, meta, 4, 960, rot, qadd, sumq)
+    ores = osearch.beam_search(og.adj, og.active, og.entry, src, len(q), 48)
+    idx = jb.rabitq_fit(jb.VectorDataset(x), bits=4, seed=9)
+    g = _graph_from_oracle(og)
+    _oracle_check(jb.run_beam_searches(g, idx, q, 48), ores)
+    ids, ds = jb.search_knn_batch(g, idx, q, jb.SearchParams(beam_width=48, k=10, rerank=True),
+                                  exact_data=jb.VectorDataset(x))
+    oids, ods = osearch.topk(ores, 10, queries=q, rerank_data=x)
+    np.testing.assert_array_equal(ids, oids)
+    np.testing.assert_array_equal(ds, ods)
+
+
+def test_medoid_matches_reference_golden():
+    f = golden("misc")
+    assert jb.medoid(jb.VectorDataset(gaussian(3000, 32, 0))) == int(f["medoid32"])
+    assert jb.medoid(jb.VectorDataset(lowrank(4000, 128, 12, 0.05, 7))) == int(f["medoid128"])
