@@ -7,6 +7,7 @@ sm_100a CUDA kernels in libjasper_b200.so (C ABI: include/jasper_b200.h).
 There is no CPU fallback: without the library or a CUDA device, calls raise.
 """
 
+from .build import BuildParams, EdgeBuffer, batch_insert, build, insert_stream
 from .core import DistanceKind, ElementKind, VectorDataset, dot, gen_lowrank, gen_synthetic, sq_l2
 from .graph import Candidate, FormatError, GraphIndex, medoid, robust_prune
 from .rabitq import QueryPrep, RaBitQIndex, estimate_sq_dist, prep_query, rotate
@@ -17,6 +18,7 @@ from .search import (SearchParams, SearchResult, SearchStats, beam_search, run_b
 __version__ = "0.1.0"
 
 __all__ = [
+    "BuildParams", "EdgeBuffer", "batch_insert", "build", "insert_stream",
     "Candidate", "DistanceKind", "ElementKind", "FormatError", "GraphIndex", "QueryPrep", "RaBitQIndex",
     "SearchParams", "SearchResult", "SearchStats", "VectorDataset", "beam_search", "dot", "estimate_sq_dist",
     "gen_lowrank", "gen_synthetic", "medoid", "prep_query", "rabitq_fit", "robust_prune", "rotate",

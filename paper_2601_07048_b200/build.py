@@ -1,0 +1,196 @@
+"""Batch-parallel construction and streaming insertion on B200 (mirror of build.py).
+
+  BuildParams     build.py:35-62   same fields, defaults and validation
+  batch_insert    build.py:296-348 one jb_batch_insert call: phase-1 batched
+                  search, phase-2 warp prune + reverse triples, phase-3 sorted
+                  group merge with one owner warp per target, then connectivity
+                  repair — all on device, mutating the HBM adjacency in place
+  build           build.py:389-424 R+1 doubling schedule, entry -> global medoid
+  insert_stream   build.py:427-447 max_batch chunks
+
+The quantized-construction path (`quantizer=`) and `two_pass` refinement are
+not part of the B200 hot path (no config uses them); they raise.
+"""
+
+from __future__ import annotations
+
+import warnings
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .core import ElementKind, as_dataset
+from .graph import GraphIndex, as_graph, medoid
+from .search import MAX_BEAM_WIDTH
+
+__all__ = ["BuildParams", "EdgeBuffer", "batch_insert", "build", "insert_stream"]
+
+
+@dataclass(frozen=True)
+class BuildParams:
+    degree_cap: int = 64
+    build_beam_width: int = 128
+    alpha: float = 1.2
+    max_batch: int = 100_000
+    two_pass: bool = False
+    always_prune: bool = False
+    reverse_all_visited: bool = False
+
+    def __post_init__(self):
+        if self.degree_cap < 2:
+            raise ValueError("degree_cap must be >= 2")
+        if self.alpha < 1.0:
+            raise ValueError("alpha must be >= 1")
+        if not 1 <= self.build_beam_width <= MAX_BEAM_WIDTH:
+            raise ValueError(f"build_beam_width must be in [1, {MAX_BEAM_WIDTH}]")
+        if self.max_batch < 1:
+            raise ValueError("max_batch must be >= 1")
+        if self.build_beam_width < self.degree_cap:
+            warnings.warn("build_beam_width below degree_cap gives sparse candidate sets", stacklevel=2)
+
+
+class EdgeBuffer:
+    """Host (target, source, dist) triple buffer with the reference's ordering
+    (build.py:65-102). The device path keeps its triples in HBM; this class is
+    kept for API compatibility."""
+
+    def __init__(self):
+        self._t, self._s, self._d = [], [], []
+
+    def add(self, targets, source: int, dists) -> None:
+        t = np.asarray(targets, dtype=np.int64).ravel()
+        self._t.append(t)
+        self._s.append(np.full(t.size, source, dtype=np.int64))
+        self._d.append(np.asarray(dists, dtype=np.float64).ravel())
+
+    def __len__(self) -> int:
+        return sum(t.size for t in self._t)
+
+    def sorted_triples(self):
+        if not self._t:
+            e = np.empty(0, dtype=np.int64)
+            return e, e.copy(), np.empty(0, dtype=np.float64)
+        t, s, d = np.concatenate(self._t), np.concatenate(self._s), np.concatenate(self._d)
+        o = np.lexsort((s, d, t))
+        return t[o], s[o], d[o]
+
+    def groups(self):
+        t, s, d = self.sorted_triples()
+        if not t.size:
+            return
+        uniq, starts = np.unique(t, return_index=True)
+        bounds = np.append(starts, t.size)
+        for i, v in enumerate(uniq):
+            yield int(v), s[bounds[i]:bounds[i + 1]], d[bounds[i]:bounds[i + 1]]
+
+
+def _validate_range(graph: GraphIndex, dataset, new_ids: range):
+    """build.py:227-243 (same messages)."""
+    start, stop = new_ids.start, new_ids.stop
+    if new_ids.step != 1:
+        raise ValueError("new id range must be contiguous")
+    if start < stop and start < graph.active_count:
+        raise ValueError(f"id range [{start}, {stop}) overlaps active vertices (< {graph.active_count})")
+    if start != graph.active_count and start < stop:
+        raise ValueError(f"id range must start at active_count={graph.active_count}, got {start}")
+    if stop > dataset.count:
+        raise ValueError("id range exceeds dataset count")
+    if stop > graph.capacity:
+        raise ValueError("id range exceeds graph capacity")
+    return start, stop
+
+
+def _args(graph: GraphIndex, ds, params: BuildParams, start: int, stop: int):
+    adj, deg = graph.device()
+    dev = ds.device()
+    a = _lib.InsertArgs()
+    a.adjacency, a.degrees = _lib.ptr(adj), _lib.ptr(deg)
+    a.degree_cap, a.capacity = graph.degree_cap, graph.capacity
+    a.data, a.data_norms, a.dims, a.count = _lib.ptr(dev.x), _lib.ptr(dev.norms), dev.dims, dev.count
+    a.build_beam_width = params.build_beam_width
+    a.alpha = float(params.alpha)
+    a.always_prune = int(params.always_prune)
+    a.reverse_all_visited = int(params.reverse_all_visited)
+    a.start, a.stop = start, stop
+    a.entry_point = graph.entry_point
+    return a
+
+
+def _run(fn, graph: GraphIndex, a) -> int:
+    entry = np.zeros(1, dtype=np.int64)
+    bridges = np.zeros(1, dtype=np.int64)
+    a.entry_point_out_host = entry.ctypes.data
+    a.bridges_out_host = bridges.ctypes.data
+    try:
+        _lib.check(fn(_lib.C.byref(a), _lib.stream_ptr()))
+    finally:
+        graph.mark_device_modified()
+    graph.entry_point = int(entry[0])
+    return int(bridges[0])
+
+
+def _check_supported(params: BuildParams, quantizer):
+    if quantizer is not None:
+        raise NotImplementedError("quantized construction is not on the B200 path (build with exact rows)")
+    if params.degree_cap < 2:
+        raise ValueError("degree_cap must be >= 2")
+
+
+def batch_insert(graph, dataset, new_ids: range, params: BuildParams, quantizer=None) -> None:
+    """build.py:296-348: insert a contiguous id range as one three-phase batch (in place)."""
+    graph = as_graph(graph)
+    ds = as_dataset(dataset)
+    start, stop = _validate_range(graph, ds, new_ids)
+    if start == stop:
+        return
+    _check_supported(params, quantizer)
+    if ds.element_kind is not ElementKind.F32:
+        raise ValueError("the B200 path supports f32 datasets")
+    if graph.degree_cap != params.degree_cap:
+        raise ValueError("graph degree_cap differs from params.degree_cap")
+    a = _args(graph, ds, params, start, stop)
+    graph.last_bridges = _run(_lib.lib().jb_batch_insert, graph, a)
+    graph.active_count = stop
+
+
+def _repair(graph: GraphIndex, ds, params: BuildParams) -> int:
+    a = _args(graph, ds, params, 0, graph.active_count)
+    return _run(_lib.lib().jb_repair_connectivity, graph, a)
+
+
+def build(dataset, params: BuildParams, quantizer=None) -> GraphIndex:
+    """build.py:389-424: bulk build with the R+1 doubling batch schedule."""
+    ds = as_dataset(dataset)
+    if ds.count == 0:
+        raise ValueError("cannot build over an empty dataset")
+    _check_supported(params, quantizer)
+    if params.two_pass:
+        raise NotImplementedError("two_pass refinement is not on the B200 path")
+    graph = GraphIndex(capacity=ds.count, degree_cap=params.degree_cap)
+    global_medoid = medoid(ds)
+    size = params.degree_cap + 1
+    pos = 0
+    while pos < ds.count:
+        stop = min(ds.count, pos + size)
+        batch_insert(graph, ds, range(pos, stop), params)
+        if global_medoid < graph.active_count and graph.entry_point != global_medoid:
+            graph.entry_point = global_medoid
+            _repair(graph, ds, params)
+        pos = stop
+        size = min(size * 2, params.max_batch)
+    return graph
+
+
+def insert_stream(graph, dataset, new_range: range, params: BuildParams, quantizer=None) -> None:
+    """build.py:427-447."""
+    if len(new_range) == 0:
+        return
+    graph = as_graph(graph)
+    ds = as_dataset(dataset)
+    _validate_range(graph, ds, new_range)
+    pos = new_range.start
+    while pos < new_range.stop:
+        stop = min(new_range.stop, pos + params.max_batch)
+        batch_insert(graph, ds, range(pos, stop), params, quantizer)
+        pos = stop

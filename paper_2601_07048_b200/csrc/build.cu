@@ -1,0 +1,855 @@
+// build.cu — batch-parallel, lock-free construction and streaming insertion.
+//
+// Replaces the reference's build.py:
+//   batch_insert          build.py:296-348  (jb_batch_insert: three phases + repair)
+//   _seed_batch           build.py:246-266  (seed_prune_kernel)
+//   robust_prune          graph.py:174-228  (warp_prune, one warp per pivot)
+//   EdgeBuffer + _merge_reverse_edges  build.py:65-102, 269-293
+//                         (per-source triple slots, two stable radix sorts giving
+//                          (target, dist, source) order, one owner warp per target)
+//   _repair_connectivity  build.py:137-224  (GPU BFS, tiled nearest-donor scan,
+//                          ordered sequential attach on one warp)
+//
+// Lock-freedom: phase 2 writes only the new vertex's own row; phase 3 groups the
+// reverse triples by target so exactly one warp owns each written row. Results do
+// not depend on scheduling: triple order is fixed by the sort keys, not by atomics.
+//
+// Robust prune without a sort: the reference sorts candidates by (dist, id) and
+// repeatedly takes the first survivor. Taking the minimum (dist, id) key among
+// survivors each round extracts the same sequence, and the alpha filter is
+// element-wise, so the kept list is identical.
+#include <algorithm>
+#include <vector>
+#include <cub/cub.cuh>
+#include "common.cuh"
+#include "runtime.cuh"
+
+namespace jb {
+
+constexpr int BW = 4;  // warps per block in the per-vertex kernels
+constexpr uint32_t NO_TARGET = 0xFFFFFFFFu;
+
+// d(pivot, row) with the row in the data role and the pivot norm added last
+// (build.py:130-134): max((xn[row] - 2*dot(x[row], x[pivot])) + xn[pivot], 0).
+__device__ __forceinline__ float pair_dist(const float* __restrict__ data, const float* __restrict__ norms, int D,
+                                           const float* __restrict__ pivot_row, float pivot_norm, uint32_t row) {
+    const float dot = a1_dot<false>(data + (size_t)row * D, pivot_row, D);
+    return exact_from_dot(__ldg(norms + row), dot, pivot_norm);
+}
+
+__device__ __forceinline__ uint64_t warp_min_u64(uint64_t v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        uint64_t w = shfl_xor_u64(v, o);
+        v = w < v ? w : v;
+    }
+    return v;
+}
+
+// Warp-cooperative robust prune over n candidate keys (dist_bits << 32 | id) in
+// `cand` (modified in place). Writes kept ids/dists (extraction order) and returns
+// how many were kept. `srow` is per-warp smem of D floats for the star row.
+__device__ int warp_prune(uint64_t* cand, int n, double alpha2, int R, const float* __restrict__ data,
+                          const float* __restrict__ norms, int D, float* srow, int32_t* out_ids, float* out_d) {
+    const int lane = lane_id();
+    int kept = 0;
+    while (kept < R) {
+        uint64_t m = UMAX;
+        for (int i = lane; i < n; i += 32) { uint64_t c = cand[i]; m = c < m ? c : m; }
+        m = warp_min_u64(m);
+        if (m == UMAX) break;
+        const uint32_t star = (uint32_t)(m & 0xFFFFFFFFull);
+        if (lane == 0) {
+            out_ids[kept] = (int32_t)star;
+            out_d[kept] = __uint_as_float((uint32_t)(m >> 32));
+        }
+        for (int i = lane; i < n; i += 32)
+            if (cand[i] == m) cand[i] = UMAX;
+        ++kept;
+        if (kept >= R) break;
+        // stage the star row, then filter survivors: keep p' iff alpha^2 * d(star, p') > d(p, p')
+        __syncwarp();
+        const float* sr = data + (size_t)star * D;
+        for (int e = lane; e < D; e += 32) srow[e] = sr[e];
+        const float sn = __ldg(norms + star);
+        __syncwarp();
+        for (int i = lane; i < n; i += 32) {
+            const uint64_t c = cand[i];
+            if (c == UMAX) continue;
+            const float dsp = pair_dist(data, norms, D, srow, sn, (uint32_t)(c & 0xFFFFFFFFull));
+            const double dp = (double)__uint_as_float((uint32_t)(c >> 32));
+            if (!(__dmul_rn(alpha2, (double)dsp) > dp)) cand[i] = UMAX;
+        }
+        __syncwarp();
+    }
+    __syncwarp();
+    return kept;
+}
+
+__device__ __forceinline__ void write_row(int32_t* __restrict__ adj, int32_t* __restrict__ deg, int R, uint32_t v,
+                                          const int32_t* ids, int n) {
+    const int lane = lane_id();
+    for (int j = lane; j < R; j += 32) adj[(size_t)v * R + j] = j < n ? ids[j] : -1;
+    if (lane == 0) deg[v] = n;
+}
+
+// ---- seed batch (build.py:246-266) ------------------------------------------
+__global__ void __launch_bounds__(BW * 32)
+seed_prune_kernel(const float* __restrict__ data, const float* __restrict__ norms, int D, int64_t start, int64_t stop,
+                  double alpha2, int R, uint64_t* __restrict__ cand_all, int32_t* __restrict__ kept_ids,
+                  float* __restrict__ kept_d, int32_t* __restrict__ adj, int32_t* __restrict__ deg) {
+    extern __shared__ __align__(16) float sh[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    float* srow = sh + warp * ((D + 3) & ~3);
+    const int64_t n = stop - start;
+    const int64_t xi = (int64_t)blockIdx.x * BW + warp;
+    if (xi >= n) return;
+    const uint32_t x = (uint32_t)(start + xi);
+    uint64_t* cand = cand_all + xi * (n - 1);
+    // candidate dists d(x, others) with x as the pivot
+    const float* xr = data + (size_t)x * D;
+    for (int e = lane; e < D; e += 32) srow[e] = xr[e];
+    const float xn = norms[x];
+    __syncwarp();
+    for (int64_t j = lane; j < n - 1; j += 32) {
+        const uint32_t o = (uint32_t)(start + (j < xi ? j : j + 1));
+        cand[j] = pack_key(pair_dist(data, norms, D, srow, xn, o), o);
+    }
+    __syncwarp();
+    int32_t* ki = kept_ids + xi * R;
+    float* kd = kept_d + xi * R;
+    const int k = warp_prune(cand, (int)(n - 1), alpha2, R, data, norms, D, srow, ki, kd);
+    write_row(adj, deg, R, x, ki, k);
+}
+
+// ---- phase 2: prune each new vertex's visited trace, emit reverse triples ----
+__global__ void __launch_bounds__(BW * 32)
+phase2_kernel(const float* __restrict__ data, const float* __restrict__ norms, int D, int64_t start, int64_t nb,
+              double alpha2, int R, const int32_t* __restrict__ hops, const int32_t* __restrict__ tids,
+              const float* __restrict__ tdst, int cap, int reverse_all, uint64_t* __restrict__ cand_all,
+              int32_t* __restrict__ kept_ids, float* __restrict__ kept_d, int32_t* __restrict__ adj,
+              int32_t* __restrict__ deg, uint32_t* __restrict__ tri_target, uint64_t* __restrict__ tri_key, int W) {
+    extern __shared__ __align__(16) float sh[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    float* srow = sh + warp * ((D + 3) & ~3);
+    const int64_t xi = (int64_t)blockIdx.x * BW + warp;
+    if (xi >= nb) return;
+    const uint32_t x = (uint32_t)(start + xi);
+    const int h = min(hops[xi], cap);
+    uint64_t* cand = cand_all + xi * cap;
+    const int32_t* ti = tids + xi * cap;
+    const float* td = tdst + xi * cap;
+    for (int j = lane; j < h; j += 32) cand[j] = pack_key(td[j], (uint32_t)ti[j]);
+    __syncwarp();
+    int32_t* ki = kept_ids + xi * R;
+    float* kd = kept_d + xi * R;
+    const int k = warp_prune(cand, h, alpha2, R, data, norms, D, srow, ki, kd);
+    write_row(adj, deg, R, x, ki, k);
+    // reverse triples (target, source=x, dist): kept edges, or the whole trace
+    uint32_t* tt = tri_target + xi * W;
+    uint64_t* tk = tri_key + xi * W;
+    const int ne = reverse_all ? h : k;
+    for (int j = lane; j < W; j += 32) {
+        if (j < ne) {
+            const uint32_t t = reverse_all ? (uint32_t)ti[j] : (uint32_t)ki[j];
+            const float d = reverse_all ? td[j] : kd[j];
+            tt[j] = t;
+            tk[j] = ((uint64_t)__float_as_uint(d) << 32) | x;
+        } else {
+            tt[j] = NO_TARGET;
+            tk[j] = UMAX;
+        }
+    }
+}
+
+// ---- batched standalone robust prune (graph.py:174-228) ----------------------
+__global__ void __launch_bounds__(BW * 32)
+prune_batch_kernel(const float* __restrict__ data, const float* __restrict__ norms, int D,
+                   const int64_t* __restrict__ pivots, int64_t count, const int64_t* __restrict__ offsets,
+                   const int32_t* __restrict__ cids, const float* __restrict__ cd, double alpha2, int R,
+                   uint64_t* __restrict__ cand_all, int32_t* __restrict__ out_ids, float* __restrict__ out_d,
+                   int32_t* __restrict__ out_n) {
+    extern __shared__ __align__(16) float sh[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    float* srow = sh + warp * ((D + 3) & ~3);
+    const int64_t i = (int64_t)blockIdx.x * BW + warp;
+    if (i >= count) return;
+    const int64_t o0 = offsets[i], o1 = offsets[i + 1];
+    const int n = (int)(o1 - o0);
+    uint64_t* cand = cand_all + o0;
+    for (int j = lane; j < n; j += 32) cand[j] = pack_key(cd[o0 + j], (uint32_t)cids[o0 + j]);
+    __syncwarp();
+    const int k = warp_prune(cand, n, alpha2, R, data, norms, D, srow, out_ids + i * R, out_d + i * R);
+    if (lane == 0) out_n[i] = k;
+    (void)pivots;
+}
+
+// ---- phase 3: group heads, owner merge (build.py:269-293) ------------------
+__global__ void seg_head_kernel(const uint32_t* __restrict__ t, int64_t n, uint8_t* __restrict__ flag) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    flag[i] = (t[i] != NO_TARGET) && (i == 0 || t[i] != t[i - 1]);
+}
+
+constexpr int OWNER_SC = 256;  // smem candidate slots per owner warp
+__host__ __device__ inline int owner_per_warp(int R, int D) {
+    return ((OWNER_SC * 8 + R * 4 * 3 + ((D + 3) & ~3) * 4) + 15) & ~15;
+}
+
+__global__ void __launch_bounds__(BW * 32)
+owner_merge_kernel(const float* __restrict__ data, const float* __restrict__ norms, int D, double alpha2, int R,
+                   int always_prune, const uint32_t* __restrict__ tgt, const uint64_t* __restrict__ key, int64_t total,
+                   const int32_t* __restrict__ seg_start, const int* __restrict__ n_seg, uint64_t* __restrict__ pool,
+                   unsigned long long* __restrict__ pool_top, int pool_cap, int32_t* __restrict__ adj,
+                   int32_t* __restrict__ deg, int* __restrict__ err) {
+    extern __shared__ __align__(16) unsigned char shb[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    constexpr int SC = OWNER_SC;
+    const int per_warp = owner_per_warp(R, D);
+    unsigned char* base = shb + (size_t)warp * per_warp;
+    uint64_t* scand = reinterpret_cast<uint64_t*>(base);
+    int32_t* have = reinterpret_cast<int32_t*>(base + SC * 8);
+    int32_t* kid = have + R;
+    float* kd = reinterpret_cast<float*>(kid + R);
+    float* srow = kd + R;
+    const int64_t s = (int64_t)blockIdx.x * BW + warp;
+    if (s >= *n_seg) return;
+    const int64_t g0 = seg_start[s];
+    const uint32_t t = tgt[g0];
+    int64_t g1 = g0;
+    for (;;) {  // group end: first index whose target differs
+        const int64_t i = g1 + lane;
+        const bool same = i < total && tgt[i] == t;
+        const uint32_t m = __ballot_sync(0xFFFFFFFFu, same);
+        g1 += __popc(m);
+        if (m != 0xFFFFFFFFu) break;
+    }
+    const int g = (int)(g1 - g0);
+    const int hd = deg[t];
+    for (int j = lane; j < hd; j += 32) have[j] = adj[(size_t)t * R + j];
+    __syncwarp();
+    // candidate storage: smem when it fits, else a bump-allocated global slice
+    uint64_t* cand = scand;
+    if (hd + g > SC) {
+        unsigned long long off = 0;
+        if (lane == 0) off = atomicAdd(pool_top, (unsigned long long)(hd + g));
+        off = __shfl_sync(0xFFFFFFFFu, off, 0);
+        if (off + hd + g > (unsigned long long)pool_cap) {
+            if (lane == 0) atomicExch(err, 1);
+            return;
+        }
+        cand = pool + off;
+    }
+    // fresh = group sources not already neighbours, in (dist, source) order
+    int nf = 0;
+    for (int b = 0; b < g; b += 32) {
+        const int j = b + lane;
+        bool fresh = false;
+        uint64_t k = 0;
+        if (j < g) {
+            k = key[g0 + j];
+            const int32_t src = (int32_t)(k & 0xFFFFFFFFull);
+            fresh = true;
+            for (int e = 0; e < hd; ++e) fresh &= (have[e] != src);
+        }
+        const uint32_t m = __ballot_sync(0xFFFFFFFFu, fresh);
+        if (fresh) cand[hd + nf + __popc(m & lanemask_lt())] = k;
+        nf += __popc(m);
+    }
+    __syncwarp();
+    if (nf == 0) return;
+    if (!always_prune && hd + nf <= R) {  // append in (dist, source) order
+        for (int j = lane; j < nf; j += 32) {
+            adj[(size_t)t * R + hd + j] = (int32_t)(cand[hd + j] & 0xFFFFFFFFull);
+        }
+        if (lane == 0) deg[t] = hd + nf;
+        return;
+    }
+    // existing neighbours get recomputed distances d(t, e) (target is the pivot)
+    const float* tr = data + (size_t)t * D;
+    for (int e = lane; e < D; e += 32) srow[e] = tr[e];
+    const float tn = norms[t];
+    __syncwarp();
+    for (int j = lane; j < hd; j += 32) {
+        const uint32_t e = (uint32_t)have[j];
+        cand[j] = pack_key(pair_dist(data, norms, D, srow, tn, e), e);
+    }
+    // fresh entries already hold (stored triple dist << 32 | source) keys
+    __syncwarp();
+    const int k = warp_prune(cand, hd + nf, alpha2, R, data, norms, D, srow, kid, kd);
+    write_row(adj, deg, R, t, kid, k);
+}
+
+// ---- repair: BFS ------------------------------------------------------------
+__global__ void bfs_init_kernel(int32_t* __restrict__ seen, int64_t n, int64_t entry, int32_t* __restrict__ front,
+                                int* __restrict__ fcount) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) seen[i] = (i == entry);
+    if (i == 0) { front[0] = (int32_t)entry; *fcount = 1; }
+}
+
+__global__ void bfs_expand_kernel(const int32_t* __restrict__ adj, int R, const int32_t* __restrict__ front,
+                                  const int* __restrict__ fcount, int32_t* __restrict__ seen,
+                                  int32_t* __restrict__ next, int* __restrict__ ncount) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (int64_t)(*fcount) * R) return;
+    const int32_t v = adj[(size_t)front[i / R] * R + (i % R)];
+    if (v < 0) return;
+    if (seen[v]) return;
+    if (atomicExch(&seen[v], 1) == 0) next[atomicAdd(ncount, 1)] = v;
+}
+
+__global__ void split_kernel(const int32_t* __restrict__ seen, int64_t n, int32_t* __restrict__ lost,
+                             int* __restrict__ nlost, int32_t* __restrict__ reach, int* __restrict__ nreach) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    if (seen[i]) reach[atomicAdd(nreach, 1)] = (int32_t)i;
+    else lost[atomicAdd(nlost, 1)] = (int32_t)i;
+}
+
+// ---- repair: nearest reachable donors (build.py:185-192) --------------------
+// Block tile: 64 stranded x 64 reachable rows staged in smem; each thread owns a
+// 4x4 pair sub-tile with four A1 accumulator lanes per pair. Distances use the
+// stranded vertex as the pivot. Each block keeps a running top-16 per stranded
+// row over its slice of the reachable list; slices are merged afterwards.
+constexpr int DT = 64;      // tile edge
+constexpr int FAN = 16;     // min(R, 16) donors, upper bound
+
+__global__ void __launch_bounds__(256)
+donor_scan_kernel(const float* __restrict__ data, const float* __restrict__ norms, int D, const int32_t* __restrict__ lost,
+                  int nlost, const int32_t* __restrict__ reach, int nreach, int slices, int fan,
+                  uint64_t* __restrict__ part) {
+    extern __shared__ __align__(16) unsigned char dsh[];
+    const int KB = 16;  // elements per k-step (one A1 block)
+    float* As = reinterpret_cast<float*>(dsh);             // [DT][KB+1]  stranded
+    float* Bs = As + DT * (KB + 1);                        // [DT][KB+1]  reachable
+    float* dist = Bs + DT * (KB + 1);                      // [DT][DT+1]
+    uint64_t* top = reinterpret_cast<uint64_t*>(dist + DT * (DT + 1));  // [DT][FAN] (8B aligned: 6336 floats)
+    uint64_t* mbuf = top + DT * FAN;                                           // [8 warps][128]
+    const int tid = threadIdx.x;
+    const int tx = tid & 15, ty = tid >> 4;  // 16 x 16 threads, 4x4 pairs each
+    const int s0 = blockIdx.x * DT;
+    const int slice = blockIdx.y;
+    const int64_t per = (nreach + slices - 1) / slices;
+    const int64_t r_begin = slice * per, r_end = (nreach < r_begin + per) ? (int64_t)nreach : r_begin + per;
+    for (int i = tid; i < DT * FAN; i += 256) top[i] = UMAX;
+    __syncthreads();
+    for (int64_t r0 = r_begin; r0 < r_end; r0 += DT) {
+        Acc4 acc[4][4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int b = 0; b < 4; ++b) acc[a][b].zero();
+        for (int k0 = 0; k0 < D; k0 += KB) {
+            const int kl = min(KB, D - k0);
+            for (int i = tid; i < DT * KB; i += 256) {
+                const int row = i / KB, e = i % KB;
+                float va = 0.f, vb = 0.f;
+                if (e < kl) {
+                    if (s0 + row < nlost) va = data[(size_t)lost[s0 + row] * D + k0 + e];
+                    if (r0 + row < r_end) vb = data[(size_t)reach[r0 + row] * D + k0 + e];
+                }
+                As[row * (KB + 1) + e] = va;
+                Bs[row * (KB + 1) + e] = vb;
+            }
+            __syncthreads();
+            if (kl == KB) {
+                // A1 order inside a 16-block: vectors 3,2,1,0; lane j = element % 4
+#pragma unroll
+                for (int v = 3; v >= 0; --v) {
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        float av[4], bv[4];
+#pragma unroll
+                        for (int a = 0; a < 4; ++a) av[a] = As[(ty * 4 + a) * (KB + 1) + 4 * v + j];
+#pragma unroll
+                        for (int b = 0; b < 4; ++b) bv[b] = Bs[(tx * 4 + b) * (KB + 1) + 4 * v + j];
+#pragma unroll
+                        for (int a = 0; a < 4; ++a)
+#pragma unroll
+                            for (int b = 0; b < 4; ++b) {
+                                const float p = __fmul_rn(bv[b], av[a]);
+                                if (j == 0) acc[a][b].l0 = __fadd_rn(p, acc[a][b].l0);
+                                else if (j == 1) acc[a][b].l1 = __fadd_rn(p, acc[a][b].l1);
+                                else if (j == 2) acc[a][b].l2 = __fadd_rn(p, acc[a][b].l2);
+                                else acc[a][b].l3 = __fadd_rn(p, acc[a][b].l3);
+                            }
+                    }
+                }
+            } else {
+                for (int e = 0; e < kl; ++e) {  // tail: forward
+                    float av[4], bv[4];
+#pragma unroll
+                    for (int a = 0; a < 4; ++a) av[a] = As[(ty * 4 + a) * (KB + 1) + e];
+#pragma unroll
+                    for (int b = 0; b < 4; ++b) bv[b] = Bs[(tx * 4 + b) * (KB + 1) + e];
+#pragma unroll
+                    for (int a = 0; a < 4; ++a)
+#pragma unroll
+                        for (int b = 0; b < 4; ++b) acc[a][b].madd1((k0 + e) & 3, bv[b], av[a]);
+                }
+            }
+            __syncthreads();
+        }
+        // distances: row = reachable r (data role), pivot = stranded x (norm added last)
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+            const int si = s0 + ty * 4 + a;
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+                const int64_t ri = r0 + tx * 4 + b;
+                float d = __int_as_float(0x7F800000);
+                if (si < nlost && ri < r_end) {
+                    const uint32_t r = (uint32_t)reach[ri];
+                    d = exact_from_dot(__ldg(norms + r), acc[a][b].reduce(), __ldg(norms + lost[si]));
+                }
+                dist[(ty * 4 + a) * (DT + 1) + tx * 4 + b] = d;
+            }
+        }
+        __syncthreads();
+        // merge the 64 new candidates of each stranded row into its top-`fan`
+        const int warp = tid >> 5, lane = tid & 31;
+        for (int row = warp; row < DT; row += 8) {
+            if (s0 + row >= nlost) continue;
+            uint64_t* tp = top + row * FAN;
+            const uint64_t worst = tp[fan - 1];
+            uint64_t k0v = UMAX, k1v = UMAX;
+            if (r0 + lane < r_end) k0v = pack_key(dist[row * (DT + 1) + lane], (uint32_t)reach[r0 + lane]);
+            if (r0 + 32 + lane < r_end) k1v = pack_key(dist[row * (DT + 1) + 32 + lane], (uint32_t)reach[r0 + 32 + lane]);
+            if (k0v >= worst) k0v = UMAX;
+            if (k1v >= worst) k1v = UMAX;
+            if (!__any_sync(0xFFFFFFFFu, k0v != UMAX || k1v != UMAX)) continue;
+            // merge: current top (fan) + 64 new keys -> 128-slot buffer, sort, keep fan
+            uint64_t* mb = mbuf + warp * 128;
+            mb[lane] = lane < fan ? tp[lane] : UMAX;
+            mb[32 + lane] = k0v;
+            mb[64 + lane] = k1v;
+            mb[96 + lane] = UMAX;
+            __syncwarp();
+            warp_bitonic_sort_smem(mb, 128);
+            if (lane < fan) tp[lane] = mb[lane];
+            __syncwarp();
+        }
+        __syncthreads();
+    }
+    for (int i = tid; i < DT * FAN; i += 256) {
+        const int row = i / FAN, j = i % FAN;
+        if (s0 + row < nlost && j < fan) part[((size_t)slice * nlost + s0 + row) * fan + j] = top[row * FAN + j];
+    }
+}
+
+// merge slice top-lists: warp per stranded vertex; writes donors and the sort key
+// (nearest-donor dist bits << 32 | stranded id) for the processing order.
+__global__ void donor_merge_kernel(const uint64_t* __restrict__ part, int slices, int nlost, int fan,
+                                   const int32_t* __restrict__ lost, int32_t* __restrict__ donors,
+                                   uint64_t* __restrict__ order_key, int32_t* __restrict__ order_val) {
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (warp >= nlost) return;
+    uint64_t best = UMAX;
+    // repeated extraction of the minimum: slices*fan <= 64*16 candidates
+    uint64_t taken_last = 0;
+    bool first = true;
+    for (int j = 0; j < fan; ++j) {
+        uint64_t m = UMAX;
+        for (int i = lane; i < slices * fan; i += 32) {
+            const int sl = i / fan, q = i % fan;
+            const uint64_t k = part[((size_t)sl * nlost + warp) * fan + q];
+            if ((first || k > taken_last) && k < m) m = k;
+        }
+        m = warp_min_u64(m);
+        if (lane == 0) donors[(size_t)warp * fan + j] = (m == UMAX) ? -1 : (int32_t)(m & 0xFFFFFFFFull);
+        if (j == 0) best = m;
+        taken_last = m;
+        first = false;
+        if (m == UMAX) {
+            for (int jj = j + 1 + lane; jj < fan; jj += 32) donors[(size_t)warp * fan + jj] = -1;
+            break;
+        }
+    }
+    if (lane == 0) {
+        order_key[warp] = (best & 0xFFFFFFFF00000000ull) | (uint32_t)lost[warp];
+        order_val[warp] = warp;
+    }
+}
+
+// ---- repair: ordered sequential attach (build.py:193-224), one warp ----------
+__global__ void attach_kernel(const float* __restrict__ data, const float* __restrict__ norms, int D,
+                              int32_t* __restrict__ adj, int32_t* __restrict__ deg, int R, uint8_t* __restrict__ pinned,
+                              int32_t* __restrict__ seen, const int32_t* __restrict__ lost,
+                              const int32_t* __restrict__ order, int nlost, const int32_t* __restrict__ donors, int fan,
+                              int32_t* __restrict__ queue, unsigned long long* __restrict__ bridges,
+                              int* __restrict__ err, int32_t* __restrict__ err_vertex) {
+    extern __shared__ __align__(16) float ash[];
+    float* urow = ash;
+    const int lane = threadIdx.x;
+    unsigned long long added = 0;
+    for (int oi = 0; oi < nlost; ++oi) {
+        const int i = order[oi];
+        const int32_t x = lost[i];
+        if (*((volatile int32_t*)seen + x)) continue;
+        bool placed = false;
+        for (int j = 0; j < fan && !placed; ++j) {
+            const int32_t u = donors[(size_t)i * fan + j];
+            if (u < 0) break;
+            int du = deg[u];
+            int32_t* row = adj + (size_t)u * R;
+            uint8_t* pin = pinned + (size_t)u * R;
+            if (du >= R) {
+                // farthest non-pinned neighbour by d(u, e) (u is the pivot), first index on ties
+                const float* ur = data + (size_t)u * D;
+                for (int e = lane; e < D; e += 32) urow[e] = ur[e];
+                __syncwarp();
+                const float un = norms[u];
+                float bestd = -1.0f;
+                int bests = R;
+                for (int s = lane; s < du; s += 32) {
+                    if (pin[s]) continue;
+                    const float d = pair_dist(data, norms, D, urow, un, (uint32_t)row[s]);
+                    if (d > bestd || (d == bestd && s < bests)) { bestd = d; bests = s; }
+                }
+                for (int o = 16; o > 0; o >>= 1) {
+                    const float od = __shfl_xor_sync(0xFFFFFFFFu, bestd, o);
+                    const int os = __shfl_xor_sync(0xFFFFFFFFu, bests, o);
+                    if (od > bestd || (od == bestd && os < bests)) { bestd = od; bests = os; }
+                }
+                __syncwarp();
+                if (bests >= R) continue;  // saturated with bridges: next donor
+                // remove slot `bests`, keeping order (and pins): ascending 32-wide chunks
+                for (int c = bests; c < du - 1; c += 32) {
+                    const int sidx = c + lane;
+                    int32_t rv = -1; uint8_t pv = 0;
+                    if (sidx < du - 1) { rv = row[sidx + 1]; pv = pin[sidx + 1]; }
+                    __syncwarp();
+                    if (sidx < du - 1) { row[sidx] = rv; pin[sidx] = pv; }
+                    __syncwarp();
+                }
+                du -= 1;
+            }
+            if (lane == 0) {
+                row[du] = x;
+                pin[du] = 1;
+                deg[u] = du + 1;
+            }
+            __syncwarp();
+            placed = true;
+            ++added;
+        }
+        if (!placed) {
+            if (lane == 0) { *err = 1; *err_vertex = x; }
+            return;
+        }
+        // BFS-extend reachability from x
+        if (lane == 0) { seen[x] = 1; queue[0] = x; }
+        __syncwarp();
+        int head = 0, tail = 1;
+        while (head < tail) {
+            const int32_t v = queue[head++];
+            const int dv = deg[v];
+            for (int s = lane; s < dv; s += 32) {
+                const int32_t w = adj[(size_t)v * R + s];
+                bool nw = (w >= 0) && !seen[w];
+                // lanes hold distinct neighbours of one row, so no duplicate pushes
+                const uint32_t m = __ballot_sync(__activemask(), nw);
+                if (nw) { seen[w] = 1; queue[tail + __popc(m & lanemask_lt())] = w; }
+                tail += __popc(m);
+            }
+            tail = __shfl_sync(0xFFFFFFFFu, tail, 0);
+            __syncwarp();
+        }
+    }
+    if (lane == 0) *bridges += added;
+}
+
+// ---- host orchestration -----------------------------------------------------
+struct Bufs {
+    std::vector<Scratch*> owned;
+    ~Bufs() { for (auto* s : owned) delete s; }
+    template <class T> T* get(size_t n, cudaStream_t st, cudaError_t& e) {
+        auto* s = new Scratch();
+        owned.push_back(s);
+        e = s->alloc(n * sizeof(T), st);
+        return s->as<T>();
+    }
+};
+
+#define BALLOC(var, T, n)                       \
+    T* var = bufs.get<T>((n), st, _ce);         \
+    JB_CUDA(_ce);
+
+static int repair(const jb_insert_args& a, int64_t n_active, int64_t entry, cudaStream_t st, int64_t* bridges_out) {
+    *bridges_out = 0;
+    if (n_active < 2) return JB_OK;
+    const int R = a.degree_cap, D = a.dims;
+    const int fan = std::min(R, 16);
+    Bufs bufs;
+    cudaError_t _ce;
+    BALLOC(seen, int32_t, n_active);
+    BALLOC(fa, int32_t, n_active);
+    BALLOC(fb, int32_t, n_active);
+    BALLOC(counts, int, 8);
+    BALLOC(lost, int32_t, n_active);
+    BALLOC(reach, int32_t, n_active);
+    BALLOC(pinned, uint8_t, (size_t)n_active * R);
+    BALLOC(bridges, unsigned long long, 1);
+    BALLOC(err, int, 2);
+    JB_CUDA(cudaMemsetAsync(pinned, 0, (size_t)n_active * R, st));
+    JB_CUDA(cudaMemsetAsync(bridges, 0, sizeof(unsigned long long), st));
+    JB_CUDA(cudaMemsetAsync(err, 0, 2 * sizeof(int), st));
+    const int T = 256;
+    const unsigned nblk = (unsigned)((n_active + T - 1) / T);
+    for (int round = 0;; ++round) {
+        // BFS from the entry
+        bfs_init_kernel<<<nblk, T, 0, st>>>(seen, n_active, entry, fa, counts);
+        int fcount = 1;
+        int32_t* cur = fa;
+        int32_t* nxt = fb;
+        int* fc = counts;
+        int* nc = counts + 1;
+        while (fcount > 0) {
+            JB_CUDA(cudaMemsetAsync(nc, 0, sizeof(int), st));
+            const int64_t work = (int64_t)fcount * R;
+            bfs_expand_kernel<<<(unsigned)((work + T - 1) / T), T, 0, st>>>(a.adjacency, R, cur, fc, seen, nxt, nc);
+            JB_LAUNCH_CHECK();
+            JB_CUDA(cudaMemcpyAsync(&fcount, nc, sizeof(int), cudaMemcpyDeviceToHost, st));
+            JB_CUDA(cudaStreamSynchronize(st));
+            std::swap(cur, nxt);
+            std::swap(fc, nc);
+        }
+        JB_CUDA(cudaMemsetAsync(counts + 2, 0, 2 * sizeof(int), st));
+        split_kernel<<<nblk, T, 0, st>>>(seen, n_active, lost, counts + 2, reach, counts + 3);
+        int h[2];
+        JB_CUDA(cudaMemcpyAsync(h, counts + 2, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
+        JB_CUDA(cudaStreamSynchronize(st));
+        const int nlost = h[0], nreach = h[1];
+        if (nlost == 0) break;
+        // donors
+        const int sblocks = (nlost + DT - 1) / DT;
+        int slices = std::max(1, std::min(64, (4 * sm_count_current() + sblocks - 1) / sblocks));
+        slices = (int)std::min<int64_t>(slices, std::max<int64_t>(1, (nreach + DT - 1) / DT));
+        BALLOC(part, uint64_t, (size_t)slices * nlost * fan);
+        BALLOC(donors, int32_t, (size_t)nlost * fan);
+        BALLOC(okey, uint64_t, nlost);
+        BALLOC(oval, int32_t, nlost);
+        BALLOC(okey2, uint64_t, nlost);
+        BALLOC(oval2, int32_t, nlost);
+        const size_t dsm = (size_t)(2 * DT * 17 + DT * (DT + 1)) * 4 + DT * FAN * 8 + 8 * 128 * 8;
+        JB_CUDA(cudaFuncSetAttribute(donor_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
+        donor_scan_kernel<<<dim3(sblocks, slices), 256, dsm, st>>>(a.data, a.data_norms, D, lost, nlost, reach, nreach,
+                                                                  slices, fan, part);
+        JB_LAUNCH_CHECK();
+        donor_merge_kernel<<<(unsigned)((nlost * 32 + 255) / 256), 256, 0, st>>>(part, slices, nlost, fan, lost, donors,
+                                                                               okey, oval);
+        JB_LAUNCH_CHECK();
+        size_t tb = 0;
+        cub::DeviceRadixSort::SortPairs(nullptr, tb, okey, okey2, oval, oval2, nlost, 0, 64, st);
+        BALLOC(tmp, unsigned char, tb);
+        JB_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, okey, okey2, oval, oval2, nlost, 0, 64, st));
+        const int asm_bytes = ((D + 3) & ~3) * 4;
+        attach_kernel<<<1, 32, asm_bytes, st>>>(a.data, a.data_norms, D, a.adjacency, a.degrees, R, pinned, seen, lost,
+                                                oval2, nlost, donors, fan, fa, bridges, err, err + 1);
+        JB_LAUNCH_CHECK();
+        int herr[2];
+        JB_CUDA(cudaMemcpyAsync(herr, err, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
+        JB_CUDA(cudaStreamSynchronize(st));
+        if (herr[0]) {
+            set_error("connectivity repair: no donor for vertex %d", herr[1]);
+            return JB_ENODONOR;
+        }
+        if (round > 10000) { set_error("connectivity repair did not converge"); return JB_ECUDA; }
+    }
+    unsigned long long hb = 0;
+    JB_CUDA(cudaMemcpyAsync(&hb, bridges, sizeof(hb), cudaMemcpyDeviceToHost, st));
+    JB_CUDA(cudaStreamSynchronize(st));
+    *bridges_out = (int64_t)hb;
+    return JB_OK;
+}
+
+static int validate_insert(const jb_insert_args& a) {
+    JB_CHECK_ARG(a.adjacency && a.degrees && a.data && a.data_norms, "batch insert: missing arrays");
+    JB_CHECK_ARG(a.degree_cap >= 1 && a.dims >= 1, "batch insert: bad shape");
+    JB_CHECK_ARG(a.alpha >= 1.0, "alpha must be >= 1");
+    JB_CHECK_ARG(a.start >= 0 && a.start <= a.stop, "batch insert: bad range");
+    JB_CHECK_ARG(a.stop <= a.count, "id range exceeds dataset count");
+    JB_CHECK_ARG(a.stop <= a.capacity, "id range exceeds graph capacity");
+    JB_CHECK_ARG(a.stop < (1ll << 31), "ids exceed int32");
+    return JB_OK;
+}
+
+}  // namespace jb
+
+using namespace jb;
+
+extern "C" {
+
+int jb_repair_connectivity(const jb_insert_args* args, void* stream) {
+    JB_CHECK_ARG(args, "null args");
+    const jb_insert_args& a = *args;
+    int rc = validate_insert(a);
+    if (rc) return rc;
+    int64_t b = 0;
+    rc = repair(a, a.stop, a.entry_point, as_stream(stream), &b);
+    if (a.bridges_out_host) *a.bridges_out_host = b;
+    if (a.entry_point_out_host) *a.entry_point_out_host = a.entry_point;
+    return rc;
+}
+
+int jb_batch_insert(const jb_insert_args* args, void* stream) {
+    JB_CHECK_ARG(args, "null args");
+    const jb_insert_args& a = *args;
+    int rc = validate_insert(a);
+    if (rc) return rc;
+    cudaStream_t st = as_stream(stream);
+    const int R = a.degree_cap, D = a.dims;
+    const double alpha2 = a.alpha * a.alpha;
+    int64_t entry = a.entry_point;
+    int64_t bridges = 0;
+    if (a.entry_point_out_host) *a.entry_point_out_host = entry;
+    if (a.bridges_out_host) *a.bridges_out_host = 0;
+    if (a.start == a.stop) return JB_OK;
+    const int64_t nb = a.stop - a.start;
+    const size_t srow_bytes = (size_t)BW * ((D + 3) & ~3) * 4;
+    Bufs bufs;
+    cudaError_t _ce;
+
+    if (a.start == 0) {  // seed batch: medoid entry + mutual pruning (build.py:246-266)
+        rc = jb_medoid(a.data, a.stop, D, &entry, stream);
+        if (rc) return rc;
+        if (nb > 1) {
+            BALLOC(cand, uint64_t, (size_t)nb * (nb - 1));
+            BALLOC(kid, int32_t, (size_t)nb * R);
+            BALLOC(kd, float, (size_t)nb * R);
+            JB_CUDA(cudaFuncSetAttribute(seed_prune_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)srow_bytes));
+            seed_prune_kernel<<<(unsigned)((nb + BW - 1) / BW), BW * 32, srow_bytes, st>>>(
+                a.data, a.data_norms, D, a.start, a.stop, alpha2, R, cand, kid, kd, a.adjacency, a.degrees);
+            JB_LAUNCH_CHECK();
+        }
+        rc = repair(a, a.stop, entry, st, &bridges);
+        if (a.entry_point_out_host) *a.entry_point_out_host = entry;
+        if (a.bridges_out_host) *a.bridges_out_host = bridges;
+        return rc;
+    }
+
+    // ---- phase 1: batched search of the new rows on the read-only graph ----
+    const int L = a.build_beam_width;
+    int cap = std::max(2 * L, L + 64);
+    BALLOC(fk, uint64_t, (size_t)nb * L);
+    BALLOC(hops, int32_t, nb);
+    BALLOC(evals, int32_t, nb);
+    BALLOC(flags, int32_t, nb);
+    int32_t* tids = nullptr;
+    float* tdst = nullptr;
+    for (int attempt = 0; attempt < 2; ++attempt) {
+        tids = bufs.get<int32_t>((size_t)nb * cap, st, _ce); JB_CUDA(_ce);
+        tdst = bufs.get<float>((size_t)nb * cap, st, _ce); JB_CUDA(_ce);
+        jb_search_args s{};
+        s.adjacency = a.adjacency; s.degree_cap = R; s.active_count = a.start;
+        s.source = JB_SRC_EXACT; s.dims = D; s.data = a.data; s.data_norms = a.data_norms;
+        s.queries = a.data + (size_t)a.start * D; s.query_add = a.data_norms + a.start;
+        s.nq = nb; s.starts = nullptr; s.start_vertex = entry;
+        s.beam_width = L; s.hash_slots = 0; s.trace_cap = cap;
+        s.frontier_keys = fk; s.hops = hops; s.evals = evals; s.trace_ids = tids; s.trace_dists = tdst; s.flags = flags;
+        rc = jb_beam_search(&s, stream);
+        if (rc) return rc;
+        // longest trace
+        size_t tb = 0;
+        BALLOC(mx, int32_t, 1);
+        cub::DeviceReduce::Max(nullptr, tb, hops, mx, (int)nb, st);
+        BALLOC(tmp, unsigned char, tb);
+        JB_CUDA(cub::DeviceReduce::Max(tmp, tb, hops, mx, (int)nb, st));
+        int hmax = 0;
+        JB_CUDA(cudaMemcpyAsync(&hmax, mx, sizeof(int), cudaMemcpyDeviceToHost, st));
+        JB_CUDA(cudaStreamSynchronize(st));
+        if (hmax <= cap) break;
+        cap = hmax;  // re-run with an exact-size trace buffer (rare)
+    }
+
+    // ---- phase 2: activate, prune each new vertex, emit reverse triples ----
+    const int W = a.reverse_all_visited ? cap : R;
+    const int64_t ntri = nb * (int64_t)W;
+    BALLOC(cand, uint64_t, (size_t)nb * cap);
+    BALLOC(kid, int32_t, (size_t)nb * R);
+    BALLOC(kd, float, (size_t)nb * R);
+    BALLOC(tt, uint32_t, ntri);
+    BALLOC(tk, uint64_t, ntri);
+    JB_CUDA(cudaFuncSetAttribute(phase2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)srow_bytes));
+    phase2_kernel<<<(unsigned)((nb + BW - 1) / BW), BW * 32, srow_bytes, st>>>(
+        a.data, a.data_norms, D, a.start, nb, alpha2, R, hops, tids, tdst, cap, a.reverse_all_visited, cand, kid, kd,
+        a.adjacency, a.degrees, tt, tk, W);
+    JB_LAUNCH_CHECK();
+
+    // ---- phase 3: (target, dist, source) order via two stable radix sorts ----
+    BALLOC(tt2, uint32_t, ntri);
+    BALLOC(tk2, uint64_t, ntri);
+    {
+        size_t tb1 = 0, tb2 = 0;
+        cub::DeviceRadixSort::SortPairs(nullptr, tb1, tk, tk2, tt, tt2, (int)ntri, 0, 64, st);
+        cub::DeviceRadixSort::SortPairs(nullptr, tb2, tt2, tt, tk2, tk, (int)ntri, 0, 32, st);
+        BALLOC(tmp, unsigned char, std::max(tb1, tb2));
+        size_t tb = std::max(tb1, tb2);
+        JB_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, tk, tk2, tt, tt2, (int)ntri, 0, 64, st));  // by (dist, source)
+        tb = std::max(tb1, tb2);
+        JB_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, tt2, tt, tk2, tk, (int)ntri, 0, 32, st));  // stable by target
+    }
+    BALLOC(flag, uint8_t, ntri);
+    BALLOC(seg, int32_t, ntri);
+    BALLOC(nseg, int, 1);
+    seg_head_kernel<<<(unsigned)((ntri + 255) / 256), 256, 0, st>>>(tt, ntri, flag);
+    {
+        size_t tb = 0;
+        cub::DeviceSelect::Flagged(nullptr, tb, cub::CountingInputIterator<int32_t>(0), flag, seg, nseg, (int)ntri, st);
+        BALLOC(tmp, unsigned char, tb);
+        JB_CUDA(cub::DeviceSelect::Flagged(tmp, tb, cub::CountingInputIterator<int32_t>(0), flag, seg, nseg, (int)ntri,
+                                           st));
+    }
+    int hseg = 0;
+    JB_CUDA(cudaMemcpyAsync(&hseg, nseg, sizeof(int), cudaMemcpyDeviceToHost, st));
+    JB_CUDA(cudaStreamSynchronize(st));
+    if (hseg > 0) {
+        const int pool_cap = (int)std::min<int64_t>(2 * ntri + 1024, INT32_MAX);
+        BALLOC(pool, uint64_t, pool_cap);
+        BALLOC(ptop, unsigned long long, 1);
+        BALLOC(err, int, 1);
+        JB_CUDA(cudaMemsetAsync(ptop, 0, sizeof(unsigned long long), st));
+        JB_CUDA(cudaMemsetAsync(err, 0, sizeof(int), st));
+        const int osm = owner_per_warp(R, D) * BW;
+        JB_CUDA(cudaFuncSetAttribute(owner_merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, osm));
+        owner_merge_kernel<<<(unsigned)((hseg + BW - 1) / BW), BW * 32, osm, st>>>(
+            a.data, a.data_norms, D, alpha2, R, a.always_prune, tt, tk, ntri, seg, nseg, pool, ptop, pool_cap,
+            a.adjacency, a.degrees, err);
+        JB_LAUNCH_CHECK();
+        int herr = 0;
+        JB_CUDA(cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, st));
+        JB_CUDA(cudaStreamSynchronize(st));
+        if (herr) { set_error("phase 3: candidate pool overflow"); return JB_EOVERFLOW; }
+    }
+
+    // ---- connectivity repair over the activated graph ----
+    rc = repair(a, a.stop, entry, st, &bridges);
+    if (a.entry_point_out_host) *a.entry_point_out_host = entry;
+    if (a.bridges_out_host) *a.bridges_out_host = bridges;
+    return rc;
+}
+
+int jb_robust_prune(const float* data, const float* data_norms, int32_t dims, const int64_t* pivots, int64_t count,
+                    const int64_t* offsets, const int32_t* cand_ids, const float* cand_dists, double alpha,
+                    int32_t degree_cap, int32_t* out_ids, float* out_dists, int32_t* out_counts, void* stream) {
+    JB_CHECK_ARG(alpha >= 1.0, "alpha must be >= 1");
+    JB_CHECK_ARG(degree_cap >= 1, "degree_cap must be >= 1");
+    JB_CHECK_ARG(dims >= 1, "dims must be >= 1");
+    if (count == 0) return JB_OK;
+    cudaStream_t st = as_stream(stream);
+    int64_t total = 0;
+    JB_CUDA(cudaMemcpyAsync(&total, offsets + count, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    JB_CUDA(cudaStreamSynchronize(st));
+    Scratch cand;
+    JB_CUDA(cand.alloc((size_t)std::max<int64_t>(total, 1) * 8, st));
+    const size_t srow_bytes = (size_t)BW * ((dims + 3) & ~3) * 4;
+    JB_CUDA(cudaFuncSetAttribute(prune_batch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)srow_bytes));
+    prune_batch_kernel<<<(unsigned)((count + BW - 1) / BW), BW * 32, srow_bytes, st>>>(
+        data, data_norms, dims, pivots, count, offsets, cand_ids, cand_dists, alpha * alpha, degree_cap,
+        cand.as<uint64_t>(), out_ids, out_dists, out_counts);
+    JB_LAUNCH_CHECK();
+    return JB_OK;
+}
+
+}  // extern "C"

@@ -2,11 +2,6 @@
 #include "runtime.cuh"
 using namespace jb;
 extern "C" {
-int jb_batch_insert(const jb_insert_args*, void*) { set_error("jb_batch_insert: not built yet"); return JB_EINVAL; }
-int jb_repair_connectivity(const jb_insert_args*, void*) { set_error("jb_repair_connectivity: not built yet"); return JB_EINVAL; }
-int jb_robust_prune(const float*, const float*, int32_t, const int64_t*, int64_t, const int64_t*, const int32_t*,
-                    const float*, double, int32_t, int32_t*, float*, int32_t*, void*) {
-    set_error("jb_robust_prune: not built yet"); return JB_EINVAL; }
 int jb_exact_knn(const float*, int64_t, int32_t, const float*, int64_t, int32_t, int32_t*, float*, void*) {
     set_error("jb_exact_knn: not built yet"); return JB_EINVAL; }
 int jb_merge_shard_topk(const int32_t*, const double*, int32_t, int64_t, int32_t, const int64_t*, int64_t*, double*, void*) {

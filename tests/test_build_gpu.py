@@ -1,0 +1,130 @@
+"""GPU parity for construction: device-built graphs are IDENTICAL (adjacency,
+degrees, entry point) to graphs built by the live reference (golden fixtures)
+and by the oracle restatement, including streaming inserts and options."""
+
+import numpy as np
+import pytest
+
+from conftest import gaussian, golden, lowrank
+from oracle import vamana
+
+pytestmark = pytest.mark.gpu
+
+jb = pytest.importorskip("paper_2601_07048_b200")
+
+
+def _same_graph(g, adj, deg, entry):
+    n = adj.shape[0]
+    assert g.entry_point == entry
+    np.testing.assert_array_equal(g.degrees[:n], deg)
+    np.testing.assert_array_equal(g.adjacency[:n], adj)
+
+
+def test_build_identical_to_reference_g32():
+    f = golden("g32")
+    g = jb.build(jb.VectorDataset(gaussian(3000, 32, 0)), jb.BuildParams(degree_cap=16, build_beam_width=32, alpha=1.2))
+    _same_graph(g, f["adjacency"], f["degrees"], int(f["entry"]))
+    g.validate()
+
+
+def test_build_identical_to_reference_g33_odd_dims():
+    f = golden("g33")
+    g = jb.build(jb.VectorDataset(gaussian(800, 33, 5)), jb.BuildParams(degree_cap=8, build_beam_width=16, alpha=1.3))
+    _same_graph(g, f["adjacency"], f["degrees"], int(f["entry"]))
+
+
+def test_build_identical_to_reference_g128_and_stream():
+    f = golden("g128")
+    x = lowrank(4000, 128, 12, 0.05, 7)
+    ds = jb.VectorDataset(x)
+    g = jb.build(ds, jb.BuildParams(degree_cap=32, build_beam_width=64, alpha=1.2))
+    _same_graph(g, f["adjacency"], f["degrees"], int(f["entry"]))
+    inc = jb.GraphIndex(capacity=4000, degree_cap=32)
+    p = jb.BuildParams(degree_cap=32, build_beam_width=64, alpha=1.2, max_batch=80)
+    jb.batch_insert(inc, ds, range(0, 33), p)
+    jb.insert_stream(inc, ds, range(33, 1200), p)
+    assert inc.active_count == 1200
+    _same_graph(inc, f["inc_adjacency"], f["inc_degrees"], int(f["inc_entry"]))
+
+
+@pytest.mark.parametrize("always_prune,reverse_all", [(True, False), (False, True)])
+def test_build_options_match_oracle(always_prune, reverse_all):
+    x = gaussian(1500, 24, 61)
+    og = vamana.Graph(1500, 12)
+    d = vamana.Pairwise(x)
+    vamana.batch_insert(og, x, 0, 13, 12, 24, 1.1, d, always_prune, reverse_all)
+    vamana.batch_insert(og, x, 13, 400, 12, 24, 1.1, d, always_prune, reverse_all)
+    vamana.batch_insert(og, x, 400, 1500, 12, 24, 1.1, d, always_prune, reverse_all)
+    g = jb.GraphIndex(1500, 12)
+    p = jb.BuildParams(degree_cap=12, build_beam_width=24, alpha=1.1, always_prune=always_prune,
+                       reverse_all_visited=reverse_all)
+    ds = jb.VectorDataset(x)
+    for a, b in ((0, 13), (13, 400), (400, 1500)):
+        jb.batch_insert(g, ds, range(a, b), p)
+    _same_graph(g, og.adj, og.deg, og.entry)
+
+
+def test_build_matches_oracle_lowrank_10k():
+    x = lowrank(10000, 64, 16, 0.05, 71)
+    og = vamana.build(x, R=24, L=48, alpha=1.2, max_batch=2000)
+    g = jb.build(jb.VectorDataset(x), jb.BuildParams(degree_cap=24, build_beam_width=48, alpha=1.2, max_batch=2000))
+    _same_graph(g, og.adj, og.deg, og.entry)
+
+
+def test_robust_prune_kats_and_oracle():
+    x = np.asarray([[0, 0], [1, 0], [2, 0]], np.float32)
+    ds = jb.VectorDataset(x)
+    d = vamana.Pairwise(x)
+    kept, _ = jb.robust_prune(0, [1, 2], d(0, [1, 2]), alpha=1.0, degree_cap=4, dataset=ds)
+    assert kept.tolist() == [1]
+    x = np.asarray([[0, 0], [1, 0], [0, 3]], np.float32)
+    d = vamana.Pairwise(x)
+    kept, _ = jb.robust_prune(0, [1, 2], d(0, [1, 2]), alpha=1.0, degree_cap=4, dataset=jb.VectorDataset(x))
+    assert kept.tolist() == [1, 2]
+    x = np.asarray([[0, 0], [1, 0], [0, 1]], np.float32)
+    d = vamana.Pairwise(x)
+    kept, _ = jb.robust_prune(0, [1, 2], d(0, [1, 2]), alpha=1.2, degree_cap=4, dataset=jb.VectorDataset(x))
+    assert sorted(kept.tolist()) == [1, 2]
+    # random planar + high-dim candidates vs the oracle, several alphas / caps
+    rng = np.random.default_rng(5)
+    for D, n, alpha, R in ((2, 20, 1.2, 8), (64, 300, 1.2, 32), (128, 80, 1.0, 16), (33, 50, 1e9, 10)):
+        x = rng.standard_normal((n + 1, D)).astype(np.float32)
+        d = vamana.Pairwise(x)
+        cand = np.arange(1, n + 1)
+        cd = d(0, cand)
+        ok, okd = vamana.robust_prune(0, cand, cd, alpha, R, d)
+        gk, gkd = jb.robust_prune(0, cand, cd, alpha=alpha, degree_cap=R, dataset=jb.VectorDataset(x))
+        np.testing.assert_array_equal(gk, ok)
+        np.testing.assert_array_equal(gkd, okd)
+    with pytest.raises(ValueError, match="must not contain the pivot"):
+        jb.robust_prune(0, [0, 1], [0.0, 1.0], alpha=1.2, degree_cap=2, dataset=ds)
+    with pytest.raises(ValueError, match="alpha must be >= 1"):
+        jb.robust_prune(0, [1], [1.0], alpha=0.5, degree_cap=2, dataset=ds)
+
+
+def test_insert_validation_messages():
+    ds = jb.VectorDataset(gaussian(100, 8, 1))
+    g = jb.GraphIndex(100, 8)
+    p = jb.BuildParams(degree_cap=8, build_beam_width=16)
+    jb.batch_insert(g, ds, range(0, 20), p)
+    with pytest.raises(ValueError, match="overlaps active vertices"):
+        jb.batch_insert(g, ds, range(10, 30), p)
+    with pytest.raises(ValueError, match="must start at active_count"):
+        jb.batch_insert(g, ds, range(25, 30), p)
+    with pytest.raises(ValueError, match="exceeds dataset count"):
+        jb.batch_insert(g, ds, range(20, 200), p)
+    jb.batch_insert(g, ds, range(20, 20), p)  # empty range is a no-op
+    assert g.active_count == 20
+    with pytest.raises(ValueError, match="cannot build over an empty dataset"):
+        jb.build(jb.VectorDataset(np.zeros((0, 4), np.float32)), p)
+
+
+def test_gpu_built_graph_invariants_and_reachability():
+    x = lowrank(20000, 96, 16, 0.05, 81)
+    g = jb.build(jb.VectorDataset(x), jb.BuildParams(degree_cap=32, build_beam_width=64, alpha=1.2, max_batch=5000))
+    g.validate()
+    og = vamana.Graph(g.capacity, 32)
+    og.adj[:] = g.adjacency
+    og.deg[:] = g.degrees
+    og.active, og.entry = g.active_count, g.entry_point
+    assert vamana.reachable(og).all()
