@@ -1,0 +1,559 @@
+"""Benchmark: QPS at recall@10 >= 0.95 on a SIFT-1M-shaped synthetic index (BASELINE.json configs[1]).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+    python -m torch.distributed.run --nnodes=1 --nproc-per-node N --master-addr 127.0.0.1 \
+        --master-port P bench.py --gpus N ...
+
+Workload (per GPU shard): 1M x 128 f32 low-rank synthetic rows (SURVEY.md Appendix B:
+d_int=16, noise 0.05), Vamana R=32, L_build=64, alpha=1.2 built on device, RaBitQ
+1-bit codes (seed 1) + fp32 rerank of the full beam, 10K queries, k=10. The beam
+width L* is the smallest of a sweep whose recall@10 (reference recall_at_k
+semantics, exact f64 ground truth) reaches 0.95; a step is one search of the
+10K-query batch at L* (bind + search + rerank kernels). `value` is device-timed
+with inputs resident in HBM (L2 flushed between steps, outside the timed
+events); `e2e` is the public API `search_knn_batch` with host queries in and host
+ids/dists out. N>1: contiguous 1M-row shards per rank, queries broadcast over
+NCCL, per-shard top-k all-gathered and merged on device; a unit is one
+(query, shard) search, so per-GPU work is fixed (weak scaling).
+
+--impl reference times the reference algorithm on the host CPU (the numpy oracle
+port, every host core via forked workers) on the same index and L*; the index
+itself is built on the GPU as untimed setup (the CPU reference would need days).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+SWEEP = (16, 24, 32, 48, 64, 96, 128, 192, 256, 384, 512, 768, 1024)
+
+
+def log(*a):
+    if int(os.environ.get("RANK", "0")) == 0:
+        print("[bench]", *a, file=sys.stderr, flush=True)
+
+
+def _args():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    p.add_argument("--n", type=int, default=1_000_000, help="vectors per shard")
+    p.add_argument("--nq", type=int, default=10_000)
+    p.add_argument("--dim", type=int, default=128)
+    p.add_argument("--k", type=int, default=10)
+    p.add_argument("--bits", type=int, default=1)
+    p.add_argument("--target", type=float, default=0.95)
+    p.add_argument("--beam", type=int, default=0, help="skip the sweep and use this L")
+    p.add_argument("--cpu-seconds", type=float, default=12.0)
+    p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--out", default="")
+    return p.parse_args()
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                          "-i", str(self.index), "-lms", "200"], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx.append(float(f[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(max(mx)), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            pk = json.load(fh)
+        return float(pk["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def _traffic(workload: str):
+    try:
+        with open(os.path.join(ROOT, "profiles", "search_kernel_traffic.json")) as fh:
+            t = json.load(fh)
+        if t.get("workload") == workload:
+            return t.get("dram_bytes_per_launch")
+    except Exception:
+        pass
+    return None
+
+
+def _dist():
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    return world, rank, local
+
+
+def _gt_device(x_dev, q_dev, k: int):
+    """Exact top-k in f64 on the GPU (oracle.exact_knn semantics: xn - 2 q.x + qn,
+    clamp 0; ties broken by id via a stable sort of the candidates). Measurement only."""
+    import torch
+
+    x64 = x_dev.double()
+    xn = (x64 * x64).sum(1)
+    ids = torch.empty((q_dev.shape[0], k), dtype=torch.int64, device=x_dev.device)
+    ds = torch.empty((q_dev.shape[0], k), dtype=torch.float64, device=x_dev.device)
+    for lo in range(0, q_dev.shape[0], 1024):
+        q = q_dev[lo:lo + 1024].double()
+        s = xn[None, :] - 2.0 * (q @ x64.T) + (q * q).sum(1)[:, None]
+        s.clamp_(min=0.0)
+        d, i = torch.topk(s, k + 16, dim=1, largest=False, sorted=True)
+        # stable (dist, id) order among the candidates
+        o = torch.argsort(i, dim=1)
+        d, i = torch.gather(d, 1, o), torch.gather(i, 1, o)
+        o = torch.argsort(d, dim=1, stable=True)
+        ids[lo:lo + 1024] = torch.gather(i, 1, o)[:, :k]
+        ds[lo:lo + 1024] = torch.gather(d, 1, o)[:, :k]
+        del s
+    del x64
+    return ids, ds
+
+
+def _setup(args, world, rank):
+    """Data, device build, RaBitQ fit, ground truth (merged across shards), sweep."""
+    import torch
+
+    import paper_2601_07048_b200 as jb
+
+    t0 = time.perf_counter()
+    shard_start = rank * args.n
+    x = jb.gen_lowrank(args.n, args.dim, seed=1 + rank, d_int=16, noise=0.05, basis_seed=0)
+    q = jb.gen_lowrank(args.nq, args.dim, seed=1_000_003, d_int=16, noise=0.05, basis_seed=0)
+    ds = jb.VectorDataset(x)
+    ds.device()
+    torch.cuda.synchronize()
+    t_gen = time.perf_counter() - t0
+
+    params = jb.BuildParams(degree_cap=32, build_beam_width=64, alpha=1.2, max_batch=100_000)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    graph = jb.build(ds, params)
+    torch.cuda.synchronize()
+    t_build = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    idx = jb.rabitq_fit(ds, bits=args.bits, seed=1)
+    torch.cuda.synchronize()
+    t_fit = time.perf_counter() - t0
+    q_dev = torch.from_numpy(q).cuda()
+    gt_i, gt_d = _gt_device(ds.device().x, q_dev, 100)
+    gt_i += shard_start
+    if world > 1:
+        import torch.distributed as dist
+
+        all_i = torch.empty((world,) + tuple(gt_i.shape), dtype=gt_i.dtype, device=gt_i.device)
+        all_d = torch.empty((world,) + tuple(gt_d.shape), dtype=gt_d.dtype, device=gt_d.device)
+        dist.all_gather_into_tensor(all_i, gt_i.contiguous())
+        dist.all_gather_into_tensor(all_d, gt_d.contiguous())
+        ci = all_i.permute(1, 0, 2).reshape(args.nq, -1)
+        cd = all_d.permute(1, 0, 2).reshape(args.nq, -1)
+        o = torch.argsort(ci, dim=1)
+        ci, cd = torch.gather(ci, 1, o), torch.gather(cd, 1, o)
+        o = torch.argsort(cd, dim=1, stable=True)[:, :100]
+        gt_i, gt_d = torch.gather(ci, 1, o), torch.gather(cd, 1, o)
+    log(f"gen {t_gen:.1f}s build {t_build:.1f}s ({args.n / t_build:.0f} inserts/s) fit {t_fit:.2f}s")
+    gt = jb.measure.GroundTruth(gt_i.cpu().numpy().astype(np.int64), gt_d.cpu().numpy().astype(np.float32))
+    return dict(jb=jb, x=x, q=q, ds=ds, graph=graph, idx=idx, q_dev=q_dev, gt=gt, shard_start=shard_start,
+                t_gen=t_gen, t_build=t_build, t_fit=t_fit, params=params)
+
+
+def _search_fn(S, world, L, k):
+    """Returns f(q_dev) -> (global ids, dists) running the full per-batch path."""
+    jb = S["jb"]
+    sp = jb.SearchParams(beam_width=L, k=k, rerank=True)
+    if world == 1:
+        return lambda qd: jb.search_knn_batch_device(S["graph"], S["idx"], qd, sp, exact_data=S["ds"])
+    from paper_2601_07048_b200 import shard
+
+    return lambda qd: shard.sharded_knn(
+        lambda qq: jb.search_knn_batch_device(S["graph"], S["idx"], qq, sp, exact_data=S["ds"]), qd, k,
+        S["shard_start"], device=qd.device)
+
+
+def _calibrate(S, args, world):
+    """Smallest L of the sweep reaching the recall target (recall_at_k semantics)."""
+    import torch
+
+    jb = S["jb"]
+    pts = []
+    chosen = None
+    widths = (args.beam,) if args.beam else SWEEP
+    for L in widths:
+        ids, _ = _search_fn(S, world, L, args.k)(S["q_dev"])
+        torch.cuda.synchronize()
+        r = jb.measure.recall_at_k(ids.cpu().numpy(), S["gt"], args.k)
+        pts.append({"L": L, "recall": round(r, 4)})
+        log(f"sweep L={L} recall@{args.k}={r:.4f}")
+        if r >= args.target and chosen is None:
+            chosen = L
+            break
+    if chosen is None:
+        chosen = widths[-1]
+    return chosen, pts
+
+
+def _alg_bytes(S, L):
+    """per query sum_hops(4*deg+4) + sum_evals(record bytes) + 4D (query),
+    for the search kernel; the rerank kernel adds L_valid*(4D) rows + 4D."""
+    import torch
+
+    from paper_2601_07048_b200 import search as jsearch
+
+    jb = S["jb"]
+    g, idx = S["graph"], S["idx"]
+    bound = jsearch._Bound(idx, S["q_dev"])
+    fk, hops, evals, flags, _, _ = jsearch._launch(g, bound, L, None, 0)
+    torch.cuda.synchronize()
+    D = S["x"].shape[1]
+    R = g.degree_cap
+    code_meta = (D * idx.bits + 7) // 8 + 8
+    h = hops.double().sum().item()
+    e = evals.double().sum().item()
+    nq = S["q_dev"].shape[0]
+    # adjacency rows: the kernel reads R slots (4*R B) per hop plus the 4 B key/degree word
+    search_bytes = h * (4 * R + 4) + e * code_meta + nq * 4 * D
+    valid = (fk != -1).sum().item()
+    rerank_bytes = valid * 4 * D + nq * 4 * D
+    return dict(search_bytes=search_bytes, rerank_bytes=rerank_bytes, hops=h / nq, evals=e / nq,
+                lossy=int(flags.sum().item()), record_bytes=jb._lib.lib().jb_rabitq_record_bytes(D, idx.bits))
+
+
+def _timed_steps(S, args, world, L, clocks_idx):
+    """W warmup + K timed steps; per-kernel CUDA events on the launching stream."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2601_07048_b200 import _lib
+    from paper_2601_07048_b200 import search as jsearch
+
+    jb = S["jb"]
+    g, idx, ds = S["graph"], S["idx"], S["ds"]
+    q_dev = S["q_dev"]
+    nq, k = q_dev.shape[0], args.k
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")  # 256 MB > L2
+    rows = ds.device()
+    out_i = torch.empty((nq, k), dtype=torch.int32, device="cuda")
+    out_d = torch.empty((nq, k), dtype=torch.float64, device="cuda")
+    st = _lib.stream_ptr()
+
+    def one_step(ev):
+        ev[0].record()
+        bound = jsearch._Bound(idx, q_dev)                     # bind kernel
+        ev[1].record()
+        fk, *_ = jsearch._launch(g, bound, L, None, 0)         # search kernel
+        ev[2].record()
+        _lib.check(_lib.lib().jb_rerank_topk(_lib.ptr(rows.x), rows.dims, _lib.ptr(q_dev), nq, _lib.ptr(fk), L, k,
+                                             _lib.ptr(out_i), _lib.ptr(out_d), st))  # rerank kernel
+        if world > 1:
+            from paper_2601_07048_b200 import shard
+
+            all_i = torch.empty((world, nq, k), dtype=torch.int32, device="cuda")
+            all_d = torch.empty((world, nq, k), dtype=torch.float64, device="cuda")
+            dist.all_gather_into_tensor(all_i, out_i)
+            dist.all_gather_into_tensor(all_d, out_d)
+            shard.merge_topk_device(all_i, all_d, [r * args.n for r in range(world)], k)  # merge kernel
+        ev[3].record()
+
+    for i in range(args.warmup):
+        flush.fill_(float(i))
+        one_step([torch.cuda.Event(enable_timing=True) for _ in range(4)])
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with Clocks(clocks_idx) as clk:
+        t0 = time.perf_counter()
+        for i in range(args.steps):
+            flush.fill_(float(i + 100))
+            one_step(evs[i])
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+    if world > 1:
+        dist.barrier()
+    step_ms = [evs[i][0].elapsed_time(evs[i][3]) for i in range(args.steps)]
+    search_ms = [evs[i][1].elapsed_time(evs[i][2]) for i in range(args.steps)]
+    bind_ms = [evs[i][0].elapsed_time(evs[i][1]) for i in range(args.steps)]
+    rerank_ms = [evs[i][2].elapsed_time(evs[i][3]) for i in range(args.steps)]
+    tot = float(sum(step_ms))
+    if world > 1:
+        t = torch.tensor([tot], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot = float(t.item())
+    launches_per_step = 3 + (1 if world > 1 else 0)
+    return dict(total_ms=tot, step_ms=step_ms, search_ms=search_ms, bind_ms=bind_ms, rerank_ms=rerank_ms,
+                wall_s=wall, clocks=clk.summary(), launches=launches_per_step * args.steps)
+
+
+def _e2e(S, args, world, L):
+    """Public API with host buffers: H2D queries, search, D2H ids + dists, every step."""
+    import torch
+    import torch.distributed as dist
+
+    jb = S["jb"]
+    sp = jb.SearchParams(beam_width=L, k=args.k, rerank=True)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
+    qh = S["q"]
+    times = []
+    if world == 1:
+        for i in range(args.warmup + args.steps):
+            flush.fill_(float(i))
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            ids, ds = jb.search_knn_batch(S["graph"], S["idx"], qh, sp, exact_data=S["ds"])
+            times.append(time.perf_counter() - t0)
+        d2h = ids.nbytes + ds.nbytes
+    else:
+        from paper_2601_07048_b200.shard import ShardedIndex
+
+        si = ShardedIndex(S["graph"], S["ds"], S["shard_start"], rabitq=S["idx"])
+        rank = dist.get_rank()
+        for i in range(args.warmup + args.steps):
+            flush.fill_(float(i))
+            dist.barrier()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            gi, gd = si.search_knn_batch(qh if rank == 0 else None, sp)
+            if rank == 0:
+                ids, ds = gi.cpu().numpy(), gd.cpu().numpy()
+            torch.cuda.synchronize()
+            dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
+            dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+            times.append(float(dt.item()))
+        d2h = args.nq * args.k * (8 + 8)
+    tt = times[args.warmup:]
+    units = args.nq * world
+    return {"value": round(units * len(tt) / sum(tt), 1), "unit": "queries/s",
+            "h2d_bytes_per_step": int(qh.nbytes), "d2h_bytes_per_step": int(d2h)}
+
+
+def _cpu_worker(payload):
+    import numpy as _np
+
+    from oracle import rabitq as orq
+    from oracle import search as osr
+
+    (adj, active, entry, codes, meta, bits, dims, centroid, seed, x, qs, L, k) = payload
+    rot, qadd, sumq = orq.bind(qs, centroid, bits, seed)
+    src = orq.QuantSource(codes, meta, bits, dims, rot, qadd, sumq)
+    res = osr.beam_search(adj, active, entry, src, len(qs), L)
+    ids, _ = osr.topk(res, k, queries=qs, rerank_data=x)
+    return _np.asarray(ids)
+
+
+_SHARED = {}
+
+
+def _cpu_task(bounds):
+    lo, hi = bounds
+    s = _SHARED
+    return _cpu_worker((s["adj"], s["active"], s["entry"], s["codes"], s["meta"], s["bits"], s["dims"],
+                        s["centroid"], s["seed"], s["x"], s["q"][lo:hi], s["L"], s["k"]))
+
+
+def _cpu_baseline(S, args, L, procs: int, seconds: float):
+    """Reference algorithm (oracle port, numpy) on the host: RaBitQ search + rerank at L."""
+    import multiprocessing as mp
+
+    g, idx = S["graph"], S["idx"]
+    _SHARED.update(adj=np.ascontiguousarray(g.adjacency), active=g.active_count, entry=g.entry_point,
+                   codes=idx.codes, meta=idx.meta, bits=idx.bits, dims=idx.dims, centroid=idx.centroid,
+                   seed=idx.rotation_seed, x=S["x"], q=S["q"], L=L, k=args.k)
+    # probe single-process speed on a small slice, then size the sample to ~`seconds`
+    t0 = time.perf_counter()
+    _cpu_task((0, 50))
+    per_q = (time.perf_counter() - t0) / 50
+    n = int(max(50, min(args.nq, seconds / per_q * max(procs, 1) * 0.8)))
+    n = max(procs, n - n % max(procs, 1))
+    if procs <= 1:
+        t0 = time.perf_counter()
+        ids = _cpu_task((0, n))
+        el = time.perf_counter() - t0
+    else:
+        ctx = mp.get_context("fork")
+        os.environ["OPENBLAS_NUM_THREADS"] = "1"
+        cuts = np.linspace(0, n, procs + 1).astype(int)
+        with ctx.Pool(procs) as pool:
+            pool.map(_cpu_task, [(0, 4)] * procs)  # fork + import warmup
+            t0 = time.perf_counter()
+            parts = pool.map(_cpu_task, list(zip(cuts[:-1], cuts[1:])))
+            el = time.perf_counter() - t0
+        ids = np.concatenate(parts)
+    return n, el, ids
+
+
+def _json_base(args, world, L):
+    return {
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "metric": "QPS at recall@10=0.95", "unit": "queries/s", "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"SIFT-1M-shaped synthetic {args.n}x{args.dim} low-rank (d_int=16, noise 0.05) "
+                               f"per shard, RaBitQ {args.bits}-bit + fp32 rerank, {args.nq} queries, k={args.k}",
+                   "index": {"R": 32, "L_build": 64, "alpha": 1.2, "max_batch": 100000},
+                   "beam_width": L, "shards": world, "parallelism": f"shard{world}",
+                   "l2": "flushed between timed steps (256 MB write, outside the events)"},
+    }
+
+
+def main():
+    args = _args()
+    import torch
+
+    world, rank, local = _dist()
+    if args.impl == "reference" and world > 1 and rank != 0:
+        # reference arm: rank 0 alone runs the CPU reference (its index build uses cuda:0)
+        import torch.distributed as dist
+
+        dist.barrier()
+        dist.destroy_process_group()
+        return
+    if args.impl == "reference":
+        world_eff = 1
+    else:
+        world_eff = world
+    S = _setup(args, world_eff, rank)
+    L, sweep_pts = _calibrate(S, args, world_eff)
+
+    if args.impl == "reference":
+        procs = os.cpu_count() or 1
+        steps = []
+        for i in range(args.warmup + args.steps):
+            n, el, _ = _cpu_baseline(S, args, L, procs, seconds=max(2.0, args.cpu_seconds / 2))
+            steps.append((n, el))
+        tt = steps[args.warmup:]
+        value = sum(n for n, _ in tt) / sum(el for _, el in tt)
+        out = _json_base(args, 1, L)
+        out.update({"impl": "reference", "value": round(value, 1), "ms_per_step": round(1e3 * np.mean([e for _, e in tt]), 2),
+                    "cpu_baseline": {"value": round(value, 1), "unit": "queries/s", "cores": procs, "kind": "port",
+                                     "sample": f"{tt[0][0]} queries per step of the {args.nq}-query batch, numpy oracle "
+                                               f"(reference lockstep algorithm), {procs} forked processes"},
+                    "e2e": {"value": round(value, 1), "unit": "queries/s", "h2d_bytes_per_step": 0,
+                            "d2h_bytes_per_step": 0},
+                    "sweep": sweep_pts})
+        print(json.dumps(out), flush=True)
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    ab = _alg_bytes(S, L)
+    T = _timed_steps(S, args, world, L, local)
+    e2e = _e2e(S, args, world, L)
+    units = args.nq * world * args.steps
+    value = units / (T["total_ms"] / 1e3)
+    peak, peak_kind = _peaks()
+    search_s = float(np.mean(T["search_ms"])) / 1e3
+    achieved = ab["search_bytes"] / search_s / 1e9
+    out = _json_base(args, world, L)
+    out.update({
+        "value": round(value, 1),
+        "ms_per_step": round(T["total_ms"] / args.steps, 3),
+        "e2e": e2e,
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                     "frac": round(achieved / peak, 4), "peak_kind": peak_kind,
+                     "traffic": _traffic(out["config"]["workload"] + f" L={L}"),
+                     "kernel": "beam_search_kernel<RABITQ,1>",
+                     "alg_bytes_per_launch": int(ab["search_bytes"]),
+                     "kernel_ms": round(search_s * 1e3, 4)},
+        "gpu_launches": T["launches"],
+        "clocks": T["clocks"],
+        "recall_at_10": next(p["recall"] for p in sweep_pts if p["L"] == L),
+        "sweep": sweep_pts,
+        "per_query": {"hops": round(ab["hops"], 2), "evals": round(ab["evals"], 1), "lossy_queries": ab["lossy"]},
+        "kernel_ms": {"bind": round(float(np.mean(T["bind_ms"])), 4), "search": round(search_s * 1e3, 4),
+                      "rerank_merge": round(float(np.mean(T["rerank_ms"])), 4)},
+        "build": {"inserts_per_s": round(args.n / S["t_build"], 1), "build_s": round(S["t_build"], 2),
+                  "rabitq_fit_s": round(S["t_fit"], 3), "gen_s": round(S["t_gen"], 2)},
+    })
+    if rank == 0 and world == 1 and not args.no_cpu:
+        n, el, ids = _cpu_baseline(S, args, L, procs=1, seconds=args.cpu_seconds)
+        gpu_ids, _ = _search_fn(S, world, L, args.k)(S["q_dev"][:n])
+        out["cpu_baseline"] = {"value": round(n / el, 1), "unit": "queries/s", "cores": 1, "kind": "port",
+                               "sample": f"first {n} of the {args.nq} queries, numpy oracle port of the reference "
+                                         f"(lockstep RaBitQ search + rerank) at L={L}, 1 process",
+                               "ids_identical_to_gpu": bool(np.array_equal(ids, gpu_ids.cpu().numpy()))}
+    if rank == 0:
+        line = json.dumps(out)
+        print(line, flush=True)
+        if args.out:
+            with open(args.out, "w") as fh:
+                fh.write(line + "\n")
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -10,6 +10,7 @@ from __future__ import annotations
 
 import enum
 import threading
+import warnings
 from dataclasses import dataclass
 
 import numpy as np
@@ -133,7 +134,9 @@ class VectorDataset:
         torch = _lib.require_cuda()
         with self._dev_lock:
             if self._dev is None:
-                x = torch.from_numpy(np.ascontiguousarray(self._data)).to("cuda", non_blocking=False)
+                with warnings.catch_warnings():  # read-only numpy -> torch view, copied to HBM at once
+                    warnings.simplefilter("ignore", UserWarning)
+                    x = torch.from_numpy(np.ascontiguousarray(self._data)).to("cuda", non_blocking=False)
                 norms = torch.empty(x.shape[0], dtype=torch.float32, device=x.device)
                 if x.shape[0]:
                     _lib.check(_lib.lib().jb_row_sq_norms(_lib.ptr(x), x.shape[0], x.shape[1], _lib.ptr(norms),
@@ -199,15 +202,26 @@ def gen_synthetic(count: int, dims: int, seed: int, distribution: str = "gaussia
     return VectorDataset(x.astype(np.float32))
 
 
-def gen_lowrank(count: int, dims: int, seed: int, d_int: int = 16, noise: float = 0.05) -> np.ndarray:
+def gen_lowrank(count: int, dims: int, seed: int, d_int: int = 16, noise: float = 0.05,
+                basis_seed: int | None = None) -> np.ndarray:
     """Low-intrinsic-dimension synthetic rows: SIFT/DEEP/GIST-shaped
-    data on which recall@10 >= 0.95 is reachable. Returns f32 (count, dims)."""
-    g = np.random.default_rng(seed)
-    a = g.standard_normal((d_int, dims)) / np.sqrt(d_int)
+    data on which recall@10 >= 0.95 is reachable. Returns f32 (count, dims).
+
+    With basis_seed=None this is exactly the Appendix B recipe (one generator draws
+    the basis, then the latent rows, then the noise). With basis_seed set, the
+    basis comes from default_rng(basis_seed) and the rows from default_rng(seed),
+    so disjoint shards and held-out queries share one subspace.
+    """
+    if basis_seed is None:
+        g = np.random.default_rng(seed)
+        a = g.standard_normal((d_int, dims)) / np.sqrt(d_int)
+    else:
+        a = np.random.default_rng(basis_seed).standard_normal((d_int, dims)) / np.sqrt(d_int)
+        g = np.random.default_rng(seed)
     out = np.empty((count, dims), dtype=np.float32)
-    step = 262_144
     z_all = g.standard_normal((count, d_int))
-    for lo in range(0, count, step):
+    step = 262_144
+    for lo in range(0, count, step):  # chunked noise draws continue the same stream
         hi = min(count, lo + step)
         out[lo:hi] = z_all[lo:hi] @ a + noise * g.standard_normal((hi - lo, dims))
     return out

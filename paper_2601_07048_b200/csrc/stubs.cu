@@ -4,6 +4,4 @@ using namespace jb;
 extern "C" {
 int jb_exact_knn(const float*, int64_t, int32_t, const float*, int64_t, int32_t, int32_t*, float*, void*) {
     set_error("jb_exact_knn: not built yet"); return JB_EINVAL; }
-int jb_merge_shard_topk(const int32_t*, const double*, int32_t, int64_t, int32_t, const int64_t*, int64_t*, double*, void*) {
-    set_error("jb_merge_shard_topk: not built yet"); return JB_EINVAL; }
 }

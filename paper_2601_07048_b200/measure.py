@@ -1,0 +1,100 @@
+"""Recall / throughput measurement (mirror of the reference's bench.py).
+
+  recall_at_k   bench.py:44-66   distance-threshold matching, eps = 1e-6 relative
+  run_queries   bench.py:69-91   one batched device call (threads are unnecessary)
+  sweep         bench.py:94-137  warmup + timed pass per beam width, recall, QPS
+  SweepPoint / write_sweep_csv   io.py:39, 172-180 column layout
+"""
+
+from __future__ import annotations
+
+import csv
+import time
+from dataclasses import dataclass
+
+import numpy as np
+
+from .search import SearchParams, search_knn_batch
+
+__all__ = ["SweepPoint", "GroundTruth", "recall_at_k", "run_queries", "sweep", "write_sweep_csv"]
+
+_RELATIVE_EPS = 1e-6
+SWEEP_CSV_HEADER = ("beam_width", "k", "recall", "qps", "mean_latency_us")
+
+
+@dataclass(frozen=True)
+class GroundTruth:
+    ids: np.ndarray        # (nq, k) int32
+    distances: np.ndarray  # (nq, k) float32, rows non-decreasing
+
+    @property
+    def query_count(self) -> int:
+        return self.ids.shape[0]
+
+    @property
+    def k(self) -> int:
+        return self.ids.shape[1]
+
+
+@dataclass(frozen=True)
+class SweepPoint:
+    beam_width: int
+    k: int
+    recall: float
+    qps: float
+    mean_latency_us: float
+
+
+def recall_at_k(result_ids, gt, k: int) -> float:
+    """Mean fraction of the exact top-k recovered; ties at the k-th distance count."""
+    if not 1 <= k <= gt.k:
+        raise ValueError(f"k must be in [1, {gt.k}]")
+    res = np.asarray(result_ids)
+    if res.shape[0] != gt.query_count:
+        raise ValueError(f"result rows {res.shape[0]} != ground-truth queries {gt.query_count}")
+    if res.ndim != 2 or res.shape[1] < k:
+        raise ValueError(f"need at least {k} ids per query")
+    gd = gt.distances.astype(np.float64)
+    thr = gd[:, k - 1] + _RELATIVE_EPS * np.abs(gd[:, k - 1])
+    ok = gd <= thr[:, None]
+    got = res[:, :k].astype(np.int64)
+    hit = np.zeros(got.shape, dtype=bool)
+    for j in range(gt.k):  # membership in the within-threshold GT set
+        hit |= (got == gt.ids[:, j:j + 1].astype(np.int64)) & ok[:, j:j + 1]
+    return float(hit.sum(axis=1).mean() / k)
+
+
+def run_queries(graph, source, queries, params: SearchParams, exact_data=None, workers: int = 1):
+    """bench.py:69-91. The device path batches all queries in one launch; `workers`
+    is accepted for signature compatibility."""
+    return search_knn_batch(graph, source, queries, params, exact_data)
+
+
+def write_sweep_csv(path, points) -> None:
+    with open(path, "w", newline="") as fh:
+        w = csv.writer(fh)
+        w.writerow(SWEEP_CSV_HEADER)
+        for p in points:
+            w.writerow([p.beam_width, p.k, f"{p.recall:.6f}", f"{p.qps:.3f}", f"{p.mean_latency_us:.3f}"])
+
+
+def sweep(graph, source, queries, gt, k: int, beam_widths, *, rerank: bool = False, exact_data=None,
+          workers: int = 1, warmup: bool = True, csv_path=None) -> list[SweepPoint]:
+    """bench.py:94-137: per beam width one untimed warmup pass, then a timed pass
+    (host queries in, host ids out) for QPS, and recall against `gt`."""
+    if k > gt.k:
+        raise ValueError(f"k={k} exceeds ground-truth depth {gt.k}")
+    queries = np.atleast_2d(np.asarray(queries))
+    nq = queries.shape[0]
+    pts = []
+    for beam in beam_widths:
+        params = SearchParams(beam_width=int(beam), k=k, rerank=rerank)
+        if warmup:
+            run_queries(graph, source, queries, params, exact_data, workers)
+        t0 = time.perf_counter()
+        ids, _ = run_queries(graph, source, queries, params, exact_data, workers)
+        el = time.perf_counter() - t0
+        pts.append(SweepPoint(int(beam), k, recall_at_k(ids, gt, k), nq / el, el / nq * 1e6))
+    if csv_path is not None:
+        write_sweep_csv(csv_path, pts)
+    return pts
