@@ -9,20 +9,21 @@
 //    exactly the reference's key (search.py:139-145). Bit 31 of the id word is
 //    the device-only "expanded" flag, so a key carries its visited state when
 //    the beam is shifted by a merge.
-//  * visited ("seen") set: an open-addressing hash in smem. It never yields a
-//    false positive. If a probe run fills up, the id is treated as unseen and
-//    re-evaluated; its key is then either already in the beam (dropped by the
-//    equal-key dedupe, the incumbent keeps its flag) or worse than the full
-//    beam's last key (dropped by the filter), because the beam is always the
-//    top-L of every key evaluated so far. Frontier and trace are therefore
-//    identical to the reference's exact `seen` matrix; only `evals` can count
-//    re-evaluations, and flags[q] bit0 reports that.
+//  * visited ("seen") set: a 4-way set-associative id table in smem (one 16 B
+//    probe). It never yields a false positive. When a bucket is full an id is
+//    evicted and may later be re-evaluated; its key is then either already in
+//    the beam (dropped by the equal-key dedupe, the incumbent keeps its flag) or
+//    worse than the full beam's last key (dropped by the filter), because the
+//    beam is always the top-L of every key evaluated so far. Frontier and trace
+//    are therefore identical to the reference's exact `seen` matrix; only
+//    `evals` can count re-evaluations, and flags[q] bit0 reports evictions.
 //  * expansion: the first unexpanded key in ascending order (search.py:202-210).
-//    Neighbours are checked 32 per step (one per lane), new ids are compacted
-//    with a ballot, their distances computed one candidate per lane in the
-//    reference's exact f32 rounding order (A1), then bitonic-sorted in
-//    registers and merged into the beam by rank (binary searches), shifting
-//    beam entries right in 32-wide chunks from the top.
+//    Neighbours are checked 32 per step (one per lane); each new neighbour's
+//    distance is computed by its lane in the reference's exact f32 rounding
+//    order (A1) and merged into the beam by rank (one binary search per
+//    surviving key, a ballot loop for ranks among survivors), shifting beam
+//    entries right in 32-wide chunks from the top. Candidates worse than a full
+//    beam's last key are dropped before any of that.
 //  * exact rows are staged into smem with coalesced cp.async (one 512 B row per
 //    warp instruction at D=128) and then read per lane (16 B skew per row keeps
 //    the per-lane float4 reads bank-conflict free). RaBitQ records are read
@@ -34,61 +35,94 @@
 namespace jb {
 
 constexpr int WPB = 4;          // warps per block
-constexpr int HASH_PROBES = 16; // bounded linear probing
 
 struct SearchLayout {
     int q_off, beam_off, hash_off, newk_off, cid_off, stage_off, bytes;
     int chunk;      // staged elements per row chunk (multiple of 32, <= 128)
     int sstride;    // staged row stride in floats (chunk + 4)
-    int hbits;
+    int hbits;      // log2(number of 4-way buckets)
 };
 
-__device__ __forceinline__ bool hash_insert(uint32_t* h, int hbits, uint32_t id, int& lossy) {
-    const uint32_t mask = (1u << hbits) - 1u;
-    uint32_t s = (id * 0x9E3779B1u) >> (32 - hbits);
-#pragma unroll 1
-    for (int p = 0; p < HASH_PROBES; ++p) {
-        uint32_t cur = h[s];
-        if (cur == id) return false;
-        if (cur == EMPTY_SLOT) {
-            uint32_t old = atomicCAS(&h[s], EMPTY_SLOT, id);
-            if (old == EMPTY_SLOT) return true;
-            if (old == id) return false;
-        }
-        s = (s + 1u) & mask;
-    }
-    lossy = 1;
+// Visited table: 4-way set-associative buckets of ids in smem, one 16 B load per
+// probe. A miss inserts into the first empty way, else evicts a pseudo-random way.
+// No atomics: two lanes racing for one way can only drop an insert. Every outcome
+// is "lossy but safe": an id is never reported seen unless it was evaluated, and a
+// forgotten id is re-evaluated to the same key, which the merge drops (dedupe or
+// beam-worst filter), so frontier and trace stay exact. `lossy` records evictions.
+__device__ __forceinline__ bool visit(uint32_t* tab, int hbits, uint32_t id, int& lossy) {
+    const uint32_t h = id * 0x9E3779B1u;
+    const uint32_t b = h >> (32 - hbits);
+    uint4* bucket = reinterpret_cast<uint4*>(tab) + b;
+    const uint4 v = *bucket;
+    if (v.x == id || v.y == id || v.z == id || v.w == id) return false;
+    int way;
+    if (v.x == EMPTY_SLOT) way = 0;
+    else if (v.y == EMPTY_SLOT) way = 1;
+    else if (v.z == EMPTY_SLOT) way = 2;
+    else if (v.w == EMPTY_SLOT) way = 3;
+    else { way = (h >> 3) & 3; lossy = 1; }
+    reinterpret_cast<uint32_t*>(bucket)[way] = id;
     return true;
 }
 
 // RaBitQ estimator for one packed record (rabitq.py:235-244):
 //   dd  = A1 dot(f32(u), rotated)           (einsum 'md,md->m')
 //   est = max((qadd + data_add) + data_rescale * (dd - qsumq), 0)
+// Full 16 B pieces are unrolled with compile-time bit positions. For m = 1,
+// u*q is exactly q or +-0 and adding +-0 to an accumulator is a no-op, so the
+// product/add pair becomes one predicated add with identical rounding.
+template <int BITS>
+__device__ __forceinline__ void rq_piece_full(Acc4& acc, const uint4 w4, const float* __restrict__ qv, int e0) {
+    constexpr int PER16 = 128 / BITS;
+    constexpr uint32_t MASK = (1u << BITS) - 1u;
+    const uint32_t w[4] = {w4.x, w4.y, w4.z, w4.w};
+#pragma unroll
+    for (int blk = 0; blk < PER16 / 16; ++blk) {
+#pragma unroll
+        for (int i = 3; i >= 0; --i) {
+            const float4 q4 = *reinterpret_cast<const float4*>(qv + e0 + blk * 16 + 4 * i);
+            const float qq[4] = {q4.x, q4.y, q4.z, q4.w};
+            float* lanes[4] = {&acc.l0, &acc.l1, &acc.l2, &acc.l3};
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                constexpr int dummy = 0;
+                (void)dummy;
+                const int off = (blk * 16 + 4 * i + j) * BITS;
+                const uint32_t code = (w[off >> 5] >> (off & 31)) & MASK;
+                if (BITS == 1) {
+                    if (code) *lanes[j] = __fadd_rn(qq[j], *lanes[j]);
+                } else {
+                    *lanes[j] = __fadd_rn(__fmul_rn((float)code, qq[j]), *lanes[j]);
+                }
+            }
+        }
+    }
+}
+
 template <int BITS>
 __device__ __forceinline__ float rabitq_estimate(const uint8_t* __restrict__ rec, const float* __restrict__ qv,
                                                  int D, int meta_off, float qadd, float qsumq) {
     constexpr int PER16 = 128 / BITS;  // elements per 16-byte piece
     constexpr uint32_t MASK = (1u << BITS) - 1u;
     Acc4 acc; acc.zero();
-    for (int e0 = 0; e0 < D; e0 += PER16) {
+    int e0 = 0;
+    for (; e0 + PER16 <= D; e0 += PER16) {
+        const uint4 w4 = __ldg(reinterpret_cast<const uint4*>(rec + (e0 * BITS) / 8));
+        rq_piece_full<BITS>(acc, w4, qv, e0);
+    }
+    if (e0 < D) {  // last partial piece: runtime loop (rare shapes)
         const uint4 w4 = __ldg(reinterpret_cast<const uint4*>(rec + (e0 * BITS) / 8));
         const uint32_t w[4] = {w4.x, w4.y, w4.z, w4.w};
-        const int e1 = min(D, e0 + PER16);
         int b = e0;
-        for (; b + 16 <= e1; b += 16) {
-#pragma unroll
+        for (; b + 16 <= D; b += 16) {
             for (int i = 3; i >= 0; --i) {
-                const float4 q4 = *reinterpret_cast<const float4*>(qv + b + 4 * i);
-                const int off = (b - e0 + 4 * i) * BITS;
-                float4 u;
-                u.x = (float)((w[(off) >> 5] >> ((off) & 31)) & MASK);
-                u.y = (float)((w[(off + BITS) >> 5] >> ((off + BITS) & 31)) & MASK);
-                u.z = (float)((w[(off + 2 * BITS) >> 5] >> ((off + 2 * BITS) & 31)) & MASK);
-                u.w = (float)((w[(off + 3 * BITS) >> 5] >> ((off + 3 * BITS) & 31)) & MASK);
-                acc.madd(u, q4);
+                for (int j = 0; j < 4; ++j) {
+                    const int off = (b - e0 + 4 * i + j) * BITS;
+                    acc.madd1(j, (float)((w[off >> 5] >> (off & 31)) & MASK), qv[b + 4 * i + j]);
+                }
             }
         }
-        for (; b < e1; ++b) {
+        for (; b < D; ++b) {
             const int off = (b - e0) * BITS;
             acc.madd1(b & 3, (float)((w[off >> 5] >> (off & 31)) & MASK), qv[b]);
         }
@@ -111,6 +145,56 @@ __device__ __forceinline__ int first_unexpanded(const uint64_t* beam, int s, int
     return n;
 }
 
+// Merge up to 32 candidate keys (one per lane, UMAX = none) into the sorted beam
+// (search.py:232-237: stable sort of beam + candidates, first L kept). Keys are
+// distinct except a re-evaluated id equal to a beam key (dropped: the incumbent
+// keeps its expanded flag). Positions come from ranks, not a sort:
+//   new key: (#survivors below it) + lower_bound(beam);
+//   beam[i]: i + #{survivors whose lower_bound <= i}.
+// Returns the smallest insertion position (or bcount if nothing was inserted).
+__device__ __forceinline__ int merge_into_beam(uint64_t* beam, int& bcount, int L, uint64_t key, int* psurv) {
+    const unsigned FULL = 0xFFFFFFFFu;
+    const int lane = lane_id();
+    if (key != UMAX && bcount == L && key >= key_mask(beam[L - 1])) key = UMAX;
+    int p = 0;
+    if (key != UMAX) {
+        p = lower_bound_masked(beam, bcount, key);
+        if (p < bcount && key_mask(beam[p]) == key) key = UMAX;
+    }
+    const uint32_t sm = __ballot_sync(FULL, key != UMAX);
+    if (sm == 0) return bcount;
+    const int m2 = __popc(sm);
+    int rank = 0;
+    for (uint32_t mm = sm; mm; mm &= mm - 1) {
+        const int t = __ffs(mm) - 1;
+        rank += (shfl_u64(key, t) < key) ? 1 : 0;
+    }
+    if (key != UMAX) psurv[rank] = p;
+    __syncwarp();
+    const int p0 = psurv[0];
+    for (int cb = ((bcount - 1) >> 5) << 5; cb >= (p0 & ~31); cb -= 32) {
+        const int i = cb + lane;
+        uint64_t bk = 0;
+        int np = -1;
+        if (i >= p0 && i < bcount) {
+            bk = beam[i];
+            int sh = 0;
+            for (int j = 0; j < m2; ++j) sh += (psurv[j] <= i) ? 1 : 0;
+            np = i + sh;
+        }
+        __syncwarp();
+        if (np >= 0 && np < L) beam[np] = bk;
+        __syncwarp();
+    }
+    if (key != UMAX) {
+        const int np = rank + p;
+        if (np < L) beam[np] = key;
+    }
+    __syncwarp();
+    bcount = min(L, bcount + m2);
+    return p0;
+}
+
 template <int SRC, int BITS, bool ALIGNED>
 __global__ void __launch_bounds__(WPB * 32)
 beam_search_kernel(const jb_search_args a, const SearchLayout lay, int* __restrict__ counter) {
@@ -120,15 +204,15 @@ beam_search_kernel(const jb_search_args a, const SearchLayout lay, int* __restri
     unsigned char* base = smem + (size_t)warp * lay.bytes;
     float* qv = reinterpret_cast<float*>(base + lay.q_off);
     uint64_t* beam = reinterpret_cast<uint64_t*>(base + lay.beam_off);
-    uint32_t* hash = reinterpret_cast<uint32_t*>(base + lay.hash_off);
-    uint64_t* newk = reinterpret_cast<uint64_t*>(base + lay.newk_off);
+    uint32_t* tab = reinterpret_cast<uint32_t*>(base + lay.hash_off);
+    int* psurv = reinterpret_cast<int*>(base + lay.newk_off);
     int32_t* cid = reinterpret_cast<int32_t*>(base + lay.cid_off);
     float* stage = reinterpret_cast<float*>(base + lay.stage_off);
 
     const int L = a.beam_width;
     const int D = a.dims;
     const int R = a.degree_cap;
-    const int H = 1 << lay.hbits;
+    const int H = 4 << lay.hbits;
     const int RB = a.record_bytes;
     const int meta_off = ((((D * BITS) + 7) / 8 + 7) / 8) * 8;
     const unsigned FULL = 0xFFFFFFFFu;
@@ -142,7 +226,7 @@ beam_search_kernel(const jb_search_args a, const SearchLayout lay, int* __restri
         const float* q = a.queries + qi * D;
         for (int e = lane; e < D; e += 32) qv[e] = q[e];
         for (int i = lane; i < L; i += 32) beam[i] = UMAX;
-        for (int i = lane; i < H; i += 32) hash[i] = EMPTY_SLOT;
+        for (int i = lane; i < H / 4; i += 32) reinterpret_cast<uint4*>(tab)[i] = make_uint4(EMPTY_SLOT, EMPTY_SLOT, EMPTY_SLOT, EMPTY_SLOT);
         const float qadd = a.query_add[qi];
         const float qsumq = (SRC == JB_SRC_RABITQ) ? a.query_sumq[qi] : 0.0f;
         const uint32_t start = a.starts ? (uint32_t)a.starts[qi] : (uint32_t)a.start_vertex;
@@ -158,7 +242,7 @@ beam_search_kernel(const jb_search_args a, const SearchLayout lay, int* __restri
                 d0 = rabitq_estimate<BITS>(a.records + (size_t)start * RB, qv, D, meta_off, qadd, qsumq);
             }
             beam[0] = pack_key(d0, start);
-            hash_insert(hash, lay.hbits, start, lossy);
+            visit(tab, lay.hbits, start, lossy);
         }
         __syncwarp();
 
@@ -187,18 +271,19 @@ beam_search_kernel(const jb_search_args a, const SearchLayout lay, int* __restri
                 const int nb = (r < R) ? __ldg(adj + r) : -1;
                 __syncwarp();
                 bool isnew = false;
-                if (nb >= 0) isnew = hash_insert(hash, lay.hbits, (uint32_t)nb, lossy);
+                if (nb >= 0) isnew = visit(tab, lay.hbits, (uint32_t)nb, lossy);
                 const uint32_t nm = __ballot_sync(FULL, isnew);
                 const int nnew = __popc(nm);
                 if (nnew == 0) continue;
                 evals += nnew;
-                if (isnew) cid[__popc(nm & lanemask_lt())] = nb;
-                __syncwarp();
 
                 // ---- distances, one candidate per lane ----
                 float d = 0.0f;
-                const int myid = (lane < nnew) ? cid[lane] : 0;
+                int myid = 0;
                 if (SRC == JB_SRC_EXACT) {
+                    if (isnew) cid[__popc(nm & lanemask_lt())] = nb;
+                    __syncwarp();
+                    myid = (lane < nnew) ? cid[lane] : 0;
                     Acc4 acc; acc.zero();
                     for (int e0 = 0; e0 < D; e0 += lay.chunk) {
                         const int clen = min(lay.chunk, D - e0);
@@ -224,52 +309,14 @@ beam_search_kernel(const jb_search_args a, const SearchLayout lay, int* __restri
                     }
                     if (lane < nnew) d = exact_from_dot(__ldg(a.data_norms + myid), acc.reduce(), qadd);
                 } else {
-                    if (lane < nnew)
+                    // records are read in place by the lane that owns the neighbour
+                    myid = nb;
+                    if (isnew)
                         d = rabitq_estimate<BITS>(a.records + (size_t)myid * RB, qv, D, meta_off, qadd, qsumq);
                 }
-
-                // ---- merge into the beam (search.py:232-237 semantics) ----
-                uint64_t key = (lane < nnew) ? pack_key(d, (uint32_t)myid) : UMAX;
-                if (key != UMAX && bcount == L && key >= key_mask(beam[L - 1])) key = UMAX;
-                if (key != UMAX) {
-                    const int p = lower_bound_masked(beam, bcount, key);
-                    if (p < bcount && key_mask(beam[p]) == key) key = UMAX;  // dedupe (lossy table)
-                }
-                key = warp_sort_u64(key);
-                const int m2 = __popc(__ballot_sync(FULL, key != UMAX));
-                if (m2 == 0) continue;
-                int p = 0;
-                if (lane < m2) {
-                    p = lower_bound_masked(beam, bcount, key);
-                    newk[lane] = key;
-                }
-                __syncwarp();
-                const int p0 = __shfl_sync(FULL, p, 0);
-                // shift beam[p0, bcount) right by (#new keys below each entry), top chunk first
-                for (int cb = ((bcount - 1) >> 5) << 5; cb >= (p0 & ~31); cb -= 32) {
-                    const int i = cb + lane;
-                    uint64_t bk = 0;
-                    int np = -1;
-                    if (i >= p0 && i < bcount) {
-                        bk = beam[i];
-                        const uint64_t km = key_mask(bk);
-                        int lo = 0, hi = m2;
-                        while (lo < hi) {
-                            int mid = (lo + hi) >> 1;
-                            if (newk[mid] < km) lo = mid + 1; else hi = mid;
-                        }
-                        np = i + lo;
-                    }
-                    __syncwarp();
-                    if (np >= 0 && np < L) beam[np] = bk;
-                    __syncwarp();
-                }
-                if (lane < m2) {
-                    const int np = lane + p;
-                    if (np < L) beam[np] = key;
-                }
-                __syncwarp();
-                bcount = min(L, bcount + m2);
+                const bool have = (SRC == JB_SRC_EXACT) ? (lane < nnew) : isnew;
+                const uint64_t key = have ? pack_key(d, (uint32_t)myid) : UMAX;
+                const int p0 = merge_into_beam(beam, bcount, L, key, psurv);
                 s_min = min(s_min, p0);
             }
             cursor = first_unexpanded(beam, s_min, bcount);
@@ -364,9 +411,9 @@ static SearchLayout make_layout(int src, int D, int L, int hash_slots) {
     int off = 0;
     s.q_off = off; off += align16(D * 4);
     s.beam_off = off; off += align16(L * 8);
-    s.hbits = log2i(hash_slots);
-    s.hash_off = off; off += align16((1 << s.hbits) * 4);
-    s.newk_off = off; off += 32 * 8;
+    s.hbits = log2i(std::max(1, hash_slots / 4));   // 4-way buckets
+    s.hash_off = off; off += (4 << s.hbits) * 4;
+    s.newk_off = off; off += 32 * 4;
     s.cid_off = off; off += 32 * 4;
     s.chunk = std::min(128, ((D + 31) / 32) * 32);
     s.sstride = s.chunk + 4;
@@ -415,7 +462,7 @@ int jb_beam_search(const jb_search_args* args, void* stream) {
                  "start vertex out of range");
     if (a.nq == 0) return JB_OK;
     int hs = a.hash_slots;
-    if (hs <= 0) hs = std::min(8192, std::max(1024, pow2_ceil(32 * a.beam_width)));
+    if (hs <= 0) hs = std::min(4096, std::max(512, pow2_ceil(16 * a.beam_width)));
     hs = std::max(32, pow2_ceil(hs));
     cudaStream_t st = as_stream(stream);
     if (a.source == JB_SRC_EXACT) {
