@@ -17,9 +17,14 @@ void set_error(const char* fmt, ...) {
 }
 
 int sm_count_current() {
-    int dev = 0, n = 148;
-    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    return n;
+    static thread_local int cached_dev = -1, cached_n = 148;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return cached_n;
+    if (dev != cached_dev) {
+        cudaDeviceGetAttribute(&cached_n, cudaDevAttrMultiProcessorCount, dev);
+        cached_dev = dev;
+    }
+    return cached_n;
 }
 
 // ---- row norms (search.py:101, 113; build.py:120) ----------------------

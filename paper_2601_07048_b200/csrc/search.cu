@@ -429,9 +429,18 @@ static int launch_search(const jb_search_args& a, int hash_slots, cudaStream_t s
     auto kern = beam_search_kernel<SRC, BITS, ALIGNED>;
     const int smem = lay.bytes * WPB;
     JB_CHECK_ARG(smem <= 227 * 1024, "beam search: per-block shared memory %d B exceeds 227 KB", smem);
-    JB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    int per_sm = 0;
-    JB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, WPB * 32, smem));
+    // occupancy per (instantiation, smem size), cached: the attribute/occupancy
+    // queries cost more than the launch itself for small batches
+    static thread_local int cached_smem = -1, cached_per_sm = 0, cached_dev = -1;
+    int dev = 0;
+    JB_CUDA(cudaGetDevice(&dev));
+    if (cached_smem != smem || cached_dev != dev) {
+        JB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        JB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cached_per_sm, kern, WPB * 32, smem));
+        cached_smem = smem;
+        cached_dev = dev;
+    }
+    const int per_sm = cached_per_sm;
     JB_CHECK_ARG(per_sm >= 1, "beam search: kernel does not fit on an SM");
     int64_t need = (a.nq + WPB - 1) / WPB;
     int grid = (int)std::min<int64_t>(need, (int64_t)per_sm * sm_count_current());

@@ -15,6 +15,7 @@ instead of the reference's per-hop numpy lockstep; frontier, trace, hops and
 
 from __future__ import annotations
 
+import threading
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -119,6 +120,25 @@ class _Bound:
             self.count = ds.count
 
 
+class _Pinned(threading.local):
+    """Per-thread pinned staging buffers for host<->HBM copies (reused across calls,
+    so the public host-array API pays one async copy each way, not a pin per call)."""
+
+    def __init__(self):
+        self.bufs = {}
+
+    def get(self, name: str, nbytes: int):
+        torch = _lib.require_cuda()
+        b = self.bufs.get(name)
+        if b is None or b.numel() < nbytes:
+            b = torch.empty(max(nbytes, 1 << 16), dtype=torch.uint8, pin_memory=True)
+            self.bufs[name] = b
+        return b
+
+
+_PINNED = _Pinned()
+
+
 def _queries_to_device(queries):
     torch = _lib.require_cuda()
     if isinstance(queries, torch.Tensor):
@@ -128,8 +148,26 @@ def _queries_to_device(queries):
         return q.to(device="cuda", dtype=torch.float32).contiguous()
     q = np.atleast_2d(np.asarray(queries))
     q = np.ascontiguousarray(q, dtype=np.float32)
-    t = torch.from_numpy(q)
-    return t.pin_memory().to("cuda", non_blocking=True) if t.numel() * 4 >= (1 << 20) else t.to("cuda")
+    if q.size == 0:
+        return torch.empty(q.shape, dtype=torch.float32, device="cuda")
+    buf = _PINNED.get("q", q.nbytes)
+    host = buf[: q.nbytes].view(torch.float32).view(q.shape)
+    host.numpy()[...] = q
+    return host.to("cuda", non_blocking=True)
+
+
+def _to_host(*tensors):
+    """Async D2H of device tensors through pinned buffers, one stream sync, numpy copies out."""
+    torch = _lib.require_cuda()
+    outs = []
+    for i, t in enumerate(tensors):
+        nb = t.numel() * t.element_size()
+        buf = _PINNED.get(f"out{i}", nb)
+        h = buf[:nb].view(t.dtype).view(t.shape)
+        h.copy_(t, non_blocking=True)
+        outs.append(h)
+    torch.cuda.current_stream().synchronize()
+    return [h.numpy().copy() for h in outs]
 
 
 def _launch(graph: GraphIndex, bound: _Bound, L: int, starts_dev=None, trace_cap: int = 0, out=None):
@@ -222,7 +260,18 @@ def run_beam_searches(graph, source, queries, beam_width: int, starts=None) -> l
     else:
         tids_h, tdst_h = tids.cpu().numpy(), tdst.cpu().numpy()
     keys = fk.cpu().numpy().view(np.uint64)
-    evals_h = evals.cpu().numpy()
+    evals_h = evals.cpu().numpy().astype(np.int64)
+    lossy = np.nonzero(flags.cpu().numpy())[0]
+    if lossy.size:
+        # The visited table evicted ids for these queries, so the device counted some
+        # re-evaluations. The reference's count is |{start} U N(u) over expanded u|
+        # (every valid neighbour of an expanded vertex is evaluated exactly once).
+        adj = graph.adjacency
+        st = np.full(nq, graph.entry_point, dtype=np.int64) if starts is None else \
+            np.broadcast_to(np.asarray(starts, dtype=np.int64), (nq,))
+        for i in lossy:
+            nb = adj[tids_h[i, : int(hops_h[i])]].ravel()
+            evals_h[i] = np.unique(np.append(nb[nb >= 0], st[i])).size
     out = []
     for i in range(nq):
         kk = keys[i][keys[i] != _UMAX]
@@ -292,7 +341,8 @@ def search_knn_batch(graph, source, queries, params: SearchParams, exact_data=No
         raise ValueError("rerank over a quantized source requires exact_data")
     q_dev = _queries_to_device(queries)
     ids, dists = _knn_device(graph, source, q_dev, params, exact_data)
-    return ids.cpu().numpy(), dists.cpu().numpy()
+    ids_h, dists_h = _to_host(ids, dists)
+    return ids_h, dists_h
 
 
 def search_knn_batch_device(graph, source, q_dev, params: SearchParams, exact_data=None):
