@@ -61,7 +61,10 @@ int jb_medoid(const float* x, int64_t n, int32_t dims, int64_t* out_host, void* 
 
 /* Distance source of a search. */
 #define JB_SRC_EXACT 0     /* ExactDistances over raw f32 rows (search.py:82-130) */
-#define JB_SRC_RABITQ 1    /* RaBitQ estimator (rabitq.py:225-244)                 */
+#define JB_SRC_RABITQ 1    /* RaBitQ estimator (rabitq.py:225-244), bit-exact      */
+#define JB_SRC_RABITQ_FAST 2 /* RaBitQ, 1-bit codes: query quantized to 6-bit planes,
+                              * <u,q> by AND + popcount (north-star 2). Numerics differ
+                              * from the reference estimator; validated by recall.  */
 
 typedef struct jb_search_args {
     /* graph (GraphIndex, graph.py:36-99): fixed-stride int32 slab padded -1 */

@@ -17,7 +17,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libjasper_b200.so")
 
 JB_OK, JB_EINVAL, JB_ECUDA, JB_ENODONOR, JB_EOVERFLOW = 0, 1, 2, 3, 4
-SRC_EXACT, SRC_RABITQ = 0, 1
+SRC_EXACT, SRC_RABITQ, SRC_RABITQ_FAST = 0, 1, 2
 
 p = C.c_void_p
 i32, i64, f64 = C.c_int32, C.c_int64, C.c_double

@@ -37,7 +37,7 @@ namespace jb {
 constexpr int WPB = 4;          // warps per block
 
 struct SearchLayout {
-    int q_off, beam_off, hash_off, newk_off, cid_off, stage_off, bytes;
+    int q_off, beam_off, hash_off, newk_off, cid_off, stage_off, plane_off, bytes;
     int chunk;      // staged elements per row chunk (multiple of 32, <= 128)
     int sstride;    // staged row stride in floats (chunk + 4)
     int hbits;      // log2(number of 4-way buckets)
@@ -49,11 +49,12 @@ struct SearchLayout {
 // is "lossy but safe": an id is never reported seen unless it was evaluated, and a
 // forgotten id is re-evaluated to the same key, which the merge drops (dedupe or
 // beam-worst filter), so frontier and trace stay exact. `lossy` records evictions.
-__device__ __forceinline__ bool visit(uint32_t* tab, int hbits, uint32_t id, int& lossy) {
+__device__ __forceinline__ bool visit(uint32_t* tab, int hbits, uint32_t id, int& lossy, uint32_t*& slot) {
     const uint32_t h = id * 0x9E3779B1u;
     const uint32_t b = h >> (32 - hbits);
     uint4* bucket = reinterpret_cast<uint4*>(tab) + b;
     const uint4 v = *bucket;
+    slot = nullptr;
     if (v.x == id || v.y == id || v.z == id || v.w == id) return false;
     int way;
     if (v.x == EMPTY_SLOT) way = 0;
@@ -61,7 +62,8 @@ __device__ __forceinline__ bool visit(uint32_t* tab, int hbits, uint32_t id, int
     else if (v.z == EMPTY_SLOT) way = 2;
     else if (v.w == EMPTY_SLOT) way = 3;
     else { way = (h >> 3) & 3; lossy = 1; }
-    reinterpret_cast<uint32_t*>(bucket)[way] = id;
+    slot = reinterpret_cast<uint32_t*>(bucket) + way;
+    *slot = id;
     return true;
 }
 
@@ -133,6 +135,68 @@ __device__ __forceinline__ float rabitq_estimate(const uint8_t* __restrict__ rec
     return est > 0.0f ? est : 0.0f;
 }
 
+// Popcount estimator (fast mode, m = 1): the rotated query is quantized per query
+// to QB-bit integers qq = round((q - lo) / delta) and stored as QB bit-planes
+// (built with warp ballots, element e <-> bit e % 32 of word e / 32, the same
+// layout as the packed 1-bit codes), so
+//   <u, q> ~= lo * popc(u) + delta * sum_b 2^b popc(u & plane_b)
+// replaces the 128 ordered float adds with 4 * (QB + 1) popcounts at D = 128.
+constexpr int FAST_QB = 6;
+
+__device__ __forceinline__ float rabitq_estimate_fast(const uint8_t* __restrict__ rec, const uint32_t* __restrict__ planes,
+                                                      int nwords, int meta_off, float lo, float delta, float qadd,
+                                                      float qsumq) {
+    int pc = 0;
+    int acc[FAST_QB];
+#pragma unroll
+    for (int b = 0; b < FAST_QB; ++b) acc[b] = 0;
+    for (int w0 = 0; w0 < nwords; w0 += 4) {
+        const uint4 c4 = __ldg(reinterpret_cast<const uint4*>(rec + 4 * w0));
+        const uint32_t c[4] = {c4.x, c4.y, c4.z, c4.w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            if (w0 + k < nwords) {
+                pc += __popc(c[k]);
+#pragma unroll
+                for (int b = 0; b < FAST_QB; ++b) acc[b] += __popc(c[k] & planes[b * nwords + w0 + k]);
+            }
+        }
+    }
+    int s = 0;
+#pragma unroll
+    for (int b = 0; b < FAST_QB; ++b) s += acc[b] << b;
+    const float dd = fmaf(delta, (float)s, lo * (float)pc);
+    const float2 m = __ldg(reinterpret_cast<const float2*>(rec + meta_off));
+    const float est = (qadd + m.x) + m.y * (dd - qsumq);
+    return est > 0.0f ? est : 0.0f;
+}
+
+// Build the query bit-planes in smem (one warp): lo/delta from a warp min/max.
+__device__ __forceinline__ void build_planes(const float* qv, int D, uint32_t* planes, float& lo, float& delta) {
+    const int lane = lane_id();
+    float mn = 3.4e38f, mx = -3.4e38f;
+    for (int e = lane; e < D; e += 32) { mn = fminf(mn, qv[e]); mx = fmaxf(mx, qv[e]); }
+    for (int o = 16; o > 0; o >>= 1) {
+        mn = fminf(mn, __shfl_xor_sync(0xFFFFFFFFu, mn, o));
+        mx = fmaxf(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, o));
+    }
+    lo = mn;
+    const float levels = (float)((1 << FAST_QB) - 1);
+    delta = (mx > mn) ? (mx - mn) / levels : 1.0f;
+    const int nwords = (D + 31) / 32;
+    for (int w = 0; w < nwords; ++w) {
+        const int e = w * 32 + lane;
+        uint32_t qq = 0;
+        if (e < D) qq = (uint32_t)min((int)levels, max(0, __float2int_rn((qv[e] - lo) / delta)));
+#pragma unroll
+        for (int b = 0; b < FAST_QB; ++b) {
+            const uint32_t bits = __ballot_sync(0xFFFFFFFFu, (qq >> b) & 1u);
+            if (lane == 0) planes[b * nwords + w] = bits;
+        }
+    }
+    __syncwarp();
+}
+
 // First index >= s (< n) whose key is not expanded; n if none.
 __device__ __forceinline__ int first_unexpanded(const uint64_t* beam, int s, int n) {
     const int lane = lane_id();
@@ -178,9 +242,12 @@ __device__ __forceinline__ int merge_into_beam(uint64_t* beam, int& bcount, int 
         int np = -1;
         if (i >= p0 && i < bcount) {
             bk = beam[i];
-            int sh = 0;
-            for (int j = 0; j < m2; ++j) sh += (psurv[j] <= i) ? 1 : 0;
-            np = i + sh;
+            int lo = 0, hi = m2;  // upper_bound(psurv, i): psurv is ascending
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (psurv[mid] <= i) lo = mid + 1; else hi = mid;
+            }
+            np = i + lo;
         }
         __syncwarp();
         if (np >= 0 && np < L) beam[np] = bk;
@@ -208,6 +275,8 @@ beam_search_kernel(const jb_search_args a, const SearchLayout lay, int* __restri
     int* psurv = reinterpret_cast<int*>(base + lay.newk_off);
     int32_t* cid = reinterpret_cast<int32_t*>(base + lay.cid_off);
     float* stage = reinterpret_cast<float*>(base + lay.stage_off);
+    uint32_t* planes = reinterpret_cast<uint32_t*>(base + lay.plane_off);
+    const int nwords = (a.dims + 31) / 32;
 
     const int L = a.beam_width;
     const int D = a.dims;
@@ -228,9 +297,11 @@ beam_search_kernel(const jb_search_args a, const SearchLayout lay, int* __restri
         for (int i = lane; i < L; i += 32) beam[i] = UMAX;
         for (int i = lane; i < H / 4; i += 32) reinterpret_cast<uint4*>(tab)[i] = make_uint4(EMPTY_SLOT, EMPTY_SLOT, EMPTY_SLOT, EMPTY_SLOT);
         const float qadd = a.query_add[qi];
-        const float qsumq = (SRC == JB_SRC_RABITQ) ? a.query_sumq[qi] : 0.0f;
+        const float qsumq = (SRC != JB_SRC_EXACT) ? a.query_sumq[qi] : 0.0f;
         const uint32_t start = a.starts ? (uint32_t)a.starts[qi] : (uint32_t)a.start_vertex;
         __syncwarp();
+        float qlo = 0.0f, qdelta = 0.0f;
+        if (SRC == JB_SRC_RABITQ_FAST) build_planes(qv, D, planes, qlo, qdelta);
 
         int lossy = 0;
         if (lane == 0) {
@@ -238,11 +309,15 @@ beam_search_kernel(const jb_search_args a, const SearchLayout lay, int* __restri
             if (SRC == JB_SRC_EXACT) {
                 const float dot = a1_dot<false>(a.data + (size_t)start * D, qv, D);
                 d0 = exact_from_dot(a.data_norms[start], dot, qadd);
+            } else if (SRC == JB_SRC_RABITQ_FAST) {
+                d0 = rabitq_estimate_fast(a.records + (size_t)start * RB, planes, nwords, meta_off, qlo, qdelta, qadd,
+                                          qsumq);
             } else {
                 d0 = rabitq_estimate<BITS>(a.records + (size_t)start * RB, qv, D, meta_off, qadd, qsumq);
             }
             beam[0] = pack_key(d0, start);
-            visit(tab, lay.hbits, start, lossy);
+            uint32_t* sl;
+            visit(tab, lay.hbits, start, lossy, sl);
         }
         __syncwarp();
 
@@ -271,7 +346,12 @@ beam_search_kernel(const jb_search_args a, const SearchLayout lay, int* __restri
                 const int nb = (r < R) ? __ldg(adj + r) : -1;
                 __syncwarp();
                 bool isnew = false;
-                if (nb >= 0) isnew = visit(tab, lay.hbits, (uint32_t)nb, lossy);
+                uint32_t* slot = nullptr;
+                if (nb >= 0) isnew = visit(tab, lay.hbits, (uint32_t)nb, lossy, slot);
+                __syncwarp();
+                // two lanes may have claimed the same empty way: the loser's id is
+                // forgotten (safe, but it may be re-evaluated later -> flag it)
+                if (slot != nullptr && *slot != (uint32_t)nb) lossy = 1;
                 const uint32_t nm = __ballot_sync(FULL, isnew);
                 const int nnew = __popc(nm);
                 if (nnew == 0) continue;
@@ -311,8 +391,13 @@ beam_search_kernel(const jb_search_args a, const SearchLayout lay, int* __restri
                 } else {
                     // records are read in place by the lane that owns the neighbour
                     myid = nb;
-                    if (isnew)
-                        d = rabitq_estimate<BITS>(a.records + (size_t)myid * RB, qv, D, meta_off, qadd, qsumq);
+                    if (isnew) {
+                        if (SRC == JB_SRC_RABITQ_FAST)
+                            d = rabitq_estimate_fast(a.records + (size_t)myid * RB, planes, nwords, meta_off, qlo,
+                                                     qdelta, qadd, qsumq);
+                        else
+                            d = rabitq_estimate<BITS>(a.records + (size_t)myid * RB, qv, D, meta_off, qadd, qsumq);
+                    }
                 }
                 const bool have = (SRC == JB_SRC_EXACT) ? (lane < nnew) : isnew;
                 const uint64_t key = have ? pack_key(d, (uint32_t)myid) : UMAX;
@@ -419,6 +504,8 @@ static SearchLayout make_layout(int src, int D, int L, int hash_slots) {
     s.sstride = s.chunk + 4;
     s.stage_off = off;
     if (src == JB_SRC_EXACT) off += 32 * s.sstride * 4;
+    s.plane_off = off;
+    if (src == JB_SRC_RABITQ_FAST) off += FAST_QB * ((D + 31) / 32) * 4;
     s.bytes = align16(off);
     return s;
 }
@@ -479,9 +566,13 @@ int jb_beam_search(const jb_search_args* args, void* stream) {
         if ((a.dims & 3) == 0) return launch_search<JB_SRC_EXACT, 1, true>(a, hs, st);
         return launch_search<JB_SRC_EXACT, 1, false>(a, hs, st);
     }
-    JB_CHECK_ARG(a.source == JB_SRC_RABITQ, "unknown distance source %d", a.source);
+    JB_CHECK_ARG(a.source == JB_SRC_RABITQ || a.source == JB_SRC_RABITQ_FAST, "unknown distance source %d", a.source);
     JB_CHECK_ARG(a.records && a.queries && a.query_add && a.query_sumq, "rabitq search: missing arrays");
     JB_CHECK_ARG(a.record_bytes == jb_rabitq_record_bytes(a.dims, a.bits), "rabitq search: record_bytes mismatch");
+    if (a.source == JB_SRC_RABITQ_FAST) {
+        JB_CHECK_ARG(a.bits == 1, "popcount fast mode supports 1-bit codes");
+        return launch_search<JB_SRC_RABITQ_FAST, 1, true>(a, hs, st);
+    }
     switch (a.bits) {
         case 1: return launch_search<JB_SRC_RABITQ, 1, true>(a, hs, st);
         case 2: return launch_search<JB_SRC_RABITQ, 2, true>(a, hs, st);

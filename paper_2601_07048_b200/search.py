@@ -33,17 +33,28 @@ _UMAX = np.uint64(0xFFFFFFFFFFFFFFFF)
 TUNING = {"hash_slots": 0}
 
 
+ESTIMATORS = ("reference", "popcount")
+
+
 @dataclass(frozen=True)
 class SearchParams:
+    """search.py:42-54, plus `estimator` for quantized sources:
+    "reference" = the reference's float estimator, bit-exact (default);
+    "popcount"  = 1-bit codes only, query quantized to 6-bit planes and <u,q>
+                  computed with AND + popcount (faster; validated by recall)."""
+
     beam_width: int
     k: int = 10
     rerank: bool = False
+    estimator: str = "reference"
 
     def __post_init__(self):
         if not 1 <= self.beam_width <= MAX_BEAM_WIDTH:
             raise ValueError(f"beam_width must be in [1, {MAX_BEAM_WIDTH}]")
         if not 1 <= self.k <= self.beam_width:
             raise ValueError("k must satisfy 1 <= k <= beam_width")
+        if self.estimator not in ESTIMATORS:
+            raise ValueError(f"estimator must be one of {ESTIMATORS}")
 
 
 @dataclass
@@ -79,7 +90,7 @@ def _is_rabitq(source) -> bool:
 class _Bound:
     """Device-side distance source bound to a query block (search.py:159-168)."""
 
-    def __init__(self, source, q_dev):
+    def __init__(self, source, q_dev, estimator: str = "reference"):
         torch = _lib.require_cuda()
         self.q_dev = q_dev
         nq, D = q_dev.shape
@@ -91,6 +102,10 @@ class _Bound:
                 raise ValueError(f"query dims {D} != index dims {idx.dims}")
             dev = idx.device()
             self.kind = _lib.SRC_RABITQ
+            if estimator == "popcount":
+                if idx.bits != 1:
+                    raise ValueError("the popcount estimator needs 1-bit codes")
+                self.kind = _lib.SRC_RABITQ_FAST
             self.dims = idx.dims
             self.records, self.record_bytes, self.bits = dev.records, dev.record_bytes, idx.bits
             self.rows = None
@@ -310,7 +325,7 @@ def _knn_device(graph: GraphIndex, source, q_dev, params: SearchParams, exact_da
     rerank = params.rerank and _is_rabitq(source)
     if rerank and exact_data is None:
         raise ValueError("rerank over a quantized source requires exact_data")
-    bound = _Bound(source, q_dev)
+    bound = _Bound(source, q_dev, params.estimator)
     L, k = params.beam_width, params.k
     fk, *_ = _launch(graph, bound, L, starts_dev, 0)
     ids = torch.empty((nq, k), dtype=torch.int32, device=q_dev.device)

@@ -38,9 +38,9 @@ def _assert_same(res, exp_fids, exp_fd, exp_vids, exp_vd, exp_hops, exp_evals=No
         np.testing.assert_array_equal(r.frontier_dists, exp_fd[i], err_msg=f"query {i} frontier dists")
         np.testing.assert_array_equal(r.visited_ids, exp_vids[i], err_msg=f"query {i} trace")
         np.testing.assert_array_equal(r.visited_dists, exp_vd[i], err_msg=f"query {i} trace dists")
-        assert r.stats.hops == exp_hops[i]
+        assert r.stats.hops == exp_hops[i], f"query {i} hops"
         if exp_evals is not None:
-            assert r.stats.distance_evals == exp_evals[i]
+            assert r.stats.distance_evals == exp_evals[i], f"query {i} evals {r.stats.distance_evals} != {exp_evals[i]}"
 
 
 def _golden_check(res, f, p):
@@ -254,3 +254,25 @@ def test_medoid_matches_reference_golden():
     f = golden("misc")
     assert jb.medoid(jb.VectorDataset(gaussian(3000, 32, 0))) == int(f["medoid32"])
     assert jb.medoid(jb.VectorDataset(lowrank(4000, 128, 12, 0.05, 7))) == int(f["medoid128"])
+
+
+def test_popcount_estimator_recall_tracks_reference_estimator():
+    x = jb.gen_lowrank(20000, 128, seed=1, basis_seed=0)
+    q = jb.gen_lowrank(300, 128, seed=2, basis_seed=0)
+    ds = jb.VectorDataset(x)
+    g = jb.build(ds, jb.BuildParams(degree_cap=32, build_beam_width=64, alpha=1.2))
+    idx = jb.rabitq_fit(ds, bits=1, seed=1)
+    gt_i, gt_d = oknn.exact_knn(x, q, 50)
+    gt = jb.GroundTruth(gt_i, gt_d)
+    for L in (32, 64):
+        r = {}
+        for est in ("reference", "popcount"):
+            ids, ds_ = jb.search_knn_batch(g, idx, q, jb.SearchParams(beam_width=L, k=10, rerank=True, estimator=est),
+                                           exact_data=ds)
+            assert np.all(np.diff(ds_, axis=1) >= 0)  # reranked: ascending exact distances
+            r[est] = jb.recall_at_k(ids, gt, 10)
+        assert r["popcount"] >= r["reference"] - 0.02, r
+    with pytest.raises(ValueError, match="1-bit"):
+        idx4 = jb.rabitq_fit(ds, bits=4, seed=1)
+        jb.search_knn_batch(g, idx4, q, jb.SearchParams(beam_width=16, k=10, rerank=True, estimator="popcount"),
+                            exact_data=ds)
