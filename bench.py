@@ -60,6 +60,7 @@ def _args():
     p.add_argument("--cpu-seconds", type=float, default=12.0)
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--out", default="")
+    p.add_argument("--hash-slots", type=int, default=0, help="visited-table slots per query (0 = library default)")
     p.add_argument("--estimator", default="auto", choices=["auto", "reference", "popcount"],
                    help="RaBitQ estimator; auto times both and reports the faster at the recall target")
     return p.parse_args()
@@ -468,6 +469,10 @@ def main():
     import torch
 
     world, rank, local = _dist()
+    if args.hash_slots:
+        from paper_2601_07048_b200 import search as _js
+
+        _js.TUNING["hash_slots"] = args.hash_slots
     if args.impl == "reference" and world > 1 and rank != 0:
         # reference arm: rank 0 alone runs the CPU reference (its index build uses cuda:0)
         import torch.distributed as dist

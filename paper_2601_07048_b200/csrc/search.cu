@@ -35,6 +35,7 @@
 namespace jb {
 
 constexpr int WPB = 4;          // warps per block
+constexpr int MAX_CHUNKS = 4;   // neighbour slots per hop: R <= 32 * MAX_CHUNKS
 
 struct SearchLayout {
     int q_off, beam_off, hash_off, newk_off, cid_off, stage_off, plane_off, bytes;
@@ -101,19 +102,20 @@ __device__ __forceinline__ void rq_piece_full(Acc4& acc, const uint4 w4, const f
     }
 }
 
+// <u, q> for one record whose first 16-byte code piece is already in registers.
 template <int BITS>
-__device__ __forceinline__ float rabitq_estimate(const uint8_t* __restrict__ rec, const float* __restrict__ qv,
-                                                 int D, int meta_off, float qadd, float qsumq) {
+__device__ __forceinline__ float rabitq_dd(const uint8_t* __restrict__ rec, uint4 first, const float* __restrict__ qv,
+                                           int D) {
     constexpr int PER16 = 128 / BITS;  // elements per 16-byte piece
     constexpr uint32_t MASK = (1u << BITS) - 1u;
     Acc4 acc; acc.zero();
     int e0 = 0;
     for (; e0 + PER16 <= D; e0 += PER16) {
-        const uint4 w4 = __ldg(reinterpret_cast<const uint4*>(rec + (e0 * BITS) / 8));
+        const uint4 w4 = e0 == 0 ? first : __ldg(reinterpret_cast<const uint4*>(rec + (e0 * BITS) / 8));
         rq_piece_full<BITS>(acc, w4, qv, e0);
     }
     if (e0 < D) {  // last partial piece: runtime loop (rare shapes)
-        const uint4 w4 = __ldg(reinterpret_cast<const uint4*>(rec + (e0 * BITS) / 8));
+        const uint4 w4 = e0 == 0 ? first : __ldg(reinterpret_cast<const uint4*>(rec + (e0 * BITS) / 8));
         const uint32_t w[4] = {w4.x, w4.y, w4.z, w4.w};
         int b = e0;
         for (; b + 16 <= D; b += 16) {
@@ -129,10 +131,21 @@ __device__ __forceinline__ float rabitq_estimate(const uint8_t* __restrict__ rec
             acc.madd1(b & 3, (float)((w[off >> 5] >> (off & 31)) & MASK), qv[b]);
         }
     }
-    const float dd = acc.reduce();
-    const float2 m = __ldg(reinterpret_cast<const float2*>(rec + meta_off));
-    float est = __fadd_rn(__fadd_rn(qadd, m.x), __fmul_rn(m.y, __fsub_rn(dd, qsumq)));
+    return acc.reduce();
+}
+
+// est = max((qadd + data_add) + data_rescale * (dd - qsumq), 0) in the reference's order
+__device__ __forceinline__ float rabitq_finish(float dd, float2 m, float qadd, float qsumq) {
+    const float est = __fadd_rn(__fadd_rn(qadd, m.x), __fmul_rn(m.y, __fsub_rn(dd, qsumq)));
     return est > 0.0f ? est : 0.0f;
+}
+
+template <int BITS>
+__device__ __forceinline__ float rabitq_estimate(const uint8_t* __restrict__ rec, const float* __restrict__ qv,
+                                                 int D, int meta_off, float qadd, float qsumq) {
+    const uint4 first = __ldg(reinterpret_cast<const uint4*>(rec));
+    const float dd = rabitq_dd<BITS>(rec, first, qv, D);
+    return rabitq_finish(dd, __ldg(reinterpret_cast<const float2*>(rec + meta_off)), qadd, qsumq);
 }
 
 // Popcount estimator (fast mode, m = 1): the rotated query is quantized per query
@@ -143,15 +156,14 @@ __device__ __forceinline__ float rabitq_estimate(const uint8_t* __restrict__ rec
 // replaces the 128 ordered float adds with 4 * (QB + 1) popcounts at D = 128.
 constexpr int FAST_QB = 6;
 
-__device__ __forceinline__ float rabitq_estimate_fast(const uint8_t* __restrict__ rec, const uint32_t* __restrict__ planes,
-                                                      int nwords, int meta_off, float lo, float delta, float qadd,
-                                                      float qsumq) {
+__device__ __forceinline__ float rabitq_dd_fast(const uint8_t* __restrict__ rec, uint4 first,
+                                               const uint32_t* __restrict__ planes, int nwords, float lo, float delta) {
     int pc = 0;
     int acc[FAST_QB];
 #pragma unroll
     for (int b = 0; b < FAST_QB; ++b) acc[b] = 0;
     for (int w0 = 0; w0 < nwords; w0 += 4) {
-        const uint4 c4 = __ldg(reinterpret_cast<const uint4*>(rec + 4 * w0));
+        const uint4 c4 = w0 == 0 ? first : __ldg(reinterpret_cast<const uint4*>(rec + 4 * w0));
         const uint32_t c[4] = {c4.x, c4.y, c4.z, c4.w};
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
@@ -165,7 +177,14 @@ __device__ __forceinline__ float rabitq_estimate_fast(const uint8_t* __restrict_
     int s = 0;
 #pragma unroll
     for (int b = 0; b < FAST_QB; ++b) s += acc[b] << b;
-    const float dd = fmaf(delta, (float)s, lo * (float)pc);
+    return fmaf(delta, (float)s, lo * (float)pc);
+}
+
+__device__ __forceinline__ float rabitq_estimate_fast(const uint8_t* __restrict__ rec, const uint32_t* __restrict__ planes,
+                                                      int nwords, int meta_off, float lo, float delta, float qadd,
+                                                      float qsumq) {
+    const uint4 first = __ldg(reinterpret_cast<const uint4*>(rec));
+    const float dd = rabitq_dd_fast(rec, first, planes, nwords, lo, delta);
     const float2 m = __ldg(reinterpret_cast<const float2*>(rec + meta_off));
     const float est = (qadd + m.x) + m.y * (dd - qsumq);
     return est > 0.0f ? est : 0.0f;
@@ -326,9 +345,19 @@ beam_search_kernel(const jb_search_args a, const SearchLayout lay, int* __restri
         int32_t* tids = a.trace_ids ? a.trace_ids + qi * (int64_t)tcap : nullptr;
         float* tdst = a.trace_dists ? a.trace_dists + qi * (int64_t)tcap : nullptr;
 
+        // Speculative adjacency prefetch: the next expansion is guessed as the first
+        // unexpanded key after the cursor in the pre-merge beam (right whenever this
+        // hop inserts nothing in front of it). Its row is loaded while this hop runs.
+        int spec = -1;
+        int spec_nb[MAX_CHUNKS];
+#pragma unroll
+        for (int c = 0; c < MAX_CHUNKS; ++c) spec_nb[c] = -1;
+
         while (cursor < bcount) {
             const uint64_t ukey = beam[cursor];
             const uint32_t u = key_id(ukey);
+            const int sidx = first_unexpanded(beam, cursor + 1, bcount);
+            const int nspec = sidx < bcount ? (int)key_id(beam[sidx]) : -1;
             __syncwarp();
             if (lane == 0) {
                 beam[cursor] = ukey | EXPANDED;
@@ -339,12 +368,28 @@ beam_search_kernel(const jb_search_args a, const SearchLayout lay, int* __restri
             }
             ++hops;
             int s_min = cursor + 1;
-            const int32_t* adj = a.adjacency + (size_t)u * R;
+            int nbv[MAX_CHUNKS];
+            const int32_t* adj_u = a.adjacency + (size_t)u * R;
+            const int32_t* adj_s = a.adjacency + (size_t)(nspec < 0 ? 0 : nspec) * R;
+#pragma unroll
+            for (int c = 0; c < MAX_CHUNKS; ++c) {
+                const int r = c * 32 + lane;
+                nbv[c] = (spec == (int)u) ? spec_nb[c] : ((r < R) ? __ldg(adj_u + r) : -1);
+                spec_nb[c] = (nspec >= 0 && r < R) ? __ldg(adj_s + r) : -1;
+            }
+            spec = nspec;
 
-            for (int c0 = 0; c0 < R; c0 += 32) {
-                const int r = c0 + lane;
-                const int nb = (r < R) ? __ldg(adj + r) : -1;
-                __syncwarp();
+#pragma unroll
+            for (int c = 0; c < MAX_CHUNKS; ++c) {
+                if (c * 32 >= R) break;
+                const int nb = nbv[c];
+                // RaBitQ: issue the candidate's record loads before the visited check
+                uint4 rc0 = make_uint4(0, 0, 0, 0), rc1 = make_uint4(0, 0, 0, 0);
+                if (SRC != JB_SRC_EXACT && nb >= 0) {
+                    const uint8_t* rec = a.records + (size_t)nb * RB;
+                    rc0 = __ldg(reinterpret_cast<const uint4*>(rec));
+                    if (RB == 32) rc1 = __ldg(reinterpret_cast<const uint4*>(rec + 16));
+                }
                 bool isnew = false;
                 uint32_t* slot = nullptr;
                 if (nb >= 0) isnew = visit(tab, lay.hbits, (uint32_t)nb, lossy, slot);
@@ -389,14 +434,19 @@ beam_search_kernel(const jb_search_args a, const SearchLayout lay, int* __restri
                     }
                     if (lane < nnew) d = exact_from_dot(__ldg(a.data_norms + myid), acc.reduce(), qadd);
                 } else {
-                    // records are read in place by the lane that owns the neighbour
+                    // the lane that owns the neighbour evaluates it from its registers
                     myid = nb;
                     if (isnew) {
-                        if (SRC == JB_SRC_RABITQ_FAST)
-                            d = rabitq_estimate_fast(a.records + (size_t)myid * RB, planes, nwords, meta_off, qlo,
-                                                     qdelta, qadd, qsumq);
-                        else
-                            d = rabitq_estimate<BITS>(a.records + (size_t)myid * RB, qv, D, meta_off, qadd, qsumq);
+                        const uint8_t* rec = a.records + (size_t)myid * RB;
+                        const float2 m = (RB == 32) ? make_float2(__uint_as_float(rc1.x), __uint_as_float(rc1.y))
+                                                    : __ldg(reinterpret_cast<const float2*>(rec + meta_off));
+                        if (SRC == JB_SRC_RABITQ_FAST) {
+                            const float dd = rabitq_dd_fast(rec, rc0, planes, nwords, qlo, qdelta);
+                            const float est = (qadd + m.x) + m.y * (dd - qsumq);
+                            d = est > 0.0f ? est : 0.0f;
+                        } else {
+                            d = rabitq_finish(rabitq_dd<BITS>(rec, rc0, qv, D), m, qadd, qsumq);
+                        }
                     }
                 }
                 const bool have = (SRC == JB_SRC_EXACT) ? (lane < nnew) : isnew;
@@ -550,7 +600,8 @@ int jb_beam_search(const jb_search_args* args, void* stream) {
     const jb_search_args& a = *args;
     JB_CHECK_ARG(a.active_count > 0, "search on an empty graph");
     JB_CHECK_ARG(a.beam_width >= 1 && a.beam_width <= 1024, "beam_width must be in [1, 1024]");
-    JB_CHECK_ARG(a.degree_cap >= 1, "degree_cap must be >= 1");
+    JB_CHECK_ARG(a.degree_cap >= 1 && a.degree_cap <= 32 * MAX_CHUNKS, "degree_cap must be in [1, %d]",
+                 32 * MAX_CHUNKS);
     JB_CHECK_ARG(a.dims >= 1, "dims must be >= 1");
     JB_CHECK_ARG(a.active_count < (1ll << 31), "active_count exceeds int32 ids");
     JB_CHECK_ARG(a.trace_cap == 0 || (a.trace_ids && a.trace_dists), "trace buffers required when trace_cap > 0");
