@@ -209,10 +209,11 @@ def _setup(args, world, rank):
     if world > 1:
         import torch.distributed as dist
 
-        all_i = torch.empty((world,) + tuple(gt_i.shape), dtype=gt_i.dtype, device=gt_i.device)
-        all_d = torch.empty((world,) + tuple(gt_d.shape), dtype=gt_d.dtype, device=gt_d.device)
+        all_i = torch.empty((world * gt_i.shape[0], gt_i.shape[1]), dtype=gt_i.dtype, device=gt_i.device)
+        all_d = torch.empty((world * gt_d.shape[0], gt_d.shape[1]), dtype=gt_d.dtype, device=gt_d.device)
         dist.all_gather_into_tensor(all_i, gt_i.contiguous())
         dist.all_gather_into_tensor(all_d, gt_d.contiguous())
+        all_i, all_d = all_i.view(world, *gt_i.shape), all_d.view(world, *gt_d.shape)
         ci = all_i.permute(1, 0, 2).reshape(args.nq, -1)
         cd = all_d.permute(1, 0, 2).reshape(args.nq, -1)
         o = torch.argsort(ci, dim=1)
@@ -315,11 +316,12 @@ def _timed_steps(S, args, world, L, clocks_idx, est="reference"):
         if world > 1:
             from paper_2601_07048_b200 import shard
 
-            all_i = torch.empty((world, nq, k), dtype=torch.int32, device="cuda")
-            all_d = torch.empty((world, nq, k), dtype=torch.float64, device="cuda")
+            all_i = torch.empty((world * nq, k), dtype=torch.int32, device="cuda")
+            all_d = torch.empty((world * nq, k), dtype=torch.float64, device="cuda")
             dist.all_gather_into_tensor(all_i, out_i)
             dist.all_gather_into_tensor(all_d, out_d)
-            shard.merge_topk_device(all_i, all_d, [r * args.n for r in range(world)], k)  # merge kernel
+            shard.merge_topk_device(all_i.view(world, nq, k), all_d.view(world, nq, k),
+                                    [r * args.n for r in range(world)], k)  # merge kernel
         ev[3].record()
 
     for i in range(args.warmup):

@@ -119,8 +119,8 @@ int jb_rerank_topk(const float* data, int32_t dims, const float* queries, int64_
 
 /* ---- RaBitQ (north-star 2) --------------------------------------------- */
 
-/* Packed device record of one vector: code bytes, zero padding to 8, then
- * (data_add, data_rescale) f32, total rounded up to 16 bytes. */
+/* Packed device record of one vector: code bytes, zero padding to 16, then
+ * (data_add, data_rescale) f32, total rounded up to 16 bytes (32 B at D=128, m=1). */
 int32_t jb_rabitq_record_bytes(int32_t dims, int32_t bits);
 
 /* Build records from reference-layout codes [n, ceil(D*m/8)] and meta [n, 2].

@@ -36,3 +36,18 @@ def recall_at_k(result_ids, gt_ids: np.ndarray, gt_dists: np.ndarray, k: int) ->
         got = np.asarray(result_ids[i], dtype=np.int64)[:k]
         tot += np.isin(got, gt_ids[i][g[i] <= thr[i]]).sum() / k
     return tot / len(result_ids)
+
+
+def merge_shard_topk(ids_all: np.ndarray, dists_all: np.ndarray, offsets, k: int):
+    """Global top-k by (dist, global id) from per-shard lists [S, nq, k] (-1 = padding).
+    The checker for the device merge."""
+    S, nq, _ = ids_all.shape
+    out_i = np.full((nq, k), -1, dtype=np.int64)
+    out_d = np.full((nq, k), np.inf)
+    for q in range(nq):
+        cand = [(float(dists_all[s, q, j]), int(ids_all[s, q, j]) + int(offsets[s]))
+                for s in range(S) for j in range(ids_all.shape[2]) if ids_all[s, q, j] >= 0]
+        cand.sort()
+        for j, (d, g) in enumerate(cand[:k]):
+            out_i[q, j], out_d[q, j] = g, d
+    return out_i, out_d

@@ -3,7 +3,7 @@
 //  * jb_rabitq_encode   replaces the per-block body of rabitq.fit (rabitq.py:282-299)
 //  * jb_rabitq_bind     replaces RaBitQIndex.bind (rabitq.py:170-181)
 //  * jb_rabitq_pack_records builds the packed device record used by the search
-//    estimator (rabitq.py:235-244): code bytes | pad to 8 | data_add, data_rescale
+//    estimator (rabitq.py:235-244): code bytes | zero pad to 16 | data_add, data_rescale
 //    | pad to 16, so one vector is one aligned request (32 B at D=128, m=1).
 //
 // Bit-exactness: every f64 step follows the reference formula in the same
@@ -18,7 +18,7 @@
 namespace jb {
 
 __host__ __device__ inline int code_bytes_of(int D, int bits) { return (D * bits + 7) / 8; }
-__host__ __device__ inline int meta_off_of(int D, int bits) { return ((code_bytes_of(D, bits) + 7) / 8) * 8; }
+__host__ __device__ inline int meta_off_of(int D, int bits) { return ((code_bytes_of(D, bits) + 15) / 16) * 16; }
 __host__ __device__ inline int record_bytes_of(int D, int bits) { return ((meta_off_of(D, bits) + 8 + 15) / 16) * 16; }
 
 __global__ void pack_records_kernel(const uint8_t* __restrict__ codes, const float* __restrict__ meta, int64_t n,

@@ -156,22 +156,20 @@ __device__ __forceinline__ float rabitq_estimate(const uint8_t* __restrict__ rec
 // replaces the 128 ordered float adds with 4 * (QB + 1) popcounts at D = 128.
 constexpr int FAST_QB = 6;
 
+// planes: FAST_QB planes of `pw` words each (pw = nwords rounded up to 4, zero padded)
 __device__ __forceinline__ float rabitq_dd_fast(const uint8_t* __restrict__ rec, uint4 first,
-                                               const uint32_t* __restrict__ planes, int nwords, float lo, float delta) {
+                                               const uint32_t* __restrict__ planes, int pw, float lo, float delta) {
     int pc = 0;
     int acc[FAST_QB];
 #pragma unroll
     for (int b = 0; b < FAST_QB; ++b) acc[b] = 0;
-    for (int w0 = 0; w0 < nwords; w0 += 4) {
-        const uint4 c4 = w0 == 0 ? first : __ldg(reinterpret_cast<const uint4*>(rec + 4 * w0));
-        const uint32_t c[4] = {c4.x, c4.y, c4.z, c4.w};
+    for (int w0 = 0; w0 < pw; w0 += 4) {
+        const uint4 c = w0 == 0 ? first : __ldg(reinterpret_cast<const uint4*>(rec + 4 * w0));
+        pc += __popc(c.x) + __popc(c.y) + __popc(c.z) + __popc(c.w);
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            if (w0 + k < nwords) {
-                pc += __popc(c[k]);
-#pragma unroll
-                for (int b = 0; b < FAST_QB; ++b) acc[b] += __popc(c[k] & planes[b * nwords + w0 + k]);
-            }
+        for (int b = 0; b < FAST_QB; ++b) {
+            const uint4 p = *reinterpret_cast<const uint4*>(planes + b * pw + w0);
+            acc[b] += __popc(c.x & p.x) + __popc(c.y & p.y) + __popc(c.z & p.z) + __popc(c.w & p.w);
         }
     }
     int s = 0;
@@ -202,15 +200,15 @@ __device__ __forceinline__ void build_planes(const float* qv, int D, uint32_t* p
     lo = mn;
     const float levels = (float)((1 << FAST_QB) - 1);
     delta = (mx > mn) ? (mx - mn) / levels : 1.0f;
-    const int nwords = (D + 31) / 32;
-    for (int w = 0; w < nwords; ++w) {
+    const int pw = (((D + 31) / 32) + 3) & ~3;
+    for (int w = 0; w < pw; ++w) {
         const int e = w * 32 + lane;
         uint32_t qq = 0;
         if (e < D) qq = (uint32_t)min((int)levels, max(0, __float2int_rn((qv[e] - lo) / delta)));
 #pragma unroll
         for (int b = 0; b < FAST_QB; ++b) {
             const uint32_t bits = __ballot_sync(0xFFFFFFFFu, (qq >> b) & 1u);
-            if (lane == 0) planes[b * nwords + w] = bits;
+            if (lane == 0) planes[b * pw + w] = bits;
         }
     }
     __syncwarp();
@@ -295,14 +293,14 @@ beam_search_kernel(const jb_search_args a, const SearchLayout lay, int* __restri
     int32_t* cid = reinterpret_cast<int32_t*>(base + lay.cid_off);
     float* stage = reinterpret_cast<float*>(base + lay.stage_off);
     uint32_t* planes = reinterpret_cast<uint32_t*>(base + lay.plane_off);
-    const int nwords = (a.dims + 31) / 32;
+    const int nwords = (((a.dims + 31) / 32) + 3) & ~3;  // plane stride (16 B aligned)
 
     const int L = a.beam_width;
     const int D = a.dims;
     const int R = a.degree_cap;
     const int H = 4 << lay.hbits;
     const int RB = a.record_bytes;
-    const int meta_off = ((((D * BITS) + 7) / 8 + 7) / 8) * 8;
+    const int meta_off = ((((D * BITS) + 7) / 8 + 15) / 16) * 16;  // code zero-padded to 16 B
     const unsigned FULL = 0xFFFFFFFFu;
 
     for (;;) {
@@ -555,7 +553,7 @@ static SearchLayout make_layout(int src, int D, int L, int hash_slots) {
     s.stage_off = off;
     if (src == JB_SRC_EXACT) off += 32 * s.sstride * 4;
     s.plane_off = off;
-    if (src == JB_SRC_RABITQ_FAST) off += FAST_QB * ((D + 31) / 32) * 4;
+    if (src == JB_SRC_RABITQ_FAST) off += FAST_QB * ((((D + 31) / 32) + 3) & ~3) * 4;
     s.bytes = align16(off);
     return s;
 }

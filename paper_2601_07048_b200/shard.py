@@ -72,10 +72,12 @@ def sharded_knn(local_search, queries, k: int, shard_start: int, group=None, roo
     ids, ds = local_search(queries)
     ids = ids.to(device=dev, dtype=torch.int32).contiguous()
     ds = ds.to(device=dev, dtype=torch.float64).contiguous()
-    all_ids = torch.empty((world, nq, k), dtype=torch.int32, device=dev)
-    all_d = torch.empty((world, nq, k), dtype=torch.float64, device=dev)
+    # output as (world*nq, k): the layout every backend (NCCL, gloo) accepts
+    all_ids = torch.empty((world * nq, k), dtype=torch.int32, device=dev)
+    all_d = torch.empty((world * nq, k), dtype=torch.float64, device=dev)
     dist.all_gather_into_tensor(all_ids, ids, group=group)
     dist.all_gather_into_tensor(all_d, ds, group=group)
+    all_ids, all_d = all_ids.view(world, nq, k), all_d.view(world, nq, k)
     offs = torch.tensor([shard_start], dtype=torch.int64, device=dev)
     all_offs = torch.empty(world, dtype=torch.int64, device=dev)
     dist.all_gather_into_tensor(all_offs, offs, group=group)
