@@ -19,6 +19,8 @@
 // survivors each round extracts the same sequence, and the alpha filter is
 // element-wise, so the kept list is identical.
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <vector>
 #include <cub/cub.cuh>
 #include "common.cuh"
@@ -664,6 +666,39 @@ static int repair(const jb_insert_args& a, int64_t n_active, int64_t entry, cuda
     return JB_OK;
 }
 
+// JB_PROFILE=1: per-batch phase timings on stderr (stream events; diagnostics only)
+struct PhaseTimer {
+    bool on = false;
+    cudaStream_t st = nullptr;
+    std::vector<std::pair<const char*, cudaEvent_t>> ev;
+    explicit PhaseTimer(cudaStream_t s) : st(s) {
+        const char* e = getenv("JB_PROFILE");
+        on = e && e[0] == '1';
+        mark("start");
+    }
+    void mark(const char* name) {
+        if (!on) return;
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        cudaEventRecord(e, st);
+        ev.emplace_back(name, e);
+    }
+    void report(int64_t start, int64_t stop) {
+        if (!on) return;
+        mark("end");
+        cudaEventSynchronize(ev.back().second);
+        fprintf(stderr, "[jb] batch [%lld, %lld):", (long long)start, (long long)stop);
+        for (size_t i = 1; i < ev.size(); ++i) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, ev[i - 1].second, ev[i].second);
+            fprintf(stderr, " %s %.2fms", ev[i].first, ms);
+        }
+        fprintf(stderr, "\n");
+        for (auto& p : ev) cudaEventDestroy(p.second);
+        ev.clear();
+    }
+};
+
 static int validate_insert(const jb_insert_args& a) {
     JB_CHECK_ARG(a.adjacency && a.degrees && a.data && a.data_norms, "batch insert: missing arrays");
     JB_CHECK_ARG(a.degree_cap >= 1 && a.dims >= 1, "batch insert: bad shape");
@@ -710,6 +745,7 @@ int jb_batch_insert(const jb_insert_args* args, void* stream) {
     const size_t srow_bytes = (size_t)BW * ((D + 3) & ~3) * 4;
     Bufs bufs;
     cudaError_t _ce;
+    PhaseTimer pt(st);
 
     if (a.start == 0) {  // seed batch: medoid entry + mutual pruning (build.py:246-266)
         rc = jb_medoid(a.data, a.stop, D, &entry, stream);
@@ -763,6 +799,7 @@ int jb_batch_insert(const jb_insert_args* args, void* stream) {
         cap = hmax;  // re-run with an exact-size trace buffer (rare)
     }
 
+    pt.mark("search");
     // ---- phase 2: activate, prune each new vertex, emit reverse triples ----
     const int W = a.reverse_all_visited ? cap : R;
     const int64_t ntri = nb * (int64_t)W;
@@ -777,6 +814,7 @@ int jb_batch_insert(const jb_insert_args* args, void* stream) {
         a.adjacency, a.degrees, tt, tk, W);
     JB_LAUNCH_CHECK();
 
+    pt.mark("prune");
     // ---- phase 3: (target, dist, source) order via two stable radix sorts ----
     BALLOC(tt2, uint32_t, ntri);
     BALLOC(tk2, uint64_t, ntri);
@@ -823,8 +861,12 @@ int jb_batch_insert(const jb_insert_args* args, void* stream) {
         if (herr) { set_error("phase 3: candidate pool overflow"); return JB_EOVERFLOW; }
     }
 
+    pt.mark("merge");
     // ---- connectivity repair over the activated graph ----
     rc = repair(a, a.stop, entry, st, &bridges);
+    pt.mark("repair");
+    pt.report(a.start, a.stop);
+    if (pt.on) fprintf(stderr, "[jb]   bridges %lld\n", (long long)bridges);
     if (a.entry_point_out_host) *a.entry_point_out_host = entry;
     if (a.bridges_out_host) *a.bridges_out_host = bridges;
     return rc;
