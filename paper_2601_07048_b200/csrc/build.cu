@@ -88,6 +88,79 @@ __device__ int warp_prune(uint64_t* cand, int n, double alpha2, int R, const flo
     return kept;
 }
 
+// Stage the rows of n candidate ids (low 32 bits of `keys`) into smem rows
+// [n][rstride] with coalesced cp.async (one warp instruction per 512 B row at
+// D=128), plus their norms.
+__device__ __forceinline__ void stage_rows(float* rows, int rstride, float* cn, const uint64_t* keys, int n,
+                                           const float* __restrict__ data, const float* __restrict__ norms, int D) {
+    const int lane = lane_id();
+    if ((D & 3) == 0) {
+        const int nv = D >> 2;
+        for (int j = 0; j < n; ++j) {
+            const float* src = data + (size_t)(uint32_t)(keys[j] & 0xFFFFFFFFull) * D;
+            for (int f = lane; f < nv; f += 32) cp_async16(rows + (size_t)j * rstride + 4 * f, src + 4 * f);
+        }
+    } else {
+        for (int j = 0; j < n; ++j) {
+            const float* src = data + (size_t)(uint32_t)(keys[j] & 0xFFFFFFFFull) * D;
+            for (int f = lane; f < D; f += 32) cp_async4(rows + (size_t)j * rstride + f, src + f);
+        }
+    }
+    for (int j = lane; j < n; j += 32) cn[j] = __ldg(norms + (uint32_t)(keys[j] & 0xFFFFFFFFull));
+    cp_async_wait_all();
+    __syncwarp();
+}
+
+__device__ __forceinline__ float a1_rows(const float* a, const float* b, int D) {
+    Acc4 acc; acc.zero();
+    if ((D & 3) == 0) a1_range<true, false>(acc, a, b, 0, D);
+    else a1_range<false, false>(acc, a, b, 0, D);
+    return acc.reduce();
+}
+
+// Robust prune with every candidate row already in smem (rows[i] <-> cand[i]):
+// same extraction sequence as warp_prune, no global traffic in the rounds.
+__device__ int warp_prune_staged(uint64_t* cand, int n, double alpha2, int R, const float* rows, int rstride,
+                                 const float* cn, int D, int32_t* out_ids, float* out_d) {
+    const int lane = lane_id();
+    int kept = 0;
+    while (kept < R) {
+        uint64_t m = UMAX;
+        int mi = -1;
+        for (int i = lane; i < n; i += 32) {
+            const uint64_t c = cand[i];
+            if (c < m) { m = c; mi = i; }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const uint64_t om = shfl_xor_u64(m, o);
+            const int oi = __shfl_xor_sync(0xFFFFFFFFu, mi, o);
+            if (om < m) { m = om; mi = oi; }
+        }
+        if (m == UMAX) break;
+        if (lane == 0) {
+            out_ids[kept] = (int32_t)(m & 0xFFFFFFFFull);
+            out_d[kept] = __uint_as_float((uint32_t)(m >> 32));
+            cand[mi] = UMAX;
+        }
+        ++kept;
+        __syncwarp();
+        if (kept >= R) break;
+        const float* srow = rows + (size_t)mi * rstride;
+        const float sn = cn[mi];
+        for (int i = lane; i < n; i += 32) {
+            const uint64_t c = cand[i];
+            if (c == UMAX) continue;
+            const float dsp = exact_from_dot(cn[i], a1_rows(rows + (size_t)i * rstride, srow, D), sn);
+            const double dp = (double)__uint_as_float((uint32_t)(c >> 32));
+            if (!(__dmul_rn(alpha2, (double)dsp) > dp)) cand[i] = UMAX;
+        }
+        __syncwarp();
+    }
+    __syncwarp();
+    return kept;
+}
+
 __device__ __forceinline__ void write_row(int32_t* __restrict__ adj, int32_t* __restrict__ deg, int R, uint32_t v,
                                           const int32_t* ids, int n) {
     const int lane = lane_id();
@@ -130,10 +203,14 @@ phase2_kernel(const float* __restrict__ data, const float* __restrict__ norms, i
               double alpha2, int R, const int32_t* __restrict__ hops, const int32_t* __restrict__ tids,
               const float* __restrict__ tdst, int cap, int reverse_all, uint64_t* __restrict__ cand_all,
               int32_t* __restrict__ kept_ids, float* __restrict__ kept_d, int32_t* __restrict__ adj,
-              int32_t* __restrict__ deg, uint32_t* __restrict__ tri_target, uint64_t* __restrict__ tri_key, int W) {
+              int32_t* __restrict__ deg, uint32_t* __restrict__ tri_target, uint64_t* __restrict__ tri_key, int W,
+              int crows, int rstride) {
     extern __shared__ __align__(16) float sh[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    float* srow = sh + warp * ((D + 3) & ~3);
+    const int per_warp = ((D + 3) & ~3) + crows * rstride + ((crows + 3) & ~3);
+    float* srow = sh + (size_t)warp * per_warp;
+    float* rows = srow + ((D + 3) & ~3);
+    float* cn = rows + (size_t)crows * rstride;
     const int64_t xi = (int64_t)blockIdx.x * BW + warp;
     if (xi >= nb) return;
     const uint32_t x = (uint32_t)(start + xi);
@@ -145,7 +222,13 @@ phase2_kernel(const float* __restrict__ data, const float* __restrict__ norms, i
     __syncwarp();
     int32_t* ki = kept_ids + xi * R;
     float* kd = kept_d + xi * R;
-    const int k = warp_prune(cand, h, alpha2, R, data, norms, D, srow, ki, kd);
+    int k;
+    if (h <= crows) {
+        stage_rows(rows, rstride, cn, cand, h, data, norms, D);
+        k = warp_prune_staged(cand, h, alpha2, R, rows, rstride, cn, D, ki, kd);
+    } else {
+        k = warp_prune(cand, h, alpha2, R, data, norms, D, srow, ki, kd);
+    }
     write_row(adj, deg, R, x, ki, k);
     // reverse triples (target, source=x, dist): kept edges, or the whole trace
     uint32_t* tt = tri_target + xi * W;
@@ -194,8 +277,8 @@ __global__ void seg_head_kernel(const uint32_t* __restrict__ t, int64_t n, uint8
 }
 
 constexpr int OWNER_SC = 256;  // smem candidate slots per owner warp
-__host__ __device__ inline int owner_per_warp(int R, int D) {
-    return ((OWNER_SC * 8 + R * 4 * 3 + ((D + 3) & ~3) * 4) + 15) & ~15;
+__host__ __device__ inline int owner_per_warp(int R, int D, int crows, int rstride) {
+    return ((OWNER_SC * 8 + R * 4 * 3 + ((D + 3) & ~3) * 4 + crows * rstride * 4 + ((crows + 3) & ~3) * 4) + 15) & ~15;
 }
 
 __global__ void __launch_bounds__(BW * 32)
@@ -203,17 +286,20 @@ owner_merge_kernel(const float* __restrict__ data, const float* __restrict__ nor
                    int always_prune, const uint32_t* __restrict__ tgt, const uint64_t* __restrict__ key, int64_t total,
                    const int32_t* __restrict__ seg_start, const int* __restrict__ n_seg, uint64_t* __restrict__ pool,
                    unsigned long long* __restrict__ pool_top, int pool_cap, int32_t* __restrict__ adj,
-                   int32_t* __restrict__ deg, int* __restrict__ err) {
+                   int32_t* __restrict__ deg, int* __restrict__ err, int crows, int rstride) {
     extern __shared__ __align__(16) unsigned char shb[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     constexpr int SC = OWNER_SC;
-    const int per_warp = owner_per_warp(R, D);
+    const int per_warp = owner_per_warp(R, D, crows, rstride);
     unsigned char* base = shb + (size_t)warp * per_warp;
+    // per-warp layout, 16 B aligned pieces first: keys | star row | staged rows | norms | small arrays
     uint64_t* scand = reinterpret_cast<uint64_t*>(base);
-    int32_t* have = reinterpret_cast<int32_t*>(base + SC * 8);
+    float* srow = reinterpret_cast<float*>(base + SC * 8);
+    float* rows = srow + ((D + 3) & ~3);
+    float* cn = rows + (size_t)crows * rstride;
+    int32_t* have = reinterpret_cast<int32_t*>(cn + ((crows + 3) & ~3));
     int32_t* kid = have + R;
     float* kd = reinterpret_cast<float*>(kid + R);
-    float* srow = kd + R;
     const int64_t s = (int64_t)blockIdx.x * BW + warp;
     if (s >= *n_seg) return;
     const int64_t g0 = seg_start[s];
@@ -267,18 +353,31 @@ owner_merge_kernel(const float* __restrict__ data, const float* __restrict__ nor
         if (lane == 0) deg[t] = hd + nf;
         return;
     }
-    // existing neighbours get recomputed distances d(t, e) (target is the pivot)
+    // existing neighbours get recomputed distances d(t, e) (target is the pivot);
+    // fresh entries already hold (stored triple dist << 32 | source) keys
     const float* tr = data + (size_t)t * D;
     for (int e = lane; e < D; e += 32) srow[e] = tr[e];
     const float tn = norms[t];
-    __syncwarp();
-    for (int j = lane; j < hd; j += 32) {
-        const uint32_t e = (uint32_t)have[j];
-        cand[j] = pack_key(pair_dist(data, norms, D, srow, tn, e), e);
+    const int n = hd + nf;
+    int k;
+    if (n <= crows) {
+        for (int j = lane; j < hd; j += 32) cand[j] = (uint64_t)(uint32_t)have[j];  // id only, for staging
+        __syncwarp();
+        stage_rows(rows, rstride, cn, cand, n, data, norms, D);
+        for (int j = lane; j < hd; j += 32)
+            cand[j] = pack_key(exact_from_dot(cn[j], a1_rows(rows + (size_t)j * rstride, srow, D), tn),
+                               (uint32_t)have[j]);
+        __syncwarp();
+        k = warp_prune_staged(cand, n, alpha2, R, rows, rstride, cn, D, kid, kd);
+    } else {
+        __syncwarp();
+        for (int j = lane; j < hd; j += 32) {
+            const uint32_t e = (uint32_t)have[j];
+            cand[j] = pack_key(pair_dist(data, norms, D, srow, tn, e), e);
+        }
+        __syncwarp();
+        k = warp_prune(cand, n, alpha2, R, data, norms, D, srow, kid, kd);
     }
-    // fresh entries already hold (stored triple dist << 32 | source) keys
-    __syncwarp();
-    const int k = warp_prune(cand, hd + nf, alpha2, R, data, norms, D, srow, kid, kd);
     write_row(adj, deg, R, t, kid, k);
 }
 
@@ -808,10 +907,15 @@ int jb_batch_insert(const jb_insert_args* args, void* stream) {
     BALLOC(kd, float, (size_t)nb * R);
     BALLOC(tt, uint32_t, ntri);
     BALLOC(tk, uint64_t, ntri);
-    JB_CUDA(cudaFuncSetAttribute(phase2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)srow_bytes));
-    phase2_kernel<<<(unsigned)((nb + BW - 1) / BW), BW * 32, srow_bytes, st>>>(
+    // smem-staged candidate rows: up to ~52 KB per warp (4 warps per block)
+    const int rstride = ((D + 3) & ~3) + 4;
+    int crows2 = std::min(cap, (52 * 1024 - ((D + 3) & ~3) * 4) / (rstride * 4 + 4));
+    if (crows2 < R + 1) crows2 = 0;
+    const size_t p2_smem = (size_t)BW * 4 * (((D + 3) & ~3) + crows2 * rstride + ((crows2 + 3) & ~3));
+    JB_CUDA(cudaFuncSetAttribute(phase2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p2_smem));
+    phase2_kernel<<<(unsigned)((nb + BW - 1) / BW), BW * 32, p2_smem, st>>>(
         a.data, a.data_norms, D, a.start, nb, alpha2, R, hops, tids, tdst, cap, a.reverse_all_visited, cand, kid, kd,
-        a.adjacency, a.degrees, tt, tk, W);
+        a.adjacency, a.degrees, tt, tk, W, crows2, rstride);
     JB_LAUNCH_CHECK();
 
     pt.mark("prune");
@@ -849,11 +953,14 @@ int jb_batch_insert(const jb_insert_args* args, void* stream) {
         BALLOC(err, int, 1);
         JB_CUDA(cudaMemsetAsync(ptop, 0, sizeof(unsigned long long), st));
         JB_CUDA(cudaMemsetAsync(err, 0, sizeof(int), st));
-        const int osm = owner_per_warp(R, D) * BW;
+        // owners stage up to R + 16 candidate rows in smem when they fit in ~26 KB
+        int crows = std::min(R + 16, (26 * 1024) / (rstride * 4 + 4));
+        if (crows < R + 1) crows = 0;
+        const int osm = owner_per_warp(R, D, crows, rstride) * BW;
         JB_CUDA(cudaFuncSetAttribute(owner_merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, osm));
         owner_merge_kernel<<<(unsigned)((hseg + BW - 1) / BW), BW * 32, osm, st>>>(
             a.data, a.data_norms, D, alpha2, R, a.always_prune, tt, tk, ntri, seg, nseg, pool, ptop, pool_cap,
-            a.adjacency, a.degrees, err);
+            a.adjacency, a.degrees, err, crows, rstride);
         JB_LAUNCH_CHECK();
         int herr = 0;
         JB_CUDA(cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, st));
