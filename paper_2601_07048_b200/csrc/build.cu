@@ -907,9 +907,10 @@ int jb_batch_insert(const jb_insert_args* args, void* stream) {
     BALLOC(kd, float, (size_t)nb * R);
     BALLOC(tt, uint32_t, ntri);
     BALLOC(tk, uint64_t, ntri);
-    // smem-staged candidate rows: up to ~52 KB per warp (4 warps per block)
+    // smem-staged candidate rows when a trace fits in ~26 KB per warp; longer traces
+    // prune from L1/L2 (staging them would cost more occupancy than it saves)
     const int rstride = ((D + 3) & ~3) + 4;
-    int crows2 = std::min(cap, (52 * 1024 - ((D + 3) & ~3) * 4) / (rstride * 4 + 4));
+    int crows2 = std::min(cap, (26 * 1024 - ((D + 3) & ~3) * 4) / (rstride * 4 + 4));
     if (crows2 < R + 1) crows2 = 0;
     const size_t p2_smem = (size_t)BW * 4 * (((D + 3) & ~3) + crows2 * rstride + ((crows2 + 3) & ~3));
     JB_CUDA(cudaFuncSetAttribute(phase2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p2_smem));

@@ -610,7 +610,7 @@ int jb_beam_search(const jb_search_args* args, void* stream) {
     // Small tables win: evictions only cost re-evaluations (results stay exact),
     // while smem per warp sets occupancy (measured at L=128: 1024 slots 19% faster
     // than 2048, 512 equal to 1024).
-    if (hs <= 0) hs = std::min(2048, std::max(512, pow2_ceil(8 * a.beam_width)));
+    if (hs <= 0) hs = std::min(2048, std::max(1024, pow2_ceil(8 * a.beam_width)));
     hs = std::max(32, pow2_ceil(hs));
     cudaStream_t st = as_stream(stream);
     if (a.source == JB_SRC_EXACT) {
