@@ -1,0 +1,188 @@
+"""Secondary measurements for the other BASELINE.json configs (DESIGN.md numbers).
+bench.py stays the single headline harness (configs[1]); this script runs:
+
+  c1  synthetic 100K x 128 Gaussian, R=32 L_build=64 alpha=1.2, 10K queries, k=10, EXACT
+      distances, L sweep 16..256 (the reference's own CPU-runnable config): device QPS,
+      recall, ids checked identical to the oracle on a sample, oracle CPU QPS
+  c3  GIST-shaped 1M x 960 low-rank (d_int=32), RaBitQ m=4 + fp32 rerank: QPS at recall 0.95
+  c4  DEEP-shaped 96-d low-rank: bulk build of the first N0, then insert_stream in batches of
+      100K interleaved with a 10K-query exact search after every batch (inserts/s, QPS)
+
+    python bench_configs.py c1|c3|c4 [--n N] [--total T]
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import bench  # noqa: E402
+
+
+def _timed(fn, reps=5, warm=2):
+    import torch
+
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    evs = []
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        fn()
+        b.record()
+        evs.append((a, b))
+    torch.cuda.synchronize()
+    return float(np.mean([a.elapsed_time(b) for a, b in evs]))
+
+
+def c1(args):
+    import torch
+
+    import paper_2601_07048_b200 as jb
+    from oracle import search as osearch
+
+    x = jb.gen_synthetic(args.n or 100_000, 128, seed=0).data
+    q = jb.gen_synthetic(10_000, 128, seed=1).data
+    ds = jb.VectorDataset(x)
+    t0 = time.perf_counter()
+    g = jb.build(ds, jb.BuildParams(degree_cap=32, build_beam_width=64, alpha=1.2))
+    torch.cuda.synchronize()
+    t_build = time.perf_counter() - t0
+    q_dev = torch.from_numpy(q).cuda()
+    gi, gd = bench._gt_device(ds.device().x, q_dev, 100)
+    gt = jb.GroundTruth(gi.cpu().numpy(), gd.cpu().numpy().astype(np.float32))
+    out = {"config": "c1", "n": len(x), "build_s": round(t_build, 3), "inserts_per_s": round(len(x) / t_build, 1),
+           "sweep": []}
+    for L in (16, 32, 64, 128, 256):
+        sp = jb.SearchParams(beam_width=L, k=10)
+        ms = _timed(lambda: jb.search_knn_batch_device(g, ds, q_dev, sp))
+        ids, _ = jb.search_knn_batch_device(g, ds, q_dev, sp)
+        r = jb.recall_at_k(ids.cpu().numpy(), gt, 10)
+        out["sweep"].append({"L": L, "recall": round(r, 4), "qps_device": round(10_000 / (ms / 1e3), 1),
+                             "ms": round(ms, 3)})
+    # parity on the GPU-built graph + CPU oracle speed at L=64 (1 process)
+    ns = 1000
+    t0 = time.perf_counter()
+    ores = osearch.beam_search(np.ascontiguousarray(g.adjacency), g.active_count, g.entry_point,
+                               osearch.ExactSource(x, q[:ns]), ns, 64)
+    el = time.perf_counter() - t0
+    res = jb.run_beam_searches(g, ds, q[:ns], 64)
+    same = all(np.array_equal(a.frontier_ids, b.frontier_ids) and np.array_equal(a.visited_ids, b.visited_ids)
+               for a, b in zip(res, ores))
+    out["oracle_cpu_qps_L64_1proc"] = round(ns / el, 1)
+    out["frontier_and_trace_identical_to_oracle"] = same
+    return out
+
+
+def c3(args):
+    import torch
+
+    import paper_2601_07048_b200 as jb
+
+    n = args.n or 1_000_000
+    x = jb.gen_lowrank(n, 960, seed=1, d_int=32, noise=0.05, basis_seed=0)
+    q = jb.gen_lowrank(10_000, 960, seed=1_000_003, d_int=32, noise=0.05, basis_seed=0)
+    ds = jb.VectorDataset(x)
+    t0 = time.perf_counter()
+    g = jb.build(ds, jb.BuildParams(degree_cap=32, build_beam_width=64, alpha=1.2))
+    torch.cuda.synchronize()
+    t_build = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    idx = jb.rabitq_fit(ds, bits=4, seed=1)
+    torch.cuda.synchronize()
+    t_fit = time.perf_counter() - t0
+    q_dev = torch.from_numpy(q).cuda()
+    gi, gd = bench._gt_device(ds.device().x, q_dev, 100)
+    gt = jb.GroundTruth(gi.cpu().numpy(), gd.cpu().numpy().astype(np.float32))
+    out = {"config": "c3", "n": n, "dims": 960, "bits": 4, "build_s": round(t_build, 2),
+           "inserts_per_s": round(n / t_build, 1), "rabitq_fit_s": round(t_fit, 3),
+           "bytes_per_vector": {"f32": 3840, "rabitq_record": int(jb._lib.lib().jb_rabitq_record_bytes(960, 4))},
+           "sweep": []}
+    for L in bench.SWEEP:
+        sp = jb.SearchParams(beam_width=L, k=10, rerank=True)
+        ms = _timed(lambda: jb.search_knn_batch_device(g, idx, q_dev, sp, exact_data=ds), reps=3, warm=1)
+        ids, _ = jb.search_knn_batch_device(g, idx, q_dev, sp, exact_data=ds)
+        r = jb.recall_at_k(ids.cpu().numpy(), gt, 10)
+        out["sweep"].append({"L": L, "recall": round(r, 4), "qps_device": round(10_000 / (ms / 1e3), 1)})
+        if r >= 0.95:
+            break
+    return out
+
+
+def c4(args):
+    import torch
+
+    import paper_2601_07048_b200 as jb
+
+    total = args.total or 10_000_000
+    n0 = args.n or 1_000_000
+    x = jb.gen_lowrank(total, 96, seed=1, d_int=16, noise=0.05, basis_seed=0)
+    q = jb.gen_lowrank(10_000, 96, seed=1_000_003, d_int=16, noise=0.05, basis_seed=0)
+    ds = jb.VectorDataset(x)
+    ds.device()
+    params = jb.BuildParams(degree_cap=32, build_beam_width=64, alpha=1.2, max_batch=100_000)
+    g = jb.GraphIndex(capacity=total, degree_cap=32)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    # bulk phase on the first n0 rows: same schedule as build() over a prefix
+    size, pos = params.degree_cap + 1, 0
+    while pos < n0:
+        stop = min(n0, pos + size)
+        jb.batch_insert(g, ds, range(pos, stop), params)
+        pos, size = stop, min(size * 2, params.max_batch)
+    torch.cuda.synchronize()
+    t_bulk = time.perf_counter() - t0
+    q_dev = torch.from_numpy(q).cuda()
+    sp = jb.SearchParams(beam_width=64, k=10)
+    ins_t, qps = [], []
+    pos = n0
+    while pos < total:
+        stop = min(total, pos + params.max_batch)
+        t0 = time.perf_counter()
+        jb.insert_stream(g, ds, range(pos, stop), params)
+        torch.cuda.synchronize()
+        ins_t.append((stop - pos, time.perf_counter() - t0))
+        ms = _timed(lambda: jb.search_knn_batch_device(g, ds, q_dev, sp), reps=1, warm=0)
+        qps.append(10_000 / (ms / 1e3))
+        pos = stop
+    ids, _ = jb.search_knn_batch_device(g, ds, q_dev, sp)
+    gi, gd = bench._gt_device(ds.device().x, q_dev, 100)
+    gt = jb.GroundTruth(gi.cpu().numpy(), gd.cpu().numpy().astype(np.float32))
+    return {"config": "c4", "total": total, "bulk_n": n0, "bulk_inserts_per_s": round(n0 / t_bulk, 1),
+            "stream_batches": len(ins_t),
+            "stream_inserts_per_s": round(sum(n for n, _ in ins_t) / sum(t for _, t in ins_t), 1),
+            "stream_inserts_per_s_first_last": [round(ins_t[0][0] / ins_t[0][1], 1),
+                                                round(ins_t[-1][0] / ins_t[-1][1], 1)] if ins_t else None,
+            "search_qps_L64_exact_first_last": [round(qps[0], 1), round(qps[-1], 1)] if qps else None,
+            "final_recall_at_10_L64": round(jb.recall_at_k(ids.cpu().numpy(), gt, 10), 4)}
+
+
+def main():
+    p = argparse.ArgumentParser()
+    p.add_argument("config", choices=["c1", "c3", "c4"])
+    p.add_argument("--n", type=int, default=0)
+    p.add_argument("--total", type=int, default=0)
+    p.add_argument("--out", default="")
+    args = p.parse_args()
+    import torch
+
+    torch.cuda.set_device(0)
+    res = {"c1": c1, "c3": c3, "c4": c4}[args.config](args)
+    line = json.dumps(res)
+    print(line, flush=True)
+    if args.out:
+        with open(args.out, "w") as fh:
+            fh.write(line + "\n")
+
+
+if __name__ == "__main__":
+    main()

@@ -14,6 +14,9 @@ not part of the B200 hot path (no config uses them); they raise.
 
 from __future__ import annotations
 
+import os
+import sys
+import time
 import warnings
 from dataclasses import dataclass
 
@@ -167,16 +170,23 @@ def build(dataset, params: BuildParams, quantizer=None) -> GraphIndex:
     _check_supported(params, quantizer)
     if params.two_pass:
         raise NotImplementedError("two_pass refinement is not on the B200 path")
+    prof = os.environ.get("JB_PROFILE") == "1"
+    t0 = time.perf_counter()
     graph = GraphIndex(capacity=ds.count, degree_cap=params.degree_cap)
     global_medoid = medoid(ds)
+    if prof:
+        print(f"[jb] medoid {1e3 * (time.perf_counter() - t0):.2f}ms", file=sys.stderr)
     size = params.degree_cap + 1
     pos = 0
     while pos < ds.count:
         stop = min(ds.count, pos + size)
+        t1 = time.perf_counter()
         batch_insert(graph, ds, range(pos, stop), params)
         if global_medoid < graph.active_count and graph.entry_point != global_medoid:
             graph.entry_point = global_medoid
             _repair(graph, ds, params)
+        if prof:
+            print(f"[jb] batch wall [{pos}, {stop}) {1e3 * (time.perf_counter() - t1):.2f}ms", file=sys.stderr)
         pos = stop
         size = min(size * 2, params.max_batch)
     return graph
