@@ -146,8 +146,16 @@ def _dist():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # one process per GPU over NCCL; BENCH_DIST_BACKEND=gloo runs the same multi-rank
+        # logic with host-staged collectives (used to test N>1 on a single-GPU box)
+        backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
+        dev = local % torch.cuda.device_count()
+        torch.cuda.set_device(dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group(backend)
+        local = dev
     else:
         torch.cuda.set_device(0)
     return world, rank, local
@@ -209,11 +217,9 @@ def _setup(args, world, rank):
     if world > 1:
         import torch.distributed as dist
 
-        all_i = torch.empty((world * gt_i.shape[0], gt_i.shape[1]), dtype=gt_i.dtype, device=gt_i.device)
-        all_d = torch.empty((world * gt_d.shape[0], gt_d.shape[1]), dtype=gt_d.dtype, device=gt_d.device)
-        dist.all_gather_into_tensor(all_i, gt_i.contiguous())
-        dist.all_gather_into_tensor(all_d, gt_d.contiguous())
-        all_i, all_d = all_i.view(world, *gt_i.shape), all_d.view(world, *gt_d.shape)
+        from paper_2601_07048_b200 import comm
+
+        all_i, all_d = comm.all_gather(gt_i), comm.all_gather(gt_d)
         ci = all_i.permute(1, 0, 2).reshape(args.nq, -1)
         cd = all_d.permute(1, 0, 2).reshape(args.nq, -1)
         o = torch.argsort(ci, dim=1)
@@ -316,12 +322,10 @@ def _timed_steps(S, args, world, L, clocks_idx, est="reference"):
         if world > 1:
             from paper_2601_07048_b200 import shard
 
-            all_i = torch.empty((world * nq, k), dtype=torch.int32, device="cuda")
-            all_d = torch.empty((world * nq, k), dtype=torch.float64, device="cuda")
-            dist.all_gather_into_tensor(all_i, out_i)
-            dist.all_gather_into_tensor(all_d, out_d)
-            shard.merge_topk_device(all_i.view(world, nq, k), all_d.view(world, nq, k),
-                                    [r * args.n for r in range(world)], k)  # merge kernel
+            from paper_2601_07048_b200 import comm
+
+            shard.merge_topk_device(comm.all_gather(out_i), comm.all_gather(out_d),
+                                    [r * args.n for r in range(world)], k)  # NCCL all-gather + merge kernel
         ev[3].record()
 
     for i in range(args.warmup):
@@ -348,9 +352,10 @@ def _timed_steps(S, args, world, L, clocks_idx, est="reference"):
     rerank_ms = [evs[i][2].elapsed_time(evs[i][3]) for i in range(args.steps)]
     tot = float(sum(step_ms))
     if world > 1:
+        from paper_2601_07048_b200 import comm
+
         t = torch.tensor([tot], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        tot = float(t.item())
+        tot = float(comm.all_reduce_max(t).item())
     launches_per_step = 3 + (1 if world > 1 else 0)
     return dict(total_ms=tot, step_ms=step_ms, search_ms=search_ms, bind_ms=bind_ms, rerank_ms=rerank_ms,
                 wall_s=wall, clocks=clk.summary(), launches=launches_per_step * args.steps)
@@ -388,9 +393,10 @@ def _e2e(S, args, world, L, est="reference"):
             if rank == 0:
                 ids, ds = gi.cpu().numpy(), gd.cpu().numpy()
             torch.cuda.synchronize()
+            from paper_2601_07048_b200 import comm
+
             dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
-            dist.all_reduce(dt, op=dist.ReduceOp.MAX)
-            times.append(float(dt.item()))
+            times.append(float(comm.all_reduce_max(dt).item()))
         d2h = args.nq * args.k * (8 + 8)
     tt = times[args.warmup:]
     units = args.nq * world

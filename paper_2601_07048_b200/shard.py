@@ -58,30 +58,25 @@ def sharded_knn(local_search, queries, k: int, shard_start: int, group=None, roo
     import torch
     import torch.distributed as dist
 
-    world = dist.get_world_size(group)
+    from . import comm
+
     rank = dist.get_rank(group)
     dev = device if device is not None else (queries.device if queries is not None else torch.device("cpu"))
     shape = torch.zeros(2, dtype=torch.int64, device=dev)
     if rank == root:
         shape[0], shape[1] = queries.shape[0], queries.shape[1]
-    dist.broadcast(shape, src=root, group=group)
+    comm.broadcast(shape, src=root, group=group)
     nq, D = int(shape[0]), int(shape[1])
     if rank != root:
         queries = torch.empty((nq, D), dtype=torch.float32, device=dev)
-    dist.broadcast(queries, src=root, group=group)
+    comm.broadcast(queries, src=root, group=group)
     ids, ds = local_search(queries)
     ids = ids.to(device=dev, dtype=torch.int32).contiguous()
     ds = ds.to(device=dev, dtype=torch.float64).contiguous()
-    # output as (world*nq, k): the layout every backend (NCCL, gloo) accepts
-    all_ids = torch.empty((world * nq, k), dtype=torch.int32, device=dev)
-    all_d = torch.empty((world * nq, k), dtype=torch.float64, device=dev)
-    dist.all_gather_into_tensor(all_ids, ids, group=group)
-    dist.all_gather_into_tensor(all_d, ds, group=group)
-    all_ids, all_d = all_ids.view(world, nq, k), all_d.view(world, nq, k)
+    all_ids = comm.all_gather(ids, group=group)   # [world, nq, k]
+    all_d = comm.all_gather(ds, group=group)
     offs = torch.tensor([shard_start], dtype=torch.int64, device=dev)
-    all_offs = torch.empty(world, dtype=torch.int64, device=dev)
-    dist.all_gather_into_tensor(all_offs, offs, group=group)
-    offsets = all_offs.cpu().numpy()
+    offsets = comm.all_gather(offs, group=group).reshape(-1).cpu().numpy()
     if merge is None:
         merge = merge_topk_device
     return merge(all_ids, all_d, offsets, k)
