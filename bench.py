@@ -50,8 +50,8 @@ def _args():
     p.add_argument("--steps", type=int, default=10)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    p.add_argument("--n", type=int, default=1_000_000, help="vectors per shard")
-    p.add_argument("--nq", type=int, default=10_000)
+    p.add_argument("--shard-rows", dest="n", type=int, default=1_000_000, help="vectors per shard (GPU)")
+    p.add_argument("--queries", dest="nq", type=int, default=10_000)
     p.add_argument("--dim", type=int, default=128)
     p.add_argument("--k", type=int, default=10)
     p.add_argument("--bits", type=int, default=1)
