@@ -722,6 +722,8 @@ static int repair(const jb_insert_args& a, int64_t n_active, int64_t entry, cuda
         JB_CUDA(cudaMemcpyAsync(h, counts + 2, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
         JB_CUDA(cudaStreamSynchronize(st));
         const int nlost = h[0], nreach = h[1];
+        if (getenv("JB_PROFILE") && getenv("JB_PROFILE")[0] == '1')
+            fprintf(stderr, "[jb]   repair round %d: stranded %d reachable %d\n", round, nlost, nreach);
         if (nlost == 0) break;
         // donors
         const int sblocks = (nlost + DT - 1) / DT;
@@ -866,7 +868,8 @@ int jb_batch_insert(const jb_insert_args* args, void* stream) {
 
     // ---- phase 1: batched search of the new rows on the read-only graph ----
     const int L = a.build_beam_width;
-    int cap = std::max(2 * L, L + 64);
+    // trace capacity: generous (8 B per slot) so the exact-size re-run below stays rare
+    int cap = std::max(4 * L, L + 512);
     BALLOC(fk, uint64_t, (size_t)nb * L);
     BALLOC(hops, int32_t, nb);
     BALLOC(evals, int32_t, nb);
