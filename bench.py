@@ -313,7 +313,7 @@ def _timed_steps(S, args, world, L, clocks_idx, est="reference"):
 
     def one_step(ev):
         ev[0].record()
-        bound = jsearch._Bound(idx, q_dev, est)                # bind kernel
+        bound = jsearch._Bound(idx, q_dev, est)                # bind: rotate GEMM + finish kernels
         ev[1].record()
         fk, *_ = jsearch._launch(g, bound, L, None, 0)         # search kernel
         ev[2].record()
@@ -356,7 +356,7 @@ def _timed_steps(S, args, world, L, clocks_idx, est="reference"):
 
         t = torch.tensor([tot], dtype=torch.float64, device="cuda")
         tot = float(comm.all_reduce_max(t).item())
-    launches_per_step = 3 + (1 if world > 1 else 0)
+    launches_per_step = 4 + (1 if world > 1 else 0)  # rotate GEMM + bind finish + search + rerank (+ merge)
     return dict(total_ms=tot, step_ms=step_ms, search_ms=search_ms, bind_ms=bind_ms, rerank_ms=rerank_ms,
                 wall_s=wall, clocks=clk.summary(), launches=launches_per_step * args.steps)
 

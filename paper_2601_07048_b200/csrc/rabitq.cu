@@ -197,34 +197,77 @@ __device__ float pairwise_sum_f32(const float* a, int n) {
     return __fadd_rn(pairwise_sum_f32(a, n2), pairwise_sum_f32(a + n2, n - n2));
 }
 
-// One block (4 warps) per query.
-__global__ void __launch_bounds__(128)
-bind_kernel(const float* __restrict__ queries, int D, int bits, const float* __restrict__ centroid,
-            const double* __restrict__ rot, float* __restrict__ rotated, float* __restrict__ qadd,
-            float* __restrict__ qsumq) {
-    extern __shared__ __align__(16) float bsh[];
-    float* qc = bsh;          // [D]
-    float* rq = bsh + D;      // [D]
-    const int64_t qi = blockIdx.x;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (int d = threadIdx.x; d < D; d += blockDim.x) qc[d] = __fsub_rn(queries[qi * D + d], centroid[d]);
-    __syncthreads();
-    for (int i = warp; i < D; i += 4) {
-        const double* rr = rot + (size_t)i * D;
-        double s = 0.0;
-        for (int d = lane; d < D; d += 32) s = fma((double)qc[d], __ldg(rr + d), s);
-        for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xFFFFFFFFu, s, off);
-        if (lane == 0) {
-            const float f = __double2float_rn(s);
-            rq[i] = f;
-            rotated[qi * D + i] = f;
+// rotated = f32(f64(q - c) @ rot^T) as a tiled f64 GEMM: block = 64 queries x 64
+// outputs, 256 threads with 4x4 outputs each, 16-wide k-steps through smem.
+constexpr int RT = 64, RK = 16;
+
+__global__ void __launch_bounds__(256)
+rotate_gemm_kernel(const float* __restrict__ queries, int64_t nq, int D, const float* __restrict__ centroid,
+                   const double* __restrict__ rot, float* __restrict__ rotated) {
+    __shared__ double As[RT][RK + 1];
+    __shared__ double Bs[RT][RK + 1];
+    const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+    const int64_t q0 = (int64_t)blockIdx.x * RT;
+    const int o0 = blockIdx.y * RT;
+    double acc[4][4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+    for (int k0 = 0; k0 < D; k0 += RK) {
+        for (int i = tid; i < RT * RK; i += 256) {
+            const int r = i / RK, e = i % RK, d = k0 + e;
+            double va = 0.0, vb = 0.0;
+            if (d < D) {
+                if (q0 + r < nq) va = (double)__fsub_rn(queries[(q0 + r) * D + d], centroid[d]);
+                if (o0 + r < D) vb = rot[(size_t)(o0 + r) * D + d];
+            }
+            As[r][e] = va;
+            Bs[r][e] = vb;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int e = 0; e < RK; ++e) {
+            double av[4], bv[4];
+#pragma unroll
+            for (int a = 0; a < 4; ++a) av[a] = As[ty * 4 + a][e];
+#pragma unroll
+            for (int b = 0; b < 4; ++b) bv[b] = Bs[tx * 4 + b][e];
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+                for (int b = 0; b < 4; ++b) acc[a][b] = fma(av[a], bv[b], acc[a][b]);
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+        const int64_t q = q0 + ty * 4 + a;
+        if (q >= nq) continue;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            const int o = o0 + tx * 4 + b;
+            if (o < D) rotated[q * D + o] = __double2float_rn(acc[a][b]);
         }
     }
-    __syncthreads();
-    if (threadIdx.x == 0) {
+}
+
+// Per query (one warp): query_add = A1 dot(q - c, q - c), query_sumq =
+// f32(pairwise_sum_f32(rotated) * mid) — both sequential orders, done by lane 0.
+__global__ void bind_finish_kernel(const float* __restrict__ queries, int64_t nq, int D, int bits,
+                                   const float* __restrict__ centroid, const float* __restrict__ rotated,
+                                   float* __restrict__ qadd, float* __restrict__ qsumq) {
+    extern __shared__ __align__(16) float fsh[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t qi = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
+    if (qi >= nq) return;
+    float* qc = fsh + (size_t)warp * ((D + 3) & ~3);
+    for (int d = lane; d < D; d += 32) qc[d] = __fsub_rn(queries[qi * D + d], centroid[d]);
+    __syncwarp();
+    if (lane == 0) {
         qadd[qi] = a1_dot<false>(qc, qc, D);
         const float mid = (float)(((1 << bits) - 1) / 2.0);
-        qsumq[qi] = __fmul_rn(pairwise_sum_f32(rq, D), mid);
+        qsumq[qi] = __fmul_rn(pairwise_sum_f32(rotated + qi * D, D), mid);
     }
 }
 
@@ -269,11 +312,15 @@ int jb_rabitq_bind(const float* queries, int64_t nq, int32_t dims, int32_t bits,
                    const double* rotation, float* rotated, float* query_add, float* query_sumq, void* stream) {
     JB_CHECK_ARG(bits == 1 || bits == 2 || bits == 4 || bits == 8, "bits must be one of (1, 2, 4, 8)");
     if (nq == 0) return JB_OK;
-    const size_t smem = (size_t)dims * 8;
     cudaStream_t st = as_stream(stream);
-    JB_CUDA(cudaFuncSetAttribute(bind_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    bind_kernel<<<(unsigned)nq, 128, smem, st>>>(queries, dims, bits, centroid, rotation, rotated, query_add,
-                                                 query_sumq);
+    dim3 grid((unsigned)((nq + RT - 1) / RT), (unsigned)((dims + RT - 1) / RT));
+    rotate_gemm_kernel<<<grid, 256, 0, st>>>(queries, nq, dims, centroid, rotation, rotated);
+    JB_LAUNCH_CHECK();
+    const int wpb = 8;
+    const size_t smem = (size_t)wpb * ((dims + 3) & ~3) * 4;
+    JB_CUDA(cudaFuncSetAttribute(bind_finish_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    bind_finish_kernel<<<(unsigned)((nq + wpb - 1) / wpb), wpb * 32, smem, st>>>(queries, nq, dims, bits, centroid,
+                                                                               rotated, query_add, query_sumq);
     JB_LAUNCH_CHECK();
     return JB_OK;
 }
