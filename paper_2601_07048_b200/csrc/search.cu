@@ -29,6 +29,8 @@
 //    the per-lane float4 reads bank-conflict free). RaBitQ records are read
 //    directly, one 32 B record per lane (two 128-bit loads).
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include "common.cuh"
 #include "runtime.cuh"
 
@@ -154,41 +156,44 @@ __device__ __forceinline__ float rabitq_estimate(const uint8_t* __restrict__ rec
 // layout as the packed 1-bit codes), so
 //   <u, q> ~= lo * popc(u) + delta * sum_b 2^b popc(u & plane_b)
 // replaces the 128 ordered float adds with 4 * (QB + 1) popcounts at D = 128.
-constexpr int FAST_QB = 6;
+constexpr int FAST_QB = 6;   // default query bit-planes (template QB below)
 
 // planes: FAST_QB planes of `pw` words each (pw = nwords rounded up to 4, zero padded)
+template <int QB>
 __device__ __forceinline__ float rabitq_dd_fast(const uint8_t* __restrict__ rec, uint4 first,
                                                const uint32_t* __restrict__ planes, int pw, float lo, float delta) {
     int pc = 0;
-    int acc[FAST_QB];
+    int acc[QB];
 #pragma unroll
-    for (int b = 0; b < FAST_QB; ++b) acc[b] = 0;
+    for (int b = 0; b < QB; ++b) acc[b] = 0;
     for (int w0 = 0; w0 < pw; w0 += 4) {
         const uint4 c = w0 == 0 ? first : __ldg(reinterpret_cast<const uint4*>(rec + 4 * w0));
         pc += __popc(c.x) + __popc(c.y) + __popc(c.z) + __popc(c.w);
 #pragma unroll
-        for (int b = 0; b < FAST_QB; ++b) {
+        for (int b = 0; b < QB; ++b) {
             const uint4 p = *reinterpret_cast<const uint4*>(planes + b * pw + w0);
             acc[b] += __popc(c.x & p.x) + __popc(c.y & p.y) + __popc(c.z & p.z) + __popc(c.w & p.w);
         }
     }
     int s = 0;
 #pragma unroll
-    for (int b = 0; b < FAST_QB; ++b) s += acc[b] << b;
+    for (int b = 0; b < QB; ++b) s += acc[b] << b;
     return fmaf(delta, (float)s, lo * (float)pc);
 }
 
+template <int QB>
 __device__ __forceinline__ float rabitq_estimate_fast(const uint8_t* __restrict__ rec, const uint32_t* __restrict__ planes,
                                                       int nwords, int meta_off, float lo, float delta, float qadd,
                                                       float qsumq) {
     const uint4 first = __ldg(reinterpret_cast<const uint4*>(rec));
-    const float dd = rabitq_dd_fast(rec, first, planes, nwords, lo, delta);
+    const float dd = rabitq_dd_fast<QB>(rec, first, planes, nwords, lo, delta);
     const float2 m = __ldg(reinterpret_cast<const float2*>(rec + meta_off));
     const float est = (qadd + m.x) + m.y * (dd - qsumq);
     return est > 0.0f ? est : 0.0f;
 }
 
 // Build the query bit-planes in smem (one warp): lo/delta from a warp min/max.
+template <int QB>
 __device__ __forceinline__ void build_planes(const float* qv, int D, uint32_t* planes, float& lo, float& delta) {
     const int lane = lane_id();
     float mn = 3.4e38f, mx = -3.4e38f;
@@ -198,7 +203,7 @@ __device__ __forceinline__ void build_planes(const float* qv, int D, uint32_t* p
         mx = fmaxf(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, o));
     }
     lo = mn;
-    const float levels = (float)((1 << FAST_QB) - 1);
+    const float levels = (float)((1 << QB) - 1);
     delta = (mx > mn) ? (mx - mn) / levels : 1.0f;
     const int pw = (((D + 31) / 32) + 3) & ~3;
     for (int w = 0; w < pw; ++w) {
@@ -206,7 +211,7 @@ __device__ __forceinline__ void build_planes(const float* qv, int D, uint32_t* p
         uint32_t qq = 0;
         if (e < D) qq = (uint32_t)min((int)levels, max(0, __float2int_rn((qv[e] - lo) / delta)));
 #pragma unroll
-        for (int b = 0; b < FAST_QB; ++b) {
+        for (int b = 0; b < QB; ++b) {
             const uint32_t bits = __ballot_sync(0xFFFFFFFFu, (qq >> b) & 1u);
             if (lane == 0) planes[b * pw + w] = bits;
         }
@@ -279,8 +284,8 @@ __device__ __forceinline__ int merge_into_beam(uint64_t* beam, int& bcount, int 
     return p0;
 }
 
-template <int SRC, int BITS, bool ALIGNED>
-__global__ void __launch_bounds__(WPB * 32)
+template <int SRC, int BITS, bool ALIGNED, int CH, int MINB>
+__global__ void __launch_bounds__(WPB * 32, MINB)
 beam_search_kernel(const jb_search_args a, const SearchLayout lay, int* __restrict__ counter) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int warp = threadIdx.x >> 5;
@@ -318,7 +323,7 @@ beam_search_kernel(const jb_search_args a, const SearchLayout lay, int* __restri
         const uint32_t start = a.starts ? (uint32_t)a.starts[qi] : (uint32_t)a.start_vertex;
         __syncwarp();
         float qlo = 0.0f, qdelta = 0.0f;
-        if (SRC == JB_SRC_RABITQ_FAST) build_planes(qv, D, planes, qlo, qdelta);
+        if (SRC == JB_SRC_RABITQ_FAST) build_planes<FAST_QB>(qv, D, planes, qlo, qdelta);
 
         int lossy = 0;
         if (lane == 0) {
@@ -327,7 +332,7 @@ beam_search_kernel(const jb_search_args a, const SearchLayout lay, int* __restri
                 const float dot = a1_dot<false>(a.data + (size_t)start * D, qv, D);
                 d0 = exact_from_dot(a.data_norms[start], dot, qadd);
             } else if (SRC == JB_SRC_RABITQ_FAST) {
-                d0 = rabitq_estimate_fast(a.records + (size_t)start * RB, planes, nwords, meta_off, qlo, qdelta, qadd,
+                d0 = rabitq_estimate_fast<FAST_QB>(a.records + (size_t)start * RB, planes, nwords, meta_off, qlo, qdelta, qadd,
                                           qsumq);
             } else {
                 d0 = rabitq_estimate<BITS>(a.records + (size_t)start * RB, qv, D, meta_off, qadd, qsumq);
@@ -347,9 +352,9 @@ beam_search_kernel(const jb_search_args a, const SearchLayout lay, int* __restri
         // unexpanded key after the cursor in the pre-merge beam (right whenever this
         // hop inserts nothing in front of it). Its row is loaded while this hop runs.
         int spec = -1;
-        int spec_nb[MAX_CHUNKS];
+        int spec_nb[CH];
 #pragma unroll
-        for (int c = 0; c < MAX_CHUNKS; ++c) spec_nb[c] = -1;
+        for (int c = 0; c < CH; ++c) spec_nb[c] = -1;
 
         while (cursor < bcount) {
             const uint64_t ukey = beam[cursor];
@@ -366,11 +371,12 @@ beam_search_kernel(const jb_search_args a, const SearchLayout lay, int* __restri
             }
             ++hops;
             int s_min = cursor + 1;
-            int nbv[MAX_CHUNKS];
+            int p_ins = bcount;  // CH == 1: smallest insertion position of this hop's merge
+            int nbv[CH];
             const int32_t* adj_u = a.adjacency + (size_t)u * R;
             const int32_t* adj_s = a.adjacency + (size_t)(nspec < 0 ? 0 : nspec) * R;
 #pragma unroll
-            for (int c = 0; c < MAX_CHUNKS; ++c) {
+            for (int c = 0; c < CH; ++c) {
                 const int r = c * 32 + lane;
                 nbv[c] = (spec == (int)u) ? spec_nb[c] : ((r < R) ? __ldg(adj_u + r) : -1);
                 spec_nb[c] = (nspec >= 0 && r < R) ? __ldg(adj_s + r) : -1;
@@ -378,7 +384,7 @@ beam_search_kernel(const jb_search_args a, const SearchLayout lay, int* __restri
             spec = nspec;
 
 #pragma unroll
-            for (int c = 0; c < MAX_CHUNKS; ++c) {
+            for (int c = 0; c < CH; ++c) {
                 if (c * 32 >= R) break;
                 const int nb = nbv[c];
                 // RaBitQ: issue the candidate's record loads before the visited check
@@ -439,7 +445,7 @@ beam_search_kernel(const jb_search_args a, const SearchLayout lay, int* __restri
                         const float2 m = (RB == 32) ? make_float2(__uint_as_float(rc1.x), __uint_as_float(rc1.y))
                                                     : __ldg(reinterpret_cast<const float2*>(rec + meta_off));
                         if (SRC == JB_SRC_RABITQ_FAST) {
-                            const float dd = rabitq_dd_fast(rec, rc0, planes, nwords, qlo, qdelta);
+                            const float dd = rabitq_dd_fast<FAST_QB>(rec, rc0, planes, nwords, qlo, qdelta);
                             const float est = (qadd + m.x) + m.y * (dd - qsumq);
                             d = est > 0.0f ? est : 0.0f;
                         } else {
@@ -451,8 +457,18 @@ beam_search_kernel(const jb_search_args a, const SearchLayout lay, int* __restri
                 const uint64_t key = have ? pack_key(d, (uint32_t)myid) : UMAX;
                 const int p0 = merge_into_beam(beam, bcount, L, key, psurv);
                 s_min = min(s_min, p0);
+                p_ins = p0;
             }
-            cursor = first_unexpanded(beam, s_min, bcount);
+            if (CH == 1) {
+                // One merge per hop: the keys it inserted are unexpanded and the smallest
+                // landed at p_ins (the pre-merge bcount when nothing was inserted);
+                // entries before it are unchanged. So the first unexpanded key is at
+                // p_ins if that is at or before the pre-merge candidate sidx, else sidx
+                // did not move (nothing was inserted in front of it).
+                cursor = min(p_ins, sidx);
+            } else {
+                cursor = first_unexpanded(beam, s_min, bcount);
+            }
         }
 
         // ---- outputs ----
@@ -538,7 +554,7 @@ rerank_kernel(const float* __restrict__ data, int D, const float* __restrict__ q
 static int pow2_ceil(int v) { int p = 1; while (p < v) p <<= 1; return p; }
 static int log2i(int v) { int l = 0; while ((1 << l) < v) ++l; return l; }
 
-static SearchLayout make_layout(int src, int D, int L, int hash_slots) {
+static SearchLayout make_layout(int src, int D, int L, int hash_slots, int qb) {
     SearchLayout s{};
     auto align16 = [](int v) { return (v + 15) & ~15; };
     int off = 0;
@@ -553,15 +569,15 @@ static SearchLayout make_layout(int src, int D, int L, int hash_slots) {
     s.stage_off = off;
     if (src == JB_SRC_EXACT) off += 32 * s.sstride * 4;
     s.plane_off = off;
-    if (src == JB_SRC_RABITQ_FAST) off += FAST_QB * ((((D + 31) / 32) + 3) & ~3) * 4;
+    if (src == JB_SRC_RABITQ_FAST) off += qb * ((((D + 31) / 32) + 3) & ~3) * 4;
     s.bytes = align16(off);
     return s;
 }
 
-template <int SRC, int BITS, bool ALIGNED>
-static int launch_search(const jb_search_args& a, int hash_slots, cudaStream_t st) {
-    SearchLayout lay = make_layout(SRC, a.dims, a.beam_width, hash_slots);
-    auto kern = beam_search_kernel<SRC, BITS, ALIGNED>;
+template <int SRC, int BITS, bool ALIGNED, int CH, int MINB>
+static int launch_search_inst(const jb_search_args& a, int hash_slots, cudaStream_t st) {
+    SearchLayout lay = make_layout(SRC, a.dims, a.beam_width, hash_slots, FAST_QB);
+    auto kern = beam_search_kernel<SRC, BITS, ALIGNED, CH, MINB>;
     const int smem = lay.bytes * WPB;
     JB_CHECK_ARG(smem <= 227 * 1024, "beam search: per-block shared memory %d B exceeds 227 KB", smem);
     // occupancy per (instantiation, smem size), cached: the attribute/occupancy
@@ -587,6 +603,16 @@ static int launch_search(const jb_search_args& a, int hash_slots, cudaStream_t s
     return JB_OK;
 }
 
+// R <= 32: one neighbour chunk per hop (single merge, no rescan of the beam).
+// Blocks/SM: the popcount kernel is issue-bound and gains from 10 resident
+// blocks (48 registers, no spills); the float estimators keep 8.
+template <int SRC, int BITS, bool ALIGNED>
+static int launch_search(const jb_search_args& a, int hash_slots, cudaStream_t st) {
+    constexpr int MINB = SRC == JB_SRC_RABITQ_FAST ? 10 : 8;
+    if (a.degree_cap <= 32) return launch_search_inst<SRC, BITS, ALIGNED, 1, MINB>(a, hash_slots, st);
+    return launch_search_inst<SRC, BITS, ALIGNED, MAX_CHUNKS, 8>(a, hash_slots, st);
+}
+
 }  // namespace jb
 
 using namespace jb;
@@ -609,8 +635,8 @@ int jb_beam_search(const jb_search_args* args, void* stream) {
     int hs = a.hash_slots;
     // Small tables win: evictions only cost re-evaluations (results stay exact),
     // while smem per warp sets occupancy (measured at L=128: 1024 slots 19% faster
-    // than 2048, 512 equal to 1024).
-    if (hs <= 0) hs = std::min(2048, std::max(1024, pow2_ceil(8 * a.beam_width)));
+    // than 2048; 512 slots 1% faster than 1024 with 10 blocks/SM).
+    if (hs <= 0) hs = std::min(2048, std::max(512, pow2_ceil(4 * a.beam_width)));
     hs = std::max(32, pow2_ceil(hs));
     cudaStream_t st = as_stream(stream);
     if (a.source == JB_SRC_EXACT) {
