@@ -117,6 +117,25 @@ int jb_rerank_topk(const float* data, int32_t dims, const float* queries, int64_
                    const uint64_t* frontier_keys, int32_t beam_width, int32_t k,
                    int32_t* out_ids, double* out_dists, void* stream);
 
+/* Host-buffer search: the whole search_knn_batch call (search.py:351-383) in
+ * native code. `search` carries the graph and distance source (device pointers;
+ * its query/output/trace fields are ignored). Queries are read from host memory,
+ * (ids int32, dists f64) [nq, k] written to host memory (-1 / +inf padded), in
+ * pipelined chunks over two streams (pinned staging, H2D, bind, search, rerank,
+ * D2H). Returns after the results are in the caller's arrays. */
+typedef struct jb_knn_plan {
+    jb_search_args search;         /* graph + source + beam_width + hash_slots   */
+    const float* centroid;         /* RABITQ: f32 [D] (device)                   */
+    const double* rotation;        /* RABITQ: f64 [D, D] (device)                */
+    const float* rerank_data;      /* f32 [N, D] rows for the exact rerank, or NULL
+                                    * for the frontier's own top-k               */
+    int32_t k;
+    int32_t chunk;                 /* queries per pipeline chunk, 0 = auto       */
+} jb_knn_plan;
+
+int jb_search_knn_host(const jb_knn_plan* plan, const float* queries, int64_t nq,
+                       int32_t* out_ids, double* out_dists, void* stream);
+
 /* ---- RaBitQ (north-star 2) --------------------------------------------- */
 
 /* Packed device record of one vector: code bytes, zero padding to 16, then

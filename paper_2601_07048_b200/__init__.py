@@ -16,7 +16,7 @@ from .search import (SearchParams, SearchResult, SearchStats, beam_search, run_b
                      search_knn_batch, search_knn_batch_device)
 
 from . import measure, shard  # noqa: E402
-from .measure import GroundTruth, SweepPoint, recall_at_k, run_queries, sweep  # noqa: E402
+from .measure import GroundTruth, SweepPoint, exact_knn, recall_at_k, run_queries, sweep  # noqa: E402
 
 __version__ = "0.1.0"
 
@@ -25,5 +25,5 @@ __all__ = [
     "Candidate", "DistanceKind", "ElementKind", "FormatError", "GraphIndex", "QueryPrep", "RaBitQIndex",
     "SearchParams", "SearchResult", "SearchStats", "VectorDataset", "beam_search", "dot", "estimate_sq_dist",
     "gen_lowrank", "gen_synthetic", "medoid", "prep_query", "rabitq_fit", "robust_prune", "rotate",
-    "run_beam_searches", "search_knn", "GroundTruth", "SweepPoint", "recall_at_k", "run_queries", "sweep", "search_knn_batch", "search_knn_batch_device", "sq_l2",
+    "run_beam_searches", "search_knn", "GroundTruth", "exact_knn", "SweepPoint", "recall_at_k", "run_queries", "sweep", "search_knn_batch", "search_knn_batch_device", "sq_l2",
 ]

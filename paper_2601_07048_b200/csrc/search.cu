@@ -234,11 +234,14 @@ __device__ __forceinline__ int first_unexpanded(const uint64_t* beam, int s, int
 // Merge up to 32 candidate keys (one per lane, UMAX = none) into the sorted beam
 // (search.py:232-237: stable sort of beam + candidates, first L kept). Keys are
 // distinct except a re-evaluated id equal to a beam key (dropped: the incumbent
-// keeps its expanded flag). Positions come from ranks, not a sort:
-//   new key: (#survivors below it) + lower_bound(beam);
-//   beam[i]: i + #{survivors whose lower_bound <= i}.
-// Returns the smallest insertion position (or bcount if nothing was inserted).
-__device__ __forceinline__ int merge_into_beam(uint64_t* beam, int& bcount, int L, uint64_t key, int* psurv) {
+// keeps its expanded flag). No sort: each surviving key's final position is
+//   fs = lower_bound(beam, key) + #survivors below it,
+// distinct across survivors, recorded as bits of a per-warp position mask. Beam
+// entries are then gathered top-down, one 32-entry chunk per step: output j
+// (not a survivor slot) takes old entry j - #survivor slots below j, a popcount
+// of the mask. Returns the smallest insertion position (bcount if none).
+__device__ __forceinline__ int merge_into_beam(uint64_t* beam, int& bcount, int L, uint64_t key,
+                                               uint32_t* fmask) {
     const unsigned FULL = 0xFFFFFFFFu;
     const int lane = lane_id();
     if (key != UMAX && bcount == L && key >= key_mask(beam[L - 1])) key = UMAX;
@@ -255,32 +258,33 @@ __device__ __forceinline__ int merge_into_beam(uint64_t* beam, int& bcount, int 
         const int t = __ffs(mm) - 1;
         rank += (shfl_u64(key, t) < key) ? 1 : 0;
     }
-    if (key != UMAX) psurv[rank] = p;
+    const int fs = p + rank;
+    const bool live = key != UMAX && fs < L;
+    if (live) atomicOr(&fmask[fs >> 5], 1u << (fs & 31));
+    const uint32_t lm = __ballot_sync(FULL, live);
+    const int mlive = __popc(lm);
+    // the rank-0 survivor lands exactly at its lower bound, the smallest position
+    const int p0 = __shfl_sync(FULL, fs, __ffs(__ballot_sync(FULL, key != UMAX && rank == 0)) - 1);
+    const int nb = min(L, bcount + m2);
     __syncwarp();
-    const int p0 = psurv[0];
-    for (int cb = ((bcount - 1) >> 5) << 5; cb >= (p0 & ~31); cb -= 32) {
-        const int i = cb + lane;
-        uint64_t bk = 0;
-        int np = -1;
-        if (i >= p0 && i < bcount) {
-            bk = beam[i];
-            int lo = 0, hi = m2;  // upper_bound(psurv, i): psurv is ascending
-            while (lo < hi) {
-                const int mid = (lo + hi) >> 1;
-                if (psurv[mid] <= i) lo = mid + 1; else hi = mid;
-            }
-            np = i + lo;
-        }
+    int above = 0;  // live survivor slots in chunks above the current one
+    const uint32_t lt = lanemask_lt();
+    for (int ob = ((nb - 1) >> 5) << 5; ob >= (p0 & ~31); ob -= 32) {
+        const uint32_t w = fmask[ob >> 5];
+        const int j = ob + lane;
+        const int pw = __popc(w);
+        const bool mv = j >= p0 && j < nb && !((w >> lane) & 1u);
+        uint64_t v = 0;
+        if (mv) v = beam[j - (mlive - above - pw + __popc(w & lt))];
         __syncwarp();
-        if (np >= 0 && np < L) beam[np] = bk;
-        __syncwarp();
-    }
-    if (key != UMAX) {
-        const int np = rank + p;
-        if (np < L) beam[np] = key;
+        if (mv) beam[j] = v;
+        above += pw;
     }
     __syncwarp();
-    bcount = min(L, bcount + m2);
+    if (live) beam[fs] = key;
+    if (lane >= (p0 >> 5) && lane <= ((nb - 1) >> 5)) fmask[lane] = 0;
+    __syncwarp();
+    bcount = nb;
     return p0;
 }
 
@@ -294,7 +298,7 @@ beam_search_kernel(const jb_search_args a, const SearchLayout lay, int* __restri
     float* qv = reinterpret_cast<float*>(base + lay.q_off);
     uint64_t* beam = reinterpret_cast<uint64_t*>(base + lay.beam_off);
     uint32_t* tab = reinterpret_cast<uint32_t*>(base + lay.hash_off);
-    int* psurv = reinterpret_cast<int*>(base + lay.newk_off);
+    uint32_t* fmask = reinterpret_cast<uint32_t*>(base + lay.newk_off);  // survivor-slot mask, L/32 words
     int32_t* cid = reinterpret_cast<int32_t*>(base + lay.cid_off);
     float* stage = reinterpret_cast<float*>(base + lay.stage_off);
     uint32_t* planes = reinterpret_cast<uint32_t*>(base + lay.plane_off);
@@ -317,6 +321,7 @@ beam_search_kernel(const jb_search_args a, const SearchLayout lay, int* __restri
         const float* q = a.queries + qi * D;
         for (int e = lane; e < D; e += 32) qv[e] = q[e];
         for (int i = lane; i < L; i += 32) beam[i] = UMAX;
+        fmask[lane] = 0;
         for (int i = lane; i < H / 4; i += 32) reinterpret_cast<uint4*>(tab)[i] = make_uint4(EMPTY_SLOT, EMPTY_SLOT, EMPTY_SLOT, EMPTY_SLOT);
         const float qadd = a.query_add[qi];
         const float qsumq = (SRC != JB_SRC_EXACT) ? a.query_sumq[qi] : 0.0f;
@@ -455,7 +460,7 @@ beam_search_kernel(const jb_search_args a, const SearchLayout lay, int* __restri
                 }
                 const bool have = (SRC == JB_SRC_EXACT) ? (lane < nnew) : isnew;
                 const uint64_t key = have ? pack_key(d, (uint32_t)myid) : UMAX;
-                const int p0 = merge_into_beam(beam, bcount, L, key, psurv);
+                const int p0 = merge_into_beam(beam, bcount, L, key, fmask);
                 s_min = min(s_min, p0);
                 p_ins = p0;
             }

@@ -4,6 +4,7 @@
   run_queries   bench.py:69-91   one batched device call (threads are unnecessary)
   sweep         bench.py:94-137  warmup + timed pass per beam width, recall, QPS
   SweepPoint / write_sweep_csv   io.py:39, 172-180 column layout
+  exact_knn     oracle.py:20-62  exact f64 top-k (ground truth) on the GPU (jb_exact_knn)
 """
 
 from __future__ import annotations
@@ -14,9 +15,12 @@ from dataclasses import dataclass
 
 import numpy as np
 
+from . import _lib
+from .core import VectorDataset, as_dataset
 from .search import SearchParams, search_knn_batch
 
-__all__ = ["SweepPoint", "GroundTruth", "recall_at_k", "run_queries", "sweep", "write_sweep_csv"]
+__all__ = ["SweepPoint", "GroundTruth", "exact_knn", "exact_knn_device", "recall_at_k", "run_queries", "sweep",
+           "write_sweep_csv"]
 
 _RELATIVE_EPS = 1e-6
 SWEEP_CSV_HEADER = ("beam_width", "k", "recall", "qps", "mean_latency_us")
@@ -34,6 +38,39 @@ class GroundTruth:
     @property
     def k(self) -> int:
         return self.ids.shape[1]
+
+
+def exact_knn_device(x_dev, q_dev, k: int):
+    """Exact top-k on HBM-resident f32 rows/queries: (ids int32 [nq,k], dists f32 [nq,k])
+    ranked by (f64 score, id) like oracle.py:44-58, as device tensors."""
+    torch = _lib.require_cuda()
+    n, D = x_dev.shape
+    nq = q_dev.shape[0]
+    if not 1 <= k <= n:
+        raise ValueError(f"k must be in [1, {n}]")
+    if q_dev.shape[1] != D:
+        raise ValueError(f"dimension mismatch: data {D}, queries {q_dev.shape[1]}")
+    x_dev = x_dev.to(torch.float32).contiguous()
+    q_dev = q_dev.to(torch.float32).contiguous()
+    ids = torch.empty((nq, k), dtype=torch.int32, device=x_dev.device)
+    ds = torch.empty((nq, k), dtype=torch.float32, device=x_dev.device)
+    _lib.check(_lib.lib().jb_exact_knn(_lib.ptr(x_dev), n, D, _lib.ptr(q_dev), nq, k, _lib.ptr(ids), _lib.ptr(ds),
+                                       _lib.stream_ptr()))
+    return ids, ds
+
+
+def exact_knn(data, queries, k: int) -> GroundTruth:
+    """oracle.py:20-62: exhaustive top-k per query in f64, ties broken by id."""
+    torch = _lib.require_cuda()
+    ds = as_dataset(data) if not isinstance(data, np.ndarray) else VectorDataset(data)
+    qs = as_dataset(queries) if not isinstance(queries, np.ndarray) else VectorDataset(queries)
+    if not 1 <= k <= ds.count:
+        raise ValueError(f"k must be in [1, {ds.count}]")
+    if ds.dims != qs.dims:
+        raise ValueError(f"dimension mismatch: data {ds.dims}, queries {qs.dims}")
+    q_dev = torch.from_numpy(np.ascontiguousarray(qs.data, dtype=np.float32)).cuda()
+    ids, dists = exact_knn_device(ds.device().x, q_dev, k)
+    return GroundTruth(ids=ids.cpu().numpy(), distances=dists.cpu().numpy())
 
 
 @dataclass(frozen=True)

@@ -347,17 +347,70 @@ def _knn_device(graph: GraphIndex, source, q_dev, params: SearchParams, exact_da
 def search_knn_batch(graph, source, queries, params: SearchParams, exact_data=None):
     """search.py:351-383: (ids int32 [nq,k] padded -1, dists f64 [nq,k] padded +inf).
 
-    Host arrays in and out: queries are copied to HBM, one search launch plus
-    one top-k (or fp32 rerank) launch run, and the results are copied back.
+    Host arrays in and out, through the native host pipeline jb_search_knn_host
+    (pinned staging, H2D, bind, search, rerank/top-k, D2H in chunks over two
+    streams; csrc/pipeline.cu).
     """
     graph = as_graph(graph)
     _validate(graph, params.beam_width)
     if params.rerank and _is_rabitq(source) and exact_data is None:
         raise ValueError("rerank over a quantized source requires exact_data")
-    q_dev = _queries_to_device(queries)
-    ids, dists = _knn_device(graph, source, q_dev, params, exact_data)
-    ids_h, dists_h = _to_host(ids, dists)
-    return ids_h, dists_h
+    q = np.atleast_2d(np.asarray(queries))
+    q = np.ascontiguousarray(q, dtype=np.float32)
+    nq = q.shape[0]
+    ids = np.empty((nq, params.k), dtype=np.int32)
+    dists = np.empty((nq, params.k), dtype=np.float64)
+    plan = _knn_plan(graph, source, q.shape[1], params, exact_data)
+    _lib.check(_lib.lib().jb_search_knn_host(_lib.C.byref(plan), _lib.ptr(q), nq, _lib.ptr(ids), _lib.ptr(dists),
+                                             _lib.stream_ptr()))
+    return ids, dists
+
+
+# Host-API pipeline chunk (queries per chunk; 0 = library default). Tuning hook.
+PIPELINE = {"chunk": 0}
+
+
+def _knn_plan(graph: GraphIndex, source, D: int, params: SearchParams, exact_data=None):
+    """jb_knn_plan for jb_search_knn_host: graph + distance source as device pointers."""
+    adj, _ = graph.device()
+    plan = _lib.KnnPlan()
+    a = plan.search
+    a.adjacency = _lib.ptr(adj)
+    a.degree_cap = graph.degree_cap
+    a.active_count = graph.active_count
+    a.start_vertex = graph.entry_point
+    a.beam_width = params.beam_width
+    a.hash_slots = int(TUNING["hash_slots"])
+    a.dims = D
+    if _is_rabitq(source):
+        from .rabitq import as_rabitq
+
+        idx = as_rabitq(source)
+        if D != idx.dims:
+            raise ValueError(f"query dims {D} != index dims {idx.dims}")
+        dev = idx.device()
+        a.source = _lib.SRC_RABITQ
+        if params.estimator == "popcount":
+            if idx.bits != 1:
+                raise ValueError("the popcount estimator needs 1-bit codes")
+            a.source = _lib.SRC_RABITQ_FAST
+        a.records, a.record_bytes, a.bits = _lib.ptr(dev.records), dev.record_bytes, idx.bits
+        plan.centroid, plan.rotation = _lib.ptr(dev.centroid), _lib.ptr(dev.rotation)
+        if params.rerank:
+            rows = as_dataset(exact_data).device()
+            if rows.dims != D:
+                raise ValueError(f"query dims {D} != dataset dims {rows.dims}")
+            plan.rerank_data = _lib.ptr(rows.x)
+    else:
+        ds = as_dataset(source)
+        if D != ds.dims:
+            raise ValueError(f"query dims {D} != dataset dims {ds.dims}")
+        rows = ds.device()
+        a.source = _lib.SRC_EXACT
+        a.data, a.data_norms = _lib.ptr(rows.x), _lib.ptr(rows.norms)
+    plan.k = params.k
+    plan.chunk = int(PIPELINE["chunk"])
+    return plan
 
 
 def search_knn_batch_device(graph, source, q_dev, params: SearchParams, exact_data=None):

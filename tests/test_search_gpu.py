@@ -277,3 +277,35 @@ def test_popcount_estimator_recall_tracks_reference_estimator():
         idx4 = jb.rabitq_fit(ds, bits=4, seed=1)
         jb.search_knn_batch(g, idx4, q, jb.SearchParams(beam_width=16, k=10, rerank=True, estimator="popcount"),
                             exact_data=ds)
+
+
+@pytest.mark.parametrize("chunk", [0, 97, 1000])
+@pytest.mark.parametrize("kind", ["exact", "rabitq", "popcount"])
+def test_host_pipeline_matches_device_path(chunk, kind):
+    """jb_search_knn_host (host buffers, chunked over two streams) returns exactly
+    what the HBM-resident path returns, for every chunking."""
+    from paper_2601_07048_b200 import search as js
+
+    x = lowrank(6000, 64, 8, 0.05, 21)
+    q = lowrank(1000, 64, 8, 0.05, 22)
+    ds = jb.VectorDataset(x)
+    g = jb.build(ds, jb.BuildParams(degree_cap=24, build_beam_width=48, alpha=1.2))
+    if kind == "exact":
+        src, sp = ds, jb.SearchParams(beam_width=40, k=10)
+    else:
+        src = jb.rabitq_fit(ds, bits=1, seed=3)
+        sp = jb.SearchParams(beam_width=40, k=10, rerank=True,
+                             estimator="popcount" if kind == "popcount" else "reference")
+    import torch
+
+    di, dd = jb.search_knn_batch_device(g, src, torch.from_numpy(q).cuda(), sp, exact_data=ds)
+    js.PIPELINE["chunk"] = chunk
+    try:
+        hi, hd = jb.search_knn_batch(g, src, q, sp, exact_data=ds)
+        hi2, hd2 = jb.search_knn_batch(g, src, q[:333], sp, exact_data=ds)  # reuse of the cached context
+    finally:
+        js.PIPELINE["chunk"] = 0
+    np.testing.assert_array_equal(hi, di.cpu().numpy())
+    np.testing.assert_array_equal(hd, dd.cpu().numpy())
+    np.testing.assert_array_equal(hi2, hi[:333])
+    np.testing.assert_array_equal(hd2, hd[:333])
