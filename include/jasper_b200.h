@@ -136,6 +136,11 @@ typedef struct jb_knn_plan {
 int jb_search_knn_host(const jb_knn_plan* plan, const float* queries, int64_t nq,
                        int32_t* out_ids, double* out_dists, void* stream);
 
+/* Same with HBM-resident queries [nq, D] and outputs [nq, k] (device pointers):
+ * enqueues the chunks on the two lanes and makes `stream` wait for them. */
+int jb_search_knn_device(const jb_knn_plan* plan, const float* queries, int64_t nq,
+                         int32_t* out_ids, double* out_dists, void* stream);
+
 /* ---- RaBitQ (north-star 2) --------------------------------------------- */
 
 /* Packed device record of one vector: code bytes, zero padding to 16, then

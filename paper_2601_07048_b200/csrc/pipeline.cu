@@ -216,28 +216,66 @@ int drain(Ctx& c, Lane& l, int k, int32_t* out_ids, double* out_d, PhaseTimer& p
 
 using namespace jb;
 
-static int search_knn_host(const jb_knn_plan* plan, const float* queries, int64_t nq, int32_t* out_ids,
-                           double* out_dists, void* stream) {
-    JB_CHECK_ARG(plan != nullptr, "jb_search_knn_host: null plan");
+// Device work of one chunk on its lane: bind (or query norms), beam search,
+// rerank / top-k into (ids, dists) — device pointers, `q` already in HBM.
+static int run_chunk(const jb_knn_plan* plan, Lane& l, const float* q, int64_t m, int32_t* ids, double* dists) {
     const jb_search_args& base = plan->search;
     const int D = base.dims, L = base.beam_width, k = plan->k;
-    JB_CHECK_ARG(D >= 1, "dims must be >= 1");
-    JB_CHECK_ARG(L >= 1 && L <= 1024, "beam_width must be in [1, 1024]");
-    JB_CHECK_ARG(k >= 1 && k <= L, "k must satisfy 1 <= k <= beam_width");
-    const bool quant = base.source != JB_SRC_EXACT;
-    JB_CHECK_ARG(!quant || (plan->centroid && plan->rotation), "quantized source: centroid and rotation required");
-    if (nq == 0) return JB_OK;
-    JB_CHECK_ARG(queries && out_ids && out_dists, "jb_search_knn_host: null host buffer");
-
-    int64_t C = plan->chunk > 0 ? plan->chunk : std::max<int64_t>(1024, ((nq + 3) / 4 + 255) / 256 * 256);
-    C = std::min<int64_t>(C, nq);
-    Ctx& c = g_ctx;
-    int st = ensure(c, C, D, L, k);
+    jb_search_args a = base;
+    int st;
+    if (base.source != JB_SRC_EXACT) {
+        st = jb_rabitq_bind(q, m, D, base.bits, plan->centroid, plan->rotation, l.d_rot, l.d_qadd, l.d_sumq, l.s);
+        a.queries = l.d_rot;
+        a.query_sumq = l.d_sumq;
+    } else {
+        st = jb_row_sq_norms(q, m, D, l.d_qadd, l.s);
+        a.queries = q;
+        a.query_sumq = nullptr;
+    }
     if (st != JB_OK) return st;
-    // device data written on the caller's stream (uploads, builds) is visible to both lanes
-    cudaStream_t caller = as_stream(stream);
+    a.query_add = l.d_qadd;
+    a.nq = m;
+    a.starts = nullptr;
+    a.trace_cap = 0;
+    a.trace_ids = nullptr;
+    a.trace_dists = nullptr;
+    a.frontier_keys = l.d_fk;
+    a.hops = a.evals = a.flags = nullptr;
+    if ((st = jb_beam_search(&a, l.s)) != JB_OK) return st;
+    if (plan->rerank_data) return jb_rerank_topk(plan->rerank_data, D, q, m, l.d_fk, L, k, ids, dists, l.s);
+    return jb_frontier_topk(l.d_fk, m, L, k, ids, dists, l.s);
+}
+
+static int check_plan(const jb_knn_plan* plan) {
+    JB_CHECK_ARG(plan != nullptr, "knn search: null plan");
+    const jb_search_args& base = plan->search;
+    JB_CHECK_ARG(base.dims >= 1, "dims must be >= 1");
+    JB_CHECK_ARG(base.beam_width >= 1 && base.beam_width <= 1024, "beam_width must be in [1, 1024]");
+    JB_CHECK_ARG(plan->k >= 1 && plan->k <= base.beam_width, "k must satisfy 1 <= k <= beam_width");
+    JB_CHECK_ARG(base.source == JB_SRC_EXACT || (plan->centroid && plan->rotation),
+                 "quantized source: centroid and rotation required");
+    return JB_OK;
+}
+
+// Lanes start after everything already queued on the caller's stream (uploads, builds).
+static int fork_lanes(Ctx& c, cudaStream_t caller) {
     JB_CUDA(cudaEventRecord(c.start, caller));
     for (Lane& l : c.lane) JB_CUDA(cudaStreamWaitEvent(l.s, c.start, 0));
+    return JB_OK;
+}
+
+static int search_knn_host(const jb_knn_plan* plan, const float* queries, int64_t nq, int32_t* out_ids,
+                           double* out_dists, void* stream) {
+    int st = check_plan(plan);
+    if (st != JB_OK || nq == 0) return st;
+    JB_CHECK_ARG(queries && out_ids && out_dists, "jb_search_knn_host: null host buffer");
+    const int D = plan->search.dims, L = plan->search.beam_width, k = plan->k;
+    // chunks: two lanes, ~nq/2 each by default (concurrent kernels fill each other's tails)
+    int64_t C = plan->chunk > 0 ? plan->chunk : std::max<int64_t>(1024, ((nq + 1) / 2 + 255) / 256 * 256);
+    C = std::min<int64_t>(C, nq);
+    Ctx& c = g_ctx;
+    if ((st = ensure(c, C, D, L, k)) != JB_OK) return st;
+    if ((st = fork_lanes(c, as_stream(stream))) != JB_OK) return st;
 
     PhaseTimer pt;
     int64_t chunk_i = 0;
@@ -249,32 +287,7 @@ static int search_knn_host(const jb_knn_plan* plan, const float* queries, int64_
         c.pool->copy(l.h_q, queries + q0 * D, sizeof(float) * m * D);
         pt.tick(0);
         JB_CUDA(cudaMemcpyAsync(l.d_q, l.h_q, sizeof(float) * m * D, cudaMemcpyHostToDevice, l.s));
-        jb_search_args a = base;
-        if (quant) {
-            st = jb_rabitq_bind(l.d_q, m, D, base.bits, plan->centroid, plan->rotation, l.d_rot, l.d_qadd, l.d_sumq,
-                                l.s);
-            a.queries = l.d_rot;
-            a.query_sumq = l.d_sumq;
-        } else {
-            st = jb_row_sq_norms(l.d_q, m, D, l.d_qadd, l.s);
-            a.queries = l.d_q;
-            a.query_sumq = nullptr;
-        }
-        if (st != JB_OK) return st;
-        a.query_add = l.d_qadd;
-        a.nq = m;
-        a.starts = nullptr;
-        a.trace_cap = 0;
-        a.trace_ids = nullptr;
-        a.trace_dists = nullptr;
-        a.frontier_keys = l.d_fk;
-        a.hops = a.evals = a.flags = nullptr;
-        if ((st = jb_beam_search(&a, l.s)) != JB_OK) return st;
-        if (plan->rerank_data)
-            st = jb_rerank_topk(plan->rerank_data, D, l.d_q, m, l.d_fk, L, k, l.d_ids, l.d_d, l.s);
-        else
-            st = jb_frontier_topk(l.d_fk, m, L, k, l.d_ids, l.d_d, l.s);
-        if (st != JB_OK) return st;
+        if ((st = run_chunk(plan, l, l.d_q, m, l.d_ids, l.d_d)) != JB_OK) return st;
         JB_CUDA(cudaMemcpyAsync(l.h_ids, l.d_ids, sizeof(int32_t) * m * k, cudaMemcpyDeviceToHost, l.s));
         JB_CUDA(cudaMemcpyAsync(l.h_d, l.d_d, sizeof(double) * m * k, cudaMemcpyDeviceToHost, l.s));
         JB_CUDA(cudaEventRecord(l.done, l.s));
@@ -301,4 +314,28 @@ extern "C" int jb_search_knn_host(const jb_knn_plan* plan, const float* queries,
         }
     }
     return st;
+}
+
+// HBM-resident variant: queries and outputs are device arrays; the call only
+// enqueues (two lanes, joined back into the caller's stream).
+extern "C" int jb_search_knn_device(const jb_knn_plan* plan, const float* queries, int64_t nq, int32_t* out_ids,
+                                    double* out_dists, void* stream) {
+    int st = check_plan(plan);
+    if (st != JB_OK || nq == 0) return st;
+    const int D = plan->search.dims, L = plan->search.beam_width, k = plan->k;
+    int64_t C = plan->chunk > 0 ? plan->chunk : (nq >= 2048 ? (nq + 1) / 2 : nq);
+    C = std::min<int64_t>(C, nq);
+    Ctx& c = g_ctx;
+    if ((st = ensure(c, C, D, L, k)) != JB_OK) return st;
+    cudaStream_t caller = as_stream(stream);
+    if ((st = fork_lanes(c, caller)) != JB_OK) return st;
+    int64_t chunk_i = 0;
+    for (int64_t q0 = 0; q0 < nq; q0 += C, ++chunk_i) {
+        Lane& l = c.lane[chunk_i & 1];
+        const int64_t m = std::min<int64_t>(C, nq - q0);
+        if ((st = run_chunk(plan, l, queries + q0 * D, m, out_ids + q0 * k, out_dists + q0 * k)) != JB_OK) return st;
+        JB_CUDA(cudaEventRecord(l.done, l.s));
+    }
+    for (int i = 0; i < 2 && i < chunk_i; ++i) JB_CUDA(cudaStreamWaitEvent(caller, c.lane[i].done, 0));
+    return JB_OK;
 }

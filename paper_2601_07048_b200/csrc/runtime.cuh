@@ -33,6 +33,11 @@ inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s
 
 int sm_count_current();
 
+// Once per device: keep freed stream-ordered memory in the default pool instead
+// of returning it to the driver at every synchronization (the default release
+// threshold 0 turned each launch's small scratch allocation into a ~0.5 ms remap).
+void retain_pool_memory();
+
 // Stream-ordered scratch that frees itself (cudaFreeAsync) on scope exit.
 struct Scratch {
     void* p = nullptr;
@@ -41,6 +46,7 @@ struct Scratch {
     Scratch(const Scratch&) = delete;
     Scratch& operator=(const Scratch&) = delete;
     cudaError_t alloc(size_t bytes, cudaStream_t st) {
+        retain_pool_memory();
         s = st;
         if (bytes == 0) bytes = 16;
         return cudaMallocAsync(&p, bytes, st);

@@ -367,7 +367,7 @@ def search_knn_batch(graph, source, queries, params: SearchParams, exact_data=No
 
 
 # Host-API pipeline chunk (queries per chunk; 0 = library default). Tuning hook.
-PIPELINE = {"chunk": 0}
+PIPELINE = {"chunk": 0, "device_chunk": 0}
 
 
 def _knn_plan(graph: GraphIndex, source, D: int, params: SearchParams, exact_data=None):
@@ -414,7 +414,21 @@ def _knn_plan(graph: GraphIndex, source, D: int, params: SearchParams, exact_dat
 
 
 def search_knn_batch_device(graph, source, q_dev, params: SearchParams, exact_data=None):
-    """HBM-resident variant: queries and results stay torch CUDA tensors (no host sync)."""
+    """HBM-resident variant: queries and results stay torch CUDA tensors (no host sync).
+    One native call (jb_search_knn_device): the batch is split over two streams so
+    the second half's search kernel fills the SMs the first half's tail leaves idle;
+    the current stream waits for both."""
     graph = as_graph(graph)
     _validate(graph, params.beam_width)
-    return _knn_device(graph, source, q_dev, params, exact_data)
+    if params.rerank and _is_rabitq(source) and exact_data is None:
+        raise ValueError("rerank over a quantized source requires exact_data")
+    torch = _lib.require_cuda()
+    q_dev = q_dev.to(dtype=torch.float32).contiguous()
+    nq = q_dev.shape[0]
+    ids = torch.empty((nq, params.k), dtype=torch.int32, device=q_dev.device)
+    dists = torch.empty((nq, params.k), dtype=torch.float64, device=q_dev.device)
+    plan = _knn_plan(graph, source, q_dev.shape[1], params, exact_data)
+    plan.chunk = int(PIPELINE["device_chunk"])
+    _lib.check(_lib.lib().jb_search_knn_device(_lib.C.byref(plan), _lib.ptr(q_dev), nq, _lib.ptr(ids),
+                                               _lib.ptr(dists), _lib.stream_ptr()))
+    return ids, dists
