@@ -4,11 +4,12 @@ bench.py stays the single headline harness (configs[1]); this script runs:
   c1  synthetic 100K x 128 Gaussian, R=32 L_build=64 alpha=1.2, 10K queries, k=10, EXACT
       distances, L sweep 16..256 (the reference's own CPU-runnable config): device QPS,
       recall, ids checked identical to the oracle on a sample, oracle CPU QPS
-  c3  GIST-shaped 1M x 960 low-rank (d_int=32), RaBitQ m=4 + fp32 rerank: QPS at recall 0.95
+  c3  GIST-shaped 1M x 960 low-rank (d_int=16 default, --dint), RaBitQ m=4 + fp32 rerank: QPS at recall 0.95
   c4  DEEP-shaped 96-d low-rank: bulk build of the first N0, then insert_stream in batches of
       100K interleaved with a 10K-query exact search after every batch (inserts/s, QPS)
+  c5  one 12.5M x 96 shard of the 100M x 96 index (the per-GPU work at 8 GPUs)
 
-    python bench_configs.py c1|c3|c4 [--n N] [--total T]
+    python bench_configs.py c1|c3|c4|c5 [--n N] [--total T] [--dint D]
 """
 
 from __future__ import annotations
@@ -89,8 +90,9 @@ def c3(args):
     import paper_2601_07048_b200 as jb
 
     n = args.n or 1_000_000
-    x = jb.gen_lowrank(n, 960, seed=1, d_int=32, noise=0.05, basis_seed=0)
-    q = jb.gen_lowrank(10_000, 960, seed=1_000_003, d_int=32, noise=0.05, basis_seed=0)
+    dint = args.dint or 16
+    x = jb.gen_lowrank(n, 960, seed=1, d_int=dint, noise=0.05, basis_seed=0)
+    q = jb.gen_lowrank(10_000, 960, seed=1_000_003, d_int=dint, noise=0.05, basis_seed=0)
     ds = jb.VectorDataset(x)
     t0 = time.perf_counter()
     g = jb.build(ds, jb.BuildParams(degree_cap=32, build_beam_width=64, alpha=1.2))
@@ -103,7 +105,7 @@ def c3(args):
     q_dev = torch.from_numpy(q).cuda()
     gi, gd = bench._gt_device(ds.device().x, q_dev, 100)
     gt = jb.GroundTruth(gi.cpu().numpy(), gd.cpu().numpy().astype(np.float32))
-    out = {"config": "c3", "n": n, "dims": 960, "bits": 4, "build_s": round(t_build, 2),
+    out = {"config": "c3", "n": n, "dims": 960, "d_int": dint, "bits": 4, "build_s": round(t_build, 2),
            "inserts_per_s": round(n / t_build, 1), "rabitq_fit_s": round(t_fit, 3),
            "bytes_per_vector": {"f32": 3840, "rabitq_record": int(jb._lib.lib().jb_rabitq_record_bytes(960, 4))},
            "sweep": []}
@@ -166,9 +168,51 @@ def c4(args):
             "final_recall_at_10_L64": round(jb.recall_at_k(ids.cpu().numpy(), gt, 10), 4)}
 
 
+def c5(args):
+    """One shard of the 100M x 96 index at 8 GPUs (12.5M rows): the per-GPU work of
+    the weak-scaling configuration, built and searched on one B200. Exact and
+    RaBitQ-1 + rerank sweeps to recall@10 >= 0.95 against the shard's own exact GT."""
+    import torch
+
+    import paper_2601_07048_b200 as jb
+
+    n = args.n or 12_500_000
+    t0 = time.perf_counter()
+    x = jb.gen_lowrank(n, 96, seed=1, d_int=16, noise=0.05, basis_seed=0)
+    q = jb.gen_lowrank(10_000, 96, seed=1_000_003, d_int=16, noise=0.05, basis_seed=0)
+    t_gen = time.perf_counter() - t0
+    ds = jb.VectorDataset(x)
+    ds.device()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    g = jb.build(ds, jb.BuildParams(degree_cap=32, build_beam_width=64, alpha=1.2, max_batch=100_000))
+    torch.cuda.synchronize()
+    t_build = time.perf_counter() - t0
+    idx = jb.rabitq_fit(ds, bits=1, seed=1)
+    q_dev = torch.from_numpy(q).cuda()
+    gi, gd = bench._gt_device(ds.device().x, q_dev, 100)
+    gt = jb.GroundTruth(gi.cpu().numpy(), gd.cpu().numpy().astype(np.float32))
+    out = {"config": "c5-shard", "n": n, "dims": 96, "gen_s": round(t_gen, 1), "build_s": round(t_build, 2),
+           "inserts_per_s": round(n / t_build, 1), "hbm_bytes": {"vectors": n * 96 * 4, "graph": n * 32 * 4}}
+    for name, src, kw in (("exact", ds, {}), ("rabitq1_popcount_rerank", idx,
+                                               dict(rerank=True, estimator="popcount"))):
+        pts = []
+        for L in bench.SWEEP:
+            sp = jb.SearchParams(beam_width=L, k=10, **kw)
+            ms = _timed(lambda: jb.search_knn_batch_device(g, src, q_dev, sp, exact_data=ds), reps=3, warm=1)
+            ids, _ = jb.search_knn_batch_device(g, src, q_dev, sp, exact_data=ds)
+            r = jb.recall_at_k(ids.cpu().numpy(), gt, 10)
+            pts.append({"L": L, "recall": round(r, 4), "qps_device": round(10_000 / (ms / 1e3), 1)})
+            if r >= 0.95:
+                break
+        out[name] = pts
+    return out
+
+
 def main():
     p = argparse.ArgumentParser()
-    p.add_argument("config", choices=["c1", "c3", "c4"])
+    p.add_argument("config", choices=["c1", "c3", "c4", "c5"])
+    p.add_argument("--dint", type=int, default=0)
     p.add_argument("--n", type=int, default=0)
     p.add_argument("--total", type=int, default=0)
     p.add_argument("--out", default="")
@@ -176,7 +220,7 @@ def main():
     import torch
 
     torch.cuda.set_device(0)
-    res = {"c1": c1, "c3": c3, "c4": c4}[args.config](args)
+    res = {"c1": c1, "c3": c3, "c4": c4, "c5": c5}[args.config](args)
     line = json.dumps(res)
     print(line, flush=True)
     if args.out:

@@ -38,6 +38,7 @@ namespace jb {
 
 constexpr int WPB = 4;          // warps per block
 constexpr int MAX_CHUNKS = 4;   // neighbour slots per hop: R <= 32 * MAX_CHUNKS
+constexpr int COOP_MAX = 4;     // merge: warp-cooperative placement up to this many candidates
 
 struct SearchLayout {
     int q_off, beam_off, hash_off, newk_off, cid_off, stage_off, plane_off, bytes;
@@ -159,13 +160,16 @@ __device__ __forceinline__ float rabitq_estimate(const uint8_t* __restrict__ rec
 constexpr int FAST_QB = 6;   // default query bit-planes (template QB below)
 
 // planes: FAST_QB planes of `pw` words each (pw = nwords rounded up to 4, zero padded)
-template <int QB>
+// PW > 0: plane stride known at compile time (PW = 4 covers D <= 128 in one piece).
+template <int QB, int PW = 0>
 __device__ __forceinline__ float rabitq_dd_fast(const uint8_t* __restrict__ rec, uint4 first,
-                                               const uint32_t* __restrict__ planes, int pw, float lo, float delta) {
+                                               const uint32_t* __restrict__ planes, int pw_rt, float lo, float delta) {
+    const int pw = PW > 0 ? PW : pw_rt;
     int pc = 0;
     int acc[QB];
 #pragma unroll
     for (int b = 0; b < QB; ++b) acc[b] = 0;
+#pragma unroll
     for (int w0 = 0; w0 < pw; w0 += 4) {
         const uint4 c = w0 == 0 ? first : __ldg(reinterpret_cast<const uint4*>(rec + 4 * w0));
         pc += __popc(c.x) + __popc(c.y) + __popc(c.z) + __popc(c.w);
@@ -245,19 +249,48 @@ __device__ __forceinline__ int merge_into_beam(uint64_t* beam, int& bcount, int 
     const unsigned FULL = 0xFFFFFFFFu;
     const int lane = lane_id();
     if (key != UMAX && bcount == L && key >= key_mask(beam[L - 1])) key = UMAX;
-    int p = 0;
-    if (key != UMAX) {
-        p = lower_bound_masked(beam, bcount, key);
-        if (p < bcount && key_mask(beam[p]) == key) key = UMAX;
+    const uint32_t cm = __ballot_sync(FULL, key != UMAX);
+    if (cm == 0) return bcount;  // most hops: nothing beats the full beam
+    int p = 0, rank = 0;
+    uint32_t sm;
+    if (__popc(cm) <= COOP_MAX) {
+        // Few candidates (the common case): the whole warp locates each one in
+        // turn. Lane g holds the last key of beam group g (G = ceil(bcount/32)
+        // entries per group): popc(ballot(split < k)) counts the groups wholly
+        // below k, then lanes j < G compare k with that group's entries. Ranks
+        // among survivors and the equal-key dedupe come out of the same loop.
+        const int G = (bcount + 31) >> 5;
+        const int si = G * lane + G - 1;
+        const uint64_t split = si < bcount ? key_mask(beam[si]) : UMAX;
+        bool dup_mine = false;
+        for (uint32_t mm = cm; mm; mm &= mm - 1) {
+            const int t = __ffs(mm) - 1;
+            const uint64_t kt = shfl_u64(key, t);
+            const int g0 = G * __popc(__ballot_sync(FULL, split < kt));
+            const int e = g0 + lane;
+            const uint64_t ev = (lane < G && e < bcount) ? key_mask(beam[e]) : UMAX;
+            const int pt = g0 + __popc(__ballot_sync(FULL, ev < kt));
+            const bool dup = __ballot_sync(FULL, ev == kt) != 0;
+            if (!dup && kt < key) ++rank;
+            if (lane == t) { p = pt; dup_mine = dup; }
+        }
+        if (dup_mine) key = UMAX;
+        sm = __ballot_sync(FULL, key != UMAX);
+        if (sm == 0) return bcount;
+        if (key == UMAX) rank = 0;
+    } else {
+        if (key != UMAX) {
+            p = lower_bound_masked(beam, bcount, key);
+            if (p < bcount && key_mask(beam[p]) == key) key = UMAX;
+        }
+        sm = __ballot_sync(FULL, key != UMAX);
+        if (sm == 0) return bcount;
+        for (uint32_t mm = sm; mm; mm &= mm - 1) {
+            const int t = __ffs(mm) - 1;
+            rank += (shfl_u64(key, t) < key) ? 1 : 0;
+        }
     }
-    const uint32_t sm = __ballot_sync(FULL, key != UMAX);
-    if (sm == 0) return bcount;
     const int m2 = __popc(sm);
-    int rank = 0;
-    for (uint32_t mm = sm; mm; mm &= mm - 1) {
-        const int t = __ffs(mm) - 1;
-        rank += (shfl_u64(key, t) < key) ? 1 : 0;
-    }
     const int fs = p + rank;
     const bool live = key != UMAX && fs < L;
     if (live) atomicOr(&fmask[fs >> 5], 1u << (fs & 31));
@@ -450,7 +483,9 @@ beam_search_kernel(const jb_search_args a, const SearchLayout lay, int* __restri
                         const float2 m = (RB == 32) ? make_float2(__uint_as_float(rc1.x), __uint_as_float(rc1.y))
                                                     : __ldg(reinterpret_cast<const float2*>(rec + meta_off));
                         if (SRC == JB_SRC_RABITQ_FAST) {
-                            const float dd = rabitq_dd_fast<FAST_QB>(rec, rc0, planes, nwords, qlo, qdelta);
+                            const float dd = nwords == 4
+                                                 ? rabitq_dd_fast<FAST_QB, 4>(rec, rc0, planes, 4, qlo, qdelta)
+                                                 : rabitq_dd_fast<FAST_QB>(rec, rc0, planes, nwords, qlo, qdelta);
                             const float est = (qadd + m.x) + m.y * (dd - qsumq);
                             d = est > 0.0f ? est : 0.0f;
                         } else {
