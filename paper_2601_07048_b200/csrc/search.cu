@@ -244,12 +244,27 @@ __device__ __forceinline__ int first_unexpanded(const uint64_t* beam, int s, int
 // entries are then gathered top-down, one 32-entry chunk per step: output j
 // (not a survivor slot) takes old entry j - #survivor slots below j, a popcount
 // of the mask. Returns the smallest insertion position (bcount if none).
+#ifdef JB_MERGE_STATS
+// dev builds only (-DJB_MERGE_STATS): [0..32] histogram of candidates per merge
+// after the beam-worst filter, [33..65] of evaluated candidates per merge.
+__device__ unsigned long long g_merge_stats[66];
+#endif
+
 __device__ __forceinline__ int merge_into_beam(uint64_t* beam, int& bcount, int L, uint64_t key,
                                                uint32_t* fmask) {
     const unsigned FULL = 0xFFFFFFFFu;
     const int lane = lane_id();
+#ifdef JB_MERGE_STATS
+    const int nin = __popc(__ballot_sync(FULL, key != UMAX));
+#endif
     if (key != UMAX && bcount == L && key >= key_mask(beam[L - 1])) key = UMAX;
     const uint32_t cm = __ballot_sync(FULL, key != UMAX);
+#ifdef JB_MERGE_STATS
+    if (lane == 0) {
+        atomicAdd(&g_merge_stats[__popc(cm)], 1ull);
+        atomicAdd(&g_merge_stats[33 + nin], 1ull);
+    }
+#endif
     if (cm == 0) return bcount;  // most hops: nothing beats the full beam
     int p = 0, rank = 0;
     uint32_t sm;
@@ -658,6 +673,15 @@ static int launch_search(const jb_search_args& a, int hash_slots, cudaStream_t s
 using namespace jb;
 
 extern "C" {
+
+#ifdef JB_MERGE_STATS
+int jb_debug_merge_stats(unsigned long long* out) {
+    JB_CUDA(cudaMemcpyFromSymbol(out, g_merge_stats, sizeof(unsigned long long) * 66));
+    static const unsigned long long zero[66] = {};
+    JB_CUDA(cudaMemcpyToSymbol(g_merge_stats, zero, sizeof(zero)));
+    return JB_OK;
+}
+#endif
 
 int jb_beam_search(const jb_search_args* args, void* stream) {
     JB_CHECK_ARG(args != nullptr, "jb_beam_search: null args");
