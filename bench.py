@@ -189,10 +189,14 @@ def _setup(args, world, rank):
     # untimed warm-up build (first-call kernel attributes, allocator growth)
     jb.build(jb.VectorDataset(x[: min(args.n, 50_000)]), params)
     torch.cuda.synchronize()
+    from paper_2601_07048_b200 import build as jbuild
+
+    jbuild.WORK[:] = 0
     t0 = time.perf_counter()
     graph = jb.build(ds, params)
     torch.cuda.synchronize()
     t_build = time.perf_counter() - t0
+    work = dict(zip(jbuild.WORK_FIELDS, (int(v) for v in jbuild.WORK)))
     t0 = time.perf_counter()
     idx = jb.rabitq_fit(ds, bits=args.bits, seed=1)
     torch.cuda.synchronize()
@@ -215,7 +219,26 @@ def _setup(args, world, rank):
     log(f"gen {t_gen:.1f}s build {t_build:.1f}s ({args.n / t_build:.0f} inserts/s) fit {t_fit:.2f}s")
     gt = jb.measure.GroundTruth(gt_i.cpu().numpy().astype(np.int64), gt_d.cpu().numpy().astype(np.float32))
     return dict(jb=jb, x=x, q=q, ds=ds, graph=graph, idx=idx, q_dev=q_dev, gt=gt, shard_start=shard_start,
-                t_gen=t_gen, t_build=t_build, t_fit=t_fit, params=params)
+                t_gen=t_gen, t_build=t_build, t_fit=t_fit, params=params, work=work)
+
+
+def _insert_roofline(S, args, peak):
+    """Algorithmic bytes of the bulk build (SURVEY.md §8d C4 formula, from the
+    build's own work counters) over its wall time. Phase 1: hops x (4R+4)
+    adjacency + evals x (4D+4) rows + 4D per new row; phase 2: one row per prune
+    candidate; phase 3: each touched target's R existing rows plus one row per
+    reverse triple (upper bound: ~all targets re-prune at R=32); row writes
+    4R per new vertex and touched target. Repair scans are not counted."""
+    w, D, R = S["work"], args.dim, 32
+    row = 4 * D + 4
+    b = (w["search_hops"] * (4 * R + 4) + w["search_evals"] * row + args.n * 4 * D
+         + w["prune_candidates"] * row
+         + (w["merge_targets"] * R + w["reverse_triples"]) * row
+         + (args.n + w["merge_targets"]) * 4 * R)
+    gbs = b / S["t_build"] / 1e9
+    return {"bound": "hbm", "achieved": round(gbs, 1), "peak": peak, "unit": "GB/s", "frac": round(gbs / peak, 4),
+            "alg_bytes": int(b), "alg_bytes_per_insert": round(b / args.n, 1), "work": w,
+            "timed": "whole bulk build (wall clock, synchronized)", "traffic": None}
 
 
 def _search_fn(S, world, L, k, est="reference"):
@@ -566,7 +589,8 @@ def main():
                       "rerank": round(T["rerank_ms"], 4),
                       "note": "each kernel alone on one stream over the full batch (the step runs two lanes)"},
         "build": {"inserts_per_s": round(args.n / S["t_build"], 1), "build_s": round(S["t_build"], 2),
-                  "rabitq_fit_s": round(S["t_fit"], 3), "gen_s": round(S["t_gen"], 2)},
+                  "rabitq_fit_s": round(S["t_fit"], 3), "gen_s": round(S["t_gen"], 2),
+                  "roofline": _insert_roofline(S, args, peak)},
         "estimators": {e: {"L": runs[e][0], "value": round(runs[e][3], 1),
                            "recall_at_10": next(p["recall"] for p in cal[e][1] if p["L"] == runs[e][0]),
                            "search_kernel_ms": round(runs[e][2]["search_ms"], 4)} for e in runs},

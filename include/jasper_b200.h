@@ -192,7 +192,11 @@ typedef struct jb_insert_args {
     /* outputs (host) */
     int64_t* entry_point_out_host; /* entry point after the batch            */
     int64_t* bridges_out_host;     /* bridges added by connectivity repair   */
-    int32_t* stats_out_host;       /* [8] diagnostics, may be NULL           */
+    int64_t* stats_out_host;       /* [8] work counters of the batch, added to
+                                    * (may be NULL): [0] phase-1 hops, [1] phase-1
+                                    * distance evals, [2] phase-2 prune candidates,
+                                    * [3] phase-3 touched targets, [4] reverse
+                                    * triples, [5] repair bridges                 */
 } jb_insert_args;
 
 /* One three-phase batch: search -> prune + reverse triples -> grouped merge,

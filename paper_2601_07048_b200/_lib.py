@@ -47,7 +47,7 @@ class InsertArgs(C.Structure):
         ("data", p), ("data_norms", p), ("dims", i32), ("count", i64),
         ("build_beam_width", i32), ("alpha", f64), ("always_prune", i32), ("reverse_all_visited", i32),
         ("start", i64), ("stop", i64), ("entry_point", i64),
-        ("entry_point_out_host", p), ("bridges_out_host", p), ("stats_out_host", p),
+        ("entry_point_out_host", p), ("bridges_out_host", p), ("stats_out_host", p),  # int64 [8]
     ]
 
 

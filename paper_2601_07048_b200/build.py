@@ -120,11 +120,19 @@ def _args(graph: GraphIndex, ds, params: BuildParams, start: int, stop: int):
     return a
 
 
+# Work counters accumulated over batch_insert calls (jb_insert_args.stats_out_host):
+# phase-1 hops / distance evals, phase-2 prune candidates, phase-3 touched targets,
+# reverse triples, repair bridges. Read by bench.py for the insert roofline.
+WORK_FIELDS = ("search_hops", "search_evals", "prune_candidates", "merge_targets", "reverse_triples", "bridges")
+WORK = np.zeros(8, dtype=np.int64)
+
+
 def _run(fn, graph: GraphIndex, a) -> int:
     entry = np.zeros(1, dtype=np.int64)
     bridges = np.zeros(1, dtype=np.int64)
     a.entry_point_out_host = entry.ctypes.data
     a.bridges_out_host = bridges.ctypes.data
+    a.stats_out_host = WORK.ctypes.data
     try:
         _lib.check(fn(_lib.C.byref(a), _lib.stream_ptr()))
     finally:

@@ -767,6 +767,24 @@ static int repair(const jb_insert_args& a, int64_t n_active, int64_t entry, cuda
     return JB_OK;
 }
 
+// out[0] += sum(v[0..n)), out[1] += sum(w[0..n)) (work counters; int64 totals)
+__global__ void sum2_kernel(const int32_t* __restrict__ v, const int32_t* __restrict__ w, int64_t n,
+                            unsigned long long* __restrict__ out) {
+    unsigned long long a = 0, b = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        a += (unsigned)v[i];
+        b += (unsigned)w[i];
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        a += __shfl_xor_sync(0xFFFFFFFFu, a, o);
+        b += __shfl_xor_sync(0xFFFFFFFFu, b, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(out, a);
+        atomicAdd(out + 1, b);
+    }
+}
+
 // JB_PROFILE=1: per-batch phase timings on stderr (stream events; diagnostics only)
 struct PhaseTimer {
     bool on = false;
@@ -863,6 +881,10 @@ int jb_batch_insert(const jb_insert_args* args, void* stream) {
         rc = repair(a, a.stop, entry, st, &bridges);
         if (a.entry_point_out_host) *a.entry_point_out_host = entry;
         if (a.bridges_out_host) *a.bridges_out_host = bridges;
+        if (a.stats_out_host) {
+            a.stats_out_host[2] += nb * (nb - 1);  // seed: every vertex prunes over all others
+            a.stats_out_host[5] += bridges;
+        }
         return rc;
     }
 
@@ -901,6 +923,15 @@ int jb_batch_insert(const jb_insert_args* args, void* stream) {
         cap = hmax;  // re-run with an exact-size trace buffer (rare)
     }
 
+    unsigned long long hwork[2] = {0, 0};
+    if (a.stats_out_host) {  // phase-1 hops and evals (phase 2 prunes over the same hop traces)
+        BALLOC(work, unsigned long long, 2);
+        JB_CUDA(cudaMemsetAsync(work, 0, 2 * sizeof(unsigned long long), st));
+        sum2_kernel<<<std::max(1, std::min<int>((int)((nb + 255) / 256), 4 * sm_count_current())), 256, 0, st>>>(
+            hops, evals, nb, work);
+        JB_LAUNCH_CHECK();
+        JB_CUDA(cudaMemcpyAsync(hwork, work, sizeof(hwork), cudaMemcpyDeviceToHost, st));
+    }
     pt.mark("search");
     // ---- phase 2: activate, prune each new vertex, emit reverse triples ----
     const int W = a.reverse_all_visited ? cap : R;
@@ -980,6 +1011,15 @@ int jb_batch_insert(const jb_insert_args* args, void* stream) {
     if (pt.on) fprintf(stderr, "[jb]   bridges %lld\n", (long long)bridges);
     if (a.entry_point_out_host) *a.entry_point_out_host = entry;
     if (a.bridges_out_host) *a.bridges_out_host = bridges;
+    if (a.stats_out_host) {
+        int64_t* w = a.stats_out_host;
+        w[0] += (int64_t)hwork[0];
+        w[1] += (int64_t)hwork[1];
+        w[2] += (int64_t)hwork[0];  // each new vertex prunes over its visited trace
+        w[3] += hseg;
+        w[4] += ntri;
+        w[5] += bridges;
+    }
     return rc;
 }
 

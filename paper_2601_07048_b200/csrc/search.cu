@@ -38,7 +38,10 @@ namespace jb {
 
 constexpr int WPB = 4;          // warps per block
 constexpr int MAX_CHUNKS = 4;   // neighbour slots per hop: R <= 32 * MAX_CHUNKS
-constexpr int COOP_MAX = 4;     // merge: warp-cooperative placement up to this many candidates
+#ifndef JB_COOP_MAX
+#define JB_COOP_MAX 2
+#endif
+constexpr int COOP_MAX = JB_COOP_MAX;  // merge: warp-cooperative placement up to this many candidates
 
 struct SearchLayout {
     int q_off, beam_off, hash_off, newk_off, cid_off, stage_off, plane_off, bytes;
