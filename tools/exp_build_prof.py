@@ -7,7 +7,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 
 import paper_2601_07048_b200 as jb
-from paper_2601_07048_b200 import build as jbuild
+import importlib; jbuild = importlib.import_module("paper_2601_07048_b200.build")
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 1_000_000
 d = int(sys.argv[2]) if len(sys.argv) > 2 else 128

@@ -5,4 +5,4 @@ timeout 1200 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&
 tail -5 gpurun_out/pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo smoke rc=$?
 tail -3 gpurun_out/smoke.log
-bash profiles/profile_round.sh r01b
+bash profiles/profile_round.sh ${1:-r01}
