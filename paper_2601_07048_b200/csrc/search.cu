@@ -160,7 +160,13 @@ __device__ __forceinline__ float rabitq_estimate(const uint8_t* __restrict__ rec
 // layout as the packed 1-bit codes), so
 //   <u, q> ~= lo * popc(u) + delta * sum_b 2^b popc(u & plane_b)
 // replaces the 128 ordered float adds with 4 * (QB + 1) popcounts at D = 128.
-constexpr int FAST_QB = 6;   // default query bit-planes (template QB below)
+#ifndef JB_FAST_QB
+#define JB_FAST_QB 6
+#endif
+#ifndef JB_FAST_MINB
+#define JB_FAST_MINB 10
+#endif
+constexpr int FAST_QB = JB_FAST_QB;   // query bit-planes of the popcount estimator
 
 // planes: FAST_QB planes of `pw` words each (pw = nwords rounded up to 4, zero padded)
 // PW > 0: plane stride known at compile time (PW = 4 covers D <= 128 in one piece).
@@ -339,6 +345,95 @@ __device__ __forceinline__ int merge_into_beam(uint64_t* beam, int& bcount, int 
     return p0;
 }
 
+// Per-query state shared by the two search kernels (pointers into the warp's smem).
+struct QueryCtx {
+    const float* qv;          // query (EXACT) or rotated query (RaBitQ), D f32
+    const uint32_t* planes;   // popcount query bit-planes
+    int32_t* cid;             // EXACT: compacted new ids, 32
+    float* stage;             // EXACT: staged rows, 32 x sstride
+    float qadd, qsumq, qlo, qdelta;
+    int nwords, meta_off;
+};
+
+// One neighbour per lane (nb = -1: none): visited check, then the distance of
+// every new neighbour, returned as the lane's candidate key (UMAX = none; EXACT
+// compacts the new ids to lanes 0..nnew-1). Adds the new count to `evals`.
+template <int SRC, int BITS, bool ALIGNED>
+__device__ __forceinline__ uint64_t eval_chunk(const jb_search_args& a, const SearchLayout& lay, const QueryCtx& c,
+                                               uint32_t* tab, int nb, int& evals, int& lossy) {
+    const unsigned FULL = 0xFFFFFFFFu;
+    const int lane = lane_id();
+    const int D = a.dims;
+    const int RB = a.record_bytes;
+    // RaBitQ: issue the candidate's record loads before the visited check
+    uint4 rc0 = make_uint4(0, 0, 0, 0), rc1 = make_uint4(0, 0, 0, 0);
+    if (SRC != JB_SRC_EXACT && nb >= 0) {
+        const uint8_t* rec = a.records + (size_t)nb * RB;
+        rc0 = __ldg(reinterpret_cast<const uint4*>(rec));
+        if (RB == 32) rc1 = __ldg(reinterpret_cast<const uint4*>(rec + 16));
+    }
+    bool isnew = false;
+    uint32_t* slot = nullptr;
+    if (nb >= 0) isnew = visit(tab, lay.hbits, (uint32_t)nb, lossy, slot);
+    __syncwarp();
+    // two lanes may have claimed the same empty way: the loser's id is
+    // forgotten (safe, but it may be re-evaluated later -> flag it)
+    if (slot != nullptr && *slot != (uint32_t)nb) lossy = 1;
+    const uint32_t nm = __ballot_sync(FULL, isnew);
+    const int nnew = __popc(nm);
+    if (nnew == 0) return UMAX;
+    evals += nnew;
+
+    float d = 0.0f;
+    int myid = 0;
+    if (SRC == JB_SRC_EXACT) {
+        if (isnew) c.cid[__popc(nm & lanemask_lt())] = nb;
+        __syncwarp();
+        myid = (lane < nnew) ? c.cid[lane] : 0;
+        Acc4 acc; acc.zero();
+        for (int e0 = 0; e0 < D; e0 += lay.chunk) {
+            const int clen = min(lay.chunk, D - e0);
+            if (ALIGNED) {
+                const int nv = clen >> 2;
+                for (int j = 0; j < nnew; ++j) {
+                    const float* src = a.data + (size_t)c.cid[j] * D + e0;
+                    float* dst = c.stage + j * lay.sstride;
+                    for (int f = lane; f < nv; f += 32) cp_async16(dst + 4 * f, src + 4 * f);
+                }
+            } else {
+                for (int j = 0; j < nnew; ++j) {
+                    const float* src = a.data + (size_t)c.cid[j] * D + e0;
+                    float* dst = c.stage + j * lay.sstride;
+                    for (int f = lane; f < clen; f += 32) cp_async4(dst + f, src + f);
+                }
+            }
+            cp_async_wait_all();
+            __syncwarp();
+            if (lane < nnew) a1_range<ALIGNED, false>(acc, c.stage + lane * lay.sstride - e0, c.qv, e0, e0 + clen);
+            __syncwarp();
+        }
+        if (lane < nnew) d = exact_from_dot(__ldg(a.data_norms + myid), acc.reduce(), c.qadd);
+    } else {
+        // the lane that owns the neighbour evaluates it from its registers
+        myid = nb;
+        if (isnew) {
+            const uint8_t* rec = a.records + (size_t)myid * RB;
+            const float2 m = (RB == 32) ? make_float2(__uint_as_float(rc1.x), __uint_as_float(rc1.y))
+                                        : __ldg(reinterpret_cast<const float2*>(rec + c.meta_off));
+            if (SRC == JB_SRC_RABITQ_FAST) {
+                const float dd = c.nwords == 4 ? rabitq_dd_fast<FAST_QB, 4>(rec, rc0, c.planes, 4, c.qlo, c.qdelta)
+                                               : rabitq_dd_fast<FAST_QB>(rec, rc0, c.planes, c.nwords, c.qlo, c.qdelta);
+                const float est = (c.qadd + m.x) + m.y * (dd - c.qsumq);
+                d = est > 0.0f ? est : 0.0f;
+            } else {
+                d = rabitq_finish(rabitq_dd<BITS>(rec, rc0, c.qv, D), m, c.qadd, c.qsumq);
+            }
+        }
+    }
+    const bool have = (SRC == JB_SRC_EXACT) ? (lane < nnew) : isnew;
+    return have ? pack_key(d, (uint32_t)myid) : UMAX;
+}
+
 template <int SRC, int BITS, bool ALIGNED, int CH, int MINB>
 __global__ void __launch_bounds__(WPB * 32, MINB)
 beam_search_kernel(const jb_search_args a, const SearchLayout lay, int* __restrict__ counter) {
@@ -380,6 +475,7 @@ beam_search_kernel(const jb_search_args a, const SearchLayout lay, int* __restri
         __syncwarp();
         float qlo = 0.0f, qdelta = 0.0f;
         if (SRC == JB_SRC_RABITQ_FAST) build_planes<FAST_QB>(qv, D, planes, qlo, qdelta);
+        const QueryCtx qc{qv, planes, cid, stage, qadd, qsumq, qlo, qdelta, nwords, meta_off};
 
         int lossy = 0;
         if (lane == 0) {
@@ -442,77 +538,7 @@ beam_search_kernel(const jb_search_args a, const SearchLayout lay, int* __restri
 #pragma unroll
             for (int c = 0; c < CH; ++c) {
                 if (c * 32 >= R) break;
-                const int nb = nbv[c];
-                // RaBitQ: issue the candidate's record loads before the visited check
-                uint4 rc0 = make_uint4(0, 0, 0, 0), rc1 = make_uint4(0, 0, 0, 0);
-                if (SRC != JB_SRC_EXACT && nb >= 0) {
-                    const uint8_t* rec = a.records + (size_t)nb * RB;
-                    rc0 = __ldg(reinterpret_cast<const uint4*>(rec));
-                    if (RB == 32) rc1 = __ldg(reinterpret_cast<const uint4*>(rec + 16));
-                }
-                bool isnew = false;
-                uint32_t* slot = nullptr;
-                if (nb >= 0) isnew = visit(tab, lay.hbits, (uint32_t)nb, lossy, slot);
-                __syncwarp();
-                // two lanes may have claimed the same empty way: the loser's id is
-                // forgotten (safe, but it may be re-evaluated later -> flag it)
-                if (slot != nullptr && *slot != (uint32_t)nb) lossy = 1;
-                const uint32_t nm = __ballot_sync(FULL, isnew);
-                const int nnew = __popc(nm);
-                if (nnew == 0) continue;
-                evals += nnew;
-
-                // ---- distances, one candidate per lane ----
-                float d = 0.0f;
-                int myid = 0;
-                if (SRC == JB_SRC_EXACT) {
-                    if (isnew) cid[__popc(nm & lanemask_lt())] = nb;
-                    __syncwarp();
-                    myid = (lane < nnew) ? cid[lane] : 0;
-                    Acc4 acc; acc.zero();
-                    for (int e0 = 0; e0 < D; e0 += lay.chunk) {
-                        const int clen = min(lay.chunk, D - e0);
-                        if (ALIGNED) {
-                            const int nv = clen >> 2;
-                            for (int j = 0; j < nnew; ++j) {
-                                const float* src = a.data + (size_t)cid[j] * D + e0;
-                                float* dst = stage + j * lay.sstride;
-                                for (int f = lane; f < nv; f += 32) cp_async16(dst + 4 * f, src + 4 * f);
-                            }
-                        } else {
-                            for (int j = 0; j < nnew; ++j) {
-                                const float* src = a.data + (size_t)cid[j] * D + e0;
-                                float* dst = stage + j * lay.sstride;
-                                for (int f = lane; f < clen; f += 32) cp_async4(dst + f, src + f);
-                            }
-                        }
-                        cp_async_wait_all();
-                        __syncwarp();
-                        if (lane < nnew)
-                            a1_range<ALIGNED, false>(acc, stage + lane * lay.sstride - e0, qv, e0, e0 + clen);
-                        __syncwarp();
-                    }
-                    if (lane < nnew) d = exact_from_dot(__ldg(a.data_norms + myid), acc.reduce(), qadd);
-                } else {
-                    // the lane that owns the neighbour evaluates it from its registers
-                    myid = nb;
-                    if (isnew) {
-                        const uint8_t* rec = a.records + (size_t)myid * RB;
-                        const float2 m = (RB == 32) ? make_float2(__uint_as_float(rc1.x), __uint_as_float(rc1.y))
-                                                    : __ldg(reinterpret_cast<const float2*>(rec + meta_off));
-                        if (SRC == JB_SRC_RABITQ_FAST) {
-                            const float dd = nwords == 4
-                                                 ? rabitq_dd_fast<FAST_QB, 4>(rec, rc0, planes, 4, qlo, qdelta)
-                                                 : rabitq_dd_fast<FAST_QB>(rec, rc0, planes, nwords, qlo, qdelta);
-                            const float est = (qadd + m.x) + m.y * (dd - qsumq);
-                            d = est > 0.0f ? est : 0.0f;
-                        } else {
-                            d = rabitq_finish(rabitq_dd<BITS>(rec, rc0, qv, D), m, qadd, qsumq);
-                        }
-                    }
-                }
-                const bool have = (SRC == JB_SRC_EXACT) ? (lane < nnew) : isnew;
-                const uint64_t key = have ? pack_key(d, (uint32_t)myid) : UMAX;
+                const uint64_t key = eval_chunk<SRC, BITS, ALIGNED>(a, lay, qc, tab, nbv[c], evals, lossy);
                 const int p0 = merge_into_beam(beam, bcount, L, key, fmask);
                 s_min = min(s_min, p0);
                 p_ins = p0;
@@ -544,6 +570,7 @@ beam_search_kernel(const jb_search_args a, const SearchLayout lay, int* __restri
         __syncwarp();
     }
 }
+
 
 // ---- exact rerank of the frontier (search.py:318-320, 375-382) -----------
 // One warp per query: stage up to 32 frontier rows at a time, lane j computes
@@ -632,25 +659,41 @@ static SearchLayout make_layout(int src, int D, int L, int hash_slots, int qb) {
     return s;
 }
 
-template <int SRC, int BITS, bool ALIGNED, int CH, int MINB>
-static int launch_search_inst(const jb_search_args& a, int hash_slots, cudaStream_t st) {
-    SearchLayout lay = make_layout(SRC, a.dims, a.beam_width, hash_slots, FAST_QB);
-    auto kern = beam_search_kernel<SRC, BITS, ALIGNED, CH, MINB>;
+using SearchKernel = void (*)(const jb_search_args, const SearchLayout, int*);
+
+// Occupancy per (kernel, smem size) is cached: the attribute/occupancy queries
+// cost more than the launch itself for small batches.
+static int launch_search_kernel(SearchKernel kern, const SearchLayout& lay, const jb_search_args& a, int minb,
+                                cudaStream_t st) {
     const int smem = lay.bytes * WPB;
     JB_CHECK_ARG(smem <= 227 * 1024, "beam search: per-block shared memory %d B exceeds 227 KB", smem);
-    // occupancy per (instantiation, smem size), cached: the attribute/occupancy
-    // queries cost more than the launch itself for small batches
-    static thread_local int cached_smem = -1, cached_per_sm = 0, cached_dev = -1;
+    // the smem attribute only ever grows per (kernel, device): lowering it would
+    // invalidate a cached larger configuration of the same kernel
+    struct Entry { SearchKernel k; int smem, dev, per_sm; };
+    struct Attr { SearchKernel k; int dev, smem; };
+    static thread_local Entry cache[16] = {};
+    static thread_local Attr attrs[64] = {};
+    static thread_local int next = 0, nattr = 0;
     int dev = 0;
     JB_CUDA(cudaGetDevice(&dev));
-    if (cached_smem != smem || cached_dev != dev) {
-        JB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        JB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cached_per_sm, kern, WPB * 32, smem));
-        cached_smem = smem;
-        cached_dev = dev;
+    int per_sm = 0;
+    for (const Entry& e : cache)
+        if (e.k == kern && e.smem == smem && e.dev == dev) per_sm = e.per_sm;
+    if (per_sm == 0) {
+        Attr* at = nullptr;
+        for (int i = 0; i < nattr; ++i)
+            if (attrs[i].k == kern && attrs[i].dev == dev) at = &attrs[i];
+        if (at == nullptr || at->smem < smem) {
+            JB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+            if (at == nullptr && nattr < 64) at = &attrs[nattr++];
+            if (at != nullptr) *at = Attr{kern, dev, smem};
+        }
+        JB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, WPB * 32, smem));
+        JB_CHECK_ARG(per_sm >= 1, "beam search: kernel does not fit on an SM");
+        cache[next] = Entry{kern, smem, dev, per_sm};
+        next = (next + 1) % 16;
     }
-    const int per_sm = cached_per_sm;
-    JB_CHECK_ARG(per_sm >= 1, "beam search: kernel does not fit on an SM");
+    (void)minb;
     int64_t need = (a.nq + WPB - 1) / WPB;
     int grid = (int)std::min<int64_t>(need, (int64_t)per_sm * sm_count_current());
     Scratch ctr;
@@ -661,14 +704,16 @@ static int launch_search_inst(const jb_search_args& a, int hash_slots, cudaStrea
     return JB_OK;
 }
 
-// R <= 32: one neighbour chunk per hop (single merge, no rescan of the beam).
-// Blocks/SM: the popcount kernel is issue-bound and gains from 10 resident
-// blocks (48 registers, no spills); the float estimators keep 8.
+// R <= 32: one neighbour chunk per hop (single merge, no rescan of the beam);
+// MAX_CHUNKS for wider rows. Blocks/SM: the popcount kernel is issue-bound and
+// gains from 10 resident blocks; the float estimators keep 8.
 template <int SRC, int BITS, bool ALIGNED>
 static int launch_search(const jb_search_args& a, int hash_slots, cudaStream_t st) {
-    constexpr int MINB = SRC == JB_SRC_RABITQ_FAST ? 10 : 8;
-    if (a.degree_cap <= 32) return launch_search_inst<SRC, BITS, ALIGNED, 1, MINB>(a, hash_slots, st);
-    return launch_search_inst<SRC, BITS, ALIGNED, MAX_CHUNKS, 8>(a, hash_slots, st);
+    constexpr int MINB = SRC == JB_SRC_RABITQ_FAST ? JB_FAST_MINB : 8;
+    const int L = a.beam_width;
+    const SearchLayout lay = make_layout(SRC, a.dims, L, hash_slots, FAST_QB);
+    if (a.degree_cap <= 32) return launch_search_kernel(beam_search_kernel<SRC, BITS, ALIGNED, 1, MINB>, lay, a, MINB, st);
+    return launch_search_kernel(beam_search_kernel<SRC, BITS, ALIGNED, MAX_CHUNKS, 8>, lay, a, 8, st);
 }
 
 }  // namespace jb

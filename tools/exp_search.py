@@ -43,6 +43,6 @@ def t_search(L, est, hs=0, reps=7):
 
 for L in [int(v) for v in sys.argv[1:]] or (96, 112, 120, 128):
     for est in ("reference", "popcount"):
-        for hs in (0, 512, 1024):
+        for hs in [int(v) for v in os.environ.get("JB_EXP_HS", "0,512,1024").split(",")]:
             ms, r = t_search(L, est, hs)
             print(f"{est:9s} L={L} hash {hs:5d} {ms:7.3f} ms  {10000 / ms / 1e3:6.2f} MQPS recall {r:.4f}", flush=True)
