@@ -197,6 +197,8 @@ typedef struct jb_insert_args {
                                     * distance evals, [2] phase-2 prune candidates,
                                     * [3] phase-3 touched targets, [4] reverse
                                     * triples, [5] repair bridges                 */
+    int64_t active_count;          /* jb_refine_batch: vertices visible to the
+                                    * search (0 => stop); ignored elsewhere     */
 } jb_insert_args;
 
 /* One three-phase batch: search -> prune + reverse triples -> grouped merge,
@@ -205,6 +207,14 @@ typedef struct jb_insert_args {
  * _seed_batch (246-266), _merge_reverse_edges (269-293) and
  * _repair_connectivity (154-224). Synchronizes `stream`. */
 int jb_batch_insert(const jb_insert_args* args, void* stream);
+
+/* One batch of the two_pass refinement (_refine_pass, build.py:351-386): search
+ * rows [start, stop) on the active graph (active_count vertices), prune each
+ * vertex over its visited trace (itself excluded) plus the current neighbours
+ * missing from the trace at the final alpha, rewrite its row, then the grouped
+ * reverse-edge merge. The caller runs jb_repair_connectivity after the last
+ * batch, as the reference does. Synchronizes `stream`. */
+int jb_refine_batch(const jb_insert_args* args, void* stream);
 
 /* Connectivity repair only (after the entry point moves, build.py:415-418). */
 int jb_repair_connectivity(const jb_insert_args* args, void* stream);

@@ -6,6 +6,7 @@
   * reverse-edge buffer sorted by (target, dist, source)      build.py:65-102
   * seed batch, 3-phase batch insert, group merge             build.py:246-348
   * connectivity repair (BFS + nearest-donor bridges)         build.py:137-224
+  * two_pass refinement (search + prune at the final alpha)   build.py:351-386
   * build schedule (R+1 doubling, entry -> medoid)            build.py:389-424
   * insert_stream chunking                                    build.py:427-447
 
@@ -186,6 +187,12 @@ def batch_insert(g: Graph, x: np.ndarray, start: int, stop: int, R: int, L: int,
         tgt.append(np.asarray(e_ids, dtype=np.int64))
         srcs.append(np.full(len(e_ids), v, dtype=np.int64))
         dd.append(np.asarray(e_d, dtype=np.float64))
+    merge_reverse(g, tgt, srcs, dd, R, alpha, dist, always_prune)
+    return repair(g, dist)
+
+
+def merge_reverse(g: Graph, tgt, srcs, dd, R: int, alpha: float, dist, always_prune=False) -> None:
+    """build.py:269-293 over EdgeBuffer order (target, dist, source), build.py:65-102."""
     if tgt:
         t = np.concatenate(tgt)
         s = np.concatenate(srcs)
@@ -208,11 +215,37 @@ def batch_insert(g: Graph, x: np.ndarray, start: int, stop: int, R: int, L: int,
             kept, _ = robust_prune(target, np.concatenate([have.astype(np.int64), fs]),
                                    np.concatenate([np.asarray(hd, dtype=np.float64), fd]), alpha, R, dist)
             g.put(target, kept)
+
+
+def refine_pass(g: Graph, x: np.ndarray, R: int, L: int, alpha: float, max_batch: int,
+                dist: Pairwise | None = None, always_prune=False) -> int:
+    """build.py:351-386: per max_batch slice, search every active vertex on the
+    current graph, prune it over (visited - itself) + (current neighbours missing
+    from the trace) at the final alpha, then the grouped reverse merge; repair last."""
+    dist = dist or Pairwise(x)
+    n = g.active
+    for lo in range(0, n, max_batch):
+        hi = min(n, lo + max_batch)
+        found = beam_search(g.adj, g.active, g.entry, ExactSource(x, x[lo:hi]), hi - lo, L)
+        tgt, srcs, dd = [], [], []
+        for v, res in zip(range(lo, hi), found):
+            cur = g.nbrs(v)
+            extra = cur[~np.isin(cur, res.visited_ids)]
+            cand = np.concatenate([np.asarray(res.visited_ids, dtype=np.int64), extra.astype(np.int64)])
+            cd = np.concatenate([np.asarray(res.visited_dists, dtype=np.float64),
+                                 dist(v, extra) if extra.size else np.empty(0)])
+            keep = cand != v
+            kept, kd = robust_prune(v, cand[keep], cd[keep], alpha, R, dist)
+            g.put(v, kept)
+            tgt.append(np.asarray(kept, dtype=np.int64))
+            srcs.append(np.full(len(kept), v, dtype=np.int64))
+            dd.append(np.asarray(kd, dtype=np.float64))
+        merge_reverse(g, tgt, srcs, dd, R, alpha, dist, always_prune)
     return repair(g, dist)
 
 
-def build(x: np.ndarray, R: int, L: int, alpha: float, max_batch: int = 100_000) -> Graph:
-    """build.py:389-424 (two_pass=False)."""
+def build(x: np.ndarray, R: int, L: int, alpha: float, max_batch: int = 100_000, two_pass: bool = False) -> Graph:
+    """build.py:389-424 (two_pass: insertion passes at alpha=1, then refine_pass)."""
     x = np.ascontiguousarray(x, dtype=np.float32)
     n = x.shape[0]
     if n == 0:
@@ -223,12 +256,14 @@ def build(x: np.ndarray, R: int, L: int, alpha: float, max_batch: int = 100_000)
     size, pos = R + 1, 0
     while pos < n:
         stop = min(n, pos + size)
-        batch_insert(g, x, pos, stop, R, L, alpha, dist)
+        batch_insert(g, x, pos, stop, R, L, 1.0 if two_pass else alpha, dist)
         if m < g.active and g.entry != m:
             g.entry = m
             repair(g, dist)
         pos = stop
         size = min(size * 2, max_batch)
+    if two_pass:
+        refine_pass(g, x, R, L, alpha, max_batch, dist)
     return g
 
 

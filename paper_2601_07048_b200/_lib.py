@@ -48,6 +48,7 @@ class InsertArgs(C.Structure):
         ("build_beam_width", i32), ("alpha", f64), ("always_prune", i32), ("reverse_all_visited", i32),
         ("start", i64), ("stop", i64), ("entry_point", i64),
         ("entry_point_out_host", p), ("bridges_out_host", p), ("stats_out_host", p),  # int64 [8]
+        ("active_count", i64),
     ]
 
 
@@ -69,6 +70,7 @@ _SIGS = {
     "jb_rabitq_bind": (C.c_int, [p, i64, i32, i32, p, p, p, p, p, p]),
     "jb_batch_insert": (C.c_int, [C.POINTER(InsertArgs), p]),
     "jb_repair_connectivity": (C.c_int, [C.POINTER(InsertArgs), p]),
+    "jb_refine_batch": (C.c_int, [C.POINTER(InsertArgs), p]),
     "jb_robust_prune": (C.c_int, [p, p, i32, p, i64, p, p, p, f64, i32, p, p, p, p]),
     "jb_exact_knn": (C.c_int, [p, i64, i32, p, i64, i32, p, p, p]),
     "jb_merge_shard_topk": (C.c_int, [p, p, i32, i64, i32, p, p, p, p]),

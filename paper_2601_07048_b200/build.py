@@ -18,7 +18,7 @@ import os
 import sys
 import time
 import warnings
-from dataclasses import dataclass
+from dataclasses import dataclass, replace
 
 import numpy as np
 
@@ -176,8 +176,7 @@ def build(dataset, params: BuildParams, quantizer=None) -> GraphIndex:
     if ds.count == 0:
         raise ValueError("cannot build over an empty dataset")
     _check_supported(params, quantizer)
-    if params.two_pass:
-        raise NotImplementedError("two_pass refinement is not on the B200 path")
+    pass_params = replace(params, alpha=1.0) if params.two_pass else params
     prof = os.environ.get("JB_PROFILE") == "1"
     t0 = time.perf_counter()
     graph = GraphIndex(capacity=ds.count, degree_cap=params.degree_cap)
@@ -189,7 +188,7 @@ def build(dataset, params: BuildParams, quantizer=None) -> GraphIndex:
     while pos < ds.count:
         stop = min(ds.count, pos + size)
         t1 = time.perf_counter()
-        batch_insert(graph, ds, range(pos, stop), params)
+        batch_insert(graph, ds, range(pos, stop), pass_params)
         if global_medoid < graph.active_count and graph.entry_point != global_medoid:
             graph.entry_point = global_medoid
             _repair(graph, ds, params)
@@ -197,7 +196,24 @@ def build(dataset, params: BuildParams, quantizer=None) -> GraphIndex:
             print(f"[jb] batch wall [{pos}, {stop}) {1e3 * (time.perf_counter() - t1):.2f}ms", file=sys.stderr)
         pos = stop
         size = min(size * 2, params.max_batch)
+    if params.two_pass:
+        _refine_pass(graph, ds, params)
     return graph
+
+
+def _refine_pass(graph, dataset, params: BuildParams, quantizer=None) -> None:
+    """build.py:351-386: re-run search + prune for every active vertex at the final
+    alpha, in max_batch batches (one native call each), then connectivity repair."""
+    graph = as_graph(graph)
+    ds = as_dataset(dataset)
+    _check_supported(params, quantizer)
+    n = graph.active_count
+    for lo in range(0, n, params.max_batch):
+        hi = min(n, lo + params.max_batch)
+        a = _args(graph, ds, params, lo, hi)
+        a.active_count = n
+        _run(_lib.lib().jb_refine_batch, graph, a)
+    graph.last_bridges = _repair(graph, ds, params)
 
 
 def insert_stream(graph, dataset, new_range: range, params: BuildParams, quantizer=None) -> None:

@@ -247,6 +247,78 @@ phase2_kernel(const float* __restrict__ data, const float* __restrict__ norms, i
     }
 }
 
+// ---- two_pass refinement prune (build.py:362-381) --------------------------
+// Per vertex x of the batch: candidates = its visited trace without x itself, plus
+// its current neighbours missing from the trace (distances d(x, e) with x as the
+// pivot); robust prune at the final alpha; rewrite x's row; reverse triples for
+// the kept edges. Only warp x reads or writes row x, so the batch is parallel.
+__global__ void __launch_bounds__(BW * 32)
+refine_prune_kernel(const float* __restrict__ data, const float* __restrict__ norms, int D, int64_t start, int64_t nb,
+                    double alpha2, int R, const int32_t* __restrict__ hops, const int32_t* __restrict__ tids,
+                    const float* __restrict__ tdst, int cap, uint64_t* __restrict__ cand_all,
+                    int32_t* __restrict__ kept_ids, float* __restrict__ kept_d, int32_t* __restrict__ adj,
+                    int32_t* __restrict__ deg, uint32_t* __restrict__ tri_target, uint64_t* __restrict__ tri_key,
+                    int crows, int rstride, int32_t* __restrict__ ncand) {
+    extern __shared__ __align__(16) float sh[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int per_warp = ((D + 3) & ~3) + crows * rstride + ((crows + 3) & ~3);
+    float* srow = sh + (size_t)warp * per_warp;
+    float* rows = srow + ((D + 3) & ~3);
+    float* cn = rows + (size_t)crows * rstride;
+    const int64_t xi = (int64_t)blockIdx.x * BW + warp;
+    if (xi >= nb) return;
+    const uint32_t x = (uint32_t)(start + xi);
+    const int h = min(hops[xi], cap);
+    uint64_t* cand = cand_all + xi * (int64_t)(cap + R);
+    const int32_t* ti = tids + xi * (int64_t)cap;
+    const float* td = tdst + xi * (int64_t)cap;
+    const float* xr = data + (size_t)x * D;
+    for (int e = lane; e < D; e += 32) srow[e] = xr[e];
+    const float xn = norms[x];
+    int n = 0;
+    for (int b = 0; b < h; b += 32) {  // the visited trace, x excluded (keep = cand_ids != x)
+        const int j = b + lane;
+        const bool ok = j < h && (uint32_t)ti[j] != x;
+        const uint32_t m = __ballot_sync(0xFFFFFFFFu, ok);
+        if (ok) cand[n + __popc(m & lanemask_lt())] = pack_key(td[j], (uint32_t)ti[j]);
+        n += __popc(m);
+    }
+    __syncwarp();
+    const int hd = deg[x];
+    for (int b = 0; b < hd; b += 32) {  // extra = current[~isin(current, visited)]
+        const int e = b + lane;
+        bool extra = false;
+        int32_t id = -1;
+        if (e < hd) {
+            id = adj[(size_t)x * R + e];
+            extra = true;
+            for (int j = 0; j < h; ++j) extra &= (ti[j] != id);
+        }
+        const uint32_t m = __ballot_sync(0xFFFFFFFFu, extra);
+        if (extra) cand[n + __popc(m & lanemask_lt())] = pack_key(pair_dist(data, norms, D, srow, xn, (uint32_t)id), (uint32_t)id);
+        n += __popc(m);
+    }
+    __syncwarp();
+    if (lane == 0) ncand[xi] = n;
+    int32_t* ki = kept_ids + xi * R;
+    float* kd = kept_d + xi * R;
+    int k;
+    if (n <= crows) {
+        stage_rows(rows, rstride, cn, cand, n, data, norms, D);
+        k = warp_prune_staged(cand, n, alpha2, R, rows, rstride, cn, D, ki, kd);
+    } else {
+        k = warp_prune(cand, n, alpha2, R, data, norms, D, srow, ki, kd);
+    }
+    __syncwarp();
+    write_row(adj, deg, R, x, ki, k);
+    uint32_t* tt = tri_target + xi * R;
+    uint64_t* tk = tri_key + xi * R;
+    for (int j = lane; j < R; j += 32) {
+        tt[j] = j < k ? (uint32_t)ki[j] : NO_TARGET;
+        tk[j] = j < k ? (((uint64_t)__float_as_uint(kd[j]) << 32) | x) : UMAX;
+    }
+}
+
 // ---- batched standalone robust prune (graph.py:174-228) ----------------------
 __global__ void __launch_bounds__(BW * 32)
 prune_batch_kernel(const float* __restrict__ data, const float* __restrict__ norms, int D,
@@ -767,6 +839,102 @@ static int repair(const jb_insert_args& a, int64_t n_active, int64_t entry, cuda
     return JB_OK;
 }
 
+// Phase-1 search with visited-trace capture: queries are rows [q0, q0 + nq) of the
+// dataset, the graph shows `active` vertices. The trace capacity is generous
+// (8 B per slot); a longer trace re-runs the batch with an exact-size buffer.
+static int trace_search(const jb_insert_args& a, int64_t q0, int64_t nq, int64_t active, int64_t entry, Bufs& bufs,
+                        cudaStream_t st, int& cap, int32_t*& hops, int32_t*& evals, int32_t*& tids, float*& tdst) {
+    cudaError_t _ce;
+    const int R = a.degree_cap, D = a.dims, L = a.build_beam_width;
+    cap = std::max(4 * L, L + 512);
+    BALLOC(fk, uint64_t, (size_t)nq * L);
+    BALLOC(h, int32_t, nq);
+    BALLOC(ev, int32_t, nq);
+    BALLOC(flags, int32_t, nq);
+    hops = h;
+    evals = ev;
+    for (int attempt = 0; attempt < 2; ++attempt) {
+        tids = bufs.get<int32_t>((size_t)nq * cap, st, _ce); JB_CUDA(_ce);
+        tdst = bufs.get<float>((size_t)nq * cap, st, _ce); JB_CUDA(_ce);
+        jb_search_args s{};
+        s.adjacency = a.adjacency; s.degree_cap = R; s.active_count = active;
+        s.source = JB_SRC_EXACT; s.dims = D; s.data = a.data; s.data_norms = a.data_norms;
+        s.queries = a.data + (size_t)q0 * D; s.query_add = a.data_norms + q0;
+        s.nq = nq; s.starts = nullptr; s.start_vertex = entry;
+        s.beam_width = L; s.hash_slots = 0; s.trace_cap = cap;
+        s.frontier_keys = fk; s.hops = h; s.evals = ev; s.trace_ids = tids; s.trace_dists = tdst; s.flags = flags;
+        int rc = jb_beam_search(&s, st);
+        if (rc) return rc;
+        size_t tb = 0;
+        BALLOC(mx, int32_t, 1);
+        cub::DeviceReduce::Max(nullptr, tb, h, mx, (int)nq, st);
+        BALLOC(tmp, unsigned char, tb);
+        JB_CUDA(cub::DeviceReduce::Max(tmp, tb, h, mx, (int)nq, st));
+        int hmax = 0;
+        JB_CUDA(cudaMemcpyAsync(&hmax, mx, sizeof(int), cudaMemcpyDeviceToHost, st));
+        JB_CUDA(cudaStreamSynchronize(st));
+        if (hmax <= cap) break;
+        cap = hmax;  // re-run with an exact-size trace buffer (rare)
+    }
+    return JB_OK;
+}
+
+// Phase 3 (build.py:269-293): (target, dist, source) order via two stable radix
+// sorts of the reverse triples, segment heads, one owner warp per target.
+static int merge_phase(const jb_insert_args& a, double alpha2, uint32_t* tt, uint64_t* tk, int64_t ntri, int rstride,
+                       Bufs& bufs, cudaStream_t st, int& hseg) {
+    cudaError_t _ce;
+    const int R = a.degree_cap, D = a.dims;
+    BALLOC(tt2, uint32_t, ntri);
+    BALLOC(tk2, uint64_t, ntri);
+    {
+        size_t tb1 = 0, tb2 = 0;
+        cub::DeviceRadixSort::SortPairs(nullptr, tb1, tk, tk2, tt, tt2, (int)ntri, 0, 64, st);
+        cub::DeviceRadixSort::SortPairs(nullptr, tb2, tt2, tt, tk2, tk, (int)ntri, 0, 32, st);
+        BALLOC(tmp, unsigned char, std::max(tb1, tb2));
+        size_t tb = std::max(tb1, tb2);
+        JB_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, tk, tk2, tt, tt2, (int)ntri, 0, 64, st));  // by (dist, source)
+        tb = std::max(tb1, tb2);
+        JB_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, tt2, tt, tk2, tk, (int)ntri, 0, 32, st));  // stable by target
+    }
+    BALLOC(flag, uint8_t, ntri);
+    BALLOC(seg, int32_t, ntri);
+    BALLOC(nseg, int, 1);
+    seg_head_kernel<<<(unsigned)((ntri + 255) / 256), 256, 0, st>>>(tt, ntri, flag);
+    {
+        size_t tb = 0;
+        cub::DeviceSelect::Flagged(nullptr, tb, cub::CountingInputIterator<int32_t>(0), flag, seg, nseg, (int)ntri, st);
+        BALLOC(tmp, unsigned char, tb);
+        JB_CUDA(cub::DeviceSelect::Flagged(tmp, tb, cub::CountingInputIterator<int32_t>(0), flag, seg, nseg, (int)ntri,
+                                           st));
+    }
+    hseg = 0;
+    JB_CUDA(cudaMemcpyAsync(&hseg, nseg, sizeof(int), cudaMemcpyDeviceToHost, st));
+    JB_CUDA(cudaStreamSynchronize(st));
+    if (hseg > 0) {
+        const int pool_cap = (int)std::min<int64_t>(2 * ntri + 1024, INT32_MAX);
+        BALLOC(pool, uint64_t, pool_cap);
+        BALLOC(ptop, unsigned long long, 1);
+        BALLOC(err, int, 1);
+        JB_CUDA(cudaMemsetAsync(ptop, 0, sizeof(unsigned long long), st));
+        JB_CUDA(cudaMemsetAsync(err, 0, sizeof(int), st));
+        // owners stage up to R + 16 candidate rows in smem when they fit in ~26 KB
+        int crows = std::min(R + 16, (26 * 1024) / (rstride * 4 + 4));
+        if (crows < R + 1) crows = 0;
+        const int osm = owner_per_warp(R, D, crows, rstride) * BW;
+        JB_CUDA(cudaFuncSetAttribute(owner_merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, osm));
+        owner_merge_kernel<<<(unsigned)((hseg + BW - 1) / BW), BW * 32, osm, st>>>(
+            a.data, a.data_norms, D, alpha2, R, a.always_prune, tt, tk, ntri, seg, nseg, pool, ptop, pool_cap,
+            a.adjacency, a.degrees, err, crows, rstride);
+        JB_LAUNCH_CHECK();
+        int herr = 0;
+        JB_CUDA(cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, st));
+        JB_CUDA(cudaStreamSynchronize(st));
+        if (herr) { set_error("phase 3: candidate pool overflow"); return JB_EOVERFLOW; }
+    }
+    return JB_OK;
+}
+
 // out[0] += sum(v[0..n)), out[1] += sum(w[0..n)) (work counters; int64 totals)
 __global__ void sum2_kernel(const int32_t* __restrict__ v, const int32_t* __restrict__ w, int64_t n,
                             unsigned long long* __restrict__ out) {
@@ -890,39 +1058,11 @@ int jb_batch_insert(const jb_insert_args* args, void* stream) {
 
     // ---- phase 1: batched search of the new rows on the read-only graph ----
     const int L = a.build_beam_width;
-    // trace capacity: generous (8 B per slot) so the exact-size re-run below stays rare
-    int cap = std::max(4 * L, L + 512);
-    BALLOC(fk, uint64_t, (size_t)nb * L);
-    BALLOC(hops, int32_t, nb);
-    BALLOC(evals, int32_t, nb);
-    BALLOC(flags, int32_t, nb);
-    int32_t* tids = nullptr;
+    int cap = 0;
+    int32_t *hops = nullptr, *evals = nullptr, *tids = nullptr;
     float* tdst = nullptr;
-    for (int attempt = 0; attempt < 2; ++attempt) {
-        tids = bufs.get<int32_t>((size_t)nb * cap, st, _ce); JB_CUDA(_ce);
-        tdst = bufs.get<float>((size_t)nb * cap, st, _ce); JB_CUDA(_ce);
-        jb_search_args s{};
-        s.adjacency = a.adjacency; s.degree_cap = R; s.active_count = a.start;
-        s.source = JB_SRC_EXACT; s.dims = D; s.data = a.data; s.data_norms = a.data_norms;
-        s.queries = a.data + (size_t)a.start * D; s.query_add = a.data_norms + a.start;
-        s.nq = nb; s.starts = nullptr; s.start_vertex = entry;
-        s.beam_width = L; s.hash_slots = 0; s.trace_cap = cap;
-        s.frontier_keys = fk; s.hops = hops; s.evals = evals; s.trace_ids = tids; s.trace_dists = tdst; s.flags = flags;
-        rc = jb_beam_search(&s, stream);
-        if (rc) return rc;
-        // longest trace
-        size_t tb = 0;
-        BALLOC(mx, int32_t, 1);
-        cub::DeviceReduce::Max(nullptr, tb, hops, mx, (int)nb, st);
-        BALLOC(tmp, unsigned char, tb);
-        JB_CUDA(cub::DeviceReduce::Max(tmp, tb, hops, mx, (int)nb, st));
-        int hmax = 0;
-        JB_CUDA(cudaMemcpyAsync(&hmax, mx, sizeof(int), cudaMemcpyDeviceToHost, st));
-        JB_CUDA(cudaStreamSynchronize(st));
-        if (hmax <= cap) break;
-        cap = hmax;  // re-run with an exact-size trace buffer (rare)
-    }
-
+    rc = trace_search(a, a.start, nb, a.start, entry, bufs, st, cap, hops, evals, tids, tdst);
+    if (rc) return rc;
     unsigned long long hwork[2] = {0, 0};
     if (a.stats_out_host) {  // phase-1 hops and evals (phase 2 prunes over the same hop traces)
         BALLOC(work, unsigned long long, 2);
@@ -954,54 +1094,10 @@ int jb_batch_insert(const jb_insert_args* args, void* stream) {
     JB_LAUNCH_CHECK();
 
     pt.mark("prune");
-    // ---- phase 3: (target, dist, source) order via two stable radix sorts ----
-    BALLOC(tt2, uint32_t, ntri);
-    BALLOC(tk2, uint64_t, ntri);
-    {
-        size_t tb1 = 0, tb2 = 0;
-        cub::DeviceRadixSort::SortPairs(nullptr, tb1, tk, tk2, tt, tt2, (int)ntri, 0, 64, st);
-        cub::DeviceRadixSort::SortPairs(nullptr, tb2, tt2, tt, tk2, tk, (int)ntri, 0, 32, st);
-        BALLOC(tmp, unsigned char, std::max(tb1, tb2));
-        size_t tb = std::max(tb1, tb2);
-        JB_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, tk, tk2, tt, tt2, (int)ntri, 0, 64, st));  // by (dist, source)
-        tb = std::max(tb1, tb2);
-        JB_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, tt2, tt, tk2, tk, (int)ntri, 0, 32, st));  // stable by target
-    }
-    BALLOC(flag, uint8_t, ntri);
-    BALLOC(seg, int32_t, ntri);
-    BALLOC(nseg, int, 1);
-    seg_head_kernel<<<(unsigned)((ntri + 255) / 256), 256, 0, st>>>(tt, ntri, flag);
-    {
-        size_t tb = 0;
-        cub::DeviceSelect::Flagged(nullptr, tb, cub::CountingInputIterator<int32_t>(0), flag, seg, nseg, (int)ntri, st);
-        BALLOC(tmp, unsigned char, tb);
-        JB_CUDA(cub::DeviceSelect::Flagged(tmp, tb, cub::CountingInputIterator<int32_t>(0), flag, seg, nseg, (int)ntri,
-                                           st));
-    }
+    // ---- phase 3: grouped reverse-edge merge ----
     int hseg = 0;
-    JB_CUDA(cudaMemcpyAsync(&hseg, nseg, sizeof(int), cudaMemcpyDeviceToHost, st));
-    JB_CUDA(cudaStreamSynchronize(st));
-    if (hseg > 0) {
-        const int pool_cap = (int)std::min<int64_t>(2 * ntri + 1024, INT32_MAX);
-        BALLOC(pool, uint64_t, pool_cap);
-        BALLOC(ptop, unsigned long long, 1);
-        BALLOC(err, int, 1);
-        JB_CUDA(cudaMemsetAsync(ptop, 0, sizeof(unsigned long long), st));
-        JB_CUDA(cudaMemsetAsync(err, 0, sizeof(int), st));
-        // owners stage up to R + 16 candidate rows in smem when they fit in ~26 KB
-        int crows = std::min(R + 16, (26 * 1024) / (rstride * 4 + 4));
-        if (crows < R + 1) crows = 0;
-        const int osm = owner_per_warp(R, D, crows, rstride) * BW;
-        JB_CUDA(cudaFuncSetAttribute(owner_merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, osm));
-        owner_merge_kernel<<<(unsigned)((hseg + BW - 1) / BW), BW * 32, osm, st>>>(
-            a.data, a.data_norms, D, alpha2, R, a.always_prune, tt, tk, ntri, seg, nseg, pool, ptop, pool_cap,
-            a.adjacency, a.degrees, err, crows, rstride);
-        JB_LAUNCH_CHECK();
-        int herr = 0;
-        JB_CUDA(cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, st));
-        JB_CUDA(cudaStreamSynchronize(st));
-        if (herr) { set_error("phase 3: candidate pool overflow"); return JB_EOVERFLOW; }
-    }
+    rc = merge_phase(a, alpha2, tt, tk, ntri, rstride, bufs, st, hseg);
+    if (rc) return rc;
 
     pt.mark("merge");
     // ---- connectivity repair over the activated graph ----
@@ -1021,6 +1117,76 @@ int jb_batch_insert(const jb_insert_args* args, void* stream) {
         w[5] += bridges;
     }
     return rc;
+}
+
+int jb_refine_batch(const jb_insert_args* args, void* stream) {
+    JB_CHECK_ARG(args, "null args");
+    const jb_insert_args& a = *args;
+    int rc = validate_insert(a);
+    if (rc) return rc;
+    const int64_t active = a.active_count > 0 ? a.active_count : a.stop;
+    JB_CHECK_ARG(a.stop <= active && active <= a.capacity && active <= a.count, "refine: range beyond the active graph");
+    JB_CHECK_ARG(a.entry_point >= 0 && a.entry_point < active, "refine: entry point out of range");
+    if (a.entry_point_out_host) *a.entry_point_out_host = a.entry_point;  // refinement never moves the entry
+    if (a.bridges_out_host) *a.bridges_out_host = 0;
+    if (a.start == a.stop) return JB_OK;
+    cudaStream_t st = as_stream(stream);
+    const int R = a.degree_cap, D = a.dims;
+    const double alpha2 = a.alpha * a.alpha;
+    const int64_t nb = a.stop - a.start;
+    Bufs bufs;
+    cudaError_t _ce;
+    PhaseTimer pt(st);
+    int cap = 0;
+    int32_t *hops = nullptr, *evals = nullptr, *tids = nullptr;
+    float* tdst = nullptr;
+    rc = trace_search(a, a.start, nb, active, a.entry_point, bufs, st, cap, hops, evals, tids, tdst);
+    if (rc) return rc;
+    pt.mark("search");
+    const int64_t ntri = nb * (int64_t)R;
+    BALLOC(cand, uint64_t, (size_t)nb * (cap + R));
+    BALLOC(kid, int32_t, (size_t)nb * R);
+    BALLOC(kd, float, (size_t)nb * R);
+    BALLOC(tt, uint32_t, ntri);
+    BALLOC(tk, uint64_t, ntri);
+    BALLOC(ncand, int32_t, nb);
+    const int rstride = ((D + 3) & ~3) + 4;
+    int crows = std::min(cap + R, (26 * 1024 - ((D + 3) & ~3) * 4) / (rstride * 4 + 4));
+    if (crows < R + 1) crows = 0;
+    const size_t smem = (size_t)BW * 4 * (((D + 3) & ~3) + crows * rstride + ((crows + 3) & ~3));
+    JB_CUDA(cudaFuncSetAttribute(refine_prune_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    refine_prune_kernel<<<(unsigned)((nb + BW - 1) / BW), BW * 32, smem, st>>>(
+        a.data, a.data_norms, D, a.start, nb, alpha2, R, hops, tids, tdst, cap, cand, kid, kd, a.adjacency, a.degrees,
+        tt, tk, crows, rstride, ncand);
+    JB_LAUNCH_CHECK();
+    pt.mark("prune");
+    int hseg = 0;
+    rc = merge_phase(a, alpha2, tt, tk, ntri, rstride, bufs, st, hseg);
+    if (rc) return rc;
+    pt.mark("merge");
+    pt.report(a.start, a.stop);
+    if (a.stats_out_host) {
+        BALLOC(work, unsigned long long, 2);
+        JB_CUDA(cudaMemsetAsync(work, 0, 2 * sizeof(unsigned long long), st));
+        sum2_kernel<<<std::max(1, std::min<int>((int)((nb + 255) / 256), 4 * sm_count_current())), 256, 0, st>>>(
+            hops, evals, nb, work);
+        unsigned long long hw[2] = {0, 0};
+        JB_CUDA(cudaMemcpyAsync(hw, work, sizeof(hw), cudaMemcpyDeviceToHost, st));
+        JB_CUDA(cudaMemsetAsync(work, 0, 2 * sizeof(unsigned long long), st));
+        sum2_kernel<<<std::max(1, std::min<int>((int)((nb + 255) / 256), 4 * sm_count_current())), 256, 0, st>>>(
+            ncand, ncand, nb, work);
+        unsigned long long pc[2] = {0, 0};
+        JB_CUDA(cudaMemcpyAsync(pc, work, sizeof(pc), cudaMemcpyDeviceToHost, st));
+        JB_CUDA(cudaStreamSynchronize(st));
+        int64_t* w = a.stats_out_host;
+        w[0] += (int64_t)hw[0];
+        w[1] += (int64_t)hw[1];
+        w[2] += (int64_t)pc[0];
+        w[3] += hseg;
+        w[4] += ntri;
+    }
+    JB_CUDA(cudaStreamSynchronize(st));
+    return JB_OK;
 }
 
 int jb_robust_prune(const float* data, const float* data_norms, int32_t dims, const int64_t* pivots, int64_t count,

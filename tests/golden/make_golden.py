@@ -58,6 +58,17 @@ def graph_fixture(name, data, R, L, alpha, max_batch=100_000):
                    entry=np.int64(g.entry_point), active=np.int64(n))
 
 
+def two_pass():
+    """6. two_pass build (insertion at alpha=1, refinement at the final alpha) in several refine batches."""
+    data = ref.gen_synthetic(1500, 32, seed=21).data
+    t = time.time()
+    g = ref.build(ref.VectorDataset(data), ref.BuildParams(degree_cap=16, build_beam_width=32, alpha=1.2,
+                                                           max_batch=400, two_pass=True))
+    print(f"two_pass: reference build {data.shape} in {time.time() - t:.1f}s")
+    n = g.active_count
+    save("two_pass", adjacency=g.adjacency[:n].copy(), degrees=g.degrees[:n].copy(), entry=np.int64(g.entry_point))
+
+
 def main():
     # 1. exact search + build on a small Gaussian graph (D=32, R=16, L=32)
     data = ref.gen_synthetic(3000, 32, seed=0).data
@@ -122,4 +133,10 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    # no arguments: every fixture; otherwise the named generators (e.g. two_pass)
+    names = sys.argv[1:]
+    if not names:
+        main()
+        two_pass()
+    for n in names:
+        globals()[n]()

@@ -47,6 +47,23 @@ def test_build_identical_to_reference_g128_and_stream():
     _same_graph(inc, f["inc_adjacency"], f["inc_degrees"], int(f["inc_entry"]))
 
 
+def test_two_pass_build_identical_to_reference():
+    f = golden("two_pass")
+    g = jb.build(jb.VectorDataset(gaussian(1500, 32, 21)),
+                 jb.BuildParams(degree_cap=16, build_beam_width=32, alpha=1.2, max_batch=400, two_pass=True))
+    _same_graph(g, f["adjacency"], f["degrees"], int(f["entry"]))
+    g.validate()
+
+
+def test_two_pass_refine_matches_oracle_lowrank():
+    # refinement on a larger low-rank graph, several refine batches, always_prune merge
+    x = lowrank(6000, 64, 16, 0.05, 73)
+    og = vamana.build(x, R=24, L=48, alpha=1.3, max_batch=1500, two_pass=True)
+    g = jb.build(jb.VectorDataset(x), jb.BuildParams(degree_cap=24, build_beam_width=48, alpha=1.3, max_batch=1500,
+                                                     two_pass=True))
+    _same_graph(g, og.adj, og.deg, og.entry)
+
+
 @pytest.mark.parametrize("always_prune,reverse_all", [(True, False), (False, True)])
 def test_build_options_match_oracle(always_prune, reverse_all):
     x = gaussian(1500, 24, 61)

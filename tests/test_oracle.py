@@ -39,6 +39,14 @@ def test_build_matches_reference_g32():
     assert g.entry == int(f["entry"])
 
 
+def test_two_pass_build_matches_reference():
+    f = golden("two_pass")
+    g = vamana.build(gaussian(1500, 32, 21), R=16, L=32, alpha=1.2, max_batch=400, two_pass=True)
+    np.testing.assert_array_equal(g.adj, f["adjacency"])
+    np.testing.assert_array_equal(g.deg, f["degrees"])
+    assert g.entry == int(f["entry"])
+
+
 def test_build_matches_reference_g33_odd_dims():
     f = golden("g33")
     g = vamana.build(gaussian(800, 33, 5), R=8, L=16, alpha=1.3)
