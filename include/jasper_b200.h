@@ -57,6 +57,19 @@ int jb_row_sq_norms(const float* x, int64_t n, int32_t dims, float* out, void* s
  * *out_host (synchronizes). Replaces graph.medoid (graph.py:159-171). */
 int jb_medoid(const float* x, int64_t n, int32_t dims, int64_t* out_host, void* stream);
 
+/* u8 element kind (ElementKind.U8, core.py:32-37): integer-exact row norms
+ * sum(x*x) (core.py:162-166, search.py:94-96) and the medoid of u8 rows (the
+ * reference's f64 path on x.astype(f64): identical to jb_medoid on exact f32
+ * copies of the rows, which this entry point makes on the device). */
+int jb_row_sq_norms_u8(const uint8_t* x, int64_t n, int32_t dims, uint32_t* out, void* stream);
+int jb_medoid_u8(const uint8_t* x, int64_t n, int32_t dims, int64_t* out_host, void* stream);
+/* u8 rows -> exact f32 copy (for the f64 ground truth / medoid paths). */
+int jb_u8_to_f32(const uint8_t* x, int64_t count, float* out, void* stream);
+
+/* Element kinds of jb_insert_args.element_kind. */
+#define JB_KIND_F32 0
+#define JB_KIND_U8 1
+
 /* ---- search (north-star 1) -------------------------------------------- */
 
 /* Distance source of a search. */
@@ -65,6 +78,9 @@ int jb_medoid(const float* x, int64_t n, int32_t dims, int64_t* out_host, void* 
 #define JB_SRC_RABITQ_FAST 2 /* RaBitQ, 1-bit codes: query quantized to 6-bit planes,
                               * <u,q> by AND + popcount (north-star 2). Numerics differ
                               * from the reference estimator; validated by recall.  */
+#define JB_SRC_EXACT_U8 3  /* ExactDistances over u8 rows: integer distances
+                              * ||x||^2 - 2<x,q> + ||q||^2 (search.py:92-99,
+                              * 126-130), key word = the u32 distance            */
 
 typedef struct jb_search_args {
     /* graph (GraphIndex, graph.py:36-99): fixed-stride int32 slab padded -1 */
@@ -97,6 +113,11 @@ typedef struct jb_search_args {
     int32_t* trace_ids;            /* [nq, trace_cap] visited ids in hop order  */
     float* trace_dists;            /* [nq, trace_cap] their f32 distances       */
     int32_t* flags;                /* [nq] bit0: visited table overflowed (lossy) */
+    /* EXACT_U8 source (the f32 data/queries fields are unused) */
+    const uint8_t* data_u8;        /* [N, D] u8 rows                            */
+    const uint32_t* norms_u32;     /* [N] integer row norms                     */
+    const uint8_t* queries_u8;     /* [nq, D] u8 queries                        */
+    const uint32_t* query_norms_u32; /* [nq] integer query norms                */
 } jb_search_args;
 
 /* Batched greedy beam search, one warp per query (persistent grid).
@@ -109,6 +130,9 @@ int jb_beam_search(const jb_search_args* args, void* stream);
  * (search.py:366-383). */
 int jb_frontier_topk(const uint64_t* frontier_keys, int64_t nq, int32_t beam_width, int32_t k,
                      int32_t* out_ids, double* out_dists, void* stream);
+/* Same for integer (u8-source) keys: the key word is the u32 distance. */
+int jb_frontier_topk_u8(const uint64_t* frontier_keys, int64_t nq, int32_t beam_width, int32_t k,
+                        int32_t* out_ids, double* out_dists, void* stream);
 
 /* Exact fp32 rerank of the full frontier: dist = einsum(x-q, x-q) (A1),
  * ordered by (dist, id), first k. Replaces _exact_rescore + lexsort
@@ -199,6 +223,10 @@ typedef struct jb_insert_args {
                                     * triples, [5] repair bridges                 */
     int64_t active_count;          /* jb_refine_batch: vertices visible to the
                                     * search (0 => stop); ignored elsewhere     */
+    int32_t element_kind;          /* JB_KIND_F32 (data, data_norms) or
+                                    * JB_KIND_U8 (data_u8, norms_u32)           */
+    const uint8_t* data_u8;        /* [count, D] u8 rows                        */
+    const uint32_t* norms_u32;     /* [count] integer row norms                 */
 } jb_insert_args;
 
 /* One three-phase batch: search -> prune + reverse triples -> grouped merge,

@@ -18,15 +18,21 @@ LOW32 = np.uint64(0xFFFFFFFF)
 SEEN_BUDGET = 1 << 28  # search.py:39
 
 
-def pack(d: np.ndarray, ids: np.ndarray) -> np.ndarray:
-    """search.py:139-145 (f32 branch)."""
-    hi = np.maximum(np.asarray(d, dtype=np.float32), np.float32(0)).view(np.uint32)
-    return (hi.astype(np.uint64) << np.uint64(32)) | np.asarray(ids).astype(np.uint64)
+def pack(d: np.ndarray, ids: np.ndarray, integer: bool = False) -> np.ndarray:
+    """search.py:139-145: f32 bits of max(d, 0), or the raw integer distance (u8)."""
+    if integer:
+        hi = np.asarray(d).astype(np.uint64)
+    else:
+        hi = np.maximum(np.asarray(d, dtype=np.float32), np.float32(0)).view(np.uint32).astype(np.uint64)
+    return (hi << np.uint64(32)) | np.asarray(ids).astype(np.uint64)
 
 
-def unpack_dist(keys: np.ndarray) -> np.ndarray:
-    """search.py:148-152 (f32 branch): high word -> f32 -> f64."""
-    return (keys >> np.uint64(32)).astype(np.uint32).view(np.float32).astype(np.float64)
+def unpack_dist(keys: np.ndarray, integer: bool = False) -> np.ndarray:
+    """search.py:148-152: high word -> f32 -> f64 (or integer -> f64)."""
+    hi = keys >> np.uint64(32)
+    if integer:
+        return hi.astype(np.float64)
+    return hi.astype(np.uint32).view(np.float32).astype(np.float64)
 
 
 def unpack_id(keys: np.ndarray) -> np.ndarray:
@@ -34,17 +40,26 @@ def unpack_id(keys: np.ndarray) -> np.ndarray:
 
 
 class ExactSource:
-    """search.py:89-130: f32 rows, norms from einsum, distances in the data role."""
+    """search.py:89-130: f32 rows, norms from einsum, distances in the data role;
+    u8 rows: the same identity in exact int64 (search.py:92-99), no clamp."""
 
     def __init__(self, data: np.ndarray, queries: np.ndarray):
-        self.x = np.ascontiguousarray(data, dtype=np.float32)
+        self.integer = np.asarray(data).dtype == np.uint8
+        if self.integer:
+            if np.asarray(queries).dtype != np.uint8:
+                raise ValueError("u8 dataset requires u8 queries")
+            self.x = np.asarray(data).astype(np.int64)
+            self.q = np.atleast_2d(queries).astype(np.int64)
+        else:
+            self.x = np.ascontiguousarray(data, dtype=np.float32)
+            self.q = np.ascontiguousarray(np.atleast_2d(queries), dtype=np.float32)
         self.xn = np.einsum("nd,nd->n", self.x, self.x)
-        self.q = np.ascontiguousarray(np.atleast_2d(queries), dtype=np.float32)
         self.qn = np.einsum("qd,qd->q", self.q, self.q)
 
     def __call__(self, qrows: np.ndarray, ids: np.ndarray) -> np.ndarray:
         dots = np.einsum("md,md->m", self.x[ids], self.q[qrows])
-        return np.maximum(self.xn[ids] - 2 * dots + self.qn[qrows], np.float32(0))
+        d = self.xn[ids] - 2 * dots + self.qn[qrows]
+        return d if self.integer else np.maximum(d, np.float32(0))
 
 
 class Result:
@@ -64,7 +79,8 @@ def _lockstep(adjacency: np.ndarray, n_active: int, dist, qrows: np.ndarray,
     seen = np.zeros((nq, n_active), dtype=bool)
     evals = np.ones(nq, dtype=np.int64)
     hops = np.zeros(nq, dtype=np.int64)
-    beam[:, 0] = pack(dist(qrows, starts), starts)
+    integer = getattr(dist, "integer", False)
+    beam[:, 0] = pack(dist(qrows, starts), starts, integer)
     done[:, 0] = False
     seen[np.arange(nq), starts] = True
     log_q, log_id, log_d = [], [], []
@@ -82,7 +98,7 @@ def _lockstep(adjacency: np.ndarray, n_active: int, dist, qrows: np.ndarray,
         hops[live] += 1
         log_q.append(live)
         log_id.append(uid.astype(np.int32))
-        log_d.append(unpack_dist(ukeys))
+        log_d.append(unpack_dist(ukeys, integer))
 
         nbr = adjacency[uid]
         ok = nbr >= 0
@@ -93,7 +109,7 @@ def _lockstep(adjacency: np.ndarray, n_active: int, dist, qrows: np.ndarray,
         if r.size:
             ids = nbr[r, c].astype(np.int64)
             qsel = live[r]
-            cand[r, c] = pack(dist(qrows[qsel], ids), ids)
+            cand[r, c] = pack(dist(qrows[qsel], ids), ids, integer)
             seen[qsel, ids] = True
             evals[live] += np.bincount(r, minlength=live.size)
         merged = np.concatenate([beam[live], cand], axis=1)
@@ -115,7 +131,7 @@ def _lockstep(adjacency: np.ndarray, n_active: int, dist, qrows: np.ndarray,
     out = []
     for i in range(nq):
         k = beam[i][beam[i] != UMAX]
-        out.append(Result(unpack_id(k).astype(np.int32), unpack_dist(k),
+        out.append(Result(unpack_id(k).astype(np.int32), unpack_dist(k, integer),
                           id_all[ends[i]:ends[i + 1]], d_all[ends[i]:ends[i + 1]],
                           int(hops[i]), int(evals[i])))
     return out

@@ -44,16 +44,20 @@ class Graph:
 
 
 class Pairwise:
-    """build.py:105-134 (exact branch)."""
+    """build.py:105-134 (exact branch; u8 rows in exact int64, build.py:116-118, 132-133)."""
 
     def __init__(self, x: np.ndarray):
-        self.x = x
-        self.n = np.einsum("nd,nd->n", x, x)
+        self.integer = x.dtype == np.uint8
+        self.x = x.astype(np.int64) if self.integer else x
+        self.n = np.einsum("nd,nd->n", self.x, self.x)
 
     def __call__(self, pivot: int, ids) -> np.ndarray:
         ids = np.asarray(ids, dtype=np.int64)
         dots = np.einsum("md,d->m", self.x[ids], self.x[pivot])
-        return np.maximum(self.n[ids] - 2 * dots + self.n[pivot], np.float32(0)).astype(np.float64)
+        d = self.n[ids] - 2 * dots + self.n[pivot]
+        if self.integer:
+            return d.astype(np.float64)
+        return np.maximum(d, np.float32(0)).astype(np.float64)
 
 
 def medoid(x: np.ndarray) -> int:
@@ -246,7 +250,7 @@ def refine_pass(g: Graph, x: np.ndarray, R: int, L: int, alpha: float, max_batch
 
 def build(x: np.ndarray, R: int, L: int, alpha: float, max_batch: int = 100_000, two_pass: bool = False) -> Graph:
     """build.py:389-424 (two_pass: insertion passes at alpha=1, then refine_pass)."""
-    x = np.ascontiguousarray(x, dtype=np.float32)
+    x = np.ascontiguousarray(x) if np.asarray(x).dtype == np.uint8 else np.ascontiguousarray(x, dtype=np.float32)
     n = x.shape[0]
     if n == 0:
         raise ValueError("cannot build over an empty dataset")

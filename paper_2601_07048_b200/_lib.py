@@ -17,7 +17,8 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libjasper_b200.so")
 
 JB_OK, JB_EINVAL, JB_ECUDA, JB_ENODONOR, JB_EOVERFLOW = 0, 1, 2, 3, 4
-SRC_EXACT, SRC_RABITQ, SRC_RABITQ_FAST = 0, 1, 2
+SRC_EXACT, SRC_RABITQ, SRC_RABITQ_FAST, SRC_EXACT_U8 = 0, 1, 2, 3
+KIND_F32, KIND_U8 = 0, 1
 
 p = C.c_void_p
 i32, i64, f64 = C.c_int32, C.c_int64, C.c_double
@@ -33,6 +34,7 @@ class SearchArgs(C.Structure):
         ("beam_width", i32), ("hash_slots", i32), ("trace_cap", i32),
         ("frontier_keys", p), ("hops", p), ("evals", p), ("trace_ids", p), ("trace_dists", p),
         ("flags", p),
+        ("data_u8", p), ("norms_u32", p), ("queries_u8", p), ("query_norms_u32", p),
     ]
 
 
@@ -49,6 +51,7 @@ class InsertArgs(C.Structure):
         ("start", i64), ("stop", i64), ("entry_point", i64),
         ("entry_point_out_host", p), ("bridges_out_host", p), ("stats_out_host", p),  # int64 [8]
         ("active_count", i64),
+        ("element_kind", i32), ("data_u8", p), ("norms_u32", p),
     ]
 
 
@@ -58,8 +61,12 @@ _SIGS = {
     "jb_sm_count": (C.c_int, [C.c_int, p]),
     "jb_row_sq_norms": (C.c_int, [p, i64, i32, p, p]),
     "jb_medoid": (C.c_int, [p, i64, i32, p, p]),
+    "jb_row_sq_norms_u8": (C.c_int, [p, i64, i32, p, p]),
+    "jb_medoid_u8": (C.c_int, [p, i64, i32, p, p]),
+    "jb_u8_to_f32": (C.c_int, [p, i64, p, p]),
     "jb_beam_search": (C.c_int, [C.POINTER(SearchArgs), p]),
     "jb_frontier_topk": (C.c_int, [p, i64, i32, i32, p, p, p]),
+    "jb_frontier_topk_u8": (C.c_int, [p, i64, i32, i32, p, p, p]),
     "jb_rerank_topk": (C.c_int, [p, i32, p, i64, p, i32, i32, p, p, p]),
     "jb_search_knn_host": (C.c_int, [C.POINTER(KnnPlan), p, i64, p, p, p]),
     "jb_search_knn_device": (C.c_int, [C.POINTER(KnnPlan), p, i64, p, p, p]),

@@ -110,7 +110,11 @@ def _args(graph: GraphIndex, ds, params: BuildParams, start: int, stop: int):
     a = _lib.InsertArgs()
     a.adjacency, a.degrees = _lib.ptr(adj), _lib.ptr(deg)
     a.degree_cap, a.capacity = graph.degree_cap, graph.capacity
-    a.data, a.data_norms, a.dims, a.count = _lib.ptr(dev.x), _lib.ptr(dev.norms), dev.dims, dev.count
+    a.dims, a.count = dev.dims, dev.count
+    if ds.element_kind is ElementKind.U8:
+        a.element_kind, a.data_u8, a.norms_u32 = _lib.KIND_U8, _lib.ptr(dev.x), _lib.ptr(dev.norms)
+    else:
+        a.element_kind, a.data, a.data_norms = _lib.KIND_F32, _lib.ptr(dev.x), _lib.ptr(dev.norms)
     a.build_beam_width = params.build_beam_width
     a.alpha = float(params.alpha)
     a.always_prune = int(params.always_prune)
@@ -156,8 +160,6 @@ def batch_insert(graph, dataset, new_ids: range, params: BuildParams, quantizer=
     if start == stop:
         return
     _check_supported(params, quantizer)
-    if ds.element_kind is not ElementKind.F32:
-        raise ValueError("the B200 path supports f32 datasets")
     if graph.degree_cap != params.degree_cap:
         raise ValueError("graph degree_cap differs from params.degree_cap")
     a = _args(graph, ds, params, start, stop)

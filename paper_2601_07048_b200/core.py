@@ -40,11 +40,13 @@ class DistanceKind(enum.Enum):
 
 @dataclass
 class DeviceRows:
-    """HBM mirror of a dataset: rows [n, D] f32 and A1 norms [n] f32."""
+    """HBM mirror of a dataset: rows [n, D] (f32, or u8) and their squared norms
+    [n] (f32 in A1 order, or exact u32 integers held in an int32 tensor)."""
     x: object
     norms: object
     count: int
     dims: int
+    kind: ElementKind = ElementKind.F32
 
 
 class VectorDataset:
@@ -126,23 +128,40 @@ class VectorDataset:
 
     # ---- device mirror -------------------------------------------------
     def device(self) -> DeviceRows:
-        """Upload once (rows + A1 norms computed on device) and cache."""
+        """Upload once (rows + norms computed on device) and cache."""
         if self._dev is not None:
             return self._dev
-        if self._kind is not ElementKind.F32:
-            raise ValueError("the B200 path supports f32 datasets (u8 is not built yet)")
         torch = _lib.require_cuda()
         with self._dev_lock:
             if self._dev is None:
                 with warnings.catch_warnings():  # read-only numpy -> torch view, copied to HBM at once
                     warnings.simplefilter("ignore", UserWarning)
                     x = torch.from_numpy(np.ascontiguousarray(self._data)).to("cuda", non_blocking=False)
-                norms = torch.empty(x.shape[0], dtype=torch.float32, device=x.device)
-                if x.shape[0]:
-                    _lib.check(_lib.lib().jb_row_sq_norms(_lib.ptr(x), x.shape[0], x.shape[1], _lib.ptr(norms),
-                                                         _lib.stream_ptr()))
-                self._dev = DeviceRows(x, norms, x.shape[0], x.shape[1])
+                if self._kind is ElementKind.U8:
+                    if x.shape[1] * 255 ** 2 >= 1 << 32:
+                        raise ValueError("u8 dims too large for 32-bit packed distances")
+                    norms = torch.empty(x.shape[0], dtype=torch.int32, device=x.device)
+                    if x.shape[0]:
+                        _lib.check(_lib.lib().jb_row_sq_norms_u8(_lib.ptr(x), x.shape[0], x.shape[1], _lib.ptr(norms),
+                                                                _lib.stream_ptr()))
+                else:
+                    norms = torch.empty(x.shape[0], dtype=torch.float32, device=x.device)
+                    if x.shape[0]:
+                        _lib.check(_lib.lib().jb_row_sq_norms(_lib.ptr(x), x.shape[0], x.shape[1], _lib.ptr(norms),
+                                                             _lib.stream_ptr()))
+                self._dev = DeviceRows(x, norms, x.shape[0], x.shape[1], self._kind)
         return self._dev
+
+    def device_f32(self):
+        """Exact f32 copy of u8 rows on the device (for the f64 medoid / ground-truth
+        paths, which the reference runs on x.astype(f64)); the f32 rows otherwise."""
+        dev = self.device()
+        if self._kind is not ElementKind.U8:
+            return dev.x
+        torch = _lib.require_cuda()
+        out = torch.empty(dev.x.shape, dtype=torch.float32, device=dev.x.device)
+        _lib.check(_lib.lib().jb_u8_to_f32(_lib.ptr(dev.x), dev.x.numel(), _lib.ptr(out), _lib.stream_ptr()))
+        return out
 
 
 def as_dataset(obj) -> VectorDataset:

@@ -21,9 +21,11 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <type_traits>
 #include <vector>
 #include <cub/cub.cuh>
 #include "common.cuh"
+#include "metric.cuh"
 #include "runtime.cuh"
 
 namespace jb {
@@ -33,6 +35,7 @@ constexpr uint32_t NO_TARGET = 0xFFFFFFFFu;
 
 // d(pivot, row) with the row in the data role and the pivot norm added last
 // (build.py:130-134): max((xn[row] - 2*dot(x[row], x[pivot])) + xn[pivot], 0).
+// f32 only: the standalone robust_prune entry point (jb_robust_prune).
 __device__ __forceinline__ float pair_dist(const float* __restrict__ data, const float* __restrict__ norms, int D,
                                            const float* __restrict__ pivot_row, float pivot_norm, uint32_t row) {
     const float dot = a1_dot<false>(data + (size_t)row * D, pivot_row, D);
@@ -48,39 +51,38 @@ __device__ __forceinline__ uint64_t warp_min_u64(uint64_t v) {
     return v;
 }
 
+__device__ __forceinline__ uint64_t key_of(uint32_t bits, uint32_t id) { return ((uint64_t)bits << 32) | id; }
+
 // Warp-cooperative robust prune over n candidate keys (dist_bits << 32 | id) in
-// `cand` (modified in place). Writes kept ids/dists (extraction order) and returns
-// how many were kept. `srow` is per-warp smem of D floats for the star row.
-__device__ int warp_prune(uint64_t* cand, int n, double alpha2, int R, const float* __restrict__ data,
-                          const float* __restrict__ norms, int D, float* srow, int32_t* out_ids, float* out_d) {
+// `cand` (modified in place). Writes kept ids / dist bits (extraction order) and
+// returns how many were kept. `pv` is per-warp smem for the star (M::pivot_words).
+template <class M>
+__device__ int warp_prune(uint64_t* cand, int n, double alpha2, int R, const M& m, uint32_t* pv, int32_t* out_ids,
+                          uint32_t* out_d) {
     const int lane = lane_id();
     int kept = 0;
     while (kept < R) {
-        uint64_t m = UMAX;
-        for (int i = lane; i < n; i += 32) { uint64_t c = cand[i]; m = c < m ? c : m; }
-        m = warp_min_u64(m);
-        if (m == UMAX) break;
-        const uint32_t star = (uint32_t)(m & 0xFFFFFFFFull);
+        uint64_t mk = UMAX;
+        for (int i = lane; i < n; i += 32) { uint64_t c = cand[i]; mk = c < mk ? c : mk; }
+        mk = warp_min_u64(mk);
+        if (mk == UMAX) break;
+        const uint32_t star = (uint32_t)(mk & 0xFFFFFFFFull);
         if (lane == 0) {
             out_ids[kept] = (int32_t)star;
-            out_d[kept] = __uint_as_float((uint32_t)(m >> 32));
+            out_d[kept] = (uint32_t)(mk >> 32);
         }
         for (int i = lane; i < n; i += 32)
-            if (cand[i] == m) cand[i] = UMAX;
+            if (cand[i] == mk) cand[i] = UMAX;
         ++kept;
         if (kept >= R) break;
-        // stage the star row, then filter survivors: keep p' iff alpha^2 * d(star, p') > d(p, p')
+        // keep p' iff alpha^2 * d(star, p') > d(p, p')   (graph.py:218, f64)
         __syncwarp();
-        const float* sr = data + (size_t)star * D;
-        for (int e = lane; e < D; e += 32) srow[e] = sr[e];
-        const float sn = __ldg(norms + star);
-        __syncwarp();
+        m.load_pivot(pv, star);
         for (int i = lane; i < n; i += 32) {
             const uint64_t c = cand[i];
             if (c == UMAX) continue;
-            const float dsp = pair_dist(data, norms, D, srow, sn, (uint32_t)(c & 0xFFFFFFFFull));
-            const double dp = (double)__uint_as_float((uint32_t)(c >> 32));
-            if (!(__dmul_rn(alpha2, (double)dsp) > dp)) cand[i] = UMAX;
+            const uint32_t dsp = m.dist(pv, (uint32_t)(c & 0xFFFFFFFFull));
+            if (!(__dmul_rn(alpha2, M::value(dsp)) > M::value((uint32_t)(c >> 32)))) cand[i] = UMAX;
         }
         __syncwarp();
     }
@@ -88,72 +90,40 @@ __device__ int warp_prune(uint64_t* cand, int n, double alpha2, int R, const flo
     return kept;
 }
 
-// Stage the rows of n candidate ids (low 32 bits of `keys`) into smem rows
-// [n][rstride] with coalesced cp.async (one warp instruction per 512 B row at
-// D=128), plus their norms.
-__device__ __forceinline__ void stage_rows(float* rows, int rstride, float* cn, const uint64_t* keys, int n,
-                                           const float* __restrict__ data, const float* __restrict__ norms, int D) {
-    const int lane = lane_id();
-    if ((D & 3) == 0) {
-        const int nv = D >> 2;
-        for (int j = 0; j < n; ++j) {
-            const float* src = data + (size_t)(uint32_t)(keys[j] & 0xFFFFFFFFull) * D;
-            for (int f = lane; f < nv; f += 32) cp_async16(rows + (size_t)j * rstride + 4 * f, src + 4 * f);
-        }
-    } else {
-        for (int j = 0; j < n; ++j) {
-            const float* src = data + (size_t)(uint32_t)(keys[j] & 0xFFFFFFFFull) * D;
-            for (int f = lane; f < D; f += 32) cp_async4(rows + (size_t)j * rstride + f, src + f);
-        }
-    }
-    for (int j = lane; j < n; j += 32) cn[j] = __ldg(norms + (uint32_t)(keys[j] & 0xFFFFFFFFull));
-    cp_async_wait_all();
-    __syncwarp();
-}
-
-__device__ __forceinline__ float a1_rows(const float* a, const float* b, int D) {
-    Acc4 acc; acc.zero();
-    if ((D & 3) == 0) a1_range<true, false>(acc, a, b, 0, D);
-    else a1_range<false, false>(acc, a, b, 0, D);
-    return acc.reduce();
-}
-
-// Robust prune with every candidate row already in smem (rows[i] <-> cand[i]):
+// Robust prune with every candidate row already staged in smem (rows[i] <-> cand[i]):
 // same extraction sequence as warp_prune, no global traffic in the rounds.
-__device__ int warp_prune_staged(uint64_t* cand, int n, double alpha2, int R, const float* rows, int rstride,
-                                 const float* cn, int D, int32_t* out_ids, float* out_d) {
+template <class M>
+__device__ int warp_prune_staged(uint64_t* cand, int n, double alpha2, int R, const M& m, const uint32_t* rows,
+                                 const uint32_t* cn, int32_t* out_ids, uint32_t* out_d) {
     const int lane = lane_id();
     int kept = 0;
     while (kept < R) {
-        uint64_t m = UMAX;
+        uint64_t mk = UMAX;
         int mi = -1;
         for (int i = lane; i < n; i += 32) {
             const uint64_t c = cand[i];
-            if (c < m) { m = c; mi = i; }
+            if (c < mk) { mk = c; mi = i; }
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
-            const uint64_t om = shfl_xor_u64(m, o);
+            const uint64_t om = shfl_xor_u64(mk, o);
             const int oi = __shfl_xor_sync(0xFFFFFFFFu, mi, o);
-            if (om < m) { m = om; mi = oi; }
+            if (om < mk) { mk = om; mi = oi; }
         }
-        if (m == UMAX) break;
+        if (mk == UMAX) break;
         if (lane == 0) {
-            out_ids[kept] = (int32_t)(m & 0xFFFFFFFFull);
-            out_d[kept] = __uint_as_float((uint32_t)(m >> 32));
+            out_ids[kept] = (int32_t)(mk & 0xFFFFFFFFull);
+            out_d[kept] = (uint32_t)(mk >> 32);
             cand[mi] = UMAX;
         }
         ++kept;
         __syncwarp();
         if (kept >= R) break;
-        const float* srow = rows + (size_t)mi * rstride;
-        const float sn = cn[mi];
         for (int i = lane; i < n; i += 32) {
             const uint64_t c = cand[i];
             if (c == UMAX) continue;
-            const float dsp = exact_from_dot(cn[i], a1_rows(rows + (size_t)i * rstride, srow, D), sn);
-            const double dp = (double)__uint_as_float((uint32_t)(c >> 32));
-            if (!(__dmul_rn(alpha2, (double)dsp) > dp)) cand[i] = UMAX;
+            const uint32_t dsp = m.dist_staged(rows, cn, i, mi);
+            if (!(__dmul_rn(alpha2, M::value(dsp)) > M::value((uint32_t)(c >> 32)))) cand[i] = UMAX;
         }
         __syncwarp();
     }
@@ -168,66 +138,70 @@ __device__ __forceinline__ void write_row(int32_t* __restrict__ adj, int32_t* __
     if (lane == 0) deg[v] = n;
 }
 
+// Per-warp smem of the per-vertex kernels: pivot | staged rows (crows) | their norms.
+template <class M>
+__host__ __device__ inline int vertex_warp_words(const M& m, int crows) {
+    return m.pivot_words() + crows * m.stage_stride_words() + ((crows + 3) & ~3);
+}
+
 // ---- seed batch (build.py:246-266) ------------------------------------------
+template <class M>
 __global__ void __launch_bounds__(BW * 32)
-seed_prune_kernel(const float* __restrict__ data, const float* __restrict__ norms, int D, int64_t start, int64_t stop,
-                  double alpha2, int R, uint64_t* __restrict__ cand_all, int32_t* __restrict__ kept_ids,
-                  float* __restrict__ kept_d, int32_t* __restrict__ adj, int32_t* __restrict__ deg) {
-    extern __shared__ __align__(16) float sh[];
+seed_prune_kernel(const M m, int64_t start, int64_t stop, double alpha2, int R, uint64_t* __restrict__ cand_all,
+                  int32_t* __restrict__ kept_ids, uint32_t* __restrict__ kept_d, int32_t* __restrict__ adj,
+                  int32_t* __restrict__ deg) {
+    extern __shared__ __align__(16) uint32_t shw[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    float* srow = sh + warp * ((D + 3) & ~3);
+    uint32_t* pv = shw + warp * m.pivot_words();
     const int64_t n = stop - start;
     const int64_t xi = (int64_t)blockIdx.x * BW + warp;
     if (xi >= n) return;
     const uint32_t x = (uint32_t)(start + xi);
     uint64_t* cand = cand_all + xi * (n - 1);
     // candidate dists d(x, others) with x as the pivot
-    const float* xr = data + (size_t)x * D;
-    for (int e = lane; e < D; e += 32) srow[e] = xr[e];
-    const float xn = norms[x];
-    __syncwarp();
+    m.load_pivot(pv, x);
     for (int64_t j = lane; j < n - 1; j += 32) {
         const uint32_t o = (uint32_t)(start + (j < xi ? j : j + 1));
-        cand[j] = pack_key(pair_dist(data, norms, D, srow, xn, o), o);
+        cand[j] = key_of(m.dist(pv, o), o);
     }
     __syncwarp();
     int32_t* ki = kept_ids + xi * R;
-    float* kd = kept_d + xi * R;
-    const int k = warp_prune(cand, (int)(n - 1), alpha2, R, data, norms, D, srow, ki, kd);
+    uint32_t* kd = kept_d + xi * R;
+    const int k = warp_prune(cand, (int)(n - 1), alpha2, R, m, pv, ki, kd);
     write_row(adj, deg, R, x, ki, k);
 }
 
 // ---- phase 2: prune each new vertex's visited trace, emit reverse triples ----
+// Trace distances are the search keys' 32-bit words (tdst holds their bits).
+template <class M>
 __global__ void __launch_bounds__(BW * 32)
-phase2_kernel(const float* __restrict__ data, const float* __restrict__ norms, int D, int64_t start, int64_t nb,
-              double alpha2, int R, const int32_t* __restrict__ hops, const int32_t* __restrict__ tids,
-              const float* __restrict__ tdst, int cap, int reverse_all, uint64_t* __restrict__ cand_all,
-              int32_t* __restrict__ kept_ids, float* __restrict__ kept_d, int32_t* __restrict__ adj,
-              int32_t* __restrict__ deg, uint32_t* __restrict__ tri_target, uint64_t* __restrict__ tri_key, int W,
-              int crows, int rstride) {
-    extern __shared__ __align__(16) float sh[];
+phase2_kernel(const M m, int64_t start, int64_t nb, double alpha2, int R, const int32_t* __restrict__ hops,
+              const int32_t* __restrict__ tids, const uint32_t* __restrict__ tdst, int cap, int reverse_all,
+              uint64_t* __restrict__ cand_all, int32_t* __restrict__ kept_ids, uint32_t* __restrict__ kept_d,
+              int32_t* __restrict__ adj, int32_t* __restrict__ deg, uint32_t* __restrict__ tri_target,
+              uint64_t* __restrict__ tri_key, int W, int crows) {
+    extern __shared__ __align__(16) uint32_t shw[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int per_warp = ((D + 3) & ~3) + crows * rstride + ((crows + 3) & ~3);
-    float* srow = sh + (size_t)warp * per_warp;
-    float* rows = srow + ((D + 3) & ~3);
-    float* cn = rows + (size_t)crows * rstride;
+    uint32_t* pv = shw + (size_t)warp * vertex_warp_words(m, crows);
+    uint32_t* rows = pv + m.pivot_words();
+    uint32_t* cn = rows + (size_t)crows * m.stage_stride_words();
     const int64_t xi = (int64_t)blockIdx.x * BW + warp;
     if (xi >= nb) return;
     const uint32_t x = (uint32_t)(start + xi);
     const int h = min(hops[xi], cap);
     uint64_t* cand = cand_all + xi * cap;
     const int32_t* ti = tids + xi * cap;
-    const float* td = tdst + xi * cap;
-    for (int j = lane; j < h; j += 32) cand[j] = pack_key(td[j], (uint32_t)ti[j]);
+    const uint32_t* td = tdst + xi * cap;
+    for (int j = lane; j < h; j += 32) cand[j] = key_of(td[j], (uint32_t)ti[j]);
     __syncwarp();
     int32_t* ki = kept_ids + xi * R;
-    float* kd = kept_d + xi * R;
+    uint32_t* kd = kept_d + xi * R;
     int k;
     if (h <= crows) {
-        stage_rows(rows, rstride, cn, cand, h, data, norms, D);
-        k = warp_prune_staged(cand, h, alpha2, R, rows, rstride, cn, D, ki, kd);
+        m.stage(rows, cn, cand, h);
+        k = warp_prune_staged(cand, h, alpha2, R, m, rows, cn, ki, kd);
     } else {
-        k = warp_prune(cand, h, alpha2, R, data, norms, D, srow, ki, kd);
+        k = warp_prune(cand, h, alpha2, R, m, pv, ki, kd);
     }
     write_row(adj, deg, R, x, ki, k);
     // reverse triples (target, source=x, dist): kept edges, or the whole trace
@@ -236,10 +210,8 @@ phase2_kernel(const float* __restrict__ data, const float* __restrict__ norms, i
     const int ne = reverse_all ? h : k;
     for (int j = lane; j < W; j += 32) {
         if (j < ne) {
-            const uint32_t t = reverse_all ? (uint32_t)ti[j] : (uint32_t)ki[j];
-            const float d = reverse_all ? td[j] : kd[j];
-            tt[j] = t;
-            tk[j] = ((uint64_t)__float_as_uint(d) << 32) | x;
+            tt[j] = reverse_all ? (uint32_t)ti[j] : (uint32_t)ki[j];
+            tk[j] = key_of(reverse_all ? td[j] : kd[j], x);
         } else {
             tt[j] = NO_TARGET;
             tk[j] = UMAX;
@@ -252,36 +224,33 @@ phase2_kernel(const float* __restrict__ data, const float* __restrict__ norms, i
 // its current neighbours missing from the trace (distances d(x, e) with x as the
 // pivot); robust prune at the final alpha; rewrite x's row; reverse triples for
 // the kept edges. Only warp x reads or writes row x, so the batch is parallel.
+template <class M>
 __global__ void __launch_bounds__(BW * 32)
-refine_prune_kernel(const float* __restrict__ data, const float* __restrict__ norms, int D, int64_t start, int64_t nb,
-                    double alpha2, int R, const int32_t* __restrict__ hops, const int32_t* __restrict__ tids,
-                    const float* __restrict__ tdst, int cap, uint64_t* __restrict__ cand_all,
-                    int32_t* __restrict__ kept_ids, float* __restrict__ kept_d, int32_t* __restrict__ adj,
-                    int32_t* __restrict__ deg, uint32_t* __restrict__ tri_target, uint64_t* __restrict__ tri_key,
-                    int crows, int rstride, int32_t* __restrict__ ncand) {
-    extern __shared__ __align__(16) float sh[];
+refine_prune_kernel(const M m, int64_t start, int64_t nb, double alpha2, int R, const int32_t* __restrict__ hops,
+                    const int32_t* __restrict__ tids, const uint32_t* __restrict__ tdst, int cap,
+                    uint64_t* __restrict__ cand_all, int32_t* __restrict__ kept_ids, uint32_t* __restrict__ kept_d,
+                    int32_t* __restrict__ adj, int32_t* __restrict__ deg, uint32_t* __restrict__ tri_target,
+                    uint64_t* __restrict__ tri_key, int crows, int32_t* __restrict__ ncand) {
+    extern __shared__ __align__(16) uint32_t shw[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int per_warp = ((D + 3) & ~3) + crows * rstride + ((crows + 3) & ~3);
-    float* srow = sh + (size_t)warp * per_warp;
-    float* rows = srow + ((D + 3) & ~3);
-    float* cn = rows + (size_t)crows * rstride;
+    uint32_t* pv = shw + (size_t)warp * vertex_warp_words(m, crows);
+    uint32_t* rows = pv + m.pivot_words();
+    uint32_t* cn = rows + (size_t)crows * m.stage_stride_words();
     const int64_t xi = (int64_t)blockIdx.x * BW + warp;
     if (xi >= nb) return;
     const uint32_t x = (uint32_t)(start + xi);
     const int h = min(hops[xi], cap);
     uint64_t* cand = cand_all + xi * (int64_t)(cap + R);
     const int32_t* ti = tids + xi * (int64_t)cap;
-    const float* td = tdst + xi * (int64_t)cap;
-    const float* xr = data + (size_t)x * D;
-    for (int e = lane; e < D; e += 32) srow[e] = xr[e];
-    const float xn = norms[x];
+    const uint32_t* td = tdst + xi * (int64_t)cap;
+    m.load_pivot(pv, x);
     int n = 0;
     for (int b = 0; b < h; b += 32) {  // the visited trace, x excluded (keep = cand_ids != x)
         const int j = b + lane;
         const bool ok = j < h && (uint32_t)ti[j] != x;
-        const uint32_t m = __ballot_sync(0xFFFFFFFFu, ok);
-        if (ok) cand[n + __popc(m & lanemask_lt())] = pack_key(td[j], (uint32_t)ti[j]);
-        n += __popc(m);
+        const uint32_t msk = __ballot_sync(0xFFFFFFFFu, ok);
+        if (ok) cand[n + __popc(msk & lanemask_lt())] = key_of(td[j], (uint32_t)ti[j]);
+        n += __popc(msk);
     }
     __syncwarp();
     const int hd = deg[x];
@@ -294,20 +263,20 @@ refine_prune_kernel(const float* __restrict__ data, const float* __restrict__ no
             extra = true;
             for (int j = 0; j < h; ++j) extra &= (ti[j] != id);
         }
-        const uint32_t m = __ballot_sync(0xFFFFFFFFu, extra);
-        if (extra) cand[n + __popc(m & lanemask_lt())] = pack_key(pair_dist(data, norms, D, srow, xn, (uint32_t)id), (uint32_t)id);
-        n += __popc(m);
+        const uint32_t msk = __ballot_sync(0xFFFFFFFFu, extra);
+        if (extra) cand[n + __popc(msk & lanemask_lt())] = key_of(m.dist(pv, (uint32_t)id), (uint32_t)id);
+        n += __popc(msk);
     }
     __syncwarp();
     if (lane == 0) ncand[xi] = n;
     int32_t* ki = kept_ids + xi * R;
-    float* kd = kept_d + xi * R;
+    uint32_t* kd = kept_d + xi * R;
     int k;
     if (n <= crows) {
-        stage_rows(rows, rstride, cn, cand, n, data, norms, D);
-        k = warp_prune_staged(cand, n, alpha2, R, rows, rstride, cn, D, ki, kd);
+        m.stage(rows, cn, cand, n);
+        k = warp_prune_staged(cand, n, alpha2, R, m, rows, cn, ki, kd);
     } else {
-        k = warp_prune(cand, n, alpha2, R, data, norms, D, srow, ki, kd);
+        k = warp_prune(cand, n, alpha2, R, m, pv, ki, kd);
     }
     __syncwarp();
     write_row(adj, deg, R, x, ki, k);
@@ -315,20 +284,19 @@ refine_prune_kernel(const float* __restrict__ data, const float* __restrict__ no
     uint64_t* tk = tri_key + xi * R;
     for (int j = lane; j < R; j += 32) {
         tt[j] = j < k ? (uint32_t)ki[j] : NO_TARGET;
-        tk[j] = j < k ? (((uint64_t)__float_as_uint(kd[j]) << 32) | x) : UMAX;
+        tk[j] = j < k ? key_of(kd[j], x) : UMAX;
     }
 }
 
-// ---- batched standalone robust prune (graph.py:174-228) ----------------------
+// ---- batched standalone robust prune (graph.py:174-228), f32 rows ------------
 __global__ void __launch_bounds__(BW * 32)
-prune_batch_kernel(const float* __restrict__ data, const float* __restrict__ norms, int D,
-                   const int64_t* __restrict__ pivots, int64_t count, const int64_t* __restrict__ offsets,
-                   const int32_t* __restrict__ cids, const float* __restrict__ cd, double alpha2, int R,
-                   uint64_t* __restrict__ cand_all, int32_t* __restrict__ out_ids, float* __restrict__ out_d,
-                   int32_t* __restrict__ out_n) {
-    extern __shared__ __align__(16) float sh[];
+prune_batch_kernel(const F32Metric m, const int64_t* __restrict__ pivots, int64_t count,
+                   const int64_t* __restrict__ offsets, const int32_t* __restrict__ cids, const float* __restrict__ cd,
+                   double alpha2, int R, uint64_t* __restrict__ cand_all, int32_t* __restrict__ out_ids,
+                   float* __restrict__ out_d, int32_t* __restrict__ out_n) {
+    extern __shared__ __align__(16) uint32_t shw[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    float* srow = sh + warp * ((D + 3) & ~3);
+    uint32_t* pv = shw + warp * m.pivot_words();
     const int64_t i = (int64_t)blockIdx.x * BW + warp;
     if (i >= count) return;
     const int64_t o0 = offsets[i], o1 = offsets[i + 1];
@@ -336,7 +304,7 @@ prune_batch_kernel(const float* __restrict__ data, const float* __restrict__ nor
     uint64_t* cand = cand_all + o0;
     for (int j = lane; j < n; j += 32) cand[j] = pack_key(cd[o0 + j], (uint32_t)cids[o0 + j]);
     __syncwarp();
-    const int k = warp_prune(cand, n, alpha2, R, data, norms, D, srow, out_ids + i * R, out_d + i * R);
+    const int k = warp_prune(cand, n, alpha2, R, m, pv, out_ids + i * R, reinterpret_cast<uint32_t*>(out_d + i * R));
     if (lane == 0) out_n[i] = k;
     (void)pivots;
 }
@@ -349,29 +317,30 @@ __global__ void seg_head_kernel(const uint32_t* __restrict__ t, int64_t n, uint8
 }
 
 constexpr int OWNER_SC = 256;  // smem candidate slots per owner warp
-__host__ __device__ inline int owner_per_warp(int R, int D, int crows, int rstride) {
-    return ((OWNER_SC * 8 + R * 4 * 3 + ((D + 3) & ~3) * 4 + crows * rstride * 4 + ((crows + 3) & ~3) * 4) + 15) & ~15;
+// per-warp bytes: keys | vertex words (pivot, staged rows, norms) | have, kid, kd
+template <class M>
+__host__ __device__ inline int owner_per_warp(const M& m, int R, int crows) {
+    return ((OWNER_SC * 8 + vertex_warp_words(m, crows) * 4 + R * 4 * 3) + 15) & ~15;
 }
 
+template <class M>
 __global__ void __launch_bounds__(BW * 32)
-owner_merge_kernel(const float* __restrict__ data, const float* __restrict__ norms, int D, double alpha2, int R,
-                   int always_prune, const uint32_t* __restrict__ tgt, const uint64_t* __restrict__ key, int64_t total,
-                   const int32_t* __restrict__ seg_start, const int* __restrict__ n_seg, uint64_t* __restrict__ pool,
-                   unsigned long long* __restrict__ pool_top, int pool_cap, int32_t* __restrict__ adj,
-                   int32_t* __restrict__ deg, int* __restrict__ err, int crows, int rstride) {
+owner_merge_kernel(const M m, double alpha2, int R, int always_prune, const uint32_t* __restrict__ tgt,
+                   const uint64_t* __restrict__ key, int64_t total, const int32_t* __restrict__ seg_start,
+                   const int* __restrict__ n_seg, uint64_t* __restrict__ pool, unsigned long long* __restrict__ pool_top,
+                   int pool_cap, int32_t* __restrict__ adj, int32_t* __restrict__ deg, int* __restrict__ err, int crows) {
     extern __shared__ __align__(16) unsigned char shb[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     constexpr int SC = OWNER_SC;
-    const int per_warp = owner_per_warp(R, D, crows, rstride);
+    const int per_warp = owner_per_warp(m, R, crows);
     unsigned char* base = shb + (size_t)warp * per_warp;
-    // per-warp layout, 16 B aligned pieces first: keys | star row | staged rows | norms | small arrays
     uint64_t* scand = reinterpret_cast<uint64_t*>(base);
-    float* srow = reinterpret_cast<float*>(base + SC * 8);
-    float* rows = srow + ((D + 3) & ~3);
-    float* cn = rows + (size_t)crows * rstride;
-    int32_t* have = reinterpret_cast<int32_t*>(cn + ((crows + 3) & ~3));
+    uint32_t* pv = reinterpret_cast<uint32_t*>(base + SC * 8);
+    uint32_t* rows = pv + m.pivot_words();
+    uint32_t* cn = rows + (size_t)crows * m.stage_stride_words();
+    int32_t* have = reinterpret_cast<int32_t*>(pv + vertex_warp_words(m, crows));
     int32_t* kid = have + R;
-    float* kd = reinterpret_cast<float*>(kid + R);
+    uint32_t* kd = reinterpret_cast<uint32_t*>(kid + R);
     const int64_t s = (int64_t)blockIdx.x * BW + warp;
     if (s >= *n_seg) return;
     const int64_t g0 = seg_start[s];
@@ -380,9 +349,9 @@ owner_merge_kernel(const float* __restrict__ data, const float* __restrict__ nor
     for (;;) {  // group end: first index whose target differs
         const int64_t i = g1 + lane;
         const bool same = i < total && tgt[i] == t;
-        const uint32_t m = __ballot_sync(0xFFFFFFFFu, same);
-        g1 += __popc(m);
-        if (m != 0xFFFFFFFFu) break;
+        const uint32_t msk = __ballot_sync(0xFFFFFFFFu, same);
+        g1 += __popc(msk);
+        if (msk != 0xFFFFFFFFu) break;
     }
     const int g = (int)(g1 - g0);
     const int hd = deg[t];
@@ -412,43 +381,36 @@ owner_merge_kernel(const float* __restrict__ data, const float* __restrict__ nor
             fresh = true;
             for (int e = 0; e < hd; ++e) fresh &= (have[e] != src);
         }
-        const uint32_t m = __ballot_sync(0xFFFFFFFFu, fresh);
-        if (fresh) cand[hd + nf + __popc(m & lanemask_lt())] = k;
-        nf += __popc(m);
+        const uint32_t msk = __ballot_sync(0xFFFFFFFFu, fresh);
+        if (fresh) cand[hd + nf + __popc(msk & lanemask_lt())] = k;
+        nf += __popc(msk);
     }
     __syncwarp();
     if (nf == 0) return;
     if (!always_prune && hd + nf <= R) {  // append in (dist, source) order
-        for (int j = lane; j < nf; j += 32) {
-            adj[(size_t)t * R + hd + j] = (int32_t)(cand[hd + j] & 0xFFFFFFFFull);
-        }
+        for (int j = lane; j < nf; j += 32) adj[(size_t)t * R + hd + j] = (int32_t)(cand[hd + j] & 0xFFFFFFFFull);
         if (lane == 0) deg[t] = hd + nf;
         return;
     }
     // existing neighbours get recomputed distances d(t, e) (target is the pivot);
     // fresh entries already hold (stored triple dist << 32 | source) keys
-    const float* tr = data + (size_t)t * D;
-    for (int e = lane; e < D; e += 32) srow[e] = tr[e];
-    const float tn = norms[t];
+    m.load_pivot(pv, t);
     const int n = hd + nf;
     int k;
     if (n <= crows) {
         for (int j = lane; j < hd; j += 32) cand[j] = (uint64_t)(uint32_t)have[j];  // id only, for staging
         __syncwarp();
-        stage_rows(rows, rstride, cn, cand, n, data, norms, D);
-        for (int j = lane; j < hd; j += 32)
-            cand[j] = pack_key(exact_from_dot(cn[j], a1_rows(rows + (size_t)j * rstride, srow, D), tn),
-                               (uint32_t)have[j]);
+        m.stage(rows, cn, cand, n);
+        for (int j = lane; j < hd; j += 32) cand[j] = key_of(m.dist(pv, (uint32_t)have[j]), (uint32_t)have[j]);
         __syncwarp();
-        k = warp_prune_staged(cand, n, alpha2, R, rows, rstride, cn, D, kid, kd);
+        k = warp_prune_staged(cand, n, alpha2, R, m, rows, cn, kid, kd);
     } else {
-        __syncwarp();
         for (int j = lane; j < hd; j += 32) {
             const uint32_t e = (uint32_t)have[j];
-            cand[j] = pack_key(pair_dist(data, norms, D, srow, tn, e), e);
+            cand[j] = key_of(m.dist(pv, e), e);
         }
         __syncwarp();
-        k = warp_prune(cand, n, alpha2, R, data, norms, D, srow, kid, kd);
+        k = warp_prune(cand, n, alpha2, R, m, pv, kid, kd);
     }
     write_row(adj, deg, R, t, kid, k);
 }
@@ -611,6 +573,51 @@ donor_scan_kernel(const float* __restrict__ data, const float* __restrict__ norm
     }
 }
 
+// Generic nearest-donor scan (any metric): block = 8 warps = 8 stranded pivots
+// staged in smem, each warp scans a slice of the reachable list one row per lane
+// and keeps a running top-`fan` by (dist, id) key. Output layout as donor_scan_kernel.
+template <class M>
+__global__ void __launch_bounds__(256)
+donor_scan_generic_kernel(const M m, const int32_t* __restrict__ lost, int nlost, const int32_t* __restrict__ reach,
+                          int nreach, int slices, int fan, uint64_t* __restrict__ part) {
+    extern __shared__ __align__(16) uint32_t gsh[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    uint32_t* pv = gsh + warp * m.pivot_words();
+    uint64_t* top = reinterpret_cast<uint64_t*>(gsh + 8 * m.pivot_words()) + warp * (FAN + 64);
+    uint64_t* mb = top + FAN;  // 64-slot merge buffer (with top: 80 keys, sorted as 128)
+    const int si = blockIdx.x * 8 + warp;
+    if (si >= nlost) return;
+    const int slice = blockIdx.y;
+    const int64_t per = (nreach + slices - 1) / slices;
+    const int64_t r_begin = slice * per, r_end = (nreach < r_begin + per) ? (int64_t)nreach : r_begin + per;
+    m.load_pivot(pv, (uint32_t)lost[si]);
+    if (lane < FAN) top[lane] = UMAX;
+    __syncwarp();
+    __shared__ uint64_t sortbuf[8][128];
+    for (int64_t r0 = r_begin; r0 < r_end; r0 += 32) {
+        const int64_t ri = r0 + lane;
+        uint64_t k = UMAX;
+        if (ri < r_end) {
+            const uint32_t r = (uint32_t)reach[ri];
+            k = key_of(m.dist(pv, r), r);
+        }
+        const uint64_t worst = top[fan - 1];
+        if (k >= worst) k = UMAX;
+        if (!__any_sync(0xFFFFFFFFu, k != UMAX)) continue;
+        uint64_t* sb = sortbuf[warp];
+        sb[lane] = lane < fan ? top[lane] : UMAX;
+        sb[32 + lane] = k;
+        sb[64 + lane] = UMAX;
+        sb[96 + lane] = UMAX;
+        __syncwarp();
+        warp_bitonic_sort_smem(sb, 128);
+        if (lane < fan) top[lane] = sb[lane];
+        __syncwarp();
+    }
+    (void)mb;
+    if (lane < fan) part[((size_t)slice * nlost + si) * fan + lane] = top[lane];
+}
+
 // merge slice top-lists: warp per stranded vertex; writes donors and the sort key
 // (nearest-donor dist bits << 32 | stranded id) for the processing order.
 __global__ void donor_merge_kernel(const uint64_t* __restrict__ part, int slices, int nlost, int fan,
@@ -646,14 +653,14 @@ __global__ void donor_merge_kernel(const uint64_t* __restrict__ part, int slices
 }
 
 // ---- repair: ordered sequential attach (build.py:193-224), one warp ----------
-__global__ void attach_kernel(const float* __restrict__ data, const float* __restrict__ norms, int D,
-                              int32_t* __restrict__ adj, int32_t* __restrict__ deg, int R, uint8_t* __restrict__ pinned,
+template <class M>
+__global__ void attach_kernel(const M m, int32_t* __restrict__ adj, int32_t* __restrict__ deg, int R, uint8_t* __restrict__ pinned,
                               int32_t* __restrict__ seen, const int32_t* __restrict__ lost,
                               const int32_t* __restrict__ order, int nlost, const int32_t* __restrict__ donors, int fan,
                               int32_t* __restrict__ queue, unsigned long long* __restrict__ bridges,
                               int* __restrict__ err, int32_t* __restrict__ err_vertex) {
-    extern __shared__ __align__(16) float ash[];
-    float* urow = ash;
+    extern __shared__ __align__(16) uint32_t ash[];
+    uint32_t* pv = ash;
     const int lane = threadIdx.x;
     unsigned long long added = 0;
     for (int oi = 0; oi < nlost; ++oi) {
@@ -668,20 +675,18 @@ __global__ void attach_kernel(const float* __restrict__ data, const float* __res
             int32_t* row = adj + (size_t)u * R;
             uint8_t* pin = pinned + (size_t)u * R;
             if (du >= R) {
-                // farthest non-pinned neighbour by d(u, e) (u is the pivot), first index on ties
-                const float* ur = data + (size_t)u * D;
-                for (int e = lane; e < D; e += 32) urow[e] = ur[e];
-                __syncwarp();
-                const float un = norms[u];
-                float bestd = -1.0f;
+                // farthest non-pinned neighbour by d(u, e) (u is the pivot), first index on
+                // ties; distance words compare like the distances (non-negative)
+                m.load_pivot(pv, (uint32_t)u);
+                long long bestd = -1;
                 int bests = R;
                 for (int s = lane; s < du; s += 32) {
                     if (pin[s]) continue;
-                    const float d = pair_dist(data, norms, D, urow, un, (uint32_t)row[s]);
+                    const long long d = (long long)m.dist(pv, (uint32_t)row[s]);
                     if (d > bestd || (d == bestd && s < bests)) { bestd = d; bests = s; }
                 }
                 for (int o = 16; o > 0; o >>= 1) {
-                    const float od = __shfl_xor_sync(0xFFFFFFFFu, bestd, o);
+                    const long long od = __shfl_xor_sync(0xFFFFFFFFu, bestd, o);
                     const int os = __shfl_xor_sync(0xFFFFFFFFu, bests, o);
                     if (od > bestd || (od == bestd && os < bests)) { bestd = od; bests = os; }
                 }
@@ -749,7 +754,16 @@ struct Bufs {
     T* var = bufs.get<T>((n), st, _ce);         \
     JB_CUDA(_ce);
 
-static int repair(const jb_insert_args& a, int64_t n_active, int64_t entry, cudaStream_t st, int64_t* bridges_out) {
+// Per-warp candidate-row staging budget (~26 KB per warp beside the pivot).
+template <class M>
+static int staged_rows(const M& m, int want, int R) {
+    int crows = std::min(want, (26 * 1024 - m.pivot_words() * 4) / (m.stage_stride_words() * 4 + 4));
+    return crows < R + 1 ? 0 : crows;
+}
+
+template <class M>
+static int repair(const M& m, const jb_insert_args& a, int64_t n_active, int64_t entry, cudaStream_t st,
+                  int64_t* bridges_out) {
     *bridges_out = 0;
     if (n_active < 2) return JB_OK;
     const int R = a.degree_cap, D = a.dims;
@@ -797,20 +811,34 @@ static int repair(const jb_insert_args& a, int64_t n_active, int64_t entry, cuda
         if (getenv("JB_PROFILE") && getenv("JB_PROFILE")[0] == '1')
             fprintf(stderr, "[jb]   repair round %d: stranded %d reachable %d\n", round, nlost, nreach);
         if (nlost == 0) break;
-        // donors
-        const int sblocks = (nlost + DT - 1) / DT;
-        int slices = std::max(1, std::min(64, (4 * sm_count_current() + sblocks - 1) / sblocks));
-        slices = (int)std::min<int64_t>(slices, std::max<int64_t>(1, (nreach + DT - 1) / DT));
-        BALLOC(part, uint64_t, (size_t)slices * nlost * fan);
+        // donors: top-`fan` reachable by (d(x, r), r) for every stranded x (build.py:185-192)
         BALLOC(donors, int32_t, (size_t)nlost * fan);
         BALLOC(okey, uint64_t, nlost);
         BALLOC(oval, int32_t, nlost);
         BALLOC(okey2, uint64_t, nlost);
         BALLOC(oval2, int32_t, nlost);
-        const size_t dsm = (size_t)(2 * DT * 17 + DT * (DT + 1)) * 4 + DT * FAN * 8 + 8 * 128 * 8;
-        JB_CUDA(cudaFuncSetAttribute(donor_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
-        donor_scan_kernel<<<dim3(sblocks, slices), 256, dsm, st>>>(a.data, a.data_norms, D, lost, nlost, reach, nreach,
-                                                                  slices, fan, part);
+        int slices;
+        uint64_t* part;
+        if (std::is_same<M, F32Metric>::value) {  // tiled A1 scan on the f32 rows
+            const int sblocks = (nlost + DT - 1) / DT;
+            slices = std::max(1, std::min(64, (4 * sm_count_current() + sblocks - 1) / sblocks));
+            slices = (int)std::min<int64_t>(slices, std::max<int64_t>(1, (nreach + DT - 1) / DT));
+            part = bufs.get<uint64_t>((size_t)slices * nlost * fan, st, _ce); JB_CUDA(_ce);
+            const size_t dsm = (size_t)(2 * DT * 17 + DT * (DT + 1)) * 4 + DT * FAN * 8 + 8 * 128 * 8;
+            JB_CUDA(cudaFuncSetAttribute(donor_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
+            donor_scan_kernel<<<dim3(sblocks, slices), 256, dsm, st>>>(a.data, a.data_norms, D, lost, nlost, reach,
+                                                                      nreach, slices, fan, part);
+        } else {
+            const int sblocks = (nlost + 7) / 8;
+            slices = std::max(1, std::min(64, (8 * sm_count_current() + sblocks - 1) / sblocks));
+            slices = (int)std::min<int64_t>(slices, std::max<int64_t>(1, (nreach + 31) / 32));
+            part = bufs.get<uint64_t>((size_t)slices * nlost * fan, st, _ce); JB_CUDA(_ce);
+            const size_t gsm = (size_t)8 * m.pivot_words() * 4 + 8 * (FAN + 64) * 8;
+            JB_CUDA(cudaFuncSetAttribute(donor_scan_generic_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)gsm));
+            donor_scan_generic_kernel<M><<<dim3(sblocks, slices), 256, gsm, st>>>(m, lost, nlost, reach, nreach, slices,
+                                                                                 fan, part);
+        }
         JB_LAUNCH_CHECK();
         donor_merge_kernel<<<(unsigned)((nlost * 32 + 255) / 256), 256, 0, st>>>(part, slices, nlost, fan, lost, donors,
                                                                                okey, oval);
@@ -819,9 +847,10 @@ static int repair(const jb_insert_args& a, int64_t n_active, int64_t entry, cuda
         cub::DeviceRadixSort::SortPairs(nullptr, tb, okey, okey2, oval, oval2, nlost, 0, 64, st);
         BALLOC(tmp, unsigned char, tb);
         JB_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, okey, okey2, oval, oval2, nlost, 0, 64, st));
-        const int asm_bytes = ((D + 3) & ~3) * 4;
-        attach_kernel<<<1, 32, asm_bytes, st>>>(a.data, a.data_norms, D, a.adjacency, a.degrees, R, pinned, seen, lost,
-                                                oval2, nlost, donors, fan, fa, bridges, err, err + 1);
+        const int asm_bytes = m.pivot_words() * 4;
+        JB_CUDA(cudaFuncSetAttribute(attach_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, asm_bytes));
+        attach_kernel<M><<<1, 32, asm_bytes, st>>>(m, a.adjacency, a.degrees, R, pinned, seen, lost, oval2, nlost,
+                                                    donors, fan, fa, bridges, err, err + 1);
         JB_LAUNCH_CHECK();
         int herr[2];
         JB_CUDA(cudaMemcpyAsync(herr, err, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -842,8 +871,9 @@ static int repair(const jb_insert_args& a, int64_t n_active, int64_t entry, cuda
 // Phase-1 search with visited-trace capture: queries are rows [q0, q0 + nq) of the
 // dataset, the graph shows `active` vertices. The trace capacity is generous
 // (8 B per slot); a longer trace re-runs the batch with an exact-size buffer.
+// Trace distances are the keys' 32-bit words (f32 bits, or u32 integer distances).
 static int trace_search(const jb_insert_args& a, int64_t q0, int64_t nq, int64_t active, int64_t entry, Bufs& bufs,
-                        cudaStream_t st, int& cap, int32_t*& hops, int32_t*& evals, int32_t*& tids, float*& tdst) {
+                        cudaStream_t st, int& cap, int32_t*& hops, int32_t*& evals, int32_t*& tids, uint32_t*& tdst) {
     cudaError_t _ce;
     const int R = a.degree_cap, D = a.dims, L = a.build_beam_width;
     cap = std::max(4 * L, L + 512);
@@ -855,14 +885,22 @@ static int trace_search(const jb_insert_args& a, int64_t q0, int64_t nq, int64_t
     evals = ev;
     for (int attempt = 0; attempt < 2; ++attempt) {
         tids = bufs.get<int32_t>((size_t)nq * cap, st, _ce); JB_CUDA(_ce);
-        tdst = bufs.get<float>((size_t)nq * cap, st, _ce); JB_CUDA(_ce);
+        tdst = bufs.get<uint32_t>((size_t)nq * cap, st, _ce); JB_CUDA(_ce);
         jb_search_args s{};
-        s.adjacency = a.adjacency; s.degree_cap = R; s.active_count = active;
-        s.source = JB_SRC_EXACT; s.dims = D; s.data = a.data; s.data_norms = a.data_norms;
-        s.queries = a.data + (size_t)q0 * D; s.query_add = a.data_norms + q0;
+        s.adjacency = a.adjacency; s.degree_cap = R; s.active_count = active; s.dims = D;
+        if (a.element_kind == JB_KIND_U8) {
+            s.source = JB_SRC_EXACT_U8;
+            s.data_u8 = a.data_u8; s.norms_u32 = a.norms_u32;
+            s.queries_u8 = a.data_u8 + (size_t)q0 * D; s.query_norms_u32 = a.norms_u32 + q0;
+        } else {
+            s.source = JB_SRC_EXACT;
+            s.data = a.data; s.data_norms = a.data_norms;
+            s.queries = a.data + (size_t)q0 * D; s.query_add = a.data_norms + q0;
+        }
         s.nq = nq; s.starts = nullptr; s.start_vertex = entry;
         s.beam_width = L; s.hash_slots = 0; s.trace_cap = cap;
-        s.frontier_keys = fk; s.hops = h; s.evals = ev; s.trace_ids = tids; s.trace_dists = tdst; s.flags = flags;
+        s.frontier_keys = fk; s.hops = h; s.evals = ev; s.trace_ids = tids;
+        s.trace_dists = reinterpret_cast<float*>(tdst); s.flags = flags;
         int rc = jb_beam_search(&s, st);
         if (rc) return rc;
         size_t tb = 0;
@@ -881,10 +919,11 @@ static int trace_search(const jb_insert_args& a, int64_t q0, int64_t nq, int64_t
 
 // Phase 3 (build.py:269-293): (target, dist, source) order via two stable radix
 // sorts of the reverse triples, segment heads, one owner warp per target.
-static int merge_phase(const jb_insert_args& a, double alpha2, uint32_t* tt, uint64_t* tk, int64_t ntri, int rstride,
+template <class M>
+static int merge_phase(const M& m, const jb_insert_args& a, double alpha2, uint32_t* tt, uint64_t* tk, int64_t ntri,
                        Bufs& bufs, cudaStream_t st, int& hseg) {
     cudaError_t _ce;
-    const int R = a.degree_cap, D = a.dims;
+    const int R = a.degree_cap;
     BALLOC(tt2, uint32_t, ntri);
     BALLOC(tk2, uint64_t, ntri);
     {
@@ -918,14 +957,13 @@ static int merge_phase(const jb_insert_args& a, double alpha2, uint32_t* tt, uin
         BALLOC(err, int, 1);
         JB_CUDA(cudaMemsetAsync(ptop, 0, sizeof(unsigned long long), st));
         JB_CUDA(cudaMemsetAsync(err, 0, sizeof(int), st));
-        // owners stage up to R + 16 candidate rows in smem when they fit in ~26 KB
-        int crows = std::min(R + 16, (26 * 1024) / (rstride * 4 + 4));
-        if (crows < R + 1) crows = 0;
-        const int osm = owner_per_warp(R, D, crows, rstride) * BW;
-        JB_CUDA(cudaFuncSetAttribute(owner_merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, osm));
-        owner_merge_kernel<<<(unsigned)((hseg + BW - 1) / BW), BW * 32, osm, st>>>(
-            a.data, a.data_norms, D, alpha2, R, a.always_prune, tt, tk, ntri, seg, nseg, pool, ptop, pool_cap,
-            a.adjacency, a.degrees, err, crows, rstride);
+        // owners stage up to R + 16 candidate rows in smem when they fit
+        const int crows = staged_rows(m, R + 16, R);
+        const int osm = owner_per_warp(m, R, crows) * BW;
+        JB_CUDA(cudaFuncSetAttribute(owner_merge_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, osm));
+        owner_merge_kernel<M><<<(unsigned)((hseg + BW - 1) / BW), BW * 32, osm, st>>>(
+            m, alpha2, R, a.always_prune, tt, tk, ntri, seg, nseg, pool, ptop, pool_cap, a.adjacency, a.degrees, err,
+            crows);
         JB_LAUNCH_CHECK();
         int herr = 0;
         JB_CUDA(cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -951,6 +989,17 @@ __global__ void sum2_kernel(const int32_t* __restrict__ v, const int32_t* __rest
         atomicAdd(out, a);
         atomicAdd(out + 1, b);
     }
+}
+
+static int sum2(const int32_t* v, const int32_t* w, int64_t n, Bufs& bufs, cudaStream_t st, unsigned long long out[2]) {
+    cudaError_t _ce;
+    BALLOC(work, unsigned long long, 2);
+    JB_CUDA(cudaMemsetAsync(work, 0, 2 * sizeof(unsigned long long), st));
+    sum2_kernel<<<std::max(1, std::min<int>((int)((n + 255) / 256), 4 * sm_count_current())), 256, 0, st>>>(v, w, n,
+                                                                                                         work);
+    JB_LAUNCH_CHECK();
+    JB_CUDA(cudaMemcpyAsync(out, work, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    return JB_OK;
 }
 
 // JB_PROFILE=1: per-batch phase timings on stderr (stream events; diagnostics only)
@@ -987,7 +1036,15 @@ struct PhaseTimer {
 };
 
 static int validate_insert(const jb_insert_args& a) {
-    JB_CHECK_ARG(a.adjacency && a.degrees && a.data && a.data_norms, "batch insert: missing arrays");
+    JB_CHECK_ARG(a.adjacency && a.degrees, "batch insert: missing graph arrays");
+    JB_CHECK_ARG(a.element_kind == JB_KIND_F32 || a.element_kind == JB_KIND_U8, "unknown element kind %d",
+                 a.element_kind);
+    if (a.element_kind == JB_KIND_U8) {
+        JB_CHECK_ARG(a.data_u8 && a.norms_u32, "batch insert: missing u8 rows / norms");
+        JB_CHECK_ARG((int64_t)a.dims * 255 * 255 < (1ll << 32), "u8 dims too large for 32-bit packed distances");
+    } else {
+        JB_CHECK_ARG(a.data && a.data_norms, "batch insert: missing arrays");
+    }
     JB_CHECK_ARG(a.degree_cap >= 1 && a.dims >= 1, "batch insert: bad shape");
     JB_CHECK_ARG(a.alpha >= 1.0, "alpha must be >= 1");
     JB_CHECK_ARG(a.start >= 0 && a.start <= a.stop, "batch insert: bad range");
@@ -997,30 +1054,9 @@ static int validate_insert(const jb_insert_args& a) {
     return JB_OK;
 }
 
-}  // namespace jb
-
-using namespace jb;
-
-extern "C" {
-
-int jb_repair_connectivity(const jb_insert_args* args, void* stream) {
-    JB_CHECK_ARG(args, "null args");
-    const jb_insert_args& a = *args;
-    int rc = validate_insert(a);
-    if (rc) return rc;
-    int64_t b = 0;
-    rc = repair(a, a.stop, a.entry_point, as_stream(stream), &b);
-    if (a.bridges_out_host) *a.bridges_out_host = b;
-    if (a.entry_point_out_host) *a.entry_point_out_host = a.entry_point;
-    return rc;
-}
-
-int jb_batch_insert(const jb_insert_args* args, void* stream) {
-    JB_CHECK_ARG(args, "null args");
-    const jb_insert_args& a = *args;
-    int rc = validate_insert(a);
-    if (rc) return rc;
-    cudaStream_t st = as_stream(stream);
+template <class M>
+static int batch_insert_impl(const M& m, const jb_insert_args& a, cudaStream_t st) {
+    int rc = 0;
     const int R = a.degree_cap, D = a.dims;
     const double alpha2 = a.alpha * a.alpha;
     int64_t entry = a.entry_point;
@@ -1029,24 +1065,25 @@ int jb_batch_insert(const jb_insert_args* args, void* stream) {
     if (a.bridges_out_host) *a.bridges_out_host = 0;
     if (a.start == a.stop) return JB_OK;
     const int64_t nb = a.stop - a.start;
-    const size_t srow_bytes = (size_t)BW * ((D + 3) & ~3) * 4;
     Bufs bufs;
     cudaError_t _ce;
     PhaseTimer pt(st);
 
     if (a.start == 0) {  // seed batch: medoid entry + mutual pruning (build.py:246-266)
-        rc = jb_medoid(a.data, a.stop, D, &entry, stream);
+        rc = a.element_kind == JB_KIND_U8 ? jb_medoid_u8(a.data_u8, a.stop, D, &entry, st)
+                                          : jb_medoid(a.data, a.stop, D, &entry, st);
         if (rc) return rc;
         if (nb > 1) {
             BALLOC(cand, uint64_t, (size_t)nb * (nb - 1));
             BALLOC(kid, int32_t, (size_t)nb * R);
-            BALLOC(kd, float, (size_t)nb * R);
-            JB_CUDA(cudaFuncSetAttribute(seed_prune_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)srow_bytes));
-            seed_prune_kernel<<<(unsigned)((nb + BW - 1) / BW), BW * 32, srow_bytes, st>>>(
-                a.data, a.data_norms, D, a.start, a.stop, alpha2, R, cand, kid, kd, a.adjacency, a.degrees);
+            BALLOC(kd, uint32_t, (size_t)nb * R);
+            const int smem = BW * m.pivot_words() * 4;
+            JB_CUDA(cudaFuncSetAttribute(seed_prune_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+            seed_prune_kernel<M><<<(unsigned)((nb + BW - 1) / BW), BW * 32, smem, st>>>(
+                m, a.start, a.stop, alpha2, R, cand, kid, kd, a.adjacency, a.degrees);
             JB_LAUNCH_CHECK();
         }
-        rc = repair(a, a.stop, entry, st, &bridges);
+        rc = repair(m, a, a.stop, entry, st, &bridges);
         if (a.entry_point_out_host) *a.entry_point_out_host = entry;
         if (a.bridges_out_host) *a.bridges_out_host = bridges;
         if (a.stats_out_host) {
@@ -1057,51 +1094,42 @@ int jb_batch_insert(const jb_insert_args* args, void* stream) {
     }
 
     // ---- phase 1: batched search of the new rows on the read-only graph ----
-    const int L = a.build_beam_width;
     int cap = 0;
     int32_t *hops = nullptr, *evals = nullptr, *tids = nullptr;
-    float* tdst = nullptr;
+    uint32_t* tdst = nullptr;
     rc = trace_search(a, a.start, nb, a.start, entry, bufs, st, cap, hops, evals, tids, tdst);
     if (rc) return rc;
     unsigned long long hwork[2] = {0, 0};
-    if (a.stats_out_host) {  // phase-1 hops and evals (phase 2 prunes over the same hop traces)
-        BALLOC(work, unsigned long long, 2);
-        JB_CUDA(cudaMemsetAsync(work, 0, 2 * sizeof(unsigned long long), st));
-        sum2_kernel<<<std::max(1, std::min<int>((int)((nb + 255) / 256), 4 * sm_count_current())), 256, 0, st>>>(
-            hops, evals, nb, work);
-        JB_LAUNCH_CHECK();
-        JB_CUDA(cudaMemcpyAsync(hwork, work, sizeof(hwork), cudaMemcpyDeviceToHost, st));
-    }
+    if (a.stats_out_host && (rc = sum2(hops, evals, nb, bufs, st, hwork))) return rc;
     pt.mark("search");
+
     // ---- phase 2: activate, prune each new vertex, emit reverse triples ----
     const int W = a.reverse_all_visited ? cap : R;
     const int64_t ntri = nb * (int64_t)W;
     BALLOC(cand, uint64_t, (size_t)nb * cap);
     BALLOC(kid, int32_t, (size_t)nb * R);
-    BALLOC(kd, float, (size_t)nb * R);
+    BALLOC(kd, uint32_t, (size_t)nb * R);
     BALLOC(tt, uint32_t, ntri);
     BALLOC(tk, uint64_t, ntri);
     // smem-staged candidate rows when a trace fits in ~26 KB per warp; longer traces
     // prune from L1/L2 (staging them would cost more occupancy than it saves)
-    const int rstride = ((D + 3) & ~3) + 4;
-    int crows2 = std::min(cap, (26 * 1024 - ((D + 3) & ~3) * 4) / (rstride * 4 + 4));
-    if (crows2 < R + 1) crows2 = 0;
-    const size_t p2_smem = (size_t)BW * 4 * (((D + 3) & ~3) + crows2 * rstride + ((crows2 + 3) & ~3));
-    JB_CUDA(cudaFuncSetAttribute(phase2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p2_smem));
-    phase2_kernel<<<(unsigned)((nb + BW - 1) / BW), BW * 32, p2_smem, st>>>(
-        a.data, a.data_norms, D, a.start, nb, alpha2, R, hops, tids, tdst, cap, a.reverse_all_visited, cand, kid, kd,
-        a.adjacency, a.degrees, tt, tk, W, crows2, rstride);
+    const int crows2 = staged_rows(m, cap, R);
+    const int p2_smem = BW * 4 * vertex_warp_words(m, crows2);
+    JB_CUDA(cudaFuncSetAttribute(phase2_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, p2_smem));
+    phase2_kernel<M><<<(unsigned)((nb + BW - 1) / BW), BW * 32, p2_smem, st>>>(
+        m, a.start, nb, alpha2, R, hops, tids, tdst, cap, a.reverse_all_visited, cand, kid, kd, a.adjacency, a.degrees,
+        tt, tk, W, crows2);
     JB_LAUNCH_CHECK();
-
     pt.mark("prune");
+
     // ---- phase 3: grouped reverse-edge merge ----
     int hseg = 0;
-    rc = merge_phase(a, alpha2, tt, tk, ntri, rstride, bufs, st, hseg);
+    rc = merge_phase(m, a, alpha2, tt, tk, ntri, bufs, st, hseg);
     if (rc) return rc;
-
     pt.mark("merge");
+
     // ---- connectivity repair over the activated graph ----
-    rc = repair(a, a.stop, entry, st, &bridges);
+    rc = repair(m, a, a.stop, entry, st, &bridges);
     pt.mark("repair");
     pt.report(a.start, a.stop);
     if (pt.on) fprintf(stderr, "[jb]   bridges %lld\n", (long long)bridges);
@@ -1119,6 +1147,85 @@ int jb_batch_insert(const jb_insert_args* args, void* stream) {
     return rc;
 }
 
+template <class M>
+static int refine_batch_impl(const M& m, const jb_insert_args& a, int64_t active, cudaStream_t st) {
+    const int R = a.degree_cap;
+    const double alpha2 = a.alpha * a.alpha;
+    const int64_t nb = a.stop - a.start;
+    Bufs bufs;
+    cudaError_t _ce;
+    PhaseTimer pt(st);
+    int cap = 0;
+    int32_t *hops = nullptr, *evals = nullptr, *tids = nullptr;
+    uint32_t* tdst = nullptr;
+    int rc = trace_search(a, a.start, nb, active, a.entry_point, bufs, st, cap, hops, evals, tids, tdst);
+    if (rc) return rc;
+    pt.mark("search");
+    const int64_t ntri = nb * (int64_t)R;
+    BALLOC(cand, uint64_t, (size_t)nb * (cap + R));
+    BALLOC(kid, int32_t, (size_t)nb * R);
+    BALLOC(kd, uint32_t, (size_t)nb * R);
+    BALLOC(tt, uint32_t, ntri);
+    BALLOC(tk, uint64_t, ntri);
+    BALLOC(ncand, int32_t, nb);
+    const int crows = staged_rows(m, cap + R, R);
+    const int smem = BW * 4 * vertex_warp_words(m, crows);
+    JB_CUDA(cudaFuncSetAttribute(refine_prune_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    refine_prune_kernel<M><<<(unsigned)((nb + BW - 1) / BW), BW * 32, smem, st>>>(
+        m, a.start, nb, alpha2, R, hops, tids, tdst, cap, cand, kid, kd, a.adjacency, a.degrees, tt, tk, crows, ncand);
+    JB_LAUNCH_CHECK();
+    pt.mark("prune");
+    int hseg = 0;
+    rc = merge_phase(m, a, alpha2, tt, tk, ntri, bufs, st, hseg);
+    if (rc) return rc;
+    pt.mark("merge");
+    pt.report(a.start, a.stop);
+    if (a.stats_out_host) {
+        unsigned long long hw[2] = {0, 0}, pc[2] = {0, 0};
+        if ((rc = sum2(hops, evals, nb, bufs, st, hw))) return rc;
+        if ((rc = sum2(ncand, ncand, nb, bufs, st, pc))) return rc;
+        JB_CUDA(cudaStreamSynchronize(st));
+        int64_t* w = a.stats_out_host;
+        w[0] += (int64_t)hw[0];
+        w[1] += (int64_t)hw[1];
+        w[2] += (int64_t)pc[0];
+        w[3] += hseg;
+        w[4] += ntri;
+    }
+    JB_CUDA(cudaStreamSynchronize(st));
+    return JB_OK;
+}
+
+}  // namespace jb
+
+using namespace jb;
+
+extern "C" {
+
+int jb_repair_connectivity(const jb_insert_args* args, void* stream) {
+    JB_CHECK_ARG(args, "null args");
+    const jb_insert_args& a = *args;
+    int rc = validate_insert(a);
+    if (rc) return rc;
+    int64_t b = 0;
+    cudaStream_t st = as_stream(stream);
+    if (a.element_kind == JB_KIND_U8) rc = repair(U8Metric{a.data_u8, a.norms_u32, a.dims}, a, a.stop, a.entry_point, st, &b);
+    else rc = repair(F32Metric{a.data, a.data_norms, a.dims}, a, a.stop, a.entry_point, st, &b);
+    if (a.bridges_out_host) *a.bridges_out_host = b;
+    if (a.entry_point_out_host) *a.entry_point_out_host = a.entry_point;
+    return rc;
+}
+
+int jb_batch_insert(const jb_insert_args* args, void* stream) {
+    JB_CHECK_ARG(args, "null args");
+    const jb_insert_args& a = *args;
+    int rc = validate_insert(a);
+    if (rc) return rc;
+    cudaStream_t st = as_stream(stream);
+    if (a.element_kind == JB_KIND_U8) return batch_insert_impl(U8Metric{a.data_u8, a.norms_u32, a.dims}, a, st);
+    return batch_insert_impl(F32Metric{a.data, a.data_norms, a.dims}, a, st);
+}
+
 int jb_refine_batch(const jb_insert_args* args, void* stream) {
     JB_CHECK_ARG(args, "null args");
     const jb_insert_args& a = *args;
@@ -1131,62 +1238,8 @@ int jb_refine_batch(const jb_insert_args* args, void* stream) {
     if (a.bridges_out_host) *a.bridges_out_host = 0;
     if (a.start == a.stop) return JB_OK;
     cudaStream_t st = as_stream(stream);
-    const int R = a.degree_cap, D = a.dims;
-    const double alpha2 = a.alpha * a.alpha;
-    const int64_t nb = a.stop - a.start;
-    Bufs bufs;
-    cudaError_t _ce;
-    PhaseTimer pt(st);
-    int cap = 0;
-    int32_t *hops = nullptr, *evals = nullptr, *tids = nullptr;
-    float* tdst = nullptr;
-    rc = trace_search(a, a.start, nb, active, a.entry_point, bufs, st, cap, hops, evals, tids, tdst);
-    if (rc) return rc;
-    pt.mark("search");
-    const int64_t ntri = nb * (int64_t)R;
-    BALLOC(cand, uint64_t, (size_t)nb * (cap + R));
-    BALLOC(kid, int32_t, (size_t)nb * R);
-    BALLOC(kd, float, (size_t)nb * R);
-    BALLOC(tt, uint32_t, ntri);
-    BALLOC(tk, uint64_t, ntri);
-    BALLOC(ncand, int32_t, nb);
-    const int rstride = ((D + 3) & ~3) + 4;
-    int crows = std::min(cap + R, (26 * 1024 - ((D + 3) & ~3) * 4) / (rstride * 4 + 4));
-    if (crows < R + 1) crows = 0;
-    const size_t smem = (size_t)BW * 4 * (((D + 3) & ~3) + crows * rstride + ((crows + 3) & ~3));
-    JB_CUDA(cudaFuncSetAttribute(refine_prune_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    refine_prune_kernel<<<(unsigned)((nb + BW - 1) / BW), BW * 32, smem, st>>>(
-        a.data, a.data_norms, D, a.start, nb, alpha2, R, hops, tids, tdst, cap, cand, kid, kd, a.adjacency, a.degrees,
-        tt, tk, crows, rstride, ncand);
-    JB_LAUNCH_CHECK();
-    pt.mark("prune");
-    int hseg = 0;
-    rc = merge_phase(a, alpha2, tt, tk, ntri, rstride, bufs, st, hseg);
-    if (rc) return rc;
-    pt.mark("merge");
-    pt.report(a.start, a.stop);
-    if (a.stats_out_host) {
-        BALLOC(work, unsigned long long, 2);
-        JB_CUDA(cudaMemsetAsync(work, 0, 2 * sizeof(unsigned long long), st));
-        sum2_kernel<<<std::max(1, std::min<int>((int)((nb + 255) / 256), 4 * sm_count_current())), 256, 0, st>>>(
-            hops, evals, nb, work);
-        unsigned long long hw[2] = {0, 0};
-        JB_CUDA(cudaMemcpyAsync(hw, work, sizeof(hw), cudaMemcpyDeviceToHost, st));
-        JB_CUDA(cudaMemsetAsync(work, 0, 2 * sizeof(unsigned long long), st));
-        sum2_kernel<<<std::max(1, std::min<int>((int)((nb + 255) / 256), 4 * sm_count_current())), 256, 0, st>>>(
-            ncand, ncand, nb, work);
-        unsigned long long pc[2] = {0, 0};
-        JB_CUDA(cudaMemcpyAsync(pc, work, sizeof(pc), cudaMemcpyDeviceToHost, st));
-        JB_CUDA(cudaStreamSynchronize(st));
-        int64_t* w = a.stats_out_host;
-        w[0] += (int64_t)hw[0];
-        w[1] += (int64_t)hw[1];
-        w[2] += (int64_t)pc[0];
-        w[3] += hseg;
-        w[4] += ntri;
-    }
-    JB_CUDA(cudaStreamSynchronize(st));
-    return JB_OK;
+    if (a.element_kind == JB_KIND_U8) return refine_batch_impl(U8Metric{a.data_u8, a.norms_u32, a.dims}, a, active, st);
+    return refine_batch_impl(F32Metric{a.data, a.data_norms, a.dims}, a, active, st);
 }
 
 int jb_robust_prune(const float* data, const float* data_norms, int32_t dims, const int64_t* pivots, int64_t count,
@@ -1202,11 +1255,12 @@ int jb_robust_prune(const float* data, const float* data_norms, int32_t dims, co
     JB_CUDA(cudaStreamSynchronize(st));
     Scratch cand;
     JB_CUDA(cand.alloc((size_t)std::max<int64_t>(total, 1) * 8, st));
-    const size_t srow_bytes = (size_t)BW * ((dims + 3) & ~3) * 4;
-    JB_CUDA(cudaFuncSetAttribute(prune_batch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)srow_bytes));
-    prune_batch_kernel<<<(unsigned)((count + BW - 1) / BW), BW * 32, srow_bytes, st>>>(
-        data, data_norms, dims, pivots, count, offsets, cand_ids, cand_dists, alpha * alpha, degree_cap,
-        cand.as<uint64_t>(), out_ids, out_dists, out_counts);
+    const F32Metric m{data, data_norms, dims};
+    const int smem = BW * m.pivot_words() * 4;
+    JB_CUDA(cudaFuncSetAttribute(prune_batch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    prune_batch_kernel<<<(unsigned)((count + BW - 1) / BW), BW * 32, smem, st>>>(
+        m, pivots, count, offsets, cand_ids, cand_dists, alpha * alpha, degree_cap, cand.as<uint64_t>(), out_ids,
+        out_dists, out_counts);
     JB_LAUNCH_CHECK();
     return JB_OK;
 }

@@ -136,7 +136,7 @@ __global__ void medoid_final_kernel(const DI* __restrict__ partial, int np, int6
 
 // ---- frontier -> top-k (search.py:375-382, exact source) -----------------
 __global__ void frontier_topk_kernel(const uint64_t* __restrict__ keys, int64_t nq, int L, int k,
-                                     int32_t* __restrict__ ids, double* __restrict__ dists) {
+                                     int32_t* __restrict__ ids, double* __restrict__ dists, bool integer) {
     int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= nq * k) return;
     int64_t q = t / k;
@@ -147,8 +147,24 @@ __global__ void frontier_topk_kernel(const uint64_t* __restrict__ keys, int64_t 
         dists[t] = __longlong_as_double(0x7FF0000000000000ll);
     } else {
         ids[t] = (int32_t)(key & 0xFFFFFFFFull);
-        dists[t] = (double)__uint_as_float((uint32_t)(key >> 32));
+        const uint32_t w = (uint32_t)(key >> 32);
+        dists[t] = integer ? (double)w : (double)__uint_as_float(w);  // _decode_keys (search.py:148-153)
     }
+}
+
+// u8 rows: integer norms sum(x*x) (row_sq_norms, core.py:162-166) and exact f32 copies
+__global__ void row_sq_norms_u8_kernel(const uint8_t* __restrict__ x, int64_t n, int D, uint32_t* __restrict__ out) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint8_t* r = x + i * D;
+    uint32_t s = 0;
+    for (int e = 0; e < D; ++e) s += (uint32_t)r[e] * (uint32_t)r[e];
+    out[i] = s;
+}
+
+__global__ void u8_to_f32_kernel(const uint8_t* __restrict__ x, int64_t count, float* __restrict__ out) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = (float)x[i];
 }
 
 }  // namespace jb
@@ -223,9 +239,50 @@ int jb_frontier_topk(const uint64_t* frontier_keys, int64_t nq, int32_t beam_wid
     int64_t total = nq * k;
     int threads = 256;
     frontier_topk_kernel<<<(unsigned)((total + threads - 1) / threads), threads, 0, as_stream(stream)>>>(
-        frontier_keys, nq, beam_width, k, out_ids, out_dists);
+        frontier_keys, nq, beam_width, k, out_ids, out_dists, false);
     JB_LAUNCH_CHECK();
     return JB_OK;
+}
+
+int jb_frontier_topk_u8(const uint64_t* frontier_keys, int64_t nq, int32_t beam_width, int32_t k, int32_t* out_ids,
+                        double* out_dists, void* stream) {
+    JB_CHECK_ARG(k >= 1 && k <= beam_width, "k must satisfy 1 <= k <= beam_width");
+    if (nq == 0) return JB_OK;
+    int64_t total = nq * k;
+    int threads = 256;
+    frontier_topk_kernel<<<(unsigned)((total + threads - 1) / threads), threads, 0, as_stream(stream)>>>(
+        frontier_keys, nq, beam_width, k, out_ids, out_dists, true);
+    JB_LAUNCH_CHECK();
+    return JB_OK;
+}
+
+int jb_row_sq_norms_u8(const uint8_t* x, int64_t n, int32_t dims, uint32_t* out, void* stream) {
+    JB_CHECK_ARG(dims >= 1 && n >= 0, "jb_row_sq_norms_u8: bad shape");
+    JB_CHECK_ARG((int64_t)dims * 255 * 255 < (1ll << 32), "u8 dims too large for 32-bit packed distances");
+    if (n == 0) return JB_OK;
+    row_sq_norms_u8_kernel<<<(unsigned)((n + 255) / 256), 256, 0, as_stream(stream)>>>(x, n, dims, out);
+    JB_LAUNCH_CHECK();
+    return JB_OK;
+}
+
+int jb_u8_to_f32(const uint8_t* x, int64_t count, float* out, void* stream) {
+    JB_CHECK_ARG(count >= 0, "jb_u8_to_f32: bad count");
+    if (count == 0) return JB_OK;
+    const int blocks = (int)std::min<int64_t>((count + 255) / 256, 16 * sm_count_current());
+    u8_to_f32_kernel<<<blocks, 256, 0, as_stream(stream)>>>(x, count, out);
+    JB_LAUNCH_CHECK();
+    return JB_OK;
+}
+
+int jb_medoid_u8(const uint8_t* x, int64_t n, int32_t dims, int64_t* out_host, void* stream) {
+    JB_CHECK_ARG(n >= 1, "medoid of an empty dataset");
+    JB_CHECK_ARG(dims >= 1, "jb_medoid: bad dims");
+    cudaStream_t st = as_stream(stream);
+    Scratch f;
+    JB_CUDA(f.alloc(sizeof(float) * (size_t)n * dims, st));
+    int rc = jb_u8_to_f32(x, n * dims, f.as<float>(), stream);
+    if (rc) return rc;
+    return jb_medoid(f.as<float>(), n, dims, out_host, stream);
 }
 
 }  // extern "C"

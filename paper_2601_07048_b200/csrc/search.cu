@@ -32,6 +32,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include "common.cuh"
+#include "metric.cuh"
 #include "runtime.cuh"
 
 namespace jb {
@@ -353,6 +354,7 @@ struct QueryCtx {
     float* stage;             // EXACT: staged rows, 32 x sstride
     float qadd, qsumq, qlo, qdelta;
     int nwords, meta_off;
+    uint32_t qn;              // EXACT_U8: integer query norm (query bytes at qv)
 };
 
 // One neighbour per lane (nb = -1: none): visited check, then the distance of
@@ -384,6 +386,11 @@ __device__ __forceinline__ uint64_t eval_chunk(const jb_search_args& a, const Se
     if (nnew == 0) return UMAX;
     evals += nnew;
 
+    if (SRC == JB_SRC_EXACT_U8) {  // integer distance, evaluated by the lane that owns the neighbour
+        if (!isnew) return UMAX;
+        const uint32_t dot = u8_dot(a.data_u8 + (size_t)nb * D, reinterpret_cast<const uint8_t*>(c.qv), D);
+        return ((uint64_t)u8_dist(__ldg(a.norms_u32 + nb), dot, c.qn) << 32) | (uint32_t)nb;
+    }
     float d = 0.0f;
     int myid = 0;
     if (SRC == JB_SRC_EXACT) {
@@ -464,23 +471,32 @@ beam_search_kernel(const jb_search_args a, const SearchLayout lay, int* __restri
         qi = __shfl_sync(FULL, (long long)qi, 0);
         if (qi >= a.nq) break;
 
-        const float* q = a.queries + qi * D;
-        for (int e = lane; e < D; e += 32) qv[e] = q[e];
+        if (SRC == JB_SRC_EXACT_U8) {
+            const uint8_t* q8 = a.queries_u8 + qi * D;
+            for (int e = lane; e < D; e += 32) reinterpret_cast<uint8_t*>(qv)[e] = q8[e];
+        } else {
+            const float* q = a.queries + qi * D;
+            for (int e = lane; e < D; e += 32) qv[e] = q[e];
+        }
         for (int i = lane; i < L; i += 32) beam[i] = UMAX;
         fmask[lane] = 0;
         for (int i = lane; i < H / 4; i += 32) reinterpret_cast<uint4*>(tab)[i] = make_uint4(EMPTY_SLOT, EMPTY_SLOT, EMPTY_SLOT, EMPTY_SLOT);
-        const float qadd = a.query_add[qi];
+        const float qadd = (SRC == JB_SRC_EXACT_U8) ? 0.0f : a.query_add[qi];
+        const uint32_t qn = (SRC == JB_SRC_EXACT_U8) ? a.query_norms_u32[qi] : 0u;
         const float qsumq = (SRC != JB_SRC_EXACT) ? a.query_sumq[qi] : 0.0f;
         const uint32_t start = a.starts ? (uint32_t)a.starts[qi] : (uint32_t)a.start_vertex;
         __syncwarp();
         float qlo = 0.0f, qdelta = 0.0f;
         if (SRC == JB_SRC_RABITQ_FAST) build_planes<FAST_QB>(qv, D, planes, qlo, qdelta);
-        const QueryCtx qc{qv, planes, cid, stage, qadd, qsumq, qlo, qdelta, nwords, meta_off};
+        const QueryCtx qc{qv, planes, cid, stage, qadd, qsumq, qlo, qdelta, nwords, meta_off, qn};
 
         int lossy = 0;
         if (lane == 0) {
-            float d0;
-            if (SRC == JB_SRC_EXACT) {
+            float d0 = 0.0f;
+            if (SRC == JB_SRC_EXACT_U8) {
+                const uint32_t dot = u8_dot(a.data_u8 + (size_t)start * D, reinterpret_cast<const uint8_t*>(qv), D);
+                beam[0] = ((uint64_t)u8_dist(a.norms_u32[start], dot, qn) << 32) | start;
+            } else if (SRC == JB_SRC_EXACT) {
                 const float dot = a1_dot<false>(a.data + (size_t)start * D, qv, D);
                 d0 = exact_from_dot(a.data_norms[start], dot, qadd);
             } else if (SRC == JB_SRC_RABITQ_FAST) {
@@ -489,7 +505,7 @@ beam_search_kernel(const jb_search_args a, const SearchLayout lay, int* __restri
             } else {
                 d0 = rabitq_estimate<BITS>(a.records + (size_t)start * RB, qv, D, meta_off, qadd, qsumq);
             }
-            beam[0] = pack_key(d0, start);
+            if (SRC != JB_SRC_EXACT_U8) beam[0] = pack_key(d0, start);
             uint32_t* sl;
             visit(tab, lay.hbits, start, lossy, sl);
         }
@@ -516,9 +532,9 @@ beam_search_kernel(const jb_search_args a, const SearchLayout lay, int* __restri
             __syncwarp();
             if (lane == 0) {
                 beam[cursor] = ukey | EXPANDED;
-                if (hops < tcap) {
+                if (hops < tcap) {  // the key's distance word (f32 bits, or the u32 integer distance)
                     tids[hops] = (int32_t)u;
-                    tdst[hops] = key_dist(ukey);
+                    reinterpret_cast<uint32_t*>(tdst)[hops] = (uint32_t)(ukey >> 32);
                 }
             }
             ++hops;
@@ -751,6 +767,11 @@ int jb_beam_search(const jb_search_args* args, void* stream) {
     if (hs <= 0) hs = std::min(2048, std::max(512, pow2_ceil(4 * a.beam_width)));
     hs = std::max(32, pow2_ceil(hs));
     cudaStream_t st = as_stream(stream);
+    if (a.source == JB_SRC_EXACT_U8) {
+        JB_CHECK_ARG(a.data_u8 && a.norms_u32 && a.queries_u8 && a.query_norms_u32, "u8 search: missing arrays");
+        JB_CHECK_ARG((int64_t)a.dims * 255 * 255 < (1ll << 32), "u8 dims too large for 32-bit packed distances");
+        return launch_search<JB_SRC_EXACT_U8, 1, true>(a, hs, st);
+    }
     if (a.source == JB_SRC_EXACT) {
         JB_CHECK_ARG(a.data && a.data_norms && a.queries && a.query_add, "exact search: missing arrays");
         if ((a.dims & 3) == 0) return launch_search<JB_SRC_EXACT, 1, true>(a, hs, st);

@@ -234,7 +234,8 @@ def medoid(dataset) -> int:
         raise ValueError("medoid of an empty dataset")
     dev = ds.device()
     out = np.zeros(1, dtype=np.int64)
-    _lib.check(_lib.lib().jb_medoid(_lib.ptr(dev.x), dev.count, dev.dims, out.ctypes.data, _lib.stream_ptr()))
+    fn = _lib.lib().jb_medoid_u8 if dev.kind.value == "u8" else _lib.lib().jb_medoid
+    _lib.check(fn(_lib.ptr(dev.x), dev.count, dev.dims, out.ctypes.data, _lib.stream_ptr()))
     return int(out[0])
 
 

@@ -68,8 +68,11 @@ def exact_knn(data, queries, k: int) -> GroundTruth:
         raise ValueError(f"k must be in [1, {ds.count}]")
     if ds.dims != qs.dims:
         raise ValueError(f"dimension mismatch: data {ds.dims}, queries {qs.dims}")
+    if ds.element_kind is not qs.element_kind:
+        raise ValueError("data and queries must share an element kind")
+    # u8 rows are scored on exact f32 copies (the reference scores x.astype(f64))
     q_dev = torch.from_numpy(np.ascontiguousarray(qs.data, dtype=np.float32)).cuda()
-    ids, dists = exact_knn_device(ds.device().x, q_dev, k)
+    ids, dists = exact_knn_device(ds.device_f32(), q_dev, k)
     return GroundTruth(ids=ids.cpu().numpy(), distances=dists.cpu().numpy())
 
 

@@ -21,7 +21,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _lib
-from .core import VectorDataset, as_dataset
+from .core import ElementKind, VectorDataset, as_dataset
 from .graph import Candidate, GraphIndex, as_graph
 
 __all__ = ["SearchParams", "SearchStats", "SearchResult", "beam_search", "search_knn", "search_knn_batch",
@@ -122,16 +122,25 @@ class _Bound:
             if D != ds.dims:
                 raise ValueError(f"query dims {D} != dataset dims {ds.dims}")
             dev = ds.device()
-            self.kind = _lib.SRC_EXACT
             self.dims = ds.dims
             self.rows = dev
             self.records, self.record_bytes, self.bits = None, 0, 0
             self.rotated = q_dev
-            self.qadd = torch.empty(nq, dtype=torch.float32, device=q_dev.device)
             self.qsumq = None
-            if nq:
-                _lib.check(_lib.lib().jb_row_sq_norms(_lib.ptr(q_dev), nq, D, _lib.ptr(self.qadd),
-                                                     _lib.stream_ptr()))
+            if ds.element_kind is ElementKind.U8:  # integer distances (search.py:92-99)
+                if q_dev.dtype != torch.uint8:
+                    raise ValueError("u8 dataset requires u8 queries")
+                self.kind = _lib.SRC_EXACT_U8
+                self.qadd = torch.empty(nq, dtype=torch.int32, device=q_dev.device)
+                if nq:
+                    _lib.check(_lib.lib().jb_row_sq_norms_u8(_lib.ptr(q_dev), nq, D, _lib.ptr(self.qadd),
+                                                            _lib.stream_ptr()))
+            else:
+                self.kind = _lib.SRC_EXACT
+                self.qadd = torch.empty(nq, dtype=torch.float32, device=q_dev.device)
+                if nq:
+                    _lib.check(_lib.lib().jb_row_sq_norms(_lib.ptr(q_dev), nq, D, _lib.ptr(self.qadd),
+                                                         _lib.stream_ptr()))
             self.count = ds.count
 
 
@@ -154,14 +163,28 @@ class _Pinned(threading.local):
 _PINNED = _Pinned()
 
 
-def _queries_to_device(queries):
+def _is_u8(source) -> bool:
+    return not _is_rabitq(source) and as_dataset(source).element_kind is ElementKind.U8
+
+
+def _queries_to_device(queries, u8: bool = False):
+    """Query rows to HBM: f32, or (u8 source) uint8 — a u8 dataset requires u8
+    queries (search.py:107-110)."""
     torch = _lib.require_cuda()
     if isinstance(queries, torch.Tensor):
         q = queries
         if q.dim() == 1:
             q = q[None, :]
+        if u8:
+            if q.dtype != torch.uint8:
+                raise ValueError("u8 dataset requires u8 queries")
+            return q.to(device="cuda").contiguous()
         return q.to(device="cuda", dtype=torch.float32).contiguous()
     q = np.atleast_2d(np.asarray(queries))
+    if u8:
+        if q.dtype != np.uint8:
+            raise ValueError("u8 dataset requires u8 queries")
+        return torch.from_numpy(np.ascontiguousarray(q)).to("cuda")
     q = np.ascontiguousarray(q, dtype=np.float32)
     if q.size == 0:
         return torch.empty(q.shape, dtype=torch.float32, device="cuda")
@@ -204,7 +227,10 @@ def _launch(graph: GraphIndex, bound: _Bound, L: int, starts_dev=None, trace_cap
     a.active_count = graph.active_count
     a.source = bound.kind
     a.dims = bound.dims
-    if bound.kind == _lib.SRC_EXACT:
+    if bound.kind == _lib.SRC_EXACT_U8:
+        a.data_u8, a.norms_u32 = _lib.ptr(bound.rows.x), _lib.ptr(bound.rows.norms)
+        a.queries_u8, a.query_norms_u32 = _lib.ptr(bound.rotated), _lib.ptr(bound.qadd)
+    elif bound.kind == _lib.SRC_EXACT:
         a.data = _lib.ptr(bound.rows.x)
         a.data_norms = _lib.ptr(bound.rows.norms)
     else:
@@ -251,7 +277,8 @@ def run_beam_searches(graph, source, queries, beam_width: int, starts=None) -> l
     """search.py:272-304: one SearchResult (frontier + visited trace + stats) per query row."""
     graph = as_graph(graph)
     _validate(graph, beam_width)
-    q_dev = _queries_to_device(queries)
+    u8 = _is_u8(source)
+    q_dev = _queries_to_device(queries, u8)
     nq = q_dev.shape[0]
     starts_dev = _starts(graph, starts, nq)
     bound = _Bound(source, q_dev)
@@ -287,13 +314,16 @@ def run_beam_searches(graph, source, queries, beam_width: int, starts=None) -> l
         for i in lossy:
             nb = adj[tids_h[i, : int(hops_h[i])]].ravel()
             evals_h[i] = np.unique(np.append(nb[nb >= 0], st[i])).size
+    # key words decode as f32 bits, or as the integer distance of a u8 source (search.py:148-153)
+    word = np.uint32 if u8 else np.float32
+    tdst_h = tdst_h.view(word)
     out = []
     for i in range(nq):
         kk = keys[i][keys[i] != _UMAX]
         h = int(hops_h[i])
         out.append(SearchResult(
             frontier_ids=(kk & np.uint64(0xFFFFFFFF)).astype(np.int32),
-            frontier_dists=(kk >> np.uint64(32)).astype(np.uint32).view(np.float32).astype(np.float64),
+            frontier_dists=(kk >> np.uint64(32)).astype(np.uint32).view(word).astype(np.float64),
             visited_ids=tids_h[i, :h].copy(),
             visited_dists=tdst_h[i, :h].astype(np.float64),
             stats=SearchStats(hops=h, distance_evals=int(evals_h[i])),
@@ -312,7 +342,7 @@ def search_knn(graph, source, query, params: SearchParams, start: int | None = N
         raise ValueError("rerank over a quantized source requires exact_data")
     graph = as_graph(graph)
     _validate(graph, params.beam_width)
-    q_dev = _queries_to_device(query)
+    q_dev = _queries_to_device(query, _is_u8(source))
     ids, dists = _knn_device(graph, source, q_dev, params, exact_data, _starts(graph, start, 1))
     ids, dists = ids.cpu().numpy()[0], dists.cpu().numpy()[0]
     keep = ids >= 0
@@ -340,7 +370,8 @@ def _knn_device(graph: GraphIndex, source, q_dev, params: SearchParams, exact_da
         _lib.check(_lib.lib().jb_rerank_topk(_lib.ptr(rows.x), rows.dims, _lib.ptr(q_dev), nq, _lib.ptr(fk), L, k,
                                              _lib.ptr(ids), _lib.ptr(dists), st))
     else:
-        _lib.check(_lib.lib().jb_frontier_topk(_lib.ptr(fk), nq, L, k, _lib.ptr(ids), _lib.ptr(dists), st))
+        fn = _lib.lib().jb_frontier_topk_u8 if bound.kind == _lib.SRC_EXACT_U8 else _lib.lib().jb_frontier_topk
+        _lib.check(fn(_lib.ptr(fk), nq, L, k, _lib.ptr(ids), _lib.ptr(dists), st))
     return ids, dists
 
 
@@ -355,6 +386,9 @@ def search_knn_batch(graph, source, queries, params: SearchParams, exact_data=No
     _validate(graph, params.beam_width)
     if params.rerank and _is_rabitq(source) and exact_data is None:
         raise ValueError("rerank over a quantized source requires exact_data")
+    if _is_u8(source):  # u8 rows: one device search + top-k (the host pipeline stages f32 queries)
+        ids, dists = _knn_device(graph, source, _queries_to_device(queries, True), params, exact_data)
+        return tuple(_to_host(ids, dists))
     q = np.atleast_2d(np.asarray(queries))
     q = np.ascontiguousarray(q, dtype=np.float32)
     nq = q.shape[0]
@@ -423,6 +457,8 @@ def search_knn_batch_device(graph, source, q_dev, params: SearchParams, exact_da
     if params.rerank and _is_rabitq(source) and exact_data is None:
         raise ValueError("rerank over a quantized source requires exact_data")
     torch = _lib.require_cuda()
+    if _is_u8(source):
+        return _knn_device(graph, source, _queries_to_device(q_dev, True), params, exact_data)
     q_dev = q_dev.to(dtype=torch.float32).contiguous()
     nq = q_dev.shape[0]
     ids = torch.empty((nq, params.k), dtype=torch.int32, device=q_dev.device)

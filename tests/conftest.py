@@ -31,6 +31,13 @@ def lowrank(n, d, d_int, noise, seed):
     return x.astype(np.float32)
 
 
+def u8_rows(n, d, seed):
+    """tests/golden/make_golden.py:u8_rows — BigANN-like u8 rows from a low-rank sample."""
+    x = lowrank(n, d, 8, 0.05, seed)
+    lo, hi = x.min(), x.max()
+    return np.clip(np.rint((x - lo) / (hi - lo) * 255.0), 0, 255).astype(np.uint8)
+
+
 def split(flat, lens):
     ends = np.cumsum(lens)
     return [flat[e - n:e] for e, n in zip(ends, lens)]

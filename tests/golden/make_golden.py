@@ -69,6 +69,30 @@ def two_pass():
     save("two_pass", adjacency=g.adjacency[:n].copy(), degrees=g.degrees[:n].copy(), entry=np.int64(g.entry_point))
 
 
+def u8_rows(n, d, seed):
+    """BigANN-like u8 rows: a low-rank f32 sample affinely mapped to [0, 255] and rounded."""
+    x = lowrank(n, d, 8, 0.05, seed)
+    lo, hi = x.min(), x.max()
+    return np.clip(np.rint((x - lo) / (hi - lo) * 255.0), 0, 255).astype(np.uint8)
+
+
+def u8():
+    """7. u8 element kind: integer-distance build (several batches), search trace, top-k, GT, medoid."""
+    rows = u8_rows(2600, 32, seed=31)
+    data, q = rows[:2500], rows[2500:]
+    ds = ref.VectorDataset(data)
+    t = time.time()
+    g = ref.build(ds, ref.BuildParams(degree_cap=16, build_beam_width=32, alpha=1.2, max_batch=700))
+    print(f"u8: reference build {data.shape} in {time.time() - t:.1f}s")
+    n = g.active_count
+    res = run_beam_searches(g, ds, q, 32)
+    ids, dists = ref.search_knn_batch(g, ds, q, ref.SearchParams(beam_width=32, k=10))
+    gt = ref.exact_knn(ds, ref.VectorDataset(q), 10)
+    save("u8", adjacency=g.adjacency[:n].copy(), degrees=g.degrees[:n].copy(), entry=np.int64(g.entry_point),
+         active=np.int64(n), **{"L32_" + k: v for k, v in ragged(res).items()}, knn_ids=ids, knn_dists=dists,
+         gt_ids=gt.ids, gt_dists=gt.distances, medoid=np.int64(ref.medoid(ds)))
+
+
 def main():
     # 1. exact search + build on a small Gaussian graph (D=32, R=16, L=32)
     data = ref.gen_synthetic(3000, 32, seed=0).data
@@ -138,5 +162,6 @@ if __name__ == "__main__":
     if not names:
         main()
         two_pass()
+        u8()
     for n in names:
         globals()[n]()

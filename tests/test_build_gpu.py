@@ -5,7 +5,7 @@ and by the oracle restatement, including streaming inserts and options."""
 import numpy as np
 import pytest
 
-from conftest import gaussian, golden, lowrank
+from conftest import gaussian, golden, lowrank, u8_rows
 from oracle import vamana
 
 pytestmark = pytest.mark.gpu
@@ -45,6 +45,33 @@ def test_build_identical_to_reference_g128_and_stream():
     jb.insert_stream(inc, ds, range(33, 1200), p)
     assert inc.active_count == 1200
     _same_graph(inc, f["inc_adjacency"], f["inc_degrees"], int(f["inc_entry"]))
+
+
+def test_u8_build_identical_to_reference():
+    f = golden("u8")
+    data = u8_rows(2600, 32, 31)[:2500]
+    g = jb.build(jb.VectorDataset(data), jb.BuildParams(degree_cap=16, build_beam_width=32, alpha=1.2, max_batch=700))
+    _same_graph(g, f["adjacency"], f["degrees"], int(f["entry"]))
+    g.validate()
+
+
+def test_u8_build_two_pass_and_stream_match_oracle_128d():
+    # 128-d u8 (staged 16 B rows), streaming inserts, then a two_pass build
+    data = u8_rows(4000, 128, 43)
+    og = vamana.Graph(4000, 24)
+    d = vamana.Pairwise(data)
+    for a, b in ((0, 25), (25, 900), (900, 2500), (2500, 4000)):
+        vamana.batch_insert(og, data, a, b, 24, 48, 1.2, d)
+    g = jb.GraphIndex(4000, 24)
+    ds = jb.VectorDataset(data)
+    p = jb.BuildParams(degree_cap=24, build_beam_width=48, alpha=1.2)
+    for a, b in ((0, 25), (25, 900), (900, 2500), (2500, 4000)):
+        jb.batch_insert(g, ds, range(a, b), p)
+    _same_graph(g, og.adj, og.deg, og.entry)
+    og2 = vamana.build(data[:2000], R=16, L=32, alpha=1.3, max_batch=600, two_pass=True)
+    g2 = jb.build(jb.VectorDataset(data[:2000]),
+                  jb.BuildParams(degree_cap=16, build_beam_width=32, alpha=1.3, max_batch=600, two_pass=True))
+    _same_graph(g2, og2.adj, og2.deg, og2.entry)
 
 
 def test_two_pass_build_identical_to_reference():

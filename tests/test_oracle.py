@@ -4,7 +4,7 @@
 import numpy as np
 import pytest
 
-from conftest import gaussian, golden, lowrank, split
+from conftest import gaussian, golden, lowrank, split, u8_rows
 from oracle import knn, rabitq, search, vamana
 
 
@@ -173,3 +173,21 @@ def test_recall_threshold_matching():
     gt_d = np.array([[1.0, 2.0, 2.0]], dtype=np.float32)
     assert knn.recall_at_k([[0, 2]], gt_ids, gt_d, 2) == 1.0   # tie at the boundary counts
     assert knn.recall_at_k([[5, 0]], gt_ids, gt_d, 2) == 0.5
+
+
+def test_u8_build_search_knn_match_reference():
+    f = golden("u8")
+    rows = u8_rows(2600, 32, 31)
+    data, q = rows[:2500], rows[2500:]
+    g = vamana.build(data, R=16, L=32, alpha=1.2, max_batch=700)
+    np.testing.assert_array_equal(g.adj, f["adjacency"])
+    np.testing.assert_array_equal(g.deg, f["degrees"])
+    assert g.entry == int(f["entry"])
+    res = search.beam_search(g.adj, g.active, g.entry, search.ExactSource(data, q), len(q), 32)
+    _check_results(res, f, "L32_")
+    ids, ds = knn.exact_knn(data, q, 10)
+    np.testing.assert_array_equal(ids, f["gt_ids"])
+    np.testing.assert_array_equal(ds, f["gt_dists"])
+    assert vamana.medoid(data) == int(f["medoid"])
+    with pytest.raises(ValueError, match="u8 dataset requires u8 queries"):
+        search.ExactSource(data, q.astype(np.float32))

@@ -4,7 +4,7 @@ reference's golden outputs (identical ids, dists, traces, stats)."""
 import numpy as np
 import pytest
 
-from conftest import gaussian, golden, lowrank, split
+from conftest import gaussian, golden, lowrank, split, u8_rows
 from oracle import knn as oknn
 from oracle import rabitq as orabitq
 from oracle import search as osearch
@@ -309,3 +309,31 @@ def test_host_pipeline_matches_device_path(chunk, kind):
     np.testing.assert_array_equal(hd, dd.cpu().numpy())
     np.testing.assert_array_equal(hi2, hi[:333])
     np.testing.assert_array_equal(hd2, hd[:333])
+
+
+def test_u8_search_knn_gt_medoid_match_reference_golden():
+    f = golden("u8")
+    rows = u8_rows(2600, 32, 31)
+    data, q = rows[:2500], rows[2500:]
+    g, ds = _graph(f), jb.VectorDataset(data)
+    _golden_check(jb.run_beam_searches(g, ds, q, 32), f, "L32_")
+    ids, dists = jb.search_knn_batch(g, ds, q, jb.SearchParams(beam_width=32, k=10))
+    np.testing.assert_array_equal(ids, f["knn_ids"])
+    np.testing.assert_array_equal(dists, f["knn_dists"])
+    gt = jb.exact_knn(ds, jb.VectorDataset(q), 10)
+    np.testing.assert_array_equal(gt.ids, f["gt_ids"])
+    np.testing.assert_array_equal(gt.distances, f["gt_dists"])
+    assert jb.medoid(ds) == int(f["medoid"])
+    with pytest.raises(ValueError, match="u8 dataset requires u8 queries"):
+        jb.run_beam_searches(g, ds, q.astype(np.float32), 32)
+
+
+@pytest.mark.parametrize("L", [8, 64, 300])
+def test_u8_search_matches_oracle_128d(L):
+    # BigANN shape (128-d u8): 16 B-aligned rows, several beam widths incl. the smem merge path
+    rows = u8_rows(3100, 128, 41)
+    data, q = rows[:3000], rows[3000:]
+    og = vamana.build(data, R=24, L=48, alpha=1.2, max_batch=1000)
+    g = _graph_from_oracle(og)
+    res = jb.run_beam_searches(g, jb.VectorDataset(data), q, L)
+    _oracle_check(res, osearch.beam_search(og.adj, og.active, og.entry, osearch.ExactSource(data, q), len(q), L))
