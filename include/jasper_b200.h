@@ -227,6 +227,16 @@ typedef struct jb_insert_args {
                                     * JB_KIND_U8 (data_u8, norms_u32)           */
     const uint8_t* data_u8;        /* [count, D] u8 rows                        */
     const uint32_t* norms_u32;     /* [count] integer row norms                 */
+    /* quantized construction (build.py:105-111, 124-129; f32 rows only): every
+     * construction distance is the RaBitQ estimate of a row's record against
+     * the pivot's own row bound as a query (jb_rabitq_bind over the dataset) */
+    int32_t quantized;             /* 0: exact distances; 1: RaBitQ estimates  */
+    const uint8_t* records;        /* [count, record_bytes] packed records      */
+    int32_t record_bytes;
+    int32_t bits;                  /* 1, 2, 4 or 8                              */
+    const float* bound_rotated;    /* [count, D] rows bound as queries          */
+    const float* bound_qadd;       /* [count]                                   */
+    const float* bound_qsumq;      /* [count]                                   */
 } jb_insert_args;
 
 /* One three-phase batch: search -> prune + reverse triples -> grouped merge,

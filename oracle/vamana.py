@@ -7,6 +7,7 @@
   * seed batch, 3-phase batch insert, group merge             build.py:246-348
   * connectivity repair (BFS + nearest-donor bridges)         build.py:137-224
   * two_pass refinement (search + prune at the final alpha)   build.py:351-386
+  * quantized construction (RaBitQ estimates everywhere)      build.py:105-111, 124-129, 322-325
   * build schedule (R+1 doubling, entry -> medoid)            build.py:389-424
   * insert_stream chunking                                    build.py:427-447
 
@@ -18,6 +19,7 @@ from __future__ import annotations
 
 import numpy as np
 
+from . import rabitq as orq
 from .search import ExactSource, beam_search
 
 
@@ -58,6 +60,32 @@ class Pairwise:
         if self.integer:
             return d.astype(np.float64)
         return np.maximum(d, np.float32(0)).astype(np.float64)
+
+
+class Quant:
+    """A fitted RaBitQ index (centroid, codes, meta, bits, seed) as a construction
+    source: phase-1 searches bind the batch rows (build.py:322-325) and every
+    pairwise distance binds the pivot row and estimates the ids (build.py:124-129)."""
+
+    def __init__(self, centroid, codes, meta, bits: int, seed: int):
+        self.centroid, self.codes, self.meta, self.bits, self.seed = centroid, codes, meta, bits, seed
+
+    def source(self, queries: np.ndarray):
+        return orq.QuantSource(self.codes, self.meta, self.bits, queries.shape[1],
+                               *orq.bind(queries, self.centroid, self.bits, self.seed))
+
+    def pairwise(self, x: np.ndarray):
+        return QuantPairwise(self, x)
+
+
+class QuantPairwise:
+    def __init__(self, quant: Quant, x: np.ndarray):
+        self.quant, self.x = quant, np.ascontiguousarray(x, dtype=np.float32)
+
+    def __call__(self, pivot: int, ids) -> np.ndarray:
+        ids = np.asarray(ids, dtype=np.int64)
+        src = self.quant.source(self.x[pivot][None, :])
+        return src(np.zeros(ids.size, dtype=np.int64), ids).astype(np.float64)
 
 
 def medoid(x: np.ndarray) -> int:
@@ -165,11 +193,11 @@ def repair(g: Graph, dist: Pairwise) -> int:
 
 
 def batch_insert(g: Graph, x: np.ndarray, start: int, stop: int, R: int, L: int, alpha: float,
-                 dist: Pairwise | None = None, always_prune=False, reverse_all=False) -> int:
+                 dist: Pairwise | None = None, always_prune=False, reverse_all=False, quant: Quant | None = None) -> int:
     """build.py:296-348. Returns the number of repair bridges."""
     if start == stop:
         return 0
-    dist = dist or Pairwise(x)
+    dist = dist or (quant.pairwise(x) if quant is not None else Pairwise(x))
     if g.active == 0:
         g.active = stop
         g.entry = medoid(x[:stop])
@@ -180,7 +208,7 @@ def batch_insert(g: Graph, x: np.ndarray, start: int, stop: int, R: int, L: int,
                 kept, _ = robust_prune(v, rest, dist(v, rest), alpha, R, dist)
                 g.put(v, kept)
         return repair(g, dist)
-    src = ExactSource(x, x[start:stop])
+    src = quant.source(x[start:stop]) if quant is not None else ExactSource(x, x[start:stop])
     found = beam_search(g.adj, g.active, g.entry, src, stop - start, L)
     g.active = stop
     tgt, srcs, dd = [], [], []
@@ -222,15 +250,16 @@ def merge_reverse(g: Graph, tgt, srcs, dd, R: int, alpha: float, dist, always_pr
 
 
 def refine_pass(g: Graph, x: np.ndarray, R: int, L: int, alpha: float, max_batch: int,
-                dist: Pairwise | None = None, always_prune=False) -> int:
+                dist: Pairwise | None = None, always_prune=False, quant: Quant | None = None) -> int:
     """build.py:351-386: per max_batch slice, search every active vertex on the
     current graph, prune it over (visited - itself) + (current neighbours missing
     from the trace) at the final alpha, then the grouped reverse merge; repair last."""
-    dist = dist or Pairwise(x)
+    dist = dist or (quant.pairwise(x) if quant is not None else Pairwise(x))
     n = g.active
     for lo in range(0, n, max_batch):
         hi = min(n, lo + max_batch)
-        found = beam_search(g.adj, g.active, g.entry, ExactSource(x, x[lo:hi]), hi - lo, L)
+        src = quant.source(x[lo:hi]) if quant is not None else ExactSource(x, x[lo:hi])
+        found = beam_search(g.adj, g.active, g.entry, src, hi - lo, L)
         tgt, srcs, dd = [], [], []
         for v, res in zip(range(lo, hi), found):
             cur = g.nbrs(v)
@@ -248,26 +277,27 @@ def refine_pass(g: Graph, x: np.ndarray, R: int, L: int, alpha: float, max_batch
     return repair(g, dist)
 
 
-def build(x: np.ndarray, R: int, L: int, alpha: float, max_batch: int = 100_000, two_pass: bool = False) -> Graph:
+def build(x: np.ndarray, R: int, L: int, alpha: float, max_batch: int = 100_000, two_pass: bool = False,
+          quant: Quant | None = None) -> Graph:
     """build.py:389-424 (two_pass: insertion passes at alpha=1, then refine_pass)."""
     x = np.ascontiguousarray(x) if np.asarray(x).dtype == np.uint8 else np.ascontiguousarray(x, dtype=np.float32)
     n = x.shape[0]
     if n == 0:
         raise ValueError("cannot build over an empty dataset")
     g = Graph(n, R)
-    dist = Pairwise(x)
+    dist = quant.pairwise(x) if quant is not None else Pairwise(x)
     m = medoid(x)
     size, pos = R + 1, 0
     while pos < n:
         stop = min(n, pos + size)
-        batch_insert(g, x, pos, stop, R, L, 1.0 if two_pass else alpha, dist)
+        batch_insert(g, x, pos, stop, R, L, 1.0 if two_pass else alpha, dist, quant=quant)
         if m < g.active and g.entry != m:
             g.entry = m
             repair(g, dist)
         pos = stop
         size = min(size * 2, max_batch)
     if two_pass:
-        refine_pass(g, x, R, L, alpha, max_batch, dist)
+        refine_pass(g, x, R, L, alpha, max_batch, dist, quant=quant)
     return g
 
 

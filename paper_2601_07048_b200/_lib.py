@@ -52,6 +52,8 @@ class InsertArgs(C.Structure):
         ("entry_point_out_host", p), ("bridges_out_host", p), ("stats_out_host", p),  # int64 [8]
         ("active_count", i64),
         ("element_kind", i32), ("data_u8", p), ("norms_u32", p),
+        ("quantized", i32), ("records", p), ("record_bytes", i32), ("bits", i32),
+        ("bound_rotated", p), ("bound_qadd", p), ("bound_qsumq", p),
     ]
 
 

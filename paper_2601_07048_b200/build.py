@@ -7,9 +7,11 @@
                   repair — all on device, mutating the HBM adjacency in place
   build           build.py:389-424 R+1 doubling schedule, entry -> global medoid
   insert_stream   build.py:427-447 max_batch chunks
+  _refine_pass    build.py:351-386 two_pass refinement, one jb_refine_batch per batch
 
-The quantized-construction path (`quantizer=`) and `two_pass` refinement are
-not part of the B200 hot path (no config uses them); they raise.
+Element kinds: f32 rows (einsum-order f32 distances) and u8 rows (exact integer
+distances). `quantizer=` (a RaBitQIndex) switches every construction distance to
+the RaBitQ estimate against the pivot's bound row (build.py:105-111, 124-129).
 """
 
 from __future__ import annotations
@@ -104,7 +106,34 @@ def _validate_range(graph: GraphIndex, dataset, new_ids: range):
     return start, stop
 
 
-def _args(graph: GraphIndex, ds, params: BuildParams, start: int, stop: int):
+def _bound_rows(quantizer, ds):
+    """Quantized construction (build.py:105-111, 124-129): the dataset's rows bound
+    as RaBitQ queries (rotated, query_add, query_sumq), the pivot side of every
+    construction distance. One jb_rabitq_bind over all rows, cached per dataset."""
+    from .rabitq import as_rabitq
+
+    idx = as_rabitq(quantizer)
+    if ds.element_kind is not ElementKind.F32:
+        raise ValueError("quantized construction requires f32 data")
+    if idx.dims != ds.dims:
+        raise ValueError(f"quantizer dims {idx.dims} != dataset dims {ds.dims}")
+    cache = getattr(idx, "_jb_bound", None)
+    if cache is not None and cache[0] is ds:
+        return idx, cache[1]
+    torch = _lib.require_cuda()
+    dev, x = idx.device(), ds.device().x
+    n, D = x.shape
+    rot = torch.empty((n, D), dtype=torch.float32, device=x.device)
+    qa = torch.empty(n, dtype=torch.float32, device=x.device)
+    qs = torch.empty(n, dtype=torch.float32, device=x.device)
+    if n:
+        _lib.check(_lib.lib().jb_rabitq_bind(_lib.ptr(x), n, D, idx.bits, _lib.ptr(dev.centroid), _lib.ptr(dev.rotation),
+                                             _lib.ptr(rot), _lib.ptr(qa), _lib.ptr(qs), _lib.stream_ptr()))
+    idx._jb_bound = (ds, (rot, qa, qs))
+    return idx, (rot, qa, qs)
+
+
+def _args(graph: GraphIndex, ds, params: BuildParams, start: int, stop: int, quantizer=None):
     adj, deg = graph.device()
     dev = ds.device()
     a = _lib.InsertArgs()
@@ -121,6 +150,13 @@ def _args(graph: GraphIndex, ds, params: BuildParams, start: int, stop: int):
     a.reverse_all_visited = int(params.reverse_all_visited)
     a.start, a.stop = start, stop
     a.entry_point = graph.entry_point
+    if quantizer is not None:
+        idx, (rot, qa, qs) = _bound_rows(quantizer, ds)
+        if idx.count < max(stop, graph.active_count):
+            raise ValueError(f"quantizer covers {idx.count} rows, the batch needs {max(stop, graph.active_count)}")
+        rec = idx.device()
+        a.quantized, a.records, a.record_bytes, a.bits = 1, _lib.ptr(rec.records), rec.record_bytes, idx.bits
+        a.bound_rotated, a.bound_qadd, a.bound_qsumq = _lib.ptr(rot), _lib.ptr(qa), _lib.ptr(qs)
     return a
 
 
@@ -146,8 +182,6 @@ def _run(fn, graph: GraphIndex, a) -> int:
 
 
 def _check_supported(params: BuildParams, quantizer):
-    if quantizer is not None:
-        raise NotImplementedError("quantized construction is not on the B200 path (build with exact rows)")
     if params.degree_cap < 2:
         raise ValueError("degree_cap must be >= 2")
 
@@ -162,13 +196,13 @@ def batch_insert(graph, dataset, new_ids: range, params: BuildParams, quantizer=
     _check_supported(params, quantizer)
     if graph.degree_cap != params.degree_cap:
         raise ValueError("graph degree_cap differs from params.degree_cap")
-    a = _args(graph, ds, params, start, stop)
+    a = _args(graph, ds, params, start, stop, quantizer)
     graph.last_bridges = _run(_lib.lib().jb_batch_insert, graph, a)
     graph.active_count = stop
 
 
-def _repair(graph: GraphIndex, ds, params: BuildParams) -> int:
-    a = _args(graph, ds, params, 0, graph.active_count)
+def _repair(graph: GraphIndex, ds, params: BuildParams, quantizer=None) -> int:
+    a = _args(graph, ds, params, 0, graph.active_count, quantizer)
     return _run(_lib.lib().jb_repair_connectivity, graph, a)
 
 
@@ -190,16 +224,16 @@ def build(dataset, params: BuildParams, quantizer=None) -> GraphIndex:
     while pos < ds.count:
         stop = min(ds.count, pos + size)
         t1 = time.perf_counter()
-        batch_insert(graph, ds, range(pos, stop), pass_params)
+        batch_insert(graph, ds, range(pos, stop), pass_params, quantizer)
         if global_medoid < graph.active_count and graph.entry_point != global_medoid:
             graph.entry_point = global_medoid
-            _repair(graph, ds, params)
+            _repair(graph, ds, params, quantizer)
         if prof:
             print(f"[jb] batch wall [{pos}, {stop}) {1e3 * (time.perf_counter() - t1):.2f}ms", file=sys.stderr)
         pos = stop
         size = min(size * 2, params.max_batch)
     if params.two_pass:
-        _refine_pass(graph, ds, params)
+        _refine_pass(graph, ds, params, quantizer)
     return graph
 
 
@@ -212,10 +246,10 @@ def _refine_pass(graph, dataset, params: BuildParams, quantizer=None) -> None:
     n = graph.active_count
     for lo in range(0, n, params.max_batch):
         hi = min(n, lo + params.max_batch)
-        a = _args(graph, ds, params, lo, hi)
+        a = _args(graph, ds, params, lo, hi, quantizer)
         a.active_count = n
         _run(_lib.lib().jb_refine_batch, graph, a)
-    graph.last_bridges = _repair(graph, ds, params)
+    graph.last_bridges = _repair(graph, ds, params, quantizer)
 
 
 def insert_stream(graph, dataset, new_range: range, params: BuildParams, quantizer=None) -> None:

@@ -757,6 +757,7 @@ struct Bufs {
 // Per-warp candidate-row staging budget (~26 KB per warp beside the pivot).
 template <class M>
 static int staged_rows(const M& m, int want, int R) {
+    if (!M::kStage) return 0;
     int crows = std::min(want, (26 * 1024 - m.pivot_words() * 4) / (m.stage_stride_words() * 4 + 4));
     return crows < R + 1 ? 0 : crows;
 }
@@ -888,7 +889,12 @@ static int trace_search(const jb_insert_args& a, int64_t q0, int64_t nq, int64_t
         tdst = bufs.get<uint32_t>((size_t)nq * cap, st, _ce); JB_CUDA(_ce);
         jb_search_args s{};
         s.adjacency = a.adjacency; s.degree_cap = R; s.active_count = active; s.dims = D;
-        if (a.element_kind == JB_KIND_U8) {
+        if (a.quantized) {  // run_beam_searches(graph, quantizer, rows) (build.py:322-325)
+            s.source = JB_SRC_RABITQ;
+            s.records = a.records; s.record_bytes = a.record_bytes; s.bits = a.bits;
+            s.queries = a.bound_rotated + (size_t)q0 * D; s.query_add = a.bound_qadd + q0;
+            s.query_sumq = a.bound_qsumq + q0;
+        } else if (a.element_kind == JB_KIND_U8) {
             s.source = JB_SRC_EXACT_U8;
             s.data_u8 = a.data_u8; s.norms_u32 = a.norms_u32;
             s.queries_u8 = a.data_u8 + (size_t)q0 * D; s.query_norms_u32 = a.norms_u32 + q0;
@@ -1037,6 +1043,13 @@ struct PhaseTimer {
 
 static int validate_insert(const jb_insert_args& a) {
     JB_CHECK_ARG(a.adjacency && a.degrees, "batch insert: missing graph arrays");
+    if (a.quantized) {
+        JB_CHECK_ARG(a.element_kind == JB_KIND_F32, "quantized construction requires f32 data");
+        JB_CHECK_ARG(a.bits == 1 || a.bits == 2 || a.bits == 4 || a.bits == 8, "bits must be one of (1, 2, 4, 8)");
+        JB_CHECK_ARG(a.records && a.bound_rotated && a.bound_qadd && a.bound_qsumq,
+                     "quantized construction: missing records / bound rows");
+        JB_CHECK_ARG(a.record_bytes == jb_rabitq_record_bytes(a.dims, a.bits), "quantized construction: record_bytes");
+    }
     JB_CHECK_ARG(a.element_kind == JB_KIND_F32 || a.element_kind == JB_KIND_U8, "unknown element kind %d",
                  a.element_kind);
     if (a.element_kind == JB_KIND_U8) {
@@ -1196,6 +1209,21 @@ static int refine_batch_impl(const M& m, const jb_insert_args& a, int64_t active
     return JB_OK;
 }
 
+// Run f with the construction metric of the call: RaBitQ estimates, u8 or f32 rows.
+template <class F>
+static int with_metric(const jb_insert_args& a, F&& f) {
+    if (a.quantized) {
+        switch (a.bits) {
+            case 1: return f(RabitqMetric<1>{a.records, a.record_bytes, a.bound_rotated, a.bound_qadd, a.bound_qsumq, a.dims});
+            case 2: return f(RabitqMetric<2>{a.records, a.record_bytes, a.bound_rotated, a.bound_qadd, a.bound_qsumq, a.dims});
+            case 4: return f(RabitqMetric<4>{a.records, a.record_bytes, a.bound_rotated, a.bound_qadd, a.bound_qsumq, a.dims});
+            default: return f(RabitqMetric<8>{a.records, a.record_bytes, a.bound_rotated, a.bound_qadd, a.bound_qsumq, a.dims});
+        }
+    }
+    if (a.element_kind == JB_KIND_U8) return f(U8Metric{a.data_u8, a.norms_u32, a.dims});
+    return f(F32Metric{a.data, a.data_norms, a.dims});
+}
+
 }  // namespace jb
 
 using namespace jb;
@@ -1209,8 +1237,7 @@ int jb_repair_connectivity(const jb_insert_args* args, void* stream) {
     if (rc) return rc;
     int64_t b = 0;
     cudaStream_t st = as_stream(stream);
-    if (a.element_kind == JB_KIND_U8) rc = repair(U8Metric{a.data_u8, a.norms_u32, a.dims}, a, a.stop, a.entry_point, st, &b);
-    else rc = repair(F32Metric{a.data, a.data_norms, a.dims}, a, a.stop, a.entry_point, st, &b);
+    rc = with_metric(a, [&](auto m) { return repair(m, a, a.stop, a.entry_point, st, &b); });
     if (a.bridges_out_host) *a.bridges_out_host = b;
     if (a.entry_point_out_host) *a.entry_point_out_host = a.entry_point;
     return rc;
@@ -1222,8 +1249,7 @@ int jb_batch_insert(const jb_insert_args* args, void* stream) {
     int rc = validate_insert(a);
     if (rc) return rc;
     cudaStream_t st = as_stream(stream);
-    if (a.element_kind == JB_KIND_U8) return batch_insert_impl(U8Metric{a.data_u8, a.norms_u32, a.dims}, a, st);
-    return batch_insert_impl(F32Metric{a.data, a.data_norms, a.dims}, a, st);
+    return with_metric(a, [&](auto m) { return batch_insert_impl(m, a, st); });
 }
 
 int jb_refine_batch(const jb_insert_args* args, void* stream) {
@@ -1238,8 +1264,7 @@ int jb_refine_batch(const jb_insert_args* args, void* stream) {
     if (a.bridges_out_host) *a.bridges_out_host = 0;
     if (a.start == a.stop) return JB_OK;
     cudaStream_t st = as_stream(stream);
-    if (a.element_kind == JB_KIND_U8) return refine_batch_impl(U8Metric{a.data_u8, a.norms_u32, a.dims}, a, active, st);
-    return refine_batch_impl(F32Metric{a.data, a.data_norms, a.dims}, a, active, st);
+    return with_metric(a, [&](auto m) { return refine_batch_impl(m, a, active, st); });
 }
 
 int jb_robust_prune(const float* data, const float* data_norms, int32_t dims, const int64_t* pivots, int64_t count,

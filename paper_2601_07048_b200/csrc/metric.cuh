@@ -8,11 +8,12 @@
 // Keys everywhere are (dist_bits << 32) | id, ordered as unsigned integers,
 // which orders non-negative f32 distances and u32 integer distances alike.
 //
-//   F32Metric  exact f32 rows, numpy einsum rounding (A1)     search.py:82-130
-//   U8Metric   exact u8 rows, integer distances               search.py:92-99
+//   F32Metric     exact f32 rows, numpy einsum rounding (A1)   search.py:82-130
+//   U8Metric      exact u8 rows, integer distances             search.py:92-99
+//   RabitqMetric  RaBitQ estimates (quantized construction)    build.py:124-129
 //
 // Candidate rows can also be staged in smem (`stage`/`dist_staged`) when a
-// prune's candidate set fits; both policies stage 16-byte-aligned rows.
+// prune's candidate set fits (kStage); the exact policies stage 16-byte-aligned rows.
 #pragma once
 #include "common.cuh"
 
@@ -23,6 +24,7 @@ struct F32Metric {
     const float* norms;
     int D;
     static constexpr bool kInt = false;
+    static constexpr bool kStage = true;
 
     __host__ __device__ int row_bytes() const { return D * 4; }
     // smem words of one staged row (16 B skew keeps per-lane float4 reads conflict free)
@@ -109,6 +111,7 @@ struct U8Metric {
     const uint32_t* norms;
     int D;
     static constexpr bool kInt = true;
+    static constexpr bool kStage = true;
 
     __host__ __device__ int row_bytes() const { return D; }
     __host__ __device__ int stage_stride_words() const { return ((D + 15) & ~15) / 4 + 4; }
@@ -153,6 +156,132 @@ struct U8Metric {
         const uint8_t* b = reinterpret_cast<const uint8_t*>(rows + (size_t)p * rs);
         return u8_dist(cn[i], u8_dot(a, b, D), cn[p]);
     }
+};
+
+// ---- RaBitQ estimator (shared by the search kernel and RabitqMetric) --------
+// RaBitQ estimator for one packed record (rabitq.py:235-244):
+//   dd  = A1 dot(f32(u), rotated)           (einsum 'md,md->m')
+//   est = max((qadd + data_add) + data_rescale * (dd - qsumq), 0)
+// Full 16 B pieces are unrolled with compile-time bit positions. For m = 1,
+// u*q is exactly q or +-0 and adding +-0 to an accumulator is a no-op, so the
+// product/add pair becomes one predicated add with identical rounding.
+template <int BITS>
+__device__ __forceinline__ void rq_piece_full(Acc4& acc, const uint4 w4, const float* __restrict__ qv, int e0) {
+    constexpr int PER16 = 128 / BITS;
+    constexpr uint32_t MASK = (1u << BITS) - 1u;
+    const uint32_t w[4] = {w4.x, w4.y, w4.z, w4.w};
+#pragma unroll
+    for (int blk = 0; blk < PER16 / 16; ++blk) {
+#pragma unroll
+        for (int i = 3; i >= 0; --i) {
+            const float4 q4 = *reinterpret_cast<const float4*>(qv + e0 + blk * 16 + 4 * i);
+            const float qq[4] = {q4.x, q4.y, q4.z, q4.w};
+            float* lanes[4] = {&acc.l0, &acc.l1, &acc.l2, &acc.l3};
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                constexpr int dummy = 0;
+                (void)dummy;
+                const int off = (blk * 16 + 4 * i + j) * BITS;
+                const uint32_t code = (w[off >> 5] >> (off & 31)) & MASK;
+                if (BITS == 1) {
+                    if (code) *lanes[j] = __fadd_rn(qq[j], *lanes[j]);
+                } else {
+                    *lanes[j] = __fadd_rn(__fmul_rn((float)code, qq[j]), *lanes[j]);
+                }
+            }
+        }
+    }
+}
+
+// <u, q> for one record whose first 16-byte code piece is already in registers.
+template <int BITS>
+__device__ __forceinline__ float rabitq_dd(const uint8_t* __restrict__ rec, uint4 first, const float* __restrict__ qv,
+                                           int D) {
+    constexpr int PER16 = 128 / BITS;  // elements per 16-byte piece
+    constexpr uint32_t MASK = (1u << BITS) - 1u;
+    Acc4 acc; acc.zero();
+    int e0 = 0;
+    for (; e0 + PER16 <= D; e0 += PER16) {
+        const uint4 w4 = e0 == 0 ? first : __ldg(reinterpret_cast<const uint4*>(rec + (e0 * BITS) / 8));
+        rq_piece_full<BITS>(acc, w4, qv, e0);
+    }
+    if (e0 < D) {  // last partial piece: runtime loop (rare shapes)
+        const uint4 w4 = e0 == 0 ? first : __ldg(reinterpret_cast<const uint4*>(rec + (e0 * BITS) / 8));
+        const uint32_t w[4] = {w4.x, w4.y, w4.z, w4.w};
+        int b = e0;
+        for (; b + 16 <= D; b += 16) {
+            for (int i = 3; i >= 0; --i) {
+                for (int j = 0; j < 4; ++j) {
+                    const int off = (b - e0 + 4 * i + j) * BITS;
+                    acc.madd1(j, (float)((w[off >> 5] >> (off & 31)) & MASK), qv[b + 4 * i + j]);
+                }
+            }
+        }
+        for (; b < D; ++b) {
+            const int off = (b - e0) * BITS;
+            acc.madd1(b & 3, (float)((w[off >> 5] >> (off & 31)) & MASK), qv[b]);
+        }
+    }
+    return acc.reduce();
+}
+
+// est = max((qadd + data_add) + data_rescale * (dd - qsumq), 0) in the reference's order
+__device__ __forceinline__ float rabitq_finish(float dd, float2 m, float qadd, float qsumq) {
+    const float est = __fadd_rn(__fadd_rn(qadd, m.x), __fmul_rn(m.y, __fsub_rn(dd, qsumq)));
+    return est > 0.0f ? est : 0.0f;
+}
+
+template <int BITS>
+__device__ __forceinline__ float rabitq_estimate(const uint8_t* __restrict__ rec, const float* __restrict__ qv,
+                                                 int D, int meta_off, float qadd, float qsumq) {
+    const uint4 first = __ldg(reinterpret_cast<const uint4*>(rec));
+    const float dd = rabitq_dd<BITS>(rec, first, qv, D);
+    return rabitq_finish(dd, __ldg(reinterpret_cast<const float2*>(rec + meta_off)), qadd, qsumq);
+}
+
+
+// Quantized construction (build.py:105-111, 124-129): every d(pivot, row) is the
+// RaBitQ estimate of the row's code against the pivot's own row bound as a query
+// (RaBitQIndex.bind(x[pivot]), rabitq.py:170-181). The bound rows (rotated f32,
+// query_add, query_sumq) are computed once for the dataset by jb_rabitq_bind.
+// No smem staging: candidates are 16-32 B records read in place.
+template <int BITS>
+struct RabitqMetric {
+    const uint8_t* records;
+    int record_bytes;
+    const float* rotated;   // [count, D] bound rows
+    const float* qadd;      // [count]
+    const float* qsumq;     // [count]
+    int D;
+    static constexpr bool kInt = false;
+    static constexpr bool kStage = false;
+
+    __host__ __device__ int meta_off() const { return ((((D * BITS) + 7) / 8 + 15) / 16) * 16; }
+    __host__ __device__ int row_bytes() const { return record_bytes; }
+    __host__ __device__ int stage_stride_words() const { return 4; }
+    __host__ __device__ int pivot_words() const { return ((D + 3) & ~3) + 4; }
+    __device__ static double value(uint32_t bits) { return (double)__uint_as_float(bits); }
+
+    __device__ void load_pivot(uint32_t* pv, uint32_t v) const {
+        const int lane = lane_id();
+        const float* r = rotated + (size_t)v * D;
+        float* f = reinterpret_cast<float*>(pv);
+        for (int e = lane; e < D; e += 32) f[e] = r[e];
+        if (lane == 0) {
+            f[((D + 3) & ~3)] = qadd[v];
+            f[((D + 3) & ~3) + 1] = qsumq[v];
+        }
+        __syncwarp();
+    }
+    __device__ uint32_t dist(const uint32_t* pv, uint32_t row) const {
+        const float* f = reinterpret_cast<const float*>(pv);
+        const float est = rabitq_estimate<BITS>(records + (size_t)row * record_bytes, f, D, meta_off(),
+                                                f[((D + 3) & ~3)], f[((D + 3) & ~3) + 1]);
+        return __float_as_uint(est);
+    }
+    // never staged (the host passes crows = 0); present for the shared kernel bodies
+    __device__ void stage(uint32_t*, uint32_t*, const uint64_t*, int) const { __trap(); }
+    __device__ uint32_t dist_staged(const uint32_t*, const uint32_t*, int, int) const { __trap(); return 0; }
 };
 
 }  // namespace jb

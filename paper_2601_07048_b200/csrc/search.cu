@@ -75,86 +75,6 @@ __device__ __forceinline__ bool visit(uint32_t* tab, int hbits, uint32_t id, int
     return true;
 }
 
-// RaBitQ estimator for one packed record (rabitq.py:235-244):
-//   dd  = A1 dot(f32(u), rotated)           (einsum 'md,md->m')
-//   est = max((qadd + data_add) + data_rescale * (dd - qsumq), 0)
-// Full 16 B pieces are unrolled with compile-time bit positions. For m = 1,
-// u*q is exactly q or +-0 and adding +-0 to an accumulator is a no-op, so the
-// product/add pair becomes one predicated add with identical rounding.
-template <int BITS>
-__device__ __forceinline__ void rq_piece_full(Acc4& acc, const uint4 w4, const float* __restrict__ qv, int e0) {
-    constexpr int PER16 = 128 / BITS;
-    constexpr uint32_t MASK = (1u << BITS) - 1u;
-    const uint32_t w[4] = {w4.x, w4.y, w4.z, w4.w};
-#pragma unroll
-    for (int blk = 0; blk < PER16 / 16; ++blk) {
-#pragma unroll
-        for (int i = 3; i >= 0; --i) {
-            const float4 q4 = *reinterpret_cast<const float4*>(qv + e0 + blk * 16 + 4 * i);
-            const float qq[4] = {q4.x, q4.y, q4.z, q4.w};
-            float* lanes[4] = {&acc.l0, &acc.l1, &acc.l2, &acc.l3};
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                constexpr int dummy = 0;
-                (void)dummy;
-                const int off = (blk * 16 + 4 * i + j) * BITS;
-                const uint32_t code = (w[off >> 5] >> (off & 31)) & MASK;
-                if (BITS == 1) {
-                    if (code) *lanes[j] = __fadd_rn(qq[j], *lanes[j]);
-                } else {
-                    *lanes[j] = __fadd_rn(__fmul_rn((float)code, qq[j]), *lanes[j]);
-                }
-            }
-        }
-    }
-}
-
-// <u, q> for one record whose first 16-byte code piece is already in registers.
-template <int BITS>
-__device__ __forceinline__ float rabitq_dd(const uint8_t* __restrict__ rec, uint4 first, const float* __restrict__ qv,
-                                           int D) {
-    constexpr int PER16 = 128 / BITS;  // elements per 16-byte piece
-    constexpr uint32_t MASK = (1u << BITS) - 1u;
-    Acc4 acc; acc.zero();
-    int e0 = 0;
-    for (; e0 + PER16 <= D; e0 += PER16) {
-        const uint4 w4 = e0 == 0 ? first : __ldg(reinterpret_cast<const uint4*>(rec + (e0 * BITS) / 8));
-        rq_piece_full<BITS>(acc, w4, qv, e0);
-    }
-    if (e0 < D) {  // last partial piece: runtime loop (rare shapes)
-        const uint4 w4 = e0 == 0 ? first : __ldg(reinterpret_cast<const uint4*>(rec + (e0 * BITS) / 8));
-        const uint32_t w[4] = {w4.x, w4.y, w4.z, w4.w};
-        int b = e0;
-        for (; b + 16 <= D; b += 16) {
-            for (int i = 3; i >= 0; --i) {
-                for (int j = 0; j < 4; ++j) {
-                    const int off = (b - e0 + 4 * i + j) * BITS;
-                    acc.madd1(j, (float)((w[off >> 5] >> (off & 31)) & MASK), qv[b + 4 * i + j]);
-                }
-            }
-        }
-        for (; b < D; ++b) {
-            const int off = (b - e0) * BITS;
-            acc.madd1(b & 3, (float)((w[off >> 5] >> (off & 31)) & MASK), qv[b]);
-        }
-    }
-    return acc.reduce();
-}
-
-// est = max((qadd + data_add) + data_rescale * (dd - qsumq), 0) in the reference's order
-__device__ __forceinline__ float rabitq_finish(float dd, float2 m, float qadd, float qsumq) {
-    const float est = __fadd_rn(__fadd_rn(qadd, m.x), __fmul_rn(m.y, __fsub_rn(dd, qsumq)));
-    return est > 0.0f ? est : 0.0f;
-}
-
-template <int BITS>
-__device__ __forceinline__ float rabitq_estimate(const uint8_t* __restrict__ rec, const float* __restrict__ qv,
-                                                 int D, int meta_off, float qadd, float qsumq) {
-    const uint4 first = __ldg(reinterpret_cast<const uint4*>(rec));
-    const float dd = rabitq_dd<BITS>(rec, first, qv, D);
-    return rabitq_finish(dd, __ldg(reinterpret_cast<const float2*>(rec + meta_off)), qadd, qsumq);
-}
-
 // Popcount estimator (fast mode, m = 1): the rotated query is quantized per query
 // to QB-bit integers qq = round((q - lo) / delta) and stored as QB bit-planes
 // (built with warp ballots, element e <-> bit e % 32 of word e / 32, the same

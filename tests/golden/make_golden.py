@@ -93,6 +93,25 @@ def u8():
          gt_ids=gt.ids, gt_dists=gt.distances, medoid=np.int64(ref.medoid(ds)))
 
 
+def quantized():
+    """8. quantized construction: build with a RaBitQ quantizer (m=1 and m=4), two_pass at m=4."""
+    data = ref.gen_synthetic(1200, 32, seed=51).data
+    ds = ref.VectorDataset(data)
+    out = {}
+    for bits, two in ((1, False), (4, False), (4, True)):
+        idx = ref.rabitq_fit(ds, bits=bits, seed=52)
+        t = time.time()
+        g = ref.build(ds, ref.BuildParams(degree_cap=16, build_beam_width=32, alpha=1.2, max_batch=300, two_pass=two),
+                      quantizer=idx)
+        tag = f"m{bits}" + ("_2p" if two else "")
+        print(f"quantized {tag}: reference build {data.shape} in {time.time() - t:.1f}s")
+        n = g.active_count
+        out[tag + "_adjacency"] = g.adjacency[:n].copy()
+        out[tag + "_degrees"] = g.degrees[:n].copy()
+        out[tag + "_entry"] = np.int64(g.entry_point)
+    save("quantized", **out)
+
+
 def main():
     # 1. exact search + build on a small Gaussian graph (D=32, R=16, L=32)
     data = ref.gen_synthetic(3000, 32, seed=0).data
@@ -163,5 +182,6 @@ if __name__ == "__main__":
         main()
         two_pass()
         u8()
+        quantized()
     for n in names:
         globals()[n]()

@@ -74,6 +74,40 @@ def test_u8_build_two_pass_and_stream_match_oracle_128d():
     _same_graph(g2, og2.adj, og2.deg, og2.entry)
 
 
+@pytest.mark.parametrize("tag,bits,two", [("m1", 1, False), ("m4", 4, False), ("m4_2p", 4, True)])
+def test_quantized_construction_identical_to_reference(tag, bits, two):
+    f = golden("quantized")
+    ds = jb.VectorDataset(gaussian(1200, 32, 51))
+    idx = jb.rabitq_fit(ds, bits=bits, seed=52)
+    g = jb.build(ds, jb.BuildParams(degree_cap=16, build_beam_width=32, alpha=1.2, max_batch=300, two_pass=two),
+                 quantizer=idx)
+    _same_graph(g, f[tag + "_adjacency"], f[tag + "_degrees"], int(f[tag + "_entry"]))
+    g.validate()
+
+
+def test_quantized_construction_matches_oracle_128d_stream():
+    # 128-d m=1 (one 32 B record per row), streaming batches
+    from oracle import rabitq as orq
+
+    x = lowrank(3000, 128, 16, 0.05, 53)
+    c, codes, meta = orq.fit(x, 1, 54)
+    q = vamana.Quant(c, codes, meta, 1, 54)
+    og = vamana.Graph(3000, 24)
+    d = q.pairwise(x)
+    for a, b in ((0, 25), (25, 1000), (1000, 3000)):
+        vamana.batch_insert(og, x, a, b, 24, 48, 1.2, d, quant=q)
+    ds = jb.VectorDataset(x)
+    idx = jb.rabitq_fit(ds, bits=1, seed=54)
+    g = jb.GraphIndex(3000, 24)
+    p = jb.BuildParams(degree_cap=24, build_beam_width=48, alpha=1.2)
+    for a, b in ((0, 25), (25, 1000), (1000, 3000)):
+        jb.batch_insert(g, ds, range(a, b), p, quantizer=idx)
+    _same_graph(g, og.adj, og.deg, og.entry)
+    with pytest.raises(ValueError, match="quantized construction requires f32 data"):
+        jb.batch_insert(jb.GraphIndex(10, 4), jb.VectorDataset(np.zeros((10, 128), np.uint8)), range(0, 10),
+                        jb.BuildParams(degree_cap=4, build_beam_width=8), quantizer=idx)
+
+
 def test_two_pass_build_identical_to_reference():
     f = golden("two_pass")
     g = jb.build(jb.VectorDataset(gaussian(1500, 32, 21)),

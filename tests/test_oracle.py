@@ -191,3 +191,15 @@ def test_u8_build_search_knn_match_reference():
     assert vamana.medoid(data) == int(f["medoid"])
     with pytest.raises(ValueError, match="u8 dataset requires u8 queries"):
         search.ExactSource(data, q.astype(np.float32))
+
+
+@pytest.mark.parametrize("tag,bits,two", [("m1", 1, False), ("m4", 4, False), ("m4_2p", 4, True)])
+def test_quantized_construction_matches_reference(tag, bits, two):
+    f = golden("quantized")
+    x = gaussian(1200, 32, 51)
+    c, codes, meta = rabitq.fit(x, bits, 52)
+    g = vamana.build(x, R=16, L=32, alpha=1.2, max_batch=300, two_pass=two,
+                     quant=vamana.Quant(c, codes, meta, bits, 52))
+    np.testing.assert_array_equal(g.adj, f[tag + "_adjacency"])
+    np.testing.assert_array_equal(g.deg, f[tag + "_degrees"])
+    assert g.entry == int(f[tag + "_entry"])
