@@ -273,6 +273,20 @@ int jb_robust_prune(const float* data, const float* data_norms, int32_t dims,
 int jb_exact_knn(const float* data, int64_t n, int32_t dims, const float* queries, int64_t nq,
                  int32_t k, int32_t* out_ids, float* out_dists, void* stream);
 
+/* exact_knn with a distance kind (oracle.py:20-62): inner_product = 0 ranks by
+ * the squared Euclidean score above, 1 by -(q . x) (DistanceKind.INNER_PRODUCT,
+ * oracle.py:53-54); ties by id. */
+int jb_exact_knn_kind(const float* data, int64_t n, int32_t dims, const float* queries, int64_t nq, int32_t k,
+                      int32_t inner_product, int32_t* out_ids, float* out_dists, void* stream);
+
+/* ---- MIPS reduction (core.py:169-206) ----------------------------------- */
+
+/* mips_augment on the device: aug_data [n, dims+1] = [x, f32(sqrt(M^2 - ||x||^2))]
+ * with M^2 the largest f64 row norm (numpy einsum order), aug_queries
+ * [nq, dims+1] = [q, 0]; M^2 written to *max_sq_out_host. Synchronizes. */
+int jb_mips_augment(const float* data, int64_t n, int32_t dims, const float* queries, int64_t nq,
+                    float* aug_data, float* aug_queries, double* max_sq_out_host, void* stream);
+
 /* ---- sharding (north-star 4) ------------------------------------------- */
 
 /* Merge per-shard top-k lists gathered from `shards` ranks into a global top-k

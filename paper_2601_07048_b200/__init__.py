@@ -8,7 +8,8 @@ There is no CPU fallback: without the library or a CUDA device, calls raise.
 """
 
 from .build import BuildParams, EdgeBuffer, batch_insert, build, insert_stream
-from .core import DistanceKind, ElementKind, VectorDataset, dot, gen_lowrank, gen_synthetic, sq_l2
+from .core import (AugmentedDataset, DistanceKind, ElementKind, VectorDataset, dot, gen_lowrank, gen_synthetic,
+                   mips_augment, sq_l2)
 from .graph import Candidate, FormatError, GraphIndex, medoid, robust_prune
 from .rabitq import QueryPrep, RaBitQIndex, estimate_sq_dist, prep_query, rotate
 from .rabitq import fit as rabitq_fit
@@ -22,7 +23,7 @@ __version__ = "0.1.0"
 
 __all__ = [
     "BuildParams", "EdgeBuffer", "batch_insert", "build", "insert_stream",
-    "Candidate", "DistanceKind", "ElementKind", "FormatError", "GraphIndex", "QueryPrep", "RaBitQIndex",
+    "AugmentedDataset", "mips_augment", "Candidate", "DistanceKind", "ElementKind", "FormatError", "GraphIndex", "QueryPrep", "RaBitQIndex",
     "SearchParams", "SearchResult", "SearchStats", "VectorDataset", "beam_search", "dot", "estimate_sq_dist",
     "gen_lowrank", "gen_synthetic", "medoid", "prep_query", "rabitq_fit", "robust_prune", "rotate",
     "run_beam_searches", "search_knn", "GroundTruth", "exact_knn", "SweepPoint", "recall_at_k", "run_queries", "sweep", "search_knn_batch", "search_knn_batch_device", "sq_l2",

@@ -82,6 +82,8 @@ _SIGS = {
     "jb_refine_batch": (C.c_int, [C.POINTER(InsertArgs), p]),
     "jb_robust_prune": (C.c_int, [p, p, i32, p, i64, p, p, p, f64, i32, p, p, p, p]),
     "jb_exact_knn": (C.c_int, [p, i64, i32, p, i64, i32, p, p, p]),
+    "jb_exact_knn_kind": (C.c_int, [p, i64, i32, p, i64, i32, i32, p, p, p]),
+    "jb_mips_augment": (C.c_int, [p, i64, i32, p, i64, p, p, p, p]),
     "jb_merge_shard_topk": (C.c_int, [p, p, i32, i64, i32, p, p, p, p]),
 }
 

@@ -17,7 +17,8 @@ import numpy as np
 
 from . import _lib
 
-__all__ = ["ElementKind", "DistanceKind", "VectorDataset", "sq_l2", "dot", "gen_synthetic", "gen_lowrank"]
+__all__ = ["ElementKind", "DistanceKind", "VectorDataset", "AugmentedDataset", "mips_augment", "sq_l2", "dot",
+           "gen_synthetic", "gen_lowrank"]
 
 
 class ElementKind(enum.Enum):
@@ -164,11 +165,57 @@ class VectorDataset:
         return out
 
 
+@dataclass(frozen=True)
+class AugmentedDataset:
+    """A dataset lifted into dims+1 space so inner-product ranking becomes L2
+    ranking (core.py:111-130): data rows carry sqrt(M^2 - ||x||^2) in the last
+    coordinate, query rows carry 0."""
+
+    dataset: VectorDataset
+    base_dims: int
+    max_norm: float
+    role: str  # "data" or "query"
+
+    def __post_init__(self):
+        if self.dataset.dims != self.base_dims + 1:
+            raise ValueError("augmented dims must equal base dims + 1")
+        if self.role not in ("data", "query"):
+            raise ValueError(f"role must be 'data' or 'query', got {self.role!r}")
+
+
+def mips_augment(data, queries) -> tuple[AugmentedDataset, AugmentedDataset]:
+    """core.py:169-206 on the device (jb_mips_augment): [x, sqrt(M^2 - ||x||^2)] and
+    [q, 0] written straight into HBM; the returned datasets wrap those rows."""
+    data, queries = as_dataset(data), as_dataset(queries)
+    if data.element_kind is not ElementKind.F32 or queries.element_kind is not ElementKind.F32:
+        raise ValueError("mips_augment requires f32 datasets")
+    if data.count == 0:
+        raise ValueError("mips_augment requires non-empty data")
+    if data.dims != queries.dims:
+        raise ValueError(f"dimension mismatch: data dims {data.dims}, query dims {queries.dims}")
+    torch = _lib.require_cuda()
+    x, q = data.device().x, queries.device().x if queries.count else None
+    D = data.dims
+    ad = torch.empty((data.count, D + 1), dtype=torch.float32, device=x.device)
+    aq = torch.empty((queries.count, D + 1), dtype=torch.float32, device=x.device)
+    m2 = np.zeros(1, dtype=np.float64)
+    _lib.check(_lib.lib().jb_mips_augment(_lib.ptr(x), data.count, D, _lib.ptr(q), queries.count, _lib.ptr(ad),
+                                          _lib.ptr(aq), m2.ctypes.data, _lib.stream_ptr()))
+    max_sq = float(m2[0])
+    if not np.isfinite(max_sq):
+        raise ValueError("non-finite norms in data")
+    m = float(np.sqrt(max_sq))
+    return (AugmentedDataset(VectorDataset.from_device(ad), D, m, "data"),
+            AugmentedDataset(VectorDataset.from_device(aq), D, m, "query"))
+
+
 def as_dataset(obj) -> VectorDataset:
     """Accept this package's VectorDataset or any object with a 2-D `.data` array
     (e.g. the reference's beamann.VectorDataset) — the drop-in path."""
     if isinstance(obj, VectorDataset):
         return obj
+    if isinstance(obj, AugmentedDataset) or (hasattr(obj, "dataset") and hasattr(obj, "base_dims")):
+        return as_dataset(obj.dataset)
     data = getattr(obj, "data", None)
     if isinstance(data, np.ndarray) and data.ndim == 2:
         cache = getattr(obj, "_jb_dataset", None)

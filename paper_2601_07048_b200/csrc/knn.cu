@@ -1,8 +1,9 @@
 // knn.cu — exact brute-force top-k in f64 (ground truth), sm_100a.
 //
 // Replaces `exact_knn` (oracle.py:20-62): scores = (xn - 2 q.x) + qn in f64,
-// clamped at 0, ranked by (score, id) ascending (numpy's stable argsort), the
-// first k written as int32 ids and f32 distances.
+// clamped at 0 (squared Euclidean), or -(q.x) (inner product, oracle.py:53-54),
+// ranked by (score, id) ascending (numpy's stable argsort), the first k written
+// as int32 ids and f32 distances.
 //
 // Layout: queries are processed in blocks of QB (a multiple of 64 sized so the
 // f64 score block QB x n stays ~2 GB in HBM).
@@ -49,7 +50,7 @@ __global__ void knn_norms_kernel(const float* __restrict__ x, int64_t n, int D, 
 // S[q, i] = max((xn[i] - 2 * <q, x_i>) + qn[q], 0) for q in [0, nqb), i in [0, n).
 __global__ void __launch_bounds__(256)
 knn_scores_kernel(const float* __restrict__ x, int64_t n, int D, const float* __restrict__ q, int64_t nqb,
-                  const double* __restrict__ xn, const double* __restrict__ qn, double* __restrict__ S) {
+                  const double* __restrict__ xn, const double* __restrict__ qn, double* __restrict__ S, bool ip) {
     __shared__ double qs[KNN_KC][KNN_TILE + 2];
     __shared__ double xs[KNN_KC][KNN_TILE + 2];
     const int tid = threadIdx.x;
@@ -93,13 +94,24 @@ knn_scores_kernel(const float* __restrict__ x, int64_t n, int D, const float* __
         for (int b = 0; b < 4; ++b) {
             const int64_t xi = x0 + tx + 16 * b;
             if (xi >= n) continue;
-            double s = (xn[xi] - 2.0 * acc[a][b]) + qn[qi];
-            S[qi * n + xi] = s > 0.0 ? s : 0.0;
+            if (ip) {
+                S[qi * n + xi] = 0.0 - acc[a][b];  // -(q @ x.T); 0 - 0 = +0, so no -0 patterns
+            } else {
+                double s = (xn[xi] - 2.0 * acc[a][b]) + qn[qi];
+                S[qi * n + xi] = s > 0.0 ? s : 0.0;
+            }
         }
     }
 }
 
-__device__ __forceinline__ uint64_t dbits(double v) { return (uint64_t)__double_as_longlong(v); }
+// f64 -> u64 with the same order (negative scores appear in inner-product mode)
+__device__ __forceinline__ uint64_t dbits(double v) {
+    const uint64_t b = (uint64_t)__double_as_longlong(v);
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double dval(uint64_t k) {
+    return __longlong_as_double((long long)((k >> 63) ? (k & 0x7FFFFFFFFFFFFFFFull) : ~k));
+}
 
 __global__ void __launch_bounds__(SEL_THREADS)
 knn_select_kernel(const double* __restrict__ S, int64_t n, int k, int32_t* __restrict__ out_ids,
@@ -188,7 +200,7 @@ knn_select_kernel(const double* __restrict__ S, int64_t n, int k, int32_t* __res
     }
     for (int j = tid; j < k; j += SEL_THREADS) {
         out_ids[(int64_t)blockIdx.x * k + j] = sid[j];
-        out_d[(int64_t)blockIdx.x * k + j] = (float)__longlong_as_double((long long)skey[j]);
+        out_d[(int64_t)blockIdx.x * k + j] = (float)dval(skey[j]);
     }
 }
 
@@ -196,8 +208,8 @@ knn_select_kernel(const double* __restrict__ S, int64_t n, int k, int32_t* __res
 
 using namespace jb;
 
-extern "C" int jb_exact_knn(const float* data, int64_t n, int32_t dims, const float* queries, int64_t nq, int32_t k,
-                            int32_t* out_ids, float* out_dists, void* stream) {
+extern "C" int jb_exact_knn_kind(const float* data, int64_t n, int32_t dims, const float* queries, int64_t nq,
+                                 int32_t k, int32_t inner_product, int32_t* out_ids, float* out_dists, void* stream) {
     JB_CHECK_ARG(dims >= 1, "dims must be >= 1");
     JB_CHECK_ARG(n >= 1 && n < (1ll << 31), "exact_knn: n must be in [1, 2^31)");
     JB_CHECK_ARG(k >= 1 && k <= n, "k must be in [1, %lld]", (long long)n);
@@ -221,10 +233,15 @@ extern "C" int jb_exact_knn(const float* data, int64_t n, int32_t dims, const fl
         knn_norms_kernel<<<(unsigned)((m + 255) / 256), 256, 0, st>>>(qp, m, dims, qn.as<double>());
         dim3 grid((unsigned)((n + KNN_TILE - 1) / KNN_TILE), (unsigned)((m + KNN_TILE - 1) / KNN_TILE));
         knn_scores_kernel<<<grid, 256, 0, st>>>(data, n, dims, qp, m, xn.as<double>(), qn.as<double>(),
-                                                sc.as<double>());
+                                                sc.as<double>(), inner_product != 0);
         knn_select_kernel<<<(unsigned)m, SEL_THREADS, SEL_SMEM, st>>>(sc.as<double>(), n, k, out_ids + q0 * k,
                                                                out_dists + q0 * k);
         JB_LAUNCH_CHECK();
     }
     return JB_OK;
+}
+
+extern "C" int jb_exact_knn(const float* data, int64_t n, int32_t dims, const float* queries, int64_t nq, int32_t k,
+                            int32_t* out_ids, float* out_dists, void* stream) {
+    return jb_exact_knn_kind(data, n, dims, queries, nq, k, 0, out_ids, out_dists, stream);
 }

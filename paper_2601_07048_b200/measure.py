@@ -16,7 +16,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _lib
-from .core import VectorDataset, as_dataset
+from .core import DistanceKind, VectorDataset, as_dataset
 from .search import SearchParams, search_knn_batch
 
 __all__ = ["SweepPoint", "GroundTruth", "exact_knn", "exact_knn_device", "recall_at_k", "run_queries", "sweep",
@@ -40,7 +40,7 @@ class GroundTruth:
         return self.ids.shape[1]
 
 
-def exact_knn_device(x_dev, q_dev, k: int):
+def exact_knn_device(x_dev, q_dev, k: int, inner_product: bool = False):
     """Exact top-k on HBM-resident f32 rows/queries: (ids int32 [nq,k], dists f32 [nq,k])
     ranked by (f64 score, id) like oracle.py:44-58, as device tensors."""
     torch = _lib.require_cuda()
@@ -54,13 +54,16 @@ def exact_knn_device(x_dev, q_dev, k: int):
     q_dev = q_dev.to(torch.float32).contiguous()
     ids = torch.empty((nq, k), dtype=torch.int32, device=x_dev.device)
     ds = torch.empty((nq, k), dtype=torch.float32, device=x_dev.device)
-    _lib.check(_lib.lib().jb_exact_knn(_lib.ptr(x_dev), n, D, _lib.ptr(q_dev), nq, k, _lib.ptr(ids), _lib.ptr(ds),
-                                       _lib.stream_ptr()))
+    _lib.check(_lib.lib().jb_exact_knn_kind(_lib.ptr(x_dev), n, D, _lib.ptr(q_dev), nq, k, int(inner_product),
+                                            _lib.ptr(ids), _lib.ptr(ds), _lib.stream_ptr()))
     return ids, ds
 
 
-def exact_knn(data, queries, k: int) -> GroundTruth:
-    """oracle.py:20-62: exhaustive top-k per query in f64, ties broken by id."""
+def exact_knn(data, queries, k: int, distance_kind=DistanceKind.SQUARED_EUCLIDEAN) -> GroundTruth:
+    """oracle.py:20-62: exhaustive top-k per query in f64, ties broken by id;
+    inner product ranks by -(q . x) (the stored distances are the negated products)."""
+    if distance_kind not in (DistanceKind.SQUARED_EUCLIDEAN, DistanceKind.INNER_PRODUCT):
+        raise ValueError(f"unsupported distance kind {distance_kind}")
     torch = _lib.require_cuda()
     ds = as_dataset(data) if not isinstance(data, np.ndarray) else VectorDataset(data)
     qs = as_dataset(queries) if not isinstance(queries, np.ndarray) else VectorDataset(queries)
@@ -72,7 +75,7 @@ def exact_knn(data, queries, k: int) -> GroundTruth:
         raise ValueError("data and queries must share an element kind")
     # u8 rows are scored on exact f32 copies (the reference scores x.astype(f64))
     q_dev = torch.from_numpy(np.ascontiguousarray(qs.data, dtype=np.float32)).cuda()
-    ids, dists = exact_knn_device(ds.device_f32(), q_dev, k)
+    ids, dists = exact_knn_device(ds.device_f32(), q_dev, k, distance_kind is DistanceKind.INNER_PRODUCT)
     return GroundTruth(ids=ids.cpu().numpy(), distances=dists.cpu().numpy())
 
 

@@ -112,6 +112,19 @@ def quantized():
     save("quantized", **out)
 
 
+def mips():
+    """9. MIPS: mips_augment, inner-product ground truth, build + search on the augmented rows."""
+    data = ref.gen_synthetic(2000, 24, seed=61).data * np.linspace(0.5, 2.0, 2000, dtype=np.float32)[:, None]
+    q = ref.gen_synthetic(60, 24, seed=62).data
+    ad, aq = ref.mips_augment(ref.VectorDataset(data), ref.VectorDataset(q))
+    gt = ref.exact_knn(ref.VectorDataset(data), ref.VectorDataset(q), 10, ref.DistanceKind.INNER_PRODUCT)
+    g = ref.build(ad.dataset, ref.BuildParams(degree_cap=16, build_beam_width=32, alpha=1.2))
+    ids, dists = ref.search_knn_batch(g, ad.dataset, aq.dataset.data, ref.SearchParams(beam_width=32, k=10))
+    save("mips", aug_data=ad.dataset.data, aug_queries=aq.dataset.data, max_norm=np.float64(ad.max_norm),
+         gt_ids=gt.ids, gt_dists=gt.distances, adjacency=g.adjacency[:g.active_count].copy(),
+         degrees=g.degrees[:g.active_count].copy(), entry=np.int64(g.entry_point), knn_ids=ids, knn_dists=dists)
+
+
 def main():
     # 1. exact search + build on a small Gaussian graph (D=32, R=16, L=32)
     data = ref.gen_synthetic(3000, 32, seed=0).data
@@ -183,5 +196,6 @@ if __name__ == "__main__":
         two_pass()
         u8()
         quantized()
+        mips()
     for n in names:
         globals()[n]()

@@ -79,3 +79,27 @@ def test_exact_knn_validation():
         jb.exact_knn(x, x, 11)
     with pytest.raises(ValueError):
         jb.exact_knn(x, gaussian(3, 5, 0), 2)
+
+
+def test_mips_augment_inner_product_gt_build_and_search_match_reference():
+    from conftest import gaussian as _g
+
+    f = golden("mips")
+    data = _g(2000, 24, 61) * np.linspace(0.5, 2.0, 2000, dtype=np.float32)[:, None]
+    q = _g(60, 24, 62)
+    ad, aq = jb.mips_augment(jb.VectorDataset(data), jb.VectorDataset(q))
+    assert isinstance(ad, jb.AugmentedDataset) and ad.role == "data" and aq.role == "query" and ad.base_dims == 24
+    np.testing.assert_array_equal(ad.dataset.data, f["aug_data"])   # bit-exact f64 norms / sqrt
+    np.testing.assert_array_equal(aq.dataset.data, f["aug_queries"])
+    assert ad.max_norm == float(f["max_norm"])
+    gt = jb.exact_knn(jb.VectorDataset(data), jb.VectorDataset(q), 10, jb.DistanceKind.INNER_PRODUCT)
+    np.testing.assert_array_equal(gt.ids, f["gt_ids"])
+    np.testing.assert_allclose(gt.distances, f["gt_dists"], rtol=1e-6, atol=1e-6)
+    g = jb.build(ad, jb.BuildParams(degree_cap=16, build_beam_width=32, alpha=1.2))
+    np.testing.assert_array_equal(g.adjacency[:2000], f["adjacency"])
+    assert g.entry_point == int(f["entry"])
+    ids, dists = jb.search_knn_batch(g, ad, aq.dataset.data, jb.SearchParams(beam_width=32, k=10))
+    np.testing.assert_array_equal(ids, f["knn_ids"])
+    np.testing.assert_array_equal(dists, f["knn_dists"])
+    with pytest.raises(ValueError, match="mips_augment requires f32 datasets"):
+        jb.mips_augment(jb.VectorDataset(np.zeros((4, 3), np.uint8)), jb.VectorDataset(np.zeros((1, 3), np.uint8)))

@@ -203,3 +203,18 @@ def test_quantized_construction_matches_reference(tag, bits, two):
     np.testing.assert_array_equal(g.adj, f[tag + "_adjacency"])
     np.testing.assert_array_equal(g.deg, f[tag + "_degrees"])
     assert g.entry == int(f[tag + "_entry"])
+
+
+def test_mips_augment_and_inner_product_gt_match_reference():
+    f = golden("mips")
+    data = gaussian(2000, 24, 61) * np.linspace(0.5, 2.0, 2000, dtype=np.float32)[:, None]
+    q = gaussian(60, 24, 62)
+    ad, aq, m = knn.mips_augment(data, q)
+    np.testing.assert_array_equal(ad, f["aug_data"])
+    np.testing.assert_array_equal(aq, f["aug_queries"])
+    assert m == float(f["max_norm"])
+    ids, ds = knn.exact_knn(data, q, 10, inner_product=True)
+    np.testing.assert_array_equal(ids, f["gt_ids"])
+    np.testing.assert_array_equal(ds, f["gt_dists"])
+    g = vamana.build(ad, R=16, L=32, alpha=1.2)
+    np.testing.assert_array_equal(g.adj, f["adjacency"])
