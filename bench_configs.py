@@ -8,8 +8,10 @@ bench.py stays the single headline harness (configs[1]); this script runs:
   c4  DEEP-shaped 96-d low-rank: bulk build of the first N0, then insert_stream in batches of
       100K interleaved with a 10K-query exact search after every batch (inserts/s, QPS)
   c5  one 12.5M x 96 shard of the 100M x 96 index (the per-GPU work at 8 GPUs)
+  u8  BigANN-shaped 1M x 128 u8 rows (the paper's headline dataset kind; not a BASELINE
+      config): exact integer-distance build and search, QPS at recall 0.95
 
-    python bench_configs.py c1|c3|c4|c5 [--n N] [--total T] [--dint D]
+    python bench_configs.py c1|c3|c4|c5|u8 [--n N] [--total T] [--dint D]
 """
 
 from __future__ import annotations
@@ -209,9 +211,45 @@ def c5(args):
     return out
 
 
+def u8(args):
+    """BigANN-shaped u8: low-rank rows (d_int 16) mapped affinely to [0, 255]."""
+    import torch
+
+    import paper_2601_07048_b200 as jb
+
+    n = args.n or 1_000_000
+    x = jb.gen_lowrank(n + 10_000, 128, seed=1, d_int=args.dint or 16, noise=0.05, basis_seed=0)
+    lo, hi = float(x.min()), float(x.max())
+    rows = np.clip(np.rint((x - lo) / (hi - lo) * 255.0), 0, 255).astype(np.uint8)
+    data, q = rows[:n], rows[n:]
+    ds = jb.VectorDataset(data)
+    ds.device()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    g = jb.build(ds, jb.BuildParams(degree_cap=32, build_beam_width=64, alpha=1.2, max_batch=100_000))
+    torch.cuda.synchronize()
+    t_build = time.perf_counter() - t0
+    q_dev = torch.from_numpy(q).cuda()
+    gi, gd = bench._gt_device(ds.device_f32(), q_dev.float(), 100)
+    gt = jb.GroundTruth(gi.cpu().numpy(), gd.cpu().numpy().astype(np.float32))
+    out = {"config": "u8-bigann-shaped", "n": n, "dims": 128, "build_s": round(t_build, 2),
+           "inserts_per_s": round(n / t_build, 1), "bytes_per_vector": 128}
+    pts = []
+    for L in bench.SWEEP:
+        sp = jb.SearchParams(beam_width=L, k=10)
+        ms = _timed(lambda: jb.search_knn_batch_device(g, ds, q_dev, sp), reps=3, warm=1)
+        ids, _ = jb.search_knn_batch_device(g, ds, q_dev, sp)
+        r = jb.recall_at_k(ids.cpu().numpy(), gt, 10)
+        pts.append({"L": L, "recall": round(r, 4), "qps_device": round(10_000 / (ms / 1e3), 1)})
+        if r >= 0.95:
+            break
+    out["exact_u8"] = pts
+    return out
+
+
 def main():
     p = argparse.ArgumentParser()
-    p.add_argument("config", choices=["c1", "c3", "c4", "c5"])
+    p.add_argument("config", choices=["c1", "c3", "c4", "c5", "u8"])
     p.add_argument("--dint", type=int, default=0)
     p.add_argument("--n", type=int, default=0)
     p.add_argument("--total", type=int, default=0)
@@ -220,7 +258,7 @@ def main():
     import torch
 
     torch.cuda.set_device(0)
-    res = {"c1": c1, "c3": c3, "c4": c4, "c5": c5}[args.config](args)
+    res = {"c1": c1, "c3": c3, "c4": c4, "c5": c5, "u8": u8}[args.config](args)
     line = json.dumps(res)
     print(line, flush=True)
     if args.out:
