@@ -6,7 +6,8 @@
 // host memory. Everything between the two host arrays runs in native code:
 //
 //   chunk c (lane c % 2, one CUDA stream per lane):
-//     host memcpy queries -> pinned staging      (CPU; overlaps chunk c-1 on the GPU)
+//     host memcpy queries -> pinned staging      (CPU; overlaps chunk c-1 on the GPU;
+//                                                 skipped when the caller's buffer is pinned)
 //     H2D, bind (rotate GEMM + finish) or A1 query norms, beam search, rerank/top-k,
 //     D2H ids + dists -> pinned, event
 //   lane reuse / drain: event sync, pinned -> caller's arrays
@@ -277,6 +278,12 @@ static int search_knn_host(const jb_knn_plan* plan, const float* queries, int64_
     if ((st = ensure(c, C, D, L, k)) != JB_OK) return st;
     if ((st = fork_lanes(c, as_stream(stream))) != JB_OK) return st;
 
+    // Queries already in page-locked memory (cudaHostAlloc / registered) are copied
+    // to HBM straight from the caller's buffer; pageable ones go through staging.
+    cudaPointerAttributes pa{};
+    const bool pinned_in = cudaPointerGetAttributes(&pa, queries) == cudaSuccess && pa.type == cudaMemoryTypeHost;
+    cudaGetLastError();  // a pageable pointer may leave an error behind on older drivers
+
     PhaseTimer pt;
     int64_t chunk_i = 0;
     for (int64_t q0 = 0; q0 < nq; q0 += C, ++chunk_i) {
@@ -284,9 +291,13 @@ static int search_knn_host(const jb_knn_plan* plan, const float* queries, int64_
         const int64_t m = std::min<int64_t>(C, nq - q0);
         if ((st = drain(c, l, k, out_ids, out_dists, pt)) != JB_OK) return st;
         pt.tick(1);
-        c.pool->copy(l.h_q, queries + q0 * D, sizeof(float) * m * D);
+        const float* src = queries + q0 * D;
+        if (!pinned_in) {
+            c.pool->copy(l.h_q, src, sizeof(float) * m * D);
+            src = l.h_q;
+        }
         pt.tick(0);
-        JB_CUDA(cudaMemcpyAsync(l.d_q, l.h_q, sizeof(float) * m * D, cudaMemcpyHostToDevice, l.s));
+        JB_CUDA(cudaMemcpyAsync(l.d_q, src, sizeof(float) * m * D, cudaMemcpyHostToDevice, l.s));
         if ((st = run_chunk(plan, l, l.d_q, m, l.d_ids, l.d_d)) != JB_OK) return st;
         JB_CUDA(cudaMemcpyAsync(l.h_ids, l.d_ids, sizeof(int32_t) * m * k, cudaMemcpyDeviceToHost, l.s));
         JB_CUDA(cudaMemcpyAsync(l.h_d, l.d_d, sizeof(double) * m * k, cudaMemcpyDeviceToHost, l.s));

@@ -303,12 +303,17 @@ def test_host_pipeline_matches_device_path(chunk, kind):
     try:
         hi, hd = jb.search_knn_batch(g, src, q, sp, exact_data=ds)
         hi2, hd2 = jb.search_knn_batch(g, src, q[:333], sp, exact_data=ds)  # reuse of the cached context
+        qp = torch.empty(q.shape, dtype=torch.float32, pin_memory=True).numpy()  # pinned: no staging copy
+        qp[...] = q
+        hi3, hd3 = jb.search_knn_batch(g, src, qp, sp, exact_data=ds)
     finally:
         js.PIPELINE["chunk"] = 0
     np.testing.assert_array_equal(hi, di.cpu().numpy())
     np.testing.assert_array_equal(hd, dd.cpu().numpy())
     np.testing.assert_array_equal(hi2, hi[:333])
     np.testing.assert_array_equal(hd2, hd[:333])
+    np.testing.assert_array_equal(hi3, hi)
+    np.testing.assert_array_equal(hd3, hd)
 
 
 def test_u8_search_knn_gt_medoid_match_reference_golden():
