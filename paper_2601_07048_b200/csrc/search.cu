@@ -38,6 +38,7 @@
 namespace jb {
 
 constexpr int WPB = 4;          // warps per block
+constexpr int RR_WARPS = 8;     // warps per block of the rerank kernel
 constexpr int MAX_CHUNKS = 4;   // neighbour slots per hop: R <= 32 * MAX_CHUNKS
 #ifndef JB_COOP_MAX
 #define JB_COOP_MAX 2
@@ -509,60 +510,83 @@ beam_search_kernel(const jb_search_args a, const SearchLayout lay, int* __restri
 
 
 // ---- exact rerank of the frontier (search.py:318-320, 375-382) -----------
-// One warp per query: stage up to 32 frontier rows at a time, lane j computes
-// einsum(x - q, x - q) in A1 order, keys (dist, id) collected in smem, then a
-// bitonic sort and the first k written out.
-template <bool ALIGNED>
-__global__ void __launch_bounds__(WPB * 32)
+// One warp per query, 8 frontier rows at a time: the rows are staged into smem
+// with coalesced cp.async (512 B per warp instruction at D = 128), then 4 lanes
+// per row each run one A1 accumulator chain j of einsum(x - q, x - q) (elements
+// e = j mod 4, 16-element blocks with vectors 3,2,1,0, then the tail forward;
+// conflict-free scalar smem reads) and the chains combine as (l0 + l1) + (l2 + l3)
+// over two shuffles. ~6 KB of smem per warp keeps ~32 warps per SM loading.
+// Keys (dist, id) are then sorted (bitonic, smem) and the first k written.
+__global__ void __launch_bounds__(RR_WARPS * 32)
 rerank_kernel(const float* __restrict__ data, int D, const float* __restrict__ queries, int64_t nq,
-              const uint64_t* __restrict__ fkeys, int L, int k, int chunk, int sstride, int lpad, int per_warp,
+              const uint64_t* __restrict__ fkeys, int L, int k, int lpad, int rstride, int per_warp,
               int32_t* __restrict__ out_ids, double* __restrict__ out_dists) {
+    const int wpb = blockDim.x >> 5;
     extern __shared__ __align__(16) unsigned char smem[];
+    const unsigned FULL = 0xFFFFFFFFu;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     unsigned char* base = smem + (size_t)warp * per_warp;
     float* qv = reinterpret_cast<float*>(base);
     uint64_t* keys = reinterpret_cast<uint64_t*>(base + ((D * 4 + 15) / 16) * 16);
     float* stage = reinterpret_cast<float*>(reinterpret_cast<unsigned char*>(keys) + (size_t)lpad * 8);
-    const int64_t qi = (int64_t)blockIdx.x * WPB + warp;
+    const int64_t qi = (int64_t)blockIdx.x * wpb + warp;
     if (qi >= nq) return;
     const float* q = queries + qi * D;
     for (int e = lane; e < D; e += 32) qv[e] = q[e];
     const uint64_t* fk = fkeys + qi * (int64_t)L;
-    // count valid keys (frontier is sorted; UMAX padding at the end)
+    // valid keys (the frontier is sorted; UMAX padding at the end)
     int n = 0;
     for (int b = 0; b < L; b += 32) {
         const int i = b + lane;
-        const uint32_t m = __ballot_sync(0xFFFFFFFFu, i < L && fk[i] != UMAX);
-        n += __popc(m);
+        n += __popc(__ballot_sync(FULL, i < L && fk[i] != UMAX));
     }
     for (int i = lane; i < lpad; i += 32) keys[i] = UMAX;
     __syncwarp();
-    for (int c = 0; c < n; c += 32) {
-        const int cnt = min(32, n - c);
+    const int r = lane >> 2, j = lane & 3;
+    const int D16 = D & ~15;
+    const bool vec = (D & 3) == 0;
+    for (int c = 0; c < n; c += 8) {
+        const int cnt = min(8, n - c);
         const uint32_t myid = lane < cnt ? (uint32_t)(fk[c + lane] & 0xFFFFFFFFull) : 0u;
-        Acc4 acc; acc.zero();
-        for (int e0 = 0; e0 < D; e0 += chunk) {
-            const int clen = min(chunk, D - e0);
-            for (int j = 0; j < cnt; ++j) {
-                const uint32_t id = __shfl_sync(0xFFFFFFFFu, myid, j);
-                const float* src = data + (size_t)id * D + e0;
-                float* dst = stage + j * sstride;
-                if (ALIGNED) { for (int f = lane; f < (clen >> 2); f += 32) cp_async16(dst + 4 * f, src + 4 * f); }
-                else { for (int f = lane; f < clen; f += 32) cp_async4(dst + f, src + f); }
-            }
-            cp_async_wait_all();
-            __syncwarp();
-            if (lane < cnt) a1_range<ALIGNED, true>(acc, stage + lane * sstride - e0, qv, e0, e0 + clen);
-            __syncwarp();
+        for (int t = 0; t < cnt; ++t) {
+            const uint32_t id = __shfl_sync(FULL, myid, t);
+            const float* src = data + (size_t)id * D;
+            float* dst = stage + t * rstride;
+            if (vec) { for (int f = lane; f < (D >> 2); f += 32) cp_async16(dst + 4 * f, src + 4 * f); }
+            else { for (int f = lane; f < D; f += 32) cp_async4(dst + f, src + f); }
         }
-        if (lane < cnt) keys[c + lane] = pack_key(acc.reduce(), myid);
+        cp_async_wait_all();
+        __syncwarp();
+        const bool on = r < cnt;
+        const float* row = stage + r * rstride;
+        float acc = 0.0f;
+        if (on) {
+            for (int b = 0; b < D16; b += 16) {
+#pragma unroll
+                for (int i = 3; i >= 0; --i) {
+                    const int e = b + 4 * i + j;
+                    const float d = __fsub_rn(row[e], qv[e]);
+                    acc = __fadd_rn(__fmul_rn(d, d), acc);
+                }
+            }
+            for (int e = D16 + j; e < D; e += 4) {  // tail: forward, element e -> chain e % 4
+                const float d = __fsub_rn(row[e], qv[e]);
+                acc = __fadd_rn(__fmul_rn(d, d), acc);
+            }
+        }
+        // (l0 + l1) + (l2 + l3)
+        const float pair = __fadd_rn(acc, __shfl_down_sync(FULL, acc, 1));
+        const float tot = __fadd_rn(pair, __shfl_down_sync(FULL, pair, 2));
+        const uint32_t rid = __shfl_sync(FULL, myid, r);
+        if (on && j == 0) keys[c + r] = pack_key(tot, rid);
+        __syncwarp();
     }
     __syncwarp();
     warp_bitonic_sort_smem(keys, lpad);
-    for (int j = lane; j < k; j += 32) {
-        const uint64_t key = keys[j];
-        const int64_t o = qi * k + j;
-        if (j < n) {
+    for (int jj = lane; jj < k; jj += 32) {
+        const uint64_t key = keys[jj];
+        const int64_t o = qi * k + jj;
+        if (jj < n) {
             out_ids[o] = (int32_t)(key & 0xFFFFFFFFull);
             out_dists[o] = (double)__uint_as_float((uint32_t)(key >> 32));
         } else {
@@ -719,23 +743,19 @@ int jb_rerank_topk(const float* data, int32_t dims, const float* queries, int64_
     JB_CHECK_ARG(k >= 1 && k <= beam_width, "k must satisfy 1 <= k <= beam_width");
     JB_CHECK_ARG(dims >= 1, "dims must be >= 1");
     if (nq == 0) return JB_OK;
-    const int chunk = std::min(128, ((dims + 31) / 32) * 32);
-    const int sstride = chunk + 4;
     const int lpad = std::max(32, pow2_ceil(beam_width));
-    const int per_warp = ((dims * 4 + 15) / 16) * 16 + lpad * 8 + 32 * sstride * 4;
-    const int smem = per_warp * WPB;
+    // staged row stride: 16 B aligned, and 4 (mod 32) words so the 8 rows x 4 chains
+    // of a scalar smem read hit 32 distinct banks
+    const int rstride = ((dims + 3) & ~3) + ((4 - (((dims + 3) & ~3) % 32) + 32) % 32);
+    const int per_warp = ((dims * 4 + 15) / 16) * 16 + lpad * 8 + 8 * rstride * 4;
+    const int wpb = std::max(1, std::min(RR_WARPS, (200 * 1024) / per_warp));  // high-D rows: fewer warps per block
+    const int smem = per_warp * wpb;
     JB_CHECK_ARG(smem <= 227 * 1024, "rerank: shared memory %d B exceeds 227 KB", smem);
     cudaStream_t st = as_stream(stream);
-    const unsigned grid = (unsigned)((nq + WPB - 1) / WPB);
-    if ((dims & 3) == 0) {
-        JB_CUDA(cudaFuncSetAttribute(rerank_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        rerank_kernel<true><<<grid, WPB * 32, smem, st>>>(data, dims, queries, nq, frontier_keys, beam_width, k,
-                                                          chunk, sstride, lpad, per_warp, out_ids, out_dists);
-    } else {
-        JB_CUDA(cudaFuncSetAttribute(rerank_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        rerank_kernel<false><<<grid, WPB * 32, smem, st>>>(data, dims, queries, nq, frontier_keys, beam_width, k,
-                                                           chunk, sstride, lpad, per_warp, out_ids, out_dists);
-    }
+    const unsigned grid = (unsigned)((nq + wpb - 1) / wpb);
+    JB_CUDA(cudaFuncSetAttribute(rerank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    rerank_kernel<<<grid, wpb * 32, smem, st>>>(data, dims, queries, nq, frontier_keys, beam_width, k, lpad, rstride,
+                                                per_warp, out_ids, out_dists);
     JB_LAUNCH_CHECK();
     return JB_OK;
 }
