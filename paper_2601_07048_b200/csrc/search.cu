@@ -38,7 +38,14 @@
 namespace jb {
 
 constexpr int WPB = 4;          // warps per block
-constexpr int RR_WARPS = 8;     // warps per block of the rerank kernel
+#ifndef JB_RR_WARPS
+#define JB_RR_WARPS 4
+#endif
+#ifndef JB_RR_ROWS
+#define JB_RR_ROWS 8
+#endif
+constexpr int RR_WARPS = JB_RR_WARPS;  // warps per block of the rerank kernel
+constexpr int RR_ROWS = JB_RR_ROWS;    // frontier rows staged per step (4 lanes each, RR_ROWS <= 8)
 constexpr int MAX_CHUNKS = 4;   // neighbour slots per hop: R <= 32 * MAX_CHUNKS
 #ifndef JB_COOP_MAX
 #define JB_COOP_MAX 2
@@ -545,8 +552,8 @@ rerank_kernel(const float* __restrict__ data, int D, const float* __restrict__ q
     const int r = lane >> 2, j = lane & 3;
     const int D16 = D & ~15;
     const bool vec = (D & 3) == 0;
-    for (int c = 0; c < n; c += 8) {
-        const int cnt = min(8, n - c);
+    for (int c = 0; c < n; c += RR_ROWS) {
+        const int cnt = min(RR_ROWS, n - c);
         const uint32_t myid = lane < cnt ? (uint32_t)(fk[c + lane] & 0xFFFFFFFFull) : 0u;
         for (int t = 0; t < cnt; ++t) {
             const uint32_t id = __shfl_sync(FULL, myid, t);
@@ -747,7 +754,7 @@ int jb_rerank_topk(const float* data, int32_t dims, const float* queries, int64_
     // staged row stride: 16 B aligned, and 4 (mod 32) words so the 8 rows x 4 chains
     // of a scalar smem read hit 32 distinct banks
     const int rstride = ((dims + 3) & ~3) + ((4 - (((dims + 3) & ~3) % 32) + 32) % 32);
-    const int per_warp = ((dims * 4 + 15) / 16) * 16 + lpad * 8 + 8 * rstride * 4;
+    const int per_warp = ((dims * 4 + 15) / 16) * 16 + lpad * 8 + RR_ROWS * rstride * 4;
     const int wpb = std::max(1, std::min(RR_WARPS, (200 * 1024) / per_warp));  // high-D rows: fewer warps per block
     const int smem = per_warp * wpb;
     JB_CHECK_ARG(smem <= 227 * 1024, "rerank: shared memory %d B exceeds 227 KB", smem);
