@@ -198,14 +198,17 @@ __device__ float pairwise_sum_f32(const float* a, int n) {
 }
 
 // rotated = f32(f64(q - c) @ rot^T) as a tiled f64 GEMM: block = 64 queries x 64
-// outputs, 256 threads with 4x4 outputs each, 16-wide k-steps through smem.
+// outputs, 256 threads with 4x4 outputs each, 16-wide k-steps through smem. Every
+// output is one sequential FMA chain over d = 0..D-1 (the order the tests pin).
+// Tiles are stored k-major ([k][row], 16 B aligned rows) so a thread's 4 query
+// values and 4 rotation values are two 32 B vector reads.
 constexpr int RT = 64, RK = 16;
 
 __global__ void __launch_bounds__(256)
 rotate_gemm_kernel(const float* __restrict__ queries, int64_t nq, int D, const float* __restrict__ centroid,
                    const double* __restrict__ rot, float* __restrict__ rotated) {
-    __shared__ double As[RT][RK + 1];
-    __shared__ double Bs[RT][RK + 1];
+    __shared__ __align__(16) double As[RK][RT + 2];
+    __shared__ __align__(16) double Bs[RK][RT + 2];
     const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
     const int64_t q0 = (int64_t)blockIdx.x * RT;
     const int o0 = blockIdx.y * RT;
@@ -222,17 +225,18 @@ rotate_gemm_kernel(const float* __restrict__ queries, int64_t nq, int D, const f
                 if (q0 + r < nq) va = (double)__fsub_rn(queries[(q0 + r) * D + d], centroid[d]);
                 if (o0 + r < D) vb = rot[(size_t)(o0 + r) * D + d];
             }
-            As[r][e] = va;
-            Bs[r][e] = vb;
+            As[e][r] = va;
+            Bs[e][r] = vb;
         }
         __syncthreads();
 #pragma unroll
         for (int e = 0; e < RK; ++e) {
-            double av[4], bv[4];
-#pragma unroll
-            for (int a = 0; a < 4; ++a) av[a] = As[ty * 4 + a][e];
-#pragma unroll
-            for (int b = 0; b < 4; ++b) bv[b] = Bs[tx * 4 + b][e];
+            const double2 a01 = *reinterpret_cast<const double2*>(&As[e][ty * 4]);
+            const double2 a23 = *reinterpret_cast<const double2*>(&As[e][ty * 4 + 2]);
+            const double2 b01 = *reinterpret_cast<const double2*>(&Bs[e][tx * 4]);
+            const double2 b23 = *reinterpret_cast<const double2*>(&Bs[e][tx * 4 + 2]);
+            const double av[4] = {a01.x, a01.y, a23.x, a23.y};
+            const double bv[4] = {b01.x, b01.y, b23.x, b23.y};
 #pragma unroll
             for (int a = 0; a < 4; ++a)
 #pragma unroll
