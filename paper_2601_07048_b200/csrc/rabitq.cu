@@ -197,12 +197,12 @@ __device__ float pairwise_sum_f32(const float* a, int n) {
     return __fadd_rn(pairwise_sum_f32(a, n2), pairwise_sum_f32(a + n2, n - n2));
 }
 
-// rotated = f32(f64(q - c) @ rot^T) as a tiled f64 GEMM: block = 64 queries x 64
-// outputs, 256 threads with 4x4 outputs each, 16-wide k-steps through smem. Every
-// output is one sequential FMA chain over d = 0..D-1 (the order the tests pin).
-// Tiles are stored k-major ([k][row], 16 B aligned rows) so a thread's 4 query
-// values and 4 rotation values are two 32 B vector reads.
-constexpr int RT = 64, RK = 16;
+// rotated = f32(f64(q - c) @ rot^T) as a tiled f64 GEMM: block = 32 queries x 32
+// outputs, 256 threads with 2x2 outputs each (many small blocks: a 5K-query
+// lane still puts ~40 warps on every SM), 16-wide k-steps through k-major smem
+// tiles. Every output is one sequential FMA chain over d = 0..D-1 (the order the
+// tests pin against the reference's dgemm results).
+constexpr int RT = 32, RK = 16;
 
 __global__ void __launch_bounds__(256)
 rotate_gemm_kernel(const float* __restrict__ queries, int64_t nq, int D, const float* __restrict__ centroid,
@@ -212,11 +212,7 @@ rotate_gemm_kernel(const float* __restrict__ queries, int64_t nq, int D, const f
     const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
     const int64_t q0 = (int64_t)blockIdx.x * RT;
     const int o0 = blockIdx.y * RT;
-    double acc[4][4];
-#pragma unroll
-    for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+    double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
     for (int k0 = 0; k0 < D; k0 += RK) {
         for (int i = tid; i < RT * RK; i += 256) {
             const int r = i / RK, e = i % RK, d = k0 + e;
@@ -231,26 +227,22 @@ rotate_gemm_kernel(const float* __restrict__ queries, int64_t nq, int D, const f
         __syncthreads();
 #pragma unroll
         for (int e = 0; e < RK; ++e) {
-            const double2 a01 = *reinterpret_cast<const double2*>(&As[e][ty * 4]);
-            const double2 a23 = *reinterpret_cast<const double2*>(&As[e][ty * 4 + 2]);
-            const double2 b01 = *reinterpret_cast<const double2*>(&Bs[e][tx * 4]);
-            const double2 b23 = *reinterpret_cast<const double2*>(&Bs[e][tx * 4 + 2]);
-            const double av[4] = {a01.x, a01.y, a23.x, a23.y};
-            const double bv[4] = {b01.x, b01.y, b23.x, b23.y};
-#pragma unroll
-            for (int a = 0; a < 4; ++a)
-#pragma unroll
-                for (int b = 0; b < 4; ++b) acc[a][b] = fma(av[a], bv[b], acc[a][b]);
+            const double2 a2 = *reinterpret_cast<const double2*>(&As[e][ty * 2]);
+            const double2 b2 = *reinterpret_cast<const double2*>(&Bs[e][tx * 2]);
+            acc[0][0] = fma(a2.x, b2.x, acc[0][0]);
+            acc[0][1] = fma(a2.x, b2.y, acc[0][1]);
+            acc[1][0] = fma(a2.y, b2.x, acc[1][0]);
+            acc[1][1] = fma(a2.y, b2.y, acc[1][1]);
         }
         __syncthreads();
     }
 #pragma unroll
-    for (int a = 0; a < 4; ++a) {
-        const int64_t q = q0 + ty * 4 + a;
+    for (int a = 0; a < 2; ++a) {
+        const int64_t q = q0 + ty * 2 + a;
         if (q >= nq) continue;
 #pragma unroll
-        for (int b = 0; b < 4; ++b) {
-            const int o = o0 + tx * 4 + b;
+        for (int b = 0; b < 2; ++b) {
+            const int o = o0 + tx * 2 + b;
             if (o < D) rotated[q * D + o] = __double2float_rn(acc[a][b]);
         }
     }
