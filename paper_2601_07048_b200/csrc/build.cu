@@ -31,6 +31,12 @@
 namespace jb {
 
 constexpr int BW = 4;  // warps per block in the per-vertex kernels
+#ifndef JB_STAGE_KB
+#define JB_STAGE_KB 26     // per-warp smem budget for staged candidate rows
+#endif
+#ifndef JB_OWNER_EXTRA
+#define JB_OWNER_EXTRA 16  // owner-merge staging: up to R + this many candidate rows
+#endif
 constexpr uint32_t NO_TARGET = 0xFFFFFFFFu;
 
 // d(pivot, row) with the row in the data role and the pivot norm added last
@@ -758,7 +764,7 @@ struct Bufs {
 template <class M>
 static int staged_rows(const M& m, int want, int R) {
     if (!M::kStage) return 0;
-    int crows = std::min(want, (26 * 1024 - m.pivot_words() * 4) / (m.stage_stride_words() * 4 + 4));
+    int crows = std::min(want, (JB_STAGE_KB * 1024 - m.pivot_words() * 4) / (m.stage_stride_words() * 4 + 4));
     return crows < R + 1 ? 0 : crows;
 }
 
@@ -964,7 +970,7 @@ static int merge_phase(const M& m, const jb_insert_args& a, double alpha2, uint3
         JB_CUDA(cudaMemsetAsync(ptop, 0, sizeof(unsigned long long), st));
         JB_CUDA(cudaMemsetAsync(err, 0, sizeof(int), st));
         // owners stage up to R + 16 candidate rows in smem when they fit
-        const int crows = staged_rows(m, R + 16, R);
+        const int crows = staged_rows(m, R + JB_OWNER_EXTRA, R);
         const int osm = owner_per_warp(m, R, crows) * BW;
         JB_CUDA(cudaFuncSetAttribute(owner_merge_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, osm));
         owner_merge_kernel<M><<<(unsigned)((hseg + BW - 1) / BW), BW * 32, osm, st>>>(

@@ -17,11 +17,12 @@ ds.device()
 p = jb.BuildParams(degree_cap=32, build_beam_width=64, alpha=1.2, max_batch=100_000)
 jb.build(jb.VectorDataset(x[:50_000]), p)  # warm-up
 torch.cuda.synchronize()
-os.environ["JB_PROFILE"] = "1"
-jbuild.WORK[:] = 0
-t = time.perf_counter()
-g = jb.build(ds, p)
-torch.cuda.synchronize()
-el = time.perf_counter() - t
-print(f"build {n}x{d}: {el:.3f} s, {n / el:.0f} inserts/s; work {dict(zip(jbuild.WORK_FIELDS, jbuild.WORK.tolist()))}",
-      file=sys.stderr)
+os.environ["JB_PROFILE"] = os.environ.get("JB_EXP_PROFILE", "0")
+for rep in range(int(os.environ.get("JB_EXP_REPS", "1"))):
+    jbuild.WORK[:] = 0
+    t = time.perf_counter()
+    g = jb.build(ds, p)
+    torch.cuda.synchronize()
+    el = time.perf_counter() - t
+    print(f"build {n}x{d}: {el:.3f} s, {n / el:.0f} inserts/s; work {dict(zip(jbuild.WORK_FIELDS, jbuild.WORK.tolist()))}",
+          file=sys.stderr)
