@@ -186,8 +186,9 @@ def _setup(args, world, rank):
     t_gen = time.perf_counter() - t0
 
     params = jb.BuildParams(degree_cap=32, build_beam_width=64, alpha=1.2, max_batch=100_000)
-    # untimed warm-up build (first-call kernel attributes, allocator growth)
-    jb.build(jb.VectorDataset(x[: min(args.n, 50_000)]), params)
+    # untimed warm-up build (first-call kernel attributes; the stream-ordered pool grows to the
+    # size of a max_batch=100K insert batch, which a production process has done long before)
+    jb.build(jb.VectorDataset(x[: min(args.n, 250_000)]), params)  # reaches 100K batches: pool grown
     torch.cuda.synchronize()
     import importlib
 

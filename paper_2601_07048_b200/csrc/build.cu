@@ -125,11 +125,22 @@ __device__ int warp_prune_staged(uint64_t* cand, int n, double alpha2, int R, co
         ++kept;
         __syncwarp();
         if (kept >= R) break;
-        for (int i = lane; i < n; i += 32) {
+        // survivors two per lane per step (the second slot is i + 32), sharing the star's reads
+        for (int i = lane; i < n; i += 64) {
+            const int i2 = i + 32;
             const uint64_t c = cand[i];
-            if (c == UMAX) continue;
-            const uint32_t dsp = m.dist_staged(rows, cn, i, mi);
-            if (!(__dmul_rn(alpha2, M::value(dsp)) > M::value((uint32_t)(c >> 32)))) cand[i] = UMAX;
+            const uint64_t c2 = i2 < n ? cand[i2] : UMAX;
+            if (c != UMAX && c2 != UMAX) {
+                uint32_t d0, d1;
+                m.dist_staged2(rows, cn, i, i2, mi, d0, d1);
+                if (!(__dmul_rn(alpha2, M::value(d0)) > M::value((uint32_t)(c >> 32)))) cand[i] = UMAX;
+                if (!(__dmul_rn(alpha2, M::value(d1)) > M::value((uint32_t)(c2 >> 32)))) cand[i2] = UMAX;
+            } else if (c != UMAX || c2 != UMAX) {
+                const int ii = c != UMAX ? i : i2;
+                const uint64_t cc = c != UMAX ? c : c2;
+                const uint32_t dsp = m.dist_staged(rows, cn, ii, mi);
+                if (!(__dmul_rn(alpha2, M::value(dsp)) > M::value((uint32_t)(cc >> 32)))) cand[ii] = UMAX;
+            }
         }
         __syncwarp();
     }

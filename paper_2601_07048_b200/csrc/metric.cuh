@@ -78,6 +78,34 @@ struct F32Metric {
         else a1_range<false, false>(acc, a, b, 0, D);
         return __float_as_uint(exact_from_dot(__uint_as_float(cn[i]), acc.reduce(), __uint_as_float(cn[p])));
     }
+    // two rows against one pivot: the pivot's vectors are read once, the two A1
+    // chains interleave (same per-row order, twice the independent work per lane)
+    __device__ void dist_staged2(const uint32_t* rows, const uint32_t* cn, int i0, int i1, int p, uint32_t& d0,
+                                 uint32_t& d1) const {
+        if ((D & 15) != 0) {
+            d0 = dist_staged(rows, cn, i0, p);
+            d1 = dist_staged(rows, cn, i1, p);
+            return;
+        }
+        const int rs = stage_stride_words();
+        const float4* a0 = reinterpret_cast<const float4*>(rows + (size_t)i0 * rs);
+        const float4* a1 = reinterpret_cast<const float4*>(rows + (size_t)i1 * rs);
+        const float4* b = reinterpret_cast<const float4*>(rows + (size_t)p * rs);
+        Acc4 x0, x1;
+        x0.zero();
+        x1.zero();
+        for (int v = 0; v < (D >> 2); v += 4) {
+#pragma unroll
+            for (int i = 3; i >= 0; --i) {
+                const float4 bv = b[v + i];
+                x0.madd(a0[v + i], bv);
+                x1.madd(a1[v + i], bv);
+            }
+        }
+        const float pn = __uint_as_float(cn[p]);
+        d0 = __float_as_uint(exact_from_dot(__uint_as_float(cn[i0]), x0.reduce(), pn));
+        d1 = __float_as_uint(exact_from_dot(__uint_as_float(cn[i1]), x1.reduce(), pn));
+    }
 };
 
 // <a, b> of two u8 rows; a in global or smem, b in smem (16 B aligned). Exact.
@@ -155,6 +183,11 @@ struct U8Metric {
         const uint8_t* a = reinterpret_cast<const uint8_t*>(rows + (size_t)i * rs);
         const uint8_t* b = reinterpret_cast<const uint8_t*>(rows + (size_t)p * rs);
         return u8_dist(cn[i], u8_dot(a, b, D), cn[p]);
+    }
+    __device__ void dist_staged2(const uint32_t* rows, const uint32_t* cn, int i0, int i1, int p, uint32_t& d0,
+                                 uint32_t& d1) const {
+        d0 = dist_staged(rows, cn, i0, p);
+        d1 = dist_staged(rows, cn, i1, p);
     }
 };
 
@@ -282,6 +315,9 @@ struct RabitqMetric {
     // never staged (the host passes crows = 0); present for the shared kernel bodies
     __device__ void stage(uint32_t*, uint32_t*, const uint64_t*, int) const { __trap(); }
     __device__ uint32_t dist_staged(const uint32_t*, const uint32_t*, int, int) const { __trap(); return 0; }
+    __device__ void dist_staged2(const uint32_t*, const uint32_t*, int, int, int, uint32_t&, uint32_t&) const {
+        __trap();
+    }
 };
 
 }  // namespace jb

@@ -552,15 +552,29 @@ rerank_kernel(const float* __restrict__ data, int D, const float* __restrict__ q
     const int r = lane >> 2, j = lane & 3;
     const int D16 = D & ~15;
     const bool vec = (D & 3) == 0;
+    const int nv = D >> 2;  // 16 B chunks per row
+    const uint32_t stage_s = (uint32_t)__cvta_generic_to_shared(stage);
     for (int c = 0; c < n; c += RR_ROWS) {
         const int cnt = min(RR_ROWS, n - c);
         const uint32_t myid = lane < cnt ? (uint32_t)(fk[c + lane] & 0xFFFFFFFFull) : 0u;
-        for (int t = 0; t < cnt; ++t) {
-            const uint32_t id = __shfl_sync(FULL, myid, t);
-            const float* src = data + (size_t)id * D;
-            float* dst = stage + t * rstride;
-            if (vec) { for (int f = lane; f < (D >> 2); f += 32) cp_async16(dst + 4 * f, src + 4 * f); }
-            else { for (int f = lane; f < D; f += 32) cp_async4(dst + f, src + f); }
+        if (vec && nv <= 32) {  // one 16 B chunk per lane per row (D <= 128)
+#pragma unroll
+            for (int t = 0; t < RR_ROWS; ++t) {
+                const uint32_t id = __shfl_sync(FULL, myid, t);
+                if (t < cnt && lane < nv) {
+                    const float* src = data + (size_t)id * D + 4 * lane;
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(stage_s + (t * rstride + 4 * lane) * 4),
+                                 "l"(src));
+                }
+            }
+        } else {
+            for (int t = 0; t < cnt; ++t) {
+                const uint32_t id = __shfl_sync(FULL, myid, t);
+                const float* src = data + (size_t)id * D;
+                float* dst = stage + t * rstride;
+                if (vec) { for (int f = lane; f < nv; f += 32) cp_async16(dst + 4 * f, src + 4 * f); }
+                else { for (int f = lane; f < D; f += 32) cp_async4(dst + f, src + f); }
+            }
         }
         cp_async_wait_all();
         __syncwarp();
@@ -589,6 +603,37 @@ rerank_kernel(const float* __restrict__ data, int D, const float* __restrict__ q
         __syncwarp();
     }
     __syncwarp();
+    if (k <= 32) {  // the k smallest (dist, id) keys in order: repeated warp minimum
+        uint64_t mine = UMAX;  // this lane's answer slot (rank == lane)
+        for (int jj = 0; jj < k; ++jj) {
+            uint64_t m = UMAX;
+            int mi = -1;
+            for (int i = lane; i < n; i += 32) {
+                const uint64_t c = keys[i];
+                if (c < m) { m = c; mi = i; }
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const uint64_t om = shfl_xor_u64(m, o);
+                const int oi = __shfl_xor_sync(FULL, mi, o);
+                if (om < m) { m = om; mi = oi; }
+            }
+            if (lane == jj) mine = m;
+            if (lane == 0 && mi >= 0) keys[mi] = UMAX;
+            __syncwarp();
+        }
+        if (lane < k) {
+            const int64_t o = qi * k + lane;
+            if (mine != UMAX) {
+                out_ids[o] = (int32_t)(mine & 0xFFFFFFFFull);
+                out_dists[o] = (double)__uint_as_float((uint32_t)(mine >> 32));
+            } else {
+                out_ids[o] = -1;
+                out_dists[o] = __longlong_as_double(0x7FF0000000000000ll);
+            }
+        }
+        return;
+    }
     warp_bitonic_sort_smem(keys, lpad);
     for (int jj = lane; jj < k; jj += 32) {
         const uint64_t key = keys[jj];

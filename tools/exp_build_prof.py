@@ -15,7 +15,7 @@ x = jb.gen_lowrank(n, d, seed=1, d_int=16, noise=0.05, basis_seed=0)
 ds = jb.VectorDataset(x)
 ds.device()
 p = jb.BuildParams(degree_cap=32, build_beam_width=64, alpha=1.2, max_batch=100_000)
-jb.build(jb.VectorDataset(x[:50_000]), p)  # warm-up
+jb.build(jb.VectorDataset(x[:250_000]), p)  # warm-up (pool grown to 100K batches)
 torch.cuda.synchronize()
 os.environ["JB_PROFILE"] = os.environ.get("JB_EXP_PROFILE", "0")
 for rep in range(int(os.environ.get("JB_EXP_REPS", "1"))):
