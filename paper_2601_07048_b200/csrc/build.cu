@@ -418,7 +418,7 @@ owner_merge_kernel(const M m, double alpha2, int R, int always_prune, const uint
         for (int j = lane; j < hd; j += 32) cand[j] = (uint64_t)(uint32_t)have[j];  // id only, for staging
         __syncwarp();
         m.stage(rows, cn, cand, n);
-        for (int j = lane; j < hd; j += 32) cand[j] = key_of(m.dist(pv, (uint32_t)have[j]), (uint32_t)have[j]);
+        for (int j = lane; j < hd; j += 32) cand[j] = key_of(m.dist_pivot_staged(pv, rows, cn, j), (uint32_t)have[j]);
         __syncwarp();
         k = warp_prune_staged(cand, n, alpha2, R, m, rows, cn, kid, kd);
     } else {
@@ -771,6 +771,39 @@ struct Bufs {
     T* var = bufs.get<T>((n), st, _ce);         \
     JB_CUDA(_ce);
 
+// JB_PROFILE=1: per-batch phase timings on stderr (stream events; diagnostics only)
+struct PhaseTimer {
+    bool on = false;
+    cudaStream_t st = nullptr;
+    std::vector<std::pair<const char*, cudaEvent_t>> ev;
+    explicit PhaseTimer(cudaStream_t s) : st(s) {
+        const char* e = getenv("JB_PROFILE");
+        on = e && e[0] == '1';
+        mark("start");
+    }
+    void mark(const char* name) {
+        if (!on) return;
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        cudaEventRecord(e, st);
+        ev.emplace_back(name, e);
+    }
+    void report(int64_t start, int64_t stop, const char* what = "batch") {
+        if (!on) return;
+        mark("end");
+        cudaEventSynchronize(ev.back().second);
+        fprintf(stderr, "[jb] %s [%lld, %lld):", what, (long long)start, (long long)stop);
+        for (size_t i = 1; i < ev.size(); ++i) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, ev[i - 1].second, ev[i].second);
+            fprintf(stderr, " %s %.2fms", ev[i].first, ms);
+        }
+        fprintf(stderr, "\n");
+        for (auto& p : ev) cudaEventDestroy(p.second);
+        ev.clear();
+    }
+};
+
 // Per-warp candidate-row staging budget (~26 KB per warp beside the pivot).
 template <class M>
 static int staged_rows(const M& m, int want, int R) {
@@ -803,6 +836,7 @@ static int repair(const M& m, const jb_insert_args& a, int64_t n_active, int64_t
     const int T = 256;
     const unsigned nblk = (unsigned)((n_active + T - 1) / T);
     for (int round = 0;; ++round) {
+        PhaseTimer rt(st);
         // BFS from the entry
         bfs_init_kernel<<<nblk, T, 0, st>>>(seen, n_active, entry, fa, counts);
         int fcount = 1;
@@ -826,9 +860,13 @@ static int repair(const M& m, const jb_insert_args& a, int64_t n_active, int64_t
         JB_CUDA(cudaMemcpyAsync(h, counts + 2, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
         JB_CUDA(cudaStreamSynchronize(st));
         const int nlost = h[0], nreach = h[1];
+        rt.mark("bfs");
         if (getenv("JB_PROFILE") && getenv("JB_PROFILE")[0] == '1')
             fprintf(stderr, "[jb]   repair round %d: stranded %d reachable %d\n", round, nlost, nreach);
-        if (nlost == 0) break;
+        if (nlost == 0) {
+            rt.report(round, round, "  repair timings round");
+            break;
+        }
         // donors: top-`fan` reachable by (d(x, r), r) for every stranded x (build.py:185-192)
         BALLOC(donors, int32_t, (size_t)nlost * fan);
         BALLOC(okey, uint64_t, nlost);
@@ -858,6 +896,7 @@ static int repair(const M& m, const jb_insert_args& a, int64_t n_active, int64_t
                                                                                  fan, part);
         }
         JB_LAUNCH_CHECK();
+        rt.mark("scan");
         donor_merge_kernel<<<(unsigned)((nlost * 32 + 255) / 256), 256, 0, st>>>(part, slices, nlost, fan, lost, donors,
                                                                                okey, oval);
         JB_LAUNCH_CHECK();
@@ -867,9 +906,12 @@ static int repair(const M& m, const jb_insert_args& a, int64_t n_active, int64_t
         JB_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, okey, okey2, oval, oval2, nlost, 0, 64, st));
         const int asm_bytes = m.pivot_words() * 4;
         JB_CUDA(cudaFuncSetAttribute(attach_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, asm_bytes));
+        rt.mark("order");
         attach_kernel<M><<<1, 32, asm_bytes, st>>>(m, a.adjacency, a.degrees, R, pinned, seen, lost, oval2, nlost,
                                                     donors, fan, fa, bridges, err, err + 1);
         JB_LAUNCH_CHECK();
+        rt.mark("attach");
+        rt.report(round, round, "  repair timings round");
         int herr[2];
         JB_CUDA(cudaMemcpyAsync(herr, err, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
         JB_CUDA(cudaStreamSynchronize(st));
@@ -1025,38 +1067,6 @@ static int sum2(const int32_t* v, const int32_t* w, int64_t n, Bufs& bufs, cudaS
     return JB_OK;
 }
 
-// JB_PROFILE=1: per-batch phase timings on stderr (stream events; diagnostics only)
-struct PhaseTimer {
-    bool on = false;
-    cudaStream_t st = nullptr;
-    std::vector<std::pair<const char*, cudaEvent_t>> ev;
-    explicit PhaseTimer(cudaStream_t s) : st(s) {
-        const char* e = getenv("JB_PROFILE");
-        on = e && e[0] == '1';
-        mark("start");
-    }
-    void mark(const char* name) {
-        if (!on) return;
-        cudaEvent_t e;
-        cudaEventCreate(&e);
-        cudaEventRecord(e, st);
-        ev.emplace_back(name, e);
-    }
-    void report(int64_t start, int64_t stop) {
-        if (!on) return;
-        mark("end");
-        cudaEventSynchronize(ev.back().second);
-        fprintf(stderr, "[jb] batch [%lld, %lld):", (long long)start, (long long)stop);
-        for (size_t i = 1; i < ev.size(); ++i) {
-            float ms = 0.f;
-            cudaEventElapsedTime(&ms, ev[i - 1].second, ev[i].second);
-            fprintf(stderr, " %s %.2fms", ev[i].first, ms);
-        }
-        fprintf(stderr, "\n");
-        for (auto& p : ev) cudaEventDestroy(p.second);
-        ev.clear();
-    }
-};
 
 static int validate_insert(const jb_insert_args& a) {
     JB_CHECK_ARG(a.adjacency && a.degrees, "batch insert: missing graph arrays");

@@ -78,6 +78,15 @@ struct F32Metric {
         else a1_range<false, false>(acc, a, b, 0, D);
         return __float_as_uint(exact_from_dot(__uint_as_float(cn[i]), acc.reduce(), __uint_as_float(cn[p])));
     }
+    // d(pivot in pv, staged row i): same operation order as dist() on the global row
+    __device__ uint32_t dist_pivot_staged(const uint32_t* pv, const uint32_t* rows, const uint32_t* cn, int i) const {
+        const float* f = reinterpret_cast<const float*>(pv);
+        const float* a = reinterpret_cast<const float*>(rows + (size_t)i * stage_stride_words());
+        Acc4 acc; acc.zero();
+        if ((D & 3) == 0) a1_range<true, false>(acc, a, f, 0, D);
+        else a1_range<false, false>(acc, a, f, 0, D);
+        return __float_as_uint(exact_from_dot(__uint_as_float(cn[i]), acc.reduce(), f[((D + 3) & ~3)]));
+    }
     // two rows against one pivot: the pivot's vectors are read once, the two A1
     // chains interleave (same per-row order, twice the independent work per lane)
     __device__ void dist_staged2(const uint32_t* rows, const uint32_t* cn, int i0, int i1, int p, uint32_t& d0,
@@ -188,6 +197,10 @@ struct U8Metric {
                                  uint32_t& d1) const {
         d0 = dist_staged(rows, cn, i0, p);
         d1 = dist_staged(rows, cn, i1, p);
+    }
+    __device__ uint32_t dist_pivot_staged(const uint32_t* pv, const uint32_t* rows, const uint32_t* cn, int i) const {
+        const uint8_t* a = reinterpret_cast<const uint8_t*>(rows + (size_t)i * stage_stride_words());
+        return u8_dist(cn[i], u8_dot(a, reinterpret_cast<const uint8_t*>(pv), D), pv[((D + 15) & ~15) / 4]);
     }
 };
 
@@ -317,6 +330,10 @@ struct RabitqMetric {
     __device__ uint32_t dist_staged(const uint32_t*, const uint32_t*, int, int) const { __trap(); return 0; }
     __device__ void dist_staged2(const uint32_t*, const uint32_t*, int, int, int, uint32_t&, uint32_t&) const {
         __trap();
+    }
+    __device__ uint32_t dist_pivot_staged(const uint32_t*, const uint32_t*, const uint32_t*, int) const {
+        __trap();
+        return 0;
     }
 };
 
