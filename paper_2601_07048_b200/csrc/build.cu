@@ -467,17 +467,18 @@ __global__ void split_kernel(const int32_t* __restrict__ seen, int64_t n, int32_
 constexpr int DT = 64;      // tile edge
 constexpr int FAN = 16;     // min(R, 16) donors, upper bound
 
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 2)
 donor_scan_kernel(const float* __restrict__ data, const float* __restrict__ norms, int D, const int32_t* __restrict__ lost,
                   int nlost, const int32_t* __restrict__ reach, int nreach, int slices, int fan,
                   uint64_t* __restrict__ part) {
     extern __shared__ __align__(16) unsigned char dsh[];
     const int KB = 16;  // elements per k-step (one A1 block)
-    float* As = reinterpret_cast<float*>(dsh);             // [DT][KB+1]  stranded
-    float* Bs = As + DT * (KB + 1);                        // [DT][KB+1]  reachable
+    const int AS = D + 1;                                  // resident stranded tile row stride
+    float* Ares = reinterpret_cast<float*>(dsh);           // [DT][D+1]  stranded rows, whole slice
+    float* Bs = Ares + DT * AS;                            // [DT][KB+1] reachable k-step
     float* dist = Bs + DT * (KB + 1);                      // [DT][DT+1]
-    uint64_t* top = reinterpret_cast<uint64_t*>(dist + DT * (DT + 1));  // [DT][FAN] (8B aligned: 6336 floats)
-    uint64_t* mbuf = top + DT * FAN;                                           // [8 warps][128]
+    uint64_t* top = reinterpret_cast<uint64_t*>(dist + DT * (DT + 1) + ((DT * AS + DT * (KB + 1) + DT * (DT + 1)) & 1));
+    uint64_t* mbuf = top + DT * FAN;                       // [8 warps][128]
     const int tid = threadIdx.x;
     const int tx = tid & 15, ty = tid >> 4;  // 16 x 16 threads, 4x4 pairs each
     const int s0 = blockIdx.x * DT;
@@ -485,26 +486,44 @@ donor_scan_kernel(const float* __restrict__ data, const float* __restrict__ norm
     const int64_t per = (nreach + slices - 1) / slices;
     const int64_t r_begin = slice * per, r_end = (nreach < r_begin + per) ? (int64_t)nreach : r_begin + per;
     for (int i = tid; i < DT * FAN; i += 256) top[i] = UMAX;
+    // the 64 stranded rows stay in smem for the whole slice
+    for (int i = tid; i < DT * D; i += 256) {
+        const int row = i / D, e = i % D;
+        Ares[row * AS + e] = (s0 + row < nlost) ? data[(size_t)lost[s0 + row] * D + e] : 0.f;
+    }
     __syncthreads();
+    // reachable rows stream through a 64 x 16 smem tile; each thread prefetches its 4
+    // elements of the next k-step into registers while the current one is consumed
     for (int64_t r0 = r_begin; r0 < r_end; r0 += DT) {
         Acc4 acc[4][4];
 #pragma unroll
         for (int a = 0; a < 4; ++a)
 #pragma unroll
             for (int b = 0; b < 4; ++b) acc[a][b].zero();
+        // prefetch k-step 0
+        float pf[4];
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+            const int i = tid + 256 * h, row = i / KB, e = i % KB;
+            pf[h] = (e < min(KB, D) && r0 + row < r_end) ? __ldg(data + (size_t)reach[r0 + row] * D + e) : 0.f;
+        }
         for (int k0 = 0; k0 < D; k0 += KB) {
             const int kl = min(KB, D - k0);
-            for (int i = tid; i < DT * KB; i += 256) {
-                const int row = i / KB, e = i % KB;
-                float va = 0.f, vb = 0.f;
-                if (e < kl) {
-                    if (s0 + row < nlost) va = data[(size_t)lost[s0 + row] * D + k0 + e];
-                    if (r0 + row < r_end) vb = data[(size_t)reach[r0 + row] * D + k0 + e];
-                }
-                As[row * (KB + 1) + e] = va;
-                Bs[row * (KB + 1) + e] = vb;
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+                const int i = tid + 256 * h, row = i / KB, e = i % KB;
+                Bs[row * (KB + 1) + e] = pf[h];
             }
             __syncthreads();
+            if (k0 + KB < D) {  // next k-step's loads in flight during this step's math
+                const int kn = min(KB, D - k0 - KB);
+#pragma unroll
+                for (int h = 0; h < 4; ++h) {
+                    const int i = tid + 256 * h, row = i / KB, e = i % KB;
+                    pf[h] = (e < kn && r0 + row < r_end) ? __ldg(data + (size_t)reach[r0 + row] * D + k0 + KB + e) : 0.f;
+                }
+            }
+            const float* Ak = Ares + k0;
             if (kl == KB) {
                 // A1 order inside a 16-block: vectors 3,2,1,0; lane j = element % 4
 #pragma unroll
@@ -513,7 +532,7 @@ donor_scan_kernel(const float* __restrict__ data, const float* __restrict__ norm
                     for (int j = 0; j < 4; ++j) {
                         float av[4], bv[4];
 #pragma unroll
-                        for (int a = 0; a < 4; ++a) av[a] = As[(ty * 4 + a) * (KB + 1) + 4 * v + j];
+                        for (int a = 0; a < 4; ++a) av[a] = Ak[(ty * 4 + a) * AS + 4 * v + j];
 #pragma unroll
                         for (int b = 0; b < 4; ++b) bv[b] = Bs[(tx * 4 + b) * (KB + 1) + 4 * v + j];
 #pragma unroll
@@ -532,7 +551,7 @@ donor_scan_kernel(const float* __restrict__ data, const float* __restrict__ norm
                 for (int e = 0; e < kl; ++e) {  // tail: forward
                     float av[4], bv[4];
 #pragma unroll
-                    for (int a = 0; a < 4; ++a) av[a] = As[(ty * 4 + a) * (KB + 1) + e];
+                    for (int a = 0; a < 4; ++a) av[a] = Ak[(ty * 4 + a) * AS + e];
 #pragma unroll
                     for (int b = 0; b < 4; ++b) bv[b] = Bs[(tx * 4 + b) * (KB + 1) + e];
 #pragma unroll
@@ -875,12 +894,12 @@ static int repair(const M& m, const jb_insert_args& a, int64_t n_active, int64_t
         BALLOC(oval2, int32_t, nlost);
         int slices;
         uint64_t* part;
-        if (std::is_same<M, F32Metric>::value) {  // tiled A1 scan on the f32 rows
+        if (std::is_same<M, F32Metric>::value && D <= 256) {  // tiled A1 scan on the f32 rows
             const int sblocks = (nlost + DT - 1) / DT;
-            slices = std::max(1, std::min(64, (4 * sm_count_current() + sblocks - 1) / sblocks));
+            slices = std::max(1, std::min(128, (4 * sm_count_current() + sblocks - 1) / sblocks));
             slices = (int)std::min<int64_t>(slices, std::max<int64_t>(1, (nreach + DT - 1) / DT));
             part = bufs.get<uint64_t>((size_t)slices * nlost * fan, st, _ce); JB_CUDA(_ce);
-            const size_t dsm = (size_t)(2 * DT * 17 + DT * (DT + 1)) * 4 + DT * FAN * 8 + 8 * 128 * 8;
+            const size_t dsm = (size_t)(DT * (D + 1) + DT * 17 + DT * (DT + 1) + 1) * 4 + DT * FAN * 8 + 8 * 128 * 8;
             JB_CUDA(cudaFuncSetAttribute(donor_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
             donor_scan_kernel<<<dim3(sblocks, slices), 256, dsm, st>>>(a.data, a.data_norms, D, lost, nlost, reach,
                                                                       nreach, slices, fan, part);
