@@ -34,6 +34,9 @@ constexpr int BW = 4;  // warps per block in the per-vertex kernels
 #ifndef JB_STAGE_KB
 #define JB_STAGE_KB 26     // per-warp smem budget for staged candidate rows
 #endif
+#ifndef JB_P2_KB
+#define JB_P2_KB 20  // phase-2 (new vertex) prune staging budget per warp
+#endif
 #ifndef JB_OWNER_EXTRA
 #define JB_OWNER_EXTRA 16  // owner-merge staging: up to R + this many candidate rows
 #endif
@@ -333,7 +336,10 @@ __global__ void seg_head_kernel(const uint32_t* __restrict__ t, int64_t n, uint8
     flag[i] = (t[i] != NO_TARGET) && (i == 0 || t[i] != t[i - 1]);
 }
 
-constexpr int OWNER_SC = 256;  // smem candidate slots per owner warp
+#ifndef JB_OWNER_SC
+#define JB_OWNER_SC 64
+#endif
+constexpr int OWNER_SC = JB_OWNER_SC;  // smem candidate slots per owner warp (larger groups use the global pool)
 // per-warp bytes: keys | vertex words (pivot, staged rows, norms) | have, kid, kd
 template <class M>
 __host__ __device__ inline int owner_per_warp(const M& m, int R, int crows) {
@@ -825,9 +831,9 @@ struct PhaseTimer {
 
 // Per-warp candidate-row staging budget (~26 KB per warp beside the pivot).
 template <class M>
-static int staged_rows(const M& m, int want, int R) {
+static int staged_rows(const M& m, int want, int R, int budget_kb = JB_STAGE_KB) {
     if (!M::kStage) return 0;
-    int crows = std::min(want, (JB_STAGE_KB * 1024 - m.pivot_words() * 4) / (m.stage_stride_words() * 4 + 4));
+    int crows = std::min(want, (budget_kb * 1024 - m.pivot_words() * 4) / (m.stage_stride_words() * 4 + 4));
     return crows < R + 1 ? 0 : crows;
 }
 
@@ -1041,8 +1047,14 @@ static int merge_phase(const M& m, const jb_insert_args& a, double alpha2, uint3
         BALLOC(err, int, 1);
         JB_CUDA(cudaMemsetAsync(ptop, 0, sizeof(unsigned long long), st));
         JB_CUDA(cudaMemsetAsync(err, 0, sizeof(int), st));
-        // owners stage up to R + 16 candidate rows in smem when they fit
-        const int crows = staged_rows(m, R + JB_OWNER_EXTRA, R);
+        // owners stage up to R + 16 candidate rows in smem when they fit; R + 8 instead
+        // when that lifts the kernel from 2 to 3 resident blocks per SM (short rows)
+        int crows = staged_rows(m, R + JB_OWNER_EXTRA, R);
+        const int crows_lo = staged_rows(m, R + JB_OWNER_EXTRA / 2, R);
+        const int smem_sm = 227 * 1024;
+        if (crows_lo > 0 && smem_sm / (owner_per_warp(m, R, crows) * BW) < 3 &&
+            smem_sm / (owner_per_warp(m, R, crows_lo) * BW) >= 3)
+            crows = crows_lo;
         const int osm = owner_per_warp(m, R, crows) * BW;
         JB_CUDA(cudaFuncSetAttribute(owner_merge_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, osm));
         owner_merge_kernel<M><<<(unsigned)((hseg + BW - 1) / BW), BW * 32, osm, st>>>(
@@ -1172,7 +1184,7 @@ static int batch_insert_impl(const M& m, const jb_insert_args& a, cudaStream_t s
     BALLOC(tk, uint64_t, ntri);
     // smem-staged candidate rows when a trace fits in ~26 KB per warp; longer traces
     // prune from L1/L2 (staging them would cost more occupancy than it saves)
-    const int crows2 = staged_rows(m, cap, R);
+    const int crows2 = staged_rows(m, cap, R, JB_P2_KB);
     const int p2_smem = BW * 4 * vertex_warp_words(m, crows2);
     JB_CUDA(cudaFuncSetAttribute(phase2_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, p2_smem));
     phase2_kernel<M><<<(unsigned)((nb + BW - 1) / BW), BW * 32, p2_smem, st>>>(
