@@ -14,6 +14,10 @@ timeout 1200 ncu --set full --clock-control none --import-source on --nvtx --nvt
     -k regex:beam_search_kernel -c 1 -o gpurun_out/prof_search_${TAG} -f python bench.py "$@" --beam $L --estimator $EST --no-cpu \
     --steps 1 --warmup 1 > gpurun_out/ncu_${TAG}.log 2>&1
 tail -3 gpurun_out/ncu_${TAG}.log
+timeout 900 ncu --set full --clock-control none --import-source on --nvtx --nvtx-include "timed/" \
+    -k regex:rerank_kernel -c 1 -o gpurun_out/prof_rerank_${TAG} -f python bench.py "$@" --beam $L --estimator $EST --no-cpu \
+    --steps 1 --warmup 1 > gpurun_out/ncu_rerank_${TAG}.log 2>&1
+tail -2 gpurun_out/ncu_rerank_${TAG}.log
 ls -la gpurun_out
 # per-launch DRAM traffic of the profiled search kernel -> bench.py's roofline.traffic
 python - <<PY
