@@ -59,6 +59,33 @@ struct SearchLayout {
     int hbits;      // log2(number of 4-way buckets)
 };
 
+static int pow2_ceil(int v) { int p = 1; while (p < v) p <<= 1; return p; }
+__host__ __device__ constexpr int log2i(int v) { int l = 0; while ((1 << l) < v) ++l; return l; }
+
+// Per-warp smem layout. The fixed-size pieces come first and the beam (L keys)
+// last, so for a compile-time D and visited-table size every offset is a
+// constant (the specialised kernels then address smem as base + immediate).
+__host__ __device__ constexpr SearchLayout make_layout(int src, int D, int L, int hash_slots, int qb) {
+    SearchLayout s{};
+    int off = 0;
+    s.q_off = off; off += ((D * 4) + 15) & ~15;
+    s.hbits = log2i(hash_slots / 4 > 1 ? hash_slots / 4 : 1);   // 4-way buckets
+    s.hash_off = off; off += (4 << s.hbits) * 4;
+    s.newk_off = off; off += 32 * 4;
+    s.cid_off = off; off += 32 * 4;
+    s.chunk = ((D + 31) / 32) * 32 < 128 ? ((D + 31) / 32) * 32 : 128;
+    s.sstride = s.chunk + 4;
+    s.stage_off = off;
+    if (src == JB_SRC_EXACT) off += 32 * s.sstride * 4;
+    s.plane_off = off;
+    if (src == JB_SRC_RABITQ_FAST) off += qb * ((((D + 31) / 32) + 3) & ~3) * 4;
+    off = (off + 15) & ~15;
+    s.beam_off = off; off += ((L * 8) + 15) & ~15;
+    s.bytes = (off + 15) & ~15;
+    return s;
+}
+
+
 // Visited table: 4-way set-associative buckets of ids in smem, one 16 B load per
 // probe. A miss inserts into the first empty way, else evicts a pseudo-random way.
 // No atomics: two lanes racing for one way can only drop an insert. Every outcome
@@ -288,12 +315,12 @@ struct QueryCtx {
 // One neighbour per lane (nb = -1: none): visited check, then the distance of
 // every new neighbour, returned as the lane's candidate key (UMAX = none; EXACT
 // compacts the new ids to lanes 0..nnew-1). Adds the new count to `evals`.
-template <int SRC, int BITS, bool ALIGNED>
+template <int SRC, int BITS, bool ALIGNED, int KD = 0>
 __device__ __forceinline__ uint64_t eval_chunk(const jb_search_args& a, const SearchLayout& lay, const QueryCtx& c,
                                                uint32_t* tab, int nb, int& evals, int& lossy) {
     const unsigned FULL = 0xFFFFFFFFu;
     const int lane = lane_id();
-    const int D = a.dims;
+    const int D = KD > 0 ? KD : a.dims;
     const int RB = a.record_bytes;
     // RaBitQ: issue the candidate's record loads before the visited check
     uint4 rc0 = make_uint4(0, 0, 0, 0), rc1 = make_uint4(0, 0, 0, 0);
@@ -369,12 +396,20 @@ __device__ __forceinline__ uint64_t eval_chunk(const jb_search_args& a, const Se
     return have ? pack_key(d, (uint32_t)myid) : UMAX;
 }
 
-template <int SRC, int BITS, bool ALIGNED, int CH, int MINB>
+// KD > 0 and KHB > 0: compile-time dims and visited-table buckets (log2), so the
+// per-warp smem offsets are constants; the beam length (L) stays a runtime value.
+template <int SRC, int BITS, bool ALIGNED, int CH, int MINB, int KD = 0, int KHB = 0>
 __global__ void __launch_bounds__(WPB * 32, MINB)
-beam_search_kernel(const jb_search_args a, const SearchLayout lay, int* __restrict__ counter) {
+beam_search_kernel(const jb_search_args a, const SearchLayout lay_arg, int* __restrict__ counter) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
+    SearchLayout lay = lay_arg;
+    if (KD > 0 && KHB > 0) {
+        constexpr SearchLayout c = make_layout(SRC, KD > 0 ? KD : 1, 0, 4 << (KHB > 0 ? KHB : 1), FAST_QB);
+        lay = c;
+        lay.bytes = lay_arg.bytes;
+    }
     unsigned char* base = smem + (size_t)warp * lay.bytes;
     float* qv = reinterpret_cast<float*>(base + lay.q_off);
     uint64_t* beam = reinterpret_cast<uint64_t*>(base + lay.beam_off);
@@ -383,10 +418,10 @@ beam_search_kernel(const jb_search_args a, const SearchLayout lay, int* __restri
     int32_t* cid = reinterpret_cast<int32_t*>(base + lay.cid_off);
     float* stage = reinterpret_cast<float*>(base + lay.stage_off);
     uint32_t* planes = reinterpret_cast<uint32_t*>(base + lay.plane_off);
-    const int nwords = (((a.dims + 31) / 32) + 3) & ~3;  // plane stride (16 B aligned)
+    const int D = KD > 0 ? KD : a.dims;
+    const int nwords = (((D + 31) / 32) + 3) & ~3;  // plane stride (16 B aligned)
 
     const int L = a.beam_width;
-    const int D = a.dims;
     const int R = a.degree_cap;
     const int H = 4 << lay.hbits;
     const int RB = a.record_bytes;
@@ -482,7 +517,7 @@ beam_search_kernel(const jb_search_args a, const SearchLayout lay, int* __restri
 #pragma unroll
             for (int c = 0; c < CH; ++c) {
                 if (c * 32 >= R) break;
-                const uint64_t key = eval_chunk<SRC, BITS, ALIGNED>(a, lay, qc, tab, nbv[c], evals, lossy);
+                const uint64_t key = eval_chunk<SRC, BITS, ALIGNED, KD>(a, lay, qc, tab, nbv[c], evals, lossy);
                 const int p0 = merge_into_beam(beam, bcount, L, key, fmask);
                 s_min = min(s_min, p0);
                 p_ins = p0;
@@ -648,30 +683,17 @@ rerank_kernel(const float* __restrict__ data, int D, const float* __restrict__ q
     }
 }
 
-static int pow2_ceil(int v) { int p = 1; while (p < v) p <<= 1; return p; }
-static int log2i(int v) { int l = 0; while ((1 << l) < v) ++l; return l; }
-
-static SearchLayout make_layout(int src, int D, int L, int hash_slots, int qb) {
-    SearchLayout s{};
-    auto align16 = [](int v) { return (v + 15) & ~15; };
-    int off = 0;
-    s.q_off = off; off += align16(D * 4);
-    s.beam_off = off; off += align16(L * 8);
-    s.hbits = log2i(std::max(1, hash_slots / 4));   // 4-way buckets
-    s.hash_off = off; off += (4 << s.hbits) * 4;
-    s.newk_off = off; off += 32 * 4;
-    s.cid_off = off; off += 32 * 4;
-    s.chunk = std::min(128, ((D + 31) / 32) * 32);
-    s.sstride = s.chunk + 4;
-    s.stage_off = off;
-    if (src == JB_SRC_EXACT) off += 32 * s.sstride * 4;
-    s.plane_off = off;
-    if (src == JB_SRC_RABITQ_FAST) off += qb * ((((D + 31) / 32) + 3) & ~3) * 4;
-    s.bytes = align16(off);
-    return s;
-}
 
 using SearchKernel = void (*)(const jb_search_args, const SearchLayout, int*);
+
+// JB_SEARCH_SPEC=0 disables the compile-time-shape kernels (A/B and debugging)
+static bool specialize_off() {
+    static const bool off = [] {
+        const char* e = std::getenv("JB_SEARCH_SPEC");
+        return e && e[0] == '0';
+    }();
+    return off;
+}
 
 // Occupancy per (kernel, smem size) is cached: the attribute/occupancy queries
 // cost more than the launch itself for small batches.
@@ -724,6 +746,18 @@ static int launch_search(const jb_search_args& a, int hash_slots, cudaStream_t s
     constexpr int MINB = SRC == JB_SRC_RABITQ_FAST ? JB_FAST_MINB : 8;
     const int L = a.beam_width;
     const SearchLayout lay = make_layout(SRC, a.dims, L, hash_slots, FAST_QB);
+    if (a.degree_cap <= 32 && SRC == JB_SRC_RABITQ_FAST) {
+        // specialised shapes: D in {96, 128} with a 512- or 1024-slot visited table (popcount
+        // estimator only: measured -2% at L=128; the float estimators got slower, +4%)
+        const int hb = lay.hbits;
+#define JB_SPEC(KD_, KHB_)                                                                                   \
+    if (a.dims == KD_ && hb == KHB_)                                                                         \
+        return launch_search_kernel(beam_search_kernel<SRC, BITS, ALIGNED, 1, MINB, KD_, KHB_>, lay, a, MINB, st);
+        if (ALIGNED && !specialize_off()) {
+            JB_SPEC(128, 7) JB_SPEC(128, 8) JB_SPEC(96, 7) JB_SPEC(96, 8)
+        }
+#undef JB_SPEC
+    }
     if (a.degree_cap <= 32) return launch_search_kernel(beam_search_kernel<SRC, BITS, ALIGNED, 1, MINB>, lay, a, MINB, st);
     return launch_search_kernel(beam_search_kernel<SRC, BITS, ALIGNED, MAX_CHUNKS, 8>, lay, a, 8, st);
 }
