@@ -47,6 +47,9 @@ constexpr int WPB = 4;          // warps per block
 constexpr int RR_WARPS = JB_RR_WARPS;  // warps per block of the rerank kernel
 constexpr int RR_ROWS = JB_RR_ROWS;    // frontier rows staged per step (4 lanes each, RR_ROWS <= 8)
 constexpr int MAX_CHUNKS = 4;   // neighbour slots per hop: R <= 32 * MAX_CHUNKS
+#ifndef JB_EXACT_CHUNK
+#define JB_EXACT_CHUNK 128      // exact source: row elements staged per pass (multiple of 32)
+#endif
 #ifndef JB_COOP_MAX
 #define JB_COOP_MAX 2
 #endif
@@ -73,7 +76,7 @@ __host__ __device__ constexpr SearchLayout make_layout(int src, int D, int L, in
     s.hash_off = off; off += (4 << s.hbits) * 4;
     s.newk_off = off; off += 32 * 4;
     s.cid_off = off; off += 32 * 4;
-    s.chunk = ((D + 31) / 32) * 32 < 128 ? ((D + 31) / 32) * 32 : 128;
+    s.chunk = ((D + 31) / 32) * 32 < JB_EXACT_CHUNK ? ((D + 31) / 32) * 32 : JB_EXACT_CHUNK;
     s.sstride = s.chunk + 4;
     s.stage_off = off;
     if (src == JB_SRC_EXACT) off += 32 * s.sstride * 4;
