@@ -108,9 +108,21 @@ def recall_at_k(result_ids, gt, k: int) -> float:
 
 
 def run_queries(graph, source, queries, params: SearchParams, exact_data=None, workers: int = 1):
-    """bench.py:69-91. The device path batches all queries in one launch; `workers`
-    is accepted for signature compatibility."""
-    return search_knn_batch(graph, source, queries, params, exact_data)
+    """bench.py:69-91: top-k for a query batch, optionally split across worker
+    threads exactly as the reference splits it. Each thread's search_knn_batch
+    runs on its own native context (streams, pinned staging), so the calls are
+    re-entrant; one batch (workers=1) is the fastest use of the GPU."""
+    queries = np.atleast_2d(np.asarray(queries))
+    if workers <= 1 or queries.shape[0] < 2 * workers:
+        return search_knn_batch(graph, source, queries, params, exact_data)
+    from concurrent.futures import ThreadPoolExecutor
+
+    chunks = np.array_split(np.arange(queries.shape[0]), workers)
+    with ThreadPoolExecutor(max_workers=workers) as pool:
+        futures = [pool.submit(search_knn_batch, graph, source, queries[c], params, exact_data)
+                   for c in chunks if c.size]
+        parts = [f.result() for f in futures]
+    return np.concatenate([p_[0] for p_ in parts], axis=0), np.concatenate([p_[1] for p_ in parts], axis=0)
 
 
 def write_sweep_csv(path, points) -> None:

@@ -342,3 +342,21 @@ def test_u8_search_matches_oracle_128d(L):
     g = _graph_from_oracle(og)
     res = jb.run_beam_searches(g, jb.VectorDataset(data), q, L)
     _oracle_check(res, osearch.beam_search(og.adj, og.active, og.entry, osearch.ExactSource(data, q), len(q), L))
+
+
+def test_run_queries_threads_and_sweep_match_single_batch():
+    """run_queries(workers=N) splits the batch over threads like bench.py:69-91; the
+    concurrent native calls (per-thread contexts) return exactly the one-batch result."""
+    x = lowrank(4000, 64, 8, 0.05, 81)
+    q = lowrank(600, 64, 8, 0.05, 82)
+    ds = jb.VectorDataset(x)
+    g = jb.build(ds, jb.BuildParams(degree_cap=20, build_beam_width=40, alpha=1.2))
+    idx = jb.rabitq_fit(ds, bits=1, seed=7)
+    sp = jb.SearchParams(beam_width=40, k=10, rerank=True)
+    one = jb.run_queries(g, idx, q, sp, exact_data=ds, workers=1)
+    many = jb.run_queries(g, idx, q, sp, exact_data=ds, workers=6)
+    np.testing.assert_array_equal(one[0], many[0])
+    np.testing.assert_array_equal(one[1], many[1])
+    gt = jb.exact_knn(ds, jb.VectorDataset(q), 20)
+    pts = jb.sweep(g, ds, q, gt, 10, [16, 32], workers=3)
+    assert [p.beam_width for p in pts] == [16, 32] and pts[1].recall >= pts[0].recall > 0.5
