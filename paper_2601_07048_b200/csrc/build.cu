@@ -346,6 +346,16 @@ __host__ __device__ inline int owner_per_warp(const M& m, int R, int crows) {
     return ((OWNER_SC * 8 + vertex_warp_words(m, crows) * 4 + R * 4 * 3) + 15) & ~15;
 }
 
+#ifdef JB_OWNER_STATS
+__device__ unsigned long long g_owner_stats[16];
+extern "C" int jb_debug_owner_stats(unsigned long long* out) {
+    JB_CUDA(cudaMemcpyFromSymbol(out, g_owner_stats, sizeof(unsigned long long) * 16));
+    static const unsigned long long zero[16] = {};
+    JB_CUDA(cudaMemcpyToSymbol(g_owner_stats, zero, sizeof(zero)));
+    return JB_OK;
+}
+#endif
+
 template <class M>
 __global__ void __launch_bounds__(BW * 32)
 owner_merge_kernel(const M m, double alpha2, int R, int always_prune, const uint32_t* __restrict__ tgt,
@@ -420,6 +430,17 @@ owner_merge_kernel(const M m, double alpha2, int R, int always_prune, const uint
     m.load_pivot(pv, t);
     const int n = hd + nf;
     int k;
+#ifdef JB_OWNER_STATS
+    if (lane == 0) {
+        atomicAdd(&g_owner_stats[0], 1ull);                      // pruned targets
+        atomicAdd(&g_owner_stats[1], (unsigned long long)n);     // candidates
+        if (n > crows) {
+            atomicAdd(&g_owner_stats[2], 1ull);                  // unstaged targets
+            atomicAdd(&g_owner_stats[3], (unsigned long long)n); // their candidates
+        }
+        atomicAdd(&g_owner_stats[4 + min(n / 16, 11)], 1ull);    // histogram of n in 16s
+    }
+#endif
     if (n <= crows) {
         for (int j = lane; j < hd; j += 32) cand[j] = (uint64_t)(uint32_t)have[j];  // id only, for staging
         __syncwarp();
