@@ -1,0 +1,86 @@
+"""SPEC.md RaBitQ known answers and properties,
+on the device fit/estimator. Host-only parts run on CPU."""
+
+import numpy as np
+import pytest
+
+from conftest import gaussian, lowrank
+
+jb = pytest.importorskip("paper_2601_07048_b200")
+
+
+def _has_gpu():
+    try:
+        import torch
+        return torch.cuda.is_available()
+    except Exception:
+        return False
+
+
+@pytest.mark.parametrize("bits", [1, 2, 4, 8])
+def test_pack_unpack_round_trip_and_storage(bits):
+    rng = np.random.default_rng(bits)
+    for d in (1, 7, 33, 128, 960):
+        u = rng.integers(0, 2 ** bits, size=(5, d), dtype=np.uint8)
+        packed = jb.rabitq.pack_codes(u, bits)
+        assert packed.shape == (5, (d * bits + 7) // 8)
+        np.testing.assert_array_equal(jb.rabitq.unpack_codes(packed, bits, d), u)
+    # storage per vector: code bytes + (data_add, data_rescale) f32
+    idx = jb.RaBitQIndex(128, 4, 0, np.zeros(128, np.float32), np.zeros((3, 64), np.uint8), np.zeros((3, 2), np.float32))
+    assert idx.per_vector_bytes == 64 + 8
+    idx960 = jb.RaBitQIndex(960, 4, 0, np.zeros(960, np.float32), np.zeros((2, 480), np.uint8),
+                            np.zeros((2, 2), np.float32))
+    assert idx960.per_vector_bytes == 488
+
+
+def _estimates(idx, q):
+    """Host restatement of the estimator (rabitq.py:235-244) from the device bind."""
+    rot, qa, qs = idx.bind(q[None, :])
+    u = jb.rabitq.unpack_codes(idx.codes, idx.bits, idx.dims).astype(np.float32)
+    dd = u @ rot[0]
+    return qa[0] + idx.meta[:, 0] + idx.meta[:, 1] * (dd - qs[0])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("bits", [1, 4, 8])
+def test_zero_residual_row_has_zero_metadata(bits):
+    a = gaussian(10, 32, 3)
+    x = np.concatenate([a, -a, np.zeros((1, 32), np.float32)])  # mean 0: the last row is the centroid
+    idx = jb.rabitq_fit(jb.VectorDataset(x), bits=bits, seed=2)
+    np.testing.assert_array_equal(idx.centroid, np.zeros(32, np.float32))
+    np.testing.assert_array_equal(idx.meta[-1], [0.0, 0.0])
+    mid = 1 << (bits - 1)
+    np.testing.assert_array_equal(jb.rabitq.unpack_codes(idx.codes[-1:], bits, 32)[0], np.full(32, mid))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("bits,min_rho", [(8, 0.99), (4, 0.99), (1, 0.8)])
+def test_estimator_rank_correlation(bits, min_rho):
+    from scipy.stats import spearmanr
+
+    x = gaussian(4000, 128, 11)
+    q = gaussian(3, 128, 12)
+    idx = jb.rabitq_fit(jb.VectorDataset(x), bits=bits, seed=5)
+    for qq in q:
+        est = _estimates(idx, qq)
+        exact = ((x.astype(np.float64) - qq) ** 2).sum(axis=1)
+        rho = spearmanr(est, exact).correlation
+        assert rho >= min_rho, (bits, rho)
+        rel = (est - exact) / exact
+        assert abs(float(np.mean(rel))) < 0.05  # unbiased on average
+
+
+@pytest.mark.gpu
+def test_960d_m4_rerank_recall_within_3_points_of_exact():
+    """SPEC.md:625 at reduced N: 960-d, m = 4 (488 B per vector) + fp32 rerank."""
+    x = lowrank(5000, 960, 24, 0.05, 21)
+    q = lowrank(200, 960, 24, 0.05, 22)
+    ds = jb.VectorDataset(x)
+    g = jb.build(ds, jb.BuildParams(degree_cap=24, build_beam_width=48, alpha=1.2))
+    idx = jb.rabitq_fit(ds, bits=4, seed=3)
+    assert idx.per_vector_bytes == 488
+    gt = jb.exact_knn(ds, jb.VectorDataset(q), 10)
+    ex, _ = jb.search_knn_batch(g, ds, q, jb.SearchParams(beam_width=48, k=10))
+    rq, _ = jb.search_knn_batch(g, idx, q, jb.SearchParams(beam_width=48, k=10, rerank=True), exact_data=ds)
+    r_exact, r_quant = jb.recall_at_k(ex, gt, 10), jb.recall_at_k(rq, gt, 10)
+    assert r_quant >= r_exact - 0.03, (r_exact, r_quant)

@@ -360,3 +360,25 @@ def test_run_queries_threads_and_sweep_match_single_batch():
     gt = jb.exact_knn(ds, jb.VectorDataset(q), 20)
     pts = jb.sweep(g, ds, q, gt, 10, [16, 32], workers=3)
     assert [p.beam_width for p in pts] == [16, 32] and pts[1].recall >= pts[0].recall > 0.5
+
+
+def test_search_properties_spec():
+    """no double evaluation, deterministic visitation order, recall
+    non-decreasing in L."""
+    x = lowrank(5000, 48, 8, 0.05, 91)
+    q = lowrank(300, 48, 8, 0.05, 92)
+    ds = jb.VectorDataset(x)
+    g = jb.build(ds, jb.BuildParams(degree_cap=16, build_beam_width=32, alpha=1.2))
+    a = jb.run_beam_searches(g, ds, q, 64)
+    b = jb.run_beam_searches(g, ds, q, 64)
+    for ra, rb in zip(a, b):
+        np.testing.assert_array_equal(ra.visited_ids, rb.visited_ids)
+        np.testing.assert_array_equal(ra.frontier_ids, rb.frontier_ids)
+        assert np.unique(ra.visited_ids).size == ra.visited_ids.size  # every vertex expanded at most once
+        # every evaluated id is the start or a neighbour of an expanded vertex, each counted once
+        nb = g.adjacency[ra.visited_ids].ravel()
+        assert ra.stats.distance_evals == np.unique(np.append(nb[nb >= 0], g.entry_point)).size
+    gt = jb.exact_knn(ds, jb.VectorDataset(q), 10)
+    rec = [jb.recall_at_k(jb.search_knn_batch(g, ds, q, jb.SearchParams(beam_width=L, k=10))[0], gt, 10)
+           for L in (16, 32, 64, 128)]
+    assert all(r2 >= r1 - 1e-9 for r1, r2 in zip(rec, rec[1:])), rec
