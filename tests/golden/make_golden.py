@@ -125,6 +125,27 @@ def mips():
          degrees=g.degrees[:g.active_count].copy(), entry=np.int64(g.entry_point), knn_ids=ids, knn_dists=dists)
 
 
+def c1_graph():
+    """10. BASELINE config 1 at full size (100K x 128 Gaussian, R=32, L=64, alpha=1.2): the
+    reference build takes ~13 min here; only hashes are committed (c1_graph.json)."""
+    import hashlib
+    import json
+
+    x = ref.gen_synthetic(100_000, 128, seed=0).data
+    t = time.time()
+    g = ref.build(ref.VectorDataset(x), ref.BuildParams(degree_cap=32, build_beam_width=64, alpha=1.2))
+    n = g.active_count
+    out = {"what": "reference (beamann) build of BASELINE config 1: gen_synthetic(100000, 128, seed=0), "
+                   "BuildParams(degree_cap=32, build_beam_width=64, alpha=1.2); SHA-1 of the int32 adjacency "
+                   "[100000, 32] and degrees, and the entry point",
+           "made_by": f"tests/golden/make_golden.py c1_graph ({time.time() - t:.0f} s on the container CPU)",
+           "adjacency_sha1": hashlib.sha1(np.ascontiguousarray(g.adjacency[:n]).tobytes()).hexdigest(),
+           "degrees_sha1": hashlib.sha1(np.ascontiguousarray(g.degrees[:n]).tobytes()).hexdigest(),
+           "entry": int(g.entry_point)}
+    with open(os.path.join(HERE, "c1_graph.json"), "w") as fh:
+        json.dump(out, fh, indent=1)
+
+
 def main():
     # 1. exact search + build on a small Gaussian graph (D=32, R=16, L=32)
     data = ref.gen_synthetic(3000, 32, seed=0).data

@@ -206,3 +206,20 @@ def test_gpu_built_graph_invariants_and_reachability():
     og.deg[:] = g.degrees
     og.active, og.entry = g.active_count, g.entry_point
     assert vamana.reachable(og).all()
+
+
+def test_config1_100k_build_identical_to_reference():
+    """BASELINE config 1 at full size: the device build of 100K x 128 Gaussian rows
+    (R=32, L=64, alpha=1.2) is byte-identical to the reference's own 13-minute build."""
+    import hashlib
+    import json
+    import os
+
+    from conftest import GOLDEN
+
+    ref = json.load(open(os.path.join(GOLDEN, "c1_graph.json")))
+    g = jb.build(jb.VectorDataset(gaussian(100_000, 128, 0)),
+                 jb.BuildParams(degree_cap=32, build_beam_width=64, alpha=1.2))
+    assert g.entry_point == ref["entry"]
+    assert hashlib.sha1(np.ascontiguousarray(g.degrees[:100_000]).tobytes()).hexdigest() == ref["degrees_sha1"]
+    assert hashlib.sha1(np.ascontiguousarray(g.adjacency[:100_000]).tobytes()).hexdigest() == ref["adjacency_sha1"]
