@@ -382,3 +382,24 @@ def test_search_properties_spec():
     rec = [jb.recall_at_k(jb.search_knn_batch(g, ds, q, jb.SearchParams(beam_width=L, k=10))[0], gt, 10)
            for L in (16, 32, 64, 128)]
     assert all(r2 >= r1 - 1e-9 for r1, r2 in zip(rec, rec[1:])), rec
+
+
+def test_bench_scale_rabitq_fit_and_bind_identical_to_reference():
+    """The headline index's RaBitQ codes / metadata / centroid (1M x 128, m=1) and its
+    10K bound queries are bit-identical to beamann's (hashes of the reference run)."""
+    import hashlib
+    import json
+    import os
+
+    from conftest import GOLDEN
+
+    ref = json.load(open(os.path.join(GOLDEN, "bench_rabitq.json")))
+    h = lambda a: hashlib.sha1(np.ascontiguousarray(a).tobytes()).hexdigest()  # noqa: E731
+    x = jb.gen_lowrank(1_000_000, 128, seed=1, d_int=16, noise=0.05, basis_seed=0)
+    q = jb.gen_lowrank(10_000, 128, seed=1_000_003, d_int=16, noise=0.05, basis_seed=0)
+    idx = jb.rabitq_fit(jb.VectorDataset(x), bits=1, seed=1)
+    assert h(idx.centroid) == ref["centroid"]
+    assert h(idx.codes) == ref["codes"]
+    assert h(idx.meta) == ref["meta"]
+    rot, qa, qs = idx.bind(q)
+    assert (h(rot), h(qa), h(qs)) == (ref["rotated"], ref["qadd"], ref["sumq"])
