@@ -927,7 +927,7 @@ static int repair(const M& m, const jb_insert_args& a, int64_t n_active, int64_t
             slices = (int)std::min<int64_t>(slices, std::max<int64_t>(1, (nreach + DT - 1) / DT));
             part = bufs.get<uint64_t>((size_t)slices * nlost * fan, st, _ce); JB_CUDA(_ce);
             const size_t dsm = (size_t)(DT * (D + 1) + DT * 17 + DT * (DT + 1) + 1) * 4 + DT * FAN * 8 + 8 * 128 * 8;
-            JB_CUDA(cudaFuncSetAttribute(donor_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
+            JB_CUDA_RC(grow_smem(donor_scan_kernel, (int)dsm));
             donor_scan_kernel<<<dim3(sblocks, slices), 256, dsm, st>>>(a.data, a.data_norms, D, lost, nlost, reach,
                                                                       nreach, slices, fan, part);
         } else {
@@ -936,8 +936,7 @@ static int repair(const M& m, const jb_insert_args& a, int64_t n_active, int64_t
             slices = (int)std::min<int64_t>(slices, std::max<int64_t>(1, (nreach + 31) / 32));
             part = bufs.get<uint64_t>((size_t)slices * nlost * fan, st, _ce); JB_CUDA(_ce);
             const size_t gsm = (size_t)8 * m.pivot_words() * 4 + 8 * (FAN + 64) * 8;
-            JB_CUDA(cudaFuncSetAttribute(donor_scan_generic_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)gsm));
+            JB_CUDA_RC(grow_smem(donor_scan_generic_kernel<M>, (int)gsm));
             donor_scan_generic_kernel<M><<<dim3(sblocks, slices), 256, gsm, st>>>(m, lost, nlost, reach, nreach, slices,
                                                                                  fan, part);
         }
@@ -951,7 +950,7 @@ static int repair(const M& m, const jb_insert_args& a, int64_t n_active, int64_t
         BALLOC(tmp, unsigned char, tb);
         JB_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, okey, okey2, oval, oval2, nlost, 0, 64, st));
         const int asm_bytes = m.pivot_words() * 4;
-        JB_CUDA(cudaFuncSetAttribute(attach_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, asm_bytes));
+        JB_CUDA_RC(grow_smem(attach_kernel<M>, asm_bytes));
         rt.mark("order");
         attach_kernel<M><<<1, 32, asm_bytes, st>>>(m, a.adjacency, a.degrees, R, pinned, seen, lost, oval2, nlost,
                                                     donors, fan, fa, bridges, err, err + 1);
@@ -1077,7 +1076,7 @@ static int merge_phase(const M& m, const jb_insert_args& a, double alpha2, uint3
             smem_sm / (owner_per_warp(m, R, crows_lo) * BW) >= 3)
             crows = crows_lo;
         const int osm = owner_per_warp(m, R, crows) * BW;
-        JB_CUDA(cudaFuncSetAttribute(owner_merge_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, osm));
+        JB_CUDA_RC(grow_smem(owner_merge_kernel<M>, osm));
         owner_merge_kernel<M><<<(unsigned)((hseg + BW - 1) / BW), BW * 32, osm, st>>>(
             m, alpha2, R, a.always_prune, tt, tk, ntri, seg, nseg, pool, ptop, pool_cap, a.adjacency, a.degrees, err,
             crows);
@@ -1170,7 +1169,7 @@ static int batch_insert_impl(const M& m, const jb_insert_args& a, cudaStream_t s
             BALLOC(kid, int32_t, (size_t)nb * R);
             BALLOC(kd, uint32_t, (size_t)nb * R);
             const int smem = BW * m.pivot_words() * 4;
-            JB_CUDA(cudaFuncSetAttribute(seed_prune_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+            JB_CUDA_RC(grow_smem(seed_prune_kernel<M>, smem));
             seed_prune_kernel<M><<<(unsigned)((nb + BW - 1) / BW), BW * 32, smem, st>>>(
                 m, a.start, a.stop, alpha2, R, cand, kid, kd, a.adjacency, a.degrees);
             JB_LAUNCH_CHECK();
@@ -1207,7 +1206,7 @@ static int batch_insert_impl(const M& m, const jb_insert_args& a, cudaStream_t s
     // prune from L1/L2 (staging them would cost more occupancy than it saves)
     const int crows2 = staged_rows(m, cap, R, JB_P2_KB);
     const int p2_smem = BW * 4 * vertex_warp_words(m, crows2);
-    JB_CUDA(cudaFuncSetAttribute(phase2_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, p2_smem));
+    JB_CUDA_RC(grow_smem(phase2_kernel<M>, p2_smem));
     phase2_kernel<M><<<(unsigned)((nb + BW - 1) / BW), BW * 32, p2_smem, st>>>(
         m, a.start, nb, alpha2, R, hops, tids, tdst, cap, a.reverse_all_visited, cand, kid, kd, a.adjacency, a.degrees,
         tt, tk, W, crows2);
@@ -1262,7 +1261,7 @@ static int refine_batch_impl(const M& m, const jb_insert_args& a, int64_t active
     BALLOC(ncand, int32_t, nb);
     const int crows = staged_rows(m, cap + R, R);
     const int smem = BW * 4 * vertex_warp_words(m, crows);
-    JB_CUDA(cudaFuncSetAttribute(refine_prune_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    JB_CUDA_RC(grow_smem(refine_prune_kernel<M>, smem));
     refine_prune_kernel<M><<<(unsigned)((nb + BW - 1) / BW), BW * 32, smem, st>>>(
         m, a.start, nb, alpha2, R, hops, tids, tdst, cap, cand, kid, kd, a.adjacency, a.degrees, tt, tk, crows, ncand);
     JB_LAUNCH_CHECK();
@@ -1361,7 +1360,7 @@ int jb_robust_prune(const float* data, const float* data_norms, int32_t dims, co
     JB_CUDA(cand.alloc((size_t)std::max<int64_t>(total, 1) * 8, st));
     const F32Metric m{data, data_norms, dims};
     const int smem = BW * m.pivot_words() * 4;
-    JB_CUDA(cudaFuncSetAttribute(prune_batch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    JB_CUDA_RC(grow_smem(prune_batch_kernel, smem));
     prune_batch_kernel<<<(unsigned)((count + BW - 1) / BW), BW * 32, smem, st>>>(
         m, pivots, count, offsets, cand_ids, cand_dists, alpha * alpha, degree_cap, cand.as<uint64_t>(), out_ids,
         out_dists, out_counts);

@@ -224,7 +224,7 @@ extern "C" int jb_exact_knn_kind(const float* data, int64_t n, int32_t dims, con
     JB_CUDA(xn.alloc(sizeof(double) * n, st));
     JB_CUDA(qn.alloc(sizeof(double) * qb, st));
     JB_CUDA(sc.alloc(sizeof(double) * qb * n, st));
-    JB_CUDA(cudaFuncSetAttribute(knn_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SEL_SMEM));
+    JB_CUDA_RC(grow_smem(knn_select_kernel, SEL_SMEM));
     knn_norms_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(data, n, dims, xn.as<double>());
     JB_LAUNCH_CHECK();
     for (int64_t q0 = 0; q0 < nq; q0 += qb) {

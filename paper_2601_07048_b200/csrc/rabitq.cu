@@ -297,7 +297,7 @@ int jb_rabitq_encode(const float* x, int64_t n, int32_t dims, int32_t bits, cons
     JB_CHECK_ARG(TV >= 1, "rabitq encode: dims %d too large for shared memory", dims);
     const size_t smem = (size_t)TV * dims * 16 + (size_t)TV * 8;
     cudaStream_t st = as_stream(stream);
-    JB_CUDA(cudaFuncSetAttribute(encode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    JB_CUDA_RC(grow_smem(encode_kernel, (int)smem));
     encode_kernel<<<(unsigned)((n + TV - 1) / TV), ENC_WARPS * 32, smem, st>>>(x, n, dims, bits, centroid, rotation,
                                                                                TV, codes, meta);
     JB_LAUNCH_CHECK();
@@ -314,7 +314,7 @@ int jb_rabitq_bind(const float* queries, int64_t nq, int32_t dims, int32_t bits,
     JB_LAUNCH_CHECK();
     const int wpb = 8;
     const size_t smem = (size_t)wpb * ((dims + 3) & ~3) * 4;
-    JB_CUDA(cudaFuncSetAttribute(bind_finish_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    JB_CUDA_RC(grow_smem(bind_finish_kernel, (int)smem));
     bind_finish_kernel<<<(unsigned)((nq + wpb - 1) / wpb), wpb * 32, smem, st>>>(queries, nq, dims, bits, centroid,
                                                                                rotated, query_add, query_sumq);
     JB_LAUNCH_CHECK();

@@ -3,6 +3,8 @@
 #include <cstdarg>
 #include <cstring>
 #include "common.cuh"
+#include <map>
+#include <mutex>
 #include "runtime.cuh"
 
 namespace jb {
@@ -14,6 +16,20 @@ void set_error(const char* fmt, ...) {
     va_start(ap, fmt);
     vsnprintf(g_err, sizeof(g_err), fmt, ap);
     va_end(ap);
+}
+
+int grow_smem_attr(const void* func, int bytes) {
+    static std::mutex mu;
+    static std::map<std::pair<const void*, int>, int> set;
+    int dev = 0;
+    JB_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> g(mu);
+    int& cur = set[{func, dev}];
+    if (cur < bytes) {
+        JB_CUDA(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+        cur = bytes;
+    }
+    return JB_OK;
 }
 
 int sm_count_current() {
@@ -222,8 +238,7 @@ int jb_medoid(const float* x, int64_t n, int32_t dims, int64_t* out_host, void* 
     int threads = 128, blocks = (dims + threads - 1) / threads;
     column_sum_f64_kernel<<<blocks, threads, 0, st>>>(x, n, dims, sum);
     mean_finish_kernel<<<blocks, threads, 0, st>>>(sum, n, dims, center, nullptr);
-    JB_CUDA(cudaFuncSetAttribute(medoid_partial_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)(sizeof(double) * dims)));
+    JB_CUDA_RC(grow_smem(medoid_partial_kernel, (int)(sizeof(double) * dims)));
     medoid_partial_kernel<<<nb, 256, sizeof(double) * dims, st>>>(x, n, dims, center, part);
     medoid_final_kernel<<<1, 1, 0, st>>>(part, nb, dout);
     JB_LAUNCH_CHECK();

@@ -29,9 +29,24 @@ void set_error(const char* fmt, ...);
 
 #define JB_LAUNCH_CHECK() JB_CUDA(cudaGetLastError())
 
+// propagate a JB_* status from a helper
+#define JB_CUDA_RC(expr)            \
+    do {                            \
+        const int _rc = (expr);     \
+        if (_rc != JB_OK) return _rc; \
+    } while (0)
+
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
 int sm_count_current();
+
+// Raise a kernel's dynamic smem limit to at least `bytes` on the current device.
+// The limit is process-wide state of the kernel, so it only ever grows (under a
+// lock): concurrent host threads launching the same kernel with different smem
+// sizes cannot lower it under each other.
+int grow_smem_attr(const void* func, int bytes);
+template <class F>
+inline int grow_smem(F* func, size_t bytes) { return grow_smem_attr(reinterpret_cast<const void*>(func), (int)bytes); }
 
 // Once per device: keep freed stream-ordered memory in the default pool instead
 // of returning it to the driver at every synchronization (the default release

@@ -47,6 +47,9 @@ constexpr int WPB = 4;          // warps per block
 constexpr int RR_WARPS = JB_RR_WARPS;  // warps per block of the rerank kernel
 constexpr int RR_ROWS = JB_RR_ROWS;    // frontier rows staged per step (4 lanes each, RR_ROWS <= 8)
 constexpr int MAX_CHUNKS = 4;   // neighbour slots per hop: R <= 32 * MAX_CHUNKS
+#ifndef JB_EXACT_DIRECT
+#define JB_EXACT_DIRECT 1       // exact source, aligned rows: lane-owned global row reads, no smem staging
+#endif
 #ifndef JB_EXACT_CHUNK
 #define JB_EXACT_CHUNK 128      // exact source: row elements staged per pass (multiple of 32)
 #endif
@@ -79,7 +82,7 @@ __host__ __device__ constexpr SearchLayout make_layout(int src, int D, int L, in
     s.chunk = ((D + 31) / 32) * 32 < JB_EXACT_CHUNK ? ((D + 31) / 32) * 32 : JB_EXACT_CHUNK;
     s.sstride = s.chunk + 4;
     s.stage_off = off;
-    if (src == JB_SRC_EXACT) off += 32 * s.sstride * 4;
+    if (src == JB_SRC_EXACT && !(JB_EXACT_DIRECT && (D & 3) == 0)) off += 32 * s.sstride * 4;
     s.plane_off = off;
     if (src == JB_SRC_RABITQ_FAST) off += qb * ((((D + 31) / 32) + 3) & ~3) * 4;
     off = (off + 15) & ~15;
@@ -351,7 +354,15 @@ __device__ __forceinline__ uint64_t eval_chunk(const jb_search_args& a, const Se
     }
     float d = 0.0f;
     int myid = 0;
-    if (SRC == JB_SRC_EXACT) {
+    if (SRC == JB_SRC_EXACT && ALIGNED && JB_EXACT_DIRECT) {
+        // the lane that owns the neighbour reads its row straight from global (A1 order)
+        myid = nb;
+        if (isnew) {
+            Acc4 acc; acc.zero();
+            a1_range<true, false>(acc, a.data + (size_t)nb * D, c.qv, 0, D);
+            d = exact_from_dot(__ldg(a.data_norms + nb), acc.reduce(), c.qadd);
+        }
+    } else if (SRC == JB_SRC_EXACT) {
         if (isnew) c.cid[__popc(nm & lanemask_lt())] = nb;
         __syncwarp();
         myid = (lane < nnew) ? c.cid[lane] : 0;
@@ -395,7 +406,7 @@ __device__ __forceinline__ uint64_t eval_chunk(const jb_search_args& a, const Se
             }
         }
     }
-    const bool have = (SRC == JB_SRC_EXACT) ? (lane < nnew) : isnew;
+    const bool have = (SRC == JB_SRC_EXACT && !(ALIGNED && JB_EXACT_DIRECT)) ? (lane < nnew) : isnew;
     return have ? pack_key(d, (uint32_t)myid) : UMAX;
 }
 
@@ -704,27 +715,19 @@ static int launch_search_kernel(SearchKernel kern, const SearchLayout& lay, cons
                                 cudaStream_t st) {
     const int smem = lay.bytes * WPB;
     JB_CHECK_ARG(smem <= 227 * 1024, "beam search: per-block shared memory %d B exceeds 227 KB", smem);
-    // the smem attribute only ever grows per (kernel, device): lowering it would
-    // invalidate a cached larger configuration of the same kernel
+    // The smem attribute only grows, process-wide (grow_smem), so no host thread can
+    // lower it below another thread's cached launch configuration. Occupancy per
+    // (kernel, smem, device) is cached per thread (the query costs more than a launch).
     struct Entry { SearchKernel k; int smem, dev, per_sm; };
-    struct Attr { SearchKernel k; int dev, smem; };
     static thread_local Entry cache[16] = {};
-    static thread_local Attr attrs[64] = {};
-    static thread_local int next = 0, nattr = 0;
+    static thread_local int next = 0;
     int dev = 0;
     JB_CUDA(cudaGetDevice(&dev));
     int per_sm = 0;
     for (const Entry& e : cache)
         if (e.k == kern && e.smem == smem && e.dev == dev) per_sm = e.per_sm;
     if (per_sm == 0) {
-        Attr* at = nullptr;
-        for (int i = 0; i < nattr; ++i)
-            if (attrs[i].k == kern && attrs[i].dev == dev) at = &attrs[i];
-        if (at == nullptr || at->smem < smem) {
-            JB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-            if (at == nullptr && nattr < 64) at = &attrs[nattr++];
-            if (at != nullptr) *at = Attr{kern, dev, smem};
-        }
+        JB_CUDA_RC(grow_smem(kern, smem));
         JB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, WPB * 32, smem));
         JB_CHECK_ARG(per_sm >= 1, "beam search: kernel does not fit on an SM");
         cache[next] = Entry{kern, smem, dev, per_sm};
@@ -842,7 +845,7 @@ int jb_rerank_topk(const float* data, int32_t dims, const float* queries, int64_
     JB_CHECK_ARG(smem <= 227 * 1024, "rerank: shared memory %d B exceeds 227 KB", smem);
     cudaStream_t st = as_stream(stream);
     const unsigned grid = (unsigned)((nq + wpb - 1) / wpb);
-    JB_CUDA(cudaFuncSetAttribute(rerank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    JB_CUDA_RC(grow_smem(rerank_kernel, smem));
     rerank_kernel<<<grid, wpb * 32, smem, st>>>(data, dims, queries, nq, frontier_keys, beam_width, k, lpad, rstride,
                                                 per_warp, out_ids, out_dists);
     JB_LAUNCH_CHECK();
