@@ -9,6 +9,7 @@ handles) with PyTorch.
 
 from __future__ import annotations
 
+import concurrent.futures
 import glob
 import os
 import subprocess
@@ -34,7 +35,7 @@ def _newest_header() -> float:
 def build(verbose: bool = False, ptxas_info: bool = False) -> str:
     os.makedirs(OBJ, exist_ok=True)
     hdr = _newest_header()
-    objs = []
+    objs, jobs = [], []
     for cu in sorted(glob.glob(os.path.join(CSRC, "*.cu"))):
         o = os.path.join(OBJ, os.path.basename(cu)[:-3] + ".o")
         objs.append(o)
@@ -43,6 +44,10 @@ def build(verbose: bool = False, ptxas_info: bool = False) -> str:
         cmd = [NVCC, *ARCH, *FLAGS, "-c", cu, "-o", o]
         if ptxas_info:
             cmd += ["-Xptxas", "-v"]
+        jobs.append((cu, cmd))
+
+    def compile_one(job):
+        cu, cmd = job
         if verbose:
             print(" ".join(cmd), flush=True)
         r = subprocess.run(cmd, capture_output=True, text=True)
@@ -50,6 +55,10 @@ def build(verbose: bool = False, ptxas_info: bool = False) -> str:
             raise RuntimeError(f"nvcc failed for {cu}:\n{r.stdout}\n{r.stderr}")
         if (verbose or ptxas_info) and r.stderr:
             print(r.stderr, flush=True)
+
+    # translation units compile in parallel (build.cu and search.cu dominate)
+    with concurrent.futures.ThreadPoolExecutor(max_workers=max(1, min(len(jobs), os.cpu_count() or 1))) as pool:
+        list(pool.map(compile_one, jobs))
     newest = max(os.path.getmtime(o) for o in objs)
     if not os.path.exists(LIB) or os.path.getmtime(LIB) < newest:
         cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-cudart", "static"]
