@@ -531,7 +531,7 @@ def main():
     elif args.estimator == "popcount":
         ests = ["popcount"]
     else:
-        ests = ["reference", "popcount"] if args.bits == 1 else ["reference"]
+        ests = ["reference", "popcount"]
     cal = {e: _calibrate(S, args, world_eff, e) for e in ests}
     L, sweep_pts = cal["reference"] if "reference" in cal else cal[ests[0]]
 
@@ -583,7 +583,7 @@ def main():
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "peak_kind": peak_kind,
                      "traffic": _traffic(out["config"]["workload"] + f" L={L} {est}"),
-                     "kernel": f"beam_search_kernel<{'RABITQ_FAST' if est == 'popcount' else 'RABITQ'},1>",
+                     "kernel": f"beam_search_kernel<{'RABITQ_FAST' if est == 'popcount' else 'RABITQ'},{args.bits}>",
                      "alg_bytes_per_launch": int(ab["search_bytes"]),
                      "kernel_ms": round(search_s * 1e3, 4)},
         "gpu_launches": T["launches"],

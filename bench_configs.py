@@ -110,15 +110,16 @@ def c3(args):
     out = {"config": "c3", "n": n, "dims": 960, "d_int": dint, "bits": 4, "build_s": round(t_build, 2),
            "inserts_per_s": round(n / t_build, 1), "rabitq_fit_s": round(t_fit, 3),
            "bytes_per_vector": {"f32": 3840, "rabitq_record": int(jb._lib.lib().jb_rabitq_record_bytes(960, 4))},
-           "sweep": []}
-    for L in bench.SWEEP:
-        sp = jb.SearchParams(beam_width=L, k=10, rerank=True)
-        ms = _timed(lambda: jb.search_knn_batch_device(g, idx, q_dev, sp, exact_data=ds), reps=3, warm=1)
-        ids, _ = jb.search_knn_batch_device(g, idx, q_dev, sp, exact_data=ds)
-        r = jb.recall_at_k(ids.cpu().numpy(), gt, 10)
-        out["sweep"].append({"L": L, "recall": round(r, 4), "qps_device": round(10_000 / (ms / 1e3), 1)})
-        if r >= 0.95:
-            break
+           "sweep": [], "sweep_popcount": []}
+    for est, key in (("reference", "sweep"), ("popcount", "sweep_popcount")):
+        for L in bench.SWEEP:
+            sp = jb.SearchParams(beam_width=L, k=10, rerank=True, estimator=est)
+            ms = _timed(lambda: jb.search_knn_batch_device(g, idx, q_dev, sp, exact_data=ds), reps=3, warm=1)
+            ids, _ = jb.search_knn_batch_device(g, idx, q_dev, sp, exact_data=ds)
+            r = jb.recall_at_k(ids.cpu().numpy(), gt, 10)
+            out[key].append({"L": L, "recall": round(r, 4), "qps_device": round(10_000 / (ms / 1e3), 1)})
+            if r >= 0.95:
+                break
     return out
 
 

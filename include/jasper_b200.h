@@ -75,9 +75,11 @@ int jb_u8_to_f32(const uint8_t* x, int64_t count, float* out, void* stream);
 /* Distance source of a search. */
 #define JB_SRC_EXACT 0     /* ExactDistances over raw f32 rows (search.py:82-130) */
 #define JB_SRC_RABITQ 1    /* RaBitQ estimator (rabitq.py:225-244), bit-exact      */
-#define JB_SRC_RABITQ_FAST 2 /* RaBitQ, 1-bit codes: query quantized to 6-bit planes,
-                              * <u,q> by AND + popcount (north-star 2). Numerics differ
-                              * from the reference estimator; validated by recall.  */
+#define JB_SRC_RABITQ_FAST 2 /* RaBitQ: query quantized to 6-bit planes, <u,q> by
+                              * AND + popcount over the code bit-planes (m = 1, 2, 4, 8;
+                              * records from jb_rabitq_pack_planes) (north-star 2).
+                              * Numerics differ from the reference estimator;
+                              * validated by recall.                              */
 #define JB_SRC_EXACT_U8 3  /* ExactDistances over u8 rows: integer distances
                               * ||x||^2 - 2<x,q> + ||q||^2 (search.py:92-99,
                               * 126-130), key word = the u32 distance            */
@@ -170,6 +172,14 @@ int jb_search_knn_device(const jb_knn_plan* plan, const float* queries, int64_t 
 /* Packed device record of one vector: code bytes, zero padding to 16, then
  * (data_add, data_rescale) f32, total rounded up to 16 bytes (32 B at D=128, m=1). */
 int32_t jb_rabitq_record_bytes(int32_t dims, int32_t bits);
+
+/* Bit-plane records for the popcount estimator (JB_SRC_RABITQ_FAST, any m):
+ * per vector m planes of ceil(D/32) words (rounded up to 4), plane b' bit e =
+ * bit b' of the code of dimension e, then (data_add, data_rescale). For m = 1
+ * the layout equals jb_rabitq_pack_records'. */
+int32_t jb_rabitq_plane_record_bytes(int32_t dims, int32_t bits);
+int jb_rabitq_pack_planes(const uint8_t* codes, const float* meta, int64_t n, int32_t dims, int32_t bits,
+                          uint8_t* records, void* stream);
 
 /* Build records from reference-layout codes [n, ceil(D*m/8)] and meta [n, 2].
  * (RaBitQIndex layout, rabitq.py:113-168). */

@@ -73,6 +73,8 @@ _SIGS = {
     "jb_search_knn_host": (C.c_int, [C.POINTER(KnnPlan), p, i64, p, p, p]),
     "jb_search_knn_device": (C.c_int, [C.POINTER(KnnPlan), p, i64, p, p, p]),
     "jb_rabitq_record_bytes": (i32, [i32, i32]),
+    "jb_rabitq_plane_record_bytes": (i32, [i32, i32]),
+    "jb_rabitq_pack_planes": (C.c_int, [p, p, i64, i32, i32, p, p]),
     "jb_rabitq_pack_records": (C.c_int, [p, p, i64, i32, i32, p, p]),
     "jb_rabitq_encode": (C.c_int, [p, i64, i32, i32, p, p, p, p, p]),
     "jb_column_mean_f32": (C.c_int, [p, i64, i32, p, p]),

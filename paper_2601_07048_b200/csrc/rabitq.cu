@@ -21,6 +21,40 @@ __host__ __device__ inline int code_bytes_of(int D, int bits) { return (D * bits
 __host__ __device__ inline int meta_off_of(int D, int bits) { return ((code_bytes_of(D, bits) + 15) / 16) * 16; }
 __host__ __device__ inline int record_bytes_of(int D, int bits) { return ((meta_off_of(D, bits) + 8 + 15) / 16) * 16; }
 
+__host__ __device__ inline int plane_words_of(int D) { return (((D + 31) / 32) + 3) & ~3; }
+__host__ __device__ inline int plane_record_bytes_of(int D, int bits) {
+    return ((bits * plane_words_of(D) * 4 + 8 + 15) / 16) * 16;
+}
+
+// Bit-plane records for the popcount estimator: plane b' word w bit i = bit b' of the
+// code of dimension 32w + i; (data_add, data_rescale) after the planes. One thread per
+// (vector, word).
+__global__ void pack_planes_kernel(const uint8_t* __restrict__ codes, const float* __restrict__ meta, int64_t n, int D,
+                                   int bits, int cb, int pw, int rb, uint8_t* __restrict__ rec) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n * pw) return;
+    const int64_t v = t / pw;
+    const int w = (int)(t % pw);
+    const uint8_t* c = codes + v * cb;
+    uint32_t* out = reinterpret_cast<uint32_t*>(rec + v * rb);
+    const uint32_t mask = (1u << bits) - 1u;
+    for (int bp = 0; bp < bits; ++bp) {
+        uint32_t word = 0;
+        for (int i = 0; i < 32; ++i) {
+            const int e = 32 * w + i;
+            if (e >= D) break;
+            const int off = e * bits;
+            const uint32_t u = (c[off >> 3] >> (off & 7)) & mask;  // codes never straddle a byte
+            word |= ((u >> bp) & 1u) << i;
+        }
+        out[bp * pw + w] = word;
+    }
+    if (w == 0) {
+        *reinterpret_cast<float2*>(rec + v * rb + bits * pw * 4) = make_float2(meta[2 * v], meta[2 * v + 1]);
+        for (int i = bits * pw * 4 + 8; i < rb; ++i) rec[v * rb + i] = 0;
+    }
+}
+
 __global__ void pack_records_kernel(const uint8_t* __restrict__ codes, const float* __restrict__ meta, int64_t n,
                                     int cb, int moff, int rb, uint8_t* __restrict__ rec) {
     int64_t v = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
@@ -274,6 +308,20 @@ using namespace jb;
 extern "C" {
 
 int32_t jb_rabitq_record_bytes(int32_t dims, int32_t bits) { return record_bytes_of(dims, bits); }
+int32_t jb_rabitq_plane_record_bytes(int32_t dims, int32_t bits) { return plane_record_bytes_of(dims, bits); }
+
+int jb_rabitq_pack_planes(const uint8_t* codes, const float* meta, int64_t n, int32_t dims, int32_t bits,
+                          uint8_t* records, void* stream) {
+    JB_CHECK_ARG(bits == 1 || bits == 2 || bits == 4 || bits == 8, "bits must be one of (1, 2, 4, 8)");
+    JB_CHECK_ARG(dims >= 1, "dims must be >= 1");
+    if (n == 0) return JB_OK;
+    const int pw = plane_words_of(dims);
+    const int64_t threads = n * pw;
+    pack_planes_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, as_stream(stream)>>>(
+        codes, meta, n, dims, bits, code_bytes_of(dims, bits), pw, plane_record_bytes_of(dims, bits), records);
+    JB_LAUNCH_CHECK();
+    return JB_OK;
+}
 
 int jb_rabitq_pack_records(const uint8_t* codes, const float* meta, int64_t n, int32_t dims, int32_t bits,
                            uint8_t* records, void* stream) {

@@ -130,7 +130,11 @@ constexpr int FAST_QB = JB_FAST_QB;   // query bit-planes of the popcount estima
 
 // planes: FAST_QB planes of `pw` words each (pw = nwords rounded up to 4, zero padded)
 // PW > 0: plane stride known at compile time (PW = 4 covers D <= 128 in one piece).
-template <int QB, int PW = 0>
+// m-bit codes (MB > 1) are read as MB code bit-planes of `pw` words (plane records,
+// jb_rabitq_pack_planes): u = sum_b' 2^b' c_b', so
+//   <u, q> ~= lo * sum_b' 2^b' popc(c_b') + delta * sum_b' sum_b 2^(b'+b) popc(c_b' & plane_b).
+// For MB = 1 the plane record is the packed record itself.
+template <int QB, int PW = 0, int MB = 1>
 __device__ __forceinline__ float rabitq_dd_fast(const uint8_t* __restrict__ rec, uint4 first,
                                                const uint32_t* __restrict__ planes, int pw_rt, float lo, float delta) {
     const int pw = PW > 0 ? PW : pw_rt;
@@ -138,28 +142,36 @@ __device__ __forceinline__ float rabitq_dd_fast(const uint8_t* __restrict__ rec,
     int acc[QB];
 #pragma unroll
     for (int b = 0; b < QB; ++b) acc[b] = 0;
-#pragma unroll
-    for (int w0 = 0; w0 < pw; w0 += 4) {
-        const uint4 c = w0 == 0 ? first : __ldg(reinterpret_cast<const uint4*>(rec + 4 * w0));
-        pc += __popc(c.x) + __popc(c.y) + __popc(c.z) + __popc(c.w);
-#pragma unroll
-        for (int b = 0; b < QB; ++b) {
-            const uint4 p = *reinterpret_cast<const uint4*>(planes + b * pw + w0);
-            acc[b] += __popc(c.x & p.x) + __popc(c.y & p.y) + __popc(c.z & p.z) + __popc(c.w & p.w);
-        }
-    }
     int s = 0;
 #pragma unroll
-    for (int b = 0; b < QB; ++b) s += acc[b] << b;
+    for (int w0 = 0; w0 < pw; w0 += 4) {
+#pragma unroll
+        for (int bp = 0; bp < MB; ++bp) {
+            const uint4 c = (w0 == 0 && bp == 0) ? first
+                                                 : __ldg(reinterpret_cast<const uint4*>(rec + 4 * (bp * pw + w0)));
+            pc += (__popc(c.x) + __popc(c.y) + __popc(c.z) + __popc(c.w)) << bp;
+#pragma unroll
+            for (int b = 0; b < QB; ++b) {
+                const uint4 p = *reinterpret_cast<const uint4*>(planes + b * pw + w0);
+                const int t = __popc(c.x & p.x) + __popc(c.y & p.y) + __popc(c.z & p.z) + __popc(c.w & p.w);
+                if (MB == 1) acc[b] += t;
+                else s += t << (b + bp);
+            }
+        }
+    }
+    if (MB == 1) {
+#pragma unroll
+        for (int b = 0; b < QB; ++b) s += acc[b] << b;
+    }
     return fmaf(delta, (float)s, lo * (float)pc);
 }
 
-template <int QB>
+template <int QB, int MB = 1>
 __device__ __forceinline__ float rabitq_estimate_fast(const uint8_t* __restrict__ rec, const uint32_t* __restrict__ planes,
                                                       int nwords, int meta_off, float lo, float delta, float qadd,
                                                       float qsumq) {
     const uint4 first = __ldg(reinterpret_cast<const uint4*>(rec));
-    const float dd = rabitq_dd_fast<QB>(rec, first, planes, nwords, lo, delta);
+    const float dd = rabitq_dd_fast<QB, 0, MB>(rec, first, planes, nwords, lo, delta);
     const float2 m = __ldg(reinterpret_cast<const float2*>(rec + meta_off));
     const float est = (qadd + m.x) + m.y * (dd - qsumq);
     return est > 0.0f ? est : 0.0f;
@@ -398,8 +410,9 @@ __device__ __forceinline__ uint64_t eval_chunk(const jb_search_args& a, const Se
             const float2 m = (RB == 32) ? make_float2(__uint_as_float(rc1.x), __uint_as_float(rc1.y))
                                         : __ldg(reinterpret_cast<const float2*>(rec + c.meta_off));
             if (SRC == JB_SRC_RABITQ_FAST) {
-                const float dd = c.nwords == 4 ? rabitq_dd_fast<FAST_QB, 4>(rec, rc0, c.planes, 4, c.qlo, c.qdelta)
-                                               : rabitq_dd_fast<FAST_QB>(rec, rc0, c.planes, c.nwords, c.qlo, c.qdelta);
+                const float dd = (BITS == 1 && c.nwords == 4)
+                                     ? rabitq_dd_fast<FAST_QB, 4, 1>(rec, rc0, c.planes, 4, c.qlo, c.qdelta)
+                                     : rabitq_dd_fast<FAST_QB, 0, BITS>(rec, rc0, c.planes, c.nwords, c.qlo, c.qdelta);
                 const float est = (c.qadd + m.x) + m.y * (dd - c.qsumq);
                 d = est > 0.0f ? est : 0.0f;
             } else {
@@ -440,7 +453,8 @@ beam_search_kernel(const jb_search_args a, const SearchLayout lay_arg, int* __re
     const int R = a.degree_cap;
     const int H = 4 << lay.hbits;
     const int RB = a.record_bytes;
-    const int meta_off = ((((D * BITS) + 7) / 8 + 15) / 16) * 16;  // code zero-padded to 16 B
+    // packed record: code zero-padded to 16 B; popcount plane record: BITS planes of nwords words
+    const int meta_off = SRC == JB_SRC_RABITQ_FAST ? BITS * nwords * 4 : ((((D * BITS) + 7) / 8 + 15) / 16) * 16;
     const unsigned FULL = 0xFFFFFFFFu;
 
     for (;;) {
@@ -478,7 +492,7 @@ beam_search_kernel(const jb_search_args a, const SearchLayout lay_arg, int* __re
                 const float dot = a1_dot<false>(a.data + (size_t)start * D, qv, D);
                 d0 = exact_from_dot(a.data_norms[start], dot, qadd);
             } else if (SRC == JB_SRC_RABITQ_FAST) {
-                d0 = rabitq_estimate_fast<FAST_QB>(a.records + (size_t)start * RB, planes, nwords, meta_off, qlo, qdelta, qadd,
+                d0 = rabitq_estimate_fast<FAST_QB, BITS>(a.records + (size_t)start * RB, planes, nwords, meta_off, qlo, qdelta, qadd,
                                           qsumq);
             } else {
                 d0 = rabitq_estimate<BITS>(a.records + (size_t)start * RB, qv, D, meta_off, qadd, qsumq);
@@ -770,7 +784,7 @@ static int launch_search(const jb_search_args& a, int hash_slots, cudaStream_t s
     constexpr int MINB = SRC == JB_SRC_RABITQ_FAST ? JB_FAST_MINB : 8;
     const int L = a.beam_width;
     const SearchLayout lay = make_layout(SRC, a.dims, L, hash_slots, FAST_QB);
-    if (a.degree_cap <= 32 && SRC == JB_SRC_RABITQ_FAST) {
+    if (a.degree_cap <= 32 && SRC == JB_SRC_RABITQ_FAST && BITS == 1) {
         // specialised shapes: D in {96, 128} with a 512- or 1024-slot visited table (popcount
         // estimator only: measured -2% at L=128; the float estimators got slower, +4%)
         const int hb = lay.hbits;
@@ -837,11 +851,18 @@ int jb_beam_search(const jb_search_args* args, void* stream) {
     }
     JB_CHECK_ARG(a.source == JB_SRC_RABITQ || a.source == JB_SRC_RABITQ_FAST, "unknown distance source %d", a.source);
     JB_CHECK_ARG(a.records && a.queries && a.query_add && a.query_sumq, "rabitq search: missing arrays");
-    JB_CHECK_ARG(a.record_bytes == jb_rabitq_record_bytes(a.dims, a.bits), "rabitq search: record_bytes mismatch");
-    if (a.source == JB_SRC_RABITQ_FAST) {
-        JB_CHECK_ARG(a.bits == 1, "popcount fast mode supports 1-bit codes");
-        return launch_search<JB_SRC_RABITQ_FAST, 1, true>(a, hs, st);
+    if (a.source == JB_SRC_RABITQ_FAST) {  // bit-plane records (jb_rabitq_pack_planes; = packed for m = 1)
+        JB_CHECK_ARG(a.record_bytes == jb_rabitq_plane_record_bytes(a.dims, a.bits),
+                     "popcount search: record_bytes mismatch (plane records expected)");
+        switch (a.bits) {
+            case 1: return launch_search<JB_SRC_RABITQ_FAST, 1, true>(a, hs, st);
+            case 2: return launch_search<JB_SRC_RABITQ_FAST, 2, true>(a, hs, st);
+            case 4: return launch_search<JB_SRC_RABITQ_FAST, 4, true>(a, hs, st);
+            case 8: return launch_search<JB_SRC_RABITQ_FAST, 8, true>(a, hs, st);
+            default: JB_CHECK_ARG(false, "bits must be one of (1, 2, 4, 8)");
+        }
     }
+    JB_CHECK_ARG(a.record_bytes == jb_rabitq_record_bytes(a.dims, a.bits), "rabitq search: record_bytes mismatch");
     switch (a.bits) {
         case 1: return launch_search<JB_SRC_RABITQ, 1, true>(a, hs, st);
         case 2: return launch_search<JB_SRC_RABITQ, 2, true>(a, hs, st);

@@ -102,12 +102,11 @@ class _Bound:
                 raise ValueError(f"query dims {D} != index dims {idx.dims}")
             dev = idx.device()
             self.kind = _lib.SRC_RABITQ
-            if estimator == "popcount":
-                if idx.bits != 1:
-                    raise ValueError("the popcount estimator needs 1-bit codes")
-                self.kind = _lib.SRC_RABITQ_FAST
             self.dims = idx.dims
             self.records, self.record_bytes, self.bits = dev.records, dev.record_bytes, idx.bits
+            if estimator == "popcount":
+                self.kind = _lib.SRC_RABITQ_FAST
+                self.records, self.record_bytes = idx.device_planes()
             self.rows = None
             self.rotated = torch.empty((nq, D), dtype=torch.float32, device=q_dev.device)
             self.qadd = torch.empty(nq, dtype=torch.float32, device=q_dev.device)
@@ -424,11 +423,11 @@ def _knn_plan(graph: GraphIndex, source, D: int, params: SearchParams, exact_dat
             raise ValueError(f"query dims {D} != index dims {idx.dims}")
         dev = idx.device()
         a.source = _lib.SRC_RABITQ
-        if params.estimator == "popcount":
-            if idx.bits != 1:
-                raise ValueError("the popcount estimator needs 1-bit codes")
-            a.source = _lib.SRC_RABITQ_FAST
         a.records, a.record_bytes, a.bits = _lib.ptr(dev.records), dev.record_bytes, idx.bits
+        if params.estimator == "popcount":
+            a.source = _lib.SRC_RABITQ_FAST
+            pl, pb = idx.device_planes()
+            a.records, a.record_bytes = _lib.ptr(pl), pb
         plan.centroid, plan.rotation = _lib.ptr(dev.centroid), _lib.ptr(dev.rotation)
         if params.rerank:
             rows = as_dataset(exact_data).device()

@@ -273,10 +273,34 @@ def test_popcount_estimator_recall_tracks_reference_estimator():
             assert np.all(np.diff(ds_, axis=1) >= 0)  # reranked: ascending exact distances
             r[est] = jb.recall_at_k(ids, gt, 10)
         assert r["popcount"] >= r["reference"] - 0.02, r
-    with pytest.raises(ValueError, match="1-bit"):
-        idx4 = jb.rabitq_fit(ds, bits=4, seed=1)
-        jb.search_knn_batch(g, idx4, q, jb.SearchParams(beam_width=16, k=10, rerank=True, estimator="popcount"),
-                            exact_data=ds)
+    # multi-bit codes: the estimator runs over the code bit-planes
+    for bits in (2, 4, 8):
+        idxm = jb.rabitq_fit(ds, bits=bits, seed=1)
+        r = {}
+        for est in ("reference", "popcount"):
+            ids, _ = jb.search_knn_batch(g, idxm, q, jb.SearchParams(beam_width=48, k=10, rerank=True, estimator=est),
+                                         exact_data=ds)
+            r[est] = jb.recall_at_k(ids, gt, 10)
+        assert r["popcount"] >= r["reference"] - 0.02, (bits, r)
+
+
+@pytest.mark.parametrize("bits,D", [(2, 100), (4, 960), (8, 20), (1, 64)])
+def test_plane_records_match_host_layout(bits, D):
+    """jb_rabitq_pack_planes: plane b' bit e = bit b' of the code of dimension e, then meta."""
+    x = gaussian(300, D, 8)
+    idx = jb.rabitq_fit(jb.VectorDataset(x), bits=bits, seed=4)
+    rec, rb = idx.device_planes()
+    rec = rec.cpu().numpy()
+    pw = ((D + 31) // 32 + 3) & ~3
+    u = jb.rabitq.unpack_codes(idx.codes, bits, D).astype(np.uint64)
+    for v in (0, 7, 299):
+        words = rec[v, : bits * pw * 4].view(np.uint32).reshape(bits, pw)
+        for bp in range(bits):
+            want = np.zeros(pw, np.uint64)
+            for e in range(D):
+                want[e // 32] |= ((u[v, e] >> np.uint64(bp)) & np.uint64(1)) << np.uint64(e % 32)
+            np.testing.assert_array_equal(words[bp], want.astype(np.uint32))
+        np.testing.assert_array_equal(rec[v, bits * pw * 4: bits * pw * 4 + 8].view(np.float32), idx.meta[v])
 
 
 @pytest.mark.parametrize("chunk", [0, 97, 1000])
