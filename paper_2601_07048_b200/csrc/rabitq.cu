@@ -231,22 +231,29 @@ __device__ float pairwise_sum_f32(const float* a, int n) {
     return __fadd_rn(pairwise_sum_f32(a, n2), pairwise_sum_f32(a + n2, n - n2));
 }
 
-// rotated = f32(f64(q - c) @ rot^T) as a tiled f64 GEMM: block = 32 queries x 32
-// outputs, 256 threads with 2x2 outputs each (many small blocks: a 5K-query
-// lane still puts ~40 warps on every SM), 16-wide k-steps through k-major smem
-// tiles. Every output is one sequential FMA chain over d = 0..D-1 (the order the
-// tests pin against the reference's dgemm results).
-constexpr int RT = 32, RK = 16;
+// rotated = f32(f64(q - c) @ rot^T) as a tiled f64 GEMM: 256 threads with TM x TM
+// outputs each on a (16 TM) x (16 TM) tile, 16-wide k-steps through k-major smem
+// tiles. TM = 2 for small D (many small blocks: a 5K-query lane still puts ~40
+// warps on every SM), TM = 4 for large D (twice the FMAs per smem read). Every
+// output is one sequential FMA chain over d = 0..D-1 (the order the tests pin
+// against the reference's dgemm results).
+constexpr int RK = 16;
 
+template <int TM>
 __global__ void __launch_bounds__(256)
 rotate_gemm_kernel(const float* __restrict__ queries, int64_t nq, int D, const float* __restrict__ centroid,
                    const double* __restrict__ rot, float* __restrict__ rotated) {
+    constexpr int RT = 16 * TM;
     __shared__ __align__(16) double As[RK][RT + 2];
     __shared__ __align__(16) double Bs[RK][RT + 2];
     const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
     const int64_t q0 = (int64_t)blockIdx.x * RT;
     const int o0 = blockIdx.y * RT;
-    double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+    double acc[TM][TM];
+#pragma unroll
+    for (int a = 0; a < TM; ++a)
+#pragma unroll
+        for (int b = 0; b < TM; ++b) acc[a][b] = 0.0;
     for (int k0 = 0; k0 < D; k0 += RK) {
         for (int i = tid; i < RT * RK; i += 256) {
             const int r = i / RK, e = i % RK, d = k0 + e;
@@ -261,22 +268,28 @@ rotate_gemm_kernel(const float* __restrict__ queries, int64_t nq, int D, const f
         __syncthreads();
 #pragma unroll
         for (int e = 0; e < RK; ++e) {
-            const double2 a2 = *reinterpret_cast<const double2*>(&As[e][ty * 2]);
-            const double2 b2 = *reinterpret_cast<const double2*>(&Bs[e][tx * 2]);
-            acc[0][0] = fma(a2.x, b2.x, acc[0][0]);
-            acc[0][1] = fma(a2.x, b2.y, acc[0][1]);
-            acc[1][0] = fma(a2.y, b2.x, acc[1][0]);
-            acc[1][1] = fma(a2.y, b2.y, acc[1][1]);
+            double av[TM], bv[TM];
+#pragma unroll
+            for (int h = 0; h < TM; h += 2) {
+                const double2 a2 = *reinterpret_cast<const double2*>(&As[e][ty * TM + h]);
+                const double2 b2 = *reinterpret_cast<const double2*>(&Bs[e][tx * TM + h]);
+                av[h] = a2.x; av[h + 1] = a2.y;
+                bv[h] = b2.x; bv[h + 1] = b2.y;
+            }
+#pragma unroll
+            for (int a = 0; a < TM; ++a)
+#pragma unroll
+                for (int b = 0; b < TM; ++b) acc[a][b] = fma(av[a], bv[b], acc[a][b]);
         }
         __syncthreads();
     }
 #pragma unroll
-    for (int a = 0; a < 2; ++a) {
-        const int64_t q = q0 + ty * 2 + a;
+    for (int a = 0; a < TM; ++a) {
+        const int64_t q = q0 + ty * TM + a;
         if (q >= nq) continue;
 #pragma unroll
-        for (int b = 0; b < 2; ++b) {
-            const int o = o0 + tx * 2 + b;
+        for (int b = 0; b < TM; ++b) {
+            const int o = o0 + tx * TM + b;
             if (o < D) rotated[q * D + o] = __double2float_rn(acc[a][b]);
         }
     }
@@ -357,8 +370,13 @@ int jb_rabitq_bind(const float* queries, int64_t nq, int32_t dims, int32_t bits,
     JB_CHECK_ARG(bits == 1 || bits == 2 || bits == 4 || bits == 8, "bits must be one of (1, 2, 4, 8)");
     if (nq == 0) return JB_OK;
     cudaStream_t st = as_stream(stream);
-    dim3 grid((unsigned)((nq + RT - 1) / RT), (unsigned)((dims + RT - 1) / RT));
-    rotate_gemm_kernel<<<grid, 256, 0, st>>>(queries, nq, dims, centroid, rotation, rotated);
+    if (dims >= 256) {
+        dim3 grid((unsigned)((nq + 63) / 64), (unsigned)((dims + 63) / 64));
+        rotate_gemm_kernel<4><<<grid, 256, 0, st>>>(queries, nq, dims, centroid, rotation, rotated);
+    } else {
+        dim3 grid((unsigned)((nq + 31) / 32), (unsigned)((dims + 31) / 32));
+        rotate_gemm_kernel<2><<<grid, 256, 0, st>>>(queries, nq, dims, centroid, rotation, rotated);
+    }
     JB_LAUNCH_CHECK();
     const int wpb = 8;
     const size_t smem = (size_t)wpb * ((dims + 3) & ~3) * 4;
