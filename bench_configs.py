@@ -192,13 +192,15 @@ def c5(args):
     torch.cuda.synchronize()
     t_build = time.perf_counter() - t0
     idx = jb.rabitq_fit(ds, bits=1, seed=1)
+    idx4 = jb.rabitq_fit(ds, bits=4, seed=1)
     q_dev = torch.from_numpy(q).cuda()
     gi, gd = bench._gt_device(ds.device().x, q_dev, 100)
     gt = jb.GroundTruth(gi.cpu().numpy(), gd.cpu().numpy().astype(np.float32))
     out = {"config": "c5-shard", "n": n, "dims": 96, "gen_s": round(t_gen, 1), "build_s": round(t_build, 2),
            "inserts_per_s": round(n / t_build, 1), "hbm_bytes": {"vectors": n * 96 * 4, "graph": n * 32 * 4}}
-    for name, src, kw in (("exact", ds, {}), ("rabitq1_popcount_rerank", idx,
-                                               dict(rerank=True, estimator="popcount"))):
+    for name, src, kw in (("exact", ds, {}),
+                          ("rabitq4_popcount_rerank", idx4, dict(rerank=True, estimator="popcount")),
+                          ("rabitq1_popcount_rerank", idx, dict(rerank=True, estimator="popcount"))):
         pts = []
         for L in bench.SWEEP:
             sp = jb.SearchParams(beam_width=L, k=10, **kw)
