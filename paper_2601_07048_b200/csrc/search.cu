@@ -743,8 +743,7 @@ static bool specialize_off() {
 
 // Occupancy per (kernel, smem size) is cached: the attribute/occupancy queries
 // cost more than the launch itself for small batches.
-static int launch_search_kernel(SearchKernel kern, const SearchLayout& lay, const jb_search_args& a, int minb,
-                                cudaStream_t st) {
+static int launch_search_kernel(SearchKernel kern, const SearchLayout& lay, const jb_search_args& a, cudaStream_t st) {
     const int smem = lay.bytes * WPB;
     JB_CHECK_ARG(smem <= 227 * 1024, "beam search: per-block shared memory %d B exceeds 227 KB", smem);
     // The smem attribute only grows, process-wide (grow_smem), so no host thread can
@@ -765,7 +764,6 @@ static int launch_search_kernel(SearchKernel kern, const SearchLayout& lay, cons
         cache[next] = Entry{kern, smem, dev, per_sm};
         next = (next + 1) % 16;
     }
-    (void)minb;
     int64_t need = (a.nq + WPB - 1) / WPB;
     int grid = (int)std::min<int64_t>(need, (int64_t)per_sm * sm_count_current());
     Scratch ctr;
@@ -790,7 +788,7 @@ static int launch_search(const jb_search_args& a, int hash_slots, cudaStream_t s
         const int hb = lay.hbits;
 #define JB_SPEC(KD_, KHB_)                                                                                   \
     if (a.dims == KD_ && hb == KHB_)                                                                         \
-        return launch_search_kernel(beam_search_kernel<SRC, BITS, ALIGNED, 1, MINB, KD_, KHB_>, lay, a, MINB, st);
+        return launch_search_kernel(beam_search_kernel<SRC, BITS, ALIGNED, 1, MINB, KD_, KHB_>, lay, a, st);
         if (ALIGNED && !specialize_off()) {
             JB_SPEC(128, 7) JB_SPEC(128, 8) JB_SPEC(96, 7) JB_SPEC(96, 8)
         }
@@ -798,10 +796,10 @@ static int launch_search(const jb_search_args& a, int hash_slots, cudaStream_t s
     }
     if (SRC == JB_SRC_EXACT && ALIGNED && a.degree_cap <= 32 && rows_l2_resident(a)) {
         const SearchLayout ld = make_layout(SRC, a.dims, L, hash_slots, FAST_QB, true);
-        return launch_search_kernel(beam_search_kernel<SRC, BITS, ALIGNED, 1, MINB, 0, 0, true>, ld, a, MINB, st);
+        return launch_search_kernel(beam_search_kernel<SRC, BITS, ALIGNED, 1, MINB, 0, 0, true>, ld, a, st);
     }
-    if (a.degree_cap <= 32) return launch_search_kernel(beam_search_kernel<SRC, BITS, ALIGNED, 1, MINB>, lay, a, MINB, st);
-    return launch_search_kernel(beam_search_kernel<SRC, BITS, ALIGNED, MAX_CHUNKS, 8>, lay, a, 8, st);
+    if (a.degree_cap <= 32) return launch_search_kernel(beam_search_kernel<SRC, BITS, ALIGNED, 1, MINB>, lay, a, st);
+    return launch_search_kernel(beam_search_kernel<SRC, BITS, ALIGNED, MAX_CHUNKS, 8>, lay, a, st);
 }
 
 }  // namespace jb
