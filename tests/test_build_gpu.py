@@ -223,3 +223,30 @@ def test_config1_100k_build_identical_to_reference():
     assert g.entry_point == ref["entry"]
     assert hashlib.sha1(np.ascontiguousarray(g.degrees[:100_000]).tobytes()).hexdigest() == ref["degrees_sha1"]
     assert hashlib.sha1(np.ascontiguousarray(g.adjacency[:100_000]).tobytes()).hexdigest() == ref["adjacency_sha1"]
+
+
+def test_u8_odd_dims_and_quantized_m2_odd_dims_match_oracle():
+    """Unaligned rows: u8 with D = 37 (byte-wise staging, scalar dot tail) and a
+    quantized (m = 2) build with D = 33 (partial code pieces)."""
+    from conftest import u8_rows as _u8
+    from oracle import rabitq as orq
+    from oracle import search as osearch
+
+    data = _u8(2100, 37, 45)
+    x8, q8 = data[:2000], data[2000:]
+    og = vamana.build(x8, R=12, L=24, alpha=1.2, max_batch=500)
+    g = jb.build(jb.VectorDataset(x8), jb.BuildParams(degree_cap=12, build_beam_width=24, alpha=1.2, max_batch=500))
+    _same_graph(g, og.adj, og.deg, og.entry)
+    res = jb.run_beam_searches(g, jb.VectorDataset(x8), q8, 24)
+    ores = osearch.beam_search(og.adj, og.active, og.entry, osearch.ExactSource(x8, q8), len(q8), 24)
+    for r, o in zip(res, ores):
+        np.testing.assert_array_equal(r.visited_ids, o.visited_ids)
+        np.testing.assert_array_equal(r.frontier_dists, o.frontier_dists)
+
+    x = gaussian(1500, 33, 46)
+    c, codes, meta = orq.fit(x, 2, 47)
+    oq = vamana.build(x, R=12, L=24, alpha=1.2, max_batch=400, quant=vamana.Quant(c, codes, meta, 2, 47))
+    ds = jb.VectorDataset(x)
+    gq = jb.build(ds, jb.BuildParams(degree_cap=12, build_beam_width=24, alpha=1.2, max_batch=400),
+                  quantizer=jb.rabitq_fit(ds, bits=2, seed=47))
+    _same_graph(gq, oq.adj, oq.deg, oq.entry)
