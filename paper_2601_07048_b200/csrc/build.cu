@@ -486,6 +486,25 @@ __global__ void split_kernel(const int32_t* __restrict__ seen, int64_t n, int32_
     else lost[atomicAdd(nlost, 1)] = (int32_t)i;
 }
 
+// Sorted top-`fan` list held one key per lane (lanes >= fan hold UMAX): insert every
+// lane's candidate key c (UMAX = none) in turn. Keys are distinct (unique ids), so
+// the list after all insertions is the `fan` smallest of list u candidates.
+__device__ __forceinline__ void topk_insert_all(uint64_t& t, uint64_t c, int fan) {
+    const unsigned FULL = 0xFFFFFFFFu;
+    const int lane = lane_id();
+    for (uint32_t mm = __ballot_sync(FULL, c != UMAX); mm; mm &= mm - 1) {
+        const uint64_t k = shfl_u64(c, __ffs(mm) - 1);
+        const uint64_t worst = shfl_u64(t, fan - 1);
+        if (k >= worst) continue;  // uniform
+        const int pos = __popc(__ballot_sync(FULL, lane < fan && t < k));
+        const uint64_t up = __shfl_up_sync(FULL, t, 1);
+        if (lane < fan) {
+            if (lane > pos) t = up;
+            else if (lane == pos) t = k;
+        }
+    }
+}
+
 // ---- repair: nearest reachable donors (build.py:185-192) --------------------
 // Block tile: 64 stranded x 64 reachable rows staged in smem; each thread owns a
 // 4x4 pair sub-tile with four A1 accumulator lanes per pair. Distances use the
@@ -617,19 +636,16 @@ donor_scan_kernel(const float* __restrict__ data, const float* __restrict__ norm
             if (k0v >= worst) k0v = UMAX;
             if (k1v >= worst) k1v = UMAX;
             if (!__any_sync(0xFFFFFFFFu, k0v != UMAX || k1v != UMAX)) continue;
-            // merge: current top (fan) + 64 new keys -> 128-slot buffer, sort, keep fan
-            uint64_t* mb = mbuf + warp * 128;
-            mb[lane] = lane < fan ? tp[lane] : UMAX;
-            mb[32 + lane] = k0v;
-            mb[64 + lane] = k1v;
-            mb[96 + lane] = UMAX;
-            __syncwarp();
-            warp_bitonic_sort_smem(mb, 128);
-            if (lane < fan) tp[lane] = mb[lane];
+            // insert the survivors one at a time into the sorted top list (lanes < fan)
+            uint64_t t = lane < fan ? tp[lane] : UMAX;
+            topk_insert_all(t, k0v, fan);
+            topk_insert_all(t, k1v, fan);
+            if (lane < fan) tp[lane] = t;
             __syncwarp();
         }
         __syncthreads();
     }
+    (void)mbuf;
     for (int i = tid; i < DT * FAN; i += 256) {
         const int row = i / FAN, j = i % FAN;
         if (s0 + row < nlost && j < fan) part[((size_t)slice * nlost + s0 + row) * fan + j] = top[row * FAN + j];
