@@ -654,7 +654,7 @@ donor_scan_kernel(const float* __restrict__ data, const float* __restrict__ norm
 
 // Generic nearest-donor scan (any metric): block = 8 warps = 8 stranded pivots
 // staged in smem, each warp scans a slice of the reachable list one row per lane
-// and keeps a running top-`fan` by (dist, id) key. Output layout as donor_scan_kernel.
+// and keeps a running top-`fan` by (dist, id) key in registers (lane j = j-th best). Output layout as donor_scan_kernel.
 template <class M>
 __global__ void __launch_bounds__(256)
 donor_scan_generic_kernel(const M m, const int32_t* __restrict__ lost, int nlost, const int32_t* __restrict__ reach,
@@ -662,17 +662,15 @@ donor_scan_generic_kernel(const M m, const int32_t* __restrict__ lost, int nlost
     extern __shared__ __align__(16) uint32_t gsh[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     uint32_t* pv = gsh + warp * m.pivot_words();
-    uint64_t* top = reinterpret_cast<uint64_t*>(gsh + 8 * m.pivot_words()) + warp * (FAN + 64);
-    uint64_t* mb = top + FAN;  // 64-slot merge buffer (with top: 80 keys, sorted as 128)
     const int si = blockIdx.x * 8 + warp;
     if (si >= nlost) return;
     const int slice = blockIdx.y;
     const int64_t per = (nreach + slices - 1) / slices;
     const int64_t r_begin = slice * per, r_end = (nreach < r_begin + per) ? (int64_t)nreach : r_begin + per;
     m.load_pivot(pv, (uint32_t)lost[si]);
-    if (lane < FAN) top[lane] = UMAX;
     __syncwarp();
-    __shared__ uint64_t sortbuf[8][128];
+    // lane j holds the j-th best key (j < fan); candidates enter by warp insertion
+    uint64_t t = UMAX;
     for (int64_t r0 = r_begin; r0 < r_end; r0 += 32) {
         const int64_t ri = r0 + lane;
         uint64_t k = UMAX;
@@ -680,21 +678,9 @@ donor_scan_generic_kernel(const M m, const int32_t* __restrict__ lost, int nlost
             const uint32_t r = (uint32_t)reach[ri];
             k = key_of(m.dist(pv, r), r);
         }
-        const uint64_t worst = top[fan - 1];
-        if (k >= worst) k = UMAX;
-        if (!__any_sync(0xFFFFFFFFu, k != UMAX)) continue;
-        uint64_t* sb = sortbuf[warp];
-        sb[lane] = lane < fan ? top[lane] : UMAX;
-        sb[32 + lane] = k;
-        sb[64 + lane] = UMAX;
-        sb[96 + lane] = UMAX;
-        __syncwarp();
-        warp_bitonic_sort_smem(sb, 128);
-        if (lane < fan) top[lane] = sb[lane];
-        __syncwarp();
+        topk_insert_all(t, k, fan);
     }
-    (void)mb;
-    if (lane < fan) part[((size_t)slice * nlost + si) * fan + lane] = top[lane];
+    if (lane < fan) part[((size_t)slice * nlost + si) * fan + lane] = t;
 }
 
 // merge slice top-lists: warp per stranded vertex; writes donors and the sort key
@@ -951,7 +937,7 @@ static int repair(const M& m, const jb_insert_args& a, int64_t n_active, int64_t
             slices = std::max(1, std::min(64, (8 * sm_count_current() + sblocks - 1) / sblocks));
             slices = (int)std::min<int64_t>(slices, std::max<int64_t>(1, (nreach + 31) / 32));
             part = bufs.get<uint64_t>((size_t)slices * nlost * fan, st, _ce); JB_CUDA(_ce);
-            const size_t gsm = (size_t)8 * m.pivot_words() * 4 + 8 * (FAN + 64) * 8;
+            const size_t gsm = (size_t)8 * m.pivot_words() * 4;
             JB_CUDA_RC(grow_smem(donor_scan_generic_kernel<M>, (int)gsm));
             donor_scan_generic_kernel<M><<<dim3(sblocks, slices), 256, gsm, st>>>(m, lost, nlost, reach, nreach, slices,
                                                                                  fan, part);
