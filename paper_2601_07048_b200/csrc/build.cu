@@ -524,7 +524,6 @@ donor_scan_kernel(const float* __restrict__ data, const float* __restrict__ norm
     float* Bs = Ares + DT * AS;                            // [DT][KB+1] reachable k-step
     float* dist = Bs + DT * (KB + 1);                      // [DT][DT+1]
     uint64_t* top = reinterpret_cast<uint64_t*>(dist + DT * (DT + 1) + ((DT * AS + DT * (KB + 1) + DT * (DT + 1)) & 1));
-    uint64_t* mbuf = top + DT * FAN;                       // [8 warps][128]
     const int tid = threadIdx.x;
     const int tx = tid & 15, ty = tid >> 4;  // 16 x 16 threads, 4x4 pairs each
     const int s0 = blockIdx.x * DT;
@@ -645,7 +644,6 @@ donor_scan_kernel(const float* __restrict__ data, const float* __restrict__ norm
         }
         __syncthreads();
     }
-    (void)mbuf;
     for (int i = tid; i < DT * FAN; i += 256) {
         const int row = i / FAN, j = i % FAN;
         if (s0 + row < nlost && j < fan) part[((size_t)slice * nlost + s0 + row) * fan + j] = top[row * FAN + j];
@@ -925,16 +923,16 @@ static int repair(const M& m, const jb_insert_args& a, int64_t n_active, int64_t
         uint64_t* part;
         if (std::is_same<M, F32Metric>::value && D <= 256) {  // tiled A1 scan on the f32 rows
             const int sblocks = (nlost + DT - 1) / DT;
-            slices = std::max(1, std::min(128, (4 * sm_count_current() + sblocks - 1) / sblocks));
+            slices = std::max(1, std::min(128, 4 * sm_count_current() / sblocks));  // whole waves at 2 blocks/SM
             slices = (int)std::min<int64_t>(slices, std::max<int64_t>(1, (nreach + DT - 1) / DT));
             part = bufs.get<uint64_t>((size_t)slices * nlost * fan, st, _ce); JB_CUDA(_ce);
-            const size_t dsm = (size_t)(DT * (D + 1) + DT * 17 + DT * (DT + 1) + 1) * 4 + DT * FAN * 8 + 8 * 128 * 8;
+            const size_t dsm = (size_t)(DT * (D + 1) + DT * 17 + DT * (DT + 1) + 1) * 4 + DT * FAN * 8;
             JB_CUDA_RC(grow_smem(donor_scan_kernel, (int)dsm));
             donor_scan_kernel<<<dim3(sblocks, slices), 256, dsm, st>>>(a.data, a.data_norms, D, lost, nlost, reach,
                                                                       nreach, slices, fan, part);
         } else {
             const int sblocks = (nlost + 7) / 8;
-            slices = std::max(1, std::min(64, (8 * sm_count_current() + sblocks - 1) / sblocks));
+            slices = std::max(1, std::min(64, 8 * sm_count_current() / sblocks));
             slices = (int)std::min<int64_t>(slices, std::max<int64_t>(1, (nreach + 31) / 32));
             part = bufs.get<uint64_t>((size_t)slices * nlost * fan, st, _ce); JB_CUDA(_ce);
             const size_t gsm = (size_t)8 * m.pivot_words() * 4;
