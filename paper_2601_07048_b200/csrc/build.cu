@@ -101,9 +101,104 @@ __device__ int warp_prune(uint64_t* cand, int n, double alpha2, int R, const M& 
 
 // Robust prune with every candidate row already staged in smem (rows[i] <-> cand[i]):
 // same extraction sequence as warp_prune, no global traffic in the rounds.
+// One prune round over the survivor list (star excluded, marked UMAX), F threads
+// per pair of survivors: with few survivors left, the lanes share each distance
+// instead of idling (F = 4 below 16 survivors, 2 below 32).
+template <int F, class M>
+__device__ __forceinline__ void split_round(uint64_t* cand, const uint16_t* lst, int s, int p, double alpha2,
+                                            const M& m, const uint32_t* rows, const uint32_t* cn) {
+    constexpr int G = 32 / F;
+    const int lane = lane_id(), g = lane / F, sub = lane % F;
+    const float pn = __uint_as_float(cn[p]);
+    for (int base = 0; base < s; base += 2 * G) {
+        const int j0 = base + g, j1 = base + G + g;
+        const int i0 = j0 < s ? lst[j0] : p, i1 = j1 < s ? lst[j1] : p;
+        const uint64_t c0 = j0 < s ? cand[i0] : UMAX, c1 = j1 < s ? cand[i1] : UMAX;
+        if (!__any_sync(0xFFFFFFFFu, c0 != UMAX || c1 != UMAX)) continue;
+        float t0, t1;
+        m.template dot2_split<F>(rows, i0, i1, p, sub, t0, t1);
+        if (sub == 0) {
+            if (c0 != UMAX) {
+                const float d0 = exact_from_dot(__uint_as_float(cn[i0]), t0, pn);
+                if (!(__dmul_rn(alpha2, (double)d0) > M::value((uint32_t)(c0 >> 32)))) cand[i0] = UMAX;
+            }
+            if (c1 != UMAX) {
+                const float d1 = exact_from_dot(__uint_as_float(cn[i1]), t1, pn);
+                if (!(__dmul_rn(alpha2, (double)d1) > M::value((uint32_t)(c1 >> 32)))) cand[i1] = UMAX;
+            }
+        }
+    }
+}
+
+// Staged prune over a compacted survivor list (u16 indices into cand/rows): the
+// same extraction sequence as warp_prune; each round's argmin and distance pass
+// touch only the survivors, and the distance pass picks F by their count.
+template <class M>
+__device__ int warp_prune_split(uint64_t* cand, int n, double alpha2, int R, const M& m, const uint32_t* rows,
+                                const uint32_t* cn, uint16_t* lst, int32_t* out_ids, uint32_t* out_d) {
+    const unsigned FULL = 0xFFFFFFFFu;
+    const int lane = lane_id();
+    for (int j = lane; j < n; j += 32) lst[j] = (uint16_t)j;
+    __syncwarp();
+    int s = n, kept = 0;
+    while (kept < R && s > 0) {
+        uint64_t mk = UMAX;
+        int mi = -1;
+        for (int j = lane; j < s; j += 32) {
+            const int i = lst[j];
+            const uint64_t c = cand[i];
+            if (c < mk) { mk = c; mi = i; }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const uint64_t om = shfl_xor_u64(mk, o);
+            const int oi = __shfl_xor_sync(FULL, mi, o);
+            if (om < mk) { mk = om; mi = oi; }
+        }
+        if (mk == UMAX) break;
+        if (lane == 0) {
+            out_ids[kept] = (int32_t)(mk & 0xFFFFFFFFull);
+            out_d[kept] = (uint32_t)(mk >> 32);
+            cand[mi] = UMAX;
+        }
+        ++kept;
+        __syncwarp();
+        if (kept >= R) break;
+        if (s <= 16) split_round<4>(cand, lst, s, mi, alpha2, m, rows, cn);
+        else if (s <= 32) split_round<2>(cand, lst, s, mi, alpha2, m, rows, cn);
+        else split_round<1>(cand, lst, s, mi, alpha2, m, rows, cn);
+        __syncwarp();
+        int ns = 0;  // compact: entries only move down, within the chunk being read
+        for (int b = 0; b < s; b += 32) {
+            const int j = b + lane;
+            int i = 0;
+            bool live = false;
+            if (j < s) { i = lst[j]; live = cand[i] != UMAX; }
+            const unsigned msk = __ballot_sync(FULL, live);
+            if (live) lst[ns + __popc(msk & lanemask_lt())] = (uint16_t)i;
+            ns += __popc(msk);
+            __syncwarp();
+        }
+        s = ns;
+    }
+    __syncwarp();
+    return kept;
+}
+
+// the metric as passed to the kernels that take the split staged prune
+template <class M>
+static M split_prune(M m) {
+    if constexpr (M::kSplit) m.split = true;
+    return m;
+}
+
 template <class M>
 __device__ int warp_prune_staged(uint64_t* cand, int n, double alpha2, int R, const M& m, const uint32_t* rows,
-                                 const uint32_t* cn, int32_t* out_ids, uint32_t* out_d) {
+                                 const uint32_t* cn, uint16_t* lst, int32_t* out_ids, uint32_t* out_d) {
+    if constexpr (M::kSplit) {
+        if (m.split_ok()) return warp_prune_split(cand, n, alpha2, R, m, rows, cn, lst, out_ids, out_d);
+    }
+    (void)lst;
     const int lane = lane_id();
     int kept = 0;
     while (kept < R) {
@@ -158,10 +253,14 @@ __device__ __forceinline__ void write_row(int32_t* __restrict__ adj, int32_t* __
     if (lane == 0) deg[v] = n;
 }
 
-// Per-warp smem of the per-vertex kernels: pivot | staged rows (crows) | their norms.
+// Per-warp smem of the per-vertex kernels:
+// pivot | staged rows (crows) | their norms | u16 survivor list (split prune)
 template <class M>
 __host__ __device__ inline int vertex_warp_words(const M& m, int crows) {
-    return m.pivot_words() + crows * m.stage_stride_words() + ((crows + 3) & ~3);
+    return m.pivot_words() + crows * m.stage_stride_words() + ((crows + 3) & ~3) + ((crows + 7) & ~7) / 2;
+}
+__device__ __forceinline__ uint16_t* stage_list(uint32_t* cn, int crows) {
+    return reinterpret_cast<uint16_t*>(cn + ((crows + 3) & ~3));
 }
 
 // ---- seed batch (build.py:246-266) ------------------------------------------
@@ -219,7 +318,7 @@ phase2_kernel(const M m, int64_t start, int64_t nb, double alpha2, int R, const 
     int k;
     if (h <= crows) {
         m.stage(rows, cn, cand, h);
-        k = warp_prune_staged(cand, h, alpha2, R, m, rows, cn, ki, kd);
+        k = warp_prune_staged(cand, h, alpha2, R, m, rows, cn, stage_list(cn, crows), ki, kd);
     } else {
         k = warp_prune(cand, h, alpha2, R, m, pv, ki, kd);
     }
@@ -294,7 +393,7 @@ refine_prune_kernel(const M m, int64_t start, int64_t nb, double alpha2, int R, 
     int k;
     if (n <= crows) {
         m.stage(rows, cn, cand, n);
-        k = warp_prune_staged(cand, n, alpha2, R, m, rows, cn, ki, kd);
+        k = warp_prune_staged(cand, n, alpha2, R, m, rows, cn, stage_list(cn, crows), ki, kd);
     } else {
         k = warp_prune(cand, n, alpha2, R, m, pv, ki, kd);
     }
@@ -427,7 +526,7 @@ owner_merge_kernel(const M m, double alpha2, int R, int always_prune, const uint
     }
     // existing neighbours get recomputed distances d(t, e) (target is the pivot);
     // fresh entries already hold (stored triple dist << 32 | source) keys
-    m.load_pivot(pv, t);
+    m.load_pivot_async(pv, t);  // overlaps the staging copies below
     const int n = hd + nf;
     int k;
 #ifdef JB_OWNER_STATS
@@ -447,8 +546,10 @@ owner_merge_kernel(const M m, double alpha2, int R, int always_prune, const uint
         m.stage(rows, cn, cand, n);
         for (int j = lane; j < hd; j += 32) cand[j] = key_of(m.dist_pivot_staged(pv, rows, cn, j), (uint32_t)have[j]);
         __syncwarp();
-        k = warp_prune_staged(cand, n, alpha2, R, m, rows, cn, kid, kd);
+        k = warp_prune_staged(cand, n, alpha2, R, m, rows, cn, stage_list(cn, crows), kid, kd);
     } else {
+        cp_async_wait_all();
+        __syncwarp();
         for (int j = lane; j < hd; j += 32) {
             const uint32_t e = (uint32_t)have[j];
             cand[j] = key_of(m.dist(pv, e), e);
@@ -1208,7 +1309,7 @@ static int batch_insert_impl(const M& m, const jb_insert_args& a, cudaStream_t s
     const int p2_smem = BW * 4 * vertex_warp_words(m, crows2);
     JB_CUDA_RC(grow_smem(phase2_kernel<M>, p2_smem));
     phase2_kernel<M><<<(unsigned)((nb + BW - 1) / BW), BW * 32, p2_smem, st>>>(
-        m, a.start, nb, alpha2, R, hops, tids, tdst, cap, a.reverse_all_visited, cand, kid, kd, a.adjacency, a.degrees,
+        split_prune(m), a.start, nb, alpha2, R, hops, tids, tdst, cap, a.reverse_all_visited, cand, kid, kd, a.adjacency, a.degrees,
         tt, tk, W, crows2);
     JB_LAUNCH_CHECK();
     pt.mark("prune");
@@ -1263,7 +1364,7 @@ static int refine_batch_impl(const M& m, const jb_insert_args& a, int64_t active
     const int smem = BW * 4 * vertex_warp_words(m, crows);
     JB_CUDA_RC(grow_smem(refine_prune_kernel<M>, smem));
     refine_prune_kernel<M><<<(unsigned)((nb + BW - 1) / BW), BW * 32, smem, st>>>(
-        m, a.start, nb, alpha2, R, hops, tids, tdst, cap, cand, kid, kd, a.adjacency, a.degrees, tt, tk, crows, ncand);
+        split_prune(m), a.start, nb, alpha2, R, hops, tids, tdst, cap, cand, kid, kd, a.adjacency, a.degrees, tt, tk, crows, ncand);
     JB_LAUNCH_CHECK();
     pt.mark("prune");
     int hseg = 0;

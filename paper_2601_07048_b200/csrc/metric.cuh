@@ -25,6 +25,19 @@ struct F32Metric {
     int D;
     static constexpr bool kInt = false;
     static constexpr bool kStage = true;
+    // Staged rows of D % 16 == 0 are stored 4x4-transposed inside every 16-element
+    // block (word 16b + 4k + v holds element 16b + 4v + k): the four elements that
+    // A1 accumulator lane k adds in one block are one float4, so 1, 2 or 4 threads
+    // can share a distance with the reference's rounding (dot2_split).
+    // Opt-in per launch (split_prune() in build.cu): it pays in phase 2 / refine,
+    // where many candidates are pruned per round, not in the owner merge.
+    static constexpr bool kSplit = true;
+    bool split = false;
+#ifdef JB_NO_SPLIT
+    __host__ __device__ bool split_ok() const { return false; }  // dev A/B: natural layout, flat prune
+#else
+    __host__ __device__ bool split_ok() const { return split && (D & 15) == 0; }
+#endif
 
     __host__ __device__ int row_bytes() const { return D * 4; }
     // smem words of one staged row (16 B skew keeps per-lane float4 reads conflict free)
@@ -40,6 +53,18 @@ struct F32Metric {
         for (int e = lane; e < D; e += 32) f[e] = r[e];
         if (lane == 0) f[((D + 3) & ~3)] = norms[v];
         __syncwarp();
+    }
+    // as load_pivot, but the row copy is left in flight (cp.async): the caller's next
+    // cp_async_wait_all + __syncwarp (e.g. the one closing stage()) completes it
+    __device__ void load_pivot_async(uint32_t* pv, uint32_t v) const {
+        const int lane = lane_id();
+        const float* r = data + (size_t)v * D;
+        if ((D & 3) == 0) {
+            for (int f = lane; f < (D >> 2); f += 32) cp_async16(pv + 4 * f, r + 4 * f);
+        } else {
+            for (int e = lane; e < D; e += 32) cp_async4(pv + e, r + e);
+        }
+        if (lane == 0) pv[((D + 3) & ~3)] = __float_as_uint(norms[v]);
     }
     // d(pivot, row): max((xn[row] - 2*dot(x[row], pivot)) + xn[pivot], 0)
     __device__ uint32_t dist(const uint32_t* pv, uint32_t row) const {
@@ -67,6 +92,18 @@ struct F32Metric {
             cn[j] = __float_as_uint(__ldg(norms + (uint32_t)(keys[j] & 0xFFFFFFFFull)));
         cp_async_wait_all();
         __syncwarp();
+        if (split_ok()) {  // 4x4-transpose every 16-element block in place (one block per lane)
+            const int nb = D >> 4;
+            for (int t = lane; t < n * nb; t += 32) {
+                float4* blk = reinterpret_cast<float4*>(rows + (size_t)(t / nb) * rs + 16 * (t % nb));
+                const float4 v0 = blk[0], v1 = blk[1], v2 = blk[2], v3 = blk[3];
+                blk[0] = make_float4(v0.x, v1.x, v2.x, v3.x);
+                blk[1] = make_float4(v0.y, v1.y, v2.y, v3.y);
+                blk[2] = make_float4(v0.z, v1.z, v2.z, v3.z);
+                blk[3] = make_float4(v0.w, v1.w, v2.w, v3.w);
+            }
+            __syncwarp();
+        }
     }
     // d(staged pivot p, staged row i)
     __device__ uint32_t dist_staged(const uint32_t* rows, const uint32_t* cn, int i, int p) const {
@@ -83,7 +120,18 @@ struct F32Metric {
         const float* f = reinterpret_cast<const float*>(pv);
         const float* a = reinterpret_cast<const float*>(rows + (size_t)i * stage_stride_words());
         Acc4 acc; acc.zero();
-        if ((D & 3) == 0) a1_range<true, false>(acc, a, f, 0, D);
+        if (split_ok()) {  // natural pivot, transposed row
+            const float4* P = reinterpret_cast<const float4*>(f);
+            const float4* T = reinterpret_cast<const float4*>(a);
+            for (int b = 0; b < (D >> 2); b += 4) {
+                const float4 t0 = T[b], t1 = T[b + 1], t2 = T[b + 2], t3 = T[b + 3];
+                const float4 p3 = P[b + 3], p2 = P[b + 2], p1 = P[b + 1], p0 = P[b];
+                acc.madd(make_float4(t0.w, t1.w, t2.w, t3.w), p3);
+                acc.madd(make_float4(t0.z, t1.z, t2.z, t3.z), p2);
+                acc.madd(make_float4(t0.y, t1.y, t2.y, t3.y), p1);
+                acc.madd(make_float4(t0.x, t1.x, t2.x, t3.x), p0);
+            }
+        } else if ((D & 3) == 0) a1_range<true, false>(acc, a, f, 0, D);
         else a1_range<false, false>(acc, a, f, 0, D);
         return __float_as_uint(exact_from_dot(__uint_as_float(cn[i]), acc.reduce(), f[((D + 3) & ~3)]));
     }
@@ -114,6 +162,49 @@ struct F32Metric {
         const float pn = __uint_as_float(cn[p]);
         d0 = __float_as_uint(exact_from_dot(__uint_as_float(cn[i0]), x0.reduce(), pn));
         d1 = __float_as_uint(exact_from_dot(__uint_as_float(cn[i1]), x1.reduce(), pn));
+    }
+    // A1 dots of transposed staged rows i0 and i1 against staged row p, F threads per
+    // row pair: thread `sub` runs accumulator lanes [sub*4/F, (sub+1)*4/F); the lanes
+    // are combined as (l0 + l1) + (l2 + l3), so every F gives the same bits. The full
+    // dots are valid in sub == 0 threads; all 32 lanes must call (shuffles).
+    template <int F>
+    __device__ void dot2_split(const uint32_t* rows, int i0, int i1, int p, int sub, float& d0, float& d1) const {
+        constexpr int NK = 4 / F;
+        const int rs = stage_stride_words();
+        const float4* a0 = reinterpret_cast<const float4*>(rows + (size_t)i0 * rs) + sub * NK;
+        const float4* a1 = reinterpret_cast<const float4*>(rows + (size_t)i1 * rs) + sub * NK;
+        const float4* b = reinterpret_cast<const float4*>(rows + (size_t)p * rs) + sub * NK;
+        float x0[NK], x1[NK];
+#pragma unroll
+        for (int t = 0; t < NK; ++t) x0[t] = x1[t] = 0.0f;
+        for (int v = 0; v < (D >> 2); v += 4) {
+#pragma unroll
+            for (int t = 0; t < NK; ++t) {
+                const float4 bv = b[v + t], u = a0[v + t], w = a1[v + t];
+                x0[t] = __fadd_rn(__fmul_rn(u.w, bv.w), x0[t]);
+                x1[t] = __fadd_rn(__fmul_rn(w.w, bv.w), x1[t]);
+                x0[t] = __fadd_rn(__fmul_rn(u.z, bv.z), x0[t]);
+                x1[t] = __fadd_rn(__fmul_rn(w.z, bv.z), x1[t]);
+                x0[t] = __fadd_rn(__fmul_rn(u.y, bv.y), x0[t]);
+                x1[t] = __fadd_rn(__fmul_rn(w.y, bv.y), x1[t]);
+                x0[t] = __fadd_rn(__fmul_rn(u.x, bv.x), x0[t]);
+                x1[t] = __fadd_rn(__fmul_rn(w.x, bv.x), x1[t]);
+            }
+        }
+        const unsigned FULL = 0xFFFFFFFFu;
+        if (F == 1) {
+            d0 = __fadd_rn(__fadd_rn(x0[0], x0[NK > 1 ? 1 : 0]), __fadd_rn(x0[NK > 2 ? 2 : 0], x0[NK > 3 ? 3 : 0]));
+            d1 = __fadd_rn(__fadd_rn(x1[0], x1[NK > 1 ? 1 : 0]), __fadd_rn(x1[NK > 2 ? 2 : 0], x1[NK > 3 ? 3 : 0]));
+        } else if (F == 2) {  // thread 0: l0 + l1, thread 1: l2 + l3
+            const float h0 = __fadd_rn(x0[0], x0[NK > 1 ? 1 : 0]), h1 = __fadd_rn(x1[0], x1[NK > 1 ? 1 : 0]);
+            d0 = __fadd_rn(h0, __shfl_down_sync(FULL, h0, 1));
+            d1 = __fadd_rn(h1, __shfl_down_sync(FULL, h1, 1));
+        } else {  // thread k holds l_k
+            const float q0 = __fadd_rn(x0[0], __shfl_down_sync(FULL, x0[0], 1));
+            const float q1 = __fadd_rn(x1[0], __shfl_down_sync(FULL, x1[0], 1));
+            d0 = __fadd_rn(q0, __shfl_down_sync(FULL, q0, 2));
+            d1 = __fadd_rn(q1, __shfl_down_sync(FULL, q1, 2));
+        }
     }
 };
 
@@ -149,6 +240,7 @@ struct U8Metric {
     int D;
     static constexpr bool kInt = true;
     static constexpr bool kStage = true;
+    static constexpr bool kSplit = false;
 
     __host__ __device__ int row_bytes() const { return D; }
     __host__ __device__ int stage_stride_words() const { return ((D + 15) & ~15) / 4 + 4; }
@@ -163,6 +255,7 @@ struct U8Metric {
         if (lane == 0) pv[((D + 15) & ~15) / 4] = norms[v];
         __syncwarp();
     }
+    __device__ void load_pivot_async(uint32_t* pv, uint32_t v) const { load_pivot(pv, v); }
     __device__ uint32_t dist(const uint32_t* pv, uint32_t row) const {
         const uint32_t dot = u8_dot(data + (size_t)row * D, reinterpret_cast<const uint8_t*>(pv), D);
         return u8_dist(__ldg(norms + row), dot, pv[((D + 15) & ~15) / 4]);
@@ -301,6 +394,7 @@ struct RabitqMetric {
     int D;
     static constexpr bool kInt = false;
     static constexpr bool kStage = false;
+    static constexpr bool kSplit = false;
 
     __host__ __device__ int meta_off() const { return ((((D * BITS) + 7) / 8 + 15) / 16) * 16; }
     __host__ __device__ int row_bytes() const { return record_bytes; }
@@ -319,6 +413,7 @@ struct RabitqMetric {
         }
         __syncwarp();
     }
+    __device__ void load_pivot_async(uint32_t* pv, uint32_t v) const { load_pivot(pv, v); }
     __device__ uint32_t dist(const uint32_t* pv, uint32_t row) const {
         const float* f = reinterpret_cast<const float*>(pv);
         const float est = rabitq_estimate<BITS>(records + (size_t)row * record_bytes, f, D, meta_off(),
