@@ -1178,8 +1178,13 @@ static int merge_phase(const M& m, const jb_insert_args& a, double alpha2, uint3
             crows = crows_lo;
         const int osm = owner_per_warp(m, R, crows) * BW;
         JB_CUDA_RC(grow_smem(owner_merge_kernel<M>, osm));
+#ifdef JB_OWNER_SPLIT
+        const M mo = split_prune(m);  // dev A/B
+#else
+        const M& mo = m;
+#endif
         owner_merge_kernel<M><<<(unsigned)((hseg + BW - 1) / BW), BW * 32, osm, st>>>(
-            m, alpha2, R, a.always_prune, tt, tk, ntri, seg, nseg, pool, ptop, pool_cap, a.adjacency, a.degrees, err,
+            mo, alpha2, R, a.always_prune, tt, tk, ntri, seg, nseg, pool, ptop, pool_cap, a.adjacency, a.degrees, err,
             crows);
         JB_LAUNCH_CHECK();
         int herr = 0;
