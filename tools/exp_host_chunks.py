@@ -18,7 +18,7 @@ idx = jb.rabitq_fit(ds, bits=1, seed=1)
 qp = torch.empty(q.shape, dtype=torch.float32, pin_memory=True).numpy()
 qp[...] = q
 sp = jb.SearchParams(beam_width=128, k=10, rerank=True, estimator="popcount")
-for chunk in (0, 3334, 2500, 5000, 10000):
+for chunk in [int(v) for v in sys.argv[1:]] or (0, 3334, 2500, 5000, 10000):
     js.PIPELINE["chunk"] = chunk
     for _ in range(3):
         jb.search_knn_batch(g, idx, qp, sp, exact_data=ds)
@@ -28,3 +28,30 @@ for chunk in (0, 3334, 2500, 5000, 10000):
         jb.search_knn_batch(g, idx, qp, sp, exact_data=ds)
         ts.append(time.perf_counter() - t)
     print(f"chunk {chunk:5d}: median {1e3 * np.median(ts):.3f} ms  {10_000 / np.median(ts) / 1e6:.2f} MQPS", flush=True)
+
+# fixed per-call overhead (tiny batch) and the HBM-resident API for comparison
+js.PIPELINE["chunk"] = 0
+for nq in (32, 10_000):
+    qq = qp[:nq]
+    for _ in range(3):
+        jb.search_knn_batch(g, idx, qq, sp, exact_data=ds)
+    ts = []
+    for _ in range(15):
+        t = time.perf_counter()
+        jb.search_knn_batch(g, idx, qq, sp, exact_data=ds)
+        ts.append(time.perf_counter() - t)
+    print(f"host nq={nq}: median {1e3 * np.median(ts):.3f} ms", flush=True)
+qd = torch.from_numpy(q).cuda()
+for _ in range(3):
+    jb.search_knn_batch_device(g, idx, qd, sp, exact_data=ds)
+torch.cuda.synchronize()
+ts = []
+for _ in range(15):
+    t = time.perf_counter()
+    jb.search_knn_batch_device(g, idx, qd, sp, exact_data=ds)
+    torch.cuda.synchronize()
+    ts.append(time.perf_counter() - t)
+print(f"device API nq=10000: median {1e3 * np.median(ts):.3f} ms", flush=True)
+os.environ["JB_PIPE_PROFILE"] = "1"
+for _ in range(3):
+    jb.search_knn_batch(g, idx, qp, sp, exact_data=ds)
