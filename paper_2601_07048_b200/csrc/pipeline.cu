@@ -139,6 +139,7 @@ struct Lane {
     int32_t* d_ids = nullptr;    // [C, k]
     double* d_d = nullptr;       // [C, k]
     int64_t pend_q0 = -1, pend_m = 0;
+    bool pend_direct = false;    // results went straight into the caller's pinned arrays
 };
 
 struct Ctx {
@@ -205,8 +206,10 @@ int drain(Ctx& c, Lane& l, int k, int32_t* out_ids, double* out_d, PhaseTimer& p
     pt.tick(1);
     JB_CUDA(cudaEventSynchronize(l.done));
     pt.tick(2);
-    c.pool->copy(out_ids + l.pend_q0 * k, l.h_ids, sizeof(int32_t) * l.pend_m * k);
-    c.pool->copy(out_d + l.pend_q0 * k, l.h_d, sizeof(double) * l.pend_m * k);
+    if (!l.pend_direct) {
+        c.pool->copy(out_ids + l.pend_q0 * k, l.h_ids, sizeof(int32_t) * l.pend_m * k);
+        c.pool->copy(out_d + l.pend_q0 * k, l.h_d, sizeof(double) * l.pend_m * k);
+    }
     pt.tick(3);
     l.pend_q0 = -1;
     return JB_OK;
@@ -280,9 +283,15 @@ static int search_knn_host(const jb_knn_plan* plan, const float* queries, int64_
 
     // Queries already in page-locked memory (cudaHostAlloc / registered) are copied
     // to HBM straight from the caller's buffer; pageable ones go through staging.
-    cudaPointerAttributes pa{};
-    const bool pinned_in = cudaPointerGetAttributes(&pa, queries) == cudaSuccess && pa.type == cudaMemoryTypeHost;
-    cudaGetLastError();  // a pageable pointer may leave an error behind on older drivers
+    // Likewise results: page-locked output arrays receive the D2H copies directly.
+    auto pinned = [](const void* p) {
+        cudaPointerAttributes pa{};
+        const bool r = cudaPointerGetAttributes(&pa, p) == cudaSuccess && pa.type == cudaMemoryTypeHost;
+        cudaGetLastError();  // a pageable pointer may leave an error behind on older drivers
+        return r;
+    };
+    const bool pinned_in = pinned(queries);
+    const bool pinned_out = pinned(out_ids) && pinned(out_dists);
 
     PhaseTimer pt;
     int64_t chunk_i = 0;
@@ -299,11 +308,14 @@ static int search_knn_host(const jb_knn_plan* plan, const float* queries, int64_
         pt.tick(0);
         JB_CUDA(cudaMemcpyAsync(l.d_q, src, sizeof(float) * m * D, cudaMemcpyHostToDevice, l.s));
         if ((st = run_chunk(plan, l, l.d_q, m, l.d_ids, l.d_d)) != JB_OK) return st;
-        JB_CUDA(cudaMemcpyAsync(l.h_ids, l.d_ids, sizeof(int32_t) * m * k, cudaMemcpyDeviceToHost, l.s));
-        JB_CUDA(cudaMemcpyAsync(l.h_d, l.d_d, sizeof(double) * m * k, cudaMemcpyDeviceToHost, l.s));
+        int32_t* hi = pinned_out ? out_ids + q0 * k : l.h_ids;
+        double* hd = pinned_out ? out_dists + q0 * k : l.h_d;
+        JB_CUDA(cudaMemcpyAsync(hi, l.d_ids, sizeof(int32_t) * m * k, cudaMemcpyDeviceToHost, l.s));
+        JB_CUDA(cudaMemcpyAsync(hd, l.d_d, sizeof(double) * m * k, cudaMemcpyDeviceToHost, l.s));
         JB_CUDA(cudaEventRecord(l.done, l.s));
         l.pend_q0 = q0;
         l.pend_m = m;
+        l.pend_direct = pinned_out;
     }
     for (int i = 0; i < 2; ++i) {
         // drain in submission order

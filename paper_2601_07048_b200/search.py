@@ -391,11 +391,20 @@ def search_knn_batch(graph, source, queries, params: SearchParams, exact_data=No
     q = np.atleast_2d(np.asarray(queries))
     q = np.ascontiguousarray(q, dtype=np.float32)
     nq = q.shape[0]
-    ids = np.empty((nq, params.k), dtype=np.int32)
-    dists = np.empty((nq, params.k), dtype=np.float64)
+    ids, dists = _host_results(nq, params.k)
     plan = _knn_plan(graph, source, q.shape[1], params, exact_data)
     _lib.check(_lib.lib().jb_search_knn_host(_lib.C.byref(plan), _lib.ptr(q), nq, _lib.ptr(ids), _lib.ptr(dists),
                                              _lib.stream_ptr()))
+    return ids, dists
+
+
+def _host_results(nq: int, k: int):
+    """int32 ids / f64 dists result arrays in page-locked host memory (numpy views
+    of pinned torch tensors, cached by torch's host allocator), so the pipeline's
+    device-to-host copies land in them directly instead of via staging."""
+    torch = _lib.require_cuda()
+    ids = torch.empty((nq, k), dtype=torch.int32, pin_memory=True).numpy()
+    dists = torch.empty((nq, k), dtype=torch.float64, pin_memory=True).numpy()
     return ids, dists
 
 
