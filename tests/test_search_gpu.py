@@ -330,6 +330,14 @@ def test_host_pipeline_matches_device_path(chunk, kind):
         qp = torch.empty(q.shape, dtype=torch.float32, pin_memory=True).numpy()  # pinned: no staging copy
         qp[...] = q
         hi3, hd3 = jb.search_knn_batch(g, src, qp, sp, exact_data=ds)
+        # pageable result arrays through the C ABI: the staged copy-out path
+        from paper_2601_07048_b200 import _lib
+
+        plan = js._knn_plan(g, src, q.shape[1], sp, ds)
+        hi4 = np.empty((len(q), sp.k), np.int32)
+        hd4 = np.empty((len(q), sp.k), np.float64)
+        _lib.check(_lib.lib().jb_search_knn_host(_lib.C.byref(plan), _lib.ptr(q), len(q), _lib.ptr(hi4),
+                                                 _lib.ptr(hd4), _lib.stream_ptr()))
     finally:
         js.PIPELINE["chunk"] = 0
     np.testing.assert_array_equal(hi, di.cpu().numpy())
@@ -338,6 +346,8 @@ def test_host_pipeline_matches_device_path(chunk, kind):
     np.testing.assert_array_equal(hd2, hd[:333])
     np.testing.assert_array_equal(hi3, hi)
     np.testing.assert_array_equal(hd3, hd)
+    np.testing.assert_array_equal(hi4, hi)
+    np.testing.assert_array_equal(hd4, hd)
 
 
 def test_u8_search_knn_gt_medoid_match_reference_golden():
