@@ -47,6 +47,18 @@ def _timed(fn, reps=5, warm=2):
     return float(np.mean([a.elapsed_time(b) for a, b in evs]))
 
 
+def _warm_build(jb, x, params):
+    """Untimed build on a prefix of the same rows (min(n/4, 250K)) so the timed build
+    does not pay the process's one-time costs (module loads, pool growth), as in
+    bench.py."""
+    import torch
+
+    nw = min(len(x) // 4, 250_000)
+    if nw > params.degree_cap + 1:
+        jb.build(jb.VectorDataset(x[:nw]), params)
+    torch.cuda.synchronize()
+
+
 def c1(args):
     import torch
 
@@ -56,6 +68,7 @@ def c1(args):
     x = jb.gen_synthetic(args.n or 100_000, 128, seed=0).data
     q = jb.gen_synthetic(10_000, 128, seed=1).data
     ds = jb.VectorDataset(x)
+    _warm_build(jb, x, jb.BuildParams(degree_cap=32, build_beam_width=64, alpha=1.2))
     t0 = time.perf_counter()
     g = jb.build(ds, jb.BuildParams(degree_cap=32, build_beam_width=64, alpha=1.2))
     torch.cuda.synchronize()
@@ -96,6 +109,7 @@ def c3(args):
     x = jb.gen_lowrank(n, 960, seed=1, d_int=dint, noise=0.05, basis_seed=0)
     q = jb.gen_lowrank(10_000, 960, seed=1_000_003, d_int=dint, noise=0.05, basis_seed=0)
     ds = jb.VectorDataset(x)
+    _warm_build(jb, x, jb.BuildParams(degree_cap=32, build_beam_width=64, alpha=1.2))
     t0 = time.perf_counter()
     g = jb.build(ds, jb.BuildParams(degree_cap=32, build_beam_width=64, alpha=1.2))
     torch.cuda.synchronize()
@@ -136,7 +150,7 @@ def c4(args):
     ds.device()
     params = jb.BuildParams(degree_cap=32, build_beam_width=64, alpha=1.2, max_batch=100_000)
     g = jb.GraphIndex(capacity=total, degree_cap=32)
-    torch.cuda.synchronize()
+    _warm_build(jb, x[:n0], params)
     t0 = time.perf_counter()
     # bulk phase on the first n0 rows: same schedule as build() over a prefix
     size, pos = params.degree_cap + 1, 0
@@ -156,7 +170,8 @@ def c4(args):
         jb.insert_stream(g, ds, range(pos, stop), params)
         torch.cuda.synchronize()
         ins_t.append((stop - pos, time.perf_counter() - t0))
-        ms = _timed(lambda: jb.search_knn_batch_device(g, ds, q_dev, sp), reps=1, warm=0)
+        # (the first call also allocates the search context: warm it once)
+        ms = _timed(lambda: jb.search_knn_batch_device(g, ds, q_dev, sp), reps=1, warm=0 if qps else 1)
         qps.append(10_000 / (ms / 1e3))
         pos = stop
     ids, _ = jb.search_knn_batch_device(g, ds, q_dev, sp)
@@ -186,7 +201,7 @@ def c5(args):
     t_gen = time.perf_counter() - t0
     ds = jb.VectorDataset(x)
     ds.device()
-    torch.cuda.synchronize()
+    _warm_build(jb, x, jb.BuildParams(degree_cap=32, build_beam_width=64, alpha=1.2, max_batch=100_000))
     t0 = time.perf_counter()
     g = jb.build(ds, jb.BuildParams(degree_cap=32, build_beam_width=64, alpha=1.2, max_batch=100_000))
     torch.cuda.synchronize()
@@ -227,7 +242,7 @@ def u8(args):
     data, q = rows[:n], rows[n:]
     ds = jb.VectorDataset(data)
     ds.device()
-    torch.cuda.synchronize()
+    _warm_build(jb, data, jb.BuildParams(degree_cap=32, build_beam_width=64, alpha=1.2, max_batch=100_000))
     t0 = time.perf_counter()
     g = jb.build(ds, jb.BuildParams(degree_cap=32, build_beam_width=64, alpha=1.2, max_batch=100_000))
     torch.cuda.synchronize()
