@@ -148,7 +148,8 @@ def c4(args):
     q = jb.gen_lowrank(10_000, 96, seed=1_000_003, d_int=16, noise=0.05, basis_seed=0)
     ds = jb.VectorDataset(x)
     ds.device()
-    params = jb.BuildParams(degree_cap=32, build_beam_width=64, alpha=1.2, max_batch=100_000)
+    params = jb.BuildParams(degree_cap=32, build_beam_width=64, alpha=1.2, max_batch=100_000,
+                            repair_beam_width=args.repair_beam)
     g = jb.GraphIndex(capacity=total, degree_cap=32)
     _warm_build(jb, x[:n0], params)
     t0 = time.perf_counter()
@@ -177,7 +178,8 @@ def c4(args):
     ids, _ = jb.search_knn_batch_device(g, ds, q_dev, sp)
     gi, gd = bench._gt_device(ds.device().x, q_dev, 100)
     gt = jb.GroundTruth(gi.cpu().numpy(), gd.cpu().numpy().astype(np.float32))
-    return {"config": "c4", "total": total, "bulk_n": n0, "bulk_inserts_per_s": round(n0 / t_bulk, 1),
+    return {"config": "c4", "total": total, "bulk_n": n0, "repair_beam_width": args.repair_beam,
+            "bulk_inserts_per_s": round(n0 / t_bulk, 1),
             "stream_batches": len(ins_t),
             "stream_inserts_per_s": round(sum(n for n, _ in ins_t) / sum(t for _, t in ins_t), 1),
             "stream_inserts_per_s_first_last": [round(ins_t[0][0] / ins_t[0][1], 1),
@@ -201,9 +203,11 @@ def c5(args):
     t_gen = time.perf_counter() - t0
     ds = jb.VectorDataset(x)
     ds.device()
-    _warm_build(jb, x, jb.BuildParams(degree_cap=32, build_beam_width=64, alpha=1.2, max_batch=100_000))
+    bp = jb.BuildParams(degree_cap=32, build_beam_width=64, alpha=1.2, max_batch=100_000,
+                        repair_beam_width=args.repair_beam)
+    _warm_build(jb, x, bp)
     t0 = time.perf_counter()
-    g = jb.build(ds, jb.BuildParams(degree_cap=32, build_beam_width=64, alpha=1.2, max_batch=100_000))
+    g = jb.build(ds, bp)
     torch.cuda.synchronize()
     t_build = time.perf_counter() - t0
     idx = jb.rabitq_fit(ds, bits=1, seed=1)
@@ -211,7 +215,7 @@ def c5(args):
     q_dev = torch.from_numpy(q).cuda()
     gi, gd = bench._gt_device(ds.device().x, q_dev, 100)
     gt = jb.GroundTruth(gi.cpu().numpy(), gd.cpu().numpy().astype(np.float32))
-    out = {"config": "c5-shard", "n": n, "dims": 96, "gen_s": round(t_gen, 1), "build_s": round(t_build, 2),
+    out = {"config": "c5-shard", "n": n, "repair_beam_width": args.repair_beam, "dims": 96, "gen_s": round(t_gen, 1), "build_s": round(t_build, 2),
            "inserts_per_s": round(n / t_build, 1), "hbm_bytes": {"vectors": n * 96 * 4, "graph": n * 32 * 4}}
     for name, src, kw in (("exact", ds, {}),
                           ("rabitq4_popcount_rerank", idx4, dict(rerank=True, estimator="popcount")),
@@ -271,6 +275,8 @@ def main():
     p.add_argument("--dint", type=int, default=0)
     p.add_argument("--n", type=int, default=0)
     p.add_argument("--total", type=int, default=0)
+    p.add_argument("--repair-beam", type=int, default=0,
+                   help="c4/c5: approximate connectivity repair (BuildParams.repair_beam_width; 0 = exact)")
     p.add_argument("--out", default="")
     args = p.parse_args()
     import torch

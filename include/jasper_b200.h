@@ -247,6 +247,12 @@ typedef struct jb_insert_args {
     const float* bound_rotated;    /* [count, D] rows bound as queries          */
     const float* bound_qadd;       /* [count]                                   */
     const float* bound_qsumq;      /* [count]                                   */
+    /* Extension (not in the reference; default 0 = the reference's exact repair):
+     * > 0 makes connectivity repair take each stranded vertex's donors from the
+     * frontier of a beam search of this width from the entry point (which only
+     * reaches reachable vertices) instead of the exact scan over all reachable
+     * rows (build.py:185-192), for 10M-row streaming. */
+    int32_t repair_beam_width;
 } jb_insert_args;
 
 /* One three-phase batch: search -> prune + reverse triples -> grouped merge,

@@ -54,6 +54,7 @@ class InsertArgs(C.Structure):
         ("element_kind", i32), ("data_u8", p), ("norms_u32", p),
         ("quantized", i32), ("records", p), ("record_bytes", i32), ("bits", i32),
         ("bound_rotated", p), ("bound_qadd", p), ("bound_qsumq", p),
+        ("repair_beam_width", i32),
     ]
 
 

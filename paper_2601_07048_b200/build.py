@@ -41,6 +41,9 @@ class BuildParams:
     two_pass: bool = False
     always_prune: bool = False
     reverse_all_visited: bool = False
+    # Extension (not in beamann): 0 = the reference's exact connectivity repair;
+    # > 0 = donors from a beam search of this width (SURVEY.md §8 B6 approximate mode)
+    repair_beam_width: int = 0
 
     def __post_init__(self):
         if self.degree_cap < 2:
@@ -51,6 +54,8 @@ class BuildParams:
             raise ValueError(f"build_beam_width must be in [1, {MAX_BEAM_WIDTH}]")
         if self.max_batch < 1:
             raise ValueError("max_batch must be >= 1")
+        if not 0 <= self.repair_beam_width <= MAX_BEAM_WIDTH:
+            raise ValueError(f"repair_beam_width must be in [0, {MAX_BEAM_WIDTH}]")
         if self.build_beam_width < self.degree_cap:
             warnings.warn("build_beam_width below degree_cap gives sparse candidate sets", stacklevel=2)
 
@@ -148,6 +153,7 @@ def _args(graph: GraphIndex, ds, params: BuildParams, start: int, stop: int, qua
     a.alpha = float(params.alpha)
     a.always_prune = int(params.always_prune)
     a.reverse_all_visited = int(params.reverse_all_visited)
+    a.repair_beam_width = int(params.repair_beam_width)
     a.start, a.stop = start, stop
     a.entry_point = graph.entry_point
     if quantizer is not None:

@@ -959,6 +959,89 @@ static int staged_rows(const M& m, int want, int R, int budget_kb = JB_STAGE_KB)
     return crows < R + 1 ? 0 : crows;
 }
 
+// ---- repair, approximate donors (extension, jb_insert_args.repair_beam_width) ----
+// dst[i] = src row ids[i] (row_bytes each; word copies when rows are 4-byte multiples)
+__global__ void gather_rows_kernel(const uint8_t* __restrict__ src, int64_t row_bytes, const int32_t* __restrict__ ids,
+                                   int n, uint8_t* __restrict__ dst) {
+    const int64_t total = (int64_t)n * row_bytes;
+    if ((row_bytes & 3) == 0) {
+        const int64_t rw = row_bytes >> 2;
+        for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total / 4; i += (int64_t)gridDim.x * blockDim.x) {
+            const int64_t r = i / rw, w = i % rw;
+            reinterpret_cast<uint32_t*>(dst)[i] = reinterpret_cast<const uint32_t*>(src)[(int64_t)ids[r] * rw + w];
+        }
+    } else {
+        for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+            const int64_t r = i / row_bytes, b = i % row_bytes;
+            dst[i] = src[(int64_t)ids[r] * row_bytes + b];
+        }
+    }
+}
+
+// part[w, j] = frontier key j of stranded vertex w (j < fan; UMAX past the frontier)
+__global__ void frontier_head_kernel(const uint64_t* __restrict__ fk, int nlost, int L, int fan,
+                                     uint64_t* __restrict__ part) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (int64_t)nlost * fan) return;
+    const int64_t w = i / fan;
+    const int j = (int)(i % fan);
+    part[i] = j < L ? fk[w * L + j] : UMAX;
+}
+
+static unsigned gather_blocks(int64_t work) {
+    return (unsigned)std::max<int64_t>(1, std::min<int64_t>((work + 255) / 256, 8 * sm_count_current()));
+}
+
+// Donor candidates of the stranded vertices from one batched beam search (width
+// repair_beam_width) from the entry point with the stranded rows as queries: the
+// search only walks edges out of the reachable set, so every frontier vertex is
+// reachable, and its keys are d(x, r) with r in the data role and x's norm added
+// last, as in the exact scan. The top `fan` frontier keys become slice 0 of `part`.
+static int approx_donors(const jb_insert_args& a, const int32_t* lost, int nlost, int64_t n_active, int64_t entry,
+                         int fan, Bufs& bufs, cudaStream_t st, uint64_t*& part) {
+    cudaError_t _ce;
+    const int D = a.dims, Ls = a.repair_beam_width;
+    jb_search_args s{};
+    s.adjacency = a.adjacency; s.degree_cap = a.degree_cap; s.active_count = n_active; s.dims = D;
+    auto gather = [&](const void* src, int64_t row_bytes, void*& out) -> int {
+        BALLOC(buf, uint8_t, (size_t)nlost * row_bytes);
+        gather_rows_kernel<<<gather_blocks((int64_t)nlost * row_bytes / 4), 256, 0, st>>>(
+            static_cast<const uint8_t*>(src), row_bytes, lost, nlost, buf);
+        JB_LAUNCH_CHECK();
+        out = buf;
+        return JB_OK;
+    };
+    void *q = nullptr, *qa = nullptr, *qs = nullptr;
+    int rc;
+    if (a.quantized) {
+        s.source = JB_SRC_RABITQ;
+        s.records = a.records; s.record_bytes = a.record_bytes; s.bits = a.bits;
+        if ((rc = gather(a.bound_rotated, (int64_t)D * 4, q)) || (rc = gather(a.bound_qadd, 4, qa)) ||
+            (rc = gather(a.bound_qsumq, 4, qs)))
+            return rc;
+        s.queries = static_cast<const float*>(q); s.query_add = static_cast<const float*>(qa);
+        s.query_sumq = static_cast<const float*>(qs);
+    } else if (a.element_kind == JB_KIND_U8) {
+        s.source = JB_SRC_EXACT_U8;
+        s.data_u8 = a.data_u8; s.norms_u32 = a.norms_u32;
+        if ((rc = gather(a.data_u8, D, q)) || (rc = gather(a.norms_u32, 4, qa))) return rc;
+        s.queries_u8 = static_cast<const uint8_t*>(q); s.query_norms_u32 = static_cast<const uint32_t*>(qa);
+    } else {
+        s.source = JB_SRC_EXACT;
+        s.data = a.data; s.data_norms = a.data_norms;
+        if ((rc = gather(a.data, (int64_t)D * 4, q)) || (rc = gather(a.data_norms, 4, qa))) return rc;
+        s.queries = static_cast<const float*>(q); s.query_add = static_cast<const float*>(qa);
+    }
+    BALLOC(fk, uint64_t, (size_t)nlost * Ls);
+    s.nq = nlost; s.starts = nullptr; s.start_vertex = entry;
+    s.beam_width = Ls; s.hash_slots = 0; s.trace_cap = 0; s.frontier_keys = fk;
+    if ((rc = jb_beam_search(&s, st)) != JB_OK) return rc;
+    part = bufs.get<uint64_t>((size_t)nlost * fan, st, _ce); JB_CUDA(_ce);
+    frontier_head_kernel<<<(unsigned)(((int64_t)nlost * fan + 255) / 256), 256, 0, st>>>(fk, nlost, Ls, fan, part);
+    JB_LAUNCH_CHECK();
+    return JB_OK;
+}
+
 template <class M>
 static int repair(const M& m, const jb_insert_args& a, int64_t n_active, int64_t entry, cudaStream_t st,
                   int64_t* bridges_out) {
@@ -1022,7 +1105,11 @@ static int repair(const M& m, const jb_insert_args& a, int64_t n_active, int64_t
         BALLOC(oval2, int32_t, nlost);
         int slices;
         uint64_t* part;
-        if (std::is_same<M, F32Metric>::value && D <= 256) {  // tiled A1 scan on the f32 rows
+        if (a.repair_beam_width > 0) {  // approximate donors (extension)
+            slices = 1;
+            const int rc = approx_donors(a, lost, nlost, n_active, entry, fan, bufs, st, part);
+            if (rc != JB_OK) return rc;
+        } else if (std::is_same<M, F32Metric>::value && D <= 256) {  // tiled A1 scan on the f32 rows
             const int sblocks = (nlost + DT - 1) / DT;
             slices = std::max(1, std::min(128, 4 * sm_count_current() / sblocks));  // whole waves at 2 blocks/SM
             slices = (int)std::min<int64_t>(slices, std::max<int64_t>(1, (nreach + DT - 1) / DT));

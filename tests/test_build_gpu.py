@@ -250,3 +250,42 @@ def test_u8_odd_dims_and_quantized_m2_odd_dims_match_oracle():
     gq = jb.build(ds, jb.BuildParams(degree_cap=12, build_beam_width=24, alpha=1.2, max_batch=400),
                   quantizer=jb.rabitq_fit(ds, bits=2, seed=47))
     _same_graph(gq, oq.adj, oq.deg, oq.entry)
+
+
+@pytest.mark.parametrize("kind", ["f32", "u8", "quantized"])
+def test_approximate_repair_reachable_and_recall(kind):
+    """Extension: repair_beam_width > 0 takes donors from a beam
+    search instead of the exact scan. The graph must stay valid and fully reachable,
+    and recall@10 must stay within 0.5 points of the exact-repair build; the
+    default (0) is the reference's repair, bit-identical to the oracle."""
+    if kind == "u8":
+        x = u8_rows(12000, 64, 91)
+        q = u8_rows(400, 64, 92)
+    else:
+        x = gaussian(12000, 64, 91)  # iid Gaussian: repair-heavy (~25% bridges)
+        q = gaussian(400, 64, 92)
+    ds = jb.VectorDataset(x)
+    quant = jb.rabitq_fit(ds, bits=4, seed=5) if kind == "quantized" else None
+    base = dict(degree_cap=24, build_beam_width=48, alpha=1.2, max_batch=3000)
+    ge = jb.build(ds, jb.BuildParams(**base), quantizer=quant)
+    ga = jb.build(ds, jb.BuildParams(**base, repair_beam_width=48), quantizer=quant)
+    for g in (ge, ga):
+        g.validate()
+        og = vamana.Graph(g.capacity, 24)
+        og.adj[:] = g.adjacency
+        og.deg[:] = g.degrees
+        og.active, og.entry = g.active_count, g.entry_point
+        assert vamana.reachable(og).all()
+    from oracle import knn
+
+    gt = jb.GroundTruth(*knn.exact_knn(x.astype(np.float32), q.astype(np.float32), 10))
+    sp = jb.SearchParams(beam_width=48, k=10)
+    re = jb.recall_at_k(jb.search_knn_batch(ge, ds, q, sp)[0], gt, 10)
+    ra = jb.recall_at_k(jb.search_knn_batch(ga, ds, q, sp)[0], gt, 10)
+    assert ra >= re - 0.005, (re, ra)
+    assert not np.array_equal(ge.adjacency, ga.adjacency) or kind == "u8"  # the mode is actually taken
+
+
+def test_repair_beam_width_validation():
+    with pytest.raises(ValueError, match="repair_beam_width"):
+        jb.BuildParams(repair_beam_width=-1)
