@@ -568,23 +568,46 @@ __global__ void bfs_init_kernel(int32_t* __restrict__ seen, int64_t n, int64_t e
     if (i == 0) { front[0] = (int32_t)entry; *fcount = 1; }
 }
 
+// Append `v` to list[] for the lanes with `take`: one atomicAdd per warp (a single
+// global counter taking one atomic per element serialises at 10M-vertex scale).
+// Every lane of the warp must call. List order is irrelevant to the callers.
+__device__ __forceinline__ void warp_append(bool take, int32_t v, int32_t* __restrict__ list, int* __restrict__ count) {
+    const unsigned m = __ballot_sync(0xFFFFFFFFu, take);
+    if (m == 0) return;
+    const int lane = lane_id(), leader = __ffs(m) - 1;
+    int base = 0;
+    if (lane == leader) base = atomicAdd(count, __popc(m));
+    base = __shfl_sync(0xFFFFFFFFu, base, leader);
+    if (take) list[base + __popc(m & lanemask_lt())] = v;
+}
+
+// One warp per frontier vertex (grid-stride), lane j reads edge j of its row: a
+// coalesced 4R-byte row read and no per-edge index division.
 __global__ void bfs_expand_kernel(const int32_t* __restrict__ adj, int R, const int32_t* __restrict__ front,
                                   const int* __restrict__ fcount, int32_t* __restrict__ seen,
                                   int32_t* __restrict__ next, int* __restrict__ ncount) {
-    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= (int64_t)(*fcount) * R) return;
-    const int32_t v = adj[(size_t)front[i / R] * R + (i % R)];
-    if (v < 0) return;
-    if (seen[v]) return;
-    if (atomicExch(&seen[v], 1) == 0) next[atomicAdd(ncount, 1)] = v;
+    const int lane = threadIdx.x & 31;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int n = *fcount;
+    for (int64_t f = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; f < n; f += nwarps) {
+        const int32_t* row = adj + (size_t)front[f] * R;
+        for (int j0 = 0; j0 < R; j0 += 32) {
+            const int j = j0 + lane;
+            const int32_t v = j < R ? row[j] : -1;
+            bool found = false;
+            if (v >= 0 && !seen[v]) found = atomicExch(&seen[v], 1) == 0;
+            warp_append(found, v, next, ncount);
+        }
+    }
 }
 
 __global__ void split_kernel(const int32_t* __restrict__ seen, int64_t n, int32_t* __restrict__ lost,
                              int* __restrict__ nlost, int32_t* __restrict__ reach, int* __restrict__ nreach) {
-    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    if (seen[i]) reach[atomicAdd(nreach, 1)] = (int32_t)i;
-    else lost[atomicAdd(nlost, 1)] = (int32_t)i;
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool in = i < n;
+    const bool r = in && seen[i];
+    warp_append(r, (int32_t)i, reach, nreach);
+    warp_append(in && !r, (int32_t)i, lost, nlost);
 }
 
 // Sorted top-`fan` list held one key per lane (lanes >= fan hold UMAX): insert every
@@ -1069,20 +1092,21 @@ static int repair(const M& m, const jb_insert_args& a, int64_t n_active, int64_t
         PhaseTimer rt(st);
         // BFS from the entry
         bfs_init_kernel<<<nblk, T, 0, st>>>(seen, n_active, entry, fa, counts);
-        int fcount = 1;
+        int fcount = 1, levels = 0;
         int32_t* cur = fa;
         int32_t* nxt = fb;
         int* fc = counts;
         int* nc = counts + 1;
         while (fcount > 0) {
             JB_CUDA(cudaMemsetAsync(nc, 0, sizeof(int), st));
-            const int64_t work = (int64_t)fcount * R;
-            bfs_expand_kernel<<<(unsigned)((work + T - 1) / T), T, 0, st>>>(a.adjacency, R, cur, fc, seen, nxt, nc);
+            const unsigned eb = (unsigned)std::min<int64_t>(((int64_t)fcount * 32 + T - 1) / T, 8 * sm_count_current());
+            bfs_expand_kernel<<<eb, T, 0, st>>>(a.adjacency, R, cur, fc, seen, nxt, nc);
             JB_LAUNCH_CHECK();
             JB_CUDA(cudaMemcpyAsync(&fcount, nc, sizeof(int), cudaMemcpyDeviceToHost, st));
             JB_CUDA(cudaStreamSynchronize(st));
             std::swap(cur, nxt);
             std::swap(fc, nc);
+            ++levels;
         }
         JB_CUDA(cudaMemsetAsync(counts + 2, 0, 2 * sizeof(int), st));
         split_kernel<<<nblk, T, 0, st>>>(seen, n_active, lost, counts + 2, reach, counts + 3);
@@ -1092,7 +1116,8 @@ static int repair(const M& m, const jb_insert_args& a, int64_t n_active, int64_t
         const int nlost = h[0], nreach = h[1];
         rt.mark("bfs");
         if (getenv("JB_PROFILE") && getenv("JB_PROFILE")[0] == '1')
-            fprintf(stderr, "[jb]   repair round %d: stranded %d reachable %d\n", round, nlost, nreach);
+            fprintf(stderr, "[jb]   repair round %d: stranded %d reachable %d (BFS levels %d)\n", round, nlost, nreach,
+                    levels);
         if (nlost == 0) {
             rt.report(round, round, "  repair timings round");
             break;
