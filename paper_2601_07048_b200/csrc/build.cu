@@ -228,11 +228,19 @@ __device__ int warp_prune_staged(uint64_t* cand, int n, double alpha2, int R, co
             const int i2 = i + 32;
             const uint64_t c = cand[i];
             const uint64_t c2 = i2 < n ? cand[i2] : UMAX;
-            if (c != UMAX && c2 != UMAX) {
-                uint32_t d0, d1;
-                m.dist_staged2(rows, cn, i, i2, mi, d0, d1);
-                if (!(__dmul_rn(alpha2, M::value(d0)) > M::value((uint32_t)(c >> 32)))) cand[i] = UMAX;
-                if (!(__dmul_rn(alpha2, M::value(d1)) > M::value((uint32_t)(c2 >> 32)))) cand[i2] = UMAX;
+            const bool pair = c != UMAX && c2 != UMAX;
+            if (__any_sync(__activemask(), pair)) {
+                // one code path for the warp: single-survivor lanes run the pair routine
+                // with their row twice instead of diverging into the single routine
+                if (c != UMAX || c2 != UMAX) {
+                    const int ia = c != UMAX ? i : i2;
+                    const int ib = pair ? i2 : ia;
+                    uint32_t d0, d1;
+                    m.dist_staged2(rows, cn, ia, ib, mi, d0, d1);
+                    const uint64_t ca = c != UMAX ? c : c2;
+                    if (!(__dmul_rn(alpha2, M::value(d0)) > M::value((uint32_t)(ca >> 32)))) cand[ia] = UMAX;
+                    if (pair && !(__dmul_rn(alpha2, M::value(d1)) > M::value((uint32_t)(c2 >> 32)))) cand[i2] = UMAX;
+                }
             } else if (c != UMAX || c2 != UMAX) {
                 const int ii = c != UMAX ? i : i2;
                 const uint64_t cc = c != UMAX ? c : c2;
