@@ -124,7 +124,13 @@ __device__ __forceinline__ bool visit(uint32_t* tab, int hbits, uint32_t id, int
 #define JB_FAST_QB 6
 #endif
 #ifndef JB_FAST_MINB
-#define JB_FAST_MINB 10
+#define JB_FAST_MINB 12  // blocks/SM of the popcount kernel (48 warps; 13+ spills)
+#endif
+#ifndef JB_RQ_MINB
+#define JB_RQ_MINB 10  // blocks/SM of the bit-exact RaBitQ kernel
+#endif
+#ifndef JB_OTHER_MINB
+#define JB_OTHER_MINB 8  // blocks/SM of the exact-row kernels (smem-bound: staged rows)
 #endif
 constexpr int FAST_QB = JB_FAST_QB;   // query bit-planes of the popcount estimator
 
@@ -779,7 +785,7 @@ static int launch_search_kernel(SearchKernel kern, const SearchLayout& lay, cons
 // gains from 10 resident blocks; the float estimators keep 8.
 template <int SRC, int BITS, bool ALIGNED>
 static int launch_search(const jb_search_args& a, int hash_slots, cudaStream_t st) {
-    constexpr int MINB = SRC == JB_SRC_RABITQ_FAST ? JB_FAST_MINB : 8;
+    constexpr int MINB = SRC == JB_SRC_RABITQ_FAST ? JB_FAST_MINB : SRC == JB_SRC_RABITQ ? JB_RQ_MINB : JB_OTHER_MINB;
     const int L = a.beam_width;
     const SearchLayout lay = make_layout(SRC, a.dims, L, hash_slots, FAST_QB);
     if (a.degree_cap <= 32 && SRC == JB_SRC_RABITQ_FAST && BITS == 1) {
