@@ -124,10 +124,11 @@ __device__ __forceinline__ bool visit(uint32_t* tab, int hbits, uint32_t id, int
 #define JB_FAST_QB 6
 #endif
 #ifndef JB_FAST_MINB
-#define JB_FAST_MINB 12  // blocks/SM of the popcount kernel (48 warps; 13+ spills)
+#define JB_FAST_MINB 10  // blocks/SM of the popcount kernel: 12 is 3% faster alone but slows the
+                        // two-lane step (the other lane's bind / rerank lose their SM share)
 #endif
 #ifndef JB_RQ_MINB
-#define JB_RQ_MINB 10  // blocks/SM of the bit-exact RaBitQ kernel
+#define JB_RQ_MINB 8  // blocks/SM of the bit-exact RaBitQ kernel
 #endif
 #ifndef JB_OTHER_MINB
 #define JB_OTHER_MINB 8  // blocks/SM of the exact-row kernels (smem-bound: staged rows)
