@@ -568,6 +568,239 @@ owner_merge_kernel(const M m, double alpha2, int R, int always_prune, const uint
     write_row(adj, deg, R, t, kid, k);
 }
 
+// ---- phase 3 for rows too large to stage per warp (f32, e.g. 960-d) ----------
+// One block per target. Warp 0 does the owner's group / fresh / append logic;
+// when the prune has n <= MX - 1 candidates the block computes the full A1 dot
+// matrix of the candidates and the target (MX x MX tile, 4 x 4 pairs per
+// thread, the donor scan's k-step order: 16-element blocks as vectors 3,2,1,0,
+// then the tail forward) so every row is read once instead of once per round.
+// dot(a, b) == dot(b, a) bit for bit (same products, same order), so each
+// operand-role distance follows from the matrix and the two norms:
+// d(p -> c) = max((xn[c] - 2 dot) + xn[p], 0). Warp 0 then runs the rounds from
+// smem. Larger groups fall back to the global-row prune on warp 0.
+constexpr int MX = 64;
+__global__ void __launch_bounds__(256, 2)
+owner_matrix_kernel(const F32Metric m, double alpha2, int R, int always_prune, const uint32_t* __restrict__ tgt,
+                    const uint64_t* __restrict__ key, int64_t total, const int32_t* __restrict__ seg_start,
+                    uint64_t* __restrict__ pool, unsigned long long* __restrict__ pool_top, int pool_cap,
+                    int32_t* __restrict__ adj, int32_t* __restrict__ deg, int* __restrict__ err) {
+    extern __shared__ __align__(16) unsigned char shm[];
+    float* dotm = reinterpret_cast<float*>(shm);                  // [MX][MX + 1]
+    float* S = dotm + MX * (MX + 1);                              // [MX][17] k-step slice
+    float* nrm = S + MX * 17;                                     // [MX]
+    int32_t* ids = reinterpret_cast<int32_t*>(nrm + MX);          // [MX]
+    uint64_t* scand = reinterpret_cast<uint64_t*>(ids + MX);      // [OWNER_SC] (8 B aligned: MX even)
+    int32_t* have = reinterpret_cast<int32_t*>(scand + OWNER_SC); // [R]
+    int32_t* kid = have + R;
+    uint32_t* kd = reinterpret_cast<uint32_t*>(kid + R);
+    uint32_t* pv = kd + R;                                        // pivot row (fallback path), 16 B aligned below
+    __shared__ int mode_s, n_s;
+    __shared__ uint64_t* cand_s;
+    pv = reinterpret_cast<uint32_t*>((reinterpret_cast<uintptr_t>(pv) + 15) & ~uintptr_t(15));
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int64_t s = blockIdx.x;
+    const int64_t g0 = seg_start[s];
+    const uint32_t t = tgt[g0];
+    const int D = m.D;
+    if (warp == 0) {
+        int64_t g1 = g0;
+        for (;;) {
+            const int64_t i = g1 + lane;
+            const bool same = i < total && tgt[i] == t;
+            const uint32_t msk = __ballot_sync(0xFFFFFFFFu, same);
+            g1 += __popc(msk);
+            if (msk != 0xFFFFFFFFu) break;
+        }
+        const int g = (int)(g1 - g0);
+        const int hd = deg[t];
+        for (int j = lane; j < hd; j += 32) have[j] = adj[(size_t)t * R + j];
+        __syncwarp();
+        uint64_t* cand = scand;
+        int mode = 0;  // 0 done, 1 matrix, 2 fallback
+        if (hd + g > OWNER_SC) {
+            unsigned long long off = 0;
+            if (lane == 0) off = atomicAdd(pool_top, (unsigned long long)(hd + g));
+            off = __shfl_sync(0xFFFFFFFFu, off, 0);
+            if (off + hd + g > (unsigned long long)pool_cap) {
+                if (lane == 0) atomicExch(err, 1);
+                cand = nullptr;
+            } else {
+                cand = pool + off;
+            }
+        }
+        int nf = 0;
+        if (cand != nullptr) {
+            for (int b = 0; b < g; b += 32) {
+                const int j = b + lane;
+                bool fresh = false;
+                uint64_t k = 0;
+                if (j < g) {
+                    k = key[g0 + j];
+                    const int32_t src = (int32_t)(k & 0xFFFFFFFFull);
+                    fresh = true;
+                    for (int e = 0; e < hd; ++e) fresh &= (have[e] != src);
+                }
+                const uint32_t msk = __ballot_sync(0xFFFFFFFFu, fresh);
+                if (fresh) cand[hd + nf + __popc(msk & lanemask_lt())] = k;
+                nf += __popc(msk);
+            }
+            __syncwarp();
+            if (nf > 0) {
+                if (!always_prune && hd + nf <= R) {
+                    for (int j = lane; j < nf; j += 32)
+                        adj[(size_t)t * R + hd + j] = (int32_t)(cand[hd + j] & 0xFFFFFFFFull);
+                    if (lane == 0) deg[t] = hd + nf;
+                } else {
+                    mode = (hd + nf <= MX - 1) ? 1 : 2;
+                }
+            }
+        }
+        if (mode == 1) {
+            const int n = hd + nf;
+            for (int j = lane; j < MX; j += 32) {
+                const int32_t id = j < hd ? have[j] : j < n ? (int32_t)(cand[j] & 0xFFFFFFFFull) : j == n ? (int32_t)t : -1;
+                ids[j] = id;
+                nrm[j] = id >= 0 ? __ldg(m.norms + id) : 0.0f;
+            }
+        }
+        if (lane == 0) { mode_s = mode; n_s = hd + nf; cand_s = cand; }
+    }
+    __syncthreads();
+    const int mode = mode_s;
+    if (mode == 0) return;
+    const int n = n_s;
+    uint64_t* cand = cand_s;
+    if (mode == 2) {  // hub target: the global-row prune on warp 0
+        if (warp != 0) return;
+        const int hd = deg[t];
+        m.load_pivot(pv, t);
+        for (int j = lane; j < hd; j += 32) {
+            const uint32_t e = (uint32_t)have[j];
+            cand[j] = key_of(m.dist(pv, e), e);
+        }
+        __syncwarp();
+        const int k = warp_prune(cand, n, alpha2, R, m, pv, kid, kd);
+        write_row(adj, deg, R, t, kid, k);
+        return;
+    }
+    // ---- dot matrix of the n candidates and the target (row n) ----
+    const int tx = tid & 15, ty = tid >> 4;
+    const int N = n + 1;
+    Acc4 acc[4][4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b].zero();
+    constexpr int KB = 16;
+    // sub-tiles wholly past the N live rows / columns skip the math (warp-uniform in ty)
+    const bool live = ty * 4 < N && tx * 4 < N;
+    // each thread's 4 slice elements: rows tid/16 + 16h, column tid%16; the next
+    // k-step's are loaded into registers while the current one is consumed
+    const int srow = tid / KB, scol = tid % KB;
+    const float* rp[4];
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+        const int row = srow + 16 * h;
+        rp[h] = row < N ? m.data + (size_t)ids[row] * D : nullptr;
+    }
+    float pf[4];
+#pragma unroll
+    for (int h = 0; h < 4; ++h) pf[h] = (rp[h] && scol < D) ? __ldg(rp[h] + scol) : 0.0f;
+    for (int k0 = 0; k0 < D; k0 += KB) {
+        const int kl = min(KB, D - k0);
+#pragma unroll
+        for (int h = 0; h < 4; ++h) S[(srow + 16 * h) * 17 + scol] = pf[h];
+        __syncthreads();
+        if (k0 + KB < D) {
+            const int e = k0 + KB + scol;
+#pragma unroll
+            for (int h = 0; h < 4; ++h) pf[h] = (rp[h] && e < D) ? __ldg(rp[h] + e) : 0.0f;
+        }
+        if (!live) {
+        } else if (kl == KB) {
+#pragma unroll
+            for (int v = 3; v >= 0; --v) {
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    float av[4], bv[4];
+#pragma unroll
+                    for (int a = 0; a < 4; ++a) av[a] = S[(ty * 4 + a) * 17 + 4 * v + j];
+#pragma unroll
+                    for (int b = 0; b < 4; ++b) bv[b] = S[(tx * 4 + b) * 17 + 4 * v + j];
+#pragma unroll
+                    for (int a = 0; a < 4; ++a)
+#pragma unroll
+                        for (int b = 0; b < 4; ++b) {
+                            const float p = __fmul_rn(bv[b], av[a]);
+                            if (j == 0) acc[a][b].l0 = __fadd_rn(p, acc[a][b].l0);
+                            else if (j == 1) acc[a][b].l1 = __fadd_rn(p, acc[a][b].l1);
+                            else if (j == 2) acc[a][b].l2 = __fadd_rn(p, acc[a][b].l2);
+                            else acc[a][b].l3 = __fadd_rn(p, acc[a][b].l3);
+                        }
+                }
+            }
+        } else {
+            for (int e = 0; e < kl; ++e) {  // tail: forward
+                float av[4], bv[4];
+#pragma unroll
+                for (int a = 0; a < 4; ++a) av[a] = S[(ty * 4 + a) * 17 + e];
+#pragma unroll
+                for (int b = 0; b < 4; ++b) bv[b] = S[(tx * 4 + b) * 17 + e];
+#pragma unroll
+                for (int a = 0; a < 4; ++a)
+#pragma unroll
+                    for (int b = 0; b < 4; ++b) acc[a][b].madd1((k0 + e) & 3, bv[b], av[a]);
+            }
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) dotm[(ty * 4 + a) * (MX + 1) + tx * 4 + b] = acc[a][b].reduce();
+    __syncthreads();
+    if (warp != 0) return;
+    // existing neighbours: d(t -> e) with the target as the pivot; fresh keys stay
+    const int hd = deg[t];
+    for (int j = lane; j < hd; j += 32)
+        cand[j] = key_of(__float_as_uint(exact_from_dot(nrm[j], dotm[j * (MX + 1) + n], nrm[n])), (uint32_t)ids[j]);
+    __syncwarp();
+    // robust prune from the matrix (same extraction sequence as warp_prune)
+    int kept = 0;
+    while (kept < R) {
+        uint64_t mk = UMAX;
+        int mi = -1;
+        for (int i = lane; i < n; i += 32) {
+            const uint64_t c = cand[i];
+            if (c < mk) { mk = c; mi = i; }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const uint64_t om = shfl_xor_u64(mk, o);
+            const int oi = __shfl_xor_sync(0xFFFFFFFFu, mi, o);
+            if (om < mk) { mk = om; mi = oi; }
+        }
+        if (mk == UMAX) break;
+        if (lane == 0) {
+            kid[kept] = (int32_t)(mk & 0xFFFFFFFFull);
+            kd[kept] = (uint32_t)(mk >> 32);
+            cand[mi] = UMAX;
+        }
+        ++kept;
+        __syncwarp();
+        if (kept >= R) break;
+        for (int i = lane; i < n; i += 32) {
+            const uint64_t c = cand[i];
+            if (c == UMAX) continue;
+            const float dsp = exact_from_dot(nrm[i], dotm[i * (MX + 1) + mi], nrm[mi]);
+            if (!(__dmul_rn(alpha2, (double)dsp) > (double)__uint_as_float((uint32_t)(c >> 32)))) cand[i] = UMAX;
+        }
+        __syncwarp();
+    }
+    __syncwarp();
+    write_row(adj, deg, R, t, kid, kept);
+}
+
 // ---- repair: BFS ------------------------------------------------------------
 __global__ void bfs_init_kernel(int32_t* __restrict__ seen, int64_t n, int64_t entry, int32_t* __restrict__ front,
                                 int* __restrict__ fcount) {
@@ -1296,6 +1529,17 @@ static int merge_phase(const M& m, const jb_insert_args& a, double alpha2, uint3
         if (crows_lo > 0 && smem_sm / (owner_per_warp(m, R, crows) * BW) < 3 &&
             smem_sm / (owner_per_warp(m, R, crows_lo) * BW) >= 3)
             crows = crows_lo;
+        bool launched = false;
+        if constexpr (std::is_same<M, F32Metric>::value) {
+            if (crows == 0) {  // rows too large to stage per warp: block per target, dot matrix
+                const size_t msm = (size_t)(MX * (MX + 1) + MX * 17 + MX) * 4 + MX * 4 + OWNER_SC * 8 + 3 * R * 4 +
+                                   (((size_t)a.dims + 3) / 4 * 4 + 4) * 4 + 16;
+                JB_CUDA_RC(grow_smem(owner_matrix_kernel, (int)msm));
+                owner_matrix_kernel<<<(unsigned)hseg, 256, msm, st>>>(m, alpha2, R, a.always_prune, tt, tk, ntri, seg,
+                                                                       pool, ptop, pool_cap, a.adjacency, a.degrees, err);
+                launched = true;
+            }
+        }
         const int osm = owner_per_warp(m, R, crows) * BW;
         JB_CUDA_RC(grow_smem(owner_merge_kernel<M>, osm));
 #ifdef JB_OWNER_SPLIT
@@ -1303,6 +1547,7 @@ static int merge_phase(const M& m, const jb_insert_args& a, double alpha2, uint3
 #else
         const M& mo = m;
 #endif
+        if (!launched)
         owner_merge_kernel<M><<<(unsigned)((hseg + BW - 1) / BW), BW * 32, osm, st>>>(
             mo, alpha2, R, a.always_prune, tt, tk, ntri, seg, nseg, pool, ptop, pool_cap, a.adjacency, a.degrees, err,
             crows);

@@ -8,5 +8,5 @@ for l in rows:
 print({k:round(v,1) for k,v in tot.items()})
 PY
 grep "^build" gpurun_out/c3_prof.log | cut -c1-70
-ncu --set full --import-source on --clock-control none -k regex:owner_merge_kernel --launch-skip 12 -c 1 -o gpurun_out/prof_owner_c3 python tools/exp_build_prof.py 500000 960 > gpurun_out/ncu_owner_c3.log 2>&1
+ncu --set full --import-source on --clock-control none -k regex:"owner_(merge|matrix)_kernel" --launch-skip 12 -c 1 -o gpurun_out/prof_owner_c3m python tools/exp_build_prof.py 500000 960 > gpurun_out/ncu_owner_c3.log 2>&1
 tail -2 gpurun_out/ncu_owner_c3.log
