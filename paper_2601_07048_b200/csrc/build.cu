@@ -346,6 +346,200 @@ phase2_kernel(const M m, int64_t start, int64_t nb, double alpha2, int R, const 
     }
 }
 
+// Block (256 threads) A1 dot matrix of N <= 128 f32 rows ids[0..N): 64 x 64 tile
+// pairs (tI <= tJ; both orientations written, dot(a, b) == dot(b, a) bit for bit),
+// 4 x 4 pairs per thread, k-steps of 16 elements in A1 order (vectors 3,2,1,0,
+// then the tail forward), the next k-step prefetched into registers. S holds two
+// 64 x 17 slices. Ends with __syncthreads().
+__device__ void block_dot_matrix(const float* __restrict__ data, int D, const int32_t* ids, int N, float* S,
+                                 float* dotm, int ld) {
+    constexpr int KB = 16;
+    const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+    const int srow = tid / KB, scol = tid % KB;
+    const int nt = (N + 63) / 64;
+    for (int tI = 0; tI < nt; ++tI) {
+        for (int tJ = tI; tJ < nt; ++tJ) {
+            const int nA = min(64, N - tI * 64), nB = min(64, N - tJ * 64);
+            const bool same = tI == tJ;
+            float* SA = S;
+            float* SB = same ? S : S + 64 * 17;
+            const bool live = ty * 4 < nA && tx * 4 < nB;
+            float pa[4], pb[4];
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+                const int r = srow + 16 * h;
+                pa[h] = (r < nA && scol < D) ? __ldg(data + (size_t)ids[tI * 64 + r] * D + scol) : 0.0f;
+                pb[h] = (!same && r < nB && scol < D) ? __ldg(data + (size_t)ids[tJ * 64 + r] * D + scol) : 0.0f;
+            }
+            Acc4 acc[4][4];
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+                for (int b = 0; b < 4; ++b) acc[a][b].zero();
+            for (int k0 = 0; k0 < D; k0 += KB) {
+                const int kl = min(KB, D - k0);
+#pragma unroll
+                for (int h = 0; h < 4; ++h) {
+                    SA[(srow + 16 * h) * 17 + scol] = pa[h];
+                    if (!same) SB[(srow + 16 * h) * 17 + scol] = pb[h];
+                }
+                __syncthreads();
+                if (k0 + KB < D) {
+                    const int e = k0 + KB + scol;
+#pragma unroll
+                    for (int h = 0; h < 4; ++h) {
+                        const int r = srow + 16 * h;
+                        pa[h] = (r < nA && e < D) ? __ldg(data + (size_t)ids[tI * 64 + r] * D + e) : 0.0f;
+                        pb[h] = (!same && r < nB && e < D) ? __ldg(data + (size_t)ids[tJ * 64 + r] * D + e) : 0.0f;
+                    }
+                }
+                if (!live) {
+                } else if (kl == KB) {
+#pragma unroll
+                    for (int v = 3; v >= 0; --v) {
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            float av[4], bv[4];
+#pragma unroll
+                            for (int a = 0; a < 4; ++a) av[a] = SA[(ty * 4 + a) * 17 + 4 * v + j];
+#pragma unroll
+                            for (int b = 0; b < 4; ++b) bv[b] = SB[(tx * 4 + b) * 17 + 4 * v + j];
+#pragma unroll
+                            for (int a = 0; a < 4; ++a)
+#pragma unroll
+                                for (int b = 0; b < 4; ++b) {
+                                    const float p = __fmul_rn(bv[b], av[a]);
+                                    if (j == 0) acc[a][b].l0 = __fadd_rn(p, acc[a][b].l0);
+                                    else if (j == 1) acc[a][b].l1 = __fadd_rn(p, acc[a][b].l1);
+                                    else if (j == 2) acc[a][b].l2 = __fadd_rn(p, acc[a][b].l2);
+                                    else acc[a][b].l3 = __fadd_rn(p, acc[a][b].l3);
+                                }
+                        }
+                    }
+                } else {
+                    for (int e = 0; e < kl; ++e) {  // tail: forward
+                        float av[4], bv[4];
+#pragma unroll
+                        for (int a = 0; a < 4; ++a) av[a] = SA[(ty * 4 + a) * 17 + e];
+#pragma unroll
+                        for (int b = 0; b < 4; ++b) bv[b] = SB[(tx * 4 + b) * 17 + e];
+#pragma unroll
+                        for (int a = 0; a < 4; ++a)
+#pragma unroll
+                            for (int b = 0; b < 4; ++b) acc[a][b].madd1((k0 + e) & 3, bv[b], av[a]);
+                    }
+                }
+                __syncthreads();
+            }
+            if (live) {
+#pragma unroll
+                for (int a = 0; a < 4; ++a)
+#pragma unroll
+                    for (int b = 0; b < 4; ++b) {
+                        const int i = tI * 64 + ty * 4 + a, j = tJ * 64 + tx * 4 + b;
+                        if (ty * 4 + a < nA && tx * 4 + b < nB) {
+                            const float dv = acc[a][b].reduce();
+                            dotm[i * ld + j] = dv;
+                            if (!same) dotm[j * ld + i] = dv;
+                        }
+                    }
+            }
+        }
+    }
+    __syncthreads();
+}
+
+// Phase 2 for f32 rows too large to stage per warp: one block per new vertex,
+// the trace's dot matrix (N <= 128) once, then warp 0 prunes from it (same
+// extraction sequence as warp_prune) and emits the row and reverse triples.
+// Longer traces fall back to the global-row prune on warp 0.
+constexpr int MX2 = 128;
+__global__ void __launch_bounds__(256, 2)
+phase2_matrix_kernel(const F32Metric m, int64_t start, int64_t nb, double alpha2, int R,
+                     const int32_t* __restrict__ hops, const int32_t* __restrict__ tids,
+                     const uint32_t* __restrict__ tdst, int cap, int reverse_all, uint64_t* __restrict__ cand_all,
+                     int32_t* __restrict__ kept_ids, uint32_t* __restrict__ kept_d, int32_t* __restrict__ adj,
+                     int32_t* __restrict__ deg, uint32_t* __restrict__ tri_target, uint64_t* __restrict__ tri_key,
+                     int W) {
+    extern __shared__ __align__(16) unsigned char shp[];
+    float* dotm = reinterpret_cast<float*>(shp);                 // [MX2][MX2 + 1]
+    float* S = dotm + MX2 * (MX2 + 1);                           // [2][64][17]
+    float* nrm = S + 2 * 64 * 17;                                // [MX2]
+    int32_t* ids = reinterpret_cast<int32_t*>(nrm + MX2);        // [MX2]
+    uint32_t* pv = reinterpret_cast<uint32_t*>(ids + MX2);       // fallback pivot row (16 B aligned)
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int64_t xi = blockIdx.x;
+    const uint32_t x = (uint32_t)(start + xi);
+    const int h = min(hops[xi], cap);
+    uint64_t* cand = cand_all + xi * cap;
+    const int32_t* ti = tids + xi * cap;
+    const uint32_t* td = tdst + xi * cap;
+    int32_t* ki = kept_ids + xi * R;
+    uint32_t* kd = kept_d + xi * R;
+    const bool mat = h <= MX2;
+    if (mat) {
+        for (int j = tid; j < h; j += 256) {
+            ids[j] = ti[j];
+            nrm[j] = __ldg(m.norms + ti[j]);
+        }
+        __syncthreads();
+        block_dot_matrix(m.data, m.D, ids, h, S, dotm, MX2 + 1);
+    }
+    if (warp != 0) return;
+    for (int j = lane; j < h; j += 32) cand[j] = key_of(td[j], (uint32_t)ti[j]);
+    __syncwarp();
+    int k;
+    if (!mat) {
+        k = warp_prune(cand, h, alpha2, R, m, pv, ki, kd);
+    } else {
+        k = 0;
+        while (k < R) {
+            uint64_t mk = UMAX;
+            int mi = -1;
+            for (int i = lane; i < h; i += 32) {
+                const uint64_t c = cand[i];
+                if (c < mk) { mk = c; mi = i; }
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const uint64_t om = shfl_xor_u64(mk, o);
+                const int oi = __shfl_xor_sync(0xFFFFFFFFu, mi, o);
+                if (om < mk) { mk = om; mi = oi; }
+            }
+            if (mk == UMAX) break;
+            if (lane == 0) {
+                ki[k] = (int32_t)(mk & 0xFFFFFFFFull);
+                kd[k] = (uint32_t)(mk >> 32);
+                cand[mi] = UMAX;
+            }
+            ++k;
+            __syncwarp();
+            if (k >= R) break;
+            for (int i = lane; i < h; i += 32) {
+                const uint64_t c = cand[i];
+                if (c == UMAX) continue;
+                const float dsp = exact_from_dot(nrm[i], dotm[i * (MX2 + 1) + mi], nrm[mi]);
+                if (!(__dmul_rn(alpha2, (double)dsp) > (double)__uint_as_float((uint32_t)(c >> 32)))) cand[i] = UMAX;
+            }
+            __syncwarp();
+        }
+        __syncwarp();
+    }
+    write_row(adj, deg, R, x, ki, k);
+    uint32_t* tt = tri_target + xi * W;
+    uint64_t* tk = tri_key + xi * W;
+    const int ne = reverse_all ? h : k;
+    for (int j = lane; j < W; j += 32) {
+        if (j < ne) {
+            tt[j] = reverse_all ? (uint32_t)ti[j] : (uint32_t)ki[j];
+            tk[j] = key_of(reverse_all ? td[j] : kd[j], x);
+        } else {
+            tt[j] = NO_TARGET;
+            tk[j] = UMAX;
+        }
+    }
+}
+
 // ---- two_pass refinement prune (build.py:362-381) --------------------------
 // Per vertex x of the batch: candidates = its visited trace without x itself, plus
 // its current neighbours missing from the trace (distances d(x, e) with x as the
@@ -1676,8 +1870,21 @@ static int batch_insert_impl(const M& m, const jb_insert_args& a, cudaStream_t s
     // smem-staged candidate rows when a trace fits in ~26 KB per warp; longer traces
     // prune from L1/L2 (staging them would cost more occupancy than it saves)
     const int crows2 = staged_rows(m, cap, R, JB_P2_KB);
+    bool p2_done = false;
+    if constexpr (std::is_same<M, F32Metric>::value) {
+        if (crows2 == 0) {  // rows too large to stage per warp: block per vertex, dot matrix
+            const size_t psm = (size_t)(MX2 * (MX2 + 1) + 2 * 64 * 17 + MX2) * 4 + MX2 * 4 +
+                               (((size_t)a.dims + 3) / 4 * 4 + 4) * 4;
+            JB_CUDA_RC(grow_smem(phase2_matrix_kernel, (int)psm));
+            phase2_matrix_kernel<<<(unsigned)nb, 256, psm, st>>>(m, a.start, nb, alpha2, R, hops, tids, tdst, cap,
+                                                                 a.reverse_all_visited, cand, kid, kd, a.adjacency,
+                                                                 a.degrees, tt, tk, W);
+            p2_done = true;
+        }
+    }
     const int p2_smem = BW * 4 * vertex_warp_words(m, crows2);
     JB_CUDA_RC(grow_smem(phase2_kernel<M>, p2_smem));
+    if (!p2_done)
     phase2_kernel<M><<<(unsigned)((nb + BW - 1) / BW), BW * 32, p2_smem, st>>>(
         split_prune(m), a.start, nb, alpha2, R, hops, tids, tdst, cap, a.reverse_all_visited, cand, kid, kd, a.adjacency, a.degrees,
         tt, tk, W, crows2);
