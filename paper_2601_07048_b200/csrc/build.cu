@@ -1072,14 +1072,17 @@ __device__ __forceinline__ void topk_insert_all(uint64_t& t, uint64_t c, int fan
 constexpr int DT = 64;      // tile edge
 constexpr int FAN = 16;     // min(R, 16) donors, upper bound
 
+// RES: the 64 stranded rows stay resident in smem for the whole slice (D <= 256);
+// otherwise (high D) their k-step slices stream through smem beside the reachable ones.
+template <bool RES>
 __global__ void __launch_bounds__(256, 2)
 donor_scan_kernel(const float* __restrict__ data, const float* __restrict__ norms, int D, const int32_t* __restrict__ lost,
                   int nlost, const int32_t* __restrict__ reach, int nreach, int slices, int fan,
                   uint64_t* __restrict__ part) {
     extern __shared__ __align__(16) unsigned char dsh[];
     const int KB = 16;  // elements per k-step (one A1 block)
-    const int AS = D + 1;                                  // resident stranded tile row stride
-    float* Ares = reinterpret_cast<float*>(dsh);           // [DT][D+1]  stranded rows, whole slice
+    const int AS = RES ? D + 1 : KB + 1;                   // stranded tile row stride
+    float* Ares = reinterpret_cast<float*>(dsh);           // [DT][AS]   stranded rows (whole, or the k-step)
     float* Bs = Ares + DT * AS;                            // [DT][KB+1] reachable k-step
     float* dist = Bs + DT * (KB + 1);                      // [DT][DT+1]
     uint64_t* top = reinterpret_cast<uint64_t*>(dist + DT * (DT + 1) + ((DT * AS + DT * (KB + 1) + DT * (DT + 1)) & 1));
@@ -1091,9 +1094,11 @@ donor_scan_kernel(const float* __restrict__ data, const float* __restrict__ norm
     const int64_t r_begin = slice * per, r_end = (nreach < r_begin + per) ? (int64_t)nreach : r_begin + per;
     for (int i = tid; i < DT * FAN; i += 256) top[i] = UMAX;
     // the 64 stranded rows stay in smem for the whole slice
-    for (int i = tid; i < DT * D; i += 256) {
-        const int row = i / D, e = i % D;
-        Ares[row * AS + e] = (s0 + row < nlost) ? data[(size_t)lost[s0 + row] * D + e] : 0.f;
+    if (RES) {
+        for (int i = tid; i < DT * D; i += 256) {
+            const int row = i / D, e = i % D;
+            Ares[row * AS + e] = (s0 + row < nlost) ? data[(size_t)lost[s0 + row] * D + e] : 0.f;
+        }
     }
     __syncthreads();
     // reachable rows stream through a 64 x 16 smem tile; each thread prefetches its 4
@@ -1105,11 +1110,12 @@ donor_scan_kernel(const float* __restrict__ data, const float* __restrict__ norm
 #pragma unroll
             for (int b = 0; b < 4; ++b) acc[a][b].zero();
         // prefetch k-step 0
-        float pf[4];
+        float pf[4], pa[4];
 #pragma unroll
         for (int h = 0; h < 4; ++h) {
             const int i = tid + 256 * h, row = i / KB, e = i % KB;
             pf[h] = (e < min(KB, D) && r0 + row < r_end) ? __ldg(data + (size_t)reach[r0 + row] * D + e) : 0.f;
+            if (!RES) pa[h] = (e < min(KB, D) && s0 + row < nlost) ? __ldg(data + (size_t)lost[s0 + row] * D + e) : 0.f;
         }
         for (int k0 = 0; k0 < D; k0 += KB) {
             const int kl = min(KB, D - k0);
@@ -1117,6 +1123,7 @@ donor_scan_kernel(const float* __restrict__ data, const float* __restrict__ norm
             for (int h = 0; h < 4; ++h) {
                 const int i = tid + 256 * h, row = i / KB, e = i % KB;
                 Bs[row * (KB + 1) + e] = pf[h];
+                if (!RES) Ares[row * AS + e] = pa[h];
             }
             __syncthreads();
             if (k0 + KB < D) {  // next k-step's loads in flight during this step's math
@@ -1125,9 +1132,11 @@ donor_scan_kernel(const float* __restrict__ data, const float* __restrict__ norm
                 for (int h = 0; h < 4; ++h) {
                     const int i = tid + 256 * h, row = i / KB, e = i % KB;
                     pf[h] = (e < kn && r0 + row < r_end) ? __ldg(data + (size_t)reach[r0 + row] * D + k0 + KB + e) : 0.f;
+                    if (!RES)
+                        pa[h] = (e < kn && s0 + row < nlost) ? __ldg(data + (size_t)lost[s0 + row] * D + k0 + KB + e) : 0.f;
                 }
             }
-            const float* Ak = Ares + k0;
+            const float* Ak = RES ? Ares + k0 : Ares;
             if (kl == KB) {
                 // A1 order inside a 16-block: vectors 3,2,1,0; lane j = element % 4
 #pragma unroll
@@ -1569,15 +1578,22 @@ static int repair(const M& m, const jb_insert_args& a, int64_t n_active, int64_t
             slices = 1;
             const int rc = approx_donors(a, lost, nlost, n_active, entry, fan, bufs, st, part);
             if (rc != JB_OK) return rc;
-        } else if (std::is_same<M, F32Metric>::value && D <= 256) {  // tiled A1 scan on the f32 rows
+        } else if (std::is_same<M, F32Metric>::value) {  // tiled A1 scan on the f32 rows
+            const bool res = D <= 256;
             const int sblocks = (nlost + DT - 1) / DT;
             slices = std::max(1, std::min(128, 4 * sm_count_current() / sblocks));  // whole waves at 2 blocks/SM
             slices = (int)std::min<int64_t>(slices, std::max<int64_t>(1, (nreach + DT - 1) / DT));
             part = bufs.get<uint64_t>((size_t)slices * nlost * fan, st, _ce); JB_CUDA(_ce);
-            const size_t dsm = (size_t)(DT * (D + 1) + DT * 17 + DT * (DT + 1) + 1) * 4 + DT * FAN * 8;
-            JB_CUDA_RC(grow_smem(donor_scan_kernel, (int)dsm));
-            donor_scan_kernel<<<dim3(sblocks, slices), 256, dsm, st>>>(a.data, a.data_norms, D, lost, nlost, reach,
-                                                                      nreach, slices, fan, part);
+            const size_t dsm = (size_t)(DT * (res ? D + 1 : 17) + DT * 17 + DT * (DT + 1) + 1) * 4 + DT * FAN * 8;
+            if (res) {
+                JB_CUDA_RC(grow_smem(donor_scan_kernel<true>, (int)dsm));
+                donor_scan_kernel<true><<<dim3(sblocks, slices), 256, dsm, st>>>(a.data, a.data_norms, D, lost, nlost,
+                                                                                reach, nreach, slices, fan, part);
+            } else {
+                JB_CUDA_RC(grow_smem(donor_scan_kernel<false>, (int)dsm));
+                donor_scan_kernel<false><<<dim3(sblocks, slices), 256, dsm, st>>>(a.data, a.data_norms, D, lost, nlost,
+                                                                                 reach, nreach, slices, fan, part);
+            }
         } else {
             const int sblocks = (nlost + 7) / 8;
             slices = std::max(1, std::min(64, 8 * sm_count_current() / sblocks));

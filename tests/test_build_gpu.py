@@ -291,11 +291,12 @@ def test_repair_beam_width_validation():
         jb.BuildParams(repair_beam_width=-1)
 
 
-@pytest.mark.parametrize("D", [672, 700])
-def test_high_dim_owner_matrix_path_identical_to_oracle(D):
-    """Rows too large to stage per warp (R=8: D > ~660) take the block-per-target
-    dot-matrix owner merge; D=700 also covers the A1 tail (D % 16 != 0)."""
-    x = lowrank(1500, D, 16, 0.05, 95 + D)
+@pytest.mark.parametrize("D,kind", [(672, "lowrank"), (700, "lowrank"), (704, "gaussian")])
+def test_high_dim_owner_matrix_path_identical_to_oracle(D, kind):
+    """Rows too large to stage per warp (R=8: D > ~660) take the block dot-matrix
+    phase-2 prune and owner merge and the streamed-tile donor scan; D=700 also
+    covers the A1 tail (D % 16 != 0); iid Gaussian rows make repair bridge often."""
+    x = lowrank(1500, D, 16, 0.05, 95 + D) if kind == "lowrank" else gaussian(1500, D, 95 + D)
     og = vamana.build(x, R=8, L=16, alpha=1.2, max_batch=400)
     g = jb.build(jb.VectorDataset(x), jb.BuildParams(degree_cap=8, build_beam_width=16, alpha=1.2, max_batch=400))
     _same_graph(g, og.adj, og.deg, og.entry)
