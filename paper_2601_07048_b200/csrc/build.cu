@@ -773,6 +773,11 @@ owner_merge_kernel(const M m, double alpha2, int R, int always_prune, const uint
 // d(p -> c) = max((xn[c] - 2 dot) + xn[p], 0). Warp 0 then runs the rounds from
 // smem. Larger groups fall back to the global-row prune on warp 0.
 constexpr int MX = 64;
+#ifdef JB_NO_MATRIX
+constexpr bool kNoMatrix = true;  // dev A/B: warp kernels only
+#else
+constexpr bool kNoMatrix = false;
+#endif
 __global__ void __launch_bounds__(256, 2)
 owner_matrix_kernel(const F32Metric m, double alpha2, int R, int always_prune, const uint32_t* __restrict__ tgt,
                     const uint64_t* __restrict__ key, int64_t total, const int32_t* __restrict__ seg_start,
@@ -1691,6 +1696,23 @@ static int trace_search(const jb_insert_args& a, int64_t q0, int64_t nq, int64_t
     return JB_OK;
 }
 
+// Global-pool slots the owner of segment s takes: deg[t] + g when that exceeds the
+// OWNER_SC smem candidate slots (else 0). Summed to size the pool exactly (with
+// R = 64 nearly every target spills, so no fixed multiple of the triple count fits).
+__global__ void owner_pool_need_kernel(const uint32_t* __restrict__ tgt, int64_t total,
+                                       const int32_t* __restrict__ seg_start, int nseg,
+                                       const int32_t* __restrict__ deg, unsigned long long* __restrict__ need) {
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= nseg) return;
+    const int64_t g0 = seg_start[s];
+    const uint32_t t = tgt[g0];
+    int64_t g1 = s + 1 < nseg ? (int64_t)seg_start[s + 1] : g0 + 1;
+    if (s + 1 >= nseg)
+        while (g1 < total && tgt[g1] == t) ++g1;  // last segment: ends at the NO_TARGET tail
+    const int64_t c = (int64_t)deg[t] + (g1 - g0);
+    need[s] = c > OWNER_SC ? (unsigned long long)c : 0ull;
+}
+
 // Phase 3 (build.py:269-293): (target, dist, source) order via two stable radix
 // sorts of the reverse triples, segment heads, one owner warp per target.
 template <class M>
@@ -1725,7 +1747,22 @@ static int merge_phase(const M& m, const jb_insert_args& a, double alpha2, uint3
     JB_CUDA(cudaMemcpyAsync(&hseg, nseg, sizeof(int), cudaMemcpyDeviceToHost, st));
     JB_CUDA(cudaStreamSynchronize(st));
     if (hseg > 0) {
-        const int pool_cap = (int)std::min<int64_t>(2 * ntri + 1024, INT32_MAX);
+        int pool_cap = 1024;
+        {
+            BALLOC(need, unsigned long long, hseg);
+            BALLOC(need_sum, unsigned long long, 1);
+            owner_pool_need_kernel<<<(unsigned)((hseg + 255) / 256), 256, 0, st>>>(tt, ntri, seg, hseg, a.degrees, need);
+            JB_LAUNCH_CHECK();
+            size_t tb = 0;
+            cub::DeviceReduce::Sum(nullptr, tb, need, need_sum, hseg, st);
+            BALLOC(tmp, unsigned char, tb);
+            JB_CUDA(cub::DeviceReduce::Sum(tmp, tb, need, need_sum, hseg, st));
+            unsigned long long hneed = 0;
+            JB_CUDA(cudaMemcpyAsync(&hneed, need_sum, sizeof(hneed), cudaMemcpyDeviceToHost, st));
+            JB_CUDA(cudaStreamSynchronize(st));
+            if (hneed + 1024 > (unsigned long long)INT32_MAX) { set_error("phase 3: candidate pool too large"); return JB_EOVERFLOW; }
+            pool_cap = (int)(hneed + 1024);
+        }
         BALLOC(pool, uint64_t, pool_cap);
         BALLOC(ptop, unsigned long long, 1);
         BALLOC(err, int, 1);
@@ -1741,7 +1778,9 @@ static int merge_phase(const M& m, const jb_insert_args& a, double alpha2, uint3
             crows = crows_lo;
         bool launched = false;
         if constexpr (std::is_same<M, F32Metric>::value) {
-            if (crows == 0) {  // rows too large to stage per warp: block per target, dot matrix
+            // rows too large to stage per warp: block per target, dot matrix — when the
+            // candidate sets (R + a few fresh) fit the 64-row tile; else the warp kernel
+            if (crows == 0 && R + 16 <= MX - 1 && !kNoMatrix) {
                 const size_t msm = (size_t)(MX * (MX + 1) + MX * 17 + MX) * 4 + MX * 4 + OWNER_SC * 8 + 3 * R * 4 +
                                    (((size_t)a.dims + 3) / 4 * 4 + 4) * 4 + 16;
                 JB_CUDA_RC(grow_smem(owner_matrix_kernel, (int)msm));
@@ -1888,7 +1927,9 @@ static int batch_insert_impl(const M& m, const jb_insert_args& a, cudaStream_t s
     const int crows2 = staged_rows(m, cap, R, JB_P2_KB);
     bool p2_done = false;
     if constexpr (std::is_same<M, F32Metric>::value) {
-        if (crows2 == 0) {  // rows too large to stage per warp: block per vertex, dot matrix
+        // rows too large to stage per warp: block per vertex, dot matrix — when the
+        // traces (about 1.1 x L_build) fit 128 rows; else the warp kernel
+        if (crows2 == 0 && a.build_beam_width <= 96 && !kNoMatrix) {
             const size_t psm = (size_t)(MX2 * (MX2 + 1) + 2 * 64 * 17 + MX2) * 4 + MX2 * 4 +
                                (((size_t)a.dims + 3) / 4 * 4 + 4) * 4;
             JB_CUDA_RC(grow_smem(phase2_matrix_kernel, (int)psm));

@@ -300,3 +300,14 @@ def test_high_dim_owner_matrix_path_identical_to_oracle(D, kind):
     og = vamana.build(x, R=8, L=16, alpha=1.2, max_batch=400)
     g = jb.build(jb.VectorDataset(x), jb.BuildParams(degree_cap=8, build_beam_width=16, alpha=1.2, max_batch=400))
     _same_graph(g, og.adj, og.deg, og.entry)
+
+
+def test_default_params_build_at_scale():
+    """beamann's default BuildParams (R=64, L=128): with full degree-64 rows almost
+    every touched target spills its candidates to the global pool, which is sized
+    from the exact per-segment need (a fixed multiple of the triple count overflowed)."""
+    x = lowrank(120_000, 32, 8, 0.05, 97)
+    g = jb.build(jb.VectorDataset(x), jb.BuildParams())
+    g.validate()
+    assert g.active_count == len(x)
+    assert (g.degrees[: len(x)] > 0).all()
