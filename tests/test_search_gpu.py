@@ -437,3 +437,17 @@ def test_bench_scale_rabitq_fit_and_bind_identical_to_reference():
     assert h(idx.meta) == ref["meta"]
     rot, qa, qs = idx.bind(q)
     assert (h(rot), h(qa), h(qs)) == (ref["rotated"], ref["qadd"], ref["sumq"])
+
+
+def test_default_params_r64_build_and_search_match_oracle():
+    """beamann's defaults (R=64, L=128): the build is identical to the oracle's and
+    the two-chunk (R > 32) hop of the search kernel gives identical frontiers."""
+    x = lowrank(3000, 24, 8, 0.05, 99)
+    q = lowrank(150, 24, 8, 0.05, 98)
+    og = vamana.build(x, R=64, L=128, alpha=1.2, max_batch=100_000)
+    g = jb.build(jb.VectorDataset(x), jb.BuildParams())
+    assert g.entry_point == og.entry
+    np.testing.assert_array_equal(g.degrees[:3000], og.deg[:3000])
+    np.testing.assert_array_equal(g.adjacency[:3000], og.adj[:3000])
+    ores = osearch.beam_search(og.adj, og.active, og.entry, osearch.ExactSource(x, q), len(q), 128)
+    _oracle_check(jb.run_beam_searches(g, jb.VectorDataset(x), q, 128), ores)
