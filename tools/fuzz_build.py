@@ -15,9 +15,9 @@ rng = np.random.default_rng(int(sys.argv[1]) if len(sys.argv) > 1 else 0)
 cases = int(sys.argv[2]) if len(sys.argv) > 2 else 20
 bad = 0
 for c in range(cases):
-    n = int(rng.integers(200, 2500))
-    D = int(rng.choice([3, 8, 20, 33, 64, 96, 128]))
-    R = int(rng.choice([4, 9, 24, 33, 40, 64, 100]))
+    n = int(rng.integers(200, int(os.environ.get("FUZZ_NMAX", "2500"))))
+    D = int(rng.choice([int(v) for v in os.environ.get("FUZZ_DIMS", "3,8,20,33,64,96,128").split(",")]))
+    R = int(rng.choice([int(v) for v in os.environ.get("FUZZ_R", "4,9,24,33,40,64,100").split(",")]))
     L = int(max(R, rng.choice([8, 16, 48, 100, 160])))
     alpha = float(rng.choice([1.0, 1.1, 1.2, 1.5]))
     mb = int(rng.choice([50, 300, 1000, 100_000]))

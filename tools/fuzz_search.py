@@ -17,10 +17,10 @@ rng = np.random.default_rng(int(sys.argv[1]) if len(sys.argv) > 1 else 0)
 cases = int(sys.argv[2]) if len(sys.argv) > 2 else 20
 bad = 0
 for c in range(cases):
-    n = int(rng.integers(300, 3000))
-    D = int(rng.choice([5, 16, 33, 64, 100, 128]))
-    R = int(rng.choice([6, 16, 32, 48, 64]))
-    L = int(rng.choice([1, 7, 32, 64, 200, 512]))
+    n = int(rng.integers(300, int(os.environ.get("FUZZ_NMAX", "3000"))))
+    D = int(rng.choice([int(v) for v in os.environ.get("FUZZ_DIMS", "5,16,33,64,100,128").split(",")]))
+    R = int(rng.choice([int(v) for v in os.environ.get("FUZZ_R", "6,16,32,48,64").split(",")]))
+    L = int(rng.choice([int(v) for v in os.environ.get("FUZZ_L", "1,7,32,64,200,512").split(",")]))
     k = min(L, int(rng.choice([1, 5, 10, 50])))
     bits = int(rng.choice([1, 2, 4, 8]))
     x = gaussian(n, D, c) if rng.random() < 0.5 else lowrank(n, D, min(D, 8), 0.05, c)
