@@ -23,6 +23,8 @@ for c in range(cases):
     mb = int(rng.choice([50, 300, 1000, 100_000]))
     tp = bool(rng.random() < 0.25)
     x = gaussian(n, D, c) if rng.random() < 0.5 else lowrank(n, D, min(D, 8), 0.05, c)
+    if os.environ.get("FUZZ_KIND") == "u8":  # u8 rows (integer distances)
+        x = np.clip(np.rint((x - x.min()) / (x.max() - x.min()) * 255.0), 0, 255).astype(np.uint8)
     t = time.time()
     oerr = None
     try:
