@@ -4,29 +4,36 @@
     python -m torch.distributed.run --nnodes=1 --nproc-per-node N --master-addr 127.0.0.1 \
         --master-port P bench.py --gpus N ...
 
-Workload (per GPU shard): 1M x 128 f32 low-rank synthetic rows (SURVEY.md Appendix B:
-d_int=16, noise 0.05), Vamana R=32, L_build=64, alpha=1.2 built on device, RaBitQ
-1-bit codes (seed 1) + fp32 rerank of the full beam, 10K queries, k=10. The beam
-width L* is the smallest of a sweep whose recall@10 (reference recall_at_k
-semantics, exact f64 ground truth) reaches 0.95; a step is one search of the
-10K-query batch at L* (bind + search + rerank kernels). `value` is device-timed
-with inputs resident in HBM (L2 flushed between steps, outside the timed
-events); `e2e` is the public API `search_knn_batch` with host queries in and host
-ids/dists out. N>1: contiguous 1M-row shards per rank, queries broadcast over
+Workload (per GPU shard): 1M x 128 f32 low-rank synthetic rows (workload.lowrank,
+SURVEY.md Appendix B: d_int=16, noise 0.05), Vamana R=32, L_build=64, alpha=1.2,
+max_batch=100K; RaBitQ 1-bit codes (seed 1) + fp32 rerank of the full beam, 10K
+queries, k=10. The beam width L* is the smallest of a sweep whose recall@10
+(reference recall_at_k semantics, exact f64 ground truth) reaches 0.95; a step is
+one search of the 10K-query batch at L* (bind + search + rerank).
+
+--impl b200 (default): everything on the GPU through the product library. `value`
+is device-timed with inputs resident in HBM (L2 flushed between steps, outside the
+timed events); `e2e` is the public API `search_knn_batch` with host queries in and
+host ids/dists out. N>1: contiguous 1M-row shards per rank, queries broadcast over
 NCCL, per-shard top-k all-gathered and merged on device; a unit is one
 (query, shard) search, so per-GPU work is fixed (weak scaling).
 
---impl reference times the reference algorithm on the host CPU (the numpy oracle
-port, every host core via forked workers) on the same index and L*; the index
-itself is built on the GPU as untimed setup (the CPU reference would need days).
+--impl reference: the reference's algorithm on the host CPU only. This process
+never imports the product package and never touches the GPU: it builds the same
+1M index with the C restatement of beamann's batch_insert (oracle/c/jbo.c, every
+host core; its graph hash equals the GPU arm's), fits RaBitQ with the numpy
+restatement of beamann's fit, computes the ground truth on the CPU, calibrates L*
+the same way, and times the reference search path (C port, all host threads;
+the numpy port's 1-process and all-process figures are reported beside it). Its
+`value` is the fastest of the three CPU variants.
 """
 
 from __future__ import annotations
 
 import argparse
+import hashlib
 import json
 import os
-import subprocess
 import sys
 import threading
 import time
@@ -36,7 +43,10 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+import workload  # noqa: E402  (numpy only; shared by both arms)
+
 SWEEP = (16, 24, 32, 48, 64, 80, 96, 104, 112, 120, 128, 144, 160, 192, 256, 384, 512, 768, 1024)
+INDEX = {"R": 32, "L_build": 64, "alpha": 1.2, "max_batch": 100000}
 
 
 def log(*a):
@@ -57,13 +67,246 @@ def _args():
     p.add_argument("--bits", type=int, default=1)
     p.add_argument("--target", type=float, default=0.95)
     p.add_argument("--beam", type=int, default=0, help="skip the sweep and use this L")
-    p.add_argument("--cpu-seconds", type=float, default=12.0)
+    p.add_argument("--stream-rows", dest="stream", type=int, default=20_000,
+                   help="rows of the streaming batch_insert compared with the CPU port (0 = skip)")
+    p.add_argument("--cpu-seconds", type=float, default=6.0, help="per numpy-port CPU sample")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--out", default="")
     p.add_argument("--hash-slots", type=int, default=0, help="visited-table slots per query (0 = library default)")
     p.add_argument("--estimator", default="auto", choices=["auto", "reference", "popcount"],
                    help="RaBitQ estimator; auto times both and reports the faster at the recall target")
     return p.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# shared by both arms
+
+
+def _data(args, rank: int = 0):
+    x = workload.lowrank(args.n, args.dim, seed=1 + rank, d_int=16, noise=0.05, basis_seed=0)
+    q = workload.lowrank(args.nq, args.dim, seed=1_000_003, d_int=16, noise=0.05, basis_seed=0)
+    return x, q
+
+
+def _stream_rows(args):
+    return workload.lowrank(args.stream, args.dim, seed=777_001, d_int=16, noise=0.05, basis_seed=0)
+
+
+def _graph_sha(adj: np.ndarray, deg: np.ndarray, active: int, entry: int) -> str:
+    h = hashlib.sha256()
+    h.update(np.ascontiguousarray(adj[:active], dtype=np.int32).tobytes())
+    h.update(np.ascontiguousarray(deg[:active], dtype=np.int32).tobytes())
+    h.update(np.int64(entry).tobytes())
+    return h.hexdigest()[:16]
+
+
+def _cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def _recall(ids, gt_i, gt_d, k):
+    from oracle import knn as oknn  # recall_at_k semantics (reference bench.py:44-66)
+
+    return oknn.recall_at_k(ids, gt_i, gt_d, k)
+
+
+def _config(args, world, L):
+    """Identical in both arms (same workload, same L*)."""
+    return {"workload": f"SIFT-1M-shaped synthetic {args.n}x{args.dim} low-rank (d_int=16, noise 0.05) "
+                        f"per shard, RaBitQ {args.bits}-bit + fp32 rerank, {args.nq} queries, k={args.k}",
+            "index": dict(INDEX), "beam_width": L, "shards": world, "parallelism": f"shard{world}",
+            "l2": "flushed between timed steps (256 MB write, outside the events)"}
+
+
+def _json_base(args, world, L):
+    return {
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "metric": "QPS at recall@10=0.95", "unit": "queries/s", "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": _config(args, world, L),
+    }
+
+
+# ---------------------------------------------------------------------------
+# reference arm (CPU only; never imports paper_2601_07048_b200)
+
+
+def _np_search_task(payload):
+    """numpy oracle port of beamann's search path: bind, lockstep RaBitQ search, rerank, top-k."""
+    from oracle import rabitq as orq
+    from oracle import search as osr
+
+    (adj, active, entry, codes, meta, bits, dims, centroid, seed, x, qs, L, k) = payload
+    rot, qadd, sumq = orq.bind(qs, centroid, bits, seed)
+    src = orq.QuantSource(codes, meta, bits, dims, rot, qadd, sumq)
+    res = osr.beam_search(adj, active, entry, src, len(qs), L)
+    ids, _ = osr.topk(res, k, queries=qs, rerank_data=x)
+    return np.asarray(ids)
+
+
+_SHARED = {}
+
+
+def _np_task(bounds):
+    lo, hi = bounds
+    s = _SHARED
+    return _np_search_task((s["adj"], s["active"], s["entry"], s["codes"], s["meta"], s["bits"], s["dims"],
+                            s["centroid"], s["seed"], s["x"], s["q"][lo:hi], s["L"], s["k"]))
+
+
+def _np_search_sample(shared: dict, nq: int, procs: int, seconds: float):
+    """Time the numpy port on a bounded query sample (~`seconds`); returns (n, elapsed, ids)."""
+    import multiprocessing as mp
+
+    _SHARED.clear()
+    _SHARED.update(shared)
+    t0 = time.perf_counter()
+    _np_task((0, 40))
+    per_q = (time.perf_counter() - t0) / 40
+    n = int(max(40, min(nq, seconds / per_q * max(procs, 1) * 0.8)))
+    n = max(procs, n - n % max(procs, 1))
+    if procs <= 1:
+        t0 = time.perf_counter()
+        ids = _np_task((0, n))
+        return n, time.perf_counter() - t0, ids
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    cuts = np.linspace(0, n, procs + 1).astype(int)
+    with mp.get_context("fork").Pool(procs) as pool:
+        pool.map(_np_task, [(0, 4)] * procs)  # fork + import warm-up
+        t0 = time.perf_counter()
+        parts = pool.map(_np_task, list(zip(cuts[:-1], cuts[1:])))
+        el = time.perf_counter() - t0
+    return n, el, np.concatenate(parts)
+
+
+def _c_knn(g, quant, x, q, L, k, threads):
+    """The C port of beamann's search_knn_batch path: bind (numpy, as beamann), lockstep
+    RaBitQ search, exact rerank + top-k."""
+    from oracle import cref
+
+    keys, _, _ = cref.search_rabitq(g.adj, g.active, g.entry, quant, q, L, threads=threads)
+    return cref.rerank_topk(x, q, cref.frontier_ids(keys), k, threads=threads)
+
+
+def reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return  # under torchrun, rank 0 alone runs the CPU reference
+    from oracle import cref, vamana
+
+    threads = os.cpu_count() or 1
+    t0 = time.perf_counter()
+    x, q = _data(args)
+    t_gen = time.perf_counter() - t0
+    rows = cref.Rows(x, threads)
+    t0 = time.perf_counter()
+    g = cref.build(x, INDEX["R"], INDEX["L_build"], INDEX["alpha"], INDEX["max_batch"], threads=threads, rows=rows)
+    t_build = time.perf_counter() - t0
+    sha = _graph_sha(g.adj, g.deg, g.active, g.entry)
+    log(f"[reference] C-port build {t_build:.1f}s ({args.n / t_build:.0f} inserts/s, {threads} threads) graph {sha}")
+    t0 = time.perf_counter()
+    quant = cref.Quantized.fit(x, args.bits, 1)
+    t_fit = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    gt_i, gt_d = cref.exact_knn(x, q, 100, threads=threads)
+    gt_d = gt_d.astype(np.float32)
+    log(f"[reference] fit {t_fit:.1f}s ground truth {time.perf_counter() - t0:.1f}s")
+
+    pts, L = [], None
+    for Lc in ((args.beam,) if args.beam else SWEEP):
+        ids, _ = _c_knn(g, quant, x, q, Lc, args.k, threads)
+        r = _recall(ids, gt_i, gt_d, args.k)
+        pts.append({"L": Lc, "recall": round(r, 4)})
+        log(f"[reference] sweep L={Lc} recall@{args.k}={r:.4f}")
+        if r >= args.target:
+            L = Lc
+            break
+    L = L or pts[-1]["L"]
+
+    times = []
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        ids_c, _ = _c_knn(g, quant, x, q, L, args.k, threads)
+        times.append(time.perf_counter() - t0)
+    tt = times[args.warmup:]
+    c_value = args.nq * len(tt) / sum(tt)
+
+    shared = dict(adj=g.adj, active=g.active, entry=g.entry, codes=quant.codes, meta=quant.meta, bits=args.bits,
+                  dims=args.dim, centroid=quant.centroid, seed=1, x=x, q=q, L=L, k=args.k)
+    variants = {"c_port_threads": {"value": round(c_value, 1), "cores": threads,
+                                   "sample": f"all {args.nq} queries per step, {args.steps} timed steps"}}
+    n1, e1, ids1 = _np_search_sample(shared, args.nq, 1, args.cpu_seconds)
+    variants["numpy_port_1proc"] = {"value": round(n1 / e1, 1), "cores": 1, "sample": f"first {n1} queries",
+                                    "ids_identical_to_c_port": bool(np.array_equal(ids1, ids_c[:n1]))}
+    nP, eP, idsP = _np_search_sample(shared, args.nq, threads, args.cpu_seconds)
+    variants["numpy_port_procs"] = {"value": round(nP / eP, 1), "cores": threads,
+                                    "sample": f"first {nP} queries over {threads} forked processes",
+                                    "ids_identical_to_c_port": bool(np.array_equal(idsP, ids_c[:nP]))}
+    best = max(variants, key=lambda v: variants[v]["value"])
+    value = variants[best]["value"]
+    log(f"[reference] L={L} " + ", ".join(f"{v} {variants[v]['value']:.0f} q/s" for v in variants))
+
+    inserts = {"bulk_build": {"inserts_per_s": round(args.n / t_build, 1), "cores": threads, "kind": "port",
+                              "graph_sha": sha, "sample": f"whole {args.n}-row build, C port"}}
+    if args.stream:
+        xs = _stream_rows(args)
+        xa = np.concatenate([x, xs])
+        gs = cref.Graph(args.n + args.stream, INDEX["R"])
+        gs.adj[:args.n], gs.deg[:args.n], gs.active, gs.entry = g.adj, g.deg, g.active, g.entry
+        rows2 = cref.Rows(xa, threads)
+        t0 = time.perf_counter()
+        cref.batch_insert(gs, rows2, args.n, args.n + args.stream, INDEX["L_build"], INDEX["alpha"], threads=threads)
+        t_s = time.perf_counter() - t0
+        inserts["stream_batch"] = {"inserts_per_s": round(args.stream / t_s, 1), "cores": threads, "kind": "port",
+                                   "graph_sha": _graph_sha(gs.adj, gs.deg, gs.active, gs.entry),
+                                   "sample": f"one {args.stream}-row batch_insert into the {args.n}-row graph, C port"}
+        # numpy port (beamann's own batch_insert restated): a bounded batch into the same graph;
+        # per-insert rate extrapolated from this batch size
+        nb = 300
+        vg = vamana.Graph(args.n + nb, INDEX["R"])
+        vg.adj[:args.n], vg.deg[:args.n], vg.active, vg.entry = g.adj, g.deg, g.active, g.entry
+        xv = np.ascontiguousarray(xa[:args.n + nb])
+        t0 = time.perf_counter()
+        vamana.batch_insert(vg, xv, args.n, args.n + nb, INDEX["R"], INDEX["L_build"], INDEX["alpha"])
+        t_v = time.perf_counter() - t0
+        cg = cref.Graph(args.n + nb, INDEX["R"])
+        cg.adj[:args.n], cg.deg[:args.n], cg.active, cg.entry = g.adj, g.deg, g.active, g.entry
+        cref.batch_insert(cg, cref.Rows(xv, threads), args.n, args.n + nb, INDEX["L_build"], INDEX["alpha"],
+                          threads=threads)
+        inserts["numpy_port_1proc"] = {"inserts_per_s": round(nb / t_v, 1), "cores": 1, "kind": "port",
+                                       "extrapolated": True,
+                                       "sample": f"one {nb}-row batch_insert into the {args.n}-row graph, numpy port",
+                                       "identical_to_c_port": bool(np.array_equal(vg.adj, cg.adj))}
+        log(f"[reference] inserts: " + ", ".join(f"{k} {v['inserts_per_s']:.0f}/s" for k, v in inserts.items()))
+
+    out = _json_base(args, 1, L)
+    out.update({
+        "impl": "reference", "value": value, "ms_per_step": round(1e3 * args.nq / value, 2),
+        "cpu_baseline": {"value": value, "unit": "queries/s", "cores": variants[best]["cores"], "kind": "port",
+                         "cpu_model": _cpu_model(), "host_threads": threads,
+                         "sample": f"{best}: {variants[best]['sample']}"},
+        "e2e": {"value": value, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "variants": variants, "inserts": inserts, "recall_at_10": next(p["recall"] for p in pts if p["L"] == L),
+        "sweep": pts, "setup_s": {"gen": round(t_gen, 1), "build": round(t_build, 1), "fit": round(t_fit, 1)},
+        "note": "reference algorithm restated (oracle/: C port pinned to the reference's fixtures, numpy port); "
+                "CPU only, no GPU, product package not imported",
+    })
+    line = json.dumps(out)
+    print(line, flush=True)
+    if args.out:
+        with open(args.out, "w") as fh:
+            fh.write(line + "\n")
+
+
+# ---------------------------------------------------------------------------
+# B200 arm
 
 
 class Clocks:
@@ -127,15 +370,17 @@ def _peaks():
         return 6650.0, "fallback"
 
 
-def _traffic(workload: str):
+def _ncu_record(workload_key: str):
+    """Per-launch DRAM bytes + warp instructions of the search kernel from the committed
+    ncu --set full capture of the same launch (profiles/search_kernel_traffic.json)."""
     try:
         with open(os.path.join(ROOT, "profiles", "search_kernel_traffic.json")) as fh:
             t = json.load(fh)
-        if t.get("workload") == workload:
-            return t.get("dram_bytes_per_launch")
+        if t.get("workload") == workload_key:
+            return t
     except Exception:
         pass
-    return None
+    return {}
 
 
 def _dist():
@@ -161,39 +406,29 @@ def _dist():
     return world, rank, local
 
 
-def _gt_device(x_dev, q_dev, k: int):
-    """Exact top-k ground truth on the GPU (jb_exact_knn: f64 scores, ties by id,
-    oracle.exact_knn semantics) as (int64 ids, f64 dists) tensors. Measurement only."""
-    import paper_2601_07048_b200 as jb
-
-    i, d = jb.measure.exact_knn_device(x_dev, q_dev, k)
-    return i.long(), d.double()
-
-
 def _setup(args, world, rank):
-    """Data, device build, RaBitQ fit, ground truth (merged across shards), sweep."""
+    """Data, device build, RaBitQ fit, ground truth (merged across shards)."""
+    import importlib
+
     import torch
 
     import paper_2601_07048_b200 as jb
 
     t0 = time.perf_counter()
     shard_start = rank * args.n
-    x = jb.gen_lowrank(args.n, args.dim, seed=1 + rank, d_int=16, noise=0.05, basis_seed=0)
-    q = jb.gen_lowrank(args.nq, args.dim, seed=1_000_003, d_int=16, noise=0.05, basis_seed=0)
+    x, q = _data(args, rank)
     ds = jb.VectorDataset(x)
     ds.device()
     torch.cuda.synchronize()
     t_gen = time.perf_counter() - t0
 
-    params = jb.BuildParams(degree_cap=32, build_beam_width=64, alpha=1.2, max_batch=100_000)
+    params = jb.BuildParams(degree_cap=INDEX["R"], build_beam_width=INDEX["L_build"], alpha=INDEX["alpha"],
+                            max_batch=INDEX["max_batch"])
     # untimed warm-up build (first-call kernel attributes; the stream-ordered pool grows to the
     # size of a max_batch=100K insert batch, which a production process has done long before)
-    jb.build(jb.VectorDataset(x[: min(args.n, 250_000)]), params)  # reaches 100K batches: pool grown
+    jb.build(jb.VectorDataset(x[: min(args.n, 250_000)]), params)
     torch.cuda.synchronize()
-    import importlib
-
     jbuild = importlib.import_module("paper_2601_07048_b200.build")  # the package re-exports build()
-
     jbuild.WORK[:] = 0
     t0 = time.perf_counter()
     graph = jb.build(ds, params)
@@ -205,11 +440,9 @@ def _setup(args, world, rank):
     torch.cuda.synchronize()
     t_fit = time.perf_counter() - t0
     q_dev = torch.from_numpy(q).cuda()
-    gt_i, gt_d = _gt_device(ds.device().x, q_dev, 100)
-    gt_i += shard_start
+    gt_i, gt_d = jb.measure.exact_knn_device(ds.device().x, q_dev, 100)
+    gt_i, gt_d = gt_i.long() + shard_start, gt_d.double()
     if world > 1:
-        import torch.distributed as dist
-
         from paper_2601_07048_b200 import comm
 
         all_i, all_d = comm.all_gather(gt_i), comm.all_gather(gt_d)
@@ -220,9 +453,9 @@ def _setup(args, world, rank):
         o = torch.argsort(cd, dim=1, stable=True)[:, :100]
         gt_i, gt_d = torch.gather(ci, 1, o), torch.gather(cd, 1, o)
     log(f"gen {t_gen:.1f}s build {t_build:.1f}s ({args.n / t_build:.0f} inserts/s) fit {t_fit:.2f}s")
-    gt = jb.measure.GroundTruth(gt_i.cpu().numpy().astype(np.int64), gt_d.cpu().numpy().astype(np.float32))
-    return dict(jb=jb, x=x, q=q, ds=ds, graph=graph, idx=idx, q_dev=q_dev, gt=gt, shard_start=shard_start,
-                t_gen=t_gen, t_build=t_build, t_fit=t_fit, params=params, work=work)
+    return dict(jb=jb, x=x, q=q, ds=ds, graph=graph, idx=idx, q_dev=q_dev, gt_i=gt_i.cpu().numpy(),
+                gt_d=gt_d.cpu().numpy().astype(np.float32), shard_start=shard_start, t_gen=t_gen, t_build=t_build,
+                t_fit=t_fit, params=params, work=work)
 
 
 def _insert_roofline(S, args, peak):
@@ -232,7 +465,7 @@ def _insert_roofline(S, args, peak):
     candidate; phase 3: each touched target's R existing rows plus one row per
     reverse triple (upper bound: ~all targets re-prune at R=32); row writes
     4R per new vertex and touched target. Repair scans are not counted."""
-    w, D, R = S["work"], args.dim, 32
+    w, D, R = S["work"], args.dim, INDEX["R"]
     row = 4 * D + 4
     b = (w["search_hops"] * (4 * R + 4) + w["search_evals"] * row + args.n * 4 * D
          + w["prune_candidates"] * row
@@ -252,23 +485,21 @@ def _search_fn(S, world, L, k, est="reference"):
         return lambda qd: jb.search_knn_batch_device(S["graph"], S["idx"], qd, sp, exact_data=S["ds"])
     from paper_2601_07048_b200 import shard
 
-    return lambda qd: shard.sharded_knn(
-        lambda qq: jb.search_knn_batch_device(S["graph"], S["idx"], qq, sp, exact_data=S["ds"]), qd, k,
-        S["shard_start"], device=qd.device)
+    si = shard.ShardedIndex(S["graph"], S["ds"], S["shard_start"], rabitq=S["idx"])
+    return lambda qd: si.search_knn_batch_device(qd, sp, nq=qd.shape[0])
 
 
 def _calibrate(S, args, world, est="reference"):
     """Smallest L of the sweep reaching the recall target (recall_at_k semantics)."""
     import torch
 
-    jb = S["jb"]
     pts = []
     chosen = None
     widths = (args.beam,) if args.beam else SWEEP
     for L in widths:
         ids, _ = _search_fn(S, world, L, args.k, est)(S["q_dev"])
         torch.cuda.synchronize()
-        r = jb.measure.recall_at_k(ids.cpu().numpy(), S["gt"], args.k)
+        r = _recall(ids.cpu().numpy(), S["gt_i"], S["gt_d"], args.k)
         pts.append({"L": L, "recall": round(r, 4)})
         log(f"sweep [{est}] L={L} recall@{args.k}={r:.4f}")
         if r >= args.target and chosen is None:
@@ -280,8 +511,12 @@ def _calibrate(S, args, world, est="reference"):
 
 
 def _alg_bytes(S, L, est="reference"):
-    """per query sum_hops(4*deg+4) + sum_evals(record bytes) + 4D (query),
-    for the search kernel; the rerank kernel adds L_valid*(4D) rows + 4D."""
+    """SURVEY.md §8(d) algorithmic bytes of one search launch over the batch:
+    per query sum_hops(4R + 4) adjacency + evals x (record bytes) + 4D query, where
+    evals is the REFERENCE's count |{start} U N(expanded)| (search.py:171-269),
+    computed on device from the kernel's own expansion trace. The kernel's own eval
+    counter (re-evaluations after visited-table evictions included) is reported
+    beside it; it does not enter `achieved`."""
     import torch
 
     from paper_2601_07048_b200 import search as jsearch
@@ -289,20 +524,37 @@ def _alg_bytes(S, L, est="reference"):
     jb = S["jb"]
     g, idx = S["graph"], S["idx"]
     bound = jsearch._Bound(idx, S["q_dev"], est)
-    fk, hops, evals, flags, _, _ = jsearch._launch(g, bound, L, None, 0)
+    cap = 4 * L + 64
+    fk, hops, evals, flags, tids, _ = jsearch._launch(g, bound, L, None, cap)
     torch.cuda.synchronize()
+    nq = S["q_dev"].shape[0]
+    assert int(hops.max()) <= cap, "trace capacity"
+    adj, _ = g.device()
+    uniq = torch.empty(nq, dtype=torch.int64, device=hops.device)
+    pos = torch.arange(cap, device=hops.device)
+    for lo in range(0, nq, 1000):
+        hi = min(nq, lo + 1000)
+        t = tids[lo:hi].long()
+        live = pos[None, :] < hops[lo:hi, None].long()
+        nb = adj[t.clamp(min=0)]                                  # [b, cap, R]
+        nb = torch.where(live[:, :, None] & (nb >= 0), nb, torch.full_like(nb, -1)).reshape(hi - lo, -1)
+        nb = torch.cat([nb, torch.full((hi - lo, 1), g.entry_point, dtype=nb.dtype, device=nb.device)], 1)
+        s, _ = torch.sort(nb, dim=1)
+        new = torch.ones_like(s, dtype=torch.bool)
+        new[:, 1:] = s[:, 1:] != s[:, :-1]
+        uniq[lo:hi] = (new & (s >= 0)).sum(1)
     D = S["x"].shape[1]
     R = g.degree_cap
     code_meta = (D * idx.bits + 7) // 8 + 8
     h = hops.double().sum().item()
-    e = evals.double().sum().item()
-    nq = S["q_dev"].shape[0]
-    # adjacency rows: the kernel reads R slots (4*R B) per hop plus the 4 B key/degree word
-    search_bytes = h * (4 * R + 4) + e * code_meta + nq * 4 * D
+    e_ref = uniq.double().sum().item()
+    e_dev = evals.double().sum().item()
+    search_bytes = h * (4 * R + 4) + e_ref * code_meta + nq * 4 * D
     valid = (fk != -1).sum().item()
     rerank_bytes = valid * 4 * D + nq * 4 * D
-    return dict(search_bytes=search_bytes, rerank_bytes=rerank_bytes, hops=h / nq, evals=e / nq,
-                lossy=int(flags.sum().item()), record_bytes=jb._lib.lib().jb_rabitq_record_bytes(D, idx.bits))
+    return dict(search_bytes=search_bytes, rerank_bytes=rerank_bytes, hops=h / nq, evals_ref=e_ref / nq,
+                evals_dev=e_dev / nq, lossy=int(flags.sum().item()),
+                record_bytes=jb._lib.lib().jb_rabitq_record_bytes(D, idx.bits))
 
 
 def _timed_steps(S, args, world, L, clocks_idx, est="reference"):
@@ -356,8 +608,10 @@ def _timed_steps(S, args, world, L, clocks_idx, est="reference"):
 
 def _kernel_times(S, args, L, est="reference"):
     """The dominant kernel alone (roofline): K launches of the beam-search kernel on
-    one stream over the full batch, CUDA events on that stream, L2 flushed between
-    launches outside the events; the bind and rerank kernels timed the same way."""
+    one stream over the full 10K batch, CUDA events on that stream, L2 flushed between
+    launches outside the events; the bind and rerank kernels timed the same way. The
+    search launches sit in NVTX range "kernel_alone" so the committed ncu capture is
+    of exactly this launch (profiles/profile_round.sh)."""
     import torch
 
     from paper_2601_07048_b200 import _lib
@@ -381,7 +635,11 @@ def _kernel_times(S, args, L, est="reference"):
         ev[0].record()
         bound = jsearch._Bound(idx, q_dev, est)
         ev[1].record()
+        if i == n:
+            torch.cuda.nvtx.range_push("kernel_alone")
         fk, *_ = jsearch._launch(g, bound, L, None, 0)
+        if i == n:
+            torch.cuda.nvtx.range_pop()
         ev[2].record()
         _lib.check(_lib.lib().jb_rerank_topk(_lib.ptr(rows.x), rows.dims, _lib.ptr(q_dev), nq, _lib.ptr(fk), L, k,
                                              _lib.ptr(out_i), _lib.ptr(out_d), st))
@@ -413,6 +671,7 @@ def _e2e(S, args, world, L, est="reference"):
             times.append(time.perf_counter() - t0)
         d2h = ids.nbytes + ds.nbytes
     else:
+        from paper_2601_07048_b200 import comm
         from paper_2601_07048_b200.shard import ShardedIndex
 
         si = ShardedIndex(S["graph"], S["ds"], S["shard_start"], rabitq=S["idx"])
@@ -426,8 +685,6 @@ def _e2e(S, args, world, L, est="reference"):
             if rank == 0:
                 ids, ds = gi.cpu().numpy(), gd.cpu().numpy()
             torch.cuda.synchronize()
-            from paper_2601_07048_b200 import comm
-
             dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
             times.append(float(comm.all_reduce_max(dt).item()))
         d2h = args.nq * args.k * (8 + 8)
@@ -437,76 +694,77 @@ def _e2e(S, args, world, L, est="reference"):
             "h2d_bytes_per_step": int(qh.nbytes), "d2h_bytes_per_step": int(d2h)}
 
 
-def _cpu_worker(payload):
-    import numpy as _np
+def _cpu_search_baseline(S, args, L):
+    """cpu_baseline leg: the C port of beamann's search path (oracle/cref.py, all host
+    threads) on the GPU-built index at L with the bit-exact estimator, ids checked
+    identical to the GPU's. Bounded to ~cpu_seconds of work."""
+    from oracle import cref
 
-    from oracle import rabitq as orq
-    from oracle import search as osr
-
-    (adj, active, entry, codes, meta, bits, dims, centroid, seed, x, qs, L, k) = payload
-    rot, qadd, sumq = orq.bind(qs, centroid, bits, seed)
-    src = orq.QuantSource(codes, meta, bits, dims, rot, qadd, sumq)
-    res = osr.beam_search(adj, active, entry, src, len(qs), L)
-    ids, _ = osr.topk(res, k, queries=qs, rerank_data=x)
-    return _np.asarray(ids)
-
-
-_SHARED = {}
-
-
-def _cpu_task(bounds):
-    lo, hi = bounds
-    s = _SHARED
-    return _cpu_worker((s["adj"], s["active"], s["entry"], s["codes"], s["meta"], s["bits"], s["dims"],
-                        s["centroid"], s["seed"], s["x"], s["q"][lo:hi], s["L"], s["k"]))
-
-
-def _cpu_baseline(S, args, L, procs: int, seconds: float):
-    """Reference algorithm (oracle port, numpy) on the host: RaBitQ search + rerank at L."""
-    import multiprocessing as mp
-
+    threads = os.cpu_count() or 1
     g, idx = S["graph"], S["idx"]
-    _SHARED.update(adj=np.ascontiguousarray(g.adjacency), active=g.active_count, entry=g.entry_point,
-                   codes=idx.codes, meta=idx.meta, bits=idx.bits, dims=idx.dims, centroid=idx.centroid,
-                   seed=idx.rotation_seed, x=S["x"], q=S["q"], L=L, k=args.k)
-    # probe single-process speed on a small slice, then size the sample to ~`seconds`
+    cg = cref.Graph(g.capacity, g.degree_cap)
+    cg.adj[:], cg.deg[:] = g.adjacency, g.degrees
+    cg.active, cg.entry = g.active_count, g.entry_point
+    quant = cref.Quantized(idx.centroid, idx.codes, idx.meta, idx.bits, idx.rotation_seed)
     t0 = time.perf_counter()
-    _cpu_task((0, 50))
-    per_q = (time.perf_counter() - t0) / 50
-    n = int(max(50, min(args.nq, seconds / per_q * max(procs, 1) * 0.8)))
-    n = max(procs, n - n % max(procs, 1))
-    if procs <= 1:
-        t0 = time.perf_counter()
-        ids = _cpu_task((0, n))
-        el = time.perf_counter() - t0
-    else:
-        ctx = mp.get_context("fork")
-        os.environ["OPENBLAS_NUM_THREADS"] = "1"
-        cuts = np.linspace(0, n, procs + 1).astype(int)
-        with ctx.Pool(procs) as pool:
-            pool.map(_cpu_task, [(0, 4)] * procs)  # fork + import warmup
-            t0 = time.perf_counter()
-            parts = pool.map(_cpu_task, list(zip(cuts[:-1], cuts[1:])))
-            el = time.perf_counter() - t0
-        ids = np.concatenate(parts)
-    return n, el, ids
+    ids, _ = _c_knn(cg, quant, S["x"], S["q"][:500], L, args.k, threads)
+    per_q = (time.perf_counter() - t0) / 500
+    n = int(min(args.nq, max(500, args.cpu_seconds / per_q)))
+    t0 = time.perf_counter()
+    ids, _ = _c_knn(cg, quant, S["x"], S["q"][:n], L, args.k, threads)
+    el = time.perf_counter() - t0
+    gpu_ids, _ = _search_fn(S, 1, L, args.k, "reference")(S["q_dev"][:n])
+    return {"value": round(n / el, 1), "unit": "queries/s", "cores": threads, "kind": "port",
+            "cpu_model": _cpu_model(),
+            "sample": f"first {n} of the {args.nq} queries, C port of the reference search path (bind, lockstep "
+                      f"RaBitQ search, exact rerank) at L={L}, {threads} threads",
+            "ids_identical_to_gpu": bool(np.array_equal(ids, gpu_ids.cpu().numpy()))}, cg
 
 
-def _json_base(args, world, L):
-    return {
-        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "metric": "QPS at recall@10=0.95", "unit": "queries/s", "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": f"SIFT-1M-shaped synthetic {args.n}x{args.dim} low-rank (d_int=16, noise 0.05) "
-                               f"per shard, RaBitQ {args.bits}-bit + fp32 rerank, {args.nq} queries, k={args.k}",
-                   "index": {"R": 32, "L_build": 64, "alpha": 1.2, "max_batch": 100000},
-                   "beam_width": L, "shards": world, "parallelism": f"shard{world}",
-                   "l2": "flushed between timed steps (256 MB write, outside the events)"},
-    }
+def _stream_insert(S, args, cg):
+    """One streaming batch_insert of `--stream-rows` new rows into the 1M graph: on the GPU
+    (public API) and with the C port of the reference (all host threads) on the same
+    graph; the resulting graphs must be identical."""
+    import torch
+
+    from oracle import cref
+
+    jb = S["jb"]
+    n, s, R = args.n, args.stream, INDEX["R"]
+    xs = _stream_rows(args)
+    xa = np.concatenate([S["x"], xs])
+    ds2 = jb.VectorDataset(xa)
+    ds2.device()
+    g2 = jb.GraphIndex(n + s, R)
+    adj = np.full((n + s, R), -1, dtype=np.int32)
+    deg = np.zeros(n + s, dtype=np.int32)
+    adj[:n], deg[:n] = cg.adj, cg.deg
+    g2.adjacency, g2.degrees = adj, deg
+    g2.active_count, g2.entry_point = cg.active, cg.entry
+    g2.device()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    jb.batch_insert(g2, ds2, range(n, n + s), S["params"])
+    torch.cuda.synchronize()
+    t_gpu = time.perf_counter() - t0
+    gpu_sha = _graph_sha(g2.adjacency, g2.degrees, g2.active_count, g2.entry_point)
+    threads = os.cpu_count() or 1
+    gs = cref.Graph(n + s, R)
+    gs.adj[:n], gs.deg[:n], gs.active, gs.entry = cg.adj, cg.deg, cg.active, cg.entry
+    rows2 = cref.Rows(xa, threads)
+    t0 = time.perf_counter()
+    cref.batch_insert(gs, rows2, n, n + s, INDEX["L_build"], INDEX["alpha"], threads=threads)
+    t_cpu = time.perf_counter() - t0
+    same = bool(np.array_equal(gs.adj, g2.adjacency) and gs.entry == g2.entry_point)
+    del ds2, g2
+    return {"rows": s, "base_rows": n, "inserts_per_s": round(s / t_gpu, 1), "graph_sha": gpu_sha,
+            "timed": "one batch_insert call (wall clock, synchronized)",
+            "cpu_baseline": {"inserts_per_s": round(s / t_cpu, 1), "cores": threads, "kind": "port",
+                             "sample": f"the same {s}-row batch_insert, C port of the reference, {threads} threads",
+                             "identical_graph": same}}
 
 
-def main():
-    args = _args()
+def gpu_arm(args):
     import torch
 
     world, rank, local = _dist()
@@ -514,50 +772,9 @@ def main():
         from paper_2601_07048_b200 import search as _js
 
         _js.TUNING["hash_slots"] = args.hash_slots
-    if args.impl == "reference" and world > 1 and rank != 0:
-        # reference arm: rank 0 alone runs the CPU reference (its index build uses cuda:0)
-        import torch.distributed as dist
-
-        dist.barrier()
-        dist.destroy_process_group()
-        return
-    if args.impl == "reference":
-        world_eff = 1
-    else:
-        world_eff = world
-    S = _setup(args, world_eff, rank)
-    if args.impl == "reference" or args.estimator == "reference":
-        ests = ["reference"]
-    elif args.estimator == "popcount":
-        ests = ["popcount"]
-    else:
-        ests = ["reference", "popcount"]
-    cal = {e: _calibrate(S, args, world_eff, e) for e in ests}
-    L, sweep_pts = cal["reference"] if "reference" in cal else cal[ests[0]]
-
-    if args.impl == "reference":
-        procs = os.cpu_count() or 1
-        steps = []
-        for i in range(args.warmup + args.steps):
-            n, el, _ = _cpu_baseline(S, args, L, procs, seconds=max(2.0, args.cpu_seconds / 2))
-            steps.append((n, el))
-        tt = steps[args.warmup:]
-        value = sum(n for n, _ in tt) / sum(el for _, el in tt)
-        out = _json_base(args, 1, L)
-        out.update({"impl": "reference", "value": round(value, 1), "ms_per_step": round(1e3 * np.mean([e for _, e in tt]), 2),
-                    "cpu_baseline": {"value": round(value, 1), "unit": "queries/s", "cores": procs, "kind": "port",
-                                     "sample": f"{tt[0][0]} queries per step of the {args.nq}-query batch, numpy oracle "
-                                               f"(reference lockstep algorithm), {procs} forked processes"},
-                    "e2e": {"value": round(value, 1), "unit": "queries/s", "h2d_bytes_per_step": 0,
-                            "d2h_bytes_per_step": 0},
-                    "sweep": sweep_pts})
-        print(json.dumps(out), flush=True)
-        if world > 1:
-            import torch.distributed as dist
-
-            dist.barrier()
-            dist.destroy_process_group()
-        return
+    S = _setup(args, world, rank)
+    ests = {"reference": ["reference"], "popcount": ["popcount"], "auto": ["reference", "popcount"]}[args.estimator]
+    cal = {e: _calibrate(S, args, world, e) for e in ests}
 
     runs = {}
     for e in ests:
@@ -566,7 +783,8 @@ def main():
         T = _timed_steps(S, args, world, Le, local, e)
         T.update(_kernel_times(S, args, Le, e))
         runs[e] = (Le, ab, T, args.nq * world * args.steps / (T["total_ms"] / 1e3))
-        log(f"[{e}] L={Le} value={runs[e][3]:.0f} queries/s, search kernel {T['search_ms']:.3f} ms")
+        log(f"[{e}] L={Le} value={runs[e][3]:.0f} queries/s, search kernel {T['search_ms']:.3f} ms, "
+            f"evals/query ref {ab['evals_ref']:.0f} device {ab['evals_dev']:.0f}")
     est = max(runs, key=lambda e: runs[e][3])
     L, ab, T, value = runs[est]
     sweep_pts = cal[est][1]
@@ -575,40 +793,57 @@ def main():
     search_s = T["search_ms"] / 1e3
     achieved = ab["search_bytes"] / search_s / 1e9
     out = _json_base(args, world, L)
-    out["config"]["estimator"] = est
+    wl_key = out["config"]["workload"] + f" L={L} {est}"
+    ncu = _ncu_record(wl_key)
+    clk = T["clocks"].get("sm_mhz") or 1965.0
+    issue = None
+    if ncu.get("warp_inst_per_launch"):
+        # issue roofline: 4 warp-instruction issues per clock per SM x 148 SMs
+        ipl = ncu["warp_inst_per_launch"]
+        rate = ipl / search_s
+        issue = {"warp_inst_per_launch": int(ipl), "achieved_ginst_s": round(rate / 1e9, 1),
+                 "peak_ginst_s": round(4 * 148 * clk * 1e6 / 1e9, 1),
+                 "frac": round(rate / (4 * 148 * clk * 1e6), 4), "source": ncu.get("source")}
     out.update({
+        "impl": "b200", "estimator": est,
         "value": round(value, 1),
         "ms_per_step": round(T["total_ms"] / args.steps, 3),
         "e2e": e2e,
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "peak_kind": peak_kind,
-                     "traffic": _traffic(out["config"]["workload"] + f" L={L} {est}"),
+                     "traffic": ncu.get("dram_bytes_per_launch"),
+                     "traffic_source": ncu.get("source"),
                      "kernel": f"beam_search_kernel<{'RABITQ_FAST' if est == 'popcount' else 'RABITQ'},{args.bits}>",
-                     "alg_bytes_per_launch": int(ab["search_bytes"]),
-                     "kernel_ms": round(search_s * 1e3, 4)},
+                     "alg_bytes_per_launch": int(ab["search_bytes"]), "kernel_ms": round(search_s * 1e3, 4),
+                     "evals_counted": "reference |{start} U N(expanded)| per query (device re-evaluations excluded)",
+                     "issue": issue},
         "gpu_launches": T["launches"],
         "clocks": T["clocks"],
         "recall_at_10": next(p["recall"] for p in sweep_pts if p["L"] == L),
         "sweep": sweep_pts,
-        "per_query": {"hops": round(ab["hops"], 2), "evals": round(ab["evals"], 1), "lossy_queries": ab["lossy"]},
+        "per_query": {"hops": round(ab["hops"], 2), "evals_reference": round(ab["evals_ref"], 1),
+                      "evals_device": round(ab["evals_dev"], 1),
+                      "reevaluated_frac": round(ab["evals_dev"] / ab["evals_ref"] - 1.0, 4),
+                      "lossy_queries": ab["lossy"]},
         "kernel_ms": {"bind": round(T["bind_ms"], 4), "search": round(search_s * 1e3, 4),
                       "rerank": round(T["rerank_ms"], 4),
                       "note": "each kernel alone on one stream over the full batch (the step runs two lanes)"},
         "build": {"inserts_per_s": round(args.n / S["t_build"], 1), "build_s": round(S["t_build"], 2),
                   "rabitq_fit_s": round(S["t_fit"], 3), "gen_s": round(S["t_gen"], 2),
+                  "graph_sha": _graph_sha(S["graph"].adjacency, S["graph"].degrees, S["graph"].active_count,
+                                          S["graph"].entry_point),
                   "roofline": _insert_roofline(S, args, peak)},
         "estimators": {e: {"L": runs[e][0], "value": round(runs[e][3], 1),
                            "recall_at_10": next(p["recall"] for p in cal[e][1] if p["L"] == runs[e][0]),
-                           "search_kernel_ms": round(runs[e][2]["search_ms"], 4)} for e in runs},
+                           "search_kernel_ms": round(runs[e][2]["search_ms"], 4),
+                           "bit_exact": e == "reference"} for e in runs},
     })
     if rank == 0 and world == 1 and not args.no_cpu:
         Lr = cal["reference"][0] if "reference" in cal else L
-        n, el, ids = _cpu_baseline(S, args, Lr, procs=1, seconds=args.cpu_seconds)
-        gpu_ids, _ = _search_fn(S, world, Lr, args.k, "reference")(S["q_dev"][:n])
-        out["cpu_baseline"] = {"value": round(n / el, 1), "unit": "queries/s", "cores": 1, "kind": "port",
-                               "sample": f"first {n} of the {args.nq} queries, numpy oracle port of the reference "
-                                         f"(lockstep RaBitQ search + rerank) at its L*={Lr}, 1 process",
-                               "ids_identical_to_gpu": bool(np.array_equal(ids, gpu_ids.cpu().numpy()))}
+        cb, cg = _cpu_search_baseline(S, args, Lr)
+        out["cpu_baseline"] = cb
+        if args.stream:
+            out["build"]["stream_batch"] = _stream_insert(S, args, cg)
     if rank == 0:
         line = json.dumps(out)
         print(line, flush=True)
@@ -620,6 +855,14 @@ def main():
 
         dist.barrier()
         dist.destroy_process_group()
+
+
+def main():
+    args = _args()
+    if args.impl == "reference":
+        reference_arm(args)
+    else:
+        gpu_arm(args)
 
 
 if __name__ == "__main__":

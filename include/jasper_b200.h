@@ -312,6 +312,17 @@ int jb_merge_shard_topk(const int32_t* in_ids, const double* in_dists, int32_t s
                         int32_t k, const int64_t* id_offsets_host, int64_t* out_ids,
                         double* out_dists, void* stream);
 
+/* Exchange format of the sharded path: a shard's top-k (local int32 ids, f64
+ * dists, [nq, k]) packed into 16-byte records {f64 dist, i64 global id}
+ * (id + id_offset; -1 padding kept) so one all-gather moves ids and dists. */
+int jb_pack_shard_topk(const int32_t* ids, const double* dists, int64_t nq, int32_t k, int64_t id_offset,
+                       void* out_records, void* stream);
+
+/* Global top-k by (dist, global id) from all-gathered records [shards, nq, k].
+ * Stream-ordered: no allocation, no synchronization. */
+int jb_merge_shard_records(const void* records, int32_t shards, int64_t nq, int32_t k, int64_t* out_ids,
+                           double* out_dists, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

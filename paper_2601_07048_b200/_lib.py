@@ -88,6 +88,8 @@ _SIGS = {
     "jb_exact_knn_kind": (C.c_int, [p, i64, i32, p, i64, i32, i32, p, p, p]),
     "jb_mips_augment": (C.c_int, [p, i64, i32, p, i64, p, p, p, p]),
     "jb_merge_shard_topk": (C.c_int, [p, p, i32, i64, i32, p, p, p, p]),
+    "jb_pack_shard_topk": (C.c_int, [p, p, i64, i32, i64, p, p]),
+    "jb_merge_shard_records": (C.c_int, [p, i32, i64, i32, p, p, p]),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -13,7 +13,7 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2601_07048_b200.shard import shard_range, sharded_knn
+from paper_2601_07048_b200.shard import pack_topk_host, shard_range, sharded_knn
 
 N, D, NQ, K, L = 1200, 16, 40, 5, 24
 
@@ -32,10 +32,15 @@ def _local(x, lo, hi, q, k):
     return osearch.topk(res, k)
 
 
-def _merge(all_ids, all_d, offsets, k):
+def _merge(records, k):
+    """All-gathered exchange records [S, nq, 2k] ({f64 dist, i64 global id}) -> the oracle merge."""
     from oracle.knn import merge_shard_topk
 
-    i, d = merge_shard_topk(all_ids.numpy(), all_d.numpy(), offsets, k)
+    r = records.numpy().reshape(records.shape[0], records.shape[1], k, 2)
+    d = r[..., 0].copy().view(np.float64)
+    gid = r[..., 1]
+    ids = np.where(gid >= 0, gid, -1).astype(np.int32)
+    i, d = merge_shard_topk(ids, d, [0] * records.shape[0], k)
     return torch.from_numpy(i), torch.from_numpy(d)
 
 
@@ -51,7 +56,11 @@ def _worker(rank, world, port, out):
             return torch.from_numpy(ids), torch.from_numpy(ds)
 
         qt = torch.from_numpy(q) if rank == 0 else None
+        # shape broadcast path (non-root ranks do not know the batch shape) ...
         gi, gd = sharded_knn(local_search, qt, K, lo, merge=_merge, device=torch.device("cpu"))
+        # ... and the sync-free path with the shape known on every rank
+        gi2, gd2 = sharded_knn(local_search, qt, K, lo, merge=_merge, device=torch.device("cpu"), nq=NQ, dims=D)
+        assert torch.equal(gi, gi2) and torch.equal(gd, gd2)
         out[rank] = (gi.numpy().tolist(), gd.numpy().tolist())
     finally:
         dist.destroy_process_group()
@@ -93,3 +102,11 @@ def test_sharded_search_gloo_world2_matches_single_process_merge():
         np.testing.assert_array_equal(np.asarray(gd), exp_d)
     # merged ids are global and come from both shards
     assert (exp_i >= N // 2).any() and (exp_i < N // 2).any()
+
+
+def test_pack_records_host_layout():
+    ids = torch.tensor([[3, -1], [0, 7]], dtype=torch.int32)
+    d = torch.tensor([[1.5, float("inf")], [0.0, 2.25]], dtype=torch.float64)
+    r = pack_topk_host(ids, d, 100).numpy().reshape(2, 2, 2)
+    assert r[0, 0, 1] == 103 and r[0, 1, 1] == -1 and r[1, 1, 1] == 107
+    assert r[1, 1, 0:1].view(np.float64)[0] == 2.25
