@@ -534,9 +534,9 @@ def _alg_bytes(S, L, est="reference"):
     pos = torch.arange(cap, device=hops.device)
     for lo in range(0, nq, 1000):
         hi = min(nq, lo + 1000)
-        t = tids[lo:hi].long()
         live = pos[None, :] < hops[lo:hi, None].long()
-        nb = adj[t.clamp(min=0)]                                  # [b, cap, R]
+        t = torch.where(live, tids[lo:hi].long(), torch.zeros_like(tids[lo:hi], dtype=torch.long))
+        nb = adj[t]                                               # [b, cap, R] (slots past hops: row 0, masked)
         nb = torch.where(live[:, :, None] & (nb >= 0), nb, torch.full_like(nb, -1)).reshape(hi - lo, -1)
         nb = torch.cat([nb, torch.full((hi - lo, 1), g.entry_point, dtype=nb.dtype, device=nb.device)], 1)
         s, _ = torch.sort(nb, dim=1)

@@ -283,6 +283,28 @@ int jb_robust_prune(const float* data, const float* data_norms, int32_t dims,
                     double alpha, int32_t degree_cap,
                     int32_t* out_ids, float* out_dists, int32_t* out_counts, void* stream);
 
+/* ---- distance-source protocol (search.py:82-168, rabitq.py:225-244) ------ */
+
+/* `bind_distance_source(source, queries).distances(qrows, ids)` on the device:
+ * out[i] = d(query qrows[i], vector ids[i]) for i < n, in the search kernel's
+ * rounding. args: the source + bound-query fields of jb_search_args (source,
+ * dims, data/data_norms | records/record_bytes/bits | data_u8/norms_u32,
+ * queries/query_add/query_sumq | queries_u8/query_norms_u32); graph fields are
+ * ignored. query_stride: elements between bound query rows (0 = dims); RABITQ
+ * rows need a multiple of 4 floats and U8 rows a multiple of 16 bytes (16 B
+ * aligned). out: f32 [n] (EXACT, RABITQ reference estimator) or u32 [n] (U8). */
+int jb_bound_distances(const jb_search_args* args, int64_t query_stride, const int64_t* qrows,
+                       const int64_t* ids, int64_t n, void* out, void* stream);
+
+/* robust_prune (graph.py:174-228) of one candidate set given its pairwise
+ * matrix dmat[i * n + j] = dist_fn(ids[i], [ids[j]]) (f64), candidate dists
+ * to the pivot `dists` (f64) and ids (for the (dist, id) order): writes the
+ * kept candidate POSITIONS in extraction order to out_pos[<= degree_cap] and
+ * their number to *out_count (device). */
+int jb_robust_prune_matrix(const double* dmat, const int64_t* ids, const double* dists, int32_t n,
+                           double alpha, int32_t degree_cap, int32_t* out_pos, int32_t* out_count,
+                           void* stream);
+
 /* ---- measurement -------------------------------------------------------- */
 
 /* Exact top-k in f64 (oracle.exact_knn, oracle.py:20-62): (dist, id) ascending. */

@@ -89,6 +89,8 @@ _SIGS = {
     "jb_mips_augment": (C.c_int, [p, i64, i32, p, i64, p, p, p, p]),
     "jb_merge_shard_topk": (C.c_int, [p, p, i32, i64, i32, p, p, p, p]),
     "jb_pack_shard_topk": (C.c_int, [p, p, i64, i32, i64, p, p]),
+    "jb_bound_distances": (C.c_int, [C.POINTER(SearchArgs), i64, p, p, i64, p, p]),
+    "jb_robust_prune_matrix": (C.c_int, [p, p, p, i32, f64, i32, p, p, p]),
     "jb_merge_shard_records": (C.c_int, [p, i32, i64, i32, p, p, p]),
 }
 

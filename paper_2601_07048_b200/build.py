@@ -26,8 +26,8 @@ import numpy as np
 
 from . import _lib
 from .core import ElementKind, as_dataset
-from .graph import GraphIndex, as_graph, medoid
-from .search import MAX_BEAM_WIDTH
+from .graph import GraphIndex, as_graph, medoid, write_back
+from .search import MAX_BEAM_WIDTH, MAX_DEGREE_CAP
 
 __all__ = ["BuildParams", "EdgeBuffer", "batch_insert", "build", "insert_stream"]
 
@@ -48,6 +48,8 @@ class BuildParams:
     def __post_init__(self):
         if self.degree_cap < 2:
             raise ValueError("degree_cap must be >= 2")
+        if self.degree_cap > MAX_DEGREE_CAP:
+            raise ValueError(f"degree_cap must be <= {MAX_DEGREE_CAP} (the search kernel's neighbour chunks)")
         if self.alpha < 1.0:
             raise ValueError("alpha must be >= 1")
         if not 1 <= self.build_beam_width <= MAX_BEAM_WIDTH:
@@ -194,7 +196,7 @@ def _check_supported(params: BuildParams, quantizer):
 
 def batch_insert(graph, dataset, new_ids: range, params: BuildParams, quantizer=None) -> None:
     """build.py:296-348: insert a contiguous id range as one three-phase batch (in place)."""
-    graph = as_graph(graph)
+    caller, graph = graph, as_graph(graph)
     ds = as_dataset(dataset)
     start, stop = _validate_range(graph, ds, new_ids)
     if start == stop:
@@ -205,6 +207,7 @@ def batch_insert(graph, dataset, new_ids: range, params: BuildParams, quantizer=
     a = _args(graph, ds, params, start, stop, quantizer)
     graph.last_bridges = _run(_lib.lib().jb_batch_insert, graph, a)
     graph.active_count = stop
+    write_back(graph, caller)
 
 
 def _repair(graph: GraphIndex, ds, params: BuildParams, quantizer=None) -> int:
@@ -262,7 +265,7 @@ def insert_stream(graph, dataset, new_range: range, params: BuildParams, quantiz
     """build.py:427-447."""
     if len(new_range) == 0:
         return
-    graph = as_graph(graph)
+    caller, graph = graph, as_graph(graph)
     ds = as_dataset(dataset)
     _validate_range(graph, ds, new_range)
     pos = new_range.start
@@ -270,3 +273,4 @@ def insert_stream(graph, dataset, new_range: range, params: BuildParams, quantiz
         stop = min(new_range.stop, pos + params.max_batch)
         batch_insert(graph, ds, range(pos, stop), params, quantizer)
         pos = stop
+    write_back(graph, caller)

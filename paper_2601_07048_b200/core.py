@@ -159,9 +159,13 @@ class VectorDataset:
         dev = self.device()
         if self._kind is not ElementKind.U8:
             return dev.x
+        cached = getattr(self, "_dev_f32", None)
+        if cached is not None:
+            return cached
         torch = _lib.require_cuda()
         out = torch.empty(dev.x.shape, dtype=torch.float32, device=dev.x.device)
         _lib.check(_lib.lib().jb_u8_to_f32(_lib.ptr(dev.x), dev.x.numel(), _lib.ptr(out), _lib.stream_ptr()))
+        self._dev_f32 = out  # kept: the rerank reads it asynchronously
         return out
 
 

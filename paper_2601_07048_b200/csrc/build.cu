@@ -274,17 +274,17 @@ __device__ __forceinline__ uint16_t* stage_list(uint32_t* cn, int crows) {
 // ---- seed batch (build.py:246-266) ------------------------------------------
 template <class M>
 __global__ void __launch_bounds__(BW * 32)
-seed_prune_kernel(const M m, int64_t start, int64_t stop, double alpha2, int R, uint64_t* __restrict__ cand_all,
-                  int32_t* __restrict__ kept_ids, uint32_t* __restrict__ kept_d, int32_t* __restrict__ adj,
-                  int32_t* __restrict__ deg) {
+seed_prune_kernel(const M m, int64_t start, int64_t stop, int64_t xi0, int64_t xi1, double alpha2, int R,
+                  uint64_t* __restrict__ cand_all, int32_t* __restrict__ kept_ids, uint32_t* __restrict__ kept_d,
+                  int32_t* __restrict__ adj, int32_t* __restrict__ deg) {
     extern __shared__ __align__(16) uint32_t shw[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     uint32_t* pv = shw + warp * m.pivot_words();
     const int64_t n = stop - start;
-    const int64_t xi = (int64_t)blockIdx.x * BW + warp;
-    if (xi >= n) return;
+    const int64_t xi = xi0 + (int64_t)blockIdx.x * BW + warp;  // pivots [xi0, xi1) of this tile
+    if (xi >= xi1) return;
     const uint32_t x = (uint32_t)(start + xi);
-    uint64_t* cand = cand_all + xi * (n - 1);
+    uint64_t* cand = cand_all + (xi - xi0) * (n - 1);
     // candidate dists d(x, others) with x as the pivot
     m.load_pivot(pv, x);
     for (int64_t j = lane; j < n - 1; j += 32) {
@@ -292,8 +292,8 @@ seed_prune_kernel(const M m, int64_t start, int64_t stop, double alpha2, int R, 
         cand[j] = key_of(m.dist(pv, o), o);
     }
     __syncwarp();
-    int32_t* ki = kept_ids + xi * R;
-    uint32_t* kd = kept_d + xi * R;
+    int32_t* ki = kept_ids + (xi - xi0) * R;
+    uint32_t* kd = kept_d + (xi - xi0) * R;
     const int k = warp_prune(cand, (int)(n - 1), alpha2, R, m, pv, ki, kd);
     write_row(adj, deg, R, x, ki, k);
 }
@@ -1885,14 +1885,21 @@ static int batch_insert_impl(const M& m, const jb_insert_args& a, cudaStream_t s
                                           : jb_medoid(a.data, a.stop, D, &entry, st);
         if (rc) return rc;
         if (nb > 1) {
-            BALLOC(cand, uint64_t, (size_t)nb * (nb - 1));
-            BALLOC(kid, int32_t, (size_t)nb * R);
-            BALLOC(kd, uint32_t, (size_t)nb * R);
+            // pivots in tiles: scratch is tile x (nb - 1) keys (<= 1 GiB), not nb^2. The
+            // reference's seed batch is all-pairs too (build.py:254-266); a tile's rows are
+            // written as it finishes and no pivot reads adjacency, so tiling is exact.
+            const int64_t tile = std::max<int64_t>(BW, std::min<int64_t>(nb, ((int64_t)1 << 27) / (nb - 1)));
+            BALLOC(cand, uint64_t, (size_t)tile * (nb - 1));
+            BALLOC(kid, int32_t, (size_t)tile * R);
+            BALLOC(kd, uint32_t, (size_t)tile * R);
             const int smem = BW * m.pivot_words() * 4;
             JB_CUDA_RC(grow_smem(seed_prune_kernel<M>, smem));
-            seed_prune_kernel<M><<<(unsigned)((nb + BW - 1) / BW), BW * 32, smem, st>>>(
-                m, a.start, a.stop, alpha2, R, cand, kid, kd, a.adjacency, a.degrees);
-            JB_LAUNCH_CHECK();
+            for (int64_t t0 = 0; t0 < nb; t0 += tile) {
+                const int64_t t1 = std::min(nb, t0 + tile);
+                seed_prune_kernel<M><<<(unsigned)((t1 - t0 + BW - 1) / BW), BW * 32, smem, st>>>(
+                    m, a.start, a.stop, t0, t1, alpha2, R, cand, kid, kd, a.adjacency, a.degrees);
+                JB_LAUNCH_CHECK();
+            }
         }
         rc = repair(m, a, a.stop, entry, st, &bridges);
         if (a.entry_point_out_host) *a.entry_point_out_host = entry;
@@ -1917,6 +1924,8 @@ static int batch_insert_impl(const M& m, const jb_insert_args& a, cudaStream_t s
     // ---- phase 2: activate, prune each new vertex, emit reverse triples ----
     const int W = a.reverse_all_visited ? cap : R;
     const int64_t ntri = nb * (int64_t)W;
+    JB_CHECK_ARG(ntri < INT32_MAX, "batch of %lld rows x %d reverse slots exceeds the 2^31 sort limit; "
+                 "use a smaller max_batch", (long long)nb, W);
     BALLOC(cand, uint64_t, (size_t)nb * cap);
     BALLOC(kid, int32_t, (size_t)nb * R);
     BALLOC(kd, uint32_t, (size_t)nb * R);

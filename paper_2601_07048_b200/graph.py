@@ -8,9 +8,13 @@ and the byte-identical `graph.bin` save/load.
 B200 layout: the same slab lives in HBM (R=32: one 128 B row per vertex, one
 sector-aligned request per hop). Kernels mutate the device slab during
 construction; the host arrays are refreshed lazily, so `build`/`insert_stream`
-never pay a full-slab download per batch. Reading `adjacency`/`degrees` from
-the host marks the host copy as possibly modified, so the next device use
-re-uploads it.
+never pay a full-slab download per batch. `adjacency` / `degrees` are numpy
+views that track writes: reading them costs at most one download and never a
+re-upload; an in-place write through indexing (`g.adjacency[u, :] = ...`,
+including through slices of it) marks the host copy modified, so the next
+device use uploads it. Writes that bypass `__setitem__` (np.copyto, ufunc
+`out=`, or a plain `np.asarray` view) must be followed by
+`mark_host_modified()`.
 """
 
 from __future__ import annotations
@@ -39,6 +43,32 @@ class Candidate(NamedTuple):
     dist: float
 
 
+class _TrackedArray(np.ndarray):
+    """ndarray view whose item assignment marks its GraphIndex's host copy modified.
+    Views (slices) inherit the owner; arrays computed from it (ufunc results) do not."""
+
+    def __array_finalize__(self, obj):
+        owner = getattr(obj, "_jb_owner", None)
+        self._jb_owner = owner if (owner is not None and self.base is not None) else None
+
+    def __setitem__(self, key, value):
+        super().__setitem__(key, value)
+        owner = self._jb_owner
+        if owner is not None:
+            owner._host_dirty = True
+
+    def __array_wrap__(self, arr, context=None, return_scalar=False):
+        # ufunc / reduction results are new arrays, not views of the slab: plain ndarray / scalar
+        arr = arr.view(np.ndarray)
+        return arr[()] if return_scalar else arr
+
+
+def _tracked(arr: np.ndarray, owner) -> np.ndarray:
+    v = arr.view(_TrackedArray)
+    v._jb_owner = owner
+    return v
+
+
 class GraphIndex:
     def __init__(self, capacity: int, degree_cap: int):
         if capacity < 1:
@@ -56,6 +86,8 @@ class GraphIndex:
         self._host_dirty = True    # host may differ from device -> upload before device use
         self._dev_dirty = False    # device newer -> download before host use
         self._lock = threading.RLock()
+        self.h2d_bytes = 0         # slab bytes uploaded so far (instrumentation)
+        self.d2h_bytes = 0         # slab bytes downloaded so far
 
     # ---- host view -------------------------------------------------------
     def _sync_host(self) -> None:
@@ -64,30 +96,46 @@ class GraphIndex:
                 if self._dev_dirty:
                     self._adj[:] = self._dev_adj.cpu().numpy()
                     self._deg[:] = self._dev_deg.cpu().numpy()
+                    self.d2h_bytes += self._adj.nbytes + self._deg.nbytes
                     self._dev_dirty = False
 
     @property
     def adjacency(self) -> np.ndarray:
+        """The (capacity, R) slab; writes through indexing are tracked (module doc)."""
         self._sync_host()
-        self._host_dirty = True
-        return self._adj
+        return _tracked(self._adj, self)
 
     @adjacency.setter
     def adjacency(self, value) -> None:
         self._sync_host()
-        self._adj = np.asarray(value, dtype=np.int32)
+        value = np.ascontiguousarray(value, dtype=np.int32)
+        if value.shape != (self.capacity, self.degree_cap):
+            raise ValueError(f"adjacency must have shape {(self.capacity, self.degree_cap)}")
+        self._adj = value.view(np.ndarray).copy() if isinstance(value, _TrackedArray) else value
         self._host_dirty = True
 
     @property
     def degrees(self) -> np.ndarray:
         self._sync_host()
-        self._host_dirty = True
-        return self._deg
+        return _tracked(self._deg, self)
 
     @degrees.setter
     def degrees(self, value) -> None:
         self._sync_host()
-        self._deg = np.asarray(value, dtype=np.int32)
+        value = np.ascontiguousarray(value, dtype=np.int32)
+        if value.shape != (self.capacity,):
+            raise ValueError(f"degrees must have shape {(self.capacity,)}")
+        self._deg = value.view(np.ndarray).copy() if isinstance(value, _TrackedArray) else value
+        self._host_dirty = True
+
+    def host_adjacency(self) -> np.ndarray:
+        """Up-to-date host slab for read-only internal use (untracked)."""
+        self._sync_host()
+        return self._adj
+
+    def mark_host_modified(self) -> None:
+        """Declare host-side writes that bypassed the tracked views."""
+        self._sync_host()
         self._host_dirty = True
 
     def degree(self, u: int) -> int:
@@ -150,10 +198,12 @@ class GraphIndex:
             if self._dev_adj is None:
                 self._dev_adj = torch.from_numpy(self._adj).to("cuda")
                 self._dev_deg = torch.from_numpy(self._deg).to("cuda")
+                self.h2d_bytes += self._adj.nbytes + self._deg.nbytes
                 self._host_dirty = False
             elif self._host_dirty:
                 self._dev_adj.copy_(torch.from_numpy(self._adj))
                 self._dev_deg.copy_(torch.from_numpy(self._deg))
+                self.h2d_bytes += self._adj.nbytes + self._deg.nbytes
                 self._host_dirty = False
         return self._dev_adj, self._dev_deg
 
@@ -225,6 +275,17 @@ def as_graph(obj) -> GraphIndex:
     raise TypeError(f"unsupported graph {type(obj).__name__}")
 
 
+def write_back(graph: GraphIndex, obj) -> None:
+    """After a mutating call on a graph adopted from a beamann GraphIndex (as_graph),
+    bring the caller's object up to date: the adopted host arrays are the caller's own
+    arrays, so syncing the host copy writes them in place; counters are copied."""
+    if obj is None or obj is graph:
+        return
+    graph._sync_host()
+    obj.active_count = graph.active_count
+    obj.entry_point = graph.entry_point
+
+
 def medoid(dataset) -> int:
     """graph.py:159-171 on device: f64 mean (sequential), f64 2-lane distances, lowest id."""
     from .core import as_dataset
@@ -241,11 +302,18 @@ def medoid(dataset) -> int:
 
 def robust_prune(p: int, candidate_ids, candidate_dists, *, alpha: float, degree_cap: int,
                  dist_fn: Callable | None = None, dataset=None) -> tuple[np.ndarray, np.ndarray]:
-    """graph.py:174-228 on device (one warp per pivot).
+    """graph.py:174-228 on device.
 
-    The reference takes an arbitrary `dist_fn`; the device path computes the
-    same pairwise distances itself (build.py:105-134 semantics), so it needs
-    the dataset: pass `dataset=` or a `dist_fn` that exposes `.dataset`.
+    Distance sources, in order:
+      * `dataset=` (or a `dist_fn` exposing `.dataset`) of f32 rows: one warp computes
+        the pairwise distances itself (build.py:120-134 rounding; jb_robust_prune);
+      * u8 rows, a reference-style `_PairwiseDistances` (beamann's: `_x` rows and an
+        optional `_quantizer`), or a `dist_fn` exposing `.quantizer`: the candidates'
+        pairwise matrix is evaluated by the bound-source kernel (jb_bound_distances:
+        pivot bound as the query, build.py:105-134) and pruned by jb_robust_prune_matrix;
+      * any other callable `dist_fn(pivot, ids)`: called once per candidate for its
+        matrix row (the user's own code, as in the reference), pruned on device.
+    Returns kept (int32 ids, f64 dists) in extraction order.
     """
     if alpha < 1.0:
         raise ValueError("alpha must be >= 1")
@@ -261,17 +329,45 @@ def robust_prune(p: int, candidate_ids, candidate_dists, *, alpha: float, degree
         raise ValueError("candidate set must be deduplicated")
     if ids.size == 0:
         return ids.astype(np.int32), dists
-    if dataset is None:
-        dataset = getattr(dist_fn, "dataset", None)
-    if dataset is None:
-        raise ValueError("device robust_prune needs the dataset (dataset= or dist_fn.dataset)")
-    from .core import as_dataset
+    source, quantizer = _prune_source(dist_fn, dataset)
+    from .core import ElementKind, as_dataset
 
-    dev = as_dataset(dataset).device()
+    if source is not None and quantizer is None and as_dataset(source).element_kind is ElementKind.F32:
+        d32 = dists.astype(np.float32)
+        if np.array_equal(d32.astype(np.float64), dists):
+            return _prune_f32_rows(as_dataset(source), p, ids, d32, alpha, degree_cap)
+    if source is not None:
+        dmat = _pair_matrix_device(as_dataset(source), quantizer, ids)
+    else:
+        if dist_fn is None:
+            raise ValueError("robust_prune needs dist_fn or dataset")
+        dmat = np.stack([np.asarray(dist_fn(int(c), ids), dtype=np.float64).reshape(ids.size) for c in ids])
+    return _prune_matrix(dmat, ids, dists, alpha, degree_cap)
+
+
+def _prune_source(dist_fn, dataset):
+    """(dataset-like rows, quantizer or None) behind a dist_fn, or (None, None) for an opaque callable."""
+    if dataset is not None:
+        return dataset, getattr(dist_fn, "quantizer", None) if dist_fn is not None else None
+    if dist_fn is None:
+        return None, None
+    ds = getattr(dist_fn, "dataset", None)
+    if ds is not None:
+        return ds, getattr(dist_fn, "quantizer", None)
+    x = getattr(dist_fn, "_x", None)  # beamann build._PairwiseDistances (build.py:105-134)
+    if isinstance(x, np.ndarray) and x.ndim == 2:
+        q = getattr(dist_fn, "_quantizer", None)
+        if x.dtype == np.int64:  # u8 rows widened by the reference
+            x = x.astype(np.uint8)
+        return x, q
+    return None, None
+
+
+def _prune_f32_rows(ds, p, ids, d32, alpha, degree_cap):
     torch = _lib.require_cuda()
-    d32 = dists.astype(np.float32)
-    if not np.array_equal(d32.astype(np.float64), dists):
-        raise ValueError("candidate distances must be f32-representable (they come from f32 kernels)")
+    dev = ds.device()
+    if ids.max() >= dev.count or p >= dev.count or p < 0 or ids.min() < 0:
+        raise IndexError("vertex id out of range")
     t_ids = torch.from_numpy(ids.astype(np.int32)).cuda()
     t_d = torch.from_numpy(d32).cuda()
     piv = torch.tensor([p], dtype=torch.int64, device="cuda")
@@ -285,3 +381,41 @@ def robust_prune(p: int, candidate_ids, candidate_dists, *, alpha: float, degree
                                           _lib.stream_ptr()))
     n = int(out_n.item())
     return out_i[:n].cpu().numpy(), out_d[:n].cpu().numpy().astype(np.float64)
+
+
+def _pair_matrix_device(ds, quantizer, ids):
+    """dmat[i, j] = d(ids[i] as pivot, ids[j]) on device: the candidate rows bound as queries
+    (build.py:120-134 exact rows / u8; build.py:124-129 quantized: bind(x[pivot]))."""
+    from .search import BoundDistances
+
+    torch = _lib.require_cuda()
+    if ids.max() >= ds.count or ids.min() < 0:
+        raise IndexError("vertex id out of range")
+    n = ids.size
+    rows = torch.from_numpy(np.ascontiguousarray(ds.data[ids]))
+    if quantizer is not None:
+        from .rabitq import as_rabitq
+
+        bound = as_rabitq(quantizer).bind(rows.numpy())
+    else:
+        bound = BoundDistances(ds, rows.numpy())
+    t_ids = torch.from_numpy(ids).cuda()
+    qr = torch.arange(n, device="cuda").repeat_interleave(n)
+    cols = t_ids.repeat(n)
+    return bound.distances_device(qr, cols).reshape(n, n).to(torch.float64)
+
+
+def _prune_matrix(dmat, ids, dists, alpha, degree_cap):
+    torch = _lib.require_cuda()
+    n = ids.size
+    dm = (dmat if isinstance(dmat, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(dmat))).to(
+        "cuda", torch.float64).contiguous()
+    t_ids = torch.from_numpy(ids).cuda()
+    t_d = torch.from_numpy(np.ascontiguousarray(dists)).cuda()
+    pos = torch.empty(degree_cap, dtype=torch.int32, device="cuda")
+    cnt = torch.empty(1, dtype=torch.int32, device="cuda")
+    _lib.check(_lib.lib().jb_robust_prune_matrix(_lib.ptr(dm), _lib.ptr(t_ids), _lib.ptr(t_d), n, float(alpha),
+                                                 degree_cap, _lib.ptr(pos), _lib.ptr(cnt), _lib.stream_ptr()))
+    k = int(cnt.item())
+    sel = pos[:k].long().cpu().numpy()
+    return ids[sel].astype(np.int32), dists[sel].astype(np.float64)

@@ -25,9 +25,11 @@ from .core import ElementKind, VectorDataset, as_dataset
 from .graph import Candidate, GraphIndex, as_graph
 
 __all__ = ["SearchParams", "SearchStats", "SearchResult", "beam_search", "search_knn", "search_knn_batch",
-           "run_beam_searches", "search_knn_batch_device", "MAX_BEAM_WIDTH"]
+           "run_beam_searches", "search_knn_batch_device", "MAX_BEAM_WIDTH", "ExactDistances", "BoundDistances",
+           "bind_distance_source", "MAX_DEGREE_CAP"]
 
 MAX_BEAM_WIDTH = 1024
+MAX_DEGREE_CAP = 128  # the search kernel's neighbour chunks: R <= 32 * 4
 _UMAX = np.uint64(0xFFFFFFFFFFFFFFFF)
 # Test/tuning hook: visited-table slots per query (0 = library default).
 TUNING = {"hash_slots": 0}
@@ -207,6 +209,167 @@ def _to_host(*tensors):
     return [h.numpy().copy() for h in outs]
 
 
+def _source_args(a, bound: _Bound) -> None:
+    """Fill the distance-source + bound-query fields of a jb_search_args."""
+    a.source = bound.kind
+    a.dims = bound.dims
+    if bound.kind == _lib.SRC_EXACT_U8:
+        a.data_u8, a.norms_u32 = _lib.ptr(bound.rows.x), _lib.ptr(bound.rows.norms)
+        a.queries_u8, a.query_norms_u32 = _lib.ptr(bound.rotated), _lib.ptr(bound.qadd)
+    elif bound.kind == _lib.SRC_EXACT:
+        a.data = _lib.ptr(bound.rows.x)
+        a.data_norms = _lib.ptr(bound.rows.norms)
+    else:
+        a.records = _lib.ptr(bound.records)
+        a.record_bytes = bound.record_bytes
+        a.bits = bound.bits
+    a.queries = _lib.ptr(bound.rotated)
+    a.query_add = _lib.ptr(bound.qadd)
+    a.query_sumq = _lib.ptr(bound.qsumq)
+
+
+def _pack_keys(dists, ids, is_integer: bool) -> np.ndarray:
+    """search.py:139-145: (f32 bits of max(d, 0) | integer distance) << 32 | id."""
+    dists = np.asarray(dists)
+    if is_integer:
+        hi = dists.astype(np.uint64)
+    else:
+        hi = np.maximum(dists.astype(np.float32, copy=False), np.float32(0.0)).view(np.uint32).astype(np.uint64)
+    return (hi << np.uint64(32)) | np.asarray(ids).astype(np.uint64)
+
+
+def _decode_keys(keys, is_integer: bool) -> np.ndarray:
+    """search.py:148-152."""
+    hi = np.asarray(keys, dtype=np.uint64) >> np.uint64(32)
+    if is_integer:
+        return hi.astype(np.float64)
+    return hi.astype(np.uint32).view(np.float32).astype(np.float64)
+
+
+class BoundDistances:
+    """A distance source bound to a query block (search.py:133-156 `_BoundExact`,
+    rabitq.py:225-254 `_BoundQuantized`), held in HBM: `distances(qrows, ids)` is
+    one jb_bound_distances launch in the search kernel's rounding (exact A1 f32,
+    exact integers for u8 rows, the reference RaBitQ estimator)."""
+
+    def __init__(self, source, queries, *, u8: bool | None = None):
+        u8 = _is_u8(source) if u8 is None else u8
+        q_dev = _queries_to_device(queries, u8)
+        self._bound = _Bound(source, q_dev)
+        self.source = source
+        self.is_integer = self._bound.kind == _lib.SRC_EXACT_U8
+        self.n_queries = int(q_dev.shape[0])
+        self._padded = None
+
+    def distances_device(self, qrows, ids):
+        """Device tensors in, device tensor out (f32, or int64 for u8 rows)."""
+        torch = _lib.require_cuda()
+        qr = torch.as_tensor(qrows, dtype=torch.int64).reshape(-1).to("cuda")
+        ii = torch.as_tensor(ids, dtype=torch.int64).reshape(-1).to("cuda")
+        if qr.numel() != ii.numel():
+            raise ValueError("qrows and ids length mismatch")
+        n = int(ii.numel())
+        if n:
+            lo = torch.stack([qr.min(), ii.min()]).cpu()
+            hi = torch.stack([qr.max(), ii.max()]).cpu()
+            if lo.min() < 0 or int(hi[0]) >= self.n_queries or int(hi[1]) >= self._bound.count:
+                raise IndexError("query row or vector id out of range")
+        out = torch.empty(n, dtype=torch.int32 if self.is_integer else torch.float32, device="cuda")
+        a = _lib.SearchArgs()
+        _source_args(a, self._bound)
+        stride = 0
+        if self._bound.kind in (_lib.SRC_RABITQ, _lib.SRC_EXACT_U8):
+            # the estimator / u8 dot read 16-byte words of the query row: pad the row stride
+            D = self._bound.dims
+            stride = (D + 15) // 16 * 16 if self.is_integer else (D + 3) // 4 * 4
+            if stride != D:
+                if self._padded is None:
+                    src = self._bound.rotated
+                    self._padded = torch.zeros((src.shape[0], stride), dtype=src.dtype, device=src.device)
+                    self._padded[:, :D] = src
+                if self.is_integer:
+                    a.queries_u8 = _lib.ptr(self._padded)
+                else:
+                    a.queries = _lib.ptr(self._padded)
+        _lib.check(_lib.lib().jb_bound_distances(_lib.C.byref(a), stride, _lib.ptr(qr), _lib.ptr(ii), n,
+                                                 _lib.ptr(out), _lib.stream_ptr()))
+        if self.is_integer:  # u32 distances (D * 255^2 < 2^32) -> int64 like the reference
+            return out.to(torch.int64) & 0xFFFFFFFF
+        return out
+
+    def distances(self, qrows, ids) -> np.ndarray:
+        """search.py:121-130 / rabitq.py:235-244: f32 (clamped at 0), or int64 for u8 rows."""
+        qrows = np.asarray(qrows, dtype=np.int64)
+        ids = np.asarray(ids, dtype=np.int64)
+        shape = np.broadcast_shapes(qrows.shape, ids.shape)
+        qrows, ids = np.broadcast_to(qrows, shape), np.broadcast_to(ids, shape)
+        return self.distances_device(np.ascontiguousarray(qrows), np.ascontiguousarray(ids)).cpu().numpy().reshape(
+            shape)
+
+    def pack(self, dists, ids) -> np.ndarray:
+        return _pack_keys(dists, ids, self.is_integer)
+
+    def decode(self, keys) -> np.ndarray:
+        return _decode_keys(keys, self.is_integer)
+
+
+class ExactDistances:
+    """search.py:82-116: squared distances over raw vectors; `bind(queries)` -> BoundDistances."""
+
+    def __init__(self, dataset):
+        self.dataset = as_dataset(dataset)
+        self.is_integer = self.dataset.element_kind is ElementKind.U8
+        if self.is_integer and self.dataset.dims * 255 ** 2 >= 1 << 32:
+            raise ValueError("u8 dims too large for 32-bit packed distances")
+
+    def bind(self, queries) -> BoundDistances:
+        q = np.atleast_2d(np.asarray(queries)) if not _is_tensor(queries) else queries
+        if q.shape[-1] != self.dataset.dims:
+            raise ValueError(f"query dims {q.shape[-1]} != dataset dims {self.dataset.dims}")
+        return BoundDistances(self.dataset, q, u8=self.is_integer)
+
+
+def _is_tensor(x) -> bool:
+    return type(x).__module__.startswith("torch")
+
+
+def bind_distance_source(source, queries) -> BoundDistances:
+    """search.py:159-168: bind a dataset or a quantized index to a query block."""
+    if isinstance(source, VectorDataset) or (hasattr(source, "element_kind") and hasattr(source, "data")
+                                             and not _is_rabitq(source)):
+        return ExactDistances(source).bind(queries)
+    if _is_rabitq(source):
+        from .rabitq import as_rabitq
+
+        return as_rabitq(source).bind(queries)
+    raise TypeError(f"unsupported distance source {type(source).__name__}")
+
+
+def _check_counts(graph: GraphIndex, source, exact_data=None, rerank: bool = False) -> None:
+    """The kernels read records/rows by id: a source (or rerank rows) shorter than
+    the graph's active vertices would be read out of bounds. The reference raises
+    IndexError from codes[ids] / data[ids]; this raises before any launch."""
+    n = as_rabitq_count(source)
+    if n < graph.active_count:
+        raise ValueError(f"distance source holds {n} vectors but the graph has {graph.active_count} active")
+    if rerank and exact_data is not None and as_dataset(exact_data).count < graph.active_count:
+        raise ValueError(f"exact_data holds {as_dataset(exact_data).count} rows but the graph has "
+                         f"{graph.active_count} active")
+
+
+def as_rabitq_count(source) -> int:
+    if _is_rabitq(source):
+        return int(np.asarray(source.codes).shape[0])
+    return as_dataset(source).count
+
+
+def _rerank_rows(exact_data):
+    """f32 rows for the exact rerank: u8 rows are widened exactly (the reference's
+    data[ids].astype(f32), search.py:318-320)."""
+    ds = as_dataset(exact_data)
+    return ds.device_f32(), ds.dims
+
+
 def _launch(graph: GraphIndex, bound: _Bound, L: int, starts_dev=None, trace_cap: int = 0, out=None):
     torch = _lib.require_cuda()
     nq = bound.q_dev.shape[0]
@@ -224,21 +387,7 @@ def _launch(graph: GraphIndex, bound: _Bound, L: int, starts_dev=None, trace_cap
     a.adjacency = _lib.ptr(adj)
     a.degree_cap = graph.degree_cap
     a.active_count = graph.active_count
-    a.source = bound.kind
-    a.dims = bound.dims
-    if bound.kind == _lib.SRC_EXACT_U8:
-        a.data_u8, a.norms_u32 = _lib.ptr(bound.rows.x), _lib.ptr(bound.rows.norms)
-        a.queries_u8, a.query_norms_u32 = _lib.ptr(bound.rotated), _lib.ptr(bound.qadd)
-    elif bound.kind == _lib.SRC_EXACT:
-        a.data = _lib.ptr(bound.rows.x)
-        a.data_norms = _lib.ptr(bound.rows.norms)
-    else:
-        a.records = _lib.ptr(bound.records)
-        a.record_bytes = bound.record_bytes
-        a.bits = bound.bits
-    a.queries = _lib.ptr(bound.rotated)
-    a.query_add = _lib.ptr(bound.qadd)
-    a.query_sumq = _lib.ptr(bound.qsumq)
+    _source_args(a, bound)
     a.nq = nq
     a.starts = _lib.ptr(starts_dev)
     a.start_vertex = graph.entry_point
@@ -260,6 +409,8 @@ def _validate(graph: GraphIndex, beam_width: int):
         raise ValueError("search on an empty graph")
     if not 1 <= beam_width <= MAX_BEAM_WIDTH:
         raise ValueError(f"beam_width must be in [1, {MAX_BEAM_WIDTH}]")
+    if graph.degree_cap > MAX_DEGREE_CAP:
+        raise ValueError(f"degree_cap {graph.degree_cap} exceeds the search kernel's limit {MAX_DEGREE_CAP}")
 
 
 def _starts(graph: GraphIndex, starts, nq: int):
@@ -276,6 +427,7 @@ def run_beam_searches(graph, source, queries, beam_width: int, starts=None) -> l
     """search.py:272-304: one SearchResult (frontier + visited trace + stats) per query row."""
     graph = as_graph(graph)
     _validate(graph, beam_width)
+    _check_counts(graph, source)
     u8 = _is_u8(source)
     q_dev = _queries_to_device(queries, u8)
     nq = q_dev.shape[0]
@@ -307,7 +459,7 @@ def run_beam_searches(graph, source, queries, beam_width: int, starts=None) -> l
         # The visited table evicted ids for these queries, so the device counted some
         # re-evaluations. The reference's count is |{start} U N(u) over expanded u|
         # (every valid neighbour of an expanded vertex is evaluated exactly once).
-        adj = graph.adjacency
+        adj = graph.host_adjacency()
         st = np.full(nq, graph.entry_point, dtype=np.int64) if starts is None else \
             np.broadcast_to(np.asarray(starts, dtype=np.int64), (nq,))
         for i in lossy:
@@ -354,6 +506,7 @@ def _knn_device(graph: GraphIndex, source, q_dev, params: SearchParams, exact_da
     rerank = params.rerank and _is_rabitq(source)
     if rerank and exact_data is None:
         raise ValueError("rerank over a quantized source requires exact_data")
+    _check_counts(graph, source, exact_data, rerank)
     bound = _Bound(source, q_dev, params.estimator)
     L, k = params.beam_width, params.k
     fk, *_ = _launch(graph, bound, L, starts_dev, 0)
@@ -363,10 +516,10 @@ def _knn_device(graph: GraphIndex, source, q_dev, params: SearchParams, exact_da
         return ids, dists
     st = _lib.stream_ptr()
     if rerank:
-        rows = as_dataset(exact_data).device()
-        if rows.dims != q_dev.shape[1]:
-            raise ValueError(f"query dims {q_dev.shape[1]} != dataset dims {rows.dims}")
-        _lib.check(_lib.lib().jb_rerank_topk(_lib.ptr(rows.x), rows.dims, _lib.ptr(q_dev), nq, _lib.ptr(fk), L, k,
+        rows, rdims = _rerank_rows(exact_data)
+        if rdims != q_dev.shape[1]:
+            raise ValueError(f"query dims {q_dev.shape[1]} != dataset dims {rdims}")
+        _lib.check(_lib.lib().jb_rerank_topk(_lib.ptr(rows), rdims, _lib.ptr(q_dev), nq, _lib.ptr(fk), L, k,
                                              _lib.ptr(ids), _lib.ptr(dists), st))
     else:
         fn = _lib.lib().jb_frontier_topk_u8 if bound.kind == _lib.SRC_EXACT_U8 else _lib.lib().jb_frontier_topk
@@ -414,6 +567,7 @@ PIPELINE = {"chunk": 0, "device_chunk": 0}
 
 def _knn_plan(graph: GraphIndex, source, D: int, params: SearchParams, exact_data=None):
     """jb_knn_plan for jb_search_knn_host: graph + distance source as device pointers."""
+    _check_counts(graph, source, exact_data, params.rerank and _is_rabitq(source))
     adj, _ = graph.device()
     plan = _lib.KnnPlan()
     a = plan.search
@@ -439,10 +593,10 @@ def _knn_plan(graph: GraphIndex, source, D: int, params: SearchParams, exact_dat
             a.records, a.record_bytes = _lib.ptr(pl), pb
         plan.centroid, plan.rotation = _lib.ptr(dev.centroid), _lib.ptr(dev.rotation)
         if params.rerank:
-            rows = as_dataset(exact_data).device()
-            if rows.dims != D:
-                raise ValueError(f"query dims {D} != dataset dims {rows.dims}")
-            plan.rerank_data = _lib.ptr(rows.x)
+            rows, rdims = _rerank_rows(exact_data)
+            if rdims != D:
+                raise ValueError(f"query dims {D} != dataset dims {rdims}")
+            plan.rerank_data = _lib.ptr(rows)
     else:
         ds = as_dataset(source)
         if D != ds.dims:

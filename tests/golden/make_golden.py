@@ -146,6 +146,46 @@ def c1_graph():
         json.dump(out, fh, indent=1)
 
 
+def bench_rabitq():
+    """11. The bench workload's RaBitQ fit + query bind at full size (1M x 128 m=1): hashes only
+    (bench_rabitq.json). Rows from workload.lowrank (the generator both bench arms use)."""
+    import hashlib
+    import json
+
+    sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
+    import workload
+
+    x = workload.lowrank(1_000_000, 128, seed=1, d_int=16, noise=0.05, basis_seed=0)
+    q = workload.lowrank(10_000, 128, seed=1_000_003, d_int=16, noise=0.05, basis_seed=0)
+    t = time.time()
+    idx = ref.rabitq_fit(ref.VectorDataset(x), bits=1, seed=1)
+    b = idx.bind(q)
+    sha = lambda a: hashlib.sha1(np.ascontiguousarray(a).tobytes()).hexdigest()  # noqa: E731
+    out = {"what": "reference (beamann) rabitq_fit(bits=1, seed=1) of the bench index rows gen_lowrank(1000000, 128, "
+                   "seed=1, d_int=16, noise=0.05, basis_seed=0) and bind() of its 10000 queries gen_lowrank(10000, "
+                   "128, seed=1000003, ...): SHA-1 of codes, meta, centroid, rotated queries, query_add, query_sumq",
+           "made_by": f"tests/golden/make_golden.py bench_rabitq (beamann.rabitq_fit + RaBitQIndex.bind, "
+                      f"{time.time() - t:.1f} s)",
+           "codes": sha(idx.codes), "meta": sha(idx.meta), "centroid": sha(idx.centroid),
+           "rotated": sha(b._rotated), "qadd": sha(b._qadd), "sumq": sha(b._qsumq)}
+    with open(os.path.join(HERE, "bench_rabitq.json"), "w") as fh:
+        json.dump(out, fh, indent=1)
+        fh.write("\n")
+
+
+def persistence():
+    """12. Byte-exact files written by the reference's own writers (graph.py:101-117,
+    rabitq.py:183-192): graph.bin of the g33 build and rabitq.bin of an m=4 fit."""
+    data33 = ref.gen_synthetic(800, 33, seed=5).data
+    g = ref.build(ref.VectorDataset(data33), ref.BuildParams(degree_cap=8, build_beam_width=16, alpha=1.3))
+    g.save(os.path.join(HERE, "graph_g33.bin"))
+    x = ref.gen_synthetic(300, 40, seed=71).data
+    idx = ref.rabitq_fit(ref.VectorDataset(x), bits=4, seed=72)
+    idx.save(os.path.join(HERE, "rabitq_m4.bin"))
+    for f in ("graph_g33.bin", "rabitq_m4.bin"):
+        print(f"wrote {f} ({os.path.getsize(os.path.join(HERE, f))} B)")
+
+
 def main():
     # 1. exact search + build on a small Gaussian graph (D=32, R=16, L=32)
     data = ref.gen_synthetic(3000, 32, seed=0).data

@@ -35,7 +35,8 @@ def test_pack_unpack_round_trip_and_storage(bits):
 
 def _estimates(idx, q):
     """Host restatement of the estimator (rabitq.py:235-244) from the device bind."""
-    rot, qa, qs = idx.bind(q[None, :])
+    b = idx.bind(q[None, :])
+    rot, qa, qs = b.rotated, b.query_add, b.query_sumq
     u = jb.rabitq.unpack_codes(idx.codes, idx.bits, idx.dims).astype(np.float32)
     dd = u @ rot[0]
     return qa[0] + idx.meta[:, 0] + idx.meta[:, 1] * (dd - qs[0])

@@ -201,7 +201,8 @@ def test_rabitq_fit_and_bind_bit_exact(bits):
     np.testing.assert_array_equal(idx.centroid, f[f"m{bits}_centroid"])
     np.testing.assert_array_equal(idx.codes, f[f"m{bits}_codes"])
     np.testing.assert_array_equal(idx.meta.view(np.uint32), f[f"m{bits}_meta"].view(np.uint32))
-    rot, qadd, sumq = idx.bind(qq)
+    b = idx.bind(qq)
+    rot, qadd, sumq = b.rotated, b.query_add, b.query_sumq
     np.testing.assert_array_equal(rot, f[f"m{bits}_rotated"])
     np.testing.assert_array_equal(qadd, f[f"m{bits}_qadd"])
     np.testing.assert_array_equal(sumq, f[f"m{bits}_sumq"])
@@ -435,7 +436,8 @@ def test_bench_scale_rabitq_fit_and_bind_identical_to_reference():
     assert h(idx.centroid) == ref["centroid"]
     assert h(idx.codes) == ref["codes"]
     assert h(idx.meta) == ref["meta"]
-    rot, qa, qs = idx.bind(q)
+    b = idx.bind(q)
+    rot, qa, qs = b.rotated, b.query_add, b.query_sumq
     assert (h(rot), h(qa), h(qs)) == (ref["rotated"], ref["qadd"], ref["sumq"])
 
 
