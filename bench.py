@@ -60,6 +60,9 @@ def _args():
     p.add_argument("--steps", type=int, default=10)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    p.add_argument("--config", default="c2", choices=["c2", "c5"],
+                   help="c2: BASELINE configs[1] (1M x 128 per shard, RaBitQ-1); c5: configs[4], one 12.5M x 96 "
+                        "shard of the 100M x 96 index per GPU (RaBitQ-4 + rerank)")
     p.add_argument("--shard-rows", dest="n", type=int, default=1_000_000, help="vectors per shard (GPU)")
     p.add_argument("--queries", dest="nq", type=int, default=10_000)
     p.add_argument("--dim", type=int, default=128)
@@ -75,7 +78,15 @@ def _args():
     p.add_argument("--hash-slots", type=int, default=0, help="visited-table slots per query (0 = library default)")
     p.add_argument("--estimator", default="auto", choices=["auto", "reference", "popcount"],
                    help="RaBitQ estimator; auto times both and reports the faster at the recall target")
-    return p.parse_args()
+    a = p.parse_args()
+    if a.config == "c5":
+        # DEEP-shaped 100M x 96 sharded over 8 GPUs: 12.5M rows per shard (BASELINE configs[4])
+        a.n = a.n if a.n != 1_000_000 else 12_500_000
+        a.dim = 96 if a.dim == 128 else a.dim
+        a.bits = 4 if a.bits == 1 else a.bits
+        a.stream = 0
+        a.no_cpu = True
+    return a
 
 
 # ---------------------------------------------------------------------------
@@ -119,7 +130,8 @@ def _recall(ids, gt_i, gt_d, k):
 
 def _config(args, world, L):
     """Identical in both arms (same workload, same L*)."""
-    return {"workload": f"SIFT-1M-shaped synthetic {args.n}x{args.dim} low-rank (d_int=16, noise 0.05) "
+    shape = "SIFT-1M-shaped" if args.config == "c2" else f"DEEP-100M-shaped (one shard of {8 * args.n} at 8 GPUs)"
+    return {"workload": f"{shape} synthetic {args.n}x{args.dim} low-rank (d_int=16, noise 0.05) "
                         f"per shard, RaBitQ {args.bits}-bit + fp32 rerank, {args.nq} queries, k={args.k}",
             "index": dict(INDEX), "beam_width": L, "shards": world, "parallelism": f"shard{world}",
             "l2": "flushed between timed steps (256 MB write, outside the events)"}
@@ -406,6 +418,15 @@ def _dist():
     return world, rank, local
 
 
+def _gt_device(x_dev, q_dev, k: int):
+    """Exact top-k ground truth on the GPU (jb_exact_knn: f64 scores, ties by id,
+    oracle.exact_knn semantics) as (int64 ids, f64 dists) tensors. Measurement only."""
+    import paper_2601_07048_b200 as jb
+
+    i, d = jb.measure.exact_knn_device(x_dev, q_dev, k)
+    return i.long(), d.double()
+
+
 def _setup(args, world, rank):
     """Data, device build, RaBitQ fit, ground truth (merged across shards)."""
     import importlib
@@ -440,8 +461,8 @@ def _setup(args, world, rank):
     torch.cuda.synchronize()
     t_fit = time.perf_counter() - t0
     q_dev = torch.from_numpy(q).cuda()
-    gt_i, gt_d = jb.measure.exact_knn_device(ds.device().x, q_dev, 100)
-    gt_i, gt_d = gt_i.long() + shard_start, gt_d.double()
+    gt_i, gt_d = _gt_device(ds.device().x, q_dev, 100)
+    gt_i = gt_i + shard_start
     if world > 1:
         from paper_2601_07048_b200 import comm
 

@@ -175,6 +175,7 @@ __device__ int warp_prune_split(uint64_t* cand, int n, double alpha2, int R, con
             bool live = false;
             if (j < s) { i = lst[j]; live = cand[i] != UMAX; }
             const unsigned msk = __ballot_sync(FULL, live);
+            __syncwarp();  // every lane's read of this chunk precedes the writes below (WAR)
             if (live) lst[ns + __popc(msk & lanemask_lt())] = (uint16_t)i;
             ns += __popc(msk);
             __syncwarp();

@@ -92,15 +92,31 @@ __host__ __device__ constexpr SearchLayout make_layout(int src, int D, int L, in
 
 // Visited table: 4-way set-associative buckets of ids in smem, one 16 B load per
 // probe. A miss inserts into the first empty way, else evicts a pseudo-random way.
-// No atomics: two lanes racing for one way can only drop an insert. Every outcome
-// is "lossy but safe": an id is never reported seen unless it was evaluated, and a
-// forgotten id is re-evaluated to the same key, which the merge drops (dedupe or
-// beam-worst filter), so frontier and trace stay exact. `lossy` records evictions.
+// No atomics: the lanes of one warp probe and insert concurrently, so two lanes
+// whose ids hash to one bucket may read it while the other writes (RAW) and may
+// both claim the same empty way (WAW). These races are intended and harmless:
+//  * the bucket load and the slot store are volatile (PTX relaxed, morally
+//    strong) 32-bit accesses, so a racing read returns the old or the new word
+//    and a racing write leaves exactly one of the written ids — never a torn or
+//    invented value;
+//  * every id written in a hop is an id evaluated in that hop (a lane writes only
+//    after deciding its own id is new), so whichever write survives, the table
+//    never reports an unevaluated id as seen (no false positive);
+//  * an id whose write lost (or was evicted later) is only forgotten: if it comes
+//    back it is re-evaluated to the same key, which the merge drops (equal-key
+//    dedupe, or the full beam's worst-key filter), so frontier and trace stay
+//    exact; the loser notices (re-read after __syncwarp) and flags `lossy`;
+//  * a racing reader's own id differs from the writers' ids (an adjacency row
+//    holds distinct ids), so what it reads only affects which way it picks.
+// compute-sanitizer racecheck reports exactly these two accesses.
 __device__ __forceinline__ bool visit(uint32_t* tab, int hbits, uint32_t id, int& lossy, uint32_t*& slot) {
     const uint32_t h = id * 0x9E3779B1u;
     const uint32_t b = h >> (32 - hbits);
     uint4* bucket = reinterpret_cast<uint4*>(tab) + b;
-    const uint4 v = *bucket;
+    uint4 v;
+    asm volatile("ld.volatile.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "r"((uint32_t)__cvta_generic_to_shared(bucket)));
     slot = nullptr;
     if (v.x == id || v.y == id || v.z == id || v.w == id) return false;
     int way;
@@ -110,7 +126,8 @@ __device__ __forceinline__ bool visit(uint32_t* tab, int hbits, uint32_t id, int
     else if (v.w == EMPTY_SLOT) way = 3;
     else { way = (h >> 3) & 3; lossy = 1; }
     slot = reinterpret_cast<uint32_t*>(bucket) + way;
-    *slot = id;
+    asm volatile("st.volatile.shared.u32 [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(slot)), "r"(id)
+                 : "memory");
     return true;
 }
 
@@ -361,7 +378,7 @@ __device__ __forceinline__ uint64_t eval_chunk(const jb_search_args& a, const Se
     __syncwarp();
     // two lanes may have claimed the same empty way: the loser's id is
     // forgotten (safe, but it may be re-evaluated later -> flag it)
-    if (slot != nullptr && *slot != (uint32_t)nb) lossy = 1;
+    if (slot != nullptr && *reinterpret_cast<volatile uint32_t*>(slot) != (uint32_t)nb) lossy = 1;
     const uint32_t nm = __ballot_sync(FULL, isnew);
     const int nnew = __popc(nm);
     if (nnew == 0) return UMAX;

@@ -357,9 +357,16 @@ def _prune_source(dist_fn, dataset):
     x = getattr(dist_fn, "_x", None)  # beamann build._PairwiseDistances (build.py:105-134)
     if isinstance(x, np.ndarray) and x.ndim == 2:
         q = getattr(dist_fn, "_quantizer", None)
-        if x.dtype == np.int64:  # u8 rows widened by the reference
-            x = x.astype(np.uint8)
-        return x, q
+        ds = getattr(dist_fn, "_jb_dataset", None)  # HBM copy cached on the caller's object
+        if ds is None:
+            from .core import VectorDataset
+
+            ds = VectorDataset(x.astype(np.uint8) if x.dtype == np.int64 else x)  # u8 rows widened by the reference
+            try:
+                setattr(dist_fn, "_jb_dataset", ds)
+            except AttributeError:
+                pass
+        return ds, q
     return None, None
 
 

@@ -380,9 +380,9 @@ def _launch(graph: GraphIndex, bound: _Bound, L: int, starts_dev=None, trace_cap
     evals = torch.empty(nq, dtype=torch.int32, device=dev)
     flags = torch.empty(nq, dtype=torch.int32, device=dev)
     tids = tdst = None
-    if trace_cap:
-        tids = torch.empty((nq, trace_cap), dtype=torch.int32, device=dev)
-        tdst = torch.empty((nq, trace_cap), dtype=torch.float32, device=dev)
+    if trace_cap:  # slots past a query's hop count stay -1 / 0 (defined when copied out whole)
+        tids = torch.full((nq, trace_cap), -1, dtype=torch.int32, device=dev)
+        tdst = torch.zeros((nq, trace_cap), dtype=torch.float32, device=dev)
     a = _lib.SearchArgs()
     a.adjacency = _lib.ptr(adj)
     a.degree_cap = graph.degree_cap
