@@ -230,7 +230,9 @@ typedef struct jb_insert_args {
                                     * (may be NULL): [0] phase-1 hops, [1] phase-1
                                     * distance evals, [2] phase-2 prune candidates,
                                     * [3] phase-3 touched targets, [4] reverse
-                                    * triples, [5] repair bridges                 */
+                                    * triples, [5] repair bridges, [6] stranded
+                                    * rows through the tensor-core donor screen,
+                                    * [7] of those rescanned exactly              */
     int64_t active_count;          /* jb_refine_batch: vertices visible to the
                                     * search (0 => stop); ignored elsewhere     */
     int32_t element_kind;          /* JB_KIND_F32 (data, data_norms) or

@@ -170,8 +170,10 @@ def _args(graph: GraphIndex, ds, params: BuildParams, start: int, stop: int, qua
 
 # Work counters accumulated over batch_insert calls (jb_insert_args.stats_out_host):
 # phase-1 hops / distance evals, phase-2 prune candidates, phase-3 touched targets,
-# reverse triples, repair bridges. Read by bench.py for the insert roofline.
-WORK_FIELDS = ("search_hops", "search_evals", "prune_candidates", "merge_targets", "reverse_triples", "bridges")
+# reverse triples, repair bridges, stranded rows through the tensor-core donor
+# screen and those rescanned exactly. Read by bench.py for the insert roofline.
+WORK_FIELDS = ("search_hops", "search_evals", "prune_candidates", "merge_targets", "reverse_triples", "bridges",
+               "donor_tc_rows", "donor_tc_redo")
 WORK = np.zeros(8, dtype=np.int64)
 
 

@@ -27,6 +27,7 @@
 #include "common.cuh"
 #include "metric.cuh"
 #include "runtime.cuh"
+#include "donor_tc.cuh"
 
 namespace jb {
 
@@ -1584,21 +1585,55 @@ static int repair(const M& m, const jb_insert_args& a, int64_t n_active, int64_t
             slices = 1;
             const int rc = approx_donors(a, lost, nlost, n_active, entry, fan, bufs, st, part);
             if (rc != JB_OK) return rc;
-        } else if (std::is_same<M, F32Metric>::value) {  // tiled A1 scan on the f32 rows
-            const bool res = D <= 256;
-            const int sblocks = (nlost + DT - 1) / DT;
-            slices = std::max(1, std::min(128, 4 * sm_count_current() / sblocks));  // whole waves at 2 blocks/SM
-            slices = (int)std::min<int64_t>(slices, std::max<int64_t>(1, (nreach + DT - 1) / DT));
-            part = bufs.get<uint64_t>((size_t)slices * nlost * fan, st, _ce); JB_CUDA(_ce);
-            const size_t dsm = (size_t)(DT * (res ? D + 1 : 17) + DT * 17 + DT * (DT + 1) + 1) * 4 + DT * FAN * 8;
-            if (res) {
-                JB_CUDA_RC(grow_smem(donor_scan_kernel<true>, (int)dsm));
-                donor_scan_kernel<true><<<dim3(sblocks, slices), 256, dsm, st>>>(a.data, a.data_norms, D, lost, nlost,
-                                                                                reach, nreach, slices, fan, part);
+        } else if (std::is_same<M, F32Metric>::value) {
+            // tiled A1 scan on the f32 rows of `ls` (n stranded) -> sl slices of partial top lists
+            auto exact_scan = [&](const int32_t* ls, int n, uint64_t*& pt, int& sl) -> int {
+                const bool res = D <= 256;
+                const int sblocks = (n + DT - 1) / DT;
+                sl = std::max(1, std::min(128, 4 * sm_count_current() / sblocks));  // whole waves at 2 blocks/SM
+                sl = (int)std::min<int64_t>(sl, std::max<int64_t>(1, (nreach + DT - 1) / DT));
+                pt = bufs.get<uint64_t>((size_t)sl * n * fan, st, _ce); JB_CUDA(_ce);
+                const size_t dsm = (size_t)(DT * (res ? D + 1 : 17) + DT * 17 + DT * (DT + 1) + 1) * 4 + DT * FAN * 8;
+                if (res) {
+                    JB_CUDA_RC(grow_smem(donor_scan_kernel<true>, (int)dsm));
+                    donor_scan_kernel<true><<<dim3(sblocks, sl), 256, dsm, st>>>(a.data, a.data_norms, D, ls, n, reach,
+                                                                                nreach, sl, fan, pt);
+                } else {
+                    JB_CUDA_RC(grow_smem(donor_scan_kernel<false>, (int)dsm));
+                    donor_scan_kernel<false><<<dim3(sblocks, sl), 256, dsm, st>>>(a.data, a.data_norms, D, ls, n, reach,
+                                                                                 nreach, sl, fan, pt);
+                }
+                JB_LAUNCH_CHECK();
+                return JB_OK;
+            };
+            if (donor_tc_supported(D, n_active)) {
+                // tensor-core screen + exact re-rank (donor_tc.cu); uncertified rows rescanned exactly
+                slices = 1;
+                part = bufs.get<uint64_t>((size_t)nlost * fan, st, _ce); JB_CUDA(_ce);
+                BALLOC(redo, int32_t, nlost);
+                BALLOC(nredo, int, 1);
+                JB_CUDA_RC(donor_scan_tc(a.data, a.data_norms, D, a.adjacency, R, seen, n_active, lost, nlost, fan, part,
+                                         redo, nredo, st));
+                int hredo = 0;
+                JB_CUDA(cudaMemcpyAsync(&hredo, nredo, sizeof(int), cudaMemcpyDeviceToHost, st));
+                JB_CUDA(cudaStreamSynchronize(st));
+                if (getenv("JB_PROFILE") && getenv("JB_PROFILE")[0] == '1')
+                    fprintf(stderr, "[jb]   tensor-core donor screen: %d of %d stranded rows rescanned exactly\n", hredo,
+                            nlost);
+                if (a.stats_out_host) {
+                    a.stats_out_host[6] += nlost;
+                    a.stats_out_host[7] += hredo;
+                }
+                if (hredo > 0) {
+                    BALLOC(lost2, int32_t, hredo);
+                    JB_CUDA_RC(donor_redo_ids(lost, redo, hredo, lost2, st));
+                    uint64_t* part2;
+                    int sl2;
+                    JB_CUDA_RC(exact_scan(lost2, hredo, part2, sl2));
+                    JB_CUDA_RC(donor_redo_merge(part2, sl2, hredo, fan, redo, part, st));
+                }
             } else {
-                JB_CUDA_RC(grow_smem(donor_scan_kernel<false>, (int)dsm));
-                donor_scan_kernel<false><<<dim3(sblocks, slices), 256, dsm, st>>>(a.data, a.data_norms, D, lost, nlost,
-                                                                                 reach, nreach, slices, fan, part);
+                JB_CUDA_RC(exact_scan(lost, nlost, part, slices));
             }
         } else {
             const int sblocks = (nlost + 7) / 8;
