@@ -64,6 +64,8 @@ def _args():
                    help="c2: BASELINE configs[1] (1M x 128 per shard, RaBitQ-1); c5: configs[4], one 12.5M x 96 "
                         "shard of the 100M x 96 index per GPU (RaBitQ-4 + rerank)")
     p.add_argument("--shard-rows", dest="n", type=int, default=1_000_000, help="vectors per shard (GPU)")
+    p.add_argument("--data", default="lowrank", choices=["lowrank", "gaussian"],
+                   help="synthetic rows: low-rank (default) or the reference's iid Gaussian gen_synthetic")
     p.add_argument("--queries", dest="nq", type=int, default=10_000)
     p.add_argument("--dim", type=int, default=128)
     p.add_argument("--k", type=int, default=10)
@@ -94,12 +96,16 @@ def _args():
 
 
 def _data(args, rank: int = 0):
+    if args.data == "gaussian":  # the reference's gen_synthetic rows (core.py:209-233)
+        return workload.gaussian(args.n, args.dim, 1 + rank), workload.gaussian(args.nq, args.dim, 1_000_003)
     x = workload.lowrank(args.n, args.dim, seed=1 + rank, d_int=16, noise=0.05, basis_seed=0)
     q = workload.lowrank(args.nq, args.dim, seed=1_000_003, d_int=16, noise=0.05, basis_seed=0)
     return x, q
 
 
 def _stream_rows(args):
+    if args.data == "gaussian":
+        return workload.gaussian(args.stream, args.dim, 777_001)
     return workload.lowrank(args.stream, args.dim, seed=777_001, d_int=16, noise=0.05, basis_seed=0)
 
 
@@ -131,7 +137,8 @@ def _recall(ids, gt_i, gt_d, k):
 def _config(args, world, L):
     """Identical in both arms (same workload, same L*)."""
     shape = "SIFT-1M-shaped" if args.config == "c2" else f"DEEP-100M-shaped (one shard of {8 * args.n} at 8 GPUs)"
-    return {"workload": f"{shape} synthetic {args.n}x{args.dim} low-rank (d_int=16, noise 0.05) "
+    rows = "iid Gaussian" if args.data == "gaussian" else "low-rank (d_int=16, noise 0.05)"
+    return {"workload": f"{shape} synthetic {args.n}x{args.dim} {rows} "
                         f"per shard, RaBitQ {args.bits}-bit + fp32 rerank, {args.nq} queries, k={args.k}",
             "index": dict(INDEX), "beam_width": L, "shards": world, "parallelism": f"shard{world}",
             "l2": "flushed between timed steps (256 MB write, outside the events)"}

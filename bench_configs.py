@@ -68,9 +68,10 @@ def c1(args):
     x = jb.gen_synthetic(args.n or 100_000, 128, seed=0).data
     q = jb.gen_synthetic(10_000, 128, seed=1).data
     ds = jb.VectorDataset(x)
-    _warm_build(jb, x, jb.BuildParams(degree_cap=32, build_beam_width=64, alpha=1.2))
+    R, Lb = args.R or 32, args.lbuild or 64
+    _warm_build(jb, x, jb.BuildParams(degree_cap=R, build_beam_width=Lb, alpha=1.2))
     t0 = time.perf_counter()
-    g = jb.build(ds, jb.BuildParams(degree_cap=32, build_beam_width=64, alpha=1.2))
+    g = jb.build(ds, jb.BuildParams(degree_cap=R, build_beam_width=Lb, alpha=1.2))
     torch.cuda.synchronize()
     t_build = time.perf_counter() - t0
     q_dev = torch.from_numpy(q).cuda()
@@ -109,9 +110,10 @@ def c3(args):
     x = jb.gen_lowrank(n, 960, seed=1, d_int=dint, noise=0.05, basis_seed=0)
     q = jb.gen_lowrank(10_000, 960, seed=1_000_003, d_int=dint, noise=0.05, basis_seed=0)
     ds = jb.VectorDataset(x)
-    _warm_build(jb, x, jb.BuildParams(degree_cap=32, build_beam_width=64, alpha=1.2))
+    R, Lb = args.R or 32, args.lbuild or 64
+    _warm_build(jb, x, jb.BuildParams(degree_cap=R, build_beam_width=Lb, alpha=1.2))
     t0 = time.perf_counter()
-    g = jb.build(ds, jb.BuildParams(degree_cap=32, build_beam_width=64, alpha=1.2))
+    g = jb.build(ds, jb.BuildParams(degree_cap=R, build_beam_width=Lb, alpha=1.2))
     torch.cuda.synchronize()
     t_build = time.perf_counter() - t0
     t0 = time.perf_counter()
@@ -121,7 +123,8 @@ def c3(args):
     q_dev = torch.from_numpy(q).cuda()
     gi, gd = bench._gt_device(ds.device().x, q_dev, 100)
     gt = jb.GroundTruth(gi.cpu().numpy(), gd.cpu().numpy().astype(np.float32))
-    out = {"config": "c3", "n": n, "dims": 960, "d_int": dint, "bits": 4, "build_s": round(t_build, 2),
+    out = {"config": "c3", "n": n, "dims": 960, "d_int": dint, "R": R, "L_build": Lb, "bits": 4,
+           "build_s": round(t_build, 2),
            "inserts_per_s": round(n / t_build, 1), "rabitq_fit_s": round(t_fit, 3),
            "bytes_per_vector": {"f32": 3840, "rabitq_record": int(jb._lib.lib().jb_rabitq_record_bytes(960, 4))},
            "sweep": [], "sweep_popcount": []}
@@ -273,6 +276,8 @@ def main():
     p = argparse.ArgumentParser()
     p.add_argument("config", choices=["c1", "c3", "c4", "c5", "u8"])
     p.add_argument("--dint", type=int, default=0)
+    p.add_argument("--R", type=int, default=0, help="c3: degree cap (default 32)")
+    p.add_argument("--lbuild", type=int, default=0, help="c3: build beam width (default 64)")
     p.add_argument("--n", type=int, default=0)
     p.add_argument("--total", type=int, default=0)
     p.add_argument("--repair-beam", type=int, default=0,

@@ -256,6 +256,165 @@ __device__ int warp_prune_staged(uint64_t* cand, int n, double alpha2, int R, co
     return kept;
 }
 
+// ---- Gram-screened robust prune (f32 rows, staged, n <= GP_MAX) ---------------
+// Same extraction sequence and result as warp_prune_staged. The candidates are
+// ranked once by key (the extraction order of the reference's argmin loop,
+// graph.py:205-226: keys are distinct), and each round's alpha test
+//   remove c  iff  alpha^2 * d(p, c) <= d(t, c)          (graph.py:218, f64)
+// is first decided from a tensor-core Gram block: G[p][c] = <x_p, x_c> on tf32
+// mma.sync (m16n8k8, f32 accumulate) for the 16 ranked candidates of p's block
+// against all n. With d~ = |p|^2 + |c|^2 - 2 G and |d~ - d_A1(p, c)| <= E (|p|^2 + |c|^2)
+// (E = 2^-8: tf32 operands carry 2^-10 relative error, 2x margin as in donor_tc.cu),
+// the test is certain when alpha^2 (d~ - err) > d(t, c) (keep) or alpha^2 (d~ + err)
+// <= d(t, c) (remove); only the rest get the exact A1 distance. Per warp smem:
+// ranked index list (GP_MAX bytes) + one Gram block (16 x GP_MAX f32).
+// (A warp-level product: tcgen05's 128-row tiles and per-CTA issue do not fit a
+// per-warp 48 x 48 x D Gram; the exact A1 rounds it replaces were ~45% of the
+// owner merge's instructions.)
+constexpr int GP_MAX = 64;
+constexpr int GP_BYTES = GP_MAX + 16 * GP_MAX * 4;
+
+__device__ __forceinline__ void mma_tf32_16x8x8(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                                uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
+        "{%0, %1, %2, %3};"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+// Gram block of ranked positions [16 b, 16 b + 16) x [16 b, n): gb[i][c] (row stride GP_MAX).
+// Rows are staged with stride rs (natural or block-transposed: the same element
+// permutation in every row leaves dot products unchanged). D % 8 == 0.
+__device__ __forceinline__ void gram_block(const uint32_t* __restrict__ rows, int rs, int D, const uint8_t* rk, int n,
+                                           int b, float* __restrict__ gb) {
+    const int lane = lane_id(), g = lane >> 2, t = lane & 3;
+    const int r0 = 16 * b + g, r1 = r0 + 8;
+    const uint32_t* pa0 = rows + (size_t)rk[r0 < n ? r0 : 0] * rs + t;
+    const uint32_t* pa1 = rows + (size_t)rk[r1 < n ? r1 : 0] * rs + t;
+    const int j0 = 2 * b, nj = (n + 7) >> 3;  // column blocks of 8 (positions < 16 b are never tested)
+    float acc[GP_MAX / 8][4];
+    const uint32_t* pb[GP_MAX / 8];
+#pragma unroll
+    for (int j = 0; j < GP_MAX / 8; ++j) {
+        acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
+        const int c = 8 * j + g;
+        pb[j] = rows + (size_t)rk[c < n ? c : 0] * rs + t;
+    }
+    for (int k = 0; k < D; k += 8) {
+        const uint32_t a0 = pa0[k], a1 = pa1[k], a2 = pa0[k + 4], a3 = pa1[k + 4];
+#pragma unroll
+        for (int j = 0; j < GP_MAX / 8; ++j)
+            if (j >= j0 && j < nj) mma_tf32_16x8x8(acc[j], a0, a1, a2, a3, pb[j][k], pb[j][k + 4]);
+    }
+#pragma unroll
+    for (int j = 0; j < GP_MAX / 8; ++j) {
+        if (j >= j0 && j < nj) {
+            *reinterpret_cast<float2*>(gb + g * GP_MAX + 8 * j + 2 * t) = make_float2(acc[j][0], acc[j][1]);
+            *reinterpret_cast<float2*>(gb + (g + 8) * GP_MAX + 8 * j + 2 * t) = make_float2(acc[j][2], acc[j][3]);
+        }
+    }
+}
+
+// exact A1 dot of staged rows i and p (per lane; natural or block-transposed layout)
+__device__ __forceinline__ float staged_dot(const F32Metric& m, const uint32_t* rows, int i, int p) {
+    const int rs = m.stage_stride_words();
+    if (m.split_ok()) {  // transposed 16-blocks: float4 k of a block holds chain k's 4 elements, vectors 3..0 in .w..x
+        const float4* a = reinterpret_cast<const float4*>(rows + (size_t)i * rs);
+        const float4* b = reinterpret_cast<const float4*>(rows + (size_t)p * rs);
+        Acc4 acc; acc.zero();
+        float* l[4] = {&acc.l0, &acc.l1, &acc.l2, &acc.l3};
+        for (int v = 0; v < (m.D >> 2); v += 4) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const float4 u = a[v + k], w = b[v + k];
+                *l[k] = __fadd_rn(__fmul_rn(u.w, w.w), *l[k]);
+                *l[k] = __fadd_rn(__fmul_rn(u.z, w.z), *l[k]);
+                *l[k] = __fadd_rn(__fmul_rn(u.y, w.y), *l[k]);
+                *l[k] = __fadd_rn(__fmul_rn(u.x, w.x), *l[k]);
+            }
+        }
+        return acc.reduce();
+    }
+    const float* a = reinterpret_cast<const float*>(rows + (size_t)i * rs);
+    const float* b = reinterpret_cast<const float*>(rows + (size_t)p * rs);
+    Acc4 acc; acc.zero();
+    a1_range<true, false>(acc, a, b, 0, m.D);
+    return acc.reduce();
+}
+
+__device__ int warp_prune_gram(uint64_t* cand, int n, double alpha2, int R, const F32Metric& m, const uint32_t* rows,
+                               const uint32_t* cn, uint8_t* rk, float* gb, int32_t* out_ids, uint32_t* out_d) {
+    const unsigned FULL = 0xFFFFFFFFu;
+    const int lane = lane_id();
+    const int rs = m.stage_stride_words();
+    // rank by key: rk[rank] = candidate index
+    {
+        const uint64_t k0 = lane < n ? cand[lane] : UMAX, k1 = lane + 32 < n ? cand[lane + 32] : UMAX;
+        int c0 = 0, c1 = 0;
+        for (int j = 0; j < n; ++j) {
+            const uint64_t kj = cand[j];
+            c0 += kj < k0;
+            c1 += kj < k1;
+        }
+        if (lane < n) rk[c0] = (uint8_t)lane;
+        if (lane + 32 < n) rk[c1] = (uint8_t)(lane + 32);
+        __syncwarp();
+    }
+    // this lane tests ranked positions lane and lane + 32
+    const int i0 = lane < n ? rk[lane] : 0, i1 = lane + 32 < n ? rk[lane + 32] : 0;
+    const uint64_t key0 = cand[i0], key1 = cand[i1];
+    const double dt0 = (double)__uint_as_float((uint32_t)(key0 >> 32)), dt1 = (double)__uint_as_float((uint32_t)(key1 >> 32));
+    const double n0 = (double)__uint_as_float(cn[i0]), n1 = (double)__uint_as_float(cn[i1]);
+    uint32_t alive0 = __ballot_sync(FULL, lane < n), alive1 = __ballot_sync(FULL, lane + 32 < n);
+    const double E = 0x1p-8;
+    int kept = 0, blk = -1;
+    while (kept < R && (alive0 | alive1)) {
+        const int p = alive0 ? __ffs(alive0) - 1 : 32 + __ffs(alive1) - 1;
+        const int ip = rk[p];
+        if (lane == 0) {
+            const uint64_t kp = cand[ip];
+            out_ids[kept] = (int32_t)(kp & 0xFFFFFFFFull);
+            out_d[kept] = (uint32_t)(kp >> 32);
+        }
+        if (p < 32) alive0 &= ~(1u << p); else alive1 &= ~(1u << (p - 32));
+        ++kept;
+        if (kept >= R || !(alive0 | alive1)) break;
+        if ((p >> 4) != blk) {
+            blk = p >> 4;
+            __syncwarp();
+            gram_block(rows, rs, m.D, rk, n, blk, gb);
+            __syncwarp();
+        }
+        const double np = (double)__uint_as_float(cn[ip]);
+        const float* grow = gb + (p & 15) * GP_MAX;
+        bool rm0 = false, rm1 = false;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const bool live = ((h ? alive1 : alive0) >> lane) & 1u;
+            if (!live) continue;
+            const int c = lane + 32 * h;
+            const double nc = h ? n1 : n0, dtc = h ? dt1 : dt0;
+            const double dd = np + nc - 2.0 * (double)grow[c];
+            const double err = E * (np + nc);
+            bool rm;
+            if (alpha2 * (dd - err) > dtc * (1.0 + 0x1p-40)) rm = false;        // certainly kept
+            else if (alpha2 * (dd + err) <= dtc * (1.0 - 0x1p-40)) rm = true;   // certainly pruned
+            else {                                                              // exact A1 distance
+                const int ic = h ? i1 : i0;
+                const float d = exact_from_dot(__uint_as_float(cn[ic]), staged_dot(m, rows, ic, ip),
+                                               __uint_as_float(cn[ip]));
+                rm = !(__dmul_rn(alpha2, (double)d) > dtc);
+            }
+            if (h) rm1 = rm; else rm0 = rm;
+        }
+        alive0 &= ~__ballot_sync(FULL, rm0);
+        alive1 &= ~__ballot_sync(FULL, rm1);
+    }
+    __syncwarp();
+    return kept;
+}
+
 __device__ __forceinline__ void write_row(int32_t* __restrict__ adj, int32_t* __restrict__ deg, int R, uint32_t v,
                                           const int32_t* ids, int n) {
     const int lane = lane_id();
@@ -646,7 +805,8 @@ constexpr int OWNER_SC = JB_OWNER_SC;  // smem candidate slots per owner warp (l
 // per-warp bytes: keys | vertex words (pivot, staged rows, norms) | have, kid, kd
 template <class M>
 __host__ __device__ inline int owner_per_warp(const M& m, int R, int crows) {
-    return ((OWNER_SC * 8 + vertex_warp_words(m, crows) * 4 + R * 4 * 3) + 15) & ~15;
+    const int gram = std::is_same<M, F32Metric>::value ? GP_BYTES : 0;  // warp_prune_gram scratch
+    return ((OWNER_SC * 8 + vertex_warp_words(m, crows) * 4 + R * 4 * 3 + gram) + 15) & ~15;
 }
 
 #ifdef JB_OWNER_STATS
@@ -671,7 +831,11 @@ owner_merge_kernel(const M m, double alpha2, int R, int always_prune, const uint
     const int per_warp = owner_per_warp(m, R, crows);
     unsigned char* base = shb + (size_t)warp * per_warp;
     uint64_t* scand = reinterpret_cast<uint64_t*>(base);
-    uint32_t* pv = reinterpret_cast<uint32_t*>(base + SC * 8);
+    // F32: Gram block (16 B aligned) and rank list of warp_prune_gram
+    constexpr int GB = std::is_same<M, F32Metric>::value ? GP_BYTES : 0;
+    float* gb = reinterpret_cast<float*>(base + SC * 8);
+    uint8_t* rk = reinterpret_cast<uint8_t*>(base + SC * 8 + 16 * GP_MAX * 4);
+    uint32_t* pv = reinterpret_cast<uint32_t*>(base + SC * 8 + GB);
     uint32_t* rows = pv + m.pivot_words();
     uint32_t* cn = rows + (size_t)crows * m.stage_stride_words();
     int32_t* have = reinterpret_cast<int32_t*>(pv + vertex_warp_words(m, crows));
@@ -750,7 +914,14 @@ owner_merge_kernel(const M m, double alpha2, int R, int always_prune, const uint
         m.stage(rows, cn, cand, n);
         for (int j = lane; j < hd; j += 32) cand[j] = key_of(m.dist_pivot_staged(pv, rows, cn, j), (uint32_t)have[j]);
         __syncwarp();
-        k = warp_prune_staged(cand, n, alpha2, R, m, rows, cn, stage_list(cn, crows), kid, kd);
+        bool done = false;
+        if constexpr (std::is_same<M, F32Metric>::value) {
+            if (m.gram_ok(n)) {
+                k = warp_prune_gram(cand, n, alpha2, R, m, rows, cn, rk, gb, kid, kd);
+                done = true;
+            }
+        }
+        if (!done) k = warp_prune_staged(cand, n, alpha2, R, m, rows, cn, stage_list(cn, crows), kid, kd);
     } else {
         cp_async_wait_all();
         __syncwarp();
@@ -1003,6 +1174,9 @@ owner_matrix_kernel(const F32Metric m, double alpha2, int R, int always_prune, c
 }
 
 // ---- repair: BFS ------------------------------------------------------------
+constexpr int BFS_BATCH = 8;           // BFS levels enqueued per host read
+constexpr int BFS_MAX_LEVELS = 1 << 16;
+
 __global__ void bfs_init_kernel(int32_t* __restrict__ seen, int64_t n, int64_t entry, int32_t* __restrict__ front,
                                 int* __restrict__ fcount) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -1024,7 +1198,10 @@ __device__ __forceinline__ void warp_append(bool take, int32_t v, int32_t* __res
 }
 
 // One warp per frontier vertex (grid-stride), lane j reads edge j of its row: a
-// coalesced 4R-byte row read and no per-edge index division.
+// coalesced 4R-byte row read and no per-edge index division. Level l reads the
+// frontier size cnt[l] and appends the next frontier with cnt[l + 1] (zeroed
+// beforehand), so a run of levels is enqueued without reading anything back;
+// levels past the last non-empty frontier exit at once.
 __global__ void bfs_expand_kernel(const int32_t* __restrict__ adj, int R, const int32_t* __restrict__ front,
                                   const int* __restrict__ fcount, int32_t* __restrict__ seen,
                                   int32_t* __restrict__ next, int* __restrict__ ncount) {
@@ -1529,6 +1706,7 @@ static int repair(const M& m, const jb_insert_args& a, int64_t n_active, int64_t
     BALLOC(fa, int32_t, n_active);
     BALLOC(fb, int32_t, n_active);
     BALLOC(counts, int, 8);
+    BALLOC(lvl, int, BFS_MAX_LEVELS + 1);  // frontier size per BFS level
     BALLOC(lost, int32_t, n_active);
     BALLOC(reach, int32_t, n_active);
     BALLOC(pinned, uint8_t, (size_t)n_active * R);
@@ -1542,22 +1720,22 @@ static int repair(const M& m, const jb_insert_args& a, int64_t n_active, int64_t
     for (int round = 0;; ++round) {
         PhaseTimer rt(st);
         // BFS from the entry
-        bfs_init_kernel<<<nblk, T, 0, st>>>(seen, n_active, entry, fa, counts);
-        int fcount = 1, levels = 0;
-        int32_t* cur = fa;
-        int32_t* nxt = fb;
-        int* fc = counts;
-        int* nc = counts + 1;
-        while (fcount > 0) {
-            JB_CUDA(cudaMemsetAsync(nc, 0, sizeof(int), st));
-            const unsigned eb = (unsigned)std::min<int64_t>(((int64_t)fcount * 32 + T - 1) / T, 8 * sm_count_current());
-            bfs_expand_kernel<<<eb, T, 0, st>>>(a.adjacency, R, cur, fc, seen, nxt, nc);
-            JB_LAUNCH_CHECK();
-            JB_CUDA(cudaMemcpyAsync(&fcount, nc, sizeof(int), cudaMemcpyDeviceToHost, st));
+        // levels are enqueued JB_BFS_BATCH at a time (one host read per batch, not per level)
+        bfs_init_kernel<<<nblk, T, 0, st>>>(seen, n_active, entry, fa, lvl);
+        int levels = 0;
+        const unsigned eb = (unsigned)std::min<int64_t>(((int64_t)n_active * 32 + T - 1) / T, 8 * sm_count_current());
+        for (int fcount = 1; fcount > 0;) {
+            if (levels + BFS_BATCH >= BFS_MAX_LEVELS) { set_error("connectivity repair: BFS depth"); return JB_ECUDA; }
+            JB_CUDA(cudaMemsetAsync(lvl + levels + 1, 0, BFS_BATCH * sizeof(int), st));
+            for (int l = levels; l < levels + BFS_BATCH; ++l) {
+                const bool odd = (l & 1) != 0;
+                bfs_expand_kernel<<<eb, T, 0, st>>>(a.adjacency, R, odd ? fb : fa, lvl + l, seen, odd ? fa : fb,
+                                                    lvl + l + 1);
+                JB_LAUNCH_CHECK();
+            }
+            levels += BFS_BATCH;
+            JB_CUDA(cudaMemcpyAsync(&fcount, lvl + levels, sizeof(int), cudaMemcpyDeviceToHost, st));
             JB_CUDA(cudaStreamSynchronize(st));
-            std::swap(cur, nxt);
-            std::swap(fc, nc);
-            ++levels;
         }
         JB_CUDA(cudaMemsetAsync(counts + 2, 0, 2 * sizeof(int), st));
         split_kernel<<<nblk, T, 0, st>>>(seen, n_active, lost, counts + 2, reach, counts + 3);
@@ -2079,7 +2257,10 @@ static int with_metric(const jb_insert_args& a, F&& f) {
         }
     }
     if (a.element_kind == JB_KIND_U8) return f(U8Metric{a.data_u8, a.norms_u32, a.dims});
-    return f(F32Metric{a.data, a.data_norms, a.dims});
+    F32Metric m{a.data, a.data_norms, a.dims};
+    const char* e = getenv("JB_GRAM");
+    m.gram = !(e && e[0] == '0');
+    return f(m);
 }
 
 }  // namespace jb

@@ -27,7 +27,7 @@
 //   |<r,x>_tf32 - <r,x>| < (2^-9 + 2^-17 + 2^-20) sum_e |r_e x_e| <= 2^-8.99 |r| |x|
 //   |<r,x>_A1  - <r,x>|  < 2^-19 |r| |x|       (4 chains of <= 32 adds + 2)
 //   rounding of the two distance evaluations < 2^-21 (|r|^2 + |x|^2)
-// so err = 2^-7 |r| |x| + 2^-20 (|r|^2 + |x|^2) holds with a 2x margin on each term.
+// so err = 2^-7 |r| |x| + 2^-18 (|r|^2 + |x|^2) holds with a 2x (8x) margin on each term.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cstdio>
@@ -42,15 +42,24 @@ namespace jb {
 constexpr int TC_M = 128;        // data rows per tile (TMEM lanes)
 constexpr int TC_N = 256;        // stranded rows per CTA (TMEM columns per accumulator)
 constexpr int TC_KC = 32;        // f32 elements per K chunk (one 128 B swizzle row)
-constexpr int TC_STAGES = 4;     // A-chunk pipeline depth
+constexpr int TC_MAX_STAGES = 8; // A-chunk pipeline depth: as many 16 KB stages as fit beside B
 constexpr int TC_MAXK = 4;       // D <= 128
-constexpr int TC_THREADS = 192;  // warp 0 TMA, warp 1 MMA + TMEM owner, warps 2-5 epilogue
+constexpr int TC_EPI_WARPS = 8;  // two epilogue warps per TMEM lane quarter (128 columns each)
+constexpr int TC_THREADS = 64 + 32 * TC_EPI_WARPS;  // warp 0 TMA, warp 1 MMA + TMEM owner, warps 2.. epilogue
 constexpr int TC_CAP = 1024;     // candidate slots per stranded row
+constexpr float TC_E1 = 0x1p-7f;   // error bound: E1 |r| |x| + E2 (|r|^2 + |x|^2) (see top)
+constexpr float TC_E2 = 0x1p-18f;
+constexpr float TC_E = 0.5f * TC_E1 + TC_E2;  // <= E (|r|^2 + |x|^2) form of the same bound
 constexpr uint32_t TC_A_BYTES = TC_M * 128;   // 16 KB per stage
 constexpr uint32_t TC_B_BYTES = TC_N * 128;   // 32 KB per K chunk
 
-__host__ __device__ constexpr size_t tc_smem_bytes(int nk) {
-    return 1024 /* align slack */ + (size_t)nk * TC_B_BYTES + (size_t)TC_STAGES * TC_A_BYTES + TC_N * 16 + 256;
+__host__ __device__ constexpr size_t tc_smem_bytes(int nk, int stages) {
+    return 1024 /* align slack */ + (size_t)nk * TC_B_BYTES + (size_t)stages * TC_A_BYTES + TC_N * 4 + 512;
+}
+__host__ __device__ constexpr int tc_stages(int nk) {
+    int st = TC_MAX_STAGES;
+    while (st > 2 && tc_smem_bytes(nk, st) > 227 * 1024) --st;
+    return st;
 }
 
 // ---- PTX wrappers ------------------------------------------------------------
@@ -65,14 +74,22 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* b) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
 }
-__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+__device__ __forceinline__ bool mbar_try(uint32_t addr, uint32_t parity) {
+    uint32_t ok;
     asm volatile(
-        "{\n\t.reg .pred p;\n"
-        "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(b)),
-        "r"(parity)
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(addr), "r"(parity)
         : "memory");
+    return ok != 0;
+}
+// spin with a short back-off: the waiting warps share SM sub-partitions with the
+// epilogue warps, whose issue slots a hot spin loop would take
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+    const uint32_t a = smem_u32(b);
+    while (!mbar_try(a, parity)) __nanosleep(32);
 }
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar) {
     asm volatile(
@@ -130,14 +147,16 @@ donor_screen_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_c
                        const float4* __restrict__ sinfo, int nlost, int* __restrict__ cnt, int32_t* __restrict__ list,
                        int cap) {
     extern __shared__ __align__(1024) unsigned char tsm_raw[];
-    unsigned char* tsm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(tsm_raw) + 1023) & ~(uintptr_t)1023);
+    // 1024 B alignment for the 128 B swizzle atoms (pointer arithmetic keeps the shared window)
+    unsigned char* tsm = tsm_raw + ((1024u - (smem_u32(tsm_raw) & 1023u)) & 1023u);
     unsigned char* sB = tsm;                                       // nk x [256 rows x 128 B]
     unsigned char* sA = sB + (size_t)nk * TC_B_BYTES;              // STAGES x [128 rows x 128 B]
-    float4* sInfo = reinterpret_cast<float4*>(sA + (size_t)TC_STAGES * TC_A_BYTES);  // [256]
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sInfo + TC_N);
+    const int STAGES = tc_stages(nk);
+    float* sC = reinterpret_cast<float*>(sA + (size_t)STAGES * TC_A_BYTES);  // [256] c_x per column
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sC + TC_N);
     uint64_t* full = bars;                    // [STAGES]
-    uint64_t* empty = bars + TC_STAGES;       // [STAGES]
-    uint64_t* bfull = bars + 2 * TC_STAGES;   // [1]
+    uint64_t* empty = bars + STAGES;          // [STAGES]
+    uint64_t* bfull = bars + 2 * STAGES;      // [1]
     uint64_t* tfull = bfull + 1;              // [2]
     uint64_t* tempty = tfull + 2;             // [2]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
@@ -146,9 +165,9 @@ donor_screen_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_c
     const int s_base = blockIdx.y * TC_N;
 
     if (warp == 0 && lane == 0) {
-        for (int i = 0; i < TC_STAGES; ++i) { mbar_init(full + i, 1); mbar_init(empty + i, 1); }
+        for (int i = 0; i < STAGES; ++i) { mbar_init(full + i, 1); mbar_init(empty + i, 1); }
         mbar_init(bfull, 1);
-        for (int i = 0; i < 2; ++i) { mbar_init(tfull + i, 1); mbar_init(tempty + i, 128); }
+        for (int i = 0; i < 2; ++i) { mbar_init(tfull + i, 1); mbar_init(tempty + i, TC_EPI_WARPS); }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_b)) : "memory");
@@ -157,9 +176,16 @@ donor_screen_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_c
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
+    // per stranded column: c_x = (tau_x - |x|^2 (1 - E)) / 2; -inf: no column (a row
+    // without a finite tau is rescanned exactly anyway)
     for (int i = threadIdx.x; i < TC_N; i += TC_THREADS) {
         const int s = s_base + i;
-        sInfo[i] = s < nlost ? sinfo[s] : make_float4(0.f, 0.f, -__int_as_float(0x7F800000), 0.f);
+        float c = -__int_as_float(0x7F800000);
+        if (s < nlost) {
+            const float4 si = sinfo[s];
+            if (si.z < __int_as_float(0x7F800000)) c = 0.5f * (si.z - si.x * (1.0f - TC_E));
+        }
+        sC[i] = c;
     }
     tc_fence_before();
     __syncthreads();
@@ -177,7 +203,7 @@ donor_screen_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_c
                     mbar_wait(empty + stage, phase ^ 1);
                     mbar_expect_tx(full + stage, TC_A_BYTES);
                     tma_load_2d(sA + (size_t)stage * TC_A_BYTES, &map_a, kc * TC_KC, (int)(t * TC_M), full + stage);
-                    if (++stage == TC_STAGES) { stage = 0; phase ^= 1; }
+                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
             }
         }
@@ -201,7 +227,7 @@ donor_screen_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_c
                         mma_tf32(d, ad, bd, (kc | k) != 0);
                     }
                     mma_commit(empty + stage);  // frees the A stage once these MMAs have read it
-                    if (++stage == TC_STAGES) { stage = 0; phase ^= 1; }
+                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
                 mma_commit(tfull + acc);  // accumulator ready for the epilogue
                 acc ^= 1;
@@ -210,44 +236,54 @@ donor_screen_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_c
         }
         __syncwarp();
     } else {
-        // epilogue: warp w reads TMEM lanes 32 (w % 4) .. +31 = data rows of the tile
+        // epilogue: warp w reads TMEM lanes 32 (w % 4) .. +31 = data rows of the tile, and
+        // one half of the 256 stranded columns. With err <= E (|r|^2 + |x|^2),
+        // E = E1 / 2 + E2 (E1 |r||x| <= E1 (|r|^2 + |x|^2) / 2), keep (r, x) iff
+        //   <r, x>  >=  h_r - c_x,   h_r = |r|^2 (1 - E) / 2,   c_x = (tau_x - |x|^2 (1 - E)) / 2
+        // (the rearrangement's roundings are inside E2 = 2^-18, 4x the bound's own term).
         const int q = warp & 3;
-        const float E1 = 0x1p-7f, E2 = 0x1p-20f, INF = __int_as_float(0x7F800000);
+        const int half = (warp - 2) >> 2;
+        const int col0 = half * (TC_N / 2);
+        const int ncol = min(TC_N / 2, max(0, nlost - s_base - col0));  // valid stranded columns of this half
         int acc = 0;
         uint32_t aphase = 0;
         for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
             const int64_t r = t * TC_M + 32 * q + lane;
-            bool ok = r < n_rows;
-            float xn = 0.f, nx = 0.f;
-            if (ok) {
-                ok = seen[r] != 0;
-                xn = __ldg(norms + r);
-                nx = sqrtf(xn) * (1.0f + 0x1p-10f);
-            }
+            float h = __int_as_float(0x7F800000);  // unreachable / past the end: never a candidate
+            if (r < n_rows && seen[r] != 0) h = __ldg(norms + r) * (0.5f - 0.5f * TC_E);
+            const bool any_row = __any_sync(0xFFFFFFFFu, h < __int_as_float(0x7F800000));
             mbar_wait(tfull + acc, aphase);
             tc_fence_after();
-            const uint32_t base = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(acc * TC_N);
-            for (int c0 = 0; c0 < TC_N; c0 += 32) {
-                float v[32];
-                tmem_ld32(base + c0, v);
-                if (ok) {
+            const uint32_t base = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(acc * TC_N + col0);
+            if (any_row) {
+#pragma unroll 1
+                for (int c0 = 0; c0 < ncol; c0 += 32) {
+                    float v[32];
+                    tmem_ld32(base + c0, v);
+                    const float4* cv = reinterpret_cast<const float4*>(sC + col0 + c0);
+                    bool hit = false;
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) {
-                        const float4 si = sInfo[c0 + j];  // |x|^2, |x| (rounded up), tau_x
-                        const float nn = xn + si.x;
-                        const float dt = fmaf(-2.0f, v[j], nn);
-                        const float err = fmaf(E1 * nx, si.y, E2 * nn);
-                        if (dt - err <= si.z) {
-                            const int s = s_base + c0 + j;
-                            const int slot = atomicAdd(cnt + s, 1);
-                            if (slot < cap) list[(size_t)s * cap + slot] = (int32_t)r;
+                    for (int j4 = 0; j4 < 8; ++j4) {
+                        const float4 c = cv[j4];
+                        hit |= v[4 * j4] >= h - c.x;
+                        hit |= v[4 * j4 + 1] >= h - c.y;
+                        hit |= v[4 * j4 + 2] >= h - c.z;
+                        hit |= v[4 * j4 + 3] >= h - c.w;
+                    }
+                    if (hit) {  // rare: append this group's candidates
+                        for (int j = 0; j < 32; ++j) {
+                            if (v[j] >= h - sC[col0 + c0 + j]) {
+                                const int s = s_base + col0 + c0 + j;
+                                const int slot = atomicAdd(cnt + s, 1);
+                                if (slot < cap) list[(size_t)s * cap + slot] = (int32_t)r;
+                            }
                         }
                     }
                 }
             }
-            (void)INF;
             tc_fence_before();
-            mbar_arrive(tempty + acc);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(tempty + acc);
             acc ^= 1;
             if (acc == 0) aphase ^= 1;
         }
@@ -447,7 +483,7 @@ int donor_scan_tc(const float* data, const float* norms, int D, const int32_t* a
     JB_CHECK_ARG(make_map(&ma, data, D, n_rows, TC_M) && make_map(&mb, srows, D, sp, TC_N),
                  "donor scan: cuTensorMapEncodeTiled failed");
     const int nk = (D + TC_KC - 1) / TC_KC;
-    const size_t smem = tc_smem_bytes(nk);
+    const size_t smem = tc_smem_bytes(nk, tc_stages(nk));
     JB_CUDA_RC(grow_smem(donor_screen_tc_kernel, (int)smem));
     const int64_t tiles = (n_rows + TC_M - 1) / TC_M;
     const int chunks = sp / TC_N;
