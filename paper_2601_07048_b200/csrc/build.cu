@@ -272,7 +272,7 @@ __device__ int warp_prune_staged(uint64_t* cand, int n, double alpha2, int R, co
 // per-warp 48 x 48 x D Gram; the exact A1 rounds it replaces were ~45% of the
 // owner merge's instructions.)
 constexpr int GP_MAX = 64;
-constexpr int GP_BYTES = GP_MAX + 16 * GP_MAX * 4;
+constexpr int GP_BYTES = GP_MAX + 16 * GP_MAX * 4 + GP_MAX * 4;  // ranks | Gram block | ranked norms
 
 __device__ __forceinline__ void mma_tf32_16x8x8(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
                                                 uint32_t b0, uint32_t b1) {
@@ -348,6 +348,7 @@ __device__ int warp_prune_gram(uint64_t* cand, int n, double alpha2, int R, cons
     const unsigned FULL = 0xFFFFFFFFu;
     const int lane = lane_id();
     const int rs = m.stage_stride_words();
+    float* snorm = gb + 16 * GP_MAX;  // |x|^2 of ranked positions
     // rank by key: rk[rank] = candidate index
     {
         const uint64_t k0 = lane < n ? cand[lane] : UMAX, k1 = lane + 32 < n ? cand[lane + 32] : UMAX;
@@ -357,23 +358,25 @@ __device__ int warp_prune_gram(uint64_t* cand, int n, double alpha2, int R, cons
             c0 += kj < k0;
             c1 += kj < k1;
         }
-        if (lane < n) rk[c0] = (uint8_t)lane;
-        if (lane + 32 < n) rk[c1] = (uint8_t)(lane + 32);
+        if (lane < n) { rk[c0] = (uint8_t)lane; snorm[c0] = __uint_as_float(cn[lane]); }
+        if (lane + 32 < n) { rk[c1] = (uint8_t)(lane + 32); snorm[c1] = __uint_as_float(cn[lane + 32]); }
         __syncwarp();
     }
     // this lane tests ranked positions lane and lane + 32
     const int i0 = lane < n ? rk[lane] : 0, i1 = lane + 32 < n ? rk[lane + 32] : 0;
     const uint64_t key0 = cand[i0], key1 = cand[i1];
-    const double dt0 = (double)__uint_as_float((uint32_t)(key0 >> 32)), dt1 = (double)__uint_as_float((uint32_t)(key1 >> 32));
-    const double n0 = (double)__uint_as_float(cn[i0]), n1 = (double)__uint_as_float(cn[i1]);
+    const float dt0 = __uint_as_float((uint32_t)(key0 >> 32)), dt1 = __uint_as_float((uint32_t)(key1 >> 32));
+    const float n0 = __uint_as_float(cn[i0]), n1 = __uint_as_float(cn[i1]);
+    // f32 screen with directed margins: a2lo <= alpha^2 <= a2hi; the (2^-8)(|p|^2 + |c|^2)
+    // bound absorbs the screen's own f32 roundings (relative 2^-23 each) many times over
+    const float a2lo = (float)alpha2 * (1.0f - 0x1p-20f), a2hi = (float)alpha2 * (1.0f + 0x1p-20f);
+    const float E = 0x1p-8f;
     uint32_t alive0 = __ballot_sync(FULL, lane < n), alive1 = __ballot_sync(FULL, lane + 32 < n);
-    const double E = 0x1p-8;
     int kept = 0, blk = -1;
     while (kept < R && (alive0 | alive1)) {
         const int p = alive0 ? __ffs(alive0) - 1 : 32 + __ffs(alive1) - 1;
-        const int ip = rk[p];
         if (lane == 0) {
-            const uint64_t kp = cand[ip];
+            const uint64_t kp = cand[rk[p]];
             out_ids[kept] = (int32_t)(kp & 0xFFFFFFFFull);
             out_d[kept] = (uint32_t)(kp >> 32);
         }
@@ -386,25 +389,25 @@ __device__ int warp_prune_gram(uint64_t* cand, int n, double alpha2, int R, cons
             gram_block(rows, rs, m.D, rk, n, blk, gb);
             __syncwarp();
         }
-        const double np = (double)__uint_as_float(cn[ip]);
+        const float np = snorm[p];
         const float* grow = gb + (p & 15) * GP_MAX;
         bool rm0 = false, rm1 = false;
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
             const bool live = ((h ? alive1 : alive0) >> lane) & 1u;
             if (!live) continue;
-            const int c = lane + 32 * h;
-            const double nc = h ? n1 : n0, dtc = h ? dt1 : dt0;
-            const double dd = np + nc - 2.0 * (double)grow[c];
-            const double err = E * (np + nc);
+            const float nc = h ? n1 : n0, dtc = h ? dt1 : dt0;
+            const float nn = np + nc;
+            const float dd = fmaf(-2.0f, grow[lane + 32 * h], nn);
+            const float err = E * nn;
             bool rm;
-            if (alpha2 * (dd - err) > dtc * (1.0 + 0x1p-40)) rm = false;        // certainly kept
-            else if (alpha2 * (dd + err) <= dtc * (1.0 - 0x1p-40)) rm = true;   // certainly pruned
-            else {                                                              // exact A1 distance
-                const int ic = h ? i1 : i0;
+            if (a2lo * (dd - err) > dtc) rm = false;         // certainly kept
+            else if (a2hi * (dd + err) < dtc) rm = true;     // certainly pruned
+            else {                                           // exact A1 distance, f64 test as the reference
+                const int ic = h ? i1 : i0, ip = rk[p];
                 const float d = exact_from_dot(__uint_as_float(cn[ic]), staged_dot(m, rows, ic, ip),
                                                __uint_as_float(cn[ip]));
-                rm = !(__dmul_rn(alpha2, (double)d) > dtc);
+                rm = !(__dmul_rn(alpha2, (double)d) > (double)dtc);
             }
             if (h) rm1 = rm; else rm0 = rm;
         }
@@ -486,6 +489,8 @@ phase2_kernel(const M m, int64_t start, int64_t nb, double alpha2, int R, const 
     uint32_t* kd = kept_d + xi * R;
     int k;
     if (h <= crows) {
+        // (the Gram-screened prune measured no faster here: 17.9 vs 16.8 ms per 100K batch at
+        // 3M, its extra smem costing what the screen saves; phase 2 is latency-bound)
         m.stage(rows, cn, cand, h);
         k = warp_prune_staged(cand, h, alpha2, R, m, rows, cn, stage_list(cn, crows), ki, kd);
     } else {
@@ -803,6 +808,7 @@ __global__ void seg_head_kernel(const uint32_t* __restrict__ t, int64_t n, uint8
 #endif
 constexpr int OWNER_SC = JB_OWNER_SC;  // smem candidate slots per owner warp (larger groups use the global pool)
 // per-warp bytes: keys | vertex words (pivot, staged rows, norms) | have, kid, kd
+__host__ __device__ inline int owner_light_per_warp(int R) { return ((OWNER_SC * 8 + R * 4 * 3) + 15) & ~15; }
 template <class M>
 __host__ __device__ inline int owner_per_warp(const M& m, int R, int crows) {
     const int gram = std::is_same<M, F32Metric>::value ? GP_BYTES : 0;  // warp_prune_gram scratch
@@ -819,30 +825,29 @@ extern "C" int jb_debug_owner_stats(unsigned long long* out) {
 }
 #endif
 
-template <class M>
-__global__ void __launch_bounds__(BW * 32)
-owner_merge_kernel(const M m, double alpha2, int R, int always_prune, const uint32_t* __restrict__ tgt,
-                   const uint64_t* __restrict__ key, int64_t total, const int32_t* __restrict__ seg_start,
-                   const int* __restrict__ n_seg, uint64_t* __restrict__ pool, unsigned long long* __restrict__ pool_top,
-                   int pool_cap, int32_t* __restrict__ adj, int32_t* __restrict__ deg, int* __restrict__ err, int crows) {
-    extern __shared__ __align__(16) unsigned char shb[];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+// MODE 0: every target (append, or prune with staged rows); MODE 1 (light, no row
+// staging, high occupancy): append where the fresh sources fit, defer the rest to
+// defer[] (targets needing a prune or the global pool); MODE 2: the deferred list.
+template <class M, int MODE>
+__device__ __forceinline__ void owner_one(const M& m, double alpha2, int R, int always_prune, const uint32_t* __restrict__ tgt,
+                   const uint64_t* __restrict__ key, int64_t total, const int32_t* __restrict__ seg_start, int64_t s,
+                   uint64_t* __restrict__ pool, unsigned long long* __restrict__ pool_top,
+                   int pool_cap, int32_t* __restrict__ adj, int32_t* __restrict__ deg, int* __restrict__ err, int crows,
+                   unsigned char* base, int32_t* __restrict__ defer, int* __restrict__ ndefer) {
+    const int lane = threadIdx.x & 31;
     constexpr int SC = OWNER_SC;
-    const int per_warp = owner_per_warp(m, R, crows);
-    unsigned char* base = shb + (size_t)warp * per_warp;
     uint64_t* scand = reinterpret_cast<uint64_t*>(base);
     // F32: Gram block (16 B aligned) and rank list of warp_prune_gram
-    constexpr int GB = std::is_same<M, F32Metric>::value ? GP_BYTES : 0;
+    constexpr int GB = (std::is_same<M, F32Metric>::value && MODE != 1) ? GP_BYTES : 0;
     float* gb = reinterpret_cast<float*>(base + SC * 8);
-    uint8_t* rk = reinterpret_cast<uint8_t*>(base + SC * 8 + 16 * GP_MAX * 4);
+    uint8_t* rk = reinterpret_cast<uint8_t*>(base + SC * 8 + 16 * GP_MAX * 4 + GP_MAX * 4);
     uint32_t* pv = reinterpret_cast<uint32_t*>(base + SC * 8 + GB);
     uint32_t* rows = pv + m.pivot_words();
     uint32_t* cn = rows + (size_t)crows * m.stage_stride_words();
-    int32_t* have = reinterpret_cast<int32_t*>(pv + vertex_warp_words(m, crows));
+    int32_t* have = MODE == 1 ? reinterpret_cast<int32_t*>(base + SC * 8)
+                              : reinterpret_cast<int32_t*>(pv + vertex_warp_words(m, crows));
     int32_t* kid = have + R;
     uint32_t* kd = reinterpret_cast<uint32_t*>(kid + R);
-    const int64_t s = (int64_t)blockIdx.x * BW + warp;
-    if (s >= *n_seg) return;
     const int64_t g0 = seg_start[s];
     const uint32_t t = tgt[g0];
     int64_t g1 = g0;
@@ -859,6 +864,10 @@ owner_merge_kernel(const M m, double alpha2, int R, int always_prune, const uint
     __syncwarp();
     // candidate storage: smem when it fits, else a bump-allocated global slice
     uint64_t* cand = scand;
+    if (MODE == 1 && hd + g > SC) {  // needs the global pool: the deferred pass
+        if (lane == 0) defer[atomicAdd(ndefer, 1)] = (int32_t)s;
+        return;
+    }
     if (hd + g > SC) {
         unsigned long long off = 0;
         if (lane == 0) off = atomicAdd(pool_top, (unsigned long long)(hd + g));
@@ -892,6 +901,10 @@ owner_merge_kernel(const M m, double alpha2, int R, int always_prune, const uint
         if (lane == 0) deg[t] = hd + nf;
         return;
     }
+    if (MODE == 1) {  // a prune: the deferred pass (staged rows, Gram screen)
+        if (lane == 0) defer[atomicAdd(ndefer, 1)] = (int32_t)s;
+        return;
+    }
     // existing neighbours get recomputed distances d(t, e) (target is the pivot);
     // fresh entries already hold (stored triple dist << 32 | source) keys
     m.load_pivot_async(pv, t);  // overlaps the staging copies below
@@ -922,7 +935,7 @@ owner_merge_kernel(const M m, double alpha2, int R, int always_prune, const uint
             }
         }
         if (!done) k = warp_prune_staged(cand, n, alpha2, R, m, rows, cn, stage_list(cn, crows), kid, kd);
-    } else {
+    } else if (MODE != 1) {
         cp_async_wait_all();
         __syncwarp();
         for (int j = lane; j < hd; j += 32) {
@@ -933,6 +946,30 @@ owner_merge_kernel(const M m, double alpha2, int R, int always_prune, const uint
         k = warp_prune(cand, n, alpha2, R, m, pv, kid, kd);
     }
     write_row(adj, deg, R, t, kid, k);
+}
+
+template <class M, int MODE>
+__global__ void __launch_bounds__(BW * 32)
+owner_merge_kernel(const M m, double alpha2, int R, int always_prune, const uint32_t* __restrict__ tgt,
+                   const uint64_t* __restrict__ key, int64_t total, const int32_t* __restrict__ seg_start,
+                   const int* __restrict__ n_seg, uint64_t* __restrict__ pool, unsigned long long* __restrict__ pool_top,
+                   int pool_cap, int32_t* __restrict__ adj, int32_t* __restrict__ deg, int* __restrict__ err, int crows,
+                   int32_t* __restrict__ defer, int* __restrict__ ndefer) {
+    extern __shared__ __align__(16) unsigned char shb[];
+    const int warp = threadIdx.x >> 5;
+    const int per_warp = MODE == 1 ? owner_light_per_warp(R) : owner_per_warp(m, R, crows);
+    unsigned char* base = shb + (size_t)warp * per_warp;
+    if (MODE == 2) {  // persistent over the deferred targets
+        const int nd = *ndefer;
+        for (int64_t i = (int64_t)blockIdx.x * BW + warp; i < nd; i += (int64_t)gridDim.x * BW)
+            owner_one<M, MODE>(m, alpha2, R, always_prune, tgt, key, total, seg_start, defer[i], pool, pool_top,
+                               pool_cap, adj, deg, err, crows, base, defer, ndefer);
+    } else {
+        const int64_t s = (int64_t)blockIdx.x * BW + warp;
+        if (s >= *n_seg) return;
+        owner_one<M, MODE>(m, alpha2, R, always_prune, tgt, key, total, seg_start, s, pool, pool_top, pool_cap, adj,
+                           deg, err, crows, base, defer, ndefer);
+    }
 }
 
 // ---- phase 3 for rows too large to stage per warp (f32, e.g. 960-d) ----------
@@ -2004,16 +2041,40 @@ static int merge_phase(const M& m, const jb_insert_args& a, double alpha2, uint3
             }
         }
         const int osm = owner_per_warp(m, R, crows) * BW;
-        JB_CUDA_RC(grow_smem(owner_merge_kernel<M>, osm));
 #ifdef JB_OWNER_SPLIT
         const M mo = split_prune(m);  // dev A/B
 #else
         const M& mo = m;
 #endif
-        if (!launched)
-        owner_merge_kernel<M><<<(unsigned)((hseg + BW - 1) / BW), BW * 32, osm, st>>>(
-            mo, alpha2, R, a.always_prune, tt, tk, ntri, seg, nseg, pool, ptop, pool_cap, a.adjacency, a.degrees, err,
-            crows);
+        const char* oe = getenv("JB_OWNER_DEFER");
+        if (launched) {
+        } else if (oe && oe[0] == '0') {  // A/B: one pass, every target at the staging kernel's occupancy
+            JB_CUDA_RC(grow_smem(owner_merge_kernel<M, 0>, osm));
+            owner_merge_kernel<M, 0><<<(unsigned)((hseg + BW - 1) / BW), BW * 32, osm, st>>>(
+                mo, alpha2, R, a.always_prune, tt, tk, ntri, seg, nseg, pool, ptop, pool_cap, a.adjacency, a.degrees, err,
+                crows, nullptr, nullptr);
+        } else {
+            // light pass (appends, no staged rows: high occupancy), then the targets
+            // that need a prune on a persistent grid of the staging kernel
+            BALLOC(defer, int32_t, hseg);
+            BALLOC(ndefer, int, 1);
+            JB_CUDA(cudaMemsetAsync(ndefer, 0, sizeof(int), st));
+            const int lsm = owner_light_per_warp(R) * BW;
+            JB_CUDA_RC(grow_smem(owner_merge_kernel<M, 1>, lsm));
+            owner_merge_kernel<M, 1><<<(unsigned)((hseg + BW - 1) / BW), BW * 32, lsm, st>>>(
+                mo, alpha2, R, a.always_prune, tt, tk, ntri, seg, nseg, pool, ptop, pool_cap, a.adjacency, a.degrees, err,
+                crows, defer, ndefer);
+            JB_LAUNCH_CHECK();
+            JB_CUDA_RC(grow_smem(owner_merge_kernel<M, 2>, osm));
+            int per_sm = 0;
+            JB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, owner_merge_kernel<M, 2>, BW * 32, osm));
+            const int64_t want = (hseg + BW - 1) / BW;
+            const unsigned g2 = (unsigned)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)std::max(1, per_sm) *
+                                                                                       sm_count_current()));
+            owner_merge_kernel<M, 2><<<g2, BW * 32, osm, st>>>(mo, alpha2, R, a.always_prune, tt, tk, ntri, seg, nseg,
+                                                               pool, ptop, pool_cap, a.adjacency, a.degrees, err, crows,
+                                                               defer, ndefer);
+        }
         JB_LAUNCH_CHECK();
         int herr = 0;
         JB_CUDA(cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, st));

@@ -1,6 +1,6 @@
 """Per-source-line instruction / stall breakdown of one kernel in an ncu report.
 
-    python profiles/ncu_lines.py <report.ncu-rep> [top_n] [--ops]
+    python profiles/ncu_lines.py <report.ncu-rep> [top_n] [--ops] [--kernel REGEX]
 
 Reads `ncu -i ... --page source --csv --print-source cuda,sass` (SASS rows
 interleaved under their CUDA source line) and prints, per file:line, the share
@@ -15,16 +15,19 @@ import sys
 from collections import defaultdict
 
 
-def load(rep):
-    out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
-                         capture_output=True, text=True).stdout
+def load(rep, kernel=None):
+    cmd = ["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"]
+    if kernel:
+        cmd += ["-k", f"regex:{kernel}"]
+    out = subprocess.run(cmd, capture_output=True, text=True).stdout
     return list(csv.reader(io.StringIO(out)))
 
 
 def main():
     rep = sys.argv[1]
     top = int(sys.argv[2]) if len(sys.argv) > 2 and sys.argv[2].isdigit() else 40
-    rows = load(rep)
+    kernel = sys.argv[sys.argv.index("--kernel") + 1] if "--kernel" in sys.argv else None
+    rows = load(rep, kernel)
     fname, hdr, cur = "?", None, None
     inst = defaultdict(float)
     samp = defaultdict(float)
