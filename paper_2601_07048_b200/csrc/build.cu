@@ -1238,21 +1238,46 @@ __device__ __forceinline__ void warp_append(bool take, int32_t v, int32_t* __res
 // coalesced 4R-byte row read and no per-edge index division. Level l reads the
 // frontier size cnt[l] and appends the next frontier with cnt[l + 1] (zeroed
 // beforehand), so a run of levels is enqueued without reading anything back;
-// levels past the last non-empty frontier exit at once.
-__global__ void bfs_expand_kernel(const int32_t* __restrict__ adj, int R, const int32_t* __restrict__ front,
-                                  const int* __restrict__ fcount, int32_t* __restrict__ seen,
-                                  int32_t* __restrict__ next, int* __restrict__ ncount) {
-    const int lane = threadIdx.x & 31;
-    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+// levels past the last non-empty frontier exit at once. New vertices gather in a
+// per-block smem list flushed with one global atomic per block step (a single
+// frontier counter taking one atomic per warp serialised the big levels).
+constexpr int BFS_T = 512;  // threads per block of bfs_expand_kernel
+__global__ void __launch_bounds__(BFS_T)
+bfs_expand_kernel(const int32_t* __restrict__ adj, int R, const int32_t* __restrict__ front,
+                  const int* __restrict__ fcount, int32_t* __restrict__ seen, int32_t* __restrict__ next,
+                  int* __restrict__ ncount) {
+    __shared__ int32_t buf[BFS_T];  // one step: <= 32 new vertices per warp
+    __shared__ int bn, gbase;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    constexpr int WPB = BFS_T / 32;
     const int n = *fcount;
-    for (int64_t f = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; f < n; f += nwarps) {
-        const int32_t* row = adj + (size_t)front[f] * R;
-        for (int j0 = 0; j0 < R; j0 += 32) {
-            const int j = j0 + lane;
-            const int32_t v = j < R ? row[j] : -1;
+    if (threadIdx.x == 0) bn = 0;
+    __syncthreads();
+    for (int64_t f0 = (int64_t)blockIdx.x * WPB; f0 < n; f0 += (int64_t)gridDim.x * WPB) {
+        const int64_t f = f0 + warp;
+        for (int j0 = 0; j0 < R; j0 += 32) {  // block-uniform trip count
             bool found = false;
-            if (v >= 0 && !seen[v]) found = atomicExch(&seen[v], 1) == 0;
-            warp_append(found, v, next, ncount);
+            int32_t v = -1;
+            if (f < n) {
+                const int j = j0 + lane;
+                v = j < R ? adj[(size_t)front[f] * R + j] : -1;
+                if (v >= 0 && !seen[v]) found = atomicExch(&seen[v], 1) == 0;
+            }
+            const unsigned m = __ballot_sync(0xFFFFFFFFu, found);
+            int base = 0;
+            if (lane == 0 && m) base = atomicAdd(&bn, __popc(m));
+            base = __shfl_sync(0xFFFFFFFFu, base, 0);
+            if (found) buf[base + __popc(m & lanemask_lt())] = v;
+            __syncthreads();
+            const int cnt = bn;
+            if (cnt > 0) {
+                if (threadIdx.x == 0) gbase = atomicAdd(ncount, cnt);
+                __syncthreads();
+                for (int i = threadIdx.x; i < cnt; i += BFS_T) next[gbase + i] = buf[i];
+                __syncthreads();
+                if (threadIdx.x == 0) bn = 0;
+            }
+            __syncthreads();
         }
     }
 }
@@ -1760,13 +1785,13 @@ static int repair(const M& m, const jb_insert_args& a, int64_t n_active, int64_t
         // levels are enqueued JB_BFS_BATCH at a time (one host read per batch, not per level)
         bfs_init_kernel<<<nblk, T, 0, st>>>(seen, n_active, entry, fa, lvl);
         int levels = 0;
-        const unsigned eb = (unsigned)std::min<int64_t>(((int64_t)n_active * 32 + T - 1) / T, 8 * sm_count_current());
+        const unsigned eb = (unsigned)std::min<int64_t>(((int64_t)n_active * 32 + BFS_T - 1) / BFS_T, 4 * sm_count_current());
         for (int fcount = 1; fcount > 0;) {
             if (levels + BFS_BATCH >= BFS_MAX_LEVELS) { set_error("connectivity repair: BFS depth"); return JB_ECUDA; }
             JB_CUDA(cudaMemsetAsync(lvl + levels + 1, 0, BFS_BATCH * sizeof(int), st));
             for (int l = levels; l < levels + BFS_BATCH; ++l) {
                 const bool odd = (l & 1) != 0;
-                bfs_expand_kernel<<<eb, T, 0, st>>>(a.adjacency, R, odd ? fb : fa, lvl + l, seen, odd ? fa : fb,
+                bfs_expand_kernel<<<eb, BFS_T, 0, st>>>(a.adjacency, R, odd ? fb : fa, lvl + l, seen, odd ? fa : fb,
                                                     lvl + l + 1);
                 JB_LAUNCH_CHECK();
             }

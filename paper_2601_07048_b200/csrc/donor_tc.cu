@@ -18,9 +18,10 @@
 //      |d~ - d_A1| (below), so every true donor is kept;
 //   3. exact (donor_exact_kernel, warp per x): A1-order keys of the candidates,
 //      top `fan` by (dist, id) -> the slice layout donor_merge_kernel consumes.
-// A stranded row whose candidate list overflows (or that had no finite tau)
-// is rescanned by the exact CUDA-core kernel (build.cu), so the output never
-// depends on the screen's selectivity.
+// A stranded row whose candidate list overflows gets a second screen pass with
+// tau refined from its first candidates; one with no finite tau, or a second
+// overflow, is rescanned by the exact CUDA-core kernel (build.cu), so the output
+// never depends on the screen's selectivity.
 //
 // Error bound (per pair; tf32 keeps 10 mantissa bits, |rel err| < 2^-10 per
 // operand; f32 accumulation over K <= 128 terms adds < 2^-17 relative):
@@ -356,28 +357,54 @@ __global__ void donor_seed_kernel(const float* __restrict__ data, const float* _
 // ---- 3. exact keys of the candidates, top `fan` -----------------------------------
 // part[w * fan + j] (one slice); rows whose list overflowed or had no finite tau
 // are flagged in redo[] for the exact CUDA-core scan.
+// Row w (of this pass's list; part row remap[w], or w): rows whose list overflowed
+// or that had no finite tau go to redo[] (as part rows). An overflowed row's first
+// `cap` candidates are distinct reachable vertices, so the fan-th smallest of their
+// exact distances is a valid (and usually much tighter) tau for a second screen
+// pass: written to tau2[w] (+inf when unusable).
 __global__ void donor_exact_kernel(const float* __restrict__ data, const float* __restrict__ norms, int D,
                                    const int32_t* __restrict__ lost, int nlost, const float4* __restrict__ sinfo,
                                    const int* __restrict__ cnt, const int32_t* __restrict__ list, int cap, int fan,
-                                   uint64_t* __restrict__ part, int32_t* __restrict__ redo, int* __restrict__ nredo) {
+                                   const int32_t* __restrict__ remap, uint64_t* __restrict__ part,
+                                   int32_t* __restrict__ redo, int* __restrict__ nredo, float* __restrict__ tau2) {
     const int w = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
     const int lane = threadIdx.x & 31;
     if (w >= nlost) return;
+    const int pr = remap ? remap[w] : w;
     const int n = cnt[w];
-    const bool bad = n > cap || !(sinfo[w].z < __int_as_float(0x7F800000));
-    if (bad) {
-        if (lane == 0) redo[atomicAdd(nredo, 1)] = w;
-        return;
-    }
+    const bool finite = sinfo[w].z < __int_as_float(0x7F800000);
     const uint32_t x = (uint32_t)lost[w];
     uint64_t t = UMAX;
-    for (int i0 = 0; i0 < n; i0 += 32) {
-        const int i = i0 + lane;
-        uint64_t k = UMAX;
-        if (i < n) k = donor_key(data, norms, D, (uint32_t)list[(size_t)w * cap + i], x);
-        topk_insert_distinct(t, k, fan);
+    if (finite) {
+        for (int i0 = 0; i0 < min(n, cap); i0 += 32) {
+            const int i = i0 + lane;
+            uint64_t k = UMAX;
+            if (i < min(n, cap)) k = donor_key(data, norms, D, (uint32_t)list[(size_t)w * cap + i], x);
+            topk_insert_distinct(t, k, fan);
+        }
     }
-    if (lane < fan) part[(size_t)w * fan + lane] = t;
+    if (!finite || n > cap) {
+        const uint64_t last = shfl_u64(t, fan - 1);
+        if (lane == 0) {
+            redo[atomicAdd(nredo, 1)] = pr;
+            if (tau2) tau2[w] = (finite && last != UMAX) ? key_dist(last) : __int_as_float(0x7F800000);
+        }
+        return;
+    }
+    if (lane < fan) part[(size_t)pr * fan + lane] = t;
+}
+
+// second pass inputs for the redo rows: ids, and sinfo with the refined tau
+__global__ void donor_pass2_kernel(const int32_t* __restrict__ lost, const float4* __restrict__ sinfo,
+                                   const int32_t* __restrict__ redo, int n2, const float* __restrict__ tau2,
+                                   int32_t* __restrict__ lost2, float4* __restrict__ sinfo2) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n2) return;
+    const int w = redo[i];  // part row == pass-1 row
+    lost2[i] = lost[w];
+    float4 si = sinfo[w];
+    si.z = tau2[w];
+    sinfo2[i] = si;
 }
 
 // Rows rescanned by the exact kernel: top `fan` over its `slices` partial lists
@@ -456,28 +483,24 @@ __global__ void gather_f32_rows_kernel(const float* __restrict__ data, int D, co
         dst[i] = data[(int64_t)ids[i / D] * D + i % D];
 }
 
-int donor_scan_tc(const float* data, const float* norms, int D, const int32_t* adj, int R, const int32_t* seen,
-                  int64_t n_rows, const int32_t* lost, int nlost, int fan, uint64_t* part, int32_t* redo, int* nredo,
-                  cudaStream_t st) {
+// One screen pass over `n` stranded rows (ids ls, seeds si) -> exact top lists in
+// part rows (remap), uncertified rows appended to redo (+ refined tau in tau2).
+static int screen_pass(const float* data, const float* norms, int D, const int32_t* seen, int64_t n_rows,
+                       const int32_t* ls, const float4* si, int n, int fan, const int32_t* remap, uint64_t* part,
+                       int32_t* redo, int* nredo, float* tau2, cudaStream_t st) {
     const int cap = TC_CAP;
-    const int sp = (nlost + TC_N - 1) / TC_N * TC_N;
-    Scratch s_info, s_rows, s_cnt, s_list;
-    JB_CUDA(s_info.alloc((size_t)nlost * sizeof(float4), st));
+    const int sp = (n + TC_N - 1) / TC_N * TC_N;
+    Scratch s_rows, s_cnt, s_list;
     JB_CUDA(s_rows.alloc((size_t)sp * D * 4, st));
-    JB_CUDA(s_cnt.alloc((size_t)nlost * sizeof(int), st));
-    JB_CUDA(s_list.alloc((size_t)nlost * cap * sizeof(int32_t), st));
-    float4* sinfo = s_info.as<float4>();
+    JB_CUDA(s_cnt.alloc((size_t)n * sizeof(int), st));
+    JB_CUDA(s_list.alloc((size_t)n * cap * sizeof(int32_t), st));
     float* srows = s_rows.as<float>();
     int* cnt = s_cnt.as<int>();
     int32_t* list = s_list.as<int32_t>();
-    JB_CUDA(cudaMemsetAsync(cnt, 0, (size_t)nlost * sizeof(int), st));
+    JB_CUDA(cudaMemsetAsync(cnt, 0, (size_t)n * sizeof(int), st));
     JB_CUDA(cudaMemsetAsync(srows, 0, (size_t)sp * D * 4, st));
-    JB_CUDA(cudaMemsetAsync(nredo, 0, sizeof(int), st));
-    donor_seed_kernel<<<(unsigned)(((int64_t)nlost * 32 + 255) / 256), 256, 0, st>>>(data, norms, D, adj, R, seen, n_rows,
-                                                                                   lost, nlost, fan, sinfo);
-    JB_LAUNCH_CHECK();
-    gather_f32_rows_kernel<<<(unsigned)std::min<int64_t>(((int64_t)nlost * D + 255) / 256, 4096), 256, 0, st>>>(
-        data, D, lost, nlost, srows);
+    gather_f32_rows_kernel<<<(unsigned)std::min<int64_t>(((int64_t)n * D + 255) / 256, 4096), 256, 0, st>>>(
+        data, D, ls, n, srows);
     JB_LAUNCH_CHECK();
     CUtensorMap ma, mb;
     JB_CHECK_ARG(make_map(&ma, data, D, n_rows, TC_M) && make_map(&mb, srows, D, sp, TC_N),
@@ -488,13 +511,48 @@ int donor_scan_tc(const float* data, const float* norms, int D, const int32_t* a
     const int64_t tiles = (n_rows + TC_M - 1) / TC_M;
     const int chunks = sp / TC_N;
     const int gx = (int)std::min<int64_t>(tiles, std::max(1, sm_count_current() / chunks));
-    donor_screen_tc_kernel<<<dim3(gx, chunks), TC_THREADS, smem, st>>>(ma, mb, nk, n_rows, tiles, seen, norms, sinfo,
-                                                                       nlost, cnt, list, cap);
+    donor_screen_tc_kernel<<<dim3(gx, chunks), TC_THREADS, smem, st>>>(ma, mb, nk, n_rows, tiles, seen, norms, si, n,
+                                                                       cnt, list, cap);
     JB_LAUNCH_CHECK();
-    donor_exact_kernel<<<(unsigned)(((int64_t)nlost * 32 + 255) / 256), 256, 0, st>>>(
-        data, norms, D, lost, nlost, sinfo, cnt, list, cap, fan, part, redo, nredo);
+    donor_exact_kernel<<<(unsigned)(((int64_t)n * 32 + 255) / 256), 256, 0, st>>>(
+        data, norms, D, ls, n, si, cnt, list, cap, fan, remap, part, redo, nredo, tau2);
     JB_LAUNCH_CHECK();
     return JB_OK;
+}
+
+int donor_scan_tc(const float* data, const float* norms, int D, const int32_t* adj, int R, const int32_t* seen,
+                  int64_t n_rows, const int32_t* lost, int nlost, int fan, uint64_t* part, int32_t* redo, int* nredo,
+                  cudaStream_t st) {
+    Scratch s_info, s_tau2, s_redo1, s_n1;
+    JB_CUDA(s_info.alloc((size_t)nlost * sizeof(float4), st));
+    JB_CUDA(s_tau2.alloc((size_t)nlost * sizeof(float), st));
+    JB_CUDA(s_redo1.alloc((size_t)nlost * sizeof(int32_t), st));
+    JB_CUDA(s_n1.alloc(sizeof(int), st));
+    float4* sinfo = s_info.as<float4>();
+    int32_t* redo1 = s_redo1.as<int32_t>();
+    int* n1 = s_n1.as<int>();
+    JB_CUDA(cudaMemsetAsync(n1, 0, sizeof(int), st));
+    JB_CUDA(cudaMemsetAsync(nredo, 0, sizeof(int), st));
+    donor_seed_kernel<<<(unsigned)(((int64_t)nlost * 32 + 255) / 256), 256, 0, st>>>(data, norms, D, adj, R, seen, n_rows,
+                                                                                   lost, nlost, fan, sinfo);
+    JB_LAUNCH_CHECK();
+    // pass 1: two-hop seeds
+    JB_CUDA_RC(screen_pass(data, norms, D, seen, n_rows, lost, sinfo, nlost, fan, nullptr, part, redo1, n1,
+                           s_tau2.as<float>(), st));
+    int h1 = 0;
+    JB_CUDA(cudaMemcpyAsync(&h1, n1, sizeof(int), cudaMemcpyDeviceToHost, st));
+    JB_CUDA(cudaStreamSynchronize(st));
+    if (h1 == 0) return JB_OK;
+    // pass 2: the uncertified rows again with tau refined from their pass-1 candidates;
+    // what still fails (no finite tau, or a second overflow) is left to the exact scan
+    Scratch s_l2, s_i2;
+    JB_CUDA(s_l2.alloc((size_t)h1 * sizeof(int32_t), st));
+    JB_CUDA(s_i2.alloc((size_t)h1 * sizeof(float4), st));
+    donor_pass2_kernel<<<(h1 + 255) / 256, 256, 0, st>>>(lost, sinfo, redo1, h1, s_tau2.as<float>(), s_l2.as<int32_t>(),
+                                                         s_i2.as<float4>());
+    JB_LAUNCH_CHECK();
+    return screen_pass(data, norms, D, seen, n_rows, s_l2.as<int32_t>(), s_i2.as<float4>(), h1, fan, redo1, part, redo,
+                       nredo, nullptr, st);
 }
 
 }  // namespace jb
