@@ -395,8 +395,9 @@ def _ncu_record(workload_key: str):
     try:
         with open(os.path.join(ROOT, "profiles", "search_kernel_traffic.json")) as fh:
             t = json.load(fh)
-        if t.get("workload") == workload_key:
-            return t
+        for rec in (t if isinstance(t, list) else [t]):  # one record per profiled workload
+            if rec.get("workload") == workload_key:
+                return rec
     except Exception:
         pass
     return {}

@@ -127,6 +127,15 @@ typedef struct jb_search_args {
  * visited trace are identical to the reference's (same keys, same order). */
 int jb_beam_search(const jb_search_args* args, void* stream);
 
+/* Reference-defined distance-evaluation counts (SearchStats.distance_evals,
+ * search.py:211-226): |{start} U N(u) for every expanded u| per query, from the
+ * visited traces (trace_ids [nq, trace_cap], hops[q] <= trace_cap). Queries whose
+ * flags bit 0 is clear (no visited-table eviction) keep evals[q] as given; with
+ * flags NULL every query is recounted. Replaces the host recount of lossy queries. */
+int jb_count_evals(const int32_t* adjacency, int32_t degree_cap, const int32_t* trace_ids, int32_t trace_cap,
+                   const int32_t* hops, const int32_t* starts, int64_t start_vertex, const int32_t* flags, int64_t nq,
+                   int32_t* evals, void* stream);
+
 /* Top-k extraction from frontier keys: ids (int32, -1 padded) and dists (f64,
  * +inf padded). Replaces the exact-source branch of search_knn_batch
  * (search.py:366-383). */

@@ -71,6 +71,7 @@ _SIGS = {
     "jb_frontier_topk": (C.c_int, [p, i64, i32, i32, p, p, p]),
     "jb_frontier_topk_u8": (C.c_int, [p, i64, i32, i32, p, p, p]),
     "jb_rerank_topk": (C.c_int, [p, i32, p, i64, p, i32, i32, p, p, p]),
+    "jb_count_evals": (C.c_int, [p, i32, p, i32, p, p, i64, p, i64, p, p]),
     "jb_search_knn_host": (C.c_int, [C.POINTER(KnnPlan), p, i64, p, p, p]),
     "jb_search_knn_device": (C.c_int, [C.POINTER(KnnPlan), p, i64, p, p, p]),
     "jb_rabitq_record_bytes": (i32, [i32, i32]),

@@ -344,12 +344,17 @@ __device__ __forceinline__ float rabitq_dd(const uint8_t* __restrict__ rec, uint
     constexpr uint32_t MASK = (1u << BITS) - 1u;
     Acc4 acc; acc.zero();
     int e0 = 0;
+    // the next piece's load is issued before this piece's adds (long records, e.g.
+    // 480 B of 4-bit codes at D = 960, otherwise wait out one load latency per piece)
+    uint4 cur = first;
     for (; e0 + PER16 <= D; e0 += PER16) {
-        const uint4 w4 = e0 == 0 ? first : __ldg(reinterpret_cast<const uint4*>(rec + (e0 * BITS) / 8));
-        rq_piece_full<BITS>(acc, w4, qv, e0);
+        uint4 nxt = make_uint4(0, 0, 0, 0);
+        if (e0 + PER16 < D) nxt = __ldg(reinterpret_cast<const uint4*>(rec + ((e0 + PER16) * BITS) / 8));
+        rq_piece_full<BITS>(acc, cur, qv, e0);
+        cur = nxt;
     }
     if (e0 < D) {  // last partial piece: runtime loop (rare shapes)
-        const uint4 w4 = e0 == 0 ? first : __ldg(reinterpret_cast<const uint4*>(rec + (e0 * BITS) / 8));
+        const uint4 w4 = cur;
         const uint32_t w[4] = {w4.x, w4.y, w4.z, w4.w};
         int b = e0;
         for (; b + 16 <= D; b += 16) {

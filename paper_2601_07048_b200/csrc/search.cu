@@ -737,6 +737,52 @@ rerank_kernel(const float* __restrict__ data, int D, const float* __restrict__ q
 }
 
 
+// ---- reference-defined eval counts (search.py:211-226) ----------------------
+// evals = |{start} U N(u) for every expanded u|: the reference evaluates every
+// valid neighbour of an expanded vertex exactly once (its `seen` matrix). The
+// search kernel counts its own evaluations, which include re-evaluations after
+// visited-table evictions (flags bit 0); this recount is exact. Warp per query
+// (persistent), an open-addressing id set in a per-warp global scratch slice of
+// `slots` (pow2 >= 2 x the largest possible set).
+__global__ void __launch_bounds__(256)
+count_evals_kernel(const int32_t* __restrict__ adj, int R, const int32_t* __restrict__ tids, int cap,
+                   const int32_t* __restrict__ hops, const int32_t* __restrict__ starts, int64_t start_vertex,
+                   const int32_t* __restrict__ flags, int64_t nq, uint32_t* __restrict__ scratch, int slots,
+                   int32_t* __restrict__ evals) {
+    const int lane = threadIdx.x & 31;
+    const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    uint32_t* tab = scratch + w0 * (int64_t)slots;
+    const int hb = log2i(slots);
+    for (int64_t q = w0; q < nq; q += nw) {
+        if (flags && !(flags[q] & 1)) continue;  // no eviction: the kernel's own count is exact
+        for (int i = lane; i < slots; i += 32) tab[i] = EMPTY_SLOT;
+        __syncwarp();
+        const int h = min(hops[q], cap);
+        int cnt = 0;
+        auto insert = [&](uint32_t v) {
+            uint32_t b = (v * 0x9E3779B1u) >> (32 - hb);
+            for (;;) {
+                const uint32_t old = atomicCAS(tab + b, EMPTY_SLOT, v);
+                if (old == EMPTY_SLOT) { ++cnt; return; }
+                if (old == v) return;
+                b = (b + 1) & (uint32_t)(slots - 1);
+            }
+        };
+        if (lane == 0) insert(starts ? (uint32_t)starts[q] : (uint32_t)start_vertex);
+        for (int i = 0; i < h; ++i) {
+            const int32_t u = tids[q * (int64_t)cap + i];
+            for (int j = lane; j < R; j += 32) {
+                const int32_t v = adj[(size_t)u * R + j];
+                if (v >= 0) insert((uint32_t)v);
+            }
+        }
+        for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xFFFFFFFFu, cnt, o);
+        if (lane == 0) evals[q] = cnt;
+        __syncwarp();
+    }
+}
+
 using SearchKernel = void (*)(const jb_search_args, const SearchLayout, int*);
 
 // Exact rows small enough to stay in L2 (<= half of it) are read lane-by-lane from
@@ -892,6 +938,26 @@ int jb_beam_search(const jb_search_args* args, void* stream) {
         case 8: return launch_search<JB_SRC_RABITQ, 8, true>(a, hs, st);
         default: JB_CHECK_ARG(false, "bits must be one of (1, 2, 4, 8)");
     }
+}
+
+int jb_count_evals(const int32_t* adjacency, int32_t degree_cap, const int32_t* trace_ids, int32_t trace_cap,
+                   const int32_t* hops, const int32_t* starts, int64_t start_vertex, const int32_t* flags, int64_t nq,
+                   int32_t* evals, void* stream) {
+    JB_CHECK_ARG(adjacency && trace_ids && hops && evals, "jb_count_evals: missing arrays");
+    JB_CHECK_ARG(degree_cap >= 1 && trace_cap >= 1, "jb_count_evals: bad degree_cap / trace_cap");
+    if (nq == 0) return JB_OK;
+    const int64_t most = (int64_t)trace_cap * degree_cap + 1;
+    JB_CHECK_ARG(most < (1ll << 28), "jb_count_evals: trace too long");
+    const int slots = pow2_ceil((int)(2 * most));
+    cudaStream_t st = as_stream(stream);
+    const int64_t warps = std::min<int64_t>(nq, (int64_t)sm_count_current() * 32);
+    Scratch tab;
+    JB_CUDA(tab.alloc((size_t)warps * slots * sizeof(uint32_t), st));
+    count_evals_kernel<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, st>>>(
+        adjacency, degree_cap, trace_ids, trace_cap, hops, starts, start_vertex, flags, nq, tab.as<uint32_t>(), slots,
+        evals);
+    JB_LAUNCH_CHECK();
+    return JB_OK;
 }
 
 int jb_rerank_topk(const float* data, int32_t dims, const float* queries, int64_t nq,

@@ -437,6 +437,14 @@ def run_beam_searches(graph, source, queries, beam_width: int, starts=None) -> l
     fk, hops, evals, flags, tids, tdst = _launch(graph, bound, beam_width, starts_dev, cap)
     hops_h = hops.cpu().numpy()
     over = np.nonzero(hops_h > cap)[0]
+    if not over.size:
+        # queries whose visited table evicted ids counted re-evaluations: recount them
+        # on device as |{start} U N(expanded)| (the reference's count)
+        adj, _ = graph.device()
+        _lib.check(_lib.lib().jb_count_evals(_lib.ptr(adj), graph.degree_cap, _lib.ptr(tids), cap, _lib.ptr(hops),
+                                             _lib.ptr(starts_dev), graph.entry_point, _lib.ptr(flags), nq,
+                                             _lib.ptr(evals), _lib.stream_ptr()))
+        flags.zero_()
     if over.size:  # trace buffer overflowed for a few queries: re-run exactly those with a larger cap
         torch = _lib.require_cuda()
         sel = torch.from_numpy(over).cuda()
@@ -455,7 +463,7 @@ def run_beam_searches(graph, source, queries, beam_width: int, starts=None) -> l
     keys = fk.cpu().numpy().view(np.uint64)
     evals_h = evals.cpu().numpy().astype(np.int64)
     lossy = np.nonzero(flags.cpu().numpy())[0]
-    if lossy.size:
+    if lossy.size:  # only after a trace re-run (overflowed cap): the device recount needs whole traces
         # The visited table evicted ids for these queries, so the device counted some
         # re-evaluations. The reference's count is |{start} U N(u) over expanded u|
         # (every valid neighbour of an expanded vertex is evaluated exactly once).

@@ -106,14 +106,19 @@ def test_lossy_visited_table_keeps_frontier_and_trace(graph64):
     q = gaussian(200, 64, 23)
     L = 128
     ores = osearch.beam_search(og.adj, og.active, og.entry, osearch.ExactSource(x, q), len(q), L)
+    starts = np.arange(len(q)) * 131 % og.active
+    ores_s = osearch.beam_search(og.adj, og.active, og.entry, osearch.ExactSource(x, q), len(q), L, starts=starts)
     jb.search.TUNING["hash_slots"] = 64   # far too small: forces re-evaluations
     try:
         res = jb.run_beam_searches(_graph_from_oracle(og), jb.VectorDataset(x), q, L)
+        res_s = jb.run_beam_searches(_graph_from_oracle(og), jb.VectorDataset(x), q, L, starts=starts)
     finally:
         jb.search.TUNING["hash_slots"] = 0
     # frontier, trace and even the reference's distance_evals stay exact: evicted
-    # queries get their count from |{start} U N(expanded)| (search.py semantics)
+    # queries get their count from |{start} U N(expanded)| (search.py semantics),
+    # recounted on device (jb_count_evals)
     _oracle_check(res, ores, evals=True)
+    _oracle_check(res_s, ores_s, evals=True)
 
 
 def test_explicit_starts_and_single_query(graph64):

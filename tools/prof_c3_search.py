@@ -22,7 +22,10 @@ for _ in range(2):
     jb.search_knn_batch_device(g, idx, qd, sp, exact_data=ds)
 torch.cuda.synchronize()
 torch.cuda.cudart().cudaProfilerStart()
+a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+a.record()
 jb.search_knn_batch_device(g, idx, qd, sp, exact_data=ds)
+b.record()
 torch.cuda.synchronize()
 torch.cuda.cudart().cudaProfilerStop()
-print("done", flush=True)
+print(f"C3 search L={L} {est}: {a.elapsed_time(b):.3f} ms per 10K queries", flush=True)
