@@ -167,12 +167,22 @@ __device__ __forceinline__ float rabitq_dd_fast(const uint8_t* __restrict__ rec,
 #pragma unroll
     for (int b = 0; b < QB; ++b) acc[b] = 0;
     int s = 0;
+    // runtime stride (long records, e.g. 4 planes x 128 B at D = 960): the next word
+    // group's MB plane loads are issued before this group's popcounts
+    uint4 cur[MB];
+#pragma unroll
+    for (int bp = 0; bp < MB; ++bp)
+        cur[bp] = bp == 0 ? first : __ldg(reinterpret_cast<const uint4*>(rec + 4 * (bp * pw)));
 #pragma unroll
     for (int w0 = 0; w0 < pw; w0 += 4) {
+        uint4 nxt[MB];
+#pragma unroll
+        for (int bp = 0; bp < MB; ++bp)
+            nxt[bp] = (w0 + 4 < pw) ? __ldg(reinterpret_cast<const uint4*>(rec + 4 * (bp * pw + w0 + 4)))
+                                    : make_uint4(0, 0, 0, 0);
 #pragma unroll
         for (int bp = 0; bp < MB; ++bp) {
-            const uint4 c = (w0 == 0 && bp == 0) ? first
-                                                 : __ldg(reinterpret_cast<const uint4*>(rec + 4 * (bp * pw + w0)));
+            const uint4 c = cur[bp];
             pc += (__popc(c.x) + __popc(c.y) + __popc(c.z) + __popc(c.w)) << bp;
 #pragma unroll
             for (int b = 0; b < QB; ++b) {
@@ -182,6 +192,8 @@ __device__ __forceinline__ float rabitq_dd_fast(const uint8_t* __restrict__ rec,
                 else s += t << (b + bp);
             }
         }
+#pragma unroll
+        for (int bp = 0; bp < MB; ++bp) cur[bp] = nxt[bp];
     }
     if (MB == 1) {
 #pragma unroll
@@ -849,7 +861,10 @@ static int launch_search_kernel(SearchKernel kern, const SearchLayout& lay, cons
 // gains from 10 resident blocks; the float estimators keep 8.
 template <int SRC, int BITS, bool ALIGNED>
 static int launch_search(const jb_search_args& a, int hash_slots, cudaStream_t st) {
-    constexpr int MINB = SRC == JB_SRC_RABITQ_FAST ? JB_FAST_MINB : SRC == JB_SRC_RABITQ ? JB_RQ_MINB : JB_OTHER_MINB;
+    // multi-bit popcount records keep MB code planes live: 8 blocks/SM (64 registers) instead of spilling
+    constexpr int MINB = SRC == JB_SRC_RABITQ_FAST ? (BITS == 1 ? JB_FAST_MINB : 8)
+                         : SRC == JB_SRC_RABITQ    ? JB_RQ_MINB
+                                                   : JB_OTHER_MINB;
     const int L = a.beam_width;
     const SearchLayout lay = make_layout(SRC, a.dims, L, hash_slots, FAST_QB);
     if (a.degree_cap <= 32 && SRC == JB_SRC_RABITQ_FAST && BITS == 1) {
