@@ -191,4 +191,46 @@ __device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::); }
 
+// ---- per-warp bulk row staging (the copy engine's cp.async.bulk, sm_90+) -----
+// One lane per row issues one bulk copy (16 B multiples, 16 B aligned); completion
+// is counted in bytes on a per-warp mbarrier (count 1: lane 0's expect_tx arrive).
+// Replaces a warp-wide loop of 16 B cp.async per row: one instruction per row.
+__device__ __forceinline__ void wbar_init(uint64_t* bar) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((uint32_t)__cvta_generic_to_shared(bar)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+// lane 0 announces `bytes`, then each lane with a row issues its copy; every lane
+// must have finished reading the destination rows (generic proxy) before: the
+// proxy fence + __syncwarp order those reads before the async writes
+__device__ __forceinline__ void wbar_expect(uint64_t* bar, uint32_t bytes) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0)
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                         (uint32_t)__cvta_generic_to_shared(bar)),
+                     "r"(bytes)
+                     : "memory");
+    __syncwarp();
+}
+__device__ __forceinline__ void bulk_row(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     (uint32_t)__cvta_generic_to_shared(dst)),
+                 "l"(src), "r"(bytes), "r"((uint32_t)__cvta_generic_to_shared(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void wbar_wait(uint64_t* bar, uint32_t& phase) {
+    const uint32_t a = (uint32_t)__cvta_generic_to_shared(bar);
+    uint32_t ok = 0;
+    while (!ok) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(ok)
+            : "r"(a), "r"(phase)
+            : "memory");
+    }
+    phase ^= 1;
+}
+
 }  // namespace jb

@@ -56,7 +56,7 @@ constexpr int MAX_CHUNKS = 4;   // neighbour slots per hop: R <= 32 * MAX_CHUNKS
 constexpr int COOP_MAX = JB_COOP_MAX;  // merge: warp-cooperative placement up to this many candidates
 
 struct SearchLayout {
-    int q_off, beam_off, hash_off, newk_off, cid_off, stage_off, plane_off, bytes;
+    int q_off, beam_off, hash_off, newk_off, cid_off, bar_off, stage_off, plane_off, bytes;
     int chunk;      // staged elements per row chunk (multiple of 32, <= 128)
     int sstride;    // staged row stride in floats (chunk + 4)
     int hbits;      // log2(number of 4-way buckets)
@@ -77,6 +77,7 @@ __host__ __device__ constexpr SearchLayout make_layout(int src, int D, int L, in
     s.hash_off = off; off += (4 << s.hbits) * 4;
     s.newk_off = off; off += 32 * 4;
     s.cid_off = off; off += 32 * 4;
+    s.bar_off = off; off += 16;   // per-warp mbarrier of the bulk row staging
     s.chunk = ((D + 31) / 32) * 32 < JB_EXACT_CHUNK ? ((D + 31) / 32) * 32 : JB_EXACT_CHUNK;
     s.sstride = s.chunk + 4;
     s.stage_off = off;
@@ -362,6 +363,7 @@ struct QueryCtx {
     float qadd, qsumq, qlo, qdelta;
     int nwords, meta_off;
     uint32_t qn;              // EXACT_U8: integer query norm (query bytes at qv)
+    uint64_t* bar;            // EXACT: bulk-staging mbarrier
 };
 
 // One neighbour per lane (nb = -1: none): visited check, then the distance of
@@ -370,9 +372,12 @@ struct QueryCtx {
 // DIRECT (exact source, 16 B aligned rows): the lane that owns a new neighbour reads
 // its row straight from global memory instead of the warp staging rows in smem —
 // faster when the rows are L2-resident, slower from HBM (uncoalesced sectors).
+#ifndef JB_BULK
+#define JB_BULK 1  // exact rows staged by cp.async.bulk (one instruction per row); 0: warp-wide 16 B cp.async
+#endif
 template <int SRC, int BITS, bool ALIGNED, int KD = 0, bool DIRECT = false>
 __device__ __forceinline__ uint64_t eval_chunk(const jb_search_args& a, const SearchLayout& lay, const QueryCtx& c,
-                                               uint32_t* tab, int nb, int& evals, int& lossy) {
+                                               uint32_t* tab, int nb, int& evals, int& lossy, uint32_t& bphase) {
     const unsigned FULL = 0xFFFFFFFFu;
     const int lane = lane_id();
     const int D = KD > 0 ? KD : a.dims;
@@ -418,7 +423,12 @@ __device__ __forceinline__ uint64_t eval_chunk(const jb_search_args& a, const Se
         Acc4 acc; acc.zero();
         for (int e0 = 0; e0 < D; e0 += lay.chunk) {
             const int clen = min(lay.chunk, D - e0);
-            if (ALIGNED) {
+            if (ALIGNED && JB_BULK) {  // lane j copies row j's chunk (clen * 4 B, a 16 B multiple)
+                const uint32_t bytes = (uint32_t)clen * 4;
+                wbar_expect(c.bar, bytes * (uint32_t)nnew);
+                if (lane < nnew) bulk_row(c.stage + lane * lay.sstride, a.data + (size_t)myid * D + e0, bytes, c.bar);
+                wbar_wait(c.bar, bphase);
+            } else if (ALIGNED) {
                 const int nv = clen >> 2;
                 for (int j = 0; j < nnew; ++j) {
                     const float* src = a.data + (size_t)c.cid[j] * D + e0;
@@ -432,7 +442,7 @@ __device__ __forceinline__ uint64_t eval_chunk(const jb_search_args& a, const Se
                     for (int f = lane; f < clen; f += 32) cp_async4(dst + f, src + f);
                 }
             }
-            cp_async_wait_all();
+            if (!(ALIGNED && JB_BULK)) cp_async_wait_all();
             __syncwarp();
             if (lane < nnew) a1_range<ALIGNED, false>(acc, c.stage + lane * lay.sstride - e0, c.qv, e0, e0 + clen);
             __syncwarp();
@@ -481,6 +491,12 @@ beam_search_kernel(const jb_search_args a, const SearchLayout lay_arg, int* __re
     uint32_t* fmask = reinterpret_cast<uint32_t*>(base + lay.newk_off);  // survivor-slot mask, L/32 words
     int32_t* cid = reinterpret_cast<int32_t*>(base + lay.cid_off);
     float* stage = reinterpret_cast<float*>(base + lay.stage_off);
+    uint64_t* wbar = reinterpret_cast<uint64_t*>(base + lay.bar_off);
+    uint32_t bphase = 0;
+    if (SRC == JB_SRC_EXACT && ALIGNED && !DIRECT && JB_BULK) {
+        if (lane == 0) wbar_init(wbar);
+        __syncwarp();
+    }
     uint32_t* planes = reinterpret_cast<uint32_t*>(base + lay.plane_off);
     const int D = KD > 0 ? KD : a.dims;
     const int nwords = (((D + 31) / 32) + 3) & ~3;  // plane stride (16 B aligned)
@@ -516,7 +532,7 @@ beam_search_kernel(const jb_search_args a, const SearchLayout lay_arg, int* __re
         __syncwarp();
         float qlo = 0.0f, qdelta = 0.0f;
         if (SRC == JB_SRC_RABITQ_FAST) build_planes<FAST_QB>(qv, D, planes, qlo, qdelta);
-        const QueryCtx qc{qv, planes, cid, stage, qadd, qsumq, qlo, qdelta, nwords, meta_off, qn};
+        const QueryCtx qc{qv, planes, cid, stage, qadd, qsumq, qlo, qdelta, nwords, meta_off, qn, wbar};
 
         int lossy = 0;
         if (lane == 0) {
@@ -582,7 +598,8 @@ beam_search_kernel(const jb_search_args a, const SearchLayout lay_arg, int* __re
 #pragma unroll
             for (int c = 0; c < CH; ++c) {
                 if (c * 32 >= R) break;
-                const uint64_t key = eval_chunk<SRC, BITS, ALIGNED, KD, DIRECT>(a, lay, qc, tab, nbv[c], evals, lossy);
+                const uint64_t key =
+                    eval_chunk<SRC, BITS, ALIGNED, KD, DIRECT>(a, lay, qc, tab, nbv[c], evals, lossy, bphase);
                 const int p0 = merge_into_beam(beam, bcount, L, key, fmask);
                 s_min = min(s_min, p0);
                 p_ins = p0;
