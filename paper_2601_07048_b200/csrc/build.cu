@@ -429,7 +429,18 @@ __device__ __forceinline__ void write_row(int32_t* __restrict__ adj, int32_t* __
 // pivot | staged rows (crows) | their norms | u16 survivor list (split prune)
 template <class M>
 __host__ __device__ inline int vertex_warp_words(const M& m, int crows) {
-    return m.pivot_words() + crows * m.stage_stride_words() + ((crows + 3) & ~3) + ((crows + 7) & ~7) / 2;
+    return m.pivot_words() + crows * m.stage_stride_words() + ((crows + 3) & ~3) + ((crows + 7) & ~7) / 2 + 4;
+}
+// per-warp mbarrier of the bulk row staging (after the survivor list; 16 B aligned)
+__device__ __forceinline__ uint64_t* stage_bar(uint32_t* cn, int crows) {
+    return reinterpret_cast<uint64_t*>(cn + ((crows + 3) & ~3) + ((crows + 7) & ~7) / 2);
+}
+// lane 0 initialises the warp's staging barrier (once per kernel, before any stage())
+__device__ __forceinline__ uint64_t* init_stage_bar(uint32_t* cn, int crows) {
+    uint64_t* b = stage_bar(cn, crows);
+    if (crows > 0 && lane_id() == 0) wbar_init(b);
+    __syncwarp();
+    return b;
 }
 __device__ __forceinline__ uint16_t* stage_list(uint32_t* cn, int crows) {
     return reinterpret_cast<uint16_t*>(cn + ((crows + 3) & ~3));
@@ -491,7 +502,8 @@ phase2_kernel(const M m, int64_t start, int64_t nb, double alpha2, int R, const 
     if (h <= crows) {
         // (the Gram-screened prune measured no faster here: 17.9 vs 16.8 ms per 100K batch at
         // 3M, its extra smem costing what the screen saves; phase 2 is latency-bound)
-        m.stage(rows, cn, cand, h);
+        uint32_t sph = 0;
+        m.stage(rows, cn, cand, h, init_stage_bar(cn, crows), &sph);
         k = warp_prune_staged(cand, h, alpha2, R, m, rows, cn, stage_list(cn, crows), ki, kd);
     } else {
         k = warp_prune(cand, h, alpha2, R, m, pv, ki, kd);
@@ -760,7 +772,8 @@ refine_prune_kernel(const M m, int64_t start, int64_t nb, double alpha2, int R, 
     uint32_t* kd = kept_d + xi * R;
     int k;
     if (n <= crows) {
-        m.stage(rows, cn, cand, n);
+        uint32_t sph = 0;
+        m.stage(rows, cn, cand, n, init_stage_bar(cn, crows), &sph);
         k = warp_prune_staged(cand, n, alpha2, R, m, rows, cn, stage_list(cn, crows), ki, kd);
     } else {
         k = warp_prune(cand, n, alpha2, R, m, pv, ki, kd);
@@ -833,7 +846,7 @@ __device__ __forceinline__ void owner_one(const M& m, double alpha2, int R, int 
                    const uint64_t* __restrict__ key, int64_t total, const int32_t* __restrict__ seg_start, int64_t s,
                    uint64_t* __restrict__ pool, unsigned long long* __restrict__ pool_top,
                    int pool_cap, int32_t* __restrict__ adj, int32_t* __restrict__ deg, int* __restrict__ err, int crows,
-                   unsigned char* base, int32_t* __restrict__ defer, int* __restrict__ ndefer) {
+                   unsigned char* base, int32_t* __restrict__ defer, int* __restrict__ ndefer, uint32_t& sph) {
     const int lane = threadIdx.x & 31;
     constexpr int SC = OWNER_SC;
     uint64_t* scand = reinterpret_cast<uint64_t*>(base);
@@ -924,7 +937,7 @@ __device__ __forceinline__ void owner_one(const M& m, double alpha2, int R, int 
     if (n <= crows) {
         for (int j = lane; j < hd; j += 32) cand[j] = (uint64_t)(uint32_t)have[j];  // id only, for staging
         __syncwarp();
-        m.stage(rows, cn, cand, n);
+        m.stage(rows, cn, cand, n, stage_bar(cn, crows), &sph);
         for (int j = lane; j < hd; j += 32) cand[j] = key_of(m.dist_pivot_staged(pv, rows, cn, j), (uint32_t)have[j]);
         __syncwarp();
         bool done = false;
@@ -959,16 +972,23 @@ owner_merge_kernel(const M m, double alpha2, int R, int always_prune, const uint
     const int warp = threadIdx.x >> 5;
     const int per_warp = MODE == 1 ? owner_light_per_warp(R) : owner_per_warp(m, R, crows);
     unsigned char* base = shb + (size_t)warp * per_warp;
+    uint32_t sph = 0;  // the warp's staging-barrier phase (MODE 0 / 2 stage rows)
+    if (MODE != 1) {
+        constexpr int GB = std::is_same<M, F32Metric>::value ? GP_BYTES : 0;
+        uint32_t* cn = reinterpret_cast<uint32_t*>(base + OWNER_SC * 8 + GB) + m.pivot_words() +
+                       (size_t)crows * m.stage_stride_words();
+        init_stage_bar(cn, crows);
+    }
     if (MODE == 2) {  // persistent over the deferred targets
         const int nd = *ndefer;
         for (int64_t i = (int64_t)blockIdx.x * BW + warp; i < nd; i += (int64_t)gridDim.x * BW)
             owner_one<M, MODE>(m, alpha2, R, always_prune, tgt, key, total, seg_start, defer[i], pool, pool_top,
-                               pool_cap, adj, deg, err, crows, base, defer, ndefer);
+                               pool_cap, adj, deg, err, crows, base, defer, ndefer, sph);
     } else {
         const int64_t s = (int64_t)blockIdx.x * BW + warp;
         if (s >= *n_seg) return;
         owner_one<M, MODE>(m, alpha2, R, always_prune, tgt, key, total, seg_start, s, pool, pool_top, pool_cap, adj,
-                           deg, err, crows, base, defer, ndefer);
+                           deg, err, crows, base, defer, ndefer, sph);
     }
 }
 

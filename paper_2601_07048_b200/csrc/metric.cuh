@@ -76,11 +76,19 @@ struct F32Metric {
         const float dot = a1_dot<false>(data + (size_t)row * D, f, D);
         return __float_as_uint(exact_from_dot(__ldg(norms + row), dot, f[((D + 3) & ~3)]));
     }
-    // stage n candidate rows (ids in the low words of keys) + their norms
-    __device__ void stage(uint32_t* rows, uint32_t* cn, const uint64_t* keys, int n) const {
+    // stage n candidate rows (ids in the low words of keys) + their norms; with a
+    // per-warp mbarrier (bar, its phase) the rows go through cp.async.bulk, one
+    // copy-engine instruction per row instead of a warp-wide 16 B cp.async loop
+    __device__ void stage(uint32_t* rows, uint32_t* cn, const uint64_t* keys, int n, uint64_t* bar = nullptr,
+                          uint32_t* phase = nullptr) const {
         const int lane = lane_id();
         const int rs = stage_stride_words();
-        if ((D & 3) == 0) {
+        if (bar && (D & 3) == 0) {
+            wbar_expect(bar, (uint32_t)n * (uint32_t)D * 4u);
+            for (int j = lane; j < n; j += 32)
+                bulk_row(rows + (size_t)j * rs, data + (size_t)(uint32_t)(keys[j] & 0xFFFFFFFFull) * D, (uint32_t)D * 4u,
+                         bar);
+        } else if ((D & 3) == 0) {
             const int nv = D >> 2;
             for (int j = 0; j < n; ++j) {
                 const float* src = data + (size_t)(uint32_t)(keys[j] & 0xFFFFFFFFull) * D;
@@ -94,7 +102,8 @@ struct F32Metric {
         }
         for (int j = lane; j < n; j += 32)
             cn[j] = __float_as_uint(__ldg(norms + (uint32_t)(keys[j] & 0xFFFFFFFFull)));
-        cp_async_wait_all();
+        cp_async_wait_all();  // (also the caller's cp.async pivot copy, load_pivot_async)
+        if (bar && (D & 3) == 0) wbar_wait(bar, *phase);
         __syncwarp();
         if (split_ok()) {  // 4x4-transpose every 16-element block in place (one block per lane)
             const int nb = D >> 4;
@@ -264,7 +273,8 @@ struct U8Metric {
         const uint32_t dot = u8_dot(data + (size_t)row * D, reinterpret_cast<const uint8_t*>(pv), D);
         return u8_dist(__ldg(norms + row), dot, pv[((D + 15) & ~15) / 4]);
     }
-    __device__ void stage(uint32_t* rows, uint32_t* cn, const uint64_t* keys, int n) const {
+    __device__ void stage(uint32_t* rows, uint32_t* cn, const uint64_t* keys, int n, uint64_t* = nullptr,
+                          uint32_t* = nullptr) const {
         const int lane = lane_id();
         const int rs = stage_stride_words();
         if ((D & 15) == 0) {
@@ -430,7 +440,9 @@ struct RabitqMetric {
         return __float_as_uint(est);
     }
     // never staged (the host passes crows = 0); present for the shared kernel bodies
-    __device__ void stage(uint32_t*, uint32_t*, const uint64_t*, int) const { __trap(); }
+    __device__ void stage(uint32_t*, uint32_t*, const uint64_t*, int, uint64_t* = nullptr, uint32_t* = nullptr) const {
+        __trap();
+    }
     __device__ uint32_t dist_staged(const uint32_t*, const uint32_t*, int, int) const { __trap(); return 0; }
     __device__ void dist_staged2(const uint32_t*, const uint32_t*, int, int, int, uint32_t&, uint32_t&) const {
         __trap();
