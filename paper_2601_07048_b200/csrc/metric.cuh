@@ -346,8 +346,16 @@ __device__ __forceinline__ void rq_piece_full(Acc4& acc, const uint4 w4, const f
     }
 }
 
-// <u, q> for one record whose first 16-byte code piece is already in registers.
-template <int BITS>
+// 16 B load from a global record (read-only path) or a smem-staged one
+template <bool GL>
+__device__ __forceinline__ uint4 ld16(const uint8_t* p) {
+    if (GL) return __ldg(reinterpret_cast<const uint4*>(p));
+    return *reinterpret_cast<const uint4*>(p);
+}
+
+// <u, q> for one record whose first 16-byte code piece is already in registers
+// (GL: the record is in global memory; else staged in smem).
+template <int BITS, bool GL = true>
 __device__ __forceinline__ float rabitq_dd(const uint8_t* __restrict__ rec, uint4 first, const float* __restrict__ qv,
                                            int D) {
     constexpr int PER16 = 128 / BITS;  // elements per 16-byte piece
@@ -359,7 +367,7 @@ __device__ __forceinline__ float rabitq_dd(const uint8_t* __restrict__ rec, uint
     uint4 cur = first;
     for (; e0 + PER16 <= D; e0 += PER16) {
         uint4 nxt = make_uint4(0, 0, 0, 0);
-        if (e0 + PER16 < D) nxt = __ldg(reinterpret_cast<const uint4*>(rec + ((e0 + PER16) * BITS) / 8));
+        if (e0 + PER16 < D) nxt = ld16<GL>(rec + ((e0 + PER16) * BITS) / 8);
         rq_piece_full<BITS>(acc, cur, qv, e0);
         cur = nxt;
     }

@@ -56,7 +56,8 @@ constexpr int MAX_CHUNKS = 4;   // neighbour slots per hop: R <= 32 * MAX_CHUNKS
 constexpr int COOP_MAX = JB_COOP_MAX;  // merge: warp-cooperative placement up to this many candidates
 
 struct SearchLayout {
-    int q_off, beam_off, hash_off, newk_off, cid_off, bar_off, stage_off, plane_off, bytes;
+    int q_off, beam_off, hash_off, newk_off, cid_off, bar_off, stage_off, plane_off, rec_off, bytes;
+    int rec_stride;  // SREC: staged record stride (bytes, = 16 mod 128: conflict-free 16 B lane reads)
     int chunk;      // staged elements per row chunk (multiple of 32, <= 128)
     int sstride;    // staged row stride in floats (chunk + 4)
     int hbits;      // log2(number of 4-way buckets)
@@ -69,7 +70,7 @@ __host__ __device__ constexpr int log2i(int v) { int l = 0; while ((1 << l) < v)
 // last, so for a compile-time D and visited-table size every offset is a
 // constant (the specialised kernels then address smem as base + immediate).
 __host__ __device__ constexpr SearchLayout make_layout(int src, int D, int L, int hash_slots, int qb,
-                                                      bool direct = false) {
+                                                      bool direct = false, int rec_bytes = 0) {
     SearchLayout s{};
     int off = 0;
     s.q_off = off; off += ((D * 4) + 15) & ~15;
@@ -85,6 +86,12 @@ __host__ __device__ constexpr SearchLayout make_layout(int src, int D, int L, in
     s.plane_off = off;
     if (src == JB_SRC_RABITQ_FAST) off += qb * ((((D + 31) / 32) + 3) & ~3) * 4;
     off = (off + 15) & ~15;
+    s.rec_off = off;
+    s.rec_stride = 0;
+    if (rec_bytes > 0) {  // staged records, one slot per lane
+        s.rec_stride = ((rec_bytes - 16 + 127) / 128) * 128 + 16;
+        off += 32 * s.rec_stride;
+    }
     s.beam_off = off; off += ((L * 8) + 15) & ~15;
     s.bytes = (off + 15) & ~15;
     return s;
@@ -159,7 +166,7 @@ constexpr int FAST_QB = JB_FAST_QB;   // query bit-planes of the popcount estima
 // jb_rabitq_pack_planes): u = sum_b' 2^b' c_b', so
 //   <u, q> ~= lo * sum_b' 2^b' popc(c_b') + delta * sum_b' sum_b 2^(b'+b) popc(c_b' & plane_b).
 // For MB = 1 the plane record is the packed record itself.
-template <int QB, int PW = 0, int MB = 1>
+template <int QB, int PW = 0, int MB = 1, bool GL = true>
 __device__ __forceinline__ float rabitq_dd_fast(const uint8_t* __restrict__ rec, uint4 first,
                                                const uint32_t* __restrict__ planes, int pw_rt, float lo, float delta) {
     const int pw = PW > 0 ? PW : pw_rt;
@@ -173,14 +180,13 @@ __device__ __forceinline__ float rabitq_dd_fast(const uint8_t* __restrict__ rec,
     uint4 cur[MB];
 #pragma unroll
     for (int bp = 0; bp < MB; ++bp)
-        cur[bp] = bp == 0 ? first : __ldg(reinterpret_cast<const uint4*>(rec + 4 * (bp * pw)));
+        cur[bp] = bp == 0 ? first : ld16<GL>(rec + 4 * (bp * pw));
 #pragma unroll
     for (int w0 = 0; w0 < pw; w0 += 4) {
         uint4 nxt[MB];
 #pragma unroll
         for (int bp = 0; bp < MB; ++bp)
-            nxt[bp] = (w0 + 4 < pw) ? __ldg(reinterpret_cast<const uint4*>(rec + 4 * (bp * pw + w0 + 4)))
-                                    : make_uint4(0, 0, 0, 0);
+            nxt[bp] = (w0 + 4 < pw) ? ld16<GL>(rec + 4 * (bp * pw + w0 + 4)) : make_uint4(0, 0, 0, 0);
 #pragma unroll
         for (int bp = 0; bp < MB; ++bp) {
             const uint4 c = cur[bp];
@@ -363,7 +369,8 @@ struct QueryCtx {
     float qadd, qsumq, qlo, qdelta;
     int nwords, meta_off;
     uint32_t qn;              // EXACT_U8: integer query norm (query bytes at qv)
-    uint64_t* bar;            // EXACT: bulk-staging mbarrier
+    uint64_t* bar;            // EXACT / SREC: bulk-staging mbarrier
+    unsigned char* recs;      // SREC: staged records (rec_stride apart, slot = lane)
 };
 
 // One neighbour per lane (nb = -1: none): visited check, then the distance of
@@ -375,7 +382,7 @@ struct QueryCtx {
 #ifndef JB_BULK
 #define JB_BULK 1  // exact rows staged by cp.async.bulk (one instruction per row); 0: warp-wide 16 B cp.async
 #endif
-template <int SRC, int BITS, bool ALIGNED, int KD = 0, bool DIRECT = false>
+template <int SRC, int BITS, bool ALIGNED, int KD = 0, bool DIRECT = false, bool SREC = false>
 __device__ __forceinline__ uint64_t eval_chunk(const jb_search_args& a, const SearchLayout& lay, const QueryCtx& c,
                                                uint32_t* tab, int nb, int& evals, int& lossy, uint32_t& bphase) {
     const unsigned FULL = 0xFFFFFFFFu;
@@ -384,7 +391,7 @@ __device__ __forceinline__ uint64_t eval_chunk(const jb_search_args& a, const Se
     const int RB = a.record_bytes;
     // RaBitQ: issue the candidate's record loads before the visited check
     uint4 rc0 = make_uint4(0, 0, 0, 0), rc1 = make_uint4(0, 0, 0, 0);
-    if (SRC != JB_SRC_EXACT && nb >= 0) {
+    if (SRC != JB_SRC_EXACT && !SREC && nb >= 0) {
         const uint8_t* rec = a.records + (size_t)nb * RB;
         rc0 = __ldg(reinterpret_cast<const uint4*>(rec));
         if (RB == 32) rc1 = __ldg(reinterpret_cast<const uint4*>(rec + 16));
@@ -448,6 +455,25 @@ __device__ __forceinline__ uint64_t eval_chunk(const jb_search_args& a, const Se
             __syncwarp();
         }
         if (lane < nnew) d = exact_from_dot(__ldg(a.data_norms + myid), acc.reduce(), c.qadd);
+    } else if (SREC) {
+        // long records (high D): each new lane's record is staged into its smem slot
+        // by one cp.async.bulk (issued together), then read conflict-free from smem
+        myid = nb;
+        unsigned char* srec = c.recs + lane * lay.rec_stride;
+        wbar_expect(c.bar, (uint32_t)RB * (uint32_t)nnew);
+        if (isnew) bulk_row(srec, a.records + (size_t)myid * RB, (uint32_t)RB, c.bar);
+        wbar_wait(c.bar, bphase);
+        if (isnew) {
+            const uint4 f = ld16<false>(srec);
+            const float2 m = *reinterpret_cast<const float2*>(srec + c.meta_off);
+            if (SRC == JB_SRC_RABITQ_FAST) {
+                const float dd = rabitq_dd_fast<FAST_QB, 0, BITS, false>(srec, f, c.planes, c.nwords, c.qlo, c.qdelta);
+                const float est = (c.qadd + m.x) + m.y * (dd - c.qsumq);
+                d = est > 0.0f ? est : 0.0f;
+            } else {
+                d = rabitq_finish(rabitq_dd<BITS, false>(srec, f, c.qv, D), m, c.qadd, c.qsumq);
+            }
+        }
     } else {
         // the lane that owns the neighbour evaluates it from its registers
         myid = nb;
@@ -472,7 +498,8 @@ __device__ __forceinline__ uint64_t eval_chunk(const jb_search_args& a, const Se
 
 // KD > 0 and KHB > 0: compile-time dims and visited-table buckets (log2), so the
 // per-warp smem offsets are constants; the beam length (L) stays a runtime value.
-template <int SRC, int BITS, bool ALIGNED, int CH, int MINB, int KD = 0, int KHB = 0, bool DIRECT = false>
+template <int SRC, int BITS, bool ALIGNED, int CH, int MINB, int KD = 0, int KHB = 0, bool DIRECT = false,
+          bool SREC = false>
 __global__ void __launch_bounds__(WPB * 32, MINB)
 beam_search_kernel(const jb_search_args a, const SearchLayout lay_arg, int* __restrict__ counter) {
     extern __shared__ __align__(16) unsigned char smem[];
@@ -493,7 +520,8 @@ beam_search_kernel(const jb_search_args a, const SearchLayout lay_arg, int* __re
     float* stage = reinterpret_cast<float*>(base + lay.stage_off);
     uint64_t* wbar = reinterpret_cast<uint64_t*>(base + lay.bar_off);
     uint32_t bphase = 0;
-    if (SRC == JB_SRC_EXACT && ALIGNED && !DIRECT && JB_BULK) {
+    unsigned char* srecs = base + lay.rec_off;
+    if ((SRC == JB_SRC_EXACT && ALIGNED && !DIRECT && JB_BULK) || SREC) {
         if (lane == 0) wbar_init(wbar);
         __syncwarp();
     }
@@ -532,7 +560,7 @@ beam_search_kernel(const jb_search_args a, const SearchLayout lay_arg, int* __re
         __syncwarp();
         float qlo = 0.0f, qdelta = 0.0f;
         if (SRC == JB_SRC_RABITQ_FAST) build_planes<FAST_QB>(qv, D, planes, qlo, qdelta);
-        const QueryCtx qc{qv, planes, cid, stage, qadd, qsumq, qlo, qdelta, nwords, meta_off, qn, wbar};
+        const QueryCtx qc{qv, planes, cid, stage, qadd, qsumq, qlo, qdelta, nwords, meta_off, qn, wbar, srecs};
 
         int lossy = 0;
         if (lane == 0) {
@@ -599,7 +627,7 @@ beam_search_kernel(const jb_search_args a, const SearchLayout lay_arg, int* __re
             for (int c = 0; c < CH; ++c) {
                 if (c * 32 >= R) break;
                 const uint64_t key =
-                    eval_chunk<SRC, BITS, ALIGNED, KD, DIRECT>(a, lay, qc, tab, nbv[c], evals, lossy, bphase);
+                    eval_chunk<SRC, BITS, ALIGNED, KD, DIRECT, SREC>(a, lay, qc, tab, nbv[c], evals, lossy, bphase);
                 const int p0 = merge_into_beam(beam, bcount, L, key, fmask);
                 s_min = min(s_min, p0);
                 p_ins = p0;
@@ -831,6 +859,18 @@ static bool rows_l2_resident(const jb_search_args& a) {
     return (double)a.active_count * a.dims * 4.0 <= 0.5 * (double)l2;
 }
 
+#ifndef JB_SREC_MIN
+#define JB_SREC_MIN 256  // records of at least this many bytes are staged into smem (SREC kernels)
+#endif
+// JB_SREC=0 keeps high-D records on per-lane global loads (A/B)
+static bool srec_on() {
+    static const bool on = [] {
+        const char* e = std::getenv("JB_SREC");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 // JB_SEARCH_SPEC=0 disables the compile-time-shape kernels (A/B and debugging)
 static bool specialize_off() {
     static const bool off = [] {
@@ -895,6 +935,13 @@ static int launch_search(const jb_search_args& a, int hash_slots, cudaStream_t s
             JB_SPEC(128, 7) JB_SPEC(128, 8) JB_SPEC(96, 7) JB_SPEC(96, 8)
         }
 #undef JB_SPEC
+    }
+    if constexpr (SRC == JB_SRC_RABITQ || SRC == JB_SRC_RABITQ_FAST) {
+        if (a.degree_cap <= 32 && a.record_bytes >= JB_SREC_MIN && srec_on()) {
+            // high-D records (e.g. 496 B at D = 960, m = 4): staged per lane by the copy engine
+            const SearchLayout lr = make_layout(SRC, a.dims, L, hash_slots, FAST_QB, false, a.record_bytes);
+            return launch_search_kernel(beam_search_kernel<SRC, BITS, ALIGNED, 1, 8, 0, 0, false, true>, lr, a, st);
+        }
     }
     if (SRC == JB_SRC_EXACT && ALIGNED && a.degree_cap <= 32 && rows_l2_resident(a)) {
         const SearchLayout ld = make_layout(SRC, a.dims, L, hash_slots, FAST_QB, true);
