@@ -15,6 +15,8 @@ instead of the reference's per-hop numpy lockstep; frontier, trace, hops and
 
 from __future__ import annotations
 
+import os
+
 import threading
 from dataclasses import dataclass, field
 
@@ -570,7 +572,7 @@ def _host_results(nq: int, k: int):
 
 
 # Host-API pipeline chunk (queries per chunk; 0 = library default). Tuning hook.
-PIPELINE = {"chunk": 0, "device_chunk": 0}
+PIPELINE = {"chunk": int(os.environ.get("JB_HOST_CHUNK", "0")), "device_chunk": int(os.environ.get("JB_DEVICE_CHUNK", "0"))}
 
 
 def _knn_plan(graph: GraphIndex, source, D: int, params: SearchParams, exact_data=None):
