@@ -36,7 +36,8 @@ constexpr int BW = 4;  // warps per block in the per-vertex kernels
 #define JB_STAGE_KB 26     // per-warp smem budget for staged candidate rows
 #endif
 #ifndef JB_P2_KB
-#define JB_P2_KB 20  // phase-2 (new vertex) prune staging budget per warp
+#define JB_P2_KB 48  // phase-2 (new vertex) prune staging budget per warp (20 before bulk staging;
+                     // 48: prune 17.3 -> 13.4 ms per 100K batch at 3M x 96, C2 build +5%)
 #endif
 #ifndef JB_OWNER_EXTRA
 #define JB_OWNER_EXTRA 16  // owner-merge staging: up to R + this many candidate rows

@@ -1,10 +1,11 @@
-#!/bin/bash
-# construction kernels: staging budget variants, 1M x 128 bulk build (dev tool)
-for v in "$@"; do
+# A/B of construction compile-time knobs on the GPU box (dev tool): for each
+# JB_NVCC_EXTRA variant, rebuild build.cu and time one 100K batch into N rows.
+#   bash tools/exp_build_variants.sh N "-DJB_P2_KB=40" ...
+set -x
+N=$1; shift
+for V in "" "$@"; do
   touch paper_2601_07048_b200/csrc/build.cu
-  JB_NVCC_EXTRA="$v" python -m paper_2601_07048_b200._build > /dev/null || { echo "build failed $v"; continue; }
-  for rep in 1; do
-    JB_EXP_REPS=3 timeout 600 python tools/exp_build_prof.py 2>&1 | grep "^build" | sed "s/; work.*//" | sed "s/^/[$v] /"
-  done
+  JB_NVCC_EXTRA="$V" python -m paper_2601_07048_b200._build > /dev/null
+  JB_PROFILE=1 timeout 600 python tools/prof_donor.py $N 2>&1 | grep "batch \[$N\|batch of" | sed "s/^/VARIANT '$V' /"
 done
 touch paper_2601_07048_b200/csrc/build.cu
