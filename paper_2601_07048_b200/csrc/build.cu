@@ -272,7 +272,10 @@ __device__ int warp_prune_staged(uint64_t* cand, int n, double alpha2, int R, co
 // (A warp-level product: tcgen05's 128-row tiles and per-CTA issue do not fit a
 // per-warp 48 x 48 x D Gram; the exact A1 rounds it replaces were ~45% of the
 // owner merge's instructions.)
-constexpr int GP_MAX = 64;
+#ifndef JB_GP_MAX
+#define JB_GP_MAX 48  // = the owner staging limit at R = 32 (R + 16); 64 cost occupancy: merge 32.4 vs 29.6 ms per batch at 3M
+#endif
+constexpr int GP_MAX = JB_GP_MAX;  // candidates per Gram-screened prune (multiple of 16, <= 64)
 constexpr int GP_BYTES = GP_MAX + 16 * GP_MAX * 4 + GP_MAX * 4;  // ranks | Gram block | ranked norms
 
 __device__ __forceinline__ void mma_tf32_16x8x8(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
@@ -943,7 +946,7 @@ __device__ __forceinline__ void owner_one(const M& m, double alpha2, int R, int 
         __syncwarp();
         bool done = false;
         if constexpr (std::is_same<M, F32Metric>::value) {
-            if (m.gram_ok(n)) {
+            if (m.gram_ok(n, GP_MAX)) {
                 k = warp_prune_gram(cand, n, alpha2, R, m, rows, cn, rk, gb, kid, kd);
                 done = true;
             }

@@ -36,7 +36,7 @@ struct F32Metric {
     // Gram-screened staged prune (warp_prune_gram, build.cu) for <= 64 candidates;
     // JB_GRAM=0 turns it off (A/B). Requires D % 8 == 0.
     bool gram = false;
-    __host__ __device__ bool gram_ok(int n) const { return gram && (D & 7) == 0 && n <= 64; }
+    __host__ __device__ bool gram_ok(int n, int nmax = 64) const { return gram && (D & 7) == 0 && n <= nmax; }
 #ifdef JB_NO_SPLIT
     __host__ __device__ bool split_ok() const { return false; }  // dev A/B: natural layout, flat prune
 #else
