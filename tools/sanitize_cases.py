@@ -9,6 +9,9 @@ Cases (each tiny, so the instrumented run finishes in seconds):
              repair (BFS, donor scan, attach) all run; checked against the oracle
   pipeline   search_knn_batch host pipeline (two streams, chunked) + rerank
   protocol   bound distances, robust prune (row and matrix forms), shard pack/merge
+  staged     round-2 paths: exact search with bulk-staged rows (JB_EXACT_DIRECT=0),
+             960-d RaBitQ-4 search with bulk-staged records, a repair-heavy build
+             (tensor-core donor screen, Gram-screened owner prune, bulk staging)
 """
 
 from __future__ import annotations
@@ -103,9 +106,30 @@ def case_protocol():
     print("protocol ok")
 
 
+def case_staged():
+    import paper_2601_07048_b200 as jb
+    from conftest import gaussian, lowrank
+    from oracle import vamana
+
+    os.environ["JB_EXACT_DIRECT"] = "0"
+    x, q = gaussian(3000, 64, 7), gaussian(40, 64, 8)
+    p = jb.BuildParams(degree_cap=16, build_beam_width=32, alpha=1.2, max_batch=600)
+    g = jb.build(jb.VectorDataset(x), p)
+    og = vamana.build(x, R=16, L=32, alpha=1.2, max_batch=600)
+    assert np.array_equal(g.adjacency, og.adj)
+    jb.search_knn_batch(g, jb.VectorDataset(x), q, jb.SearchParams(beam_width=32, k=10))
+    xh, qh = lowrank(600, 960, 16, 0.05, 9), lowrank(8, 960, 16, 0.05, 10)
+    dh = jb.VectorDataset(xh)
+    gh = jb.build(dh, jb.BuildParams(degree_cap=8, build_beam_width=16, alpha=1.2))
+    ih = jb.rabitq_fit(dh, bits=4, seed=3)
+    for est in ("reference", "popcount"):
+        jb.search_knn_batch(gh, ih, qh, jb.SearchParams(beam_width=16, k=5, rerank=True, estimator=est), exact_data=dh)
+    print("staged ok")
+
+
 if __name__ == "__main__":
     import torch
 
     torch.cuda.set_device(0)
-    for name in (sys.argv[1:] or ["search", "insert", "pipeline", "protocol"]):
+    for name in (sys.argv[1:] or ["search", "insert", "pipeline", "protocol", "staged"]):
         globals()["case_" + name]()
