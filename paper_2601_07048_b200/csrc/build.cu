@@ -158,6 +158,7 @@ __device__ int warp_prune_split(uint64_t* cand, int n, double alpha2, int R, con
             if (om < mk) { mk = om; mi = oi; }
         }
         if (mk == UMAX) break;
+        __syncwarp();  // every lane's argmin reads of cand precede lane 0's write (WAR)
         if (lane == 0) {
             out_ids[kept] = (int32_t)(mk & 0xFFFFFFFFull);
             out_d[kept] = (uint32_t)(mk >> 32);
@@ -218,6 +219,7 @@ __device__ int warp_prune_staged(uint64_t* cand, int n, double alpha2, int R, co
             if (om < mk) { mk = om; mi = oi; }
         }
         if (mk == UMAX) break;
+        __syncwarp();  // every lane's argmin reads of cand precede lane 0's write (WAR)
         if (lane == 0) {
             out_ids[kept] = (int32_t)(mk & 0xFFFFFFFFull);
             out_d[kept] = (uint32_t)(mk >> 32);
@@ -1214,6 +1216,7 @@ owner_matrix_kernel(const F32Metric m, double alpha2, int R, int always_prune, c
             if (om < mk) { mk = om; mi = oi; }
         }
         if (mk == UMAX) break;
+        __syncwarp();  // every lane's argmin reads of cand precede lane 0's write (WAR)
         if (lane == 0) {
             kid[kept] = (int32_t)(mk & 0xFFFFFFFFull);
             kd[kept] = (uint32_t)(mk >> 32);
