@@ -506,6 +506,50 @@ def _insert_roofline(S, args, peak):
             "timed": "whole bulk build (wall clock, synchronized)", "traffic": None}
 
 
+def _insert_search_roofline(S, args, peak):
+    """The build's dominant HBM kernel alone: the phase-1 traced exact search
+    (`beam_search_kernel<EXACT>`, rows staged by cp.async.bulk) over 100K dataset
+    rows as queries at L_build on the built graph, CUDA events on the launching
+    stream. Algorithmic bytes = hops x (4R + 4) + reference-defined evals
+    (jb_count_evals: |{start} U N(expanded)|) x (4D + 4) + 4D per query."""
+    import torch
+
+    from paper_2601_07048_b200 import search as jsearch
+
+    jb = S["jb"]
+    g, ds = S["graph"], S["ds"]
+    nq = min(100_000, args.n)
+    q = ds.device().x[:nq].contiguous()
+    bound = jsearch._Bound(ds, q)
+    L, R, D = INDEX["L_build"], INDEX["R"], args.dim
+    cap = 4 * L + 64
+    out = None
+    for _ in range(2):
+        out = jsearch._launch(g, bound, L, None, cap)
+    ts = []
+    for _ in range(3):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        out = jsearch._launch(g, bound, L, None, cap)
+        b.record()
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    _, hops, evals, _, tids, _ = out
+    adj, _ = g.device()
+    ev = evals.clone()
+    jb._lib.check(jb._lib.lib().jb_count_evals(jb._lib.ptr(adj), R, jb._lib.ptr(tids), cap, jb._lib.ptr(hops), None,
+                                              g.entry_point, None, nq, jb._lib.ptr(ev), jb._lib.stream_ptr()))
+    torch.cuda.synchronize()
+    h, e = hops.double().sum().item(), ev.double().sum().item()
+    alg = h * (4 * R + 4) + e * (4 * D + 4) + nq * 4 * D
+    ms = float(np.median(ts))
+    gbs = alg / (ms / 1e3) / 1e9
+    return {"kernel": "beam_search_kernel<EXACT> (build phase-1 traced search)", "queries": nq, "L": L,
+            "bound": "hbm", "achieved": round(gbs, 1), "peak": peak, "unit": "GB/s", "frac": round(gbs / peak, 4),
+            "kernel_ms": round(ms, 3), "alg_bytes": int(alg), "hops_per_query": round(h / nq, 2),
+            "evals_reference_per_query": round(e / nq, 1)}
+
+
 def _search_fn(S, world, L, k, est="reference"):
     """Returns f(q_dev) -> (global ids, dists) running the full per-batch path."""
     jb = S["jb"]
@@ -861,7 +905,8 @@ def gpu_arm(args):
                   "rabitq_fit_s": round(S["t_fit"], 3), "gen_s": round(S["t_gen"], 2),
                   "graph_sha": _graph_sha(S["graph"].adjacency, S["graph"].degrees, S["graph"].active_count,
                                           S["graph"].entry_point),
-                  "roofline": _insert_roofline(S, args, peak)},
+                  "roofline": _insert_roofline(S, args, peak),
+                  "search_kernel_roofline": _insert_search_roofline(S, args, peak)},
         "estimators": {e: {"L": runs[e][0], "value": round(runs[e][3], 1),
                            "recall_at_10": next(p["recall"] for p in cal[e][1] if p["L"] == runs[e][0]),
                            "search_kernel_ms": round(runs[e][2]["search_ms"], 4),
