@@ -37,7 +37,10 @@
 
 namespace jb {
 
-constexpr int WPB = 4;          // warps per block
+#ifndef JB_WPB
+#define JB_WPB 4
+#endif
+constexpr int WPB = JB_WPB;     // warps per block
 #ifndef JB_RR_WARPS
 #define JB_RR_WARPS 4
 #endif
@@ -498,9 +501,15 @@ __device__ __forceinline__ uint64_t eval_chunk(const jb_search_args& a, const Se
 
 // KD > 0 and KHB > 0: compile-time dims and visited-table buckets (log2), so the
 // per-warp smem offsets are constants; the beam length (L) stays a runtime value.
+// warps per block: 2 for exact f32 rows (smem-bound by the staged rows: finer
+// blocks fit more warps per SM — the insert-path search 18.3 -> 15.7 ms per 100K at
+// 3M, 0.57 -> 0.66 of HBM), WPB otherwise (the popcount kernel: 4 measured best)
+template <int SRC>
+constexpr int warps_per_block() { return SRC == JB_SRC_EXACT ? 2 : WPB; }
+
 template <int SRC, int BITS, bool ALIGNED, int CH, int MINB, int KD = 0, int KHB = 0, bool DIRECT = false,
           bool SREC = false>
-__global__ void __launch_bounds__(WPB * 32, MINB)
+__global__ void __launch_bounds__(warps_per_block<SRC>() * 32, MINB)
 beam_search_kernel(const jb_search_args a, const SearchLayout lay_arg, int* __restrict__ counter) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int warp = threadIdx.x >> 5;
@@ -882,8 +891,9 @@ static bool specialize_off() {
 
 // Occupancy per (kernel, smem size) is cached: the attribute/occupancy queries
 // cost more than the launch itself for small batches.
-static int launch_search_kernel(SearchKernel kern, const SearchLayout& lay, const jb_search_args& a, cudaStream_t st) {
-    const int smem = lay.bytes * WPB;
+static int launch_search_kernel(SearchKernel kern, const SearchLayout& lay, const jb_search_args& a, cudaStream_t st,
+                                int nw = WPB) {
+    const int smem = lay.bytes * nw;
     JB_CHECK_ARG(smem <= 227 * 1024, "beam search: per-block shared memory %d B exceeds 227 KB", smem);
     // The smem attribute only grows, process-wide (grow_smem), so no host thread can
     // lower it below another thread's cached launch configuration. Occupancy per
@@ -898,17 +908,17 @@ static int launch_search_kernel(SearchKernel kern, const SearchLayout& lay, cons
         if (e.k == kern && e.smem == smem && e.dev == dev) per_sm = e.per_sm;
     if (per_sm == 0) {
         JB_CUDA_RC(grow_smem(kern, smem));
-        JB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, WPB * 32, smem));
+        JB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nw * 32, smem));
         JB_CHECK_ARG(per_sm >= 1, "beam search: kernel does not fit on an SM");
         cache[next] = Entry{kern, smem, dev, per_sm};
         next = (next + 1) % 16;
     }
-    int64_t need = (a.nq + WPB - 1) / WPB;
+    int64_t need = (a.nq + nw - 1) / nw;
     int grid = (int)std::min<int64_t>(need, (int64_t)per_sm * sm_count_current());
     Scratch ctr;
     JB_CUDA(ctr.alloc(sizeof(int), st));
     JB_CUDA(cudaMemsetAsync(ctr.p, 0, sizeof(int), st));
-    kern<<<grid, WPB * 32, smem, st>>>(a, lay, ctr.as<int>());
+    kern<<<grid, nw * 32, smem, st>>>(a, lay, ctr.as<int>());
     JB_LAUNCH_CHECK();
     return JB_OK;
 }
@@ -922,6 +932,7 @@ static int launch_search(const jb_search_args& a, int hash_slots, cudaStream_t s
     constexpr int MINB = SRC == JB_SRC_RABITQ_FAST ? (BITS == 1 ? JB_FAST_MINB : 8)
                          : SRC == JB_SRC_RABITQ    ? JB_RQ_MINB
                                                    : JB_OTHER_MINB;
+    constexpr int NW = warps_per_block<SRC>();
     const int L = a.beam_width;
     const SearchLayout lay = make_layout(SRC, a.dims, L, hash_slots, FAST_QB);
     if (a.degree_cap <= 32 && SRC == JB_SRC_RABITQ_FAST && BITS == 1) {
@@ -930,7 +941,7 @@ static int launch_search(const jb_search_args& a, int hash_slots, cudaStream_t s
         const int hb = lay.hbits;
 #define JB_SPEC(KD_, KHB_)                                                                                   \
     if (a.dims == KD_ && hb == KHB_)                                                                         \
-        return launch_search_kernel(beam_search_kernel<SRC, BITS, ALIGNED, 1, MINB, KD_, KHB_>, lay, a, st);
+        return launch_search_kernel(beam_search_kernel<SRC, BITS, ALIGNED, 1, MINB, KD_, KHB_>, lay, a, st, NW);
         if (ALIGNED && !specialize_off()) {
             JB_SPEC(128, 7) JB_SPEC(128, 8) JB_SPEC(96, 7) JB_SPEC(96, 8)
         }
@@ -940,15 +951,15 @@ static int launch_search(const jb_search_args& a, int hash_slots, cudaStream_t s
         if (a.degree_cap <= 32 && a.record_bytes >= JB_SREC_MIN && srec_on()) {
             // high-D records (e.g. 496 B at D = 960, m = 4): staged per lane by the copy engine
             const SearchLayout lr = make_layout(SRC, a.dims, L, hash_slots, FAST_QB, false, a.record_bytes);
-            return launch_search_kernel(beam_search_kernel<SRC, BITS, ALIGNED, 1, 8, 0, 0, false, true>, lr, a, st);
+            return launch_search_kernel(beam_search_kernel<SRC, BITS, ALIGNED, 1, 8, 0, 0, false, true>, lr, a, st, NW);
         }
     }
     if (SRC == JB_SRC_EXACT && ALIGNED && a.degree_cap <= 32 && rows_l2_resident(a)) {
         const SearchLayout ld = make_layout(SRC, a.dims, L, hash_slots, FAST_QB, true);
-        return launch_search_kernel(beam_search_kernel<SRC, BITS, ALIGNED, 1, MINB, 0, 0, true>, ld, a, st);
+        return launch_search_kernel(beam_search_kernel<SRC, BITS, ALIGNED, 1, MINB, 0, 0, true>, ld, a, st, NW);
     }
-    if (a.degree_cap <= 32) return launch_search_kernel(beam_search_kernel<SRC, BITS, ALIGNED, 1, MINB>, lay, a, st);
-    return launch_search_kernel(beam_search_kernel<SRC, BITS, ALIGNED, MAX_CHUNKS, 8>, lay, a, st);
+    if (a.degree_cap <= 32) return launch_search_kernel(beam_search_kernel<SRC, BITS, ALIGNED, 1, MINB>, lay, a, st, NW);
+    return launch_search_kernel(beam_search_kernel<SRC, BITS, ALIGNED, MAX_CHUNKS, 8>, lay, a, st, NW);
 }
 
 }  // namespace jb
