@@ -32,6 +32,10 @@
 namespace jb {
 
 constexpr int BW = 4;  // warps per block in the per-vertex kernels
+#ifndef JB_OWNER_BW
+#define JB_OWNER_BW 3  // 9 warps/SM instead of 8 at ~24 KB per warp: merge 29.9 -> 29.1 ms per batch at 3M
+#endif
+constexpr int OWNER_BW = JB_OWNER_BW;  // warps per block of the deferred owner pass (smem-bound)
 #ifndef JB_STAGE_KB
 #define JB_STAGE_KB 26     // per-warp smem budget for staged candidate rows
 #endif
@@ -987,7 +991,8 @@ owner_merge_kernel(const M m, double alpha2, int R, int always_prune, const uint
     }
     if (MODE == 2) {  // persistent over the deferred targets
         const int nd = *ndefer;
-        for (int64_t i = (int64_t)blockIdx.x * BW + warp; i < nd; i += (int64_t)gridDim.x * BW)
+        const int wpb = (int)(blockDim.x >> 5);  // the deferred pass runs OWNER_BW-warp blocks
+        for (int64_t i = (int64_t)blockIdx.x * wpb + warp; i < nd; i += (int64_t)gridDim.x * wpb)
             owner_one<M, MODE>(m, alpha2, R, always_prune, tgt, key, total, seg_start, defer[i], pool, pool_top,
                                pool_cap, adj, deg, err, crows, base, defer, ndefer, sph);
     } else {
@@ -2117,13 +2122,14 @@ static int merge_phase(const M& m, const jb_insert_args& a, double alpha2, uint3
                 mo, alpha2, R, a.always_prune, tt, tk, ntri, seg, nseg, pool, ptop, pool_cap, a.adjacency, a.degrees, err,
                 crows, defer, ndefer);
             JB_LAUNCH_CHECK();
-            JB_CUDA_RC(grow_smem(owner_merge_kernel<M, 2>, osm));
+            const int osm2 = owner_per_warp(m, R, crows) * OWNER_BW;
+            JB_CUDA_RC(grow_smem(owner_merge_kernel<M, 2>, osm2));
             int per_sm = 0;
-            JB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, owner_merge_kernel<M, 2>, BW * 32, osm));
-            const int64_t want = (hseg + BW - 1) / BW;
+            JB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, owner_merge_kernel<M, 2>, OWNER_BW * 32, osm2));
+            const int64_t want = (hseg + OWNER_BW - 1) / OWNER_BW;
             const unsigned g2 = (unsigned)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)std::max(1, per_sm) *
                                                                                        sm_count_current()));
-            owner_merge_kernel<M, 2><<<g2, BW * 32, osm, st>>>(mo, alpha2, R, a.always_prune, tt, tk, ntri, seg, nseg,
+            owner_merge_kernel<M, 2><<<g2, OWNER_BW * 32, osm2, st>>>(mo, alpha2, R, a.always_prune, tt, tk, ntri, seg, nseg,
                                                                pool, ptop, pool_cap, a.adjacency, a.degrees, err, crows,
                                                                defer, ndefer);
         }
