@@ -35,13 +35,20 @@ constexpr int BW = 4;  // warps per block in the per-vertex kernels
 #ifndef JB_OWNER_BW
 #define JB_OWNER_BW 3  // 9 warps/SM instead of 8 at ~24 KB per warp: merge 29.9 -> 29.1 ms per batch at 3M
 #endif
+#ifndef JB_P2_BW
+#define JB_P2_BW 1
+#endif
+#ifndef JB_P2_ROWS
+#define JB_P2_ROWS 80  // phase-2 staged trace rows (traces average ~70 candidates at L_build = 64;
+                       // at 3M x 96: 68 rows 16.3 ms, 76 rows 7.0 ms, 84 rows 7.6 ms per 100K batch)
+#endif
+constexpr int P2_BW = JB_P2_BW;  // warps per block of phase 2 (smem-bound by the staged traces)
 constexpr int OWNER_BW = JB_OWNER_BW;  // warps per block of the deferred owner pass (smem-bound)
 #ifndef JB_STAGE_KB
 #define JB_STAGE_KB 26     // per-warp smem budget for staged candidate rows
 #endif
 #ifndef JB_P2_KB
-#define JB_P2_KB 48  // phase-2 (new vertex) prune staging budget per warp (20 before bulk staging;
-                     // 48: prune 17.3 -> 13.4 ms per 100K batch at 3M x 96, C2 build +5%)
+#define JB_P2_KB 64  // phase-2 (new vertex) prune staging budget per warp (cap; JB_P2_ROWS sets the size)
 #endif
 #ifndef JB_OWNER_EXTRA
 #define JB_OWNER_EXTRA 16  // owner-merge staging: up to R + this many candidate rows
@@ -497,7 +504,7 @@ phase2_kernel(const M m, int64_t start, int64_t nb, double alpha2, int R, const 
     uint32_t* pv = shw + (size_t)warp * vertex_warp_words(m, crows);
     uint32_t* rows = pv + m.pivot_words();
     uint32_t* cn = rows + (size_t)crows * m.stage_stride_words();
-    const int64_t xi = (int64_t)blockIdx.x * BW + warp;
+    const int64_t xi = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;  // P2_BW-warp blocks
     if (xi >= nb) return;
     const uint32_t x = (uint32_t)(start + xi);
     const int h = min(hops[xi], cap);
@@ -2266,7 +2273,9 @@ static int batch_insert_impl(const M& m, const jb_insert_args& a, cudaStream_t s
     BALLOC(tk, uint64_t, ntri);
     // smem-staged candidate rows when a trace fits in ~26 KB per warp; longer traces
     // prune from L1/L2 (staging them would cost more occupancy than it saves)
-    const int crows2 = staged_rows(m, cap, R, JB_P2_KB);
+    // stage traces of up to P2_ROWS candidates (1-warp blocks: smem per warp sets the
+    // occupancy exactly); longer traces prune from global rows
+    const int crows2 = staged_rows(m, std::min(cap, JB_P2_ROWS), R, JB_P2_KB);
     bool p2_done = false;
     if constexpr (std::is_same<M, F32Metric>::value) {
         // rows too large to stage per warp: block per vertex, dot matrix — when the
@@ -2281,10 +2290,10 @@ static int batch_insert_impl(const M& m, const jb_insert_args& a, cudaStream_t s
             p2_done = true;
         }
     }
-    const int p2_smem = BW * 4 * vertex_warp_words(m, crows2);
+    const int p2_smem = P2_BW * 4 * vertex_warp_words(m, crows2);
     JB_CUDA_RC(grow_smem(phase2_kernel<M>, p2_smem));
     if (!p2_done)
-    phase2_kernel<M><<<(unsigned)((nb + BW - 1) / BW), BW * 32, p2_smem, st>>>(
+    phase2_kernel<M><<<(unsigned)((nb + P2_BW - 1) / P2_BW), P2_BW * 32, p2_smem, st>>>(
         split_prune(m), a.start, nb, alpha2, R, hops, tids, tdst, cap, a.reverse_all_visited, cand, kid, kd, a.adjacency, a.degrees,
         tt, tk, W, crows2);
     JB_LAUNCH_CHECK();
