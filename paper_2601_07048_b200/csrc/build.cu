@@ -1574,11 +1574,12 @@ __global__ void attach_kernel(const M m, int32_t* __restrict__ adj, int32_t* __r
                               int32_t* __restrict__ seen, const int32_t* __restrict__ lost,
                               const int32_t* __restrict__ order, int nlost, const int32_t* __restrict__ donors, int fan,
                               int32_t* __restrict__ queue, unsigned long long* __restrict__ bridges,
-                              int* __restrict__ err, int32_t* __restrict__ err_vertex) {
+                              int* __restrict__ err, int32_t* __restrict__ err_vertex, int* __restrict__ evictions) {
     extern __shared__ __align__(16) uint32_t ash[];
     uint32_t* pv = ash;
     const int lane = threadIdx.x;
     unsigned long long added = 0;
+    int evicted = 0;
     for (int oi = 0; oi < nlost; ++oi) {
         const int i = order[oi];
         const int32_t x = lost[i];
@@ -1608,6 +1609,7 @@ __global__ void attach_kernel(const M m, int32_t* __restrict__ adj, int32_t* __r
                 }
                 __syncwarp();
                 if (bests >= R) continue;  // saturated with bridges: next donor
+                ++evicted;
                 // remove slot `bests`, keeping order (and pins): ascending 32-wide chunks
                 for (int c = bests; c < du - 1; c += 32) {
                     const int sidx = c + lane;
@@ -1651,7 +1653,10 @@ __global__ void attach_kernel(const M m, int32_t* __restrict__ adj, int32_t* __r
             __syncwarp();
         }
     }
-    if (lane == 0) *bridges += added;
+    if (lane == 0) {
+        *bridges += added;
+        *evictions = evicted;
+    }
 }
 
 // ---- host orchestration -----------------------------------------------------
@@ -1812,10 +1817,10 @@ static int repair(const M& m, const jb_insert_args& a, int64_t n_active, int64_t
     BALLOC(reach, int32_t, n_active);
     BALLOC(pinned, uint8_t, (size_t)n_active * R);
     BALLOC(bridges, unsigned long long, 1);
-    BALLOC(err, int, 2);
+    BALLOC(err, int, 3);  // no-donor flag, its vertex, evictions of the round
     JB_CUDA(cudaMemsetAsync(pinned, 0, (size_t)n_active * R, st));
     JB_CUDA(cudaMemsetAsync(bridges, 0, sizeof(unsigned long long), st));
-    JB_CUDA(cudaMemsetAsync(err, 0, 2 * sizeof(int), st));
+    JB_CUDA(cudaMemsetAsync(err, 0, 3 * sizeof(int), st));
     const int T = 256;
     const unsigned nblk = (unsigned)((n_active + T - 1) / T);
     for (int round = 0;; ++round) {
@@ -1937,16 +1942,24 @@ static int repair(const M& m, const jb_insert_args& a, int64_t n_active, int64_t
         JB_CUDA_RC(grow_smem(attach_kernel<M>, asm_bytes));
         rt.mark("order");
         attach_kernel<M><<<1, 32, asm_bytes, st>>>(m, a.adjacency, a.degrees, R, pinned, seen, lost, oval2, nlost,
-                                                    donors, fan, fa, bridges, err, err + 1);
+                                                    donors, fan, fa, bridges, err, err + 1, err + 2);
         JB_LAUNCH_CHECK();
         rt.mark("attach");
         rt.report(round, round, "  repair timings round");
-        int herr[2];
-        JB_CUDA(cudaMemcpyAsync(herr, err, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
+        int herr[3];
+        JB_CUDA(cudaMemcpyAsync(herr, err, 3 * sizeof(int), cudaMemcpyDeviceToHost, st));
         JB_CUDA(cudaStreamSynchronize(st));
         if (herr[0]) {
             set_error("connectivity repair: no donor for vertex %d", herr[1]);
             return JB_ENODONOR;
+        }
+        // Without evictions the round only added edges: every vertex reachable before
+        // still is, and the attach kernel's BFS-extend marked each bridged vertex and
+        // what it reaches, so the next round's BFS would find nothing stranded.
+        if (herr[2] == 0) {
+            if (getenv("JB_PROFILE") && getenv("JB_PROFILE")[0] == '1')
+                fprintf(stderr, "[jb]   repair round %d: no evictions, reachability complete\n", round);
+            break;
         }
         if (round > 10000) { set_error("connectivity repair did not converge"); return JB_ECUDA; }
     }
