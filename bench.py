@@ -305,7 +305,17 @@ def reference_arm(args):
                                        "identical_to_c_port": bool(np.array_equal(vg.adj, cg.adj))}
         log(f"[reference] inserts: " + ", ".join(f"{k} {v['inserts_per_s']:.0f}/s" for k, v in inserts.items()))
 
-    out = _json_base(args, 1, L)
+    # Under torchrun with N > 1 the GPU arm searches N shards of args.n rows (weak
+    # scaling; every query visits every shard). The CPU reference on the same host
+    # cores would search the N shards one after another: the shard-0 rate divided
+    # by N (the shards are statistically identical; sample stated in cpu_baseline).
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world > 1:
+        value = round(value / world, 1)
+        for v in variants.values():
+            v["value"] = round(v["value"] / world, 1)
+            v["sample"] += f"; shard 0 timed, {world} shards -> rate / {world}"
+    out = _json_base(args, world, L)
     out.update({
         "impl": "reference", "value": value, "ms_per_step": round(1e3 * args.nq / value, 2),
         "cpu_baseline": {"value": value, "unit": "queries/s", "cores": variants[best]["cores"], "kind": "port",
