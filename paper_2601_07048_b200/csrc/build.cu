@@ -878,19 +878,31 @@ __device__ __forceinline__ void owner_one(const M& m, double alpha2, int R, int 
                               : reinterpret_cast<int32_t*>(pv + vertex_warp_words(m, crows));
     int32_t* kid = have + R;
     uint32_t* kd = reinterpret_cast<uint32_t*>(kid + R);
+    // Dependent global round trips kept to three: the segment start; its first 32
+    // targets and keys together; the target's degree and whole row together.
     const int64_t g0 = seg_start[s];
-    const uint32_t t = tgt[g0];
-    int64_t g1 = g0;
-    for (;;) {  // group end: first index whose target differs
-        const int64_t i = g1 + lane;
-        const bool same = i < total && tgt[i] == t;
-        const uint32_t msk = __ballot_sync(0xFFFFFFFFu, same);
-        g1 += __popc(msk);
-        if (msk != 0xFFFFFFFFu) break;
+    const uint32_t tl = (g0 + lane < total) ? tgt[g0 + lane] : NO_TARGET;
+    const uint64_t kl = (g0 + lane < total) ? key[g0 + lane] : 0;
+    const uint32_t t = __shfl_sync(0xFFFFFFFFu, tl, 0);
+    int64_t g1 = g0 + __popc(__ballot_sync(0xFFFFFFFFu, tl == t));
+    if (g1 - g0 == 32) {
+        for (;;) {  // group end: first index whose target differs
+            const int64_t i = g1 + lane;
+            const bool same = i < total && tgt[i] == t;
+            const uint32_t msk = __ballot_sync(0xFFFFFFFFu, same);
+            g1 += __popc(msk);
+            if (msk != 0xFFFFFFFFu) break;
+        }
     }
     const int g = (int)(g1 - g0);
-    const int hd = deg[t];
-    for (int j = lane; j < hd; j += 32) have[j] = adj[(size_t)t * R + j];
+    int hd;
+    {
+        const int32_t* row = adj + (size_t)t * R;
+        int32_t r0 = lane < R ? row[lane] : -1;
+        hd = deg[t];
+        if (lane < hd) have[lane] = r0;
+        for (int j = lane + 32; j < hd; j += 32) have[j] = row[j];
+    }
     __syncwarp();
     // candidate storage: smem when it fits, else a bump-allocated global slice
     uint64_t* cand = scand;
@@ -915,7 +927,7 @@ __device__ __forceinline__ void owner_one(const M& m, double alpha2, int R, int 
         bool fresh = false;
         uint64_t k = 0;
         if (j < g) {
-            k = key[g0 + j];
+            k = b == 0 ? kl : key[g0 + j];
             const int32_t src = (int32_t)(k & 0xFFFFFFFFull);
             fresh = true;
             for (int e = 0; e < hd; ++e) fresh &= (have[e] != src);
