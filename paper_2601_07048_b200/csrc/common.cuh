@@ -170,14 +170,16 @@ __device__ __forceinline__ void warp_bitonic_sort_smem(uint64_t* s, int n) {
     }
 }
 
-// lower_bound over a sorted u64 array (masked compare)
+// lower_bound over a sorted u64 array (masked compare). Branch-free halving: the
+// trip count depends on n only, so the lanes of a warp (same n) stay converged.
 __device__ __forceinline__ int lower_bound_masked(const uint64_t* a, int n, uint64_t key) {
-    int lo = 0, hi = n;
-    while (lo < hi) {
-        int mid = (lo + hi) >> 1;
-        if (key_mask(a[mid]) < key) lo = mid + 1; else hi = mid;
+    int base = 0, len = n;
+    while (len > 1) {
+        const int half = len >> 1;
+        base += (key_mask(a[base + half - 1]) < key) ? half : 0;
+        len -= half;
     }
-    return lo;
+    return base + ((len == 1 && key_mask(a[base]) < key) ? 1 : 0);
 }
 
 // cp.async helpers (LDGSTS on sm_100a)

@@ -391,7 +391,10 @@ __device__ __forceinline__ uint64_t eval_chunk(const jb_search_args& a, const Se
     const unsigned FULL = 0xFFFFFFFFu;
     const int lane = lane_id();
     const int D = KD > 0 ? KD : a.dims;
-    const int RB = a.record_bytes;
+    // compile-time record size for the specialised popcount kernels (KD > 0: m = 1 plane
+    // records of KD bits + 8 B metadata, rounded to 16 B)
+    const int RB = (SRC == JB_SRC_RABITQ_FAST && KD > 0 && BITS == 1) ? ((((KD + 31) / 32 + 3) & ~3) * 4 + 8 + 15) / 16 * 16
+                                                                      : a.record_bytes;
     // RaBitQ: issue the candidate's record loads before the visited check
     uint4 rc0 = make_uint4(0, 0, 0, 0), rc1 = make_uint4(0, 0, 0, 0);
     if (SRC != JB_SRC_EXACT && !SREC && nb >= 0) {
