@@ -264,6 +264,13 @@ typedef struct jb_insert_args {
      * reaches reachable vertices) instead of the exact scan over all reachable
      * rows (build.py:185-192), for 10M-row streaming. */
     int32_t repair_beam_width;
+    /* Extension: per-vertex prune closure, [capacity] f64 on device (or NULL = off;
+     * f32 builds only). closure[v] = alpha^2 of the robust prune that last wrote
+     * v's row, 0 after an append or a bridge; the owner merge of a row closed at
+     * alpha_a^2 <= alpha^2 only tests the pairs that involve its fresh sources
+     * (same result). Must be zeroed whenever the adjacency is written outside
+     * these calls (the Python GraphIndex does so on every host upload). */
+    double* closure;
 } jb_insert_args;
 
 /* One three-phase batch: search -> prune + reverse triples -> grouped merge,

@@ -55,6 +55,7 @@ class InsertArgs(C.Structure):
         ("quantized", i32), ("records", p), ("record_bytes", i32), ("bits", i32),
         ("bound_rotated", p), ("bound_qadd", p), ("bound_qsumq", p),
         ("repair_beam_width", i32),
+        ("closure", p),
     ]
 
 

@@ -16,6 +16,8 @@ the RaBitQ estimate against the pivot's bound row (build.py:105-111, 124-129).
 
 from __future__ import annotations
 
+import itertools
+
 import os
 import sys
 import time
@@ -140,6 +142,22 @@ def _bound_rows(quantizer, ds):
     return idx, (rot, qa, qs)
 
 
+_TOKENS = itertools.count(1)
+
+
+def _rows_token(dev) -> int:
+    """A never-reused identity of a dataset's device rows (the prune-closure key: a
+    device address can be reused by another dataset after the first is freed)."""
+    tok = getattr(dev, "_closure_token", None)
+    if tok is None:
+        tok = next(_TOKENS)
+        try:
+            dev._closure_token = tok
+        except AttributeError:  # immutable holder: no reuse across calls, closure restarts
+            pass
+    return tok
+
+
 def _args(graph: GraphIndex, ds, params: BuildParams, start: int, stop: int, quantizer=None):
     adj, deg = graph.device()
     dev = ds.device()
@@ -158,6 +176,12 @@ def _args(graph: GraphIndex, ds, params: BuildParams, start: int, stop: int, qua
     a.repair_beam_width = int(params.repair_beam_width)
     a.start, a.stop = start, stop
     a.entry_point = graph.entry_point
+    # prune closure (extension): f32 rows only; any other build writes rows without
+    # maintaining it, so it is invalidated
+    if quantizer is None and ds.element_kind is not ElementKind.U8:
+        a.closure = _lib.ptr(graph.device_closure(_rows_token(dev)))
+    else:
+        graph.invalidate_closure()
     if quantizer is not None:
         idx, (rot, qa, qs) = _bound_rows(quantizer, ds)
         if idx.count < max(stop, graph.active_count):

@@ -289,7 +289,8 @@ __device__ int warp_prune_staged(uint64_t* cand, int n, double alpha2, int R, co
 #define JB_GP_MAX 48  // = the owner staging limit at R = 32 (R + 16); 64 cost occupancy: merge 32.4 vs 29.6 ms per batch at 3M
 #endif
 constexpr int GP_MAX = JB_GP_MAX;  // candidates per Gram-screened prune (multiple of 16, <= 64)
-constexpr int GP_BYTES = GP_MAX + 16 * GP_MAX * 4 + GP_MAX * 4;  // ranks | Gram block | ranked norms
+// Gram block | ranked norms | ranks | closed-row prune: 16 x 2 domination masks + 16 fresh positions
+constexpr int GP_BYTES = ((16 * GP_MAX * 4 + GP_MAX * 4 + GP_MAX + 7) & ~7) + 16 * 8 * 2 + 32;
 
 __device__ __forceinline__ void mma_tf32_16x8x8(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
                                                 uint32_t b0, uint32_t b1) {
@@ -333,6 +334,38 @@ __device__ __forceinline__ void gram_block(const uint32_t* __restrict__ rows, in
     }
 }
 
+// Gram rows of an explicit candidate list (arow[0 .. na), na <= 16) against every
+// ranked position: gb[i][c] = <x_arow[i], x_rk[c]> for c < n (row stride GP_MAX).
+__device__ __forceinline__ void gram_rows(const uint32_t* __restrict__ rows, int rs, int D, const uint8_t* arow, int na,
+                                          const uint8_t* rk, int n, float* __restrict__ gb) {
+    const int lane = lane_id(), g = lane >> 2, t = lane & 3;
+    const uint32_t* pa0 = rows + (size_t)arow[g < na ? g : 0] * rs + t;
+    const uint32_t* pa1 = rows + (size_t)arow[g + 8 < na ? g + 8 : 0] * rs + t;
+    const int nj = (n + 7) >> 3;
+    float acc[GP_MAX / 8][4];
+    const uint32_t* pb[GP_MAX / 8];
+#pragma unroll
+    for (int j = 0; j < GP_MAX / 8; ++j) {
+        acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
+        const int c = 8 * j + g;
+        pb[j] = rows + (size_t)rk[c < n ? c : 0] * rs + t;
+    }
+    for (int k = 0; k < D; k += 8) {
+        const uint32_t a0 = pa0[k], a1 = pa1[k], a2 = pa0[k + 4], a3 = pa1[k + 4];
+#pragma unroll
+        for (int j = 0; j < GP_MAX / 8; ++j)
+            if (j < nj) mma_tf32_16x8x8(acc[j], a0, a1, a2, a3, pb[j][k], pb[j][k + 4]);
+    }
+#pragma unroll
+    for (int j = 0; j < GP_MAX / 8; ++j) {
+        if (j < nj) {
+            *reinterpret_cast<float2*>(gb + g * GP_MAX + 8 * j + 2 * t) = make_float2(acc[j][0], acc[j][1]);
+            if (na > 8)
+                *reinterpret_cast<float2*>(gb + (g + 8) * GP_MAX + 8 * j + 2 * t) = make_float2(acc[j][2], acc[j][3]);
+        }
+    }
+}
+
 // exact A1 dot of staged rows i and p (per lane; natural or block-transposed layout)
 __device__ __forceinline__ float staged_dot(const F32Metric& m, const uint32_t* rows, int i, int p) {
     const int rs = m.stage_stride_words();
@@ -361,7 +394,8 @@ __device__ __forceinline__ float staged_dot(const F32Metric& m, const uint32_t* 
 }
 
 __device__ int warp_prune_gram(uint64_t* cand, int n, double alpha2, int R, const F32Metric& m, const uint32_t* rows,
-                               const uint32_t* cn, uint8_t* rk, float* gb, int32_t* out_ids, uint32_t* out_d) {
+                               const uint32_t* cn, uint8_t* rk, float* gb, int32_t* out_ids, uint32_t* out_d,
+                               int hd_closed = -1) {
     const unsigned FULL = 0xFFFFFFFFu;
     const int lane = lane_id();
     const int rs = m.stage_stride_words();
@@ -388,6 +422,83 @@ __device__ int warp_prune_gram(uint64_t* cand, int n, double alpha2, int R, cons
     // bound absorbs the screen's own f32 roundings (relative 2^-23 each) many times over
     const float a2lo = (float)alpha2 * (1.0f - 0x1p-20f), a2hi = (float)alpha2 * (1.0f + 0x1p-20f);
     const float E = 0x1p-8f;
+    // one pair test, screened: does ranked position `s` (as the star) prune ranked `c`?
+    // (alpha^2 d(s, c) <= d(t, c); d symmetric bit for bit, so one Gram entry serves both roles)
+    auto prunes = [&](float g, float ns, float nc, float dtc, int is, int ic) -> bool {
+        const float nn = ns + nc;
+        const float dd = fmaf(-2.0f, g, nn);
+        const float err = E * nn;
+        if (a2lo * (dd - err) > dtc) return false;
+        if (a2hi * (dd + err) < dtc) return true;
+        const float d = exact_from_dot(__uint_as_float(cn[ic]), staged_dot(m, rows, ic, is), __uint_as_float(cn[is]));
+        return !(__dmul_rn(alpha2, (double)d) > (double)dtc);
+    };
+    if (hd_closed >= 0 && n - hd_closed >= 1 && n - hd_closed <= 16) {
+        // Closed row (its hd_closed existing members came out of a robust prune at
+        // alpha_a^2 <= alpha^2, so none of them prunes another): only pairs with a
+        // fresh source (candidate index >= hd_closed) can prune. Per fresh f:
+        // doms[f] = ranked candidates after f that f prunes, domby[f] = ranked
+        // candidates before f that prune f; one scan in rank order then keeps c iff
+        // no kept candidate before it prunes it — the reference's extraction result.
+        uint64_t* fdoms = reinterpret_cast<uint64_t*>(rk + GP_MAX);
+        uint64_t* fdomby = fdoms + 16;
+        uint8_t* fpos = reinterpret_cast<uint8_t*>(fdomby + 16);
+        const bool fr0 = lane < n && i0 >= hd_closed, fr1 = lane + 32 < n && i1 >= hd_closed;
+        const uint32_t fm0 = __ballot_sync(FULL, fr0), fm1 = __ballot_sync(FULL, fr1);
+        const int nf = __popc(fm0) + __popc(fm1);
+        if (fr0) fpos[__popc(fm0 & lanemask_lt())] = (uint8_t)lane;
+        if (fr1) fpos[__popc(fm0) + __popc(fm1 & lanemask_lt())] = (uint8_t)(lane + 32);
+        __syncwarp();
+        uint8_t* arow = fpos + 16;  // candidate indices of the fresh rows (the Gram's A operand)
+        if (lane < nf) arow[lane] = rk[fpos[lane]];
+        __syncwarp();
+        gram_rows(rows, rs, m.D, arow, nf, rk, n, gb);
+        __syncwarp();
+        for (int f = 0; f < nf; ++f) {
+            const int pf = fpos[f];
+            const int ifr = rk[pf];
+            const float nfr = snorm[pf];
+            const float dtf = __uint_as_float((uint32_t)(cand[ifr] >> 32));
+            const float* grow = gb + f * GP_MAX;
+            bool d0 = false, b0 = false, d1 = false, b1 = false;
+            if (lane < n && lane != pf) {
+                const float g = grow[lane];
+                if (lane > pf) d0 = prunes(g, nfr, n0, dt0, ifr, i0);
+                else b0 = prunes(g, n0, nfr, dtf, i0, ifr);
+            }
+            if (lane + 32 < n && lane + 32 != pf) {
+                const float g = grow[lane + 32];
+                if (lane + 32 > pf) d1 = prunes(g, nfr, n1, dt1, ifr, i1);
+                else b1 = prunes(g, n1, nfr, dtf, i1, ifr);
+            }
+            const uint64_t dm = (uint64_t)__ballot_sync(FULL, d0) | ((uint64_t)__ballot_sync(FULL, d1) << 32);
+            const uint64_t bm = (uint64_t)__ballot_sync(FULL, b0) | ((uint64_t)__ballot_sync(FULL, b1) << 32);
+            if (lane == 0) { fdoms[f] = dm; fdomby[f] = bm; }
+        }
+        __syncwarp();
+        const uint64_t fmask = (uint64_t)fm0 | ((uint64_t)fm1 << 32);
+        uint64_t kept_mask = 0, kdoms = 0;
+        int kept = 0, f = 0;
+        for (int c = 0; c < n && kept < R; ++c) {
+            bool dominated;
+            const bool isf = (fmask >> c) & 1ull;
+            if (isf) dominated = (fdomby[f] & kept_mask) != 0;
+            else dominated = ((kdoms >> c) & 1ull) != 0;
+            if (!dominated) {
+                kept_mask |= 1ull << c;
+                if (isf) kdoms |= fdoms[f];
+                if (lane == 0) {
+                    const uint64_t kc = cand[rk[c]];
+                    out_ids[kept] = (int32_t)(kc & 0xFFFFFFFFull);
+                    out_d[kept] = (uint32_t)(kc >> 32);
+                }
+                ++kept;
+            }
+            if (isf) ++f;
+        }
+        __syncwarp();
+        return kept;
+    }
     uint32_t alive0 = __ballot_sync(FULL, lane < n), alive1 = __ballot_sync(FULL, lane + 32 < n);
     int kept = 0, blk = -1;
     while (kept < R && (alive0 | alive1)) {
@@ -435,11 +546,17 @@ __device__ int warp_prune_gram(uint64_t* cand, int n, double alpha2, int R, cons
     return kept;
 }
 
-__device__ __forceinline__ void write_row(int32_t* __restrict__ adj, int32_t* __restrict__ deg, int R, uint32_t v,
-                                          const int32_t* ids, int n) {
+// Every row written here is the output of a robust prune at alpha2: the row is
+// recorded as closed at alpha2 (F32 builds with closure tracking; else a no-op).
+template <class M>
+__device__ __forceinline__ void write_row(const M& m, double alpha2, int32_t* __restrict__ adj,
+                                          int32_t* __restrict__ deg, int R, uint32_t v, const int32_t* ids, int n) {
     const int lane = lane_id();
     for (int j = lane; j < R; j += 32) adj[(size_t)v * R + j] = j < n ? ids[j] : -1;
-    if (lane == 0) deg[v] = n;
+    if (lane == 0) {
+        deg[v] = n;
+        m.close_row(v, alpha2);
+    }
 }
 
 // Per-warp smem of the per-vertex kernels:
@@ -487,7 +604,7 @@ seed_prune_kernel(const M m, int64_t start, int64_t stop, int64_t xi0, int64_t x
     int32_t* ki = kept_ids + (xi - xi0) * R;
     uint32_t* kd = kept_d + (xi - xi0) * R;
     const int k = warp_prune(cand, (int)(n - 1), alpha2, R, m, pv, ki, kd);
-    write_row(adj, deg, R, x, ki, k);
+    write_row(m, alpha2, adj, deg, R, x, ki, k);
 }
 
 // ---- phase 2: prune each new vertex's visited trace, emit reverse triples ----
@@ -525,7 +642,7 @@ phase2_kernel(const M m, int64_t start, int64_t nb, double alpha2, int R, const 
     } else {
         k = warp_prune(cand, h, alpha2, R, m, pv, ki, kd);
     }
-    write_row(adj, deg, R, x, ki, k);
+    write_row(m, alpha2, adj, deg, R, x, ki, k);
     // reverse triples (target, source=x, dist): kept edges, or the whole trace
     uint32_t* tt = tri_target + xi * W;
     uint64_t* tk = tri_key + xi * W;
@@ -720,7 +837,7 @@ phase2_matrix_kernel(const F32Metric m, int64_t start, int64_t nb, double alpha2
         }
         __syncwarp();
     }
-    write_row(adj, deg, R, x, ki, k);
+    write_row(m, alpha2, adj, deg, R, x, ki, k);
     uint32_t* tt = tri_target + xi * W;
     uint64_t* tk = tri_key + xi * W;
     const int ne = reverse_all ? h : k;
@@ -796,7 +913,7 @@ refine_prune_kernel(const M m, int64_t start, int64_t nb, double alpha2, int R, 
         k = warp_prune(cand, n, alpha2, R, m, pv, ki, kd);
     }
     __syncwarp();
-    write_row(adj, deg, R, x, ki, k);
+    write_row(m, alpha2, adj, deg, R, x, ki, k);
     uint32_t* tt = tri_target + xi * R;
     uint64_t* tk = tri_key + xi * R;
     for (int j = lane; j < R; j += 32) {
@@ -940,7 +1057,10 @@ __device__ __forceinline__ void owner_one(const M& m, double alpha2, int R, int 
     if (nf == 0) return;
     if (!always_prune && hd + nf <= R) {  // append in (dist, source) order
         for (int j = lane; j < nf; j += 32) adj[(size_t)t * R + hd + j] = (int32_t)(cand[hd + j] & 0xFFFFFFFFull);
-        if (lane == 0) deg[t] = hd + nf;
+        if (lane == 0) {
+            deg[t] = hd + nf;
+            m.open_row(t);  // appended, not pruned: no closure
+        }
         return;
     }
     if (MODE == 1) {  // a prune: the deferred pass (staged rows, Gram screen)
@@ -972,7 +1092,8 @@ __device__ __forceinline__ void owner_one(const M& m, double alpha2, int R, int 
         bool done = false;
         if constexpr (std::is_same<M, F32Metric>::value) {
             if (m.gram_ok(n, GP_MAX)) {
-                k = warp_prune_gram(cand, n, alpha2, R, m, rows, cn, rk, gb, kid, kd);
+                k = warp_prune_gram(cand, n, alpha2, R, m, rows, cn, rk, gb, kid, kd,
+                                    m.row_closed(t, alpha2) ? hd : -1);
                 done = true;
             }
         }
@@ -987,7 +1108,7 @@ __device__ __forceinline__ void owner_one(const M& m, double alpha2, int R, int 
         __syncwarp();
         k = warp_prune(cand, n, alpha2, R, m, pv, kid, kd);
     }
-    write_row(adj, deg, R, t, kid, k);
+    write_row(m, alpha2, adj, deg, R, t, kid, k);
 }
 
 template <class M, int MODE>
@@ -1108,7 +1229,10 @@ owner_matrix_kernel(const F32Metric m, double alpha2, int R, int always_prune, c
                 if (!always_prune && hd + nf <= R) {
                     for (int j = lane; j < nf; j += 32)
                         adj[(size_t)t * R + hd + j] = (int32_t)(cand[hd + j] & 0xFFFFFFFFull);
-                    if (lane == 0) deg[t] = hd + nf;
+                    if (lane == 0) {
+                        deg[t] = hd + nf;
+                        m.open_row(t);  // appended, not pruned: no closure
+                    }
                 } else {
                     mode = (hd + nf <= MX - 1) ? 1 : 2;
                 }
@@ -1139,7 +1263,7 @@ owner_matrix_kernel(const F32Metric m, double alpha2, int R, int always_prune, c
         }
         __syncwarp();
         const int k = warp_prune(cand, n, alpha2, R, m, pv, kid, kd);
-        write_row(adj, deg, R, t, kid, k);
+        write_row(m, alpha2, adj, deg, R, t, kid, k);
         return;
     }
     // ---- dot matrix of the n candidates and the target (row n) ----
@@ -1258,7 +1382,7 @@ owner_matrix_kernel(const F32Metric m, double alpha2, int R, int always_prune, c
         __syncwarp();
     }
     __syncwarp();
-    write_row(adj, deg, R, t, kid, kept);
+    write_row(m, alpha2, adj, deg, R, t, kid, kept);
 }
 
 // ---- repair: BFS ------------------------------------------------------------
@@ -1637,6 +1761,7 @@ __global__ void attach_kernel(const M m, int32_t* __restrict__ adj, int32_t* __r
                 row[du] = x;
                 pin[du] = 1;
                 deg[u] = du + 1;
+                m.open_row((uint32_t)u);  // bridged (and maybe evicted): no closure
             }
             __syncwarp();
             placed = true;
@@ -2413,6 +2538,8 @@ static int with_metric(const jb_insert_args& a, F&& f) {
     F32Metric m{a.data, a.data_norms, a.dims};
     const char* e = getenv("JB_GRAM");
     m.gram = !(e && e[0] == '0');
+    const char* c = getenv("JB_CLOSURE");
+    m.closure = (c && c[0] == '0') ? nullptr : a.closure;  // JB_CLOSURE=0: full prunes (A/B)
     return f(m);
 }
 

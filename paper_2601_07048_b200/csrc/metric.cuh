@@ -37,6 +37,18 @@ struct F32Metric {
     // JB_GRAM=0 turns it off (A/B). Requires D % 8 == 0.
     bool gram = false;
     __host__ __device__ bool gram_ok(int n, int nmax = 64) const { return gram && (D & 7) == 0 && n <= nmax; }
+    // Prune closure per vertex (build.cu, owner merge): closure[v] = alpha^2 of the
+    // robust prune that last wrote v's row, 0 after any other write (append, bridge).
+    // A row closed at alpha_a^2 <= the current alpha^2 has no member pruning a later
+    // one, so a merge only needs the pairs involving the fresh sources. nullptr: off.
+    double* closure = nullptr;
+    __device__ void close_row(uint32_t v, double alpha2) const { if (closure) closure[v] = alpha2; }
+    __device__ void open_row(uint32_t v) const { if (closure) closure[v] = 0.0; }
+    __device__ bool row_closed(uint32_t v, double alpha2) const {
+        if (!closure) return false;
+        const double c = closure[v];
+        return c > 0.0 && c <= alpha2;
+    }
 #ifdef JB_NO_SPLIT
     __host__ __device__ bool split_ok() const { return false; }  // dev A/B: natural layout, flat prune
 #else
@@ -253,6 +265,9 @@ struct U8Metric {
     int D;
     static constexpr bool kInt = true;
     static constexpr bool kStage = true;
+    __device__ void close_row(uint32_t, double) const {}
+    __device__ void open_row(uint32_t) const {}
+    __device__ bool row_closed(uint32_t, double) const { return false; }
     static constexpr bool kSplit = false;
 
     __host__ __device__ int row_bytes() const { return D; }
@@ -421,6 +436,9 @@ struct RabitqMetric {
     int D;
     static constexpr bool kInt = false;
     static constexpr bool kStage = false;
+    __device__ void close_row(uint32_t, double) const {}
+    __device__ void open_row(uint32_t) const {}
+    __device__ bool row_closed(uint32_t, double) const { return false; }
     static constexpr bool kSplit = false;
 
     __host__ __device__ int meta_off() const { return ((((D * BITS) + 7) / 8 + 15) / 16) * 16; }

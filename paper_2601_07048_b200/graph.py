@@ -88,6 +88,8 @@ class GraphIndex:
         self._lock = threading.RLock()
         self.h2d_bytes = 0         # slab bytes uploaded so far (instrumentation)
         self.d2h_bytes = 0         # slab bytes downloaded so far
+        self._dev_closure = None   # per-vertex prune closure (jb_insert_args.closure), device f64
+        self._closure_key = None   # the f32 dataset the closure flags were computed against
 
     # ---- host view -------------------------------------------------------
     def _sync_host(self) -> None:
@@ -205,7 +207,25 @@ class GraphIndex:
                 self._dev_deg.copy_(torch.from_numpy(self._deg))
                 self.h2d_bytes += self._adj.nbytes + self._deg.nbytes
                 self._host_dirty = False
+                self.invalidate_closure()  # rows written on the host: no row is known to be closed
         return self._dev_adj, self._dev_deg
+
+    def device_closure(self, key):
+        """Per-vertex prune closure (jb_insert_args.closure) for f32 builds against the
+        dataset identified by `key`; zeroed when the dataset changes or rows are
+        written outside the library's prune kernels."""
+        torch = _lib.require_cuda()
+        with self._lock:
+            if self._dev_closure is None:
+                self._dev_closure = torch.zeros(self.capacity, dtype=torch.float64, device="cuda")
+            elif self._closure_key != key:
+                self._dev_closure.zero_()
+            self._closure_key = key
+        return self._dev_closure
+
+    def invalidate_closure(self) -> None:
+        if self._dev_closure is not None:
+            self._dev_closure.zero_()
 
     def mark_device_modified(self) -> None:
         """Called after kernels wrote the device slab."""
