@@ -1174,7 +1174,7 @@ owner_matrix_kernel(const F32Metric m, double alpha2, int R, int always_prune, c
     int32_t* kid = have + R;
     uint32_t* kd = reinterpret_cast<uint32_t*>(kid + R);
     uint32_t* pv = kd + R;                                        // pivot row (fallback path), 16 B aligned below
-    __shared__ int mode_s, n_s;
+    __shared__ int mode_s, n_s, hdc_s;
     __shared__ uint64_t* cand_s;
     pv = reinterpret_cast<uint32_t*>((reinterpret_cast<uintptr_t>(pv) + 15) & ~uintptr_t(15));
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -1246,12 +1246,17 @@ owner_matrix_kernel(const F32Metric m, double alpha2, int R, int always_prune, c
                 nrm[j] = id >= 0 ? __ldg(m.norms + id) : 0.0f;
             }
         }
-        if (lane == 0) { mode_s = mode; n_s = hd + nf; cand_s = cand; }
+        if (lane == 0) {
+            mode_s = mode; n_s = hd + nf; cand_s = cand;
+            // closed row with few fresh sources: only the fresh and target rows of the matrix
+            hdc_s = (mode == 1 && nf <= 16 && m.row_closed(t, alpha2)) ? hd : -1;
+        }
     }
     __syncthreads();
     const int mode = mode_s;
     if (mode == 0) return;
     const int n = n_s;
+    const int hdc = hdc_s;
     uint64_t* cand = cand_s;
     if (mode == 2) {  // hub target: the global-row prune on warp 0
         if (warp != 0) return;
@@ -1275,8 +1280,10 @@ owner_matrix_kernel(const F32Metric m, double alpha2, int R, int always_prune, c
 #pragma unroll
         for (int b = 0; b < 4; ++b) acc[a][b].zero();
     constexpr int KB = 16;
-    // sub-tiles wholly past the N live rows / columns skip the math (warp-uniform in ty)
-    const bool live = ty * 4 < N && tx * 4 < N;
+    // sub-tiles wholly past the N live rows / columns skip the math (warp-uniform in ty);
+    // for a closed row only the row groups holding the fresh rows and the target
+    // (rows hdc .. n) are needed
+    const bool live = ty * 4 < N && tx * 4 < N && (hdc < 0 || ty * 4 + 3 >= hdc);
     // each thread's 4 slice elements: rows tid/16 + 16h, column tid%16; the next
     // k-step's are loaded into registers while the current one is consumed
     const int srow = tid / KB, scol = tid % KB;
@@ -1344,10 +1351,82 @@ owner_matrix_kernel(const F32Metric m, double alpha2, int R, int always_prune, c
     __syncthreads();
     if (warp != 0) return;
     // existing neighbours: d(t -> e) with the target as the pivot; fresh keys stay
+    // (row n of the matrix: dot(a, b) == dot(b, a) bit for bit)
     const int hd = deg[t];
     for (int j = lane; j < hd; j += 32)
-        cand[j] = key_of(__float_as_uint(exact_from_dot(nrm[j], dotm[j * (MX + 1) + n], nrm[n])), (uint32_t)ids[j]);
+        cand[j] = key_of(__float_as_uint(exact_from_dot(nrm[j], dotm[n * (MX + 1) + j], nrm[n])), (uint32_t)ids[j]);
     __syncwarp();
+    if (hdc >= 0) {
+        // closed row: only pairs with a fresh source (candidate index >= hd) can prune
+        // (warp_prune_gram's closed path, with exact dots from the matrix rows hd .. n-1)
+        uint8_t* rk = reinterpret_cast<uint8_t*>(S);                 // [MX] ranked -> candidate
+        uint64_t* fdoms = reinterpret_cast<uint64_t*>(S + MX);       // [16]
+        uint64_t* fdomby = fdoms + 16;                               // [16]
+        uint8_t* fpos = reinterpret_cast<uint8_t*>(fdomby + 16);     // [16]
+        const unsigned FULL = 0xFFFFFFFFu;
+        const uint64_t k0 = lane < n ? cand[lane] : UMAX, k1 = lane + 32 < n ? cand[lane + 32] : UMAX;
+        int c0 = 0, c1 = 0;
+        for (int j = 0; j < n; ++j) {
+            const uint64_t kj = cand[j];
+            c0 += kj < k0;
+            c1 += kj < k1;
+        }
+        if (lane < n) rk[c0] = (uint8_t)lane;
+        if (lane + 32 < n) rk[c1] = (uint8_t)(lane + 32);
+        __syncwarp();
+        const int i0 = lane < n ? rk[lane] : 0, i1 = lane + 32 < n ? rk[lane + 32] : 0;
+        const bool fr0 = lane < n && i0 >= hd, fr1 = lane + 32 < n && i1 >= hd;
+        const uint32_t fm0 = __ballot_sync(FULL, fr0), fm1 = __ballot_sync(FULL, fr1);
+        const int nfr = __popc(fm0) + __popc(fm1);
+        if (fr0) fpos[__popc(fm0 & lanemask_lt())] = (uint8_t)lane;
+        if (fr1) fpos[__popc(fm0) + __popc(fm1 & lanemask_lt())] = (uint8_t)(lane + 32);
+        __syncwarp();
+        const float dt0 = __uint_as_float((uint32_t)(cand[i0] >> 32)), dt1 = __uint_as_float((uint32_t)(cand[i1] >> 32));
+        // does candidate `is` (as the star) prune candidate `ic`? d(is -> ic) from the fresh row f
+        auto prunes = [&](int f, int is, int ic, float dtc) -> bool {
+            const float d = exact_from_dot(nrm[ic], dotm[f * (MX + 1) + (f == is ? ic : is)], nrm[is]);
+            return !(__dmul_rn(alpha2, (double)d) > (double)dtc);
+        };
+        for (int q = 0; q < nfr; ++q) {
+            const int pf = fpos[q];
+            const int ifr = rk[pf];
+            const float dtf = __uint_as_float((uint32_t)(cand[ifr] >> 32));
+            bool d0 = false, b0 = false, d1 = false, b1 = false;
+            if (lane < n && lane != pf) {
+                if (lane > pf) d0 = prunes(ifr, ifr, i0, dt0);
+                else b0 = prunes(ifr, i0, ifr, dtf);
+            }
+            if (lane + 32 < n && lane + 32 != pf) {
+                if (lane + 32 > pf) d1 = prunes(ifr, ifr, i1, dt1);
+                else b1 = prunes(ifr, i1, ifr, dtf);
+            }
+            const uint64_t dm = (uint64_t)__ballot_sync(FULL, d0) | ((uint64_t)__ballot_sync(FULL, d1) << 32);
+            const uint64_t bm = (uint64_t)__ballot_sync(FULL, b0) | ((uint64_t)__ballot_sync(FULL, b1) << 32);
+            if (lane == 0) { fdoms[q] = dm; fdomby[q] = bm; }
+        }
+        __syncwarp();
+        const uint64_t fmask = (uint64_t)fm0 | ((uint64_t)fm1 << 32);
+        uint64_t kept_mask = 0, kdoms = 0;
+        int kept = 0, q = 0;
+        for (int c = 0; c < n && kept < R; ++c) {
+            const bool isf = (fmask >> c) & 1ull;
+            const bool dominated = isf ? (fdomby[q] & kept_mask) != 0 : ((kdoms >> c) & 1ull) != 0;
+            if (!dominated) {
+                kept_mask |= 1ull << c;
+                if (isf) kdoms |= fdoms[q];
+                if (lane == 0) {
+                    const uint64_t kc = cand[rk[c]];
+                    kid[kept] = (int32_t)(kc & 0xFFFFFFFFull);
+                    kd[kept] = (uint32_t)(kc >> 32);
+                }
+                ++kept;
+            }
+            if (isf) ++q;
+        }
+        __syncwarp();
+        write_row(m, alpha2, adj, deg, R, t, kid, kept);
+        return;
+    }
     // robust prune from the matrix (same extraction sequence as warp_prune)
     int kept = 0;
     while (kept < R) {
