@@ -972,6 +972,113 @@ extern "C" int jb_debug_owner_stats(unsigned long long* out) {
 }
 #endif
 
+// Closed-row prune for candidate sets too large to stage (rows read from global
+// memory, e.g. R = 64): the same fresh-pair masks as warp_prune_gram's closed path,
+// exact A1 distances (one dot per (fresh, candidate) pair serves both roles), up to
+// 128 candidates (4 ranked positions per lane, 128-bit masks). `pv` is free scratch
+// for one pivot row; `scr` >= 16 x 32 + 160 bytes.
+__device__ int prune_closed_global(uint64_t* cand, int n, int hd, double alpha2, int R, const F32Metric& m, uint32_t* pv,
+                                   unsigned char* scr, int32_t* out_ids, uint32_t* out_d) {
+    const unsigned FULL = 0xFFFFFFFFu;
+    const int lane = lane_id();
+    uint64_t* fdoms = reinterpret_cast<uint64_t*>(scr);  // [16][2]
+    uint64_t* fdomby = fdoms + 32;                        // [16][2]
+    uint8_t* rk = reinterpret_cast<uint8_t*>(fdomby + 32);  // [128]
+    uint8_t* fpos = rk + 128;                             // [16]
+    // rank by key (keys are distinct): position of each of this lane's candidates
+    uint64_t kk[4];
+    int rank[4] = {0, 0, 0, 0};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) kk[q] = lane + 32 * q < n ? cand[lane + 32 * q] : UMAX;
+    for (int j = 0; j < n; ++j) {
+        const uint64_t kj = cand[j];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) rank[q] += kj < kk[q];
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+        if (lane + 32 * q < n) rk[rank[q]] = (uint8_t)(lane + 32 * q);
+    __syncwarp();
+    // this lane's ranked positions lane + 32 q: candidate index, key distance, row id, norm
+    int ic[4];
+    float dt[4], nc[4];
+    uint32_t fm[4];
+    int nf = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const int c = lane + 32 * q;
+        ic[q] = c < n ? rk[c] : 0;
+        const uint64_t kc = cand[ic[q]];
+        dt[q] = __uint_as_float((uint32_t)(kc >> 32));
+        nc[q] = __ldg(m.norms + (uint32_t)(kc & 0xFFFFFFFFull));
+        fm[q] = __ballot_sync(FULL, c < n && ic[q] >= hd);
+        if (c < n && ic[q] >= hd) fpos[nf + __popc(fm[q] & lanemask_lt())] = (uint8_t)c;
+        nf += __popc(fm[q]);
+    }
+    __syncwarp();
+    const int D = m.D;
+    for (int f = 0; f < nf; ++f) {
+        const int pf = fpos[f];
+        const uint64_t kf = cand[rk[pf]];
+        const uint32_t idf = (uint32_t)(kf & 0xFFFFFFFFull);
+        const float dtf = __uint_as_float((uint32_t)(kf >> 32));
+        __syncwarp();
+        m.load_pivot(pv, idf);  // f's row + norm
+        const float* fv = reinterpret_cast<const float*>(pv);
+        const float nf_ = fv[(D + 3) & ~3];
+        uint64_t dlo = 0, dhi = 0, blo = 0, bhi = 0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int c = lane + 32 * q;
+            bool d = false, b = false;
+            if (c < n && c != pf) {
+                const uint32_t idc = (uint32_t)(cand[ic[q]] & 0xFFFFFFFFull);
+                const float dot = a1_dot<false>(m.data + (size_t)idc * D, fv, D);
+                if (c > pf) {  // does f (as the star) prune c?
+                    const float dfc = exact_from_dot(nc[q], dot, nf_);
+                    d = !(__dmul_rn(alpha2, (double)dfc) > (double)dt[q]);
+                } else {       // does c (as the star) prune f?
+                    const float dcf = exact_from_dot(nf_, dot, nc[q]);
+                    b = !(__dmul_rn(alpha2, (double)dcf) > (double)dtf);
+                }
+            }
+            const uint32_t dm = __ballot_sync(FULL, d), bm = __ballot_sync(FULL, b);
+            if (q < 2) { dlo |= (uint64_t)dm << (32 * q); blo |= (uint64_t)bm << (32 * q); }
+            else { dhi |= (uint64_t)dm << (32 * (q - 2)); bhi |= (uint64_t)bm << (32 * (q - 2)); }
+        }
+        if (lane == 0) {
+            fdoms[2 * f] = dlo; fdoms[2 * f + 1] = dhi;
+            fdomby[2 * f] = blo; fdomby[2 * f + 1] = bhi;
+        }
+    }
+    __syncwarp();
+    // scan in rank order: c kept iff no kept candidate before it prunes it
+    const uint64_t flo = (uint64_t)fm[0] | ((uint64_t)fm[1] << 32), fhi = (uint64_t)fm[2] | ((uint64_t)fm[3] << 32);
+    uint64_t klo = 0, khi = 0, kdlo = 0, kdhi = 0;
+    int kept = 0, f = 0;
+    for (int c = 0; c < n && kept < R; ++c) {
+        const bool hi = c >= 64;
+        const uint64_t bit = 1ull << (c & 63);
+        const bool isf = ((hi ? fhi : flo) & bit) != 0;
+        bool dominated;
+        if (isf) dominated = ((fdomby[2 * f] & klo) | (fdomby[2 * f + 1] & khi)) != 0;
+        else dominated = ((hi ? kdhi : kdlo) & bit) != 0;
+        if (!dominated) {
+            if (hi) khi |= bit; else klo |= bit;
+            if (isf) { kdlo |= fdoms[2 * f]; kdhi |= fdoms[2 * f + 1]; }
+            if (lane == 0) {
+                const uint64_t kc = cand[rk[c]];
+                out_ids[kept] = (int32_t)(kc & 0xFFFFFFFFull);
+                out_d[kept] = (uint32_t)(kc >> 32);
+            }
+            ++kept;
+        }
+        if (isf) ++f;
+    }
+    __syncwarp();
+    return kept;
+}
+
 // MODE 0: every target (append, or prune with staged rows); MODE 1 (light, no row
 // staging, high occupancy): append where the fresh sources fit, defer the rest to
 // defer[] (targets needing a prune or the global pool); MODE 2: the deferred list.
@@ -1106,7 +1213,14 @@ __device__ __forceinline__ void owner_one(const M& m, double alpha2, int R, int 
             cand[j] = key_of(m.dist(pv, e), e);
         }
         __syncwarp();
-        k = warp_prune(cand, n, alpha2, R, m, pv, kid, kd);
+        bool done = false;
+        if constexpr (std::is_same<M, F32Metric>::value) {
+            if (n - hd >= 1 && n - hd <= 16 && n <= 128 && m.row_closed(t, alpha2)) {
+                k = prune_closed_global(cand, n, hd, alpha2, R, m, pv, reinterpret_cast<unsigned char*>(gb), kid, kd);
+                done = true;
+            }
+        }
+        if (!done) k = warp_prune(cand, n, alpha2, R, m, pv, kid, kd);
     }
     write_row(m, alpha2, adj, deg, R, t, kid, k);
 }

@@ -88,3 +88,15 @@ def test_other_dataset_resets_closure():
     tok1 = g._closure_key
     jb.insert_stream(g, jb.VectorDataset(x.copy()), range(2000, 4000), p)
     assert g._closure_key != tok1
+
+
+def test_closure_global_row_path_identical():
+    """beamann's default R = 64 at D = 128: candidate sets too large to stage, the
+    owner merge prunes from global rows (prune_closed_global for closed rows)."""
+    x = lowrank(16000, 128, 12, 0.05, 47)
+    p = jb.BuildParams(degree_cap=64, build_beam_width=128, alpha=1.2, max_batch=2000)
+    on = _stream(x, "1", p, 6000, [4000, 6000])
+    off = _stream(x, "0", p, 6000, [4000, 6000])
+    assert on.entry_point == off.entry_point
+    np.testing.assert_array_equal(on.degrees, off.degrees)
+    np.testing.assert_array_equal(on.adjacency, off.adjacency)
