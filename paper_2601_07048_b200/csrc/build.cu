@@ -38,9 +38,9 @@ constexpr int BW = 4;  // warps per block in the per-vertex kernels
 #ifndef JB_P2_BW
 #define JB_P2_BW 1
 #endif
-#ifndef JB_P2_ROWS
-#define JB_P2_ROWS 80  // phase-2 staged trace rows (traces average ~70 candidates at L_build = 64;
-                       // at 3M x 96: 68 rows 16.3 ms, 76 rows 7.0 ms, 84 rows 7.6 ms per 100K batch)
+#ifndef JB_P2_ROWS_OVER_L
+#define JB_P2_ROWS_OVER_L 16  // phase-2 staged trace rows = L_build + this (traces average ~70 candidates at
+                              // L_build = 64; at 3M x 96: 68 rows 16.3 ms, 76 rows 7.0 ms, 84 rows 7.6 ms)
 #endif
 constexpr int P2_BW = JB_P2_BW;  // warps per block of phase 2 (smem-bound by the staged traces)
 constexpr int OWNER_BW = JB_OWNER_BW;  // warps per block of the deferred owner pass (smem-bound)
@@ -48,7 +48,7 @@ constexpr int OWNER_BW = JB_OWNER_BW;  // warps per block of the deferred owner 
 #define JB_STAGE_KB 26     // per-warp smem budget for staged candidate rows
 #endif
 #ifndef JB_P2_KB
-#define JB_P2_KB 64  // phase-2 (new vertex) prune staging budget per warp (cap; JB_P2_ROWS sets the size)
+#define JB_P2_KB 100  // phase-2 (new vertex) prune staging budget per warp (cap; the rows set the size)
 #endif
 #ifndef JB_OWNER_EXTRA
 #define JB_OWNER_EXTRA 16  // owner-merge staging: up to R + this many candidate rows
@@ -2618,7 +2618,7 @@ static int batch_insert_impl(const M& m, const jb_insert_args& a, cudaStream_t s
     // prune from L1/L2 (staging them would cost more occupancy than it saves)
     // stage traces of up to P2_ROWS candidates (1-warp blocks: smem per warp sets the
     // occupancy exactly); longer traces prune from global rows
-    const int crows2 = staged_rows(m, std::min(cap, JB_P2_ROWS), R, JB_P2_KB);
+    const int crows2 = staged_rows(m, std::min(cap, a.build_beam_width + JB_P2_ROWS_OVER_L), R, JB_P2_KB);
     bool p2_done = false;
     if constexpr (std::is_same<M, F32Metric>::value) {
         // rows too large to stage per warp: block per vertex, dot matrix — when the
