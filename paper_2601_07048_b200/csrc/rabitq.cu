@@ -254,18 +254,34 @@ rotate_gemm_kernel(const float* __restrict__ queries, int64_t nq, int D, const f
     for (int a = 0; a < TM; ++a)
 #pragma unroll
         for (int b = 0; b < TM; ++b) acc[a][b] = 0.0;
-    for (int k0 = 0; k0 < D; k0 += RK) {
-        for (int i = tid; i < RT * RK; i += 256) {
+    // each thread's slice elements of the next k-step are loaded into registers while
+    // the current k-step is consumed (RT * RK / 256 = TM * TM elements of each operand)
+    constexpr int PER = RT * RK / 256;
+    double pa[PER], pb[PER];
+    auto fetch = [&](int k0) {
+#pragma unroll
+        for (int h = 0; h < PER; ++h) {
+            const int i = tid + 256 * h;
             const int r = i / RK, e = i % RK, d = k0 + e;
             double va = 0.0, vb = 0.0;
             if (d < D) {
-                if (q0 + r < nq) va = (double)__fsub_rn(queries[(q0 + r) * D + d], centroid[d]);
-                if (o0 + r < D) vb = rot[(size_t)(o0 + r) * D + d];
+                if (q0 + r < nq) va = (double)__fsub_rn(__ldg(queries + (q0 + r) * D + d), __ldg(centroid + d));
+                if (o0 + r < D) vb = __ldg(rot + (size_t)(o0 + r) * D + d);
             }
-            As[e][r] = va;
-            Bs[e][r] = vb;
+            pa[h] = va;
+            pb[h] = vb;
+        }
+    };
+    fetch(0);
+    for (int k0 = 0; k0 < D; k0 += RK) {
+#pragma unroll
+        for (int h = 0; h < PER; ++h) {
+            const int i = tid + 256 * h;
+            As[i % RK][i / RK] = pa[h];
+            Bs[i % RK][i / RK] = pb[h];
         }
         __syncthreads();
+        if (k0 + RK < D) fetch(k0 + RK);
 #pragma unroll
         for (int e = 0; e < RK; ++e) {
             double av[TM], bv[TM];
