@@ -368,6 +368,38 @@ __device__ __forceinline__ uint4 ld16(const uint8_t* p) {
     return *reinterpret_cast<const uint4*>(p);
 }
 
+// The record's last, partial code piece (D not a multiple of 128 / BITS): A1 order
+// over 16-element blocks (vectors 3..0), then the tail forward.
+template <int BITS>
+__device__ __forceinline__ void rq_piece_partial(Acc4& acc, const uint4 w4, const float* __restrict__ qv, int e0,
+                                                 int D) {
+    constexpr uint32_t MASK = (1u << BITS) - 1u;
+    const uint32_t w[4] = {w4.x, w4.y, w4.z, w4.w};
+    int b = e0;
+    for (; b + 16 <= D; b += 16) {
+        for (int i = 3; i >= 0; --i) {
+            for (int j = 0; j < 4; ++j) {
+                const int off = (b - e0 + 4 * i + j) * BITS;
+                acc.madd1(j, (float)((w[off >> 5] >> (off & 31)) & MASK), qv[b + 4 * i + j]);
+            }
+        }
+    }
+    for (; b < D; ++b) {
+        const int off = (b - e0) * BITS;
+        acc.madd1(b & 3, (float)((w[off >> 5] >> (off & 31)) & MASK), qv[b]);
+    }
+}
+
+// 32 B load from global through the read-only path: one 256-bit LDG (sm_100), so a
+// 32 B record (or half of a 64 B one) is one L1 request instead of two 16 B ones
+// that both miss while the first is in flight (C5 ncu: 2x the L2 lookups of the
+// sectors delivered). `p` must be 32 B aligned.
+__device__ __forceinline__ void ldg32(const uint8_t* p, uint4& lo, uint4& hi) {
+    asm volatile("ld.global.nc.v8.u32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                 : "=r"(lo.x), "=r"(lo.y), "=r"(lo.z), "=r"(lo.w), "=r"(hi.x), "=r"(hi.y), "=r"(hi.z), "=r"(hi.w)
+                 : "l"(p));
+}
+
 // <u, q> for one record whose first 16-byte code piece is already in registers
 // (GL: the record is in global memory; else staged in smem).
 template <int BITS, bool GL = true>
@@ -386,23 +418,22 @@ __device__ __forceinline__ float rabitq_dd(const uint8_t* __restrict__ rec, uint
         rq_piece_full<BITS>(acc, cur, qv, e0);
         cur = nxt;
     }
-    if (e0 < D) {  // last partial piece: runtime loop (rare shapes)
-        const uint4 w4 = cur;
-        const uint32_t w[4] = {w4.x, w4.y, w4.z, w4.w};
-        int b = e0;
-        for (; b + 16 <= D; b += 16) {
-            for (int i = 3; i >= 0; --i) {
-                for (int j = 0; j < 4; ++j) {
-                    const int off = (b - e0 + 4 * i + j) * BITS;
-                    acc.madd1(j, (float)((w[off >> 5] >> (off & 31)) & MASK), qv[b + 4 * i + j]);
-                }
-            }
-        }
-        for (; b < D; ++b) {
-            const int off = (b - e0) * BITS;
-            acc.madd1(b & 3, (float)((w[off >> 5] >> (off & 31)) & MASK), qv[b]);
-        }
-    }
+    if (e0 < D) rq_piece_partial<BITS>(acc, cur, qv, e0, D);  // last partial piece (rare shapes)
+    return acc.reduce();
+}
+
+// rabitq_dd for a record held in registers as four 16 B pieces (64 B records: code
+// of at most 48 B, so at most 3 code pieces); same accumulation order.
+template <int BITS>
+__device__ __forceinline__ float rabitq_dd_regs(const uint4 p0, const uint4 p1, const uint4 p2,
+                                                const float* __restrict__ qv, int D) {
+    constexpr int PER16 = 128 / BITS;
+    Acc4 acc; acc.zero();
+    int e0 = 0;
+    if (e0 + PER16 <= D) { rq_piece_full<BITS>(acc, p0, qv, e0); e0 += PER16; }
+    if (e0 + PER16 <= D) { rq_piece_full<BITS>(acc, p1, qv, e0); e0 += PER16; }
+    if (e0 + PER16 <= D) { rq_piece_full<BITS>(acc, p2, qv, e0); e0 += PER16; }
+    if (e0 < D) rq_piece_partial<BITS>(acc, e0 == 0 ? p0 : (e0 == PER16 ? p1 : p2), qv, e0, D);
     return acc.reduce();
 }
 

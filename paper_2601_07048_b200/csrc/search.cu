@@ -53,6 +53,12 @@ constexpr int MAX_CHUNKS = 4;   // neighbour slots per hop: R <= 32 * MAX_CHUNKS
 #ifndef JB_EXACT_CHUNK
 #define JB_EXACT_CHUNK 128      // exact source: row elements staged per pass (multiple of 32)
 #endif
+#ifndef JB_LDG256_R1
+#define JB_LDG256_R1 1  // 32 B records of the float estimator (m = 1) in one 256-bit load
+#endif
+#ifndef JB_LDG256_R64
+#define JB_LDG256_R64 1  // 64 B multi-bit records in two 256-bit loads, estimated from registers
+#endif
 #ifndef JB_COOP_MAX
 #define JB_COOP_MAX 2
 #endif
@@ -396,11 +402,19 @@ __device__ __forceinline__ uint64_t eval_chunk(const jb_search_args& a, const Se
     const int RB = (SRC == JB_SRC_RABITQ_FAST && KD > 0 && BITS == 1) ? ((((KD + 31) / 32 + 3) & ~3) * 4 + 8 + 15) / 16 * 16
                                                                       : a.record_bytes;
     // RaBitQ: issue the candidate's record loads before the visited check
-    uint4 rc0 = make_uint4(0, 0, 0, 0), rc1 = make_uint4(0, 0, 0, 0);
+    // (32 and 64 B records: whole record in 256-bit loads, one L1 request per 32 B;
+    // R64: 64 B records estimated from registers, multi-bit codes only)
+    constexpr bool R64 = BITS >= 2 && JB_LDG256_R64;
+    uint4 rc0 = make_uint4(0, 0, 0, 0), rc1 = make_uint4(0, 0, 0, 0), rc2 = make_uint4(0, 0, 0, 0),
+          rc3 = make_uint4(0, 0, 0, 0);
     if (SRC != JB_SRC_EXACT && !SREC && nb >= 0) {
         const uint8_t* rec = a.records + (size_t)nb * RB;
-        rc0 = __ldg(reinterpret_cast<const uint4*>(rec));
-        if (RB == 32) rc1 = __ldg(reinterpret_cast<const uint4*>(rec + 16));
+        if (RB == 32 && (SRC == JB_SRC_RABITQ_FAST || JB_LDG256_R1)) ldg32(rec, rc0, rc1);
+        else if (RB == 64 && R64) { ldg32(rec, rc0, rc1); ldg32(rec + 32, rc2, rc3); }
+        else {
+            rc0 = __ldg(reinterpret_cast<const uint4*>(rec));
+            if (RB == 32) rc1 = __ldg(reinterpret_cast<const uint4*>(rec + 16));
+        }
     }
     bool isnew = false;
     uint32_t* slot = nullptr;
@@ -485,14 +499,18 @@ __device__ __forceinline__ uint64_t eval_chunk(const jb_search_args& a, const Se
         myid = nb;
         if (isnew) {
             const uint8_t* rec = a.records + (size_t)myid * RB;
-            const float2 m = (RB == 32) ? make_float2(__uint_as_float(rc1.x), __uint_as_float(rc1.y))
-                                        : __ldg(reinterpret_cast<const float2*>(rec + c.meta_off));
+            // metadata: in the loaded registers for 32 / 64 B records (16 B aligned offset)
+            const uint4 mp = (RB == 32) ? rc1 : (c.meta_off == 16 ? rc1 : (c.meta_off == 32 ? rc2 : rc3));
+            const float2 m = (RB == 32 || (RB == 64 && R64)) ? make_float2(__uint_as_float(mp.x), __uint_as_float(mp.y))
+                                                             : __ldg(reinterpret_cast<const float2*>(rec + c.meta_off));
             if (SRC == JB_SRC_RABITQ_FAST) {
                 const float dd = (BITS == 1 && c.nwords == 4)
                                      ? rabitq_dd_fast<FAST_QB, 4, 1>(rec, rc0, c.planes, 4, c.qlo, c.qdelta)
                                      : rabitq_dd_fast<FAST_QB, 0, BITS>(rec, rc0, c.planes, c.nwords, c.qlo, c.qdelta);
                 const float est = (c.qadd + m.x) + m.y * (dd - c.qsumq);
                 d = est > 0.0f ? est : 0.0f;
+            } else if (R64 && RB == 64) {
+                d = rabitq_finish(rabitq_dd_regs<BITS>(rc0, rc1, rc2, c.qv, D), m, c.qadd, c.qsumq);
             } else {
                 d = rabitq_finish(rabitq_dd<BITS>(rec, rc0, c.qv, D), m, c.qadd, c.qsumq);
             }
@@ -916,6 +934,11 @@ static int launch_search_kernel(SearchKernel kern, const SearchLayout& lay, cons
         cache[next] = Entry{kern, smem, dev, per_sm};
         next = (next + 1) % 16;
     }
+    static const int l2_fetch = [] {  // JB_L2_FETCH=<bytes>: L2 fetch granularity experiment
+        const char* e = std::getenv("JB_L2_FETCH");
+        return e ? std::atoi(e) : 0;
+    }();
+    if (l2_fetch > 0) JB_CUDA(cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)l2_fetch));
     int64_t need = (a.nq + nw - 1) / nw;
     int grid = (int)std::min<int64_t>(need, (int64_t)per_sm * sm_count_current());
     Scratch ctr;

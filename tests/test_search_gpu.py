@@ -257,6 +257,23 @@ def test_rabitq_search_oracle_960d_m4():
     np.testing.assert_array_equal(ds, ods)
 
 
+@pytest.mark.parametrize("bits,D", [(4, 96), (4, 88), (2, 192), (2, 180), (8, 48), (1, 384)])
+def test_rabitq_search_oracle_64b_records(bits, D):
+    """64 B records (code <= 48 B + meta): read whole by two 256-bit loads and
+    estimated from registers, incl. a partial last code piece (D = 88, 180)."""
+    assert jb._lib.lib().jb_rabitq_record_bytes(D, bits) == 64
+    x = lowrank(2000, D, 16, 0.05, 60 + D)
+    og = vamana.build(x, R=16, L=32, alpha=1.2)
+    q = lowrank(80, D, 16, 0.05, 61 + D)
+    c, codes, meta = orabitq.fit(x, bits, 5)
+    rot, qadd, sumq = orabitq.bind(q, c, bits, 5)
+    src = orabitq.QuantSource(codes, meta, bits, D, rot, qadd, sumq)
+    ores = osearch.beam_search(og.adj, og.active, og.entry, src, len(q), 40)
+    idx = jb.rabitq_fit(jb.VectorDataset(x), bits=bits, seed=5)
+    g = _graph_from_oracle(og)
+    _oracle_check(jb.run_beam_searches(g, idx, q, 40), ores)
+
+
 def test_medoid_matches_reference_golden():
     f = golden("misc")
     assert jb.medoid(jb.VectorDataset(gaussian(3000, 32, 0))) == int(f["medoid32"])

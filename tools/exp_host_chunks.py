@@ -55,3 +55,13 @@ print(f"device API nq=10000: median {1e3 * np.median(ts):.3f} ms", flush=True)
 os.environ["JB_PIPE_PROFILE"] = "1"
 for _ in range(3):
     jb.search_knn_batch(g, idx, qp, sp, exact_data=ds)
+
+# Python-side cost of one call (cProfile over 20 calls)
+import cProfile, pstats
+os.environ.pop("JB_PIPE_PROFILE", None)
+pr = cProfile.Profile()
+pr.enable()
+for _ in range(20):
+    jb.search_knn_batch(g, idx, qp, sp, exact_data=ds)
+pr.disable()
+pstats.Stats(pr).sort_stats("tottime").print_stats(18)
