@@ -64,22 +64,64 @@ __global__ void row_sq_norms_kernel(const float* __restrict__ x, int64_t n, int 
 }
 
 // ---- f64 column sum, sequential over rows (numpy mean(axis=0), A3) ------
-// One thread per column; rows are visited in order so the f64 sum matches
-// numpy's row-by-row accumulation bit-exactly.
-__global__ void column_sum_f64_kernel(const float* __restrict__ x, int64_t n, int D, double* __restrict__ out) {
-    int c = blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= D) return;
+// numpy reduces axis 0 of a C-contiguous array row by row (acc[:] += row), so
+// each column's f64 sum is one sequential chain over the rows and the result
+// is bit-exact only in that order. The chain cannot be split; what limits it is
+// feeding it. One block per group of 8 columns (one 32 B sector per row): warps
+// 1..8 stream tiles of CS_ROWS rows x 8 columns into smem (double-buffered) while
+// lanes 0..7 of warp 0 run the 8 chains from smem. (A single block of one thread
+// per column, loading its own operands, ran at ~4 GB/s: 84 ms of a 1M x 128
+// build; now the chains' DADD latency is the bound.)
+constexpr int CS_ROWS = 512;
+constexpr int CS_LOADERS = 256;                 // warps 1..8: 16 loads in flight per thread per tile
+constexpr int CS_THREADS = 32 + CS_LOADERS;
+constexpr int CS_PER = CS_ROWS * 8 / CS_LOADERS;
+
+__global__ void __launch_bounds__(CS_THREADS)
+column_sum_f64_kernel(const float* __restrict__ x, int64_t n, int D, double* __restrict__ out) {
+    __shared__ float tile[2][CS_ROWS][8];
+    const int c0 = blockIdx.x * 8;
+    const int nc = min(8, D - c0);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t ntiles = (n + CS_ROWS - 1) / CS_ROWS;
+    auto fill = [&](int64_t t, int buf) {  // all loads issued before any store
+        const int64_t r0 = t * CS_ROWS;
+        const int rows = (int)(n - r0 < CS_ROWS ? n - r0 : CS_ROWS);
+        const int t0 = threadIdx.x - 32;
+        float v[CS_PER];
+#pragma unroll
+        for (int u = 0; u < CS_PER; ++u) {
+            const int idx = t0 + u * CS_LOADERS, r = idx >> 3, j = idx & 7;
+            v[u] = (r < rows && j < nc) ? __ldg(x + (r0 + r) * D + c0 + j) : 0.0f;
+        }
+#pragma unroll
+        for (int u = 0; u < CS_PER; ++u) {
+            const int idx = t0 + u * CS_LOADERS;
+            tile[buf][idx >> 3][idx & 7] = v[u];
+        }
+    };
+    if (warp > 0 && ntiles > 0) fill(0, 0);
+    __syncthreads();
     double s = 0.0;
-    int64_t i = 0;
-    for (; i + 8 <= n; i += 8) {
-        float v[8];
+    for (int64_t t = 0; t < ntiles; ++t) {
+        const int buf = (int)(t & 1);
+        if (warp > 0) {
+            if (t + 1 < ntiles) fill(t + 1, buf ^ 1);
+        } else if (lane < nc) {
+            const int rows = (int)(n - t * CS_ROWS < CS_ROWS ? n - t * CS_ROWS : CS_ROWS);
+            int r = 0;
+            for (; r + 16 <= rows; r += 16) {
+                float v[16];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) v[u] = __ldg(x + (i + u) * D + c);
+                for (int u = 0; u < 16; ++u) v[u] = tile[buf][r + u][lane];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) s = __dadd_rn(s, (double)v[u]);
+                for (int u = 0; u < 16; ++u) s = __dadd_rn(s, (double)v[u]);
+            }
+            for (; r < rows; ++r) s = __dadd_rn(s, (double)tile[buf][r][lane]);
+        }
+        __syncthreads();
     }
-    for (; i < n; ++i) s = __dadd_rn(s, (double)__ldg(x + i * D + c));
-    out[c] = s;
+    if (warp == 0 && lane < nc) out[c0 + lane] = s;
 }
 
 __global__ void mean_finish_kernel(const double* __restrict__ sum, int64_t n, int D, double* __restrict__ mean64,
@@ -214,7 +256,7 @@ int jb_column_mean_f32(const float* x, int64_t n, int32_t dims, float* out, void
     Scratch sum;
     JB_CUDA(sum.alloc(sizeof(double) * dims, st));
     int threads = 128, blocks = (dims + threads - 1) / threads;
-    column_sum_f64_kernel<<<blocks, threads, 0, st>>>(x, n, dims, sum.as<double>());
+    column_sum_f64_kernel<<<(dims + 7) / 8, CS_THREADS, 0, st>>>(x, n, dims, sum.as<double>());
     mean_finish_kernel<<<blocks, threads, 0, st>>>(sum.as<double>(), n, dims, nullptr, out);
     JB_LAUNCH_CHECK();
     return JB_OK;
@@ -236,7 +278,7 @@ int jb_medoid(const float* x, int64_t n, int32_t dims, int64_t* out_host, void* 
     DI* part = reinterpret_cast<DI*>(b + off_part);
     int64_t* dout = reinterpret_cast<int64_t*>(b + off_out);
     int threads = 128, blocks = (dims + threads - 1) / threads;
-    column_sum_f64_kernel<<<blocks, threads, 0, st>>>(x, n, dims, sum);
+    column_sum_f64_kernel<<<(dims + 7) / 8, CS_THREADS, 0, st>>>(x, n, dims, sum);
     mean_finish_kernel<<<blocks, threads, 0, st>>>(sum, n, dims, center, nullptr);
     JB_CUDA_RC(grow_smem(medoid_partial_kernel, (int)(sizeof(double) * dims)));
     medoid_partial_kernel<<<nb, 256, sizeof(double) * dims, st>>>(x, n, dims, center, part);

@@ -77,8 +77,10 @@ class GraphIndex:
             raise ValueError("degree_cap must be >= 1")
         self.capacity = int(capacity)
         self.degree_cap = int(degree_cap)
-        self._adj = np.full((capacity, degree_cap), _NO_NEIGHBOR, dtype=np.int32)
-        self._deg = np.zeros(capacity, dtype=np.int32)
+        # host slab, materialised on first host use: a graph built on the device never
+        # pays for page-faulting (and uploading) an all-empty capacity x R host array
+        self._adj_store = None
+        self._deg_store = None
         self.entry_point = 0
         self.active_count = 0
         self._dev_adj = None
@@ -91,13 +93,37 @@ class GraphIndex:
         self._dev_closure = None   # per-vertex prune closure (jb_insert_args.closure), device f64
         self._closure_key = None   # the f32 dataset the closure flags were computed against
 
+    @property
+    def _adj(self) -> np.ndarray:
+        if self._adj_store is None:
+            self._adj_store = np.full((self.capacity, self.degree_cap), _NO_NEIGHBOR, dtype=np.int32)
+        return self._adj_store
+
+    @_adj.setter
+    def _adj(self, value: np.ndarray) -> None:
+        self._adj_store = value
+
+    @property
+    def _deg(self) -> np.ndarray:
+        if self._deg_store is None:
+            self._deg_store = np.zeros(self.capacity, dtype=np.int32)
+        return self._deg_store
+
+    @_deg.setter
+    def _deg(self, value: np.ndarray) -> None:
+        self._deg_store = value
+
     # ---- host view -------------------------------------------------------
     def _sync_host(self) -> None:
         if self._dev_dirty:
             with self._lock:
                 if self._dev_dirty:
-                    self._adj[:] = self._dev_adj.cpu().numpy()
-                    self._deg[:] = self._dev_deg.cpu().numpy()
+                    if self._adj_store is None:  # first host use: the download is the slab
+                        self._adj_store = self._dev_adj.cpu().numpy()
+                        self._deg_store = self._dev_deg.cpu().numpy()
+                    else:
+                        self._adj[:] = self._dev_adj.cpu().numpy()
+                        self._deg[:] = self._dev_deg.cpu().numpy()
                     self.d2h_bytes += self._adj.nbytes + self._deg.nbytes
                     self._dev_dirty = False
 
@@ -197,7 +223,13 @@ class GraphIndex:
         """(adjacency [capacity, R] int32, degrees [capacity] int32) in HBM, up to date."""
         torch = _lib.require_cuda()
         with self._lock:
-            if self._dev_adj is None:
+            if self._dev_adj is None and self._adj_store is None and self._deg_store is None:
+                # never touched on the host: the empty slab is created in HBM
+                self._dev_adj = torch.full((self.capacity, self.degree_cap), _NO_NEIGHBOR, dtype=torch.int32,
+                                           device="cuda")
+                self._dev_deg = torch.zeros(self.capacity, dtype=torch.int32, device="cuda")
+                self._host_dirty = False
+            elif self._dev_adj is None:
                 self._dev_adj = torch.from_numpy(self._adj).to("cuda")
                 self._dev_deg = torch.from_numpy(self._deg).to("cuda")
                 self.h2d_bytes += self._adj.nbytes + self._deg.nbytes

@@ -85,3 +85,22 @@ def test_960d_m4_rerank_recall_within_3_points_of_exact():
     rq, _ = jb.search_knn_batch(g, idx, q, jb.SearchParams(beam_width=48, k=10, rerank=True), exact_data=ds)
     r_exact, r_quant = jb.recall_at_k(ex, gt, 10), jb.recall_at_k(rq, gt, 10)
     assert r_quant >= r_exact - 0.03, (r_exact, r_quant)
+
+
+@pytest.mark.gpu
+def test_column_mean_bit_exact_on_ragged_shapes():
+    """jb_column_mean_f32 = x.astype(f64).mean(axis=0).astype(f32) (rabitq.py:273) bit for bit:
+    row counts off the 512-row smem tile and column counts off the 8-column group."""
+    import torch
+
+    from paper_2601_07048_b200 import _lib
+
+    rng = np.random.default_rng(11)
+    for n, d in ((1, 3), (5, 8), (511, 33), (70001, 33), (3000, 960), (100003, 128)):
+        x = (rng.standard_normal((n, d)) * rng.uniform(0.1, 100.0, size=d)).astype(np.float32)
+        want = x.astype(np.float64).mean(axis=0).astype(np.float32)
+        xd = torch.from_numpy(x).cuda()
+        out = torch.empty(d, dtype=torch.float32, device="cuda")
+        _lib.check(_lib.lib().jb_column_mean_f32(_lib.ptr(xd), n, d, _lib.ptr(out), _lib.stream_ptr()))
+        got = out.cpu().numpy()
+        assert got.tobytes() == want.tobytes(), (n, d)
