@@ -1081,13 +1081,19 @@ __device__ int prune_closed_global(uint64_t* cand, int n, int hd, double alpha2,
 
 // MODE 0: every target (append, or prune with staged rows); MODE 1 (light, no row
 // staging, high occupancy): append where the fresh sources fit, defer the rest to
-// defer[] (targets needing a prune or the global pool); MODE 2: the deferred list.
+// defer[] (targets needing a prune or the global pool) — except closed f32 rows
+// whose candidates fit `crows` (MODE 1's crows = the closed pass's staging size),
+// which go to defer[dstride + ...]; MODE 2: the deferred list (staged rows, Gram
+// screen); MODE 3: the closed list (almost every prune of a bulk build), the same
+// staged path on a persistent grid of 1-warp blocks (1M x 128 build 0.472 -> 0.454 s,
+// identical graphs).
 template <class M, int MODE>
 __device__ __forceinline__ void owner_one(const M& m, double alpha2, int R, int always_prune, const uint32_t* __restrict__ tgt,
                    const uint64_t* __restrict__ key, int64_t total, const int32_t* __restrict__ seg_start, int64_t s,
                    uint64_t* __restrict__ pool, unsigned long long* __restrict__ pool_top,
                    int pool_cap, int32_t* __restrict__ adj, int32_t* __restrict__ deg, int* __restrict__ err, int crows,
-                   unsigned char* base, int32_t* __restrict__ defer, int* __restrict__ ndefer, uint32_t& sph) {
+                   unsigned char* base, int32_t* __restrict__ defer, int* __restrict__ ndefer, uint32_t& sph,
+                   int64_t dstride) {
     const int lane = threadIdx.x & 31;
     constexpr int SC = OWNER_SC;
     uint64_t* scand = reinterpret_cast<uint64_t*>(base);
@@ -1170,8 +1176,14 @@ __device__ __forceinline__ void owner_one(const M& m, double alpha2, int R, int 
         }
         return;
     }
-    if (MODE == 1) {  // a prune: the deferred pass (staged rows, Gram screen)
-        if (lane == 0) defer[atomicAdd(ndefer, 1)] = (int32_t)s;
+    if (MODE == 1) {  // a prune: the deferred pass (staged rows, Gram screen) or the closed pass
+        bool closed = false;
+        if constexpr (std::is_same<M, F32Metric>::value)
+            closed = dstride > 0 && hd + nf <= crows && m.row_closed(t, alpha2);
+        if (lane == 0) {
+            if (closed) defer[dstride + atomicAdd(ndefer + 1, 1)] = (int32_t)s;
+            else defer[atomicAdd(ndefer, 1)] = (int32_t)s;
+        }
         return;
     }
     // existing neighbours get recomputed distances d(t, e) (target is the pivot);
@@ -1231,7 +1243,7 @@ owner_merge_kernel(const M m, double alpha2, int R, int always_prune, const uint
                    const uint64_t* __restrict__ key, int64_t total, const int32_t* __restrict__ seg_start,
                    const int* __restrict__ n_seg, uint64_t* __restrict__ pool, unsigned long long* __restrict__ pool_top,
                    int pool_cap, int32_t* __restrict__ adj, int32_t* __restrict__ deg, int* __restrict__ err, int crows,
-                   int32_t* __restrict__ defer, int* __restrict__ ndefer) {
+                   int32_t* __restrict__ defer, int* __restrict__ ndefer, int64_t dstride) {
     extern __shared__ __align__(16) unsigned char shb[];
     const int warp = threadIdx.x >> 5;
     const int per_warp = MODE == 1 ? owner_light_per_warp(R) : owner_per_warp(m, R, crows);
@@ -1243,17 +1255,18 @@ owner_merge_kernel(const M m, double alpha2, int R, int always_prune, const uint
                        (size_t)crows * m.stage_stride_words();
         init_stage_bar(cn, crows);
     }
-    if (MODE == 2) {  // persistent over the deferred targets
-        const int nd = *ndefer;
-        const int wpb = (int)(blockDim.x >> 5);  // the deferred pass runs OWNER_BW-warp blocks
+    if (MODE >= 2) {  // persistent over the deferred (2) or closed (3) targets
+        const int nd = ndefer[MODE - 2];
+        const int32_t* list = defer + (MODE == 3 ? dstride : 0);
+        const int wpb = (int)(blockDim.x >> 5);
         for (int64_t i = (int64_t)blockIdx.x * wpb + warp; i < nd; i += (int64_t)gridDim.x * wpb)
-            owner_one<M, MODE>(m, alpha2, R, always_prune, tgt, key, total, seg_start, defer[i], pool, pool_top,
-                               pool_cap, adj, deg, err, crows, base, defer, ndefer, sph);
+            owner_one<M, MODE>(m, alpha2, R, always_prune, tgt, key, total, seg_start, list[i], pool, pool_top,
+                               pool_cap, adj, deg, err, crows, base, defer, ndefer, sph, dstride);
     } else {
         const int64_t s = (int64_t)blockIdx.x * BW + warp;
         if (s >= *n_seg) return;
         owner_one<M, MODE>(m, alpha2, R, always_prune, tgt, key, total, seg_start, s, pool, pool_top, pool_cap, adj,
-                           deg, err, crows, base, defer, ndefer, sph);
+                           deg, err, crows, base, defer, ndefer, sph, dstride);
     }
 }
 
@@ -2371,6 +2384,20 @@ __global__ void owner_pool_need_kernel(const uint32_t* __restrict__ tgt, int64_t
     need[s] = c > OWNER_SC ? (unsigned long long)c : 0ull;
 }
 
+// JB_CLOSED_PASS=0: closed rows stay on the staged deferred pass (A/B)
+static bool closed_pass_on() {
+    const char* e = getenv("JB_CLOSED_PASS");  // read per batch (A/B within one process)
+    return !(e && e[0] == '0');
+}
+
+// staging rows beyond R of the closed pass (JB_CLOSED_EXTRA; default the deferred
+// pass's R + JB_OWNER_EXTRA: fewer rows measured no faster, 1M x 128 build 0.454 s at
+// +16 vs 0.457-0.460 s at +6..+12, `tools/exp_build_ab.py`)
+static int closed_extra() {
+    const char* e = getenv("JB_CLOSED_EXTRA");
+    return e ? std::max(1, atoi(e)) : JB_OWNER_EXTRA;
+}
+
 // Phase 3 (build.py:269-293): (target, dist, source) order via two stable radix
 // sorts of the reverse triples, segment heads, one owner warp per target.
 template <class M>
@@ -2459,19 +2486,37 @@ static int merge_phase(const M& m, const jb_insert_args& a, double alpha2, uint3
             JB_CUDA_RC(grow_smem(owner_merge_kernel<M, 0>, osm));
             owner_merge_kernel<M, 0><<<(unsigned)((hseg + BW - 1) / BW), BW * 32, osm, st>>>(
                 mo, alpha2, R, a.always_prune, tt, tk, ntri, seg, nseg, pool, ptop, pool_cap, a.adjacency, a.degrees, err,
-                crows, nullptr, nullptr);
+                crows, nullptr, nullptr, 0);
         } else {
             // light pass (appends, no staged rows: high occupancy), then the targets
             // that need a prune on a persistent grid of the staging kernel
-            BALLOC(defer, int32_t, hseg);
-            BALLOC(ndefer, int, 1);
-            JB_CUDA(cudaMemsetAsync(ndefer, 0, sizeof(int), st));
+            // closed f32 rows (prune closure on) get their own list and pass (MODE 3)
+            bool closed_pass = false;
+            if constexpr (std::is_same<M, F32Metric>::value) closed_pass = m.closure != nullptr && closed_pass_on();
+            const int64_t dstride = closed_pass ? hseg : 0;
+            BALLOC(defer, int32_t, closed_pass ? 2 * (int64_t)hseg : hseg);
+            BALLOC(ndefer, int, 2);
+            JB_CUDA(cudaMemsetAsync(ndefer, 0, 2 * sizeof(int), st));
             const int lsm = owner_light_per_warp(R) * BW;
             JB_CUDA_RC(grow_smem(owner_merge_kernel<M, 1>, lsm));
+            const int crows3 = closed_pass ? staged_rows(m, R + closed_extra(), R) : 0;
             owner_merge_kernel<M, 1><<<(unsigned)((hseg + BW - 1) / BW), BW * 32, lsm, st>>>(
                 mo, alpha2, R, a.always_prune, tt, tk, ntri, seg, nseg, pool, ptop, pool_cap, a.adjacency, a.degrees, err,
-                crows, defer, ndefer);
+                crows3, defer, ndefer, crows3 > 0 ? dstride : 0);
             JB_LAUNCH_CHECK();
+            if (closed_pass && crows3 > 0) {
+                // 1-warp blocks: the ~20 KB per-warp staging packs the SM best in single warps
+                const int osm3 = owner_per_warp(m, R, crows3);
+                JB_CUDA_RC(grow_smem(owner_merge_kernel<M, 3>, osm3));
+                int per_sm3 = 0;
+                JB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm3, owner_merge_kernel<M, 3>, 32, osm3));
+                const unsigned g3 = (unsigned)std::max<int64_t>(
+                    1, std::min<int64_t>(hseg, (int64_t)std::max(1, per_sm3) * sm_count_current()));
+                owner_merge_kernel<M, 3><<<g3, 32, osm3, st>>>(mo, alpha2, R, a.always_prune, tt, tk, ntri, seg,
+                                                              nseg, pool, ptop, pool_cap, a.adjacency, a.degrees,
+                                                              err, crows3, defer, ndefer, dstride);
+                JB_LAUNCH_CHECK();
+            }
             const int osm2 = owner_per_warp(m, R, crows) * OWNER_BW;
             JB_CUDA_RC(grow_smem(owner_merge_kernel<M, 2>, osm2));
             int per_sm = 0;
@@ -2481,7 +2526,7 @@ static int merge_phase(const M& m, const jb_insert_args& a, double alpha2, uint3
                                                                                        sm_count_current()));
             owner_merge_kernel<M, 2><<<g2, OWNER_BW * 32, osm2, st>>>(mo, alpha2, R, a.always_prune, tt, tk, ntri, seg, nseg,
                                                                pool, ptop, pool_cap, a.adjacency, a.degrees, err, crows,
-                                                               defer, ndefer);
+                                                               defer, ndefer, dstride);
         }
         JB_LAUNCH_CHECK();
         int herr = 0;
