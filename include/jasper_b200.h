@@ -52,6 +52,15 @@ int jb_sm_count(int device, int32_t* out);
  * (build.py:120). */
 int jb_row_sq_norms(const float* x, int64_t n, int32_t dims, float* out, void* stream);
 
+/* Extension (no reference counterpart): int8 screen records for the exact search
+ * (jb_search_args.screen). Record of row i (jb_screen_record_bytes(dims) bytes):
+ * int8 codes b of x_i - center (per-row scale s = max|x_i - center| / 127, codes
+ * zero-padded to a 16 B multiple), then f32 {s, |b|^2, eps, norms[i]} with
+ * eps >= |s b - (x_i - center)|_2 (f64, rounded up). */
+int32_t jb_screen_record_bytes(int32_t dims);
+int jb_screen_records(const float* x, const float* norms, int64_t n, int32_t dims, const float* center,
+                      uint8_t* out, void* stream);
+
 /* Medoid: argmin_i ||x_i - mean||^2 in f64 (mean = sequential f64 row sum / n,
  * distance = 2-lane einsum order), lowest id on ties. Writes the index to
  * *out_host (synchronizes). Replaces graph.medoid (graph.py:159-171). */
@@ -120,6 +129,15 @@ typedef struct jb_search_args {
     const uint32_t* norms_u32;     /* [N] integer row norms                     */
     const uint8_t* queries_u8;     /* [nq, D] u8 queries                        */
     const uint32_t* query_norms_u32; /* [nq] integer query norms                */
+    /* Extension (EXACT source, not in the reference; NULL = off): int8 screen
+     * records of the rows (jb_screen_records) and their centre. While the beam is
+     * full, a new neighbour whose rigorous lower bound on the exact distance
+     * (triangle inequality on int8-quantised centred rows, both quantisation
+     * errors and the f32 rounding of the exact formula accounted for) exceeds the
+     * beam's worst key is dropped without reading its f32 row: the merge would
+     * drop its exact key too, so frontier, trace and evals are unchanged. */
+    const uint8_t* screen;
+    const float* screen_center;    /* [D] f32 centre the records were built with */
 } jb_search_args;
 
 /* Batched greedy beam search, one warp per query (persistent grid).
@@ -271,6 +289,10 @@ typedef struct jb_insert_args {
      * (same result). Must be zeroed whenever the adjacency is written outside
      * these calls (the Python GraphIndex does so on every host upload). */
     double* closure;
+    /* Extension: int8 screen records of data (jb_screen_records) + centre for the
+     * phase-1 exact search (jb_search_args.screen); NULL = off. */
+    const uint8_t* screen;
+    const float* screen_center;
 } jb_insert_args;
 
 /* One three-phase batch: search -> prune + reverse triples -> grouped merge,

@@ -35,6 +35,7 @@ class SearchArgs(C.Structure):
         ("frontier_keys", p), ("hops", p), ("evals", p), ("trace_ids", p), ("trace_dists", p),
         ("flags", p),
         ("data_u8", p), ("norms_u32", p), ("queries_u8", p), ("query_norms_u32", p),
+        ("screen", p), ("screen_center", p),
     ]
 
 
@@ -55,7 +56,7 @@ class InsertArgs(C.Structure):
         ("quantized", i32), ("records", p), ("record_bytes", i32), ("bits", i32),
         ("bound_rotated", p), ("bound_qadd", p), ("bound_qsumq", p),
         ("repair_beam_width", i32),
-        ("closure", p),
+        ("closure", p), ("screen", p), ("screen_center", p),
     ]
 
 
@@ -81,6 +82,8 @@ _SIGS = {
     "jb_rabitq_pack_records": (C.c_int, [p, p, i64, i32, i32, p, p]),
     "jb_rabitq_encode": (C.c_int, [p, i64, i32, i32, p, p, p, p, p]),
     "jb_column_mean_f32": (C.c_int, [p, i64, i32, p, p]),
+    "jb_screen_record_bytes": (i32, [i32]),
+    "jb_screen_records": (C.c_int, [p, p, i64, i32, p, p, p]),
     "jb_rabitq_bind": (C.c_int, [p, i64, i32, i32, p, p, p, p, p, p]),
     "jb_batch_insert": (C.c_int, [C.POINTER(InsertArgs), p]),
     "jb_repair_connectivity": (C.c_int, [C.POINTER(InsertArgs), p]),

@@ -180,6 +180,10 @@ def _args(graph: GraphIndex, ds, params: BuildParams, start: int, stop: int, qua
     # maintaining it, so it is invalidated
     if quantizer is None and ds.element_kind is not ElementKind.U8:
         a.closure = _lib.ptr(graph.device_closure(_rows_token(dev)))
+        # int8 screen records for the phase-1 exact search (extension; JB_SCREEN=0: off)
+        scr = ds.device_screen() if os.environ.get("JB_SCREEN", "1") != "0" else None
+        if scr is not None:
+            a.screen, a.screen_center = _lib.ptr(scr[0]), _lib.ptr(scr[1])
     else:
         graph.invalidate_closure()
     if quantizer is not None:

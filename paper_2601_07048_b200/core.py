@@ -168,6 +168,28 @@ class VectorDataset:
         self._dev_f32 = out  # kept: the rerank reads it asynchronously
         return out
 
+    def device_screen(self):
+        """(records [n, jb_screen_record_bytes(D)] u8, centre [D] f32) on the device:
+        int8 screen records of the f32 rows (extension, jb_search_args.screen),
+        built once per dataset; None for u8 rows or D > 1040."""
+        dev = self.device()
+        if self._kind is ElementKind.U8 or dev.dims > 1040 or dev.count == 0:
+            return None
+        cached = getattr(self, "_dev_screen", None)
+        if cached is not None:
+            return cached
+        torch = _lib.require_cuda()
+        L = _lib.lib()
+        st = _lib.stream_ptr()
+        center = torch.empty(dev.dims, dtype=torch.float32, device=dev.x.device)
+        _lib.check(L.jb_column_mean_f32(_lib.ptr(dev.x), dev.count, dev.dims, _lib.ptr(center), st))
+        rb = int(L.jb_screen_record_bytes(dev.dims))
+        rec = torch.empty((dev.count, rb), dtype=torch.uint8, device=dev.x.device)
+        _lib.check(L.jb_screen_records(_lib.ptr(dev.x), _lib.ptr(dev.norms), dev.count, dev.dims, _lib.ptr(center),
+                                       _lib.ptr(rec), st))
+        self._dev_screen = (rec, center)
+        return self._dev_screen
+
 
 @dataclass(frozen=True)
 class AugmentedDataset:

@@ -2346,6 +2346,7 @@ static int trace_search(const jb_insert_args& a, int64_t q0, int64_t nq, int64_t
             s.source = JB_SRC_EXACT;
             s.data = a.data; s.data_norms = a.data_norms;
             s.queries = a.data + (size_t)q0 * D; s.query_add = a.data_norms + q0;
+            s.screen = a.screen; s.screen_center = a.screen_center;
         }
         s.nq = nq; s.starts = nullptr; s.start_vertex = entry;
         s.beam_width = L; s.hash_slots = 0; s.trace_cap = cap;

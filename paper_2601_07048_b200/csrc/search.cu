@@ -70,6 +70,8 @@ struct SearchLayout {
     int chunk;      // staged elements per row chunk (multiple of 32, <= 128)
     int sstride;    // staged row stride in floats (chunk + 4)
     int hbits;      // log2(number of 4-way buckets)
+    int scr_off;    // EXACT: int8 code of the centred query (screen), 16 B aligned
+    int srows;      // EXACT: rows staged per pass (32; 16 with the screen: fewer survivors, more warps)
 };
 
 static int pow2_ceil(int v) { int p = 1; while (p < v) p <<= 1; return p; }
@@ -79,10 +81,12 @@ __host__ __device__ constexpr int log2i(int v) { int l = 0; while ((1 << l) < v)
 // last, so for a compile-time D and visited-table size every offset is a
 // constant (the specialised kernels then address smem as base + immediate).
 __host__ __device__ constexpr SearchLayout make_layout(int src, int D, int L, int hash_slots, int qb,
-                                                      bool direct = false, int rec_bytes = 0) {
+                                                      bool direct = false, int rec_bytes = 0, int srows = 32) {
     SearchLayout s{};
     int off = 0;
     s.q_off = off; off += ((D * 4) + 15) & ~15;
+    s.scr_off = off;
+    if (src == JB_SRC_EXACT) off += (D + 15) & ~15;
     s.hbits = log2i(hash_slots / 4 > 1 ? hash_slots / 4 : 1);   // 4-way buckets
     s.hash_off = off; off += (4 << s.hbits) * 4;
     s.newk_off = off; off += 32 * 4;
@@ -91,7 +95,8 @@ __host__ __device__ constexpr SearchLayout make_layout(int src, int D, int L, in
     s.chunk = ((D + 31) / 32) * 32 < JB_EXACT_CHUNK ? ((D + 31) / 32) * 32 : JB_EXACT_CHUNK;
     s.sstride = s.chunk + 4;
     s.stage_off = off;
-    if (src == JB_SRC_EXACT && !direct) off += 32 * s.sstride * 4;
+    s.srows = srows;
+    if (src == JB_SRC_EXACT && !direct) off += srows * s.sstride * 4;
     s.plane_off = off;
     if (src == JB_SRC_RABITQ_FAST) off += qb * ((((D + 31) / 32) + 3) & ~3) * 4;
     off = (off + 15) & ~15;
@@ -380,7 +385,75 @@ struct QueryCtx {
     uint32_t qn;              // EXACT_U8: integer query norm (query bytes at qv)
     uint64_t* bar;            // EXACT / SREC: bulk-staging mbarrier
     unsigned char* recs;      // SREC: staged records (rec_stride apart, slot = lane)
+    const uint32_t* sa;       // screen: int8 code words of the centred query (nullptr: off)
+    float sq, sa2, seps, smq; // screen: query scale, sq^2 |a|^2, eps_q, (D + 32) 2^-24
 };
+
+// Screen (jb_search_args.screen, screen.cu): true when the new neighbour `nb` is
+// provably worse than the full beam's worst key. s0 >= sqrt(worst distance).
+// |q~ - x~|^2 from exact integer <a, b> (dp4a) with f32 roundings absorbed by a
+// 2^-19 (A + B) slack (~10 ulps needed); g <= |q~ - x~|, h >= eps + eps_q + s0 +
+// sqrt(M) with M = (D + 32) 2^-24 (|x|^2 + |q|^2) >= |d_f32 - |q - x|^2| (the A1
+// dot and norms: chains of D/4 products, two combining adds, three final ops).
+// g > h => |q - x|^2 > worst + M => the exact f32 key is above the worst key.
+__device__ __forceinline__ bool screen_drop(const jb_search_args& a, const QueryCtx& c, int D, uint32_t nb, float s0) {
+    const int dp = (D + 15) & ~15;
+    const uint8_t* rec = a.screen + (size_t)nb * (dp + 16);
+    const uint4* r = reinterpret_cast<const uint4*>(rec);
+    const float4 m = __ldg(reinterpret_cast<const float4*>(rec + dp));  // s, |b|^2, eps, |x|^2
+    int dot = 0;
+    for (int w = 0; w < (dp >> 4); ++w) {
+        const uint4 b = __ldg(r + w);
+        const uint4 q = *reinterpret_cast<const uint4*>(c.sa + 4 * w);
+        dot = __dp4a((int)b.x, (int)q.x, dot);
+        dot = __dp4a((int)b.y, (int)q.y, dot);
+        dot = __dp4a((int)b.z, (int)q.z, dot);
+        dot = __dp4a((int)b.w, (int)q.w, dot);
+    }
+    const float A = c.sa2, B = m.x * m.x * m.y;
+    const float dd = fmaf(-2.0f * c.sq * m.x, (float)dot, A + B) - 0x1p-19f * (A + B);
+    if (!(dd > 0.0f)) return false;
+    const float g = sqrtf(dd) * (1.0f - 0x1p-20f);
+    const float h = (m.z + c.seps + s0 + sqrtf(c.smq * (m.w + c.qadd)) * (1.0f + 0x1p-20f)) * (1.0f + 0x1p-20f);
+    return g > h;
+}
+
+// Screen setup for one query (warp): a = rint((q - c) / sq) in [-127, 127] (int8,
+// zero padded to 16 B), sq = max|q - c| / 127, eps_q >= |sq a - (q - c)|_2 (f64, up).
+__device__ __forceinline__ void screen_query(const float* qv, const float* __restrict__ center, int D, uint32_t* sa,
+                                             float& sq, float& sa2, float& seps) {
+    const int lane = lane_id();
+    const int dp = (D + 15) & ~15;
+    double mx = 0.0;
+    for (int e = lane; e < D; e += 32) mx = fmax(mx, fabs((double)qv[e] - (double)center[e]));
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, o));
+    const float s = mx > 0.0 ? (float)(mx / 127.0) : 1.0f;
+    double err = 0.0, nrm = 0.0;
+    int aa = 0;
+    int8_t* a8 = reinterpret_cast<int8_t*>(sa);
+    for (int e = lane; e < dp; e += 32) {
+        int b = 0;
+        if (e < D) {
+            const double qc = (double)qv[e] - (double)center[e];
+            b = (int)rint(qc / (double)s);
+            b = b > 127 ? 127 : (b < -127 ? -127 : b);
+            const double t = (double)s * (double)b - qc;
+            err += t * t;
+            nrm += fabs((double)qv[e]) + fabs((double)center[e]);
+        }
+        aa += b * b;
+        a8[e] = (int8_t)b;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        err += __shfl_xor_sync(0xFFFFFFFFu, err, o);
+        nrm += __shfl_xor_sync(0xFFFFFFFFu, nrm, o);
+        aa += __shfl_xor_sync(0xFFFFFFFFu, aa, o);
+    }
+    sq = s;
+    sa2 = s * s * (float)aa;
+    seps = __double2float_ru(sqrt(err) * (1.0 + 0x1p-30) + 0x1p-30 * nrm);
+    __syncwarp();
+}
 
 // One neighbour per lane (nb = -1: none): visited check, then the distance of
 // every new neighbour, returned as the lane's candidate key (UMAX = none; EXACT
@@ -393,7 +466,8 @@ struct QueryCtx {
 #endif
 template <int SRC, int BITS, bool ALIGNED, int KD = 0, bool DIRECT = false, bool SREC = false>
 __device__ __forceinline__ uint64_t eval_chunk(const jb_search_args& a, const SearchLayout& lay, const QueryCtx& c,
-                                               uint32_t* tab, int nb, int& evals, int& lossy, uint32_t& bphase) {
+                                               uint32_t* tab, int nb, int& evals, int& lossy, uint32_t& bphase,
+                                               float s0 = __builtin_huge_valf()) {
     const unsigned FULL = 0xFFFFFFFFu;
     const int lane = lane_id();
     const int D = KD > 0 ? KD : a.dims;
@@ -424,7 +498,7 @@ __device__ __forceinline__ uint64_t eval_chunk(const jb_search_args& a, const Se
     // forgotten (safe, but it may be re-evaluated later -> flag it)
     if (slot != nullptr && *reinterpret_cast<volatile uint32_t*>(slot) != (uint32_t)nb) lossy = 1;
     const uint32_t nm = __ballot_sync(FULL, isnew);
-    const int nnew = __popc(nm);
+    int nnew = __popc(nm);
     if (nnew == 0) return UMAX;
     evals += nnew;
 
@@ -444,36 +518,96 @@ __device__ __forceinline__ uint64_t eval_chunk(const jb_search_args& a, const Se
             d = exact_from_dot(__ldg(a.data_norms + nb), acc.reduce(), c.qadd);
         }
     } else if (SRC == JB_SRC_EXACT) {
-        if (isnew) c.cid[__popc(nm & lanemask_lt())] = nb;
+        // screen (beam full): only neighbours not provably worse than its worst key
+        // get the exact A1 distance; the others return no key, as the merge would
+        const bool ex = isnew && !(c.sa != nullptr && s0 < __builtin_huge_valf() &&
+                                   screen_drop(a, c, D, (uint32_t)nb, s0));
+        const uint32_t em = __ballot_sync(FULL, ex);
+        nnew = __popc(em);
+        if (nnew == 0) return UMAX;
+        if (ex) c.cid[__popc(em & lanemask_lt())] = nb;
         __syncwarp();
         myid = (lane < nnew) ? c.cid[lane] : 0;
+        // few rows (<= 16, e.g. the screen's survivors): 4 lanes per row, lane j of a
+        // group runs A1 chain j (elements j mod 4 of each 16-block, vectors 3..0, then
+        // the tail forward) — the same sums as one lane running all four, in a
+        // quarter (one pass) or half (two passes) of the dependent steps. Rows are
+        // staged lay.srows at a time (16 with the screen: a smaller stage, more warps).
+        const int srows = lay.srows;
+        const bool split = nnew <= 16 || srows < 32;
+        const int grp = lane >> 2, cj = lane & 3;
+        uint64_t skey = UMAX;
         Acc4 acc; acc.zero();
-        for (int e0 = 0; e0 < D; e0 += lay.chunk) {
-            const int clen = min(lay.chunk, D - e0);
-            if (ALIGNED && JB_BULK) {  // lane j copies row j's chunk (clen * 4 B, a 16 B multiple)
-                const uint32_t bytes = (uint32_t)clen * 4;
-                wbar_expect(c.bar, bytes * (uint32_t)nnew);
-                if (lane < nnew) bulk_row(c.stage + lane * lay.sstride, a.data + (size_t)myid * D + e0, bytes, c.bar);
-                wbar_wait(c.bar, bphase);
-            } else if (ALIGNED) {
-                const int nv = clen >> 2;
-                for (int j = 0; j < nnew; ++j) {
-                    const float* src = a.data + (size_t)c.cid[j] * D + e0;
-                    float* dst = c.stage + j * lay.sstride;
-                    for (int f = lane; f < nv; f += 32) cp_async16(dst + 4 * f, src + 4 * f);
+        for (int b0 = 0; b0 < nnew; b0 += srows) {
+            const int nr = min(srows, nnew - b0);
+            float sacc0 = 0.0f, sacc1 = 0.0f;
+            const int rid = lane < nr ? c.cid[b0 + lane] : 0;
+            for (int e0 = 0; e0 < D; e0 += lay.chunk) {
+                const int clen = min(lay.chunk, D - e0);
+                if (ALIGNED && JB_BULK) {  // lane j copies row b0 + j's chunk (clen * 4 B, a 16 B multiple)
+                    const uint32_t bytes = (uint32_t)clen * 4;
+                    wbar_expect(c.bar, bytes * (uint32_t)nr);
+                    if (lane < nr) bulk_row(c.stage + lane * lay.sstride, a.data + (size_t)rid * D + e0, bytes, c.bar);
+                    wbar_wait(c.bar, bphase);
+                } else if (ALIGNED) {
+                    const int nv = clen >> 2;
+                    for (int j = 0; j < nr; ++j) {
+                        const float* src = a.data + (size_t)c.cid[b0 + j] * D + e0;
+                        float* dst = c.stage + j * lay.sstride;
+                        for (int f = lane; f < nv; f += 32) cp_async16(dst + 4 * f, src + 4 * f);
+                    }
+                } else {
+                    for (int j = 0; j < nr; ++j) {
+                        const float* src = a.data + (size_t)c.cid[b0 + j] * D + e0;
+                        float* dst = c.stage + j * lay.sstride;
+                        for (int f = lane; f < clen; f += 32) cp_async4(dst + f, src + f);
+                    }
                 }
-            } else {
-                for (int j = 0; j < nnew; ++j) {
-                    const float* src = a.data + (size_t)c.cid[j] * D + e0;
-                    float* dst = c.stage + j * lay.sstride;
-                    for (int f = lane; f < clen; f += 32) cp_async4(dst + f, src + f);
+                if (!(ALIGNED && JB_BULK)) cp_async_wait_all();
+                __syncwarp();
+                if (split) {
+#pragma unroll
+                    for (int pp = 0; pp < 2; ++pp) {
+                        const int r = pp * 8 + grp;
+                        if (r < nr) {
+                            const float* row = c.stage + r * lay.sstride;
+                            const float* qq = c.qv + e0;
+                            float l = pp == 0 ? sacc0 : sacc1;
+                            int t = 0;
+                            for (; t + 16 <= clen; t += 16) {
+#pragma unroll
+                                for (int i = 3; i >= 0; --i)
+                                    l = __fadd_rn(__fmul_rn(row[t + 4 * i + cj], qq[t + 4 * i + cj]), l);
+                            }
+                            for (int u = t + cj; u < clen; u += 4) l = __fadd_rn(__fmul_rn(row[u], qq[u]), l);
+                            if (pp == 0) sacc0 = l; else sacc1 = l;
+                        }
+                    }
+                } else if (lane < nr) {
+                    a1_range<ALIGNED, false>(acc, c.stage + lane * lay.sstride - e0, c.qv, e0, e0 + clen);
+                }
+                __syncwarp();
+            }
+            if (split) {
+                // (l0 + l1) + (l2 + l3) over the group; row b0 + 8 pp + grp's key ends in
+                // lane 4 grp + b0 / 8 + pp (at most one key per lane for nnew <= 32)
+#pragma unroll
+                for (int pp = 0; pp < 2; ++pp) {
+                    const float l = pp == 0 ? sacc0 : sacc1;
+                    float t = __fadd_rn(l, __shfl_xor_sync(FULL, l, 1));
+                    t = __fadd_rn(t, __shfl_xor_sync(FULL, t, 2));
+                    const int r = pp * 8 + grp;
+                    uint64_t kp = UMAX;
+                    if (cj == 0 && r < nr) {
+                        const int id = c.cid[b0 + r];
+                        kp = pack_key(exact_from_dot(__ldg(a.data_norms + id), t, c.qadd), (uint32_t)id);
+                    }
+                    const uint64_t mv = shfl_u64(kp, lane & ~3);
+                    if (cj == (b0 >> 3) + pp) skey = mv;
                 }
             }
-            if (!(ALIGNED && JB_BULK)) cp_async_wait_all();
-            __syncwarp();
-            if (lane < nnew) a1_range<ALIGNED, false>(acc, c.stage + lane * lay.sstride - e0, c.qv, e0, e0 + clen);
-            __syncwarp();
         }
+        if (split) return skey;
         if (lane < nnew) d = exact_from_dot(__ldg(a.data_norms + myid), acc.reduce(), c.qadd);
     } else if (SREC) {
         // long records (high D): each new lane's record is staged into its smem slot
@@ -590,7 +724,14 @@ beam_search_kernel(const jb_search_args a, const SearchLayout lay_arg, int* __re
         __syncwarp();
         float qlo = 0.0f, qdelta = 0.0f;
         if (SRC == JB_SRC_RABITQ_FAST) build_planes<FAST_QB>(qv, D, planes, qlo, qdelta);
-        const QueryCtx qc{qv, planes, cid, stage, qadd, qsumq, qlo, qdelta, nwords, meta_off, qn, wbar, srecs};
+        uint32_t* sa = nullptr;
+        float ssq = 0.0f, ssa2 = 0.0f, sseps = 0.0f;
+        if (SRC == JB_SRC_EXACT && a.screen != nullptr) {
+            sa = reinterpret_cast<uint32_t*>(base + lay.scr_off);
+            screen_query(qv, a.screen_center, D, sa, ssq, ssa2, sseps);
+        }
+        const QueryCtx qc{qv, planes, cid, stage, qadd, qsumq, qlo, qdelta, nwords, meta_off, qn, wbar, srecs,
+                          sa, ssq, ssa2, sseps, (float)(D + 32) * 0x1p-24f};
 
         int lossy = 0;
         if (lane == 0) {
@@ -656,8 +797,11 @@ beam_search_kernel(const jb_search_args a, const SearchLayout lay_arg, int* __re
 #pragma unroll
             for (int c = 0; c < CH; ++c) {
                 if (c * 32 >= R) break;
-                const uint64_t key =
-                    eval_chunk<SRC, BITS, ALIGNED, KD, DIRECT, SREC>(a, lay, qc, tab, nbv[c], evals, lossy, bphase);
+                float s0 = __builtin_huge_valf();  // sqrt(worst distance), rounded up; inf: no screen
+                if (SRC == JB_SRC_EXACT && sa != nullptr && bcount == L)
+                    s0 = sqrtf(__uint_as_float((uint32_t)(beam[L - 1] >> 32))) * (1.0f + 0x1p-20f);
+                const uint64_t key = eval_chunk<SRC, BITS, ALIGNED, KD, DIRECT, SREC>(a, lay, qc, tab, nbv[c], evals,
+                                                                                     lossy, bphase, s0);
                 const int p0 = merge_into_beam(beam, bcount, L, key, fmask);
                 s_min = min(s_min, p0);
                 p_ins = p0;
@@ -949,6 +1093,13 @@ static int launch_search_kernel(SearchKernel kern, const SearchLayout& lay, cons
     return JB_OK;
 }
 
+// rows staged per pass with the screen (JB_SCREEN_SROWS, 8..32; default 16)
+static int screen_srows() {
+    const char* e = std::getenv("JB_SCREEN_SROWS");
+    const int v = e ? std::atoi(e) : 16;
+    return v >= 32 ? 32 : (v <= 8 ? 8 : 16);
+}
+
 // R <= 32: one neighbour chunk per hop (single merge, no rescan of the beam);
 // MAX_CHUNKS for wider rows. Blocks/SM: the popcount kernel is issue-bound and
 // gains from 10 resident blocks; the float estimators keep 8.
@@ -960,7 +1111,8 @@ static int launch_search(const jb_search_args& a, int hash_slots, cudaStream_t s
                                                    : JB_OTHER_MINB;
     constexpr int NW = warps_per_block<SRC>();
     const int L = a.beam_width;
-    const SearchLayout lay = make_layout(SRC, a.dims, L, hash_slots, FAST_QB);
+    const SearchLayout lay = make_layout(SRC, a.dims, L, hash_slots, FAST_QB, false, 0,
+                                         (SRC == JB_SRC_EXACT && a.screen != nullptr) ? screen_srows() : 32);
     if (a.degree_cap <= 32 && SRC == JB_SRC_RABITQ_FAST && BITS == 1) {
         // specialised shapes: D in {96, 128} with a 512- or 1024-slot visited table (popcount
         // estimator only: measured -2% at L=128; the float estimators got slower, +4%)
@@ -1030,6 +1182,8 @@ int jb_beam_search(const jb_search_args* args, void* stream) {
     }
     if (a.source == JB_SRC_EXACT) {
         JB_CHECK_ARG(a.data && a.data_norms && a.queries && a.query_add, "exact search: missing arrays");
+        JB_CHECK_ARG(a.screen == nullptr || (a.screen_center != nullptr && a.dims <= 1040),
+                     "exact search: screen records need their centre (dims <= 1040)");
         if ((a.dims & 3) == 0) return launch_search<JB_SRC_EXACT, 1, true>(a, hs, st);
         return launch_search<JB_SRC_EXACT, 1, false>(a, hs, st);
     }

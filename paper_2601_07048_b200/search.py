@@ -140,6 +140,7 @@ class _Bound:
                                                             _lib.stream_ptr()))
             else:
                 self.kind = _lib.SRC_EXACT
+                self.screen = _screen(ds)
                 self.qadd = torch.empty(nq, dtype=torch.float32, device=q_dev.device)
                 if nq:
                     _lib.check(_lib.lib().jb_row_sq_norms(_lib.ptr(q_dev), nq, D, _lib.ptr(self.qadd),
@@ -211,6 +212,14 @@ def _to_host(*tensors):
     return [h.numpy().copy() for h in outs]
 
 
+def _screen(ds):
+    """Int8 screen records of an f32 dataset for the exact search (extension,
+    jb_search_args.screen; identical results), or None. JB_SEARCH_SCREEN=0: off."""
+    if os.environ.get("JB_SEARCH_SCREEN", "1") == "0":
+        return None
+    return ds.device_screen()
+
+
 def _source_args(a, bound: _Bound) -> None:
     """Fill the distance-source + bound-query fields of a jb_search_args."""
     a.source = bound.kind
@@ -221,6 +230,9 @@ def _source_args(a, bound: _Bound) -> None:
     elif bound.kind == _lib.SRC_EXACT:
         a.data = _lib.ptr(bound.rows.x)
         a.data_norms = _lib.ptr(bound.rows.norms)
+        scr = getattr(bound, "screen", None)
+        if scr is not None:
+            a.screen, a.screen_center = _lib.ptr(scr[0]), _lib.ptr(scr[1])
     else:
         a.records = _lib.ptr(bound.records)
         a.record_bytes = bound.record_bytes
@@ -614,6 +626,9 @@ def _knn_plan(graph: GraphIndex, source, D: int, params: SearchParams, exact_dat
         rows = ds.device()
         a.source = _lib.SRC_EXACT
         a.data, a.data_norms = _lib.ptr(rows.x), _lib.ptr(rows.norms)
+        scr = _screen(ds)
+        if scr is not None:
+            a.screen, a.screen_center = _lib.ptr(scr[0]), _lib.ptr(scr[1])
     plan.k = params.k
     plan.chunk = int(PIPELINE["chunk"])
     return plan

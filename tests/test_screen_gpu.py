@@ -1,0 +1,92 @@
+"""Int8 screen of the exact search (extension, jb_search_args.screen): a new
+neighbour proven worse than the full beam's worst key is dropped without its f32
+row. Frontier, trace and evals must equal the unscreened search, and graphs
+built with the screen equal the oracle's and the unscreened build's. The staged
+(non-L2-resident) exact path is forced with JB_EXACT_DIRECT=0."""
+
+import os
+
+import numpy as np
+import pytest
+
+from conftest import gaussian, lowrank
+from oracle import cref
+
+pytestmark = pytest.mark.gpu
+
+jb = pytest.importorskip("paper_2601_07048_b200")
+
+
+class _env:
+    def __init__(self, **kv):
+        self.kv = kv
+
+    def __enter__(self):
+        self.old = {k: os.environ.get(k) for k in self.kv}
+        os.environ.update(self.kv)
+
+    def __exit__(self, *exc):
+        for k, v in self.old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+
+
+def test_screen_records_bound_the_quantisation_error():
+    import torch
+
+    from paper_2601_07048_b200 import _lib
+
+    for n, d in ((1000, 128), (300, 33), (50, 960)):
+        x = lowrank(n, d, 12, 0.05, 3)
+        ds = jb.VectorDataset(x)
+        rec, cen = ds.device_screen()
+        rb = int(_lib.lib().jb_screen_record_bytes(d))
+        assert rec.shape == (n, rb) and rb == ((d + 15) // 16) * 16 + 16
+        r = rec.cpu().numpy()
+        c = cen.cpu().numpy().astype(np.float64)
+        b = r[:, :d].view(np.int8).astype(np.float64)
+        meta = r[:, rb - 16:].copy().view(np.float32)
+        s, bb, eps, nx = meta[:, 0].astype(np.float64), meta[:, 1], meta[:, 2].astype(np.float64), meta[:, 3]
+        err = np.sqrt(((s[:, None] * b - (x.astype(np.float64) - c)) ** 2).sum(1))
+        assert (err <= eps).all()
+        assert np.array_equal(bb, (b ** 2).sum(1).astype(np.float32))
+        assert (r[:, d:rb - 16] == 0).all()
+        assert np.array_equal(nx, ds.device().norms.cpu().numpy())
+        assert np.abs(b).max() <= 127
+
+
+@pytest.mark.parametrize("L", [16, 64, 200])
+def test_screened_search_identical(L):
+    x = lowrank(30000, 128, 16, 0.05, 5)
+    q = lowrank(300, 128, 16, 0.05, 6)
+    ds = jb.VectorDataset(x)
+    g = jb.build(ds, jb.BuildParams(degree_cap=32, build_beam_width=48, alpha=1.2))
+    from paper_2601_07048_b200 import search as js
+
+    outs = []
+    for scr in ("0", "1"):
+        with _env(JB_EXACT_DIRECT="0", JB_SEARCH_SCREEN=scr):
+            outs.append(js.run_beam_searches(g, ds, q, L))
+    for a, b in zip(*outs):
+        assert np.array_equal(a.frontier_ids, b.frontier_ids)
+        assert np.array_equal(a.frontier_dists, b.frontier_dists)
+        assert np.array_equal(a.visited_ids, b.visited_ids)
+        assert a.stats == b.stats
+
+
+@pytest.mark.parametrize("D,seed", [(128, 1), (96, 2), (40, 3)])
+def test_screened_build_identical_to_oracle_and_unscreened(D, seed):
+    x = lowrank(6000, D, 12, 0.05, seed) if D != 40 else gaussian(6000, D, seed)
+    p = jb.BuildParams(degree_cap=24, build_beam_width=40, alpha=1.2, max_batch=2000)
+    graphs = []
+    for scr in ("0", "1"):
+        with _env(JB_EXACT_DIRECT="0", JB_SCREEN=scr):
+            graphs.append(jb.build(jb.VectorDataset(x), p))
+    ref = cref.build(x, 24, 40, 1.2, max_batch=2000)
+    for g in graphs:
+        n = g.active_count
+        assert np.array_equal(g.host_adjacency()[:n], ref.adj[:n])
+        assert np.array_equal(g.degrees[:n], ref.deg[:n])
+        assert g.entry_point == ref.entry
