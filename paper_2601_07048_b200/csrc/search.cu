@@ -72,6 +72,8 @@ struct SearchLayout {
     int hbits;      // log2(number of 4-way buckets)
     int scr_off;    // EXACT: int8 code of the centred query (screen), 16 B aligned
     int srows;      // EXACT: rows staged per pass (32; 16 with the screen: fewer survivors, more warps)
+    int srb;        // screen record bytes
+    int spf;        // 1: prefetch the speculative next hop's screen records into L2
 };
 
 static int pow2_ceil(int v) { int p = 1; while (p < v) p <<= 1; return p; }
@@ -96,6 +98,8 @@ __host__ __device__ constexpr SearchLayout make_layout(int src, int D, int L, in
     s.sstride = s.chunk + 4;
     s.stage_off = off;
     s.srows = srows;
+    s.srb = ((D + 15) & ~15) + 16;
+    s.spf = 0;
     if (src == JB_SRC_EXACT && !direct) off += srows * s.sstride * 4;
     s.plane_off = off;
     if (src == JB_SRC_RABITQ_FAST) off += qb * ((((D + 31) / 32) + 3) & ~3) * 4;
@@ -802,6 +806,13 @@ beam_search_kernel(const jb_search_args a, const SearchLayout lay_arg, int* __re
                     s0 = sqrtf(__uint_as_float((uint32_t)(beam[L - 1] >> 32))) * (1.0f + 0x1p-20f);
                 const uint64_t key = eval_chunk<SRC, BITS, ALIGNED, KD, DIRECT, SREC>(a, lay, qc, tab, nbv[c], evals,
                                                                                      lossy, bphase, s0);
+                if (SRC == JB_SRC_EXACT && sa != nullptr && lay.spf && spec_nb[c] >= 0) {
+                    // the speculative next hop's screen records into L2 (its adjacency row
+                    // has arrived by now): the next hop's screen then reads L2, not HBM
+                    const char* pr = reinterpret_cast<const char*>(a.screen) + (size_t)spec_nb[c] * lay.srb;
+                    asm volatile("prefetch.global.L2 [%0];" ::"l"(pr));
+                    asm volatile("prefetch.global.L2 [%0];" ::"l"(pr + lay.srb - 16));
+                }
                 const int p0 = merge_into_beam(beam, bcount, L, key, fmask);
                 s_min = min(s_min, p0);
                 p_ins = p0;
@@ -1100,6 +1111,12 @@ static int screen_srows() {
     return v >= 32 ? 32 : (v <= 8 ? 8 : 16);
 }
 
+// JB_SCREEN_PF=0: no L2 prefetch of the next hop's screen records (A/B)
+static bool screen_prefetch() {
+    const char* e = std::getenv("JB_SCREEN_PF");
+    return !(e && e[0] == '0');
+}
+
 // R <= 32: one neighbour chunk per hop (single merge, no rescan of the beam);
 // MAX_CHUNKS for wider rows. Blocks/SM: the popcount kernel is issue-bound and
 // gains from 10 resident blocks; the float estimators keep 8.
@@ -1111,8 +1128,9 @@ static int launch_search(const jb_search_args& a, int hash_slots, cudaStream_t s
                                                    : JB_OTHER_MINB;
     constexpr int NW = warps_per_block<SRC>();
     const int L = a.beam_width;
-    const SearchLayout lay = make_layout(SRC, a.dims, L, hash_slots, FAST_QB, false, 0,
-                                         (SRC == JB_SRC_EXACT && a.screen != nullptr) ? screen_srows() : 32);
+    SearchLayout lay = make_layout(SRC, a.dims, L, hash_slots, FAST_QB, false, 0,
+                                   (SRC == JB_SRC_EXACT && a.screen != nullptr) ? screen_srows() : 32);
+    lay.spf = (SRC == JB_SRC_EXACT && a.screen != nullptr && screen_prefetch()) ? 1 : 0;
     if (a.degree_cap <= 32 && SRC == JB_SRC_RABITQ_FAST && BITS == 1) {
         // specialised shapes: D in {96, 128} with a 512- or 1024-slot visited table (popcount
         // estimator only: measured -2% at L=128; the float estimators got slower, +4%)
