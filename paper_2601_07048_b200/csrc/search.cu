@@ -1044,6 +1044,26 @@ static bool rows_l2_resident(const jb_search_args& a) {
     return (double)a.active_count * a.dims * 4.0 <= 0.5 * (double)l2;
 }
 
+// The screen adds one dependent record fetch per hop in front of the survivors'
+// row fetch; it pays where the records stay largely L2-resident (measured: 1M x 128,
+// records 144 MB: phase-1 search 19.8 -> 14.0 ms per 100K) or the rows are long
+// (1M x 960: records 976 B vs 3840 B rows; build 251K -> 266K inserts/s), and loses
+// on HBM-resident short rows (12.5M x 96, 1.4 GB of records: 16.8 -> 23.4 ms).
+// JB_SCREEN_FORCE=1 / 0 overrides (A/B).
+static bool screen_pays(const jb_search_args& a) {
+    const char* e = std::getenv("JB_SCREEN_FORCE");
+    if (e && (e[0] == '0' || e[0] == '1')) return e[0] == '1';
+    static thread_local int dev = -1, l2 = 0;
+    int d = 0;
+    if (cudaGetDevice(&d) != cudaSuccess) return false;
+    if (d != dev) {
+        if (cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, d) != cudaSuccess) l2 = 0;
+        dev = d;
+    }
+    const double rec = (double)a.active_count * (((a.dims + 15) & ~15) + 16);
+    return rec <= 2.0 * (double)l2 || a.dims >= 256;
+}
+
 #ifndef JB_SREC_MIN
 #define JB_SREC_MIN 256  // records of at least this many bytes are staged into smem (SREC kernels)
 #endif
@@ -1202,6 +1222,12 @@ int jb_beam_search(const jb_search_args* args, void* stream) {
         JB_CHECK_ARG(a.data && a.data_norms && a.queries && a.query_add, "exact search: missing arrays");
         JB_CHECK_ARG(a.screen == nullptr || (a.screen_center != nullptr && a.dims <= 1040),
                      "exact search: screen records need their centre (dims <= 1040)");
+        if (a.screen != nullptr && !screen_pays(a)) {  // the screen would cost more than it saves
+            jb_search_args b = a;
+            b.screen = nullptr;
+            if ((b.dims & 3) == 0) return launch_search<JB_SRC_EXACT, 1, true>(b, hs, st);
+            return launch_search<JB_SRC_EXACT, 1, false>(b, hs, st);
+        }
         if ((a.dims & 3) == 0) return launch_search<JB_SRC_EXACT, 1, true>(a, hs, st);
         return launch_search<JB_SRC_EXACT, 1, false>(a, hs, st);
     }
