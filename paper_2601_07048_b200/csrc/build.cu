@@ -607,6 +607,165 @@ seed_prune_kernel(const M m, int64_t start, int64_t stop, int64_t xi0, int64_t x
     write_row(m, alpha2, adj, deg, R, x, ki, k);
 }
 
+// ---- int8-screened staged prune (phase 2 with screen records, f32 rows) ------
+// The extraction sequence of warp_prune_split (argmin over the survivors, then the
+// star's pair test against each survivor c: remove c iff !(alpha^2 d(p, c) > d(t, c)),
+// graph.py:218), with the pair test decided from the staged int8 screen records
+// (screen.cu) when the bound is certain: |p - c| lies within |p~ - c~| -/+ (eps_p +
+// eps_c), |p~ - c~|^2 = s_p^2|b_p|^2 + s_c^2|b_c|^2 - 2 s_p s_c <b_p, b_c> (exact
+// integer dot, f64 evaluation with 2^-40 slacks), and the f32 distance the reference
+// compares differs from |p - c|^2 by at most M = (D + 32) 2^-24 (|p|^2 + |c|^2). Only
+// undecided pairs read the two f32 rows (global, A1 order, the staged path's operand
+// roles). Records are ~3.5x smaller than f32 rows, so ~3x more warps stage a trace.
+__device__ int warp_prune_screen(uint64_t* cand, int n, double alpha2, int R, const F32Metric& m,
+                                 const unsigned char* recs, int rb, uint16_t* lst, int32_t* out_ids, uint32_t* out_d) {
+    const unsigned FULL = 0xFFFFFFFFu;
+    const int lane = lane_id();
+    const int dp = rb - 16;
+    const double Mk = (double)(m.D + 32) * 0x1p-24;
+    for (int j = lane; j < n; j += 32) lst[j] = (uint16_t)j;
+    __syncwarp();
+    int s = n, kept = 0;
+    while (kept < R && s > 0) {
+        uint64_t mk = UMAX;
+        int mi = -1;
+        for (int j = lane; j < s; j += 32) {
+            const int i = lst[j];
+            const uint64_t c = cand[i];
+            if (c < mk) { mk = c; mi = i; }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const uint64_t om = shfl_xor_u64(mk, o);
+            const int oi = __shfl_xor_sync(FULL, mi, o);
+            if (om < mk) { mk = om; mi = oi; }
+        }
+        if (mk == UMAX) break;
+        __syncwarp();  // every lane's argmin reads of cand precede lane 0's write (WAR)
+        if (lane == 0) {
+            out_ids[kept] = (int32_t)(mk & 0xFFFFFFFFull);
+            out_d[kept] = (uint32_t)(mk >> 32);
+            cand[mi] = UMAX;
+        }
+        ++kept;
+        __syncwarp();
+        if (kept >= R) break;
+        const unsigned char* rp = recs + (size_t)mi * rb;
+        const float4 mp = *reinterpret_cast<const float4*>(rp + dp);  // s, |b|^2, eps, |x|^2
+        const uint32_t idp = (uint32_t)(mk & 0xFFFFFFFFull);
+        for (int j = lane; j < s; j += 32) {
+            const int i = lst[j];
+            const uint64_t c = cand[i];
+            if (c == UMAX) continue;
+            const unsigned char* rc = recs + (size_t)i * rb;
+            int dot = 0;
+            for (int w = 0; w < dp; w += 16) {
+                const uint4 a = *reinterpret_cast<const uint4*>(rc + w);
+                const uint4 b = *reinterpret_cast<const uint4*>(rp + w);
+                dot = __dp4a((int)a.x, (int)b.x, dot);
+                dot = __dp4a((int)a.y, (int)b.y, dot);
+                dot = __dp4a((int)a.z, (int)b.z, dot);
+                dot = __dp4a((int)a.w, (int)b.w, dot);
+            }
+            const float4 mc = *reinterpret_cast<const float4*>(rc + dp);
+            const double A = (double)mp.x * mp.x * mp.y, B = (double)mc.x * mc.x * mc.y;
+            const double dd = (A + B) - 2.0 * (double)mp.x * (double)mc.x * (double)dot;
+            const double sl = 0x1p-40 * (A + B);
+            const double e = (double)mp.z + (double)mc.z;
+            const double lo = fmax(sqrt(fmax(dd - sl, 0.0)) * (1.0 - 0x1p-40) - e, 0.0);
+            const double hi = sqrt(dd + sl) * (1.0 + 0x1p-40) + e;
+            const double M = Mk * ((double)mp.w + (double)mc.w);
+            const double dlo = lo * lo * (1.0 - 0x1p-40) - M, dhi = hi * hi * (1.0 + 0x1p-40) + M;
+            const double dtc = (double)__uint_as_float((uint32_t)(c >> 32));
+            bool remove;
+            if (alpha2 * dlo * (1.0 - 0x1p-40) > dtc) remove = false;
+            else if (alpha2 * dhi * (1.0 + 0x1p-40) <= dtc) remove = true;
+            else {  // undecided: the exact A1 distance (c in the data role, the star as the pivot)
+                const uint32_t idc = (uint32_t)(c & 0xFFFFFFFFull);
+                const float d = exact_from_dot(mc.w, a1_dot<false>(m.data + (size_t)idc * m.D, m.data + (size_t)idp * m.D,
+                                                                  m.D), mp.w);
+                remove = !(__dmul_rn(alpha2, (double)d) > dtc);
+            }
+            if (remove) cand[i] = UMAX;
+        }
+        __syncwarp();
+        int ns = 0;  // compact: entries only move down, within the chunk being read
+        for (int b = 0; b < s; b += 32) {
+            const int j = b + lane;
+            int i = 0;
+            bool live = false;
+            if (j < s) { i = lst[j]; live = cand[i] != UMAX; }
+            const unsigned msk = __ballot_sync(FULL, live);
+            __syncwarp();  // every lane's read of this chunk precedes the writes below (WAR)
+            if (live) lst[ns + __popc(msk & lanemask_lt())] = (uint16_t)i;
+            ns += __popc(msk);
+            __syncwarp();
+        }
+        s = ns;
+    }
+    __syncwarp();
+    return kept;
+}
+
+// phase 2 with screen records: per warp (1-warp blocks) srows staged records |
+// u16 survivor list | staging mbarrier | pivot row (global-row prune of longer traces)
+__host__ __device__ inline int p2s_warp_bytes(int srows, int rb, int D) {
+    return ((srows * rb + srows * 2 + 15) & ~15) + 16 + ((((D + 3) & ~3) + 4) * 4);
+}
+
+__global__ void __launch_bounds__(32)
+phase2_screen_kernel(const F32Metric m, const uint8_t* __restrict__ screen, int rb, int srows, int64_t start,
+                     int64_t nb, double alpha2, int R, const int32_t* __restrict__ hops,
+                     const int32_t* __restrict__ tids, const uint32_t* __restrict__ tdst, int cap, int reverse_all,
+                     uint64_t* __restrict__ cand_all, int32_t* __restrict__ kept_ids, uint32_t* __restrict__ kept_d,
+                     int32_t* __restrict__ adj, int32_t* __restrict__ deg, uint32_t* __restrict__ tri_target,
+                     uint64_t* __restrict__ tri_key, int W) {
+    extern __shared__ __align__(16) unsigned char shs[];
+    const int lane = threadIdx.x & 31;
+    unsigned char* recs = shs;
+    uint16_t* lst = reinterpret_cast<uint16_t*>(shs + (size_t)srows * rb);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(shs + (((size_t)srows * rb + srows * 2 + 15) & ~(size_t)15));
+    uint32_t* pv = reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned char*>(bar) + 16);
+    const int64_t xi = blockIdx.x;
+    if (xi >= nb) return;
+    if (lane == 0) wbar_init(bar);
+    __syncwarp();
+    uint32_t sph = 0;
+    const uint32_t x = (uint32_t)(start + xi);
+    const int h = min(hops[xi], cap);
+    uint64_t* cand = cand_all + xi * cap;
+    const int32_t* ti = tids + xi * cap;
+    const uint32_t* td = tdst + xi * cap;
+    for (int j = lane; j < h; j += 32) cand[j] = key_of(td[j], (uint32_t)ti[j]);
+    __syncwarp();
+    int32_t* ki = kept_ids + xi * R;
+    uint32_t* kd = kept_d + xi * R;
+    int k;
+    if (h <= srows) {
+        wbar_expect(bar, (uint32_t)h * (uint32_t)rb);
+        for (int j = lane; j < h; j += 32)
+            bulk_row(recs + (size_t)j * rb, screen + (size_t)(uint32_t)ti[j] * rb, (uint32_t)rb, bar);
+        wbar_wait(bar, sph);
+        __syncwarp();
+        k = warp_prune_screen(cand, h, alpha2, R, m, recs, rb, lst, ki, kd);
+    } else {
+        k = warp_prune(cand, h, alpha2, R, m, pv, ki, kd);
+    }
+    write_row(m, alpha2, adj, deg, R, x, ki, k);
+    uint32_t* tt = tri_target + xi * W;
+    uint64_t* tk = tri_key + xi * W;
+    const int ne = reverse_all ? h : k;
+    for (int j = lane; j < W; j += 32) {
+        if (j < ne) {
+            tt[j] = reverse_all ? (uint32_t)ti[j] : (uint32_t)ki[j];
+            tk[j] = key_of(reverse_all ? td[j] : kd[j], x);
+        } else {
+            tt[j] = NO_TARGET;
+            tk[j] = UMAX;
+        }
+    }
+}
+
 // ---- phase 2: prune each new vertex's visited trace, emit reverse triples ----
 // Trace distances are the search keys' 32-bit words (tdst holds their bits).
 template <class M>
@@ -2385,6 +2544,12 @@ __global__ void owner_pool_need_kernel(const uint32_t* __restrict__ tgt, int64_t
     need[s] = c > OWNER_SC ? (unsigned long long)c : 0ull;
 }
 
+// JB_P2_SCREEN=0: phase 2 stages f32 rows even when screen records are given (A/B)
+static bool p2_screen_on() {
+    const char* e = getenv("JB_P2_SCREEN");
+    return !(e && e[0] == '0');
+}
+
 // JB_CLOSED_PASS=0: closed rows stay on the staged deferred pass (A/B)
 static bool closed_pass_on() {
     const char* e = getenv("JB_CLOSED_PASS");  // read per batch (A/B within one process)
@@ -2676,6 +2841,19 @@ static int batch_insert_impl(const M& m, const jb_insert_args& a, cudaStream_t s
             phase2_matrix_kernel<<<(unsigned)nb, 256, psm, st>>>(m, a.start, nb, alpha2, R, hops, tids, tdst, cap,
                                                                  a.reverse_all_visited, cand, kid, kd, a.adjacency,
                                                                  a.degrees, tt, tk, W);
+            p2_done = true;
+        }
+    }
+    if constexpr (std::is_same<M, F32Metric>::value) {
+        // screen records available (f32 rows): the int8-screened staged prune
+        if (!p2_done && a.screen != nullptr && p2_screen_on()) {
+            const int rb = jb_screen_record_bytes(a.dims);
+            const int srows = std::min(cap, a.build_beam_width + JB_P2_ROWS_OVER_L);
+            const int sm = p2s_warp_bytes(srows, rb, a.dims);
+            JB_CUDA_RC(grow_smem(phase2_screen_kernel, sm));
+            phase2_screen_kernel<<<(unsigned)nb, 32, sm, st>>>(m, a.screen, rb, srows, a.start, nb, alpha2, R, hops, tids,
+                                                                tdst, cap, a.reverse_all_visited, cand, kid, kd,
+                                                                a.adjacency, a.degrees, tt, tk, W);
             p2_done = true;
         }
     }
