@@ -9,6 +9,8 @@ Cases (each tiny, so the instrumented run finishes in seconds):
              repair (BFS, donor scan, attach) all run; checked against the oracle
   pipeline   search_knn_batch host pipeline (two streams, chunked) + rerank
   protocol   bound distances, robust prune (row and matrix forms), shard pack/merge
+  screen     round-2 re-entry: int8 screen records, screened search and phase-2
+             prune, closed-row owner pass (checked against the C oracle)
   staged     round-2 paths: exact search with bulk-staged rows (JB_EXACT_DIRECT=0),
              960-d RaBitQ-4 search with bulk-staged records, a repair-heavy build
              (tensor-core donor screen, Gram-screened owner prune, bulk staging)
@@ -125,6 +127,30 @@ def case_staged():
     for est in ("reference", "popcount"):
         jb.search_knn_batch(gh, ih, qh, jb.SearchParams(beam_width=16, k=5, rerank=True, estimator=est), exact_data=dh)
     print("staged ok")
+
+
+def case_screen():
+    """round-2 re-entry paths: int8 screen records, screened exact search (16-row
+    stage, chain-split A1, next-hop prefetch), screened phase-2 prune, closed-row
+    owner pass; D = 40 exercises zero-padded code words."""
+    import paper_2601_07048_b200 as jb
+    from conftest import gaussian, lowrank
+    from oracle import cref
+    from paper_2601_07048_b200 import search as js
+
+    os.environ["JB_EXACT_DIRECT"] = "0"
+    for x in (lowrank(2500, 64, 12, 0.05, 21), gaussian(2000, 40, 22)):
+        p = jb.BuildParams(degree_cap=12, build_beam_width=24, alpha=1.2, max_batch=500)
+        g = jb.build(jb.VectorDataset(x), p)
+        ref = cref.build(x, 12, 24, 1.2, max_batch=500)
+        assert np.array_equal(g.host_adjacency()[: g.active_count], ref.adj[: g.active_count])
+        q = x[:30] + 0.01
+        res = js.run_beam_searches(g, jb.VectorDataset(x), q, 48)
+        os.environ["JB_SEARCH_SCREEN"] = "0"
+        res0 = js.run_beam_searches(g, jb.VectorDataset(x), q, 48)
+        os.environ.pop("JB_SEARCH_SCREEN")
+        assert all(np.array_equal(a.frontier_ids, b.frontier_ids) for a, b in zip(res, res0))
+    print("screen ok")
 
 
 if __name__ == "__main__":
