@@ -1124,11 +1124,19 @@ static int launch_search_kernel(SearchKernel kern, const SearchLayout& lay, cons
     return JB_OK;
 }
 
-// rows staged per pass with the screen (JB_SCREEN_SROWS, 8..32; default 16)
+// rows staged per pass with the screen (JB_SCREEN_SROWS, 8..32; default 8 with the
+// 14-block kernel: 13.5 ms per 100K at 1M vs 14.0 for 16 rows at 8 blocks)
 static int screen_srows() {
     const char* e = std::getenv("JB_SCREEN_SROWS");
-    const int v = e ? std::atoi(e) : 16;
+    const int v = e ? std::atoi(e) : 8;
     return v >= 32 ? 32 : (v <= 8 ? 8 : 16);
+}
+
+// resident blocks the screened exact kernel is compiled for (JB_SCREEN_MINB: 8 or 14,
+// default 14: 72 registers with a few spills, 28 warps/SM with the 8-row stage)
+static int screen_minb() {
+    const char* e = std::getenv("JB_SCREEN_MINB");
+    return (e && std::atoi(e) == 8) ? 8 : 14;
 }
 
 // JB_SCREEN_PF=0: no L2 prefetch of the next hop's screen records (A/B)
@@ -1173,6 +1181,12 @@ static int launch_search(const jb_search_args& a, int hash_slots, cudaStream_t s
     if (SRC == JB_SRC_EXACT && ALIGNED && a.degree_cap <= 32 && rows_l2_resident(a)) {
         const SearchLayout ld = make_layout(SRC, a.dims, L, hash_slots, FAST_QB, true);
         return launch_search_kernel(beam_search_kernel<SRC, BITS, ALIGNED, 1, MINB, 0, 0, true>, ld, a, st, NW);
+    }
+    if constexpr (SRC == JB_SRC_EXACT) {
+        // screened exact rows (16- or 8-row stage): registers, not smem, cap the warps
+        // per SM at 8 blocks; the 14-block build trades a few spills for occupancy
+        if (a.degree_cap <= 32 && a.screen != nullptr && screen_minb() == 14)
+            return launch_search_kernel(beam_search_kernel<SRC, BITS, ALIGNED, 1, 14>, lay, a, st, NW);
     }
     if (a.degree_cap <= 32) return launch_search_kernel(beam_search_kernel<SRC, BITS, ALIGNED, 1, MINB>, lay, a, st, NW);
     return launch_search_kernel(beam_search_kernel<SRC, BITS, ALIGNED, MAX_CHUNKS, 8>, lay, a, st, NW);
