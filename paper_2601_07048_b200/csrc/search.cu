@@ -1109,11 +1109,6 @@ static int launch_search_kernel(SearchKernel kern, const SearchLayout& lay, cons
         cache[next] = Entry{kern, smem, dev, per_sm};
         next = (next + 1) % 16;
     }
-    static const int l2_fetch = [] {  // JB_L2_FETCH=<bytes>: L2 fetch granularity experiment
-        const char* e = std::getenv("JB_L2_FETCH");
-        return e ? std::atoi(e) : 0;
-    }();
-    if (l2_fetch > 0) JB_CUDA(cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)l2_fetch));
     int64_t need = (a.nq + nw - 1) / nw;
     int grid = (int)std::min<int64_t>(need, (int64_t)per_sm * sm_count_current());
     Scratch ctr;

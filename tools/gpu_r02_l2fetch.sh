@@ -2,7 +2,7 @@
 # L2 fetch granularity (cudaLimitMaxL2FetchGranularity) vs search kernel time / DRAM bytes
 mkdir -p gpurun_out
 python -m paper_2601_07048_b200._build > /dev/null 2>&1
-for v in 0 32 64; do
+for v in 0 32 64; do  # (JB_L2_FETCH hook removed after this experiment; see DESIGN 9b)
   JB_L2_FETCH=$v timeout 600 python bench.py --config c5 --beam 80 --estimator reference --no-cpu --steps 5 --warmup 3 \
      --out gpurun_out/l2f_c5_$v.json > gpurun_out/l2f_c5_$v.log 2>&1
   python -c "import json;b=json.load(open('gpurun_out/l2f_c5_$v.json'));print('c5 fetch $v', b['value'], b['kernel_ms'])"
