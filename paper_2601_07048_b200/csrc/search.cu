@@ -1045,10 +1045,12 @@ static bool rows_l2_resident(const jb_search_args& a) {
 }
 
 // The screen adds one dependent record fetch per hop in front of the survivors'
-// row fetch; it pays where the records stay largely L2-resident (measured: 1M x 128,
-// records 144 MB: phase-1 search 19.8 -> 14.0 ms per 100K) or the rows are long
-// (1M x 960: records 976 B vs 3840 B rows; build 251K -> 266K inserts/s), and loses
-// on HBM-resident short rows (12.5M x 96, 1.4 GB of records: 16.8 -> 23.4 ms).
+// row fetch; it pays where the records stay largely L2-resident or the rows are
+// long, and loses on HBM-resident short rows. Measured (phase-1 search per 100K,
+// 8-row stage, 14-block kernel): 1M x 128 (144 MB of records) 19.8 -> 13.5 ms;
+// 96-d: 3M (336 MB) 16.0 -> 13.8, 4.5M (504 MB) 16.4 -> 18.3, 6M 16.7 -> 20.7,
+// 12.5M 17.3 -> 24.4 ms; 1M x 960 (976 B records vs 3840 B rows) build 251K ->
+// 266K inserts/s. Hence: records <= 3 x L2 (378 MB on B200), or D >= 256.
 // JB_SCREEN_FORCE=1 / 0 overrides (A/B).
 static bool screen_pays(const jb_search_args& a) {
     const char* e = std::getenv("JB_SCREEN_FORCE");
@@ -1061,7 +1063,7 @@ static bool screen_pays(const jb_search_args& a) {
         dev = d;
     }
     const double rec = (double)a.active_count * (((a.dims + 15) & ~15) + 16);
-    return rec <= 2.0 * (double)l2 || a.dims >= 256;
+    return rec <= 3.0 * (double)l2 || a.dims >= 256;
 }
 
 #ifndef JB_SREC_MIN

@@ -17,6 +17,7 @@ x = jb.gen_lowrank(n, d, seed=1, d_int=16, noise=0.05, basis_seed=0)
 ds = jb.VectorDataset(x)
 g = jb.build(ds, jb.BuildParams(degree_cap=32, build_beam_width=64, alpha=1.2))
 q = ds.device().x[n - 100_000:].contiguous()
+os.environ.setdefault("JB_SCREEN_FORCE", "1")  # measure the screen even where the library's policy skips it
 on = js._Bound(ds, q)
 off = js._Bound(ds, q)
 off.screen = None
