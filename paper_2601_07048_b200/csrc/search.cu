@@ -810,8 +810,12 @@ beam_search_kernel(const jb_search_args a, const SearchLayout lay_arg, int* __re
                     // the speculative next hop's screen records into L2 (its adjacency row
                     // has arrived by now): the next hop's screen then reads L2, not HBM
                     const char* pr = reinterpret_cast<const char*>(a.screen) + (size_t)spec_nb[c] * lay.srb;
-                    asm volatile("prefetch.global.L2 [%0];" ::"l"(pr));
-                    asm volatile("prefetch.global.L2 [%0];" ::"l"(pr + lay.srb - 16));
+                    if (lay.spf == 2) {  // the copy engine's L2 prefetch of the whole record
+                        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(pr), "r"(lay.srb) : "memory");
+                    } else {
+                        asm volatile("prefetch.global.L2 [%0];" ::"l"(pr));
+                        asm volatile("prefetch.global.L2 [%0];" ::"l"(pr + lay.srb - 16));
+                    }
                 }
                 const int p0 = merge_into_beam(beam, bcount, L, key, fmask);
                 s_min = min(s_min, p0);
@@ -1136,10 +1140,11 @@ static int screen_minb() {
     return (e && std::atoi(e) == 8) ? 8 : 14;
 }
 
-// JB_SCREEN_PF=0: no L2 prefetch of the next hop's screen records (A/B)
-static bool screen_prefetch() {
+// JB_SCREEN_PF: 0 = no prefetch of the next hop's screen records, 1 = prefetch.global.L2
+// (default), 2 = cp.async.bulk.prefetch.L2 (better at 6M x 96, worse at 1M x 128)
+static int screen_prefetch() {
     const char* e = std::getenv("JB_SCREEN_PF");
-    return !(e && e[0] == '0');
+    return e ? std::atoi(e) : 1;
 }
 
 // R <= 32: one neighbour chunk per hop (single merge, no rescan of the beam);
@@ -1155,7 +1160,7 @@ static int launch_search(const jb_search_args& a, int hash_slots, cudaStream_t s
     const int L = a.beam_width;
     SearchLayout lay = make_layout(SRC, a.dims, L, hash_slots, FAST_QB, false, 0,
                                    (SRC == JB_SRC_EXACT && a.screen != nullptr) ? screen_srows() : 32);
-    lay.spf = (SRC == JB_SRC_EXACT && a.screen != nullptr && screen_prefetch()) ? 1 : 0;
+    lay.spf = (SRC == JB_SRC_EXACT && a.screen != nullptr) ? screen_prefetch() : 0;
     if (a.degree_cap <= 32 && SRC == JB_SRC_RABITQ_FAST && BITS == 1) {
         // specialised shapes: D in {96, 128} with a 512- or 1024-slot visited table (popcount
         // estimator only: measured -2% at L=128; the float estimators got slower, +4%)
