@@ -90,3 +90,37 @@ def test_screened_build_identical_to_oracle_and_unscreened(D, seed):
         assert np.array_equal(g.host_adjacency()[:n], ref.adj[:n])
         assert np.array_equal(g.degrees[:n], ref.deg[:n])
         assert g.entry_point == ref.entry
+
+
+@pytest.mark.parametrize("D,R", [(33, 16), (50, 24), (200, 24), (300, 16), (96, 64)])
+def test_screened_search_identical_shapes(D, R):
+    """Unaligned rows (D % 4 != 0), rows staged in several 128-element chunks with a
+    partial 16-block tail (D = 200, 300: the split A1 chains cross chunk boundaries),
+    and R = 64 (two neighbour chunks per hop, the worst key re-read between them)."""
+    x = lowrank(8000, D, 12, 0.05, D + R)
+    q = lowrank(120, D, 12, 0.05, D + R + 1)
+    ds = jb.VectorDataset(x)
+    g = jb.build(ds, jb.BuildParams(degree_cap=R, build_beam_width=40, alpha=1.2, max_batch=2000))
+    from paper_2601_07048_b200 import search as js
+
+    outs = []
+    for scr in ("0", "1"):
+        with _env(JB_EXACT_DIRECT="0", JB_SEARCH_SCREEN=scr, JB_SCREEN_FORCE="1"):
+            outs.append(js.run_beam_searches(g, ds, q, 48))
+    for a, b in zip(*outs):
+        assert np.array_equal(a.frontier_ids, b.frontier_ids)
+        assert np.array_equal(a.frontier_dists, b.frontier_dists)
+        assert np.array_equal(a.visited_ids, b.visited_ids)
+        assert a.stats == b.stats
+
+
+@pytest.mark.parametrize("D", [200, 33])
+def test_screened_build_chunked_and_unaligned_rows_identical_to_oracle(D):
+    x = lowrank(3000, D, 12, 0.05, 7 * D)
+    p = jb.BuildParams(degree_cap=16, build_beam_width=32, alpha=1.2, max_batch=1000)
+    with _env(JB_EXACT_DIRECT="0", JB_SCREEN_FORCE="1"):
+        g = jb.build(jb.VectorDataset(x), p)
+    ref = cref.build(x, 16, 32, 1.2, max_batch=1000)
+    n = g.active_count
+    assert np.array_equal(g.host_adjacency()[:n], ref.adj[:n])
+    assert g.entry_point == ref.entry
