@@ -74,6 +74,8 @@ struct SearchLayout {
     int srows;      // EXACT: rows staged per pass (32; 16 with the screen: fewer survivors, more warps)
     int srb;        // screen record bytes
     int spf;        // 1: prefetch the speculative next hop's screen records into L2
+    int snext;      // 1: stage the speculative next hop's screen records into smem (nrec_off)
+    int nrec_off;   // snext: 32 records + their mbarrier (16 B)
 };
 
 static int pow2_ceil(int v) { int p = 1; while (p < v) p <<= 1; return p; }
@@ -110,6 +112,8 @@ __host__ __device__ constexpr SearchLayout make_layout(int src, int D, int L, in
         s.rec_stride = ((rec_bytes - 16 + 127) / 128) * 128 + 16;
         off += 32 * s.rec_stride;
     }
+    s.snext = 0;
+    s.nrec_off = off;  // (sized by with_snext)
     s.beam_off = off; off += ((L * 8) + 15) & ~15;
     s.bytes = (off + 15) & ~15;
     return s;
@@ -400,14 +404,16 @@ struct QueryCtx {
 // sqrt(M) with M = (D + 32) 2^-24 (|x|^2 + |q|^2) >= |d_f32 - |q - x|^2| (the A1
 // dot and norms: chains of D/4 products, two combining adds, three final ops).
 // g > h => |q - x|^2 > worst + M => the exact f32 key is above the worst key.
-__device__ __forceinline__ bool screen_drop(const jb_search_args& a, const QueryCtx& c, int D, uint32_t nb, float s0) {
+__device__ __forceinline__ bool screen_drop(const jb_search_args& a, const QueryCtx& c, int D, uint32_t nb, float s0,
+                                            const uint8_t* srec = nullptr) {
     const int dp = (D + 15) & ~15;
-    const uint8_t* rec = a.screen + (size_t)nb * (dp + 16);
+    const bool sm = srec != nullptr;  // staged one hop ahead in smem (snext)
+    const uint8_t* rec = sm ? srec : a.screen + (size_t)nb * (dp + 16);
     const uint4* r = reinterpret_cast<const uint4*>(rec);
-    const float4 m = __ldg(reinterpret_cast<const float4*>(rec + dp));  // s, |b|^2, eps, |x|^2
+    const float4 m = sm ? *reinterpret_cast<const float4*>(rec + dp) : __ldg(reinterpret_cast<const float4*>(rec + dp));
     int dot = 0;
     for (int w = 0; w < (dp >> 4); ++w) {
-        const uint4 b = __ldg(r + w);
+        const uint4 b = sm ? r[w] : __ldg(r + w);
         const uint4 q = *reinterpret_cast<const uint4*>(c.sa + 4 * w);
         dot = __dp4a((int)b.x, (int)q.x, dot);
         dot = __dp4a((int)b.y, (int)q.y, dot);
@@ -471,7 +477,7 @@ __device__ __forceinline__ void screen_query(const float* qv, const float* __res
 template <int SRC, int BITS, bool ALIGNED, int KD = 0, bool DIRECT = false, bool SREC = false>
 __device__ __forceinline__ uint64_t eval_chunk(const jb_search_args& a, const SearchLayout& lay, const QueryCtx& c,
                                                uint32_t* tab, int nb, int& evals, int& lossy, uint32_t& bphase,
-                                               float s0 = __builtin_huge_valf()) {
+                                               float s0 = __builtin_huge_valf(), const uint8_t* srec = nullptr) {
     const unsigned FULL = 0xFFFFFFFFu;
     const int lane = lane_id();
     const int D = KD > 0 ? KD : a.dims;
@@ -525,7 +531,7 @@ __device__ __forceinline__ uint64_t eval_chunk(const jb_search_args& a, const Se
         // screen (beam full): only neighbours not provably worse than its worst key
         // get the exact A1 distance; the others return no key, as the merge would
         const bool ex = isnew && !(c.sa != nullptr && s0 < __builtin_huge_valf() &&
-                                   screen_drop(a, c, D, (uint32_t)nb, s0));
+                                   screen_drop(a, c, D, (uint32_t)nb, s0, srec));
         const uint32_t em = __ballot_sync(FULL, ex);
         nnew = __popc(em);
         if (nnew == 0) return UMAX;
@@ -693,6 +699,14 @@ beam_search_kernel(const jb_search_args a, const SearchLayout lay_arg, int* __re
         if (lane == 0) wbar_init(wbar);
         __syncwarp();
     }
+    // snext: the speculative next hop's screen records, staged into smem one hop ahead
+    unsigned char* nrec = base + lay.nrec_off;
+    uint64_t* nbar = reinterpret_cast<uint64_t*>(nrec + 32 * lay.srb);
+    uint32_t nphase = 0;
+    if (SRC == JB_SRC_EXACT && lay.snext) {
+        if (lane == 0) wbar_init(nbar);
+        __syncwarp();
+    }
     uint32_t* planes = reinterpret_cast<uint32_t*>(base + lay.plane_off);
     const int D = KD > 0 ? KD : a.dims;
     const int nwords = (((D + 31) / 32) + 3) & ~3;  // plane stride (16 B aligned)
@@ -767,6 +781,8 @@ beam_search_kernel(const jb_search_args a, const SearchLayout lay_arg, int* __re
         // unexpanded key after the cursor in the pre-merge beam (right whenever this
         // hop inserts nothing in front of it). Its row is loaded while this hop runs.
         int spec = -1;
+        int nxt_for = -1;     // snext: the vertex whose neighbours' records are staged
+        bool nxt_pend = false;
         int spec_nb[CH];
 #pragma unroll
         for (int c = 0; c < CH; ++c) spec_nb[c] = -1;
@@ -774,6 +790,12 @@ beam_search_kernel(const jb_search_args a, const SearchLayout lay_arg, int* __re
         while (cursor < bcount) {
             const uint64_t ukey = beam[cursor];
             const uint32_t u = key_id(ukey);
+            bool nxt_hit = false;
+            if (SRC == JB_SRC_EXACT && CH == 1 && lay.snext && nxt_pend) {
+                wbar_wait(nbar, nphase);
+                nxt_pend = false;
+                nxt_hit = nxt_for == (int)u;
+            }
             const int sidx = first_unexpanded(beam, cursor + 1, bcount);
             const int nspec = sidx < bcount ? (int)key_id(beam[sidx]) : -1;
             __syncwarp();
@@ -804,9 +826,22 @@ beam_search_kernel(const jb_search_args a, const SearchLayout lay_arg, int* __re
                 float s0 = __builtin_huge_valf();  // sqrt(worst distance), rounded up; inf: no screen
                 if (SRC == JB_SRC_EXACT && sa != nullptr && bcount == L)
                     s0 = sqrtf(__uint_as_float((uint32_t)(beam[L - 1] >> 32))) * (1.0f + 0x1p-20f);
+                const uint8_t* srec = (SRC == JB_SRC_EXACT && nxt_hit) ? nrec + lane * lay.srb : nullptr;
                 const uint64_t key = eval_chunk<SRC, BITS, ALIGNED, KD, DIRECT, SREC>(a, lay, qc, tab, nbv[c], evals,
-                                                                                     lossy, bphase, s0);
-                if (SRC == JB_SRC_EXACT && sa != nullptr && lay.spf && spec_nb[c] >= 0) {
+                                                                                     lossy, bphase, s0, srec);
+                if (SRC == JB_SRC_EXACT && CH == 1 && lay.snext && sa != nullptr && bcount == L) {
+                    // stage the speculative next hop's records (its adjacency row has arrived)
+                    const int have = spec_nb[0] >= 0;
+                    const uint32_t cnt = (uint32_t)__popc(__ballot_sync(0xFFFFFFFFu, have));
+                    if (cnt > 0) {
+                        wbar_expect(nbar, cnt * (uint32_t)lay.srb);
+                        if (have)
+                            bulk_row(nrec + lane * lay.srb, a.screen + (size_t)spec_nb[0] * lay.srb, (uint32_t)lay.srb,
+                                     nbar);
+                        nxt_for = spec;
+                        nxt_pend = true;
+                    }
+                } else if (SRC == JB_SRC_EXACT && sa != nullptr && lay.spf && spec_nb[c] >= 0) {
                     // the speculative next hop's screen records into L2 (its adjacency row
                     // has arrived by now): the next hop's screen then reads L2, not HBM
                     const char* pr = reinterpret_cast<const char*>(a.screen) + (size_t)spec_nb[c] * lay.srb;
@@ -833,6 +868,10 @@ beam_search_kernel(const jb_search_args a, const SearchLayout lay_arg, int* __re
             }
         }
 
+        if (SRC == JB_SRC_EXACT && CH == 1 && lay.snext && nxt_pend) {  // drain before the buffer is reused
+            wbar_wait(nbar, nphase);
+            nxt_pend = false;
+        }
         // ---- outputs ----
         uint64_t* fk = a.frontier_keys + qi * (int64_t)L;
         for (int i = lane; i < L; i += 32) {
@@ -1049,16 +1088,17 @@ static bool rows_l2_resident(const jb_search_args& a) {
 }
 
 // The screen adds one dependent record fetch per hop in front of the survivors'
-// row fetch; it pays where the records stay largely L2-resident or the rows are
-// long, and loses on HBM-resident short rows. Measured (phase-1 search per 100K,
-// 8-row stage, 14-block kernel): 1M x 128 (144 MB of records) 19.8 -> 13.5 ms;
-// 96-d: 3M (336 MB) 16.0 -> 13.8, 4.5M (504 MB) 16.4 -> 18.3, 6M 16.7 -> 20.7,
-// 12.5M 17.3 -> 24.4 ms; 1M x 960 (976 B records vs 3840 B rows) build 251K ->
-// 266K inserts/s. Hence: records <= 3 x L2 (378 MB on B200), or D >= 256.
-// JB_SCREEN_FORCE=1 / 0 overrides (A/B).
-static bool screen_pays(const jb_search_args& a) {
-    const char* e = std::getenv("JB_SCREEN_FORCE");
-    if (e && (e[0] == '0' || e[0] == '1')) return e[0] == '1';
+// row fetch. Where the records stay largely L2-resident (or the rows are long) the
+// next hop's records are prefetched into L2; beyond that (HBM-resident short rows)
+// they are staged into smem one hop ahead instead (snext: +32 records per warp,
+// fewer warps, but the fetch is off the hop's critical path). Measured, phase-1
+// search per 100K (8-row stage, 14-block kernel): 1M x 128 (144 MB of records)
+// 19.8 -> 13.5 ms with L2 prefetch (16.2 with snext); 96-d with L2 prefetch: 3M
+// (336 MB) 16.0 -> 13.8, 4.5M 16.4 -> 18.3, 6M 16.7 -> 21.1, 12.5M 17.3 -> 24.4 ms;
+// with snext: 6M 16.9 -> 16.2, 12.5M 17.5 -> 16.7 ms. So snext when the records
+// exceed 3 x L2 (378 MB on B200) and D < 256. JB_SCREEN_FORCE=0 turns the screen
+// off; JB_SCREEN_NEXT=0 / 1 forces the staging mode (A/B).
+static bool screen_big(const jb_search_args& a) {
     static thread_local int dev = -1, l2 = 0;
     int d = 0;
     if (cudaGetDevice(&d) != cudaSuccess) return false;
@@ -1067,7 +1107,11 @@ static bool screen_pays(const jb_search_args& a) {
         dev = d;
     }
     const double rec = (double)a.active_count * (((a.dims + 15) & ~15) + 16);
-    return rec <= 3.0 * (double)l2 || a.dims >= 256;
+    return rec > 3.0 * (double)l2 && a.dims < 256;
+}
+static bool screen_off() {
+    const char* e = std::getenv("JB_SCREEN_FORCE");
+    return e && e[0] == '0';
 }
 
 #ifndef JB_SREC_MIN
@@ -1133,6 +1177,13 @@ static int screen_srows() {
     return v >= 32 ? 32 : (v <= 8 ? 8 : 16);
 }
 
+// stage the speculative next hop's screen records into smem (see screen_big)
+static bool screen_next(const jb_search_args& a) {
+    const char* e = std::getenv("JB_SCREEN_NEXT");
+    if (e && (e[0] == '0' || e[0] == '1')) return e[0] == '1';
+    return screen_big(a);
+}
+
 // resident blocks the screened exact kernel is compiled for (JB_SCREEN_MINB: 8 or 14,
 // default 14: 72 registers with a few spills, 28 warps/SM with the 8-row stage)
 static int screen_minb() {
@@ -1161,6 +1212,14 @@ static int launch_search(const jb_search_args& a, int hash_slots, cudaStream_t s
     SearchLayout lay = make_layout(SRC, a.dims, L, hash_slots, FAST_QB, false, 0,
                                    (SRC == JB_SRC_EXACT && a.screen != nullptr) ? screen_srows() : 32);
     lay.spf = (SRC == JB_SRC_EXACT && a.screen != nullptr) ? screen_prefetch() : 0;
+    if (SRC == JB_SRC_EXACT && a.screen != nullptr && a.degree_cap <= 32 && screen_next(a)) {
+        // 32 staged records + mbarrier in front of the beam (the beam moves up)
+        const int extra = 32 * lay.srb + 16;
+        lay.snext = 1;
+        lay.nrec_off = lay.beam_off;
+        lay.beam_off += extra;
+        lay.bytes += extra;
+    }
     if (a.degree_cap <= 32 && SRC == JB_SRC_RABITQ_FAST && BITS == 1) {
         // specialised shapes: D in {96, 128} with a 512- or 1024-slot visited table (popcount
         // estimator only: measured -2% at L=128; the float estimators got slower, +4%)
@@ -1238,7 +1297,7 @@ int jb_beam_search(const jb_search_args* args, void* stream) {
         JB_CHECK_ARG(a.data && a.data_norms && a.queries && a.query_add, "exact search: missing arrays");
         JB_CHECK_ARG(a.screen == nullptr || (a.screen_center != nullptr && a.dims <= 1040),
                      "exact search: screen records need their centre (dims <= 1040)");
-        if (a.screen != nullptr && !screen_pays(a)) {  // the screen would cost more than it saves
+        if (a.screen != nullptr && screen_off()) {  // A/B: unscreened
             jb_search_args b = a;
             b.screen = nullptr;
             if ((b.dims & 3) == 0) return launch_search<JB_SRC_EXACT, 1, true>(b, hs, st);
