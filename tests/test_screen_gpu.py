@@ -124,3 +124,28 @@ def test_screened_build_chunked_and_unaligned_rows_identical_to_oracle(D):
     n = g.active_count
     assert np.array_equal(g.host_adjacency()[:n], ref.adj[:n])
     assert g.entry_point == ref.entry
+
+
+@pytest.mark.parametrize("D", [96, 128])
+def test_screen_next_hop_staging_identical(D):
+    """snext mode (the speculative next hop's records staged in smem one hop ahead,
+    the default beyond 3 x L2 of records) forced on small data: identical searches
+    and builds."""
+    x = lowrank(8000, D, 12, 0.05, 3 * D)
+    q = lowrank(150, D, 12, 0.05, 3 * D + 1)
+    ds = jb.VectorDataset(x)
+    p = jb.BuildParams(degree_cap=24, build_beam_width=40, alpha=1.2, max_batch=2000)
+    from paper_2601_07048_b200 import search as js
+
+    with _env(JB_EXACT_DIRECT="0", JB_SCREEN_NEXT="0"):
+        g0 = jb.build(ds, p)
+        r0 = js.run_beam_searches(g0, ds, q, 64)
+    with _env(JB_EXACT_DIRECT="0", JB_SCREEN_NEXT="1"):
+        g1 = jb.build(ds, p)
+        r1 = js.run_beam_searches(g0, ds, q, 64)
+    n = g0.active_count
+    assert np.array_equal(g0.host_adjacency()[:n], g1.host_adjacency()[:n])
+    for a, b in zip(r0, r1):
+        assert np.array_equal(a.frontier_ids, b.frontier_ids)
+        assert np.array_equal(a.visited_ids, b.visited_ids)
+        assert a.stats == b.stats
