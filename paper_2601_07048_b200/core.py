@@ -181,8 +181,10 @@ class VectorDataset:
         torch = _lib.require_cuda()
         L = _lib.lib()
         st = _lib.stream_ptr()
+        # any centre keeps the bound rigorous (eps is measured against it); the mean of
+        # the first 64K rows is close enough and its sequential f64 chain is 16x shorter
         center = torch.empty(dev.dims, dtype=torch.float32, device=dev.x.device)
-        _lib.check(L.jb_column_mean_f32(_lib.ptr(dev.x), dev.count, dev.dims, _lib.ptr(center), st))
+        _lib.check(L.jb_column_mean_f32(_lib.ptr(dev.x), min(dev.count, 65536), dev.dims, _lib.ptr(center), st))
         rb = int(L.jb_screen_record_bytes(dev.dims))
         rec = torch.empty((dev.count, rb), dtype=torch.uint8, device=dev.x.device)
         _lib.check(L.jb_screen_records(_lib.ptr(dev.x), _lib.ptr(dev.norms), dev.count, dev.dims, _lib.ptr(center),
