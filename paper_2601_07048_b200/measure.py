@@ -125,16 +125,37 @@ def run_queries(graph, source, queries, params: SearchParams, exact_data=None, w
     return np.concatenate([p_[0] for p_ in parts], axis=0), np.concatenate([p_[1] for p_ in parts], axis=0)
 
 
-def write_sweep_csv(path, points) -> None:
+# the reference's CSV plus the GPU run's context columns,
+# written only when asked for (the default file stays byte-compatible with io.py:172-180)
+SWEEP_CSV_EXTRA = ("gpus", "inserts_per_s", "alg_bytes_per_query", "hbm_frac", "cpu_qps", "cpu_cores")
+
+
+def write_sweep_csv(path, points, extra: dict | None = None) -> None:
+    """io.py:172-180 (same header and number formats: qps and latency %.2f). `extra` (optional) maps any of
+    SWEEP_CSV_EXTRA to one value per point (a scalar applies to every point); those
+    columns are appended after the reference's five."""
+    cols = []
+    if extra:
+        unknown = set(extra) - set(SWEEP_CSV_EXTRA)
+        if unknown:
+            raise ValueError(f"unknown sweep CSV columns {sorted(unknown)}; allowed {SWEEP_CSV_EXTRA}")
+        cols = [c for c in SWEEP_CSV_EXTRA if c in extra]
+
+    def cell(c, i):
+        v = extra[c]
+        v = v[i] if isinstance(v, (list, tuple, np.ndarray)) else v
+        return "" if v is None else (f"{v:.6g}" if isinstance(v, float) else str(v))
+
     with open(path, "w", newline="") as fh:
         w = csv.writer(fh)
-        w.writerow(SWEEP_CSV_HEADER)
-        for p in points:
-            w.writerow([p.beam_width, p.k, f"{p.recall:.6f}", f"{p.qps:.3f}", f"{p.mean_latency_us:.3f}"])
+        w.writerow(SWEEP_CSV_HEADER + tuple(cols))
+        for i, p in enumerate(points):
+            w.writerow([p.beam_width, p.k, f"{p.recall:.6f}", f"{p.qps:.2f}", f"{p.mean_latency_us:.2f}"] +
+                       [cell(c, i) for c in cols])
 
 
 def sweep(graph, source, queries, gt, k: int, beam_widths, *, rerank: bool = False, exact_data=None,
-          workers: int = 1, warmup: bool = True, csv_path=None) -> list[SweepPoint]:
+          workers: int = 1, warmup: bool = True, csv_path=None, csv_extra: dict | None = None) -> list[SweepPoint]:
     """bench.py:94-137: per beam width one untimed warmup pass, then a timed pass
     (host queries in, host ids out) for QPS, and recall against `gt`."""
     if k > gt.k:
@@ -151,5 +172,5 @@ def sweep(graph, source, queries, gt, k: int, beam_widths, *, rerank: bool = Fal
         el = time.perf_counter() - t0
         pts.append(SweepPoint(int(beam), k, recall_at_k(ids, gt, k), nq / el, el / nq * 1e6))
     if csv_path is not None:
-        write_sweep_csv(csv_path, pts)
+        write_sweep_csv(csv_path, pts, csv_extra)
     return pts
