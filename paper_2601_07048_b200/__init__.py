@@ -9,7 +9,7 @@ There is no CPU fallback: without the library or a CUDA device, calls raise.
 
 from .build import BuildParams, EdgeBuffer, batch_insert, build, insert_stream
 from .core import (AugmentedDataset, DistanceKind, ElementKind, VectorDataset, dot, gen_lowrank, gen_synthetic,
-                   mips_augment, sq_l2)
+                   mips_augment, row_sq_norms, sq_l2)
 from .graph import Candidate, FormatError, GraphIndex, medoid, robust_prune
 from .rabitq import QueryPrep, RaBitQIndex, estimate_sq_dist, prep_query, rotate
 from .rabitq import fit as rabitq_fit
@@ -26,5 +26,5 @@ __all__ = [
     "AugmentedDataset", "mips_augment", "Candidate", "DistanceKind", "ElementKind", "FormatError", "GraphIndex", "QueryPrep", "RaBitQIndex",
     "SearchParams", "SearchResult", "SearchStats", "VectorDataset", "beam_search", "dot", "estimate_sq_dist",
     "gen_lowrank", "gen_synthetic", "medoid", "prep_query", "rabitq_fit", "robust_prune", "rotate",
-    "run_beam_searches", "search_knn", "GroundTruth", "exact_knn", "SweepPoint", "recall_at_k", "run_queries", "sweep", "search_knn_batch", "search_knn_batch_device", "sq_l2",
+    "run_beam_searches", "search_knn", "GroundTruth", "exact_knn", "SweepPoint", "recall_at_k", "run_queries", "sweep", "search_knn_batch", "search_knn_batch_device", "sq_l2", "row_sq_norms",
 ]

@@ -18,7 +18,7 @@ import numpy as np
 from . import _lib
 
 __all__ = ["ElementKind", "DistanceKind", "VectorDataset", "AugmentedDataset", "mips_augment", "sq_l2", "dot",
-           "gen_synthetic", "gen_lowrank"]
+           "gen_synthetic", "gen_lowrank", "row_sq_norms"]
 
 
 class ElementKind(enum.Enum):
@@ -260,6 +260,31 @@ def as_dataset(obj) -> VectorDataset:
 def _require_same_shape(a: np.ndarray, b: np.ndarray) -> None:
     if a.shape != b.shape:
         raise ValueError(f"dimension mismatch: {a.shape} vs {b.shape}")
+
+
+def row_sq_norms(x) -> np.ndarray:
+    """core.py:161-166 on the device: per-row squared norms, integer-exact (int64) for
+    u8 rows, f32 in einsum('nd,nd->n') order for f32 rows (jb_row_sq_norms_u8 /
+    jb_row_sq_norms). Other dtypes: ValueError (the device path has the two element
+    kinds of the reference's datasets)."""
+    torch = _lib.require_cuda()
+    a = np.asarray(x)
+    if a.ndim != 2:
+        raise ValueError("row_sq_norms expects a 2-D array")
+    if a.dtype not in (np.float32, np.uint8):
+        raise ValueError(f"row_sq_norms: f32 or u8 rows expected, got {a.dtype}")
+    n, d = a.shape
+    if n == 0:
+        return np.zeros(0, dtype=np.int64 if a.dtype == np.uint8 else np.float32)
+    xd = torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    st = _lib.stream_ptr()
+    if a.dtype == np.uint8:
+        out = torch.empty(n, dtype=torch.int32, device="cuda")
+        _lib.check(_lib.lib().jb_row_sq_norms_u8(_lib.ptr(xd), n, d, _lib.ptr(out), st))
+        return out.cpu().numpy().view(np.uint32).astype(np.int64)
+    out = torch.empty(n, dtype=torch.float32, device="cuda")
+    _lib.check(_lib.lib().jb_row_sq_norms(_lib.ptr(xd), n, d, _lib.ptr(out), st))
+    return out.cpu().numpy()
 
 
 def sq_l2(a, b) -> float:

@@ -104,3 +104,20 @@ def test_column_mean_bit_exact_on_ragged_shapes():
         _lib.check(_lib.lib().jb_column_mean_f32(_lib.ptr(xd), n, d, _lib.ptr(out), _lib.stream_ptr()))
         got = out.cpu().numpy()
         assert got.tobytes() == want.tobytes(), (n, d)
+
+
+@pytest.mark.gpu
+def test_row_sq_norms_matches_reference_einsum():
+    """core.py:161-166: einsum('nd,nd->n') bit for bit on f32 rows, integer-exact int64 on u8."""
+    rng = np.random.default_rng(5)
+    for d in (1, 7, 33, 128, 960):
+        x = (rng.standard_normal((300, d)) * 3).astype(np.float32)
+        got = jb.row_sq_norms(x)
+        assert got.dtype == np.float32
+        assert got.tobytes() == np.einsum("nd,nd->n", x, x).tobytes()
+        u = rng.integers(0, 256, size=(200, d), dtype=np.uint8)
+        w = u.astype(np.int64)
+        gu = jb.row_sq_norms(u)
+        assert gu.dtype == np.int64 and np.array_equal(gu, np.einsum("nd,nd->n", w, w))
+    with pytest.raises(ValueError):
+        jb.row_sq_norms(np.zeros((3, 4), np.float64))
